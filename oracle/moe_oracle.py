@@ -1,0 +1,428 @@
+"""fp64 CPU oracle for the SonicMoE hot path (arXiv 2512.14080).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+module.  The product path (``paper_2512_14080_b200``) never imports it and
+shares no code with it: no kernels, helpers, tables or constants.
+
+Citations: ``P:n`` = PAPER.md line n, ``S:n`` = SPEC.md line n (the paper
+text and the CPU-desk spec written from it); ``Qk`` = reading k listed in
+DESIGN.md §3 (the ambiguities of the paper and the reading adopted).
+
+What is computed, and in which notation:
+
+* routing (``route``): token-choice top-K (§2.3; stable, ties to the
+  lower expert id, §4.3), then optionally token rounding
+  (Alg. 4) with the NR-f subroutine, then the
+  orphan rescue (Q14), gates renormalised over the kept set (Q13), and
+  the canonical grouped-row metadata (offsets, gather map, token CSR).
+* values (``forward`` / ``backward``): the plain definition of the MoE layer
+  (Alg. 1) and its textbook gradients written the paper's way
+  (Alg. 3, Alg. 5, App. C).  The method is
+  exact up to rounding ("Both yield identical results"), so the oracle
+  for values is the definition in fp64.
+* ``backward_reference``: the Y/dY-materialising path of App. C.1
+  (P:1773-1803), the cross-check of the memory-efficient rewrite.
+* ``forward_dense``: every expert on every token, masked and gate-scaled.
+
+Every array is float64 (bf16/fp32 inputs are converted exactly).  A library
+primitive (numpy matmul, numpy stable sort) serves as a step; there is no
+blocking, fusion or reordering beyond what the definitions state.
+
+Parity pins live in ``tests/test_oracle.py``: dense brute force, finite
+differences, the App. C identities, TR invariants, the SPEC worked examples
+and hand-traced golden files under ``tests/golden/``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+GEMM_M = 128  # grouped-row padding granularity of the GPU layout
+
+
+# --------------------------------------------------------------------------
+# SwiGLU (§2.2; layout [gate | up] per Q1 / S:293)
+# --------------------------------------------------------------------------
+def sigmoid(x):
+    return 1.0 / (1.0 + np.exp(-x))
+
+
+def silu(x):
+    """silu(x) = x * sigma(x)."""
+    return x * sigmoid(x)
+
+
+def dsilu(x):
+    """silu'(x) = sigma(x) (1 + x (1 - sigma(x)))."""
+    s = sigmoid(x)
+    return s * (1.0 + x * (1.0 - s))
+
+
+def swiglu(H):
+    """A = SwiGLU(H) = silu(H[:, :n]) * H[:, n:]  (Q1)."""
+    n = H.shape[-1] // 2
+    return silu(H[..., :n]) * H[..., n:]
+
+
+def dswiglu(dA, H):
+    """(A, dH) = dAct_func(dA, H) (Alg. 3).
+
+    d gate = dA * up * silu'(gate);  d up = dA * silu(gate).
+    """
+    n = H.shape[-1] // 2
+    g, u = H[..., :n], H[..., n:]
+    A = silu(g) * u
+    dH = np.concatenate([dA * u * dsilu(g), dA * silu(g)], axis=-1)
+    return A, dH
+
+
+# --------------------------------------------------------------------------
+# Routing
+# --------------------------------------------------------------------------
+def topk_tc(S, K):
+    """Token-choice TopK over each row of S (§2.3, Alg. 4 step (1) P:1135).
+
+    Order: value descending, ties to the lower expert id -- the stability the
+    paper's packed-index bitonic sort guarantees (§4.3, Q9).
+    numpy's stable argsort of -S is exactly that order.
+    """
+    S = np.asarray(S, dtype=np.float64)
+    assert np.all(np.isfinite(S)), "NaN/inf scores are invalid input (Q24)"
+    T, E = S.shape
+    assert 1 <= K <= E
+    order = np.argsort(-S, axis=1, kind="stable")[:, :K]
+    return order.astype(np.int64), np.take_along_axis(S, order, axis=1)
+
+
+def round_up(f, M):
+    """ceil(f/M)*M  (Alg. 4 step (2))."""
+    return -(-np.asarray(f) // M) * M
+
+
+def round_down(f, M):
+    """floor(f/M)*M  (Alg. 4 step (2))."""
+    return (np.asarray(f) // M) * M
+
+
+def round_nrf(f, M):
+    """NR-f round_and_sparsify decision.
+
+    "pad EC selected tokens if ceil(f)-f is smaller than f-floor(f)":
+    strict '<', so an exact tie at M/2 rounds down (Q11).
+    Returns the rounded counts.
+    """
+    f = np.asarray(f, dtype=np.int64)
+    up, dn = round_up(f, M), round_down(f, M)
+    return np.where((up - f) < (f - dn), up, dn)
+
+
+def _rank_expert_column(S_col, tc_col):
+    """Alg. 4 steps (3)-(4) for one expert: pi_e = sort(S'_e) descending.
+
+    The paper builds S' = S - 1 with the top-K entries restored to S
+     so that TC tokens rank above every non-TC token, then sorts
+    the column.  Reading Q10: the intent is the lexicographic key
+    (in-TC desc, S desc, token asc) -- S - 1 rounds tiny scores together in
+    fp32.  Ties in S go to the lower token index (Q12).
+    """
+    T = S_col.shape[0]
+    # np.lexsort: last key is primary.
+    return np.lexsort((np.arange(T), -S_col, ~tc_col))
+
+
+def _paper_S_prime(S, tc):
+    """Alg. 4 step (3) literally: S' = S - 1, TC entries restored.
+
+    Used only by the tests to pin _rank_expert_column to the paper's form.
+    """
+    Sp = np.asarray(S, np.float64) - 1.0
+    Sp[tc] = np.asarray(S, np.float64)[tc]
+    return Sp
+
+
+@dataclass
+class Routing:
+    """Routing result plus the canonical grouped-row metadata.
+
+    Fields mirror ``sonic_routing`` in include/sonic.h.
+    """
+    topk_ids: np.ndarray      # [T,K] int  TC choice, value-desc, ties -> lower id
+    topk_s: np.ndarray        # [T,K] f64
+    f: np.ndarray             # [E]   TC counts (Alg. 4 step (2))
+    f_rounded: np.ndarray     # [E]   kept counts (== f under TC)
+    kept: np.ndarray          # [T,E] bool, pi (kept set)
+    gate: np.ndarray          # [T,E] f64, g_te = S_te / sum_{kept} S_te' (0 off the kept set)
+    offsets: np.ndarray       # [E+1] exclusive prefix of f_rounded
+    pad_offsets: np.ndarray   # [E+1] exclusive prefix of ceil(f_rounded/GEMM_M)*GEMM_M
+    row_token: np.ndarray     # [R_pad] token of each grouped row, -1 on pad rows
+    row_expert: np.ndarray    # [R_pad] expert of each grouped row
+    row_gate: np.ndarray      # [R_pad] gate of each grouped row, 0 on pad rows
+    token_rowptr: np.ndarray  # [T+1]  CSR over tokens
+    token_rows: np.ndarray    # [R]    grouped rows of each token, expert-ascending
+    tile_expert: np.ndarray   # [R_pad/GEMM_M] expert of each 128-row tile
+    flipped: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))  # experts flipped by the rescue
+
+    @property
+    def R(self):
+        return int(self.offsets[-1])
+
+    @property
+    def R_pad(self):
+        return int(self.pad_offsets[-1])
+
+
+def route(S, K, mode="tc", m_tile=128, rescue=True, gate_raw=False):
+    """Routing per Alg. 4 or plain TC.
+
+    mode "tc": kept = TC top-K set.  mode "tr": token rounding with NR-f.
+    """
+    S = np.asarray(S, dtype=np.float64)
+    T, E = S.shape
+    ids, vals = topk_tc(S, K)                                  # step (1)
+    tc = np.zeros((T, E), dtype=bool)
+    tc[np.arange(T)[:, None], ids] = True
+    f = tc.sum(axis=0).astype(np.int64)                        # step (2): f_e
+    flipped = np.zeros(0, np.int64)
+    if mode == "tc":
+        f_r = f.copy()
+        kept = tc.copy()
+    elif mode == "tr":
+        f_up = np.minimum(round_up(f, m_tile), T)              # Q15: cap at T
+        f_r = np.minimum(round_nrf(f, m_tile), T)              # round_and_sparsify (NR-f)
+        kept = np.zeros((T, E), dtype=bool)
+
+        def select(e):                                         # step (4), one expert
+            kept[:, e] = False
+            order = _rank_expert_column(S[:, e], tc[:, e])     # steps (3)+(4): sort(S'_e)
+            kept[order[: f_r[e]], e] = True
+
+        for e in range(E):
+            select(e)
+        if rescue:                                             # Q14 orphan rescue
+            orphan = ~kept.any(axis=1)
+            flip = np.unique(ids[orphan, 0])
+            for e in flip:
+                f_r[e] = f_up[e]
+                select(e)
+            flipped = flip.astype(np.int64)
+            assert kept.any(axis=1).all()
+    else:
+        raise ValueError(mode)
+
+    if gate_raw:
+        gate = np.where(kept, S, 0.0)
+    else:                                                      # P:1488 renormalisation (Q13)
+        denom = np.where(kept, S, 0.0).sum(axis=1, keepdims=True)
+        gate = np.where(kept, S / np.where(denom == 0, 1.0, denom), 0.0)
+    return build_metadata(ids, vals, f, f_r, kept, gate, flipped)
+
+
+def build_metadata(ids, vals, f, f_r, kept, gate, flipped):
+    """Canonical grouped layout (P:787 footnote "routing metadata").
+
+    Segment e holds e's kept tokens in ascending token order (Q17) and starts
+    at a GEMM_M-aligned row; rows past f_r[e] inside the last tile are pad rows.
+    Token CSR lists each token's rows in ascending expert order.
+    """
+    T, E = kept.shape
+    offsets = np.zeros(E + 1, np.int64)
+    offsets[1:] = np.cumsum(f_r)
+    padded = round_up(f_r, GEMM_M)
+    pad_offsets = np.zeros(E + 1, np.int64)
+    pad_offsets[1:] = np.cumsum(padded)
+    R_pad = int(pad_offsets[-1])
+    row_token = np.full(R_pad, -1, np.int64)
+    row_expert = np.zeros(R_pad, np.int64)
+    row_gate = np.zeros(R_pad, np.float64)
+    row_of = np.full((T, E), -1, np.int64)
+    for e in range(E):
+        toks = np.nonzero(kept[:, e])[0]                       # ascending
+        base = pad_offsets[e]
+        row_token[base: base + len(toks)] = toks
+        row_expert[base: pad_offsets[e + 1]] = e
+        row_gate[base: base + len(toks)] = gate[toks, e]
+        row_of[toks, e] = base + np.arange(len(toks))
+    cnt = kept.sum(axis=1)
+    token_rowptr = np.zeros(T + 1, np.int64)
+    token_rowptr[1:] = np.cumsum(cnt)
+    token_rows = np.zeros(int(token_rowptr[-1]), np.int64)
+    for t in range(T):
+        es = np.nonzero(kept[t])[0]                            # ascending expert
+        token_rows[token_rowptr[t]: token_rowptr[t + 1]] = row_of[t, es]
+    tile_expert = row_expert[::GEMM_M].copy() if R_pad else np.zeros(0, np.int64)
+    return Routing(ids, vals, f, f_r, kept, gate, offsets, pad_offsets, row_token,
+                   row_expert, row_gate, token_rowptr, token_rows, tile_expert, flipped)
+
+
+# --------------------------------------------------------------------------
+# Forward (Alg. 1 P:200-242 as the definition; Alg. 2 P:528-592 stages)
+# --------------------------------------------------------------------------
+@dataclass
+class ForwardResult:
+    O: np.ndarray            # [T,d]
+    H: dict                  # e -> [f_e, 2n]  (cached, §3.2)
+    A: dict                  # e -> [f_e, n]
+    Y: dict                  # e -> [f_e, d]   gate-scaled (Q2)
+    tokens: dict             # e -> kept tokens ascending
+
+
+def _f64(a):
+    return np.asarray(a, dtype=np.float64)
+
+
+def forward(X, W1, W2, rt: Routing, experts=None):
+    """O_t = sum_e pi_te g_te Y_{e,t},  Y_e = SwiGLU(X_e W1_e) W2_e.
+
+    The gate multiplies Y before aggregation (Q2, P:1774 option (1)); the
+    result is identical in exact arithmetic.
+    """
+    X, W1, W2 = _f64(X), _f64(W1), _f64(W2)
+    T, d = X.shape
+    E = W1.shape[0]
+    O = np.zeros((T, d))
+    H, A, Y, tokens = {}, {}, {}, {}
+    for e in (range(E) if experts is None else experts):
+        toks = np.nonzero(rt.kept[:, e])[0]
+        Xe = X[toks]                                           # X_e = Gather(X, pi_:,e)
+        He = Xe @ W1[e]                                        # H_e = X_e W1_e
+        Ae = swiglu(He)                                        # A_e = act(H_e)
+        Ye = rt.gate[toks, e][:, None] * (Ae @ W2[e])          # Y_e scaled by g (Q2)
+        np.add.at(O, toks, Ye)                                 # O_t = sum_e ...
+        H[e], A[e], Y[e], tokens[e] = He, Ae, Ye, toks
+    return ForwardResult(O, H, A, Y, tokens)
+
+
+def forward_dense(X, W1, W2, kept, gate):
+    """Brute force: every expert on every token, masked by pi and scaled by g."""
+    X, W1, W2 = _f64(X), _f64(W1), _f64(W2)
+    O = np.zeros((X.shape[0], W2.shape[2]))
+    for e in range(W1.shape[0]):
+        Ye = swiglu(X @ W1[e]) @ W2[e]
+        O += (kept[:, e] * gate[:, e])[:, None] * Ye
+    return O
+
+
+# --------------------------------------------------------------------------
+# Backward, memory-efficient path (Alg. 3 P:595-706 + Alg. 5)
+# --------------------------------------------------------------------------
+@dataclass
+class BackwardResult:
+    dX: np.ndarray           # [T,d]
+    dW1: np.ndarray          # [E,d,2n]
+    dW2: np.ndarray          # [E,n,d]
+    dS: dict                 # e -> [f_e]  dL/dg for each kept (t,e), ascending t
+    dH: dict                 # e -> [f_e,2n]
+    A_prime: dict            # e -> [f_e,n]
+    dXt: dict                # e -> [f_e,d]  dX~ rows
+
+
+def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None):
+    """Alg. 3 then Alg. 5, row by row in the paper's notation.
+
+    dA'_e = Gather(dO) W2_e^T;  dA_e = s_e dA'_e;  (A_e, dH_e) = dSwiGLU(dA_e, H_e);
+    A'_e = s_e A_e;  dS_e,t = <dA'_e,t, A_e,t> (boxed eq. P:1752);
+    dW2_e = A'_e^T dO_e (Q4);  dX~_e = dH_e W1_e^T;  dW1_e = X_e^T dH_e;
+    dX_t = sum_e pi_te dX~_e,t.
+    H is recomputed from X unless a cache is given (only X and H are cached, §3.2).
+    ``experts`` restricts the work (dX then holds only those experts' terms).
+    """
+    dO, X, W1, W2 = _f64(dO), _f64(X), _f64(W1), _f64(W2)
+    T, d = X.shape
+    E, _, n2 = W1.shape
+    n = n2 // 2
+    dX = np.zeros((T, d))
+    dW1 = np.zeros((E, d, n2))
+    dW2 = np.zeros((E, n, d))
+    dS, dH, Ap, dXt = {}, {}, {}, {}
+    for e in (range(E) if experts is None else experts):
+        toks = np.nonzero(rt.kept[:, e])[0]
+        s = rt.gate[toks, e][:, None]                          # s_e = Gather(S, pi_:,e)
+        He = X[toks] @ W1[e] if H_cache is None else _f64(H_cache[e])
+        dOe = dO[toks]                                         # Gather(dO, pi_:,e)
+        dAp = dOe @ W2[e].T                                    # dA'_e
+        dA = s * dAp                                           # dA_e
+        Ae, dHe = dswiglu(dA, He)                              # A_e, dH_e
+        Ape = s * Ae                                           # A'_e
+        dS[e] = np.sum(dAp * Ae, axis=1)                       # <dA'_e,t, A_e,t>
+        dW2[e] = Ape.T @ dOe                                   # dW2_e = A'^T dO_e
+        dXt[e] = dHe @ W1[e].T                                 # dX~_e = dH_e W1_e^T
+        dW1[e] = X[toks].T @ dHe                               # dW1_e = X_e^T dH_e
+        np.add.at(dX, toks, dXt[e])                            # dX_t = sum_e dX~_e,t
+        dH[e], Ap[e] = dHe, Ape
+    return BackwardResult(dX, dW1, dW2, dS, dH, Ap, dXt)
+
+
+def backward_reference(dO, X, W1, W2, rt: Routing):
+    """App. C.1 path: materialise Y (unscaled) and dY = s dO.
+
+    dS_t,e = <dO_t, Y_e,t> with Y_e = A_e W2_e (P:1752 first form);
+    dW2_e = A_e^T dY_e;  dA_e = dY_e W2_e^T.
+    """
+    dO, X, W1, W2 = _f64(dO), _f64(X), _f64(W1), _f64(W2)
+    T, d = X.shape
+    E, _, n2 = W1.shape
+    n = n2 // 2
+    dX = np.zeros((T, d))
+    dW1 = np.zeros((E, d, n2))
+    dW2 = np.zeros((E, n, d))
+    dS, dH = {}, {}
+    for e in range(E):
+        toks = np.nonzero(rt.kept[:, e])[0]
+        s = rt.gate[toks, e][:, None]
+        He = X[toks] @ W1[e]
+        Ae = swiglu(He)
+        Ye = Ae @ W2[e]                                        # unscaled Y
+        dYe = s * dO[toks]                                     # eq. dY
+        dS[e] = np.sum(dO[toks] * Ye, axis=1)                  # <dO_t, Y_e,t>
+        dW2[e] = Ae.T @ dYe                                    # A^T dY
+        dA = dYe @ W2[e].T
+        _, dHe = dswiglu(dA, He)
+        dW1[e] = X[toks].T @ dHe
+        np.add.at(dX, toks, dHe @ W1[e].T)
+        dH[e] = dHe
+    return BackwardResult(dX, dW1, dW2, dS, dH, {}, {})
+
+
+# --------------------------------------------------------------------------
+# Finite differences: L = sum G * O with routing held fixed
+# --------------------------------------------------------------------------
+def loss_fixed_routing(X, W1, W2, kept, gate, G):
+    return float(np.sum(_f64(G) * forward_dense(X, W1, W2, kept, gate)))
+
+
+def fd_grad(fun, x, h=1e-5, coords=None):
+    """Central differences (f(x+h) - f(x-h)) / 2h at the given flat coords."""
+    x = np.array(x, dtype=np.float64)
+    flat = x.reshape(-1)
+    idx = range(flat.size) if coords is None else coords
+    out = {}
+    for i in idx:
+        old = flat[i]
+        flat[i] = old + h
+        fp = fun(x)
+        flat[i] = old - h
+        fm = fun(x)
+        flat[i] = old
+        out[i] = (fp - fm) / (2 * h)
+    return out
+
+
+# --------------------------------------------------------------------------
+# Closed forms (§3.2; Eq. 4)
+# --------------------------------------------------------------------------
+def model_flops(T, d, n, K, fwd_only=False):
+    """(6+12) T n K d; forward alone is 6 T n K d."""
+    return (6 if fwd_only else 18) * T * n * K * d
+
+
+def activation_bytes(T, d, n, K):
+    """2Td + 4TKn bytes: X and H in bf16."""
+    return 2 * T * d + 4 * T * K * n
+
+
+def arithmetic_intensity(T, d, n, E, K):
+    """Eq. 4: 3 / ((2+2G)/d + 3/(T rho)), G = d/n, rho = K/E."""
+    G, rho = d / n, K / E
+    return 3.0 / ((2 + 2 * G) / d + 3.0 / (T * rho))

@@ -1,0 +1,296 @@
+"""Pins for the fp64 oracle (oracle/moe_oracle.py) -- things the paper and the
+mathematics fix, chosen so that a dropped term, a wrong sign/index or a
+transposed operand anywhere in the oracle fails at least one of them.
+
+None of these tests touch the GPU path.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import moe_oracle as om
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "tr_examples.json")))
+
+
+def rand_case(seed, T, d, n, E, K, mode="tc", m_tile=4, ties=0):
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((T, d))
+    W1 = rng.standard_normal((E, d, 2 * n)) / np.sqrt(d)
+    W2 = rng.standard_normal((E, n, d)) / np.sqrt(n)
+    L = rng.standard_normal((T, E))
+    if ties:
+        L = np.round(L * ties) / ties
+    S = np.exp(L) / np.exp(L).sum(1, keepdims=True)
+    dO = rng.standard_normal((T, d))
+    rt = om.route(S, K, mode=mode, m_tile=m_tile)
+    return X, W1, W2, S, dO, rt
+
+
+# ------------------------------------------------------------------ SwiGLU
+def test_swiglu_golden():
+    g = GOLD["swiglu"]
+    assert om.swiglu(np.array([1.0, 1.0])) == pytest.approx(g["sigma1"], abs=1e-16)
+    assert om.dsilu(0.0) == g["dsilu0"]
+    assert om.dsilu(1.0) == pytest.approx(g["dsilu1"], abs=1e-15)
+    assert om.dsilu(-2.0) == pytest.approx(g["dsilu_m2"], abs=1e-15)
+    A, dH = om.dswiglu(np.array([1.0]), np.array([0.0, 1.0]))
+    assert A[0] == 0.0 and dH[0] == 0.5 and dH[1] == 0.0
+    assert om.swiglu(np.array([0.0, 7.0]))[0] == 0.0
+
+
+def test_dswiglu_matches_finite_differences():
+    rng = np.random.default_rng(1)
+    H = rng.standard_normal((5, 6))
+    dA = rng.standard_normal((5, 3))
+    _, dH = om.dswiglu(dA, H)
+    h = 1e-6
+    for i in range(5):
+        for j in range(6):
+            Hp, Hm = H.copy(), H.copy()
+            Hp[i, j] += h
+            Hm[i, j] -= h
+            fd = (np.sum(dA * om.swiglu(Hp)) - np.sum(dA * om.swiglu(Hm))) / (2 * h)
+            assert dH[i, j] == pytest.approx(fd, rel=1e-7, abs=1e-9)
+
+
+# ------------------------------------------------------------------ top-K
+def test_topk_spec_example():
+    ex = GOLD["topk"][0]
+    ids, vals = om.topk_tc(np.array([ex["row"]]), ex["K"])
+    assert ids[0].tolist() == ex["ids"] and vals[0].tolist() == ex["vals"]
+
+
+@pytest.mark.parametrize("E,K", [(8, 1), (8, 8), (64, 8), (512, 16), (4096, 16)])
+def test_topk_brute_force_with_ties(E, K):
+    rng = np.random.default_rng(E * 31 + K)
+    rows = np.round(rng.standard_normal((40, E)) * 3) / 3       # many exact ties
+    ids, vals = om.topk_tc(rows, K)
+    for r in range(rows.shape[0]):
+        ref = sorted(range(E), key=lambda i: (-rows[r, i], i))[:K]
+        assert ids[r].tolist() == ref
+        assert vals[r].tolist() == [rows[r, i] for i in ref]
+
+
+def test_topk_monotone_transform_invariance():
+    rng = np.random.default_rng(3)
+    S = rng.standard_normal((50, 32))
+    a, _ = om.topk_tc(S, 8)
+    b, _ = om.topk_tc(np.exp(3 * S) + 1.0, 8)
+    assert np.array_equal(a, b)
+
+
+# ------------------------------------------------------------------ rounding
+def test_nrf_and_updown_golden():
+    ex = GOLD["nrf"][0]
+    assert om.round_nrf(ex["f"], ex["M"]).tolist() == ex["f_r"]
+    ex = GOLD["updown"][0]
+    assert om.round_up(ex["f"], ex["M"]).tolist() == ex["up"]
+    assert om.round_down(ex["f"], ex["M"]).tolist() == ex["down"]
+
+
+@pytest.mark.parametrize("ex", GOLD["tr"], ids=lambda e: e["cite"][:40])
+def test_token_rounding_hand_traced(ex):
+    S = np.array(ex["S"])
+    rt = om.route(S, ex["K"], mode="tr", m_tile=ex["M"], rescue=ex["rescue"])
+    assert rt.f.tolist() == ex["f"]
+    assert rt.f_rounded.tolist() == ex["f_r"]
+    for e, toks in enumerate(ex["kept"]):
+        assert np.nonzero(rt.kept[:, e])[0].tolist() == toks
+    assert rt.flipped.tolist() == ex["flipped"]
+
+
+def test_rank_matches_paper_S_prime_form():
+    """Alg. 4 step (3) literally (S' = S - 1, TC restored, sorted descending,
+    ties to the lower token) ranks exactly as the lexicographic key (Q10)
+    whenever S - 1 is exact in fp64 (softmax scores of N(0,1) logits)."""
+    for seed in range(10):
+        rng = np.random.default_rng(seed)
+        L = np.round(rng.standard_normal((300, 16)) * 4) / 4
+        S = (np.exp(L) / np.exp(L).sum(1, keepdims=True)).astype(np.float32).astype(np.float64)
+        ids, _ = om.topk_tc(S, 3)
+        tc = np.zeros(S.shape, bool)
+        tc[np.arange(300)[:, None], ids] = True
+        Sp = om._paper_S_prime(S, tc)
+        for e in range(16):
+            paper = np.argsort(-Sp[:, e], kind="stable")
+            assert np.array_equal(paper, om._rank_expert_column(S[:, e], tc[:, e]))
+
+
+@pytest.mark.parametrize("M", [4, 16, 128])
+def test_token_rounding_invariants(M):
+    """North-star TR invariants + P:1236/P:1243 locality, over 100 seeds."""
+    for seed in range(100 if M < 128 else 20):
+        rng = np.random.default_rng(seed)
+        T, E, K = (64, 8, 2) if M < 128 else (1024, 16, 4)
+        L = rng.standard_normal((T, E)) + (rng.standard_normal((1, E)) if seed % 2 else 0)
+        S = np.exp(L) / np.exp(L).sum(1, keepdims=True)
+        for rescue in (False, True):
+            rt = om.route(S, K, mode="tr", m_tile=M, rescue=rescue)
+            ids, _ = om.topk_tc(S, K)
+            tc = np.zeros((T, E), bool)
+            tc[np.arange(T)[:, None], ids] = True
+            f = tc.sum(0)
+            assert np.all(rt.f == f)
+            assert np.all(rt.f_rounded % M == 0)
+            assert np.all(np.abs(rt.f_rounded - f) < M)
+            assert np.all(rt.kept.sum(0) == rt.f_rounded)
+            if not rescue:
+                assert np.all(np.abs(rt.f_rounded - f) <= M // 2)
+            else:
+                assert rt.kept.any(1).all()                     # every token keeps >= 1 expert
+            for e in range(E):
+                col_tc, col_k = tc[:, e], rt.kept[:, e]
+                if rt.f_rounded[e] >= f[e]:                     # padded: kept ⊇ TC, extra = best non-TC
+                    assert np.all(col_k[col_tc])
+                    extra = np.nonzero(col_k & ~col_tc)[0]
+                    rest = np.nonzero(~col_k & ~col_tc)[0]
+                else:                                           # dropped: kept ⊆ TC, dropped = worst TC
+                    assert not np.any(col_k & ~col_tc)
+                    extra = np.nonzero(col_k)[0]
+                    rest = np.nonzero(col_tc & ~col_k)[0]
+                if len(extra) and len(rest):
+                    worst_in = min(extra, key=lambda t: (S[t, e], -t))
+                    best_out = max(rest, key=lambda t: (S[t, e], -t))
+                    assert (S[worst_in, e], -worst_in) > (S[best_out, e], -best_out)
+
+
+def test_tr_down_on_tile_multiples_is_tc():
+    """when every f is already a tile multiple, TR == TC."""
+    T, E, K, M = 64, 4, 2, 8
+    # expert e is chosen by tokens [16e, 16e+16) first and by the next block second
+    S = np.full((T, E), 0.01)
+    for t in range(T):
+        S[t, t // 16] = 0.9
+        S[t, (t // 16 + 1) % E] = 0.5
+    S /= S.sum(1, keepdims=True)
+    a, b = om.route(S, K, "tc"), om.route(S, K, "tr", m_tile=M)
+    assert np.array_equal(a.kept, b.kept) and np.array_equal(a.f_rounded, b.f_rounded)
+
+
+# ------------------------------------------------------------------ metadata
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+def test_metadata_is_consistent(mode):
+    X, W1, W2, S, dO, rt = rand_case(5, 700, 4, 2, 12, 3, mode=mode, m_tile=128)
+    E = S.shape[1]
+    assert rt.offsets[0] == 0 and np.all(np.diff(rt.offsets) == rt.f_rounded)
+    assert np.all(rt.pad_offsets % om.GEMM_M == 0)
+    assert rt.R == rt.kept.sum() == len(rt.token_rows)
+    for e in range(E):
+        seg = rt.row_token[rt.pad_offsets[e]: rt.pad_offsets[e] + rt.f_rounded[e]]
+        assert np.all(np.diff(seg) > 0)                                     # ascending tokens
+        assert np.all(rt.row_token[rt.pad_offsets[e] + rt.f_rounded[e]: rt.pad_offsets[e + 1]] == -1)
+        assert np.all(rt.row_expert[rt.pad_offsets[e]: rt.pad_offsets[e + 1]] == e)
+    for t in range(S.shape[0]):                                             # CSR is the inverse map
+        rows = rt.token_rows[rt.token_rowptr[t]: rt.token_rowptr[t + 1]]
+        assert np.all(rt.row_token[rows] == t)
+        assert np.all(np.diff(rt.row_expert[rows]) > 0)
+        assert set(rt.row_expert[rows]) == set(np.nonzero(rt.kept[t])[0])
+        assert rt.gate[t].sum() == pytest.approx(1.0)
+    assert np.all(rt.tile_expert == rt.row_expert[:: om.GEMM_M])
+
+
+# ------------------------------------------------------------------ forward
+@pytest.mark.parametrize("T,d,n,E,K,mode", [
+    (8, 4, 2, 4, 2, "tc"), (32, 8, 4, 8, 4, "tc"), (24, 6, 3, 5, 5, "tc"),   # K = E
+    (6, 4, 2, 8, 1, "tc"),                                                   # empty experts
+    (64, 8, 4, 8, 2, "tr")])
+def test_forward_equals_dense_brute_force(T, d, n, E, K, mode):
+    X, W1, W2, S, dO, rt = rand_case(T + E, T, d, n, E, K, mode=mode, m_tile=4)
+    O = om.forward(X, W1, W2, rt).O
+    Od = om.forward_dense(X, W1, W2, rt.kept, rt.gate)
+    assert np.max(np.abs(O - Od)) <= 1e-13 * max(1.0, np.max(np.abs(Od)))
+    if E > T:
+        assert (rt.f == 0).any()
+
+
+def test_forward_special_cases():
+    X, W1, W2, S, dO, rt = rand_case(0, 16, 4, 2, 4, 2)
+    assert np.all(om.forward(np.zeros_like(X), W1, W2, rt).O == 0)
+    # E = K = 1 with gate 1: a dense SwiGLU MLP, written out element-wise
+    rng = np.random.default_rng(2)
+    X1, W11, W21 = rng.standard_normal((5, 3)), rng.standard_normal((1, 3, 4)), rng.standard_normal((1, 2, 3))
+    rt1 = om.route(np.ones((5, 1)), 1)
+    O = om.forward(X1, W11, W21, rt1).O
+    for t in range(5):
+        h = [sum(X1[t, k] * W11[0, k, j] for k in range(3)) for j in range(4)]
+        a = [h[j] / (1 + np.exp(-h[j])) * h[2 + j] for j in range(2)]
+        for c in range(3):
+            assert O[t, c] == pytest.approx(sum(a[j] * W21[0, j, c] for j in range(2)), rel=1e-12)
+
+
+def test_forward_permutation_equivariance():
+    X, W1, W2, S, dO, rt = rand_case(4, 40, 6, 3, 6, 2)
+    P = np.random.default_rng(9).permutation(40)
+    rtp = om.route(S[P], 2)
+    assert np.allclose(om.forward(X[P], W1, W2, rtp).O, om.forward(X, W1, W2, rt).O[P], rtol=0, atol=1e-13)
+
+
+# ------------------------------------------------------------------ backward
+def test_backward_finite_differences():
+    """>= 20 seeds, T<=32, d<=8, n<=4, E<=8, K<=4; h=1e-5; 1e-6 rel."""
+    for seed in range(20):
+        rng = np.random.default_rng(100 + seed)
+        T, d, n, E = int(rng.integers(4, 33)), int(rng.integers(2, 9)), int(rng.integers(1, 5)), int(rng.integers(1, 9))
+        K = int(rng.integers(1, min(4, E) + 1))
+        X, W1, W2, S, _, rt = rand_case(seed, T, d, n, E, K)
+        G = rng.standard_normal((T, d))                          # L = sum G * O  =>  dO = G
+        bw = om.backward(G, X, W1, W2, rt)
+
+        def check(an, fd):
+            for i, v in fd.items():
+                ref = an.reshape(-1)[i]
+                if abs(v) > 1e-8:
+                    assert ref == pytest.approx(v, rel=1e-6)
+                else:
+                    assert abs(ref - v) < 1e-10
+
+        pick = lambda a: rng.choice(a.size, size=min(a.size, 12), replace=False)
+        check(bw.dX, om.fd_grad(lambda x: om.loss_fixed_routing(x, W1, W2, rt.kept, rt.gate, G), X, coords=pick(X)))
+        check(bw.dW1, om.fd_grad(lambda w: om.loss_fixed_routing(X, w, W2, rt.kept, rt.gate, G), W1, coords=pick(W1)))
+        check(bw.dW2, om.fd_grad(lambda w: om.loss_fixed_routing(X, W1, w, rt.kept, rt.gate, G), W2, coords=pick(W2)))
+        # dS = dL/dg for each kept (t, e)
+        gfd = om.fd_grad(lambda g: om.loss_fixed_routing(X, W1, W2, rt.kept, g, G), rt.gate)
+        for e, toks in enumerate(np.nonzero(rt.kept[:, e])[0] for e in range(E)):
+            for i, t in enumerate(toks):
+                v = gfd[t * E + e]
+                assert bw.dS[e][i] == pytest.approx(v, rel=1e-6, abs=1e-10)
+
+
+def test_backward_dual_path_identity():
+    """App. C: memory-efficient == Y/dY path to 1e-12, 50 seeds."""
+    for seed in range(50):
+        X, W1, W2, S, dO, rt = rand_case(seed, 24, 8, 4, 6, 3, mode="tc" if seed % 2 else "tr")
+        a, b = om.backward(dO, X, W1, W2, rt), om.backward_reference(dO, X, W1, W2, rt)
+        for name in ("dX", "dW1", "dW2"):
+            assert np.max(np.abs(getattr(a, name) - getattr(b, name))) < 1e-12
+        for e in a.dS:
+            assert np.max(np.abs(a.dS[e] - b.dS[e]), initial=0) < 1e-12
+            assert np.max(np.abs(a.dH[e] - b.dH[e]), initial=0) < 1e-12
+
+
+def test_backward_zero_dO():
+    X, W1, W2, S, dO, rt = rand_case(1, 16, 4, 2, 4, 2)
+    bw = om.backward(np.zeros_like(dO), X, W1, W2, rt)
+    assert not bw.dX.any() and not bw.dW1.any() and not bw.dW2.any()
+    assert all(not v.any() for v in bw.dS.values())
+
+
+def test_backward_uses_cached_H():
+    X, W1, W2, S, dO, rt = rand_case(3, 32, 8, 4, 4, 2)
+    fw = om.forward(X, W1, W2, rt)
+    a = om.backward(dO, X, W1, W2, rt)
+    b = om.backward(dO, X, W1, W2, rt, H_cache=fw.H)
+    assert np.allclose(a.dW1, b.dW1, atol=1e-13)
+
+
+# ------------------------------------------------------------------ closed forms
+def test_cost_spot_values():
+    c = GOLD["cost"]
+    assert om.model_flops(c["T"], c["d"], c["n"], c["K"]) == c["flops"]
+    assert om.activation_bytes(c["T"], c["d"], c["n"], c["K"]) == c["act_bytes"]
+    assert om.arithmetic_intensity(c["T"], c["d"], c["n"], c["E"], c["K"]) == pytest.approx(c["ai"], abs=0.01)
+    # iso-FLOP granularity invariance of the minimal activation set
+    assert om.activation_bytes(24576, 1536, 512, 4) == om.activation_bytes(24576, 1536, 256, 8)
