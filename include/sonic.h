@@ -1,0 +1,159 @@
+/*
+ * sonic.h -- C ABI of libsonic, a B200 (sm_100a) implementation of the hot path
+ * of SonicMoE (arXiv 2512.14080): the forward and backward pass of a
+ * fine-grained sparse MoE expert layer.
+ *
+ * Citations: P:n = line n of the paper text; S:n = SPEC.md line n;
+ * Qk = reading k in DESIGN.md section 3.
+ *
+ * Conventions (all entry points):
+ *  - Every tensor pointer is a DEVICE pointer, row-major, caller-allocated and
+ *    caller-owned.  bf16 tensors are passed as `const void *` (2-byte elements).
+ *  - `stream` is a cudaStream_t passed as `void *` (NULL = legacy default stream).
+ *  - sonic_route / sonic_moe_fwd / sonic_moe_bwd are asynchronous on `stream`:
+ *    they allocate nothing, never synchronise the host with the device and never
+ *    copy device data to the host.  The routed row count R lives on the device
+ *    (routing.pad_offsets[E]); buffers are sized with the host-side upper bound
+ *    sonic_rows_max().
+ *  - Validation is synchronous and happens before any launch: a bad argument
+ *    returns SONIC_ERR_INVALID_ARG (or SONIC_ERR_UNSUPPORTED for a legal shape
+ *    the kernels do not cover; SONIC_ERR_WORKSPACE for a short workspace) and
+ *    launches nothing.  A failed launch returns SONIC_ERR_CUDA.  Device-side
+ *    index checks do not exist in release builds.  No C++ exception crosses
+ *    the ABI.
+ *  - Supported shapes: 1 <= K <= min(E, 16), E <= 4096 (the paper's top-K range,
+ *    P:1076), d % 64 == 0, n == 32 or n % 64 == 0, m_tile == 128 (the GEMM M
+ *    tile, P:1238 footnote "M_tile is GPU-dependent", Q16),
+ *    T*K + E*127 < 2^31.  All pointers 16-byte aligned.
+ *
+ * Grouped-row layout.  Expert e owns the grouped rows
+ * [pad_offsets[e], pad_offsets[e+1]); the first f_rounded[e] of them hold e's
+ * kept tokens in ascending token order (Q17), the rest (< 128, TC mode only)
+ * are pad rows with row_token = -1 and row_gate = 0.  pad_offsets[e] is a
+ * multiple of 128, so every 128-row GEMM tile belongs to exactly one expert.
+ * Under token rounding every f_rounded[e] is a multiple of 128 and there are no
+ * pad rows.  All values computed on pad rows are exactly zero.
+ */
+#ifndef SONIC_H
+#define SONIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SONIC_OK = 0,
+  SONIC_ERR_INVALID_ARG = -1,
+  SONIC_ERR_UNSUPPORTED = -2,
+  SONIC_ERR_WORKSPACE = -3,
+  SONIC_ERR_CUDA = -4,
+  SONIC_ERR_NCCL = -5
+} sonic_status;
+
+typedef enum {
+  SONIC_ROUTE_TC = 0,      /* token-choice top-K */
+  SONIC_ROUTE_TR_NRF = 1   /* token rounding, Alg. 4 with NR-f */
+} sonic_route_mode;
+
+/* flags */
+#define SONIC_F_GATE_RAW         1  /* gate = S_te (no renormalisation over the kept set, Q13) */
+#define SONIC_F_NO_ORPHAN_RESCUE 2  /* TR: skip the orphan rescue (Q14) */
+
+typedef struct {
+  int64_t T;           /* tokens in the microbatch */
+  int32_t d, n;        /* embedding dim, expert intermediate dim (H has 2n columns: [gate | up], Q1) */
+  int32_t E, K;        /* experts, experts per token */
+  int32_t m_tile;      /* TR rounding tile; must be 128 (the GEMM M tile) */
+  int32_t route_mode;  /* sonic_route_mode */
+  int32_t flags;       /* SONIC_F_* */
+} sonic_moe_desc;
+
+/* Routing metadata: written by sonic_route, read by sonic_moe_fwd/bwd.
+ * Sizes in elements; byte sizes via sonic_routing_sizes().  All device memory. */
+typedef struct {
+  int32_t *topk_ids;     /* [T,K]  TC choice, value-descending, ties -> lower expert id (Q9) */
+  float   *topk_s;       /* [T,K]  the chosen scores */
+  int32_t *f;            /* [E]    TC token count per expert (Alg. 4 step (2)) */
+  int32_t *f_rounded;    /* [E]    kept count per expert (== f under TC) */
+  int32_t *offsets;      /* [E+1]  exclusive prefix of f_rounded */
+  int32_t *pad_offsets;  /* [E+1]  exclusive prefix of ceil(f_rounded/128)*128; pad_offsets[E] = R_pad */
+  int32_t *row_token;    /* [rows_max] token of each grouped row (the gather map); -1 on pad rows */
+  float   *row_gate;     /* [rows_max] gate g_te of each grouped row; 0 on pad rows */
+  int32_t *token_rowptr; /* [T+1]  CSR over tokens */
+  int32_t *token_rows;   /* [rows_max] grouped rows of each token, expert-ascending (the scatter map) */
+  int32_t *tile_expert;  /* [rows_max/128] expert owning each 128-row tile */
+  int32_t *num_tiles;    /* [1]    R_pad / 128 */
+} sonic_routing;
+
+#define SONIC_ROUTING_NFIELDS 12
+
+/* Upper bound on grouped rows (incl. pad rows): min(T*K + E*127, E*ceil(T/128)*128),
+ * rounded up to a multiple of 128.  Returns -1 on an invalid descriptor. */
+int64_t sonic_rows_max(const sonic_moe_desc *desc);
+
+/* Byte size of each sonic_routing field, in declaration order. */
+sonic_status sonic_routing_sizes(const sonic_moe_desc *desc, size_t bytes_out[SONIC_ROUTING_NFIELDS]);
+
+size_t sonic_route_workspace_size(const sonic_moe_desc *desc);
+size_t sonic_fwd_workspace_size(const sonic_moe_desc *desc);  /* A [rows_max,n] + Y [rows_max,d] (bf16) */
+size_t sonic_bwd_workspace_size(const sonic_moe_desc *desc);  /* dH, A', dX~ (bf16) + dS partials (fp32) */
+
+/* Byte offsets of the named transients inside the fwd / bwd workspace, for
+ * inspection by tests: fwd {A, Y}; bwd {dH, A_prime, dXt, dS_part}.  which = 0 (fwd) or 1 (bwd). */
+sonic_status sonic_workspace_offsets(const sonic_moe_desc *desc, int which, size_t offs_out[4]);
+
+/*
+ * sonic_route -- router top-K, counts, token rounding and the index build
+ * (Alg. 4; TC routing P:358; "routing metadata computation" P:944).
+ *   S      [T,E] fp32 router scores (softmax probabilities; router GEMM and softmax
+ *          are the caller's, P:284 footnote).  Finite values only (Q24).  TR needs
+ *          the full S, not only the top-K entries (Q10).
+ *   out    routing metadata, every field written (rows past pad_offsets[E] untouched).
+ * Integer outputs are deterministic and equal the fp64 oracle's bit for bit.
+ * Gate: g_te = S_te / sum_{e' kept for t} S_te' (fp32, ascending-e sum), or S_te
+ * with SONIC_F_GATE_RAW.
+ */
+sonic_status sonic_route(const sonic_moe_desc *desc, const float *S, sonic_routing *out,
+                         void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * sonic_moe_fwd -- Alg. 2: up-proj A kernel (gather fused, SwiGLU
+ * epilogue), down-proj Y kernel (gate applied in the epilogue, Q2), expert
+ * aggregation O kernel (gather-and-sum, no atomics).
+ *   X  [T,d] bf16;  W1 [E,d,2n] bf16;  W2 [E,n,d] bf16;  rt from sonic_route.
+ *   O        [T,d] bf16 output.
+ *   H_cache  [rows_max,2n] bf16 output: H = X_e W1_e per grouped row, the only
+ *            activation kept for the backward (section 3.2).
+ */
+sonic_status sonic_moe_fwd(const sonic_moe_desc *desc, const void *X, const void *W1, const void *W2,
+                           const sonic_routing *rt, void *O, void *H_cache,
+                           void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * sonic_moe_bwd -- Alg. 3 + Alg. 5: dH kernel (gather
+ * of dO fused; epilogue recomputes A from H, applies dSwiGLU, writes dH, A' and
+ * dS = <dA', A>), dW2 = A'^T dO_e, dX~ = dH W1_e^T, dW1 = X_e^T dH,
+ * dX aggregation.
+ *   dO [T,d] bf16; X, H_cache, W1, W2, rt as in the forward.
+ *   dX  [T,d] bf16 output.
+ *   dW1 [E,d,2n] fp32, dW2 [E,n,d] fp32 outputs, overwritten (experts with no rows get 0).
+ *   dS  [rows_max] fp32 output: dL/dg for each grouped row (0 on pad rows).  The router
+ *       backward (renormalisation/softmax Jacobian) is outside the boundary.
+ */
+sonic_status sonic_moe_bwd(const sonic_moe_desc *desc, const void *dO, const void *X, const void *H_cache,
+                           const void *W1, const void *W2, const sonic_routing *rt,
+                           void *dX, float *dW1, float *dW2, float *dS,
+                           void *ws, size_t ws_bytes, void *stream);
+
+const char *sonic_status_string(sonic_status s);
+
+/* Number of kernels the last sonic_route/fwd/bwd call on this thread launched. */
+int sonic_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SONIC_H */

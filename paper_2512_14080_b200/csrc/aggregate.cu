@@ -1,0 +1,84 @@
+// aggregate.cu -- expert aggregation (Alg. 2 "Expert aggregation O kernel", and
+// Alg. 5 "Expert aggregation dX kernel"): each token gathers its grouped rows
+// and sums them (store-then-gather-sum, no atomics, deterministic; Fig. 7 left).
+// The gate is already applied in the down-proj epilogue (Q2), so one unweighted kernel
+// serves O and dX.  HBM-bound: reads R*d*2 B, writes T*d*2 B.
+#include "sonic_internal.h"
+
+namespace sonic {
+
+__device__ __forceinline__ void acc8(float (&a)[8], const uint4& v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    a[2 * i] += f.x;
+    a[2 * i + 1] += f.y;
+  }
+}
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// One warp per token; lanes stride over 16-byte column chunks; rows summed in CSR order.
+__global__ void __launch_bounds__(256) k_aggregate(const __nv_bfloat16* __restrict__ Y, const int* __restrict__ rowptr,
+                                                   const int* __restrict__ rows, __nv_bfloat16* __restrict__ out,
+                                                   long long T, int d) {
+  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int r0 = __ldg(rowptr + t), r1 = __ldg(rowptr + t + 1);
+  const int nch = d >> 3;
+  const uint4* Yv = reinterpret_cast<const uint4*>(Y);
+  uint4* Ov = reinterpret_cast<uint4*>(out + t * d);
+  for (int c = lane; c < nch; c += 32) {
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    int j = r0;
+    for (; j + 4 <= r1; j += 4) {
+      const int q0 = __ldg(rows + j), q1 = __ldg(rows + j + 1), q2 = __ldg(rows + j + 2), q3 = __ldg(rows + j + 3);
+      const uint4 v0 = ldg_stream(Yv + (long long)q0 * nch + c);
+      const uint4 v1 = ldg_stream(Yv + (long long)q1 * nch + c);
+      const uint4 v2 = ldg_stream(Yv + (long long)q2 * nch + c);
+      const uint4 v3 = ldg_stream(Yv + (long long)q3 * nch + c);
+      acc8(a, v0);
+      acc8(a, v1);
+      acc8(a, v2);
+      acc8(a, v3);
+    }
+    for (; j < r1; ++j) acc8(a, ldg_stream(Yv + (long long)__ldg(rows + j) * nch + c));
+    uint4 o;
+    __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) oh[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+    Ov[c] = o;
+  }
+}
+
+__global__ void k_ds_reduce(const float* __restrict__ part, int nparts, long long rows_max,
+                            const int* __restrict__ num_tiles, float* __restrict__ dS) {
+  const long long R = (long long)(*num_tiles) * GEMM_M;
+  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (long long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int j = 0; j < nparts; ++j) s += part[j * rows_max + r];
+    dS[r] = s;
+  }
+}
+
+void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows, __nv_bfloat16* out, long long T,
+                      int d, cudaStream_t st) {
+  const int threads = 256;
+  const long long blocks = (T * 32 + threads - 1) / threads;
+  k_aggregate<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
+}
+
+void launch_ds_reduce(const float* part, int nparts, long long rows_max, const int* num_tiles, float* dS,
+                      cudaStream_t st) {
+  k_ds_reduce<<<148 * 4, 256, 0, st>>>(part, nparts, rows_max, num_tiles, dS);
+}
+
+}  // namespace sonic

@@ -1,0 +1,429 @@
+// route.cu -- routing / metadata kernels of sonic_route.
+//
+// Data structure: per-expert token bitmaps bm[e][w] (bit t%32 of word t/32 set when token
+// t is routed to e).  Every integer output is a pure function of the bitmaps, built with
+// order-independent atomicOr, so the metadata is deterministic and canonical: segments
+// hold tokens in ascending order (popcount prefix over words), the token CSR lists
+// experts in ascending order.
+//
+//   k_route_topk     TC top-K per token (warp per token, exact 64-bit keys: ordered fp32
+//                    score, ties -> lower expert id, Q9) -> topk, TC bitmap
+//   k_expert_popc    per-expert popcount + exclusive word prefix (histogram f_e)
+//   k_tr_decide      NR-f rounding decision
+//   k_transpose      S -> S^T so expert columns are contiguous (TR only)
+//   k_tr_select      Alg. 4 step (4): per expert, keep the top f_r of the ranking
+//                    (in-TC, S, -t) via radix select on the ordered score + token tie pass
+//   k_orphans        tokens with no kept expert flag their top-1 expert (Q14 rescue)
+//   k_offsets        offsets, tile-aligned pad_offsets, tile -> expert map
+//   k_build_rows     gather map row_token (+ pad rows)
+//   k_token_count / k_scan_tokens / k_token_rows   token CSR and renormalised gates
+#include "sonic_internal.h"
+
+namespace sonic {
+
+__device__ __forceinline__ uint32_t ord_f32(float x) {
+  uint32_t b = __float_as_uint(x);
+  if (b == 0x80000000u) b = 0u;  // -0 == +0 (Q23)
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// ---------------------------------------------------------------- block scan helpers
+// Exclusive scan of v over the block (blockDim.x <= 1024, multiple of 32); returns the
+// exclusive prefix and writes the block total to *total.
+__device__ int block_excl_scan(int v, int* total) {
+  __shared__ int warp_sums[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int s = lane < nw ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    warp_sums[lane] = s;  // inclusive
+  }
+  __syncthreads();
+  int base = wid > 0 ? warp_sums[wid - 1] : 0;
+  int tot = warp_sums[nw - 1];
+  __syncthreads();
+  *total = tot;
+  return base + x - v;
+}
+
+// ---------------------------------------------------------------- top-K
+template <int VPL>
+__global__ void k_route_topk(const float* __restrict__ S, int T, int E, int K, int W, int* __restrict__ topk_ids,
+                             float* __restrict__ topk_s, uint32_t* __restrict__ bm_tc) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const float* row = S + (size_t)t * E;
+  unsigned long long key[VPL];
+#pragma unroll
+  for (int j = 0; j < VPL; ++j) {
+    const int e = lane + 32 * j;
+    key[j] = e < E ? ((unsigned long long)ord_f32(__ldg(row + e)) << 32) | (0xFFFFFFFFu - (uint32_t)e) : 0ull;
+  }
+  for (int k = 0; k < K; ++k) {
+    unsigned long long best = 0;
+#pragma unroll
+    for (int j = 0; j < VPL; ++j) best = key[j] > best ? key[j] : best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+      best = other > best ? other : best;
+    }
+#pragma unroll
+    for (int j = 0; j < VPL; ++j)
+      if (key[j] == best) key[j] = 0ull;
+    const int e = (int)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull));
+    if (lane == 0) {
+      topk_ids[(size_t)t * K + k] = e;
+      topk_s[(size_t)t * K + k] = __ldg(row + e);
+      atomicOr(bm_tc + (size_t)e * W + (t >> 5), 1u << (t & 31));
+    }
+  }
+}
+
+// ---------------------------------------------------------------- per-expert popcount
+__global__ void k_expert_popc(const uint32_t* __restrict__ bm, int W, int* __restrict__ wprefix,
+                              int* __restrict__ cnt) {
+  const int e = blockIdx.x;
+  int base = 0;
+  for (int w0 = 0; w0 < W; w0 += blockDim.x) {
+    const int w = w0 + threadIdx.x;
+    const int c = w < W ? __popc(bm[(size_t)e * W + w]) : 0;
+    int tot;
+    const int ex = block_excl_scan(c, &tot);
+    if (wprefix && w < W) wprefix[(size_t)e * W + w] = base + ex;
+    base += tot;
+  }
+  if (threadIdx.x == 0) cnt[e] = base;
+}
+
+// ---------------------------------------------------------------- TR decision (NR-f)
+__global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, int E, int T, int M) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const int fe = f[e];
+    const int up = min((fe + M - 1) / M * M, T);
+    const int dn = fe / M * M;
+    f_r[e] = (up - fe) < (fe - dn) ? up : dn;  // strict '<': exact M/2 ties round down (Q11)
+  }
+}
+
+// ---------------------------------------------------------------- S -> S^T
+__global__ void k_transpose(const float* __restrict__ S, float* __restrict__ ST, int T, int E) {
+  __shared__ float tile[32][33];
+  const int e0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int t = t0 + i, e = e0 + threadIdx.x;
+    tile[i][threadIdx.x] = (t < T && e < E) ? S[(size_t)t * E + e] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int e = e0 + i, t = t0 + threadIdx.x;
+    if (e < E && t < T) ST[(size_t)e * T + t] = tile[threadIdx.x][i];
+  }
+}
+
+// ---------------------------------------------------------------- TR selection
+// One block (1024 threads) per expert.  rescue == 0: every expert, f_r from k_tr_decide.
+// rescue == 1: only experts flagged by k_orphans; they round up (f_r = min(ceil, T)).
+// Selects the k largest candidates by (ordered S desc, token asc): down -> candidates are the
+// TC tokens, k = f_r; up -> candidates are the non-TC tokens, k = f_r - f (Alg. 4, Q10).
+__global__ void __launch_bounds__(1024) k_tr_select(const float* __restrict__ ST, int T, int W, int M,
+                                                    const uint32_t* __restrict__ bm_tc,
+                                                    uint32_t* __restrict__ bm_kept, const int* __restrict__ f,
+                                                    int* __restrict__ f_r, const int* __restrict__ flip, int rescue) {
+  __shared__ int hist[4096];
+  __shared__ int s_digit, s_above, s_run;
+  const int e = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int fc = f[e];
+  int fr;
+  if (rescue) {
+    if (!flip[e]) return;
+    fr = min((fc + M - 1) / M * M, T);
+    if (tid == 0) f_r[e] = fr;
+  } else {
+    fr = f_r[e];
+  }
+  const uint32_t* tcw = bm_tc + (size_t)e * W;
+  uint32_t* kw = bm_kept + (size_t)e * W;
+  if (fr == fc) {
+    for (int w = tid; w < W; w += blockDim.x) kw[w] = tcw[w];
+    return;
+  }
+  const bool up = fr > fc;
+  int k = up ? fr - fc : fr;
+  if (k == 0) {  // down to zero: drop every token
+    for (int w = tid; w < W; w += blockDim.x) kw[w] = 0u;
+    return;
+  }
+  const float* col = ST + (size_t)e * T;
+  uint32_t prefix = 0, pmask = 0;
+  const int shifts[3] = {20, 8, 0};
+  const int bits[3] = {12, 12, 8};
+  for (int p = 0; p < 3; ++p) {
+    const int sh = shifts[p], nb = 1 << bits[p];
+    for (int i = tid; i < nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int t = tid; t < T; t += blockDim.x) {
+      const bool is_tc = (tcw[t >> 5] >> (t & 31)) & 1u;
+      if (is_tc != up) {
+        const uint32_t o = ord_f32(col[t]);
+        if ((o & pmask) == prefix) atomicAdd(&hist[(o >> sh) & (nb - 1)], 1);
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {  // find the digit holding the k-th largest, scanning bins from the top
+      const int per = nb / 32;
+      const int hi = nb - 1 - tid * per;  // this lane's bins: hi, hi-1, ..., hi-per+1
+      int s = 0;
+      for (int b = 0; b < per; ++b) s += hist[hi - b];
+      int incl = s;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      const unsigned ball = __ballot_sync(0xffffffffu, incl >= k);
+      const int L = __ffs(ball) - 1;
+      if (tid == L) {
+        int cum = incl - s;
+        for (int b = 0; b < per; ++b) {
+          const int h = hist[hi - b];
+          if (cum + h >= k) {
+            s_digit = hi - b;
+            s_above = cum;
+            break;
+          }
+          cum += h;
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint32_t)s_digit << sh;
+    pmask |= (uint32_t)(nb - 1) << sh;
+    k -= s_above;
+    __syncthreads();
+  }
+  // threshold = prefix; keep all candidates above it and the first k (lowest token ids) equal to it
+  if (tid == 0) s_run = 0;
+  __syncthreads();
+  const int Tpad = (T + blockDim.x - 1) / blockDim.x * blockDim.x;
+  for (int t0 = 0; t0 < Tpad; t0 += blockDim.x) {
+    const int t = t0 + tid;
+    bool cand = false;
+    uint32_t o = 0;
+    if (t < T) {
+      const bool is_tc = (tcw[t >> 5] >> (t & 31)) & 1u;
+      cand = is_tc != up;
+      if (cand) o = ord_f32(col[t]);
+    }
+    const int eq = (cand && o == prefix) ? 1 : 0;
+    int tot;
+    const int ex = block_excl_scan(eq, &tot);
+    const int run = s_run;
+    const bool sel = cand && (o > prefix || (eq && run + ex < k));
+    const unsigned word = __ballot_sync(0xffffffffu, sel);
+    if ((tid & 31) == 0 && t < T) {
+      const int w = t >> 5;
+      kw[w] = up ? (tcw[w] | word) : word;
+    }
+    __syncthreads();
+    if (tid == 0) s_run = run + tot;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- orphan detection
+// Warp per 32-token word.  A token kept by no expert flags its top-1 TC expert.
+__global__ void k_orphans(const uint32_t* __restrict__ bm_kept, int T, int E, int W, int K,
+                          const int* __restrict__ topk_ids, int* __restrict__ flip) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= W) return;
+  uint32_t acc = 0;
+  for (int e = lane; e < E; e += 32) acc |= bm_kept[(size_t)e * W + w];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc |= __shfl_xor_sync(0xffffffffu, acc, o);
+  const int t = w * 32 + lane;
+  if (t < T && !((acc >> lane) & 1u)) flip[topk_ids[(size_t)t * K]] = 1;
+}
+
+// ---------------------------------------------------------------- offsets & tiles
+__global__ void __launch_bounds__(1024) k_offsets(const int* __restrict__ f_r, int E, int* __restrict__ offsets,
+                                                  int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
+                                                  int* __restrict__ num_tiles) {
+  __shared__ int s_pad[4097];
+  int base = 0, pbase = 0;
+  for (int e0 = 0; e0 < E; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    const int c = e < E ? f_r[e] : 0;
+    const int pc = (c + GEMM_M - 1) / GEMM_M * GEMM_M;
+    int tot, ptot;
+    const int ex = block_excl_scan(c, &tot);
+    const int pex = block_excl_scan(pc, &ptot);
+    if (e < E) {
+      offsets[e] = base + ex;
+      pad_offsets[e] = pbase + pex;
+      s_pad[e] = pbase + pex;
+    }
+    base += tot;
+    pbase += ptot;
+  }
+  if (threadIdx.x == 0) {
+    offsets[E] = base;
+    pad_offsets[E] = pbase;
+    s_pad[E] = pbase;
+    *num_tiles = pbase / GEMM_M;
+  }
+  __syncthreads();
+  const int nt = pbase / GEMM_M;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) {
+    const int r = i * GEMM_M;
+    int lo = 0, hi = E - 1;  // largest e with s_pad[e] <= r  (then s_pad[e+1] > r)
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pad[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    tile_expert[i] = lo;
+  }
+}
+
+// ---------------------------------------------------------------- gather map
+__global__ void k_build_rows(const uint32_t* __restrict__ bm_kept, const int* __restrict__ wprefix, int W,
+                             const int* __restrict__ f_r, const int* __restrict__ pad_offsets,
+                             int* __restrict__ row_token, float* __restrict__ row_gate) {
+  const int e = blockIdx.y;
+  const int base = pad_offsets[e];
+  const int w = blockIdx.x * blockDim.x + threadIdx.x;
+  if (w < W) {
+    uint32_t bits = bm_kept[(size_t)e * W + w];
+    int r = base + wprefix[(size_t)e * W + w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      row_token[r++] = w * 32 + b;
+      bits &= bits - 1;
+    }
+  }
+  if (blockIdx.x == 0) {  // pad rows of this expert's last tile
+    for (int r = base + f_r[e] + threadIdx.x; r < pad_offsets[e + 1]; r += blockDim.x) {
+      row_token[r] = -1;
+      row_gate[r] = 0.f;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- token CSR
+__global__ void k_token_count(const uint32_t* __restrict__ bm_kept, int T, int E, int W, int* __restrict__ cnt) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= W) return;
+  int c = 0;
+  for (int e = 0; e < E; ++e) c += (__ldg(bm_kept + (size_t)e * W + w) >> lane) & 1u;
+  const int t = w * 32 + lane;
+  if (t < T) cnt[t] = c;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_tokens(const int* __restrict__ cnt, int T, int* __restrict__ rowptr) {
+  int base = 0;
+  for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+    const int t = t0 + threadIdx.x;
+    const int c = t < T ? cnt[t] : 0;
+    int tot;
+    const int ex = block_excl_scan(c, &tot);
+    if (t < T) rowptr[t] = base + ex;
+    base += tot;
+  }
+  if (threadIdx.x == 0) rowptr[T] = base;
+}
+
+__global__ void k_token_rows(const uint32_t* __restrict__ bm_kept, const int* __restrict__ wprefix, int T, int E,
+                             int W, const int* __restrict__ pad_offsets, const int* __restrict__ rowptr,
+                             const float* __restrict__ S, int gate_raw, int* __restrict__ token_rows,
+                             float* __restrict__ row_gate) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= W) return;
+  const int t = w * 32 + lane;
+  const bool valid = t < T;
+  const uint32_t below = (1u << lane) - 1u;
+  int j = valid ? rowptr[t] : 0;
+  float sum = 0.f;
+  for (int e = 0; e < E; ++e) {
+    const uint32_t word = __ldg(bm_kept + (size_t)e * W + w);
+    if (valid && ((word >> lane) & 1u)) {
+      token_rows[j++] = pad_offsets[e] + wprefix[(size_t)e * W + w] + __popc(word & below);
+      sum += __ldg(S + (size_t)t * E + e);
+    }
+  }
+  const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
+  j = valid ? rowptr[t] : 0;
+  for (int e = 0; e < E; ++e) {
+    const uint32_t word = __ldg(bm_kept + (size_t)e * W + w);
+    if (valid && ((word >> lane) & 1u)) {
+      const float s = __ldg(S + (size_t)t * E + e);
+      row_gate[token_rows[j++]] = gate_raw ? s : s * inv;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launcher
+int launch_route(const RouteLaunch& L, cudaStream_t st) {
+  int nl = 0;
+  const int T = (int)L.T, E = L.E, K = L.K, W = L.W;
+  cudaMemsetAsync(L.bm_tc, 0, (size_t)E * W * 4, st);
+  {
+    const int vpl = (E + 31) / 32;
+    const int threads = 256, blocks = (T * 32 + threads - 1) / threads;
+#define TOPK_CASE(V) \
+  k_route_topk<V><<<blocks, threads, 0, st>>>(L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
+    if (vpl <= 1) TOPK_CASE(1);
+    else if (vpl <= 2) TOPK_CASE(2);
+    else if (vpl <= 4) TOPK_CASE(4);
+    else if (vpl <= 8) TOPK_CASE(8);
+    else if (vpl <= 12) TOPK_CASE(12);
+    else if (vpl <= 16) TOPK_CASE(16);
+    else if (vpl <= 32) TOPK_CASE(32);
+    else if (vpl <= 64) TOPK_CASE(64);
+    else TOPK_CASE(128);
+#undef TOPK_CASE
+    ++nl;
+  }
+  k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, nullptr, L.f); ++nl;
+  const uint32_t* bm_kept = L.bm_tc;
+  if (L.mode == 1) {  // token rounding
+    k_tr_decide<<<(E + 255) / 256, 256, 0, st>>>(L.f, L.f_r, E, T, L.m_tile); ++nl;
+    k_transpose<<<dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st>>>(L.S, L.ST, T, E); ++nl;
+    k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0); ++nl;
+    if (L.rescue) {
+      cudaMemsetAsync(L.flip, 0, (size_t)E * 4, st);
+      k_orphans<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;
+      k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1); ++nl;
+    }
+    bm_kept = L.bm_kept;
+    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r); ++nl;
+  } else {
+    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r); ++nl;
+  }
+  k_offsets<<<1, 1024, 0, st>>>(L.f_r, E, L.offsets, L.pad_offsets, L.tile_expert, L.num_tiles); ++nl;
+  k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
+                                                         L.row_gate); ++nl;
+  k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, T, E, W, L.tokcnt); ++nl;
+  k_scan_tokens<<<1, 1024, 0, st>>>(L.tokcnt, T, L.token_rowptr); ++nl;
+  k_token_rows<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, L.wprefix, T, E, W, L.pad_offsets, L.token_rowptr,
+                                                     L.S, L.gate_raw, L.token_rows, L.row_gate); ++nl;
+  return nl;
+}
+
+}  // namespace sonic

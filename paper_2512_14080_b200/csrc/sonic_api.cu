@@ -1,0 +1,428 @@
+// sonic_api.cu -- the C ABI of include/sonic.h: validation, workspace layout, TMA tensor
+// maps, and the launch sequences of sonic_route / sonic_moe_fwd / sonic_moe_bwd.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "../../include/sonic.h"
+#include "gemm.cuh"
+#include "sonic_internal.h"
+
+using namespace sonic;
+
+namespace {
+
+thread_local int g_launches = 0;
+
+// ---------------------------------------------------------------- tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D row-major [rows, cols] tensor; box {box_cols, box_rows}; 128B swizzle.
+bool map2d(CUtensorMap* m, const void* ptr, bool f32, long long rows, long long cols, int box_cols, int box_rows) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  const int es = f32 ? 4 : 2;
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)(cols * es)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr),
+             gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// 3-D row-major [E, rows, cols] tensor; box {box_cols, box_rows, 1}; 128B swizzle.
+bool map3d(CUtensorMap* m, const void* ptr, bool f32, long long E, long long rows, long long cols, int box_cols,
+           int box_rows) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  const int es = f32 ? 4 : 2;
+  cuuint64_t gdim[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)E};
+  cuuint64_t gstride[2] = {(cuuint64_t)(cols * es), (cuuint64_t)(rows * cols * es)};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr),
+             gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------- GEMM launch
+template <int KIND, int BN>
+bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
+                   const GemmArgs& args, int grid, cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(sonic_gemm_kernel<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) !=
+        cudaSuccess)
+      return false;
+    attr = true;
+  }
+  sonic_gemm_kernel<KIND, BN><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, c0, c1, args);
+  ++g_launches;
+  return true;
+}
+
+template <int KIND>
+bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
+                 const GemmArgs& args, int grid, cudaStream_t st) {
+  switch (BN) {
+    case 256: return launch_gemm_t<KIND, 256>(a, b, c0, c1, args, grid, st);
+    case 128: return launch_gemm_t<KIND, 128>(a, b, c0, c1, args, grid, st);
+    case 64: return launch_gemm_t<KIND, 64>(a, b, c0, c1, args, grid, st);
+    case 32:
+      if constexpr (KIND == K_DH) return launch_gemm_t<KIND, 32>(a, b, c0, c1, args, grid, st);
+      return false;
+    default: return false;
+  }
+}
+
+int pick_bn(long long N) { return N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64; }
+
+// ---------------------------------------------------------------- shapes & validation
+struct Shape {
+  long long T, rows_max;
+  int d, n, E, K, W;
+};
+
+bool valid_desc(const sonic_moe_desc* D) {
+  if (!D) return false;
+  if (D->T < 1 || D->d < 1 || D->n < 1 || D->E < 1 || D->K < 1) return false;
+  if (D->K > D->E || D->K > 16 || D->E > 4096) return false;
+  if (D->m_tile != 128) return false;
+  if (D->route_mode != SONIC_ROUTE_TC && D->route_mode != SONIC_ROUTE_TR_NRF) return false;
+  return true;
+}
+bool supported_dims(const sonic_moe_desc* D) {
+  if (D->d % 64 != 0) return false;
+  if (!(D->n == 32 || D->n % 64 == 0)) return false;
+  if (D->T * (long long)D->K + (long long)D->E * 127 >= (1ll << 31)) return false;
+  if ((long long)D->E * D->T >= (1ll << 40)) return false;
+  return true;
+}
+long long rows_max_of(const sonic_moe_desc* D) {
+  const long long a = D->T * D->K + (long long)D->E * (GEMM_M - 1);
+  const long long b = (long long)D->E * ((D->T + GEMM_M - 1) / GEMM_M) * GEMM_M;
+  const long long r = std::min(a, b);
+  return (r + GEMM_M - 1) / GEMM_M * GEMM_M;
+}
+Shape shape_of(const sonic_moe_desc* D) {
+  Shape s;
+  s.T = D->T;
+  s.d = D->d;
+  s.n = D->n;
+  s.E = D->E;
+  s.K = D->K;
+  s.W = (int)((D->T + 31) / 32);
+  s.rows_max = rows_max_of(D);
+  return s;
+}
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// route workspace layout
+struct RouteWs {
+  size_t bm_tc, bm_kept, wprefix, tokcnt, flip, ST, total;
+};
+RouteWs route_ws(const sonic_moe_desc* D) {
+  const Shape s = shape_of(D);
+  RouteWs w;
+  size_t o = 0;
+  const size_t bm = al((size_t)s.E * s.W * 4);
+  w.bm_tc = o; o += bm;
+  w.bm_kept = o; o += bm;
+  w.wprefix = o; o += bm;
+  w.tokcnt = o; o += al((size_t)s.T * 4);
+  w.flip = o; o += al((size_t)s.E * 4);
+  w.ST = o; o += (D->route_mode == SONIC_ROUTE_TR_NRF) ? al((size_t)s.T * s.E * 4) : 0;
+  w.total = o;
+  return w;
+}
+
+int dh_bn(int n) { return n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32; }
+
+struct FwdWs { size_t A, Y, total; };
+FwdWs fwd_ws(const sonic_moe_desc* D) {
+  const Shape s = shape_of(D);
+  FwdWs w;
+  size_t o = 0;
+  w.A = o; o += al((size_t)s.rows_max * s.n * 2);
+  w.Y = o; o += al((size_t)s.rows_max * s.d * 2);
+  w.total = o;
+  return w;
+}
+struct BwdWs { size_t dH, Ap, dXt, dSp, total; int dh_tiles; };
+BwdWs bwd_ws(const sonic_moe_desc* D) {
+  const Shape s = shape_of(D);
+  BwdWs w;
+  size_t o = 0;
+  w.dH = o; o += al((size_t)s.rows_max * 2 * s.n * 2);
+  w.Ap = o; o += al((size_t)s.rows_max * s.n * 2);
+  w.dXt = o; o += al((size_t)s.rows_max * s.d * 2);
+  w.dh_tiles = s.n / dh_bn(s.n);
+  w.dSp = o; o += w.dh_tiles > 1 ? al((size_t)w.dh_tiles * s.rows_max * 4) : 0;
+  w.total = o;
+  return w;
+}
+
+sonic_status check_launch() {
+  return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t sonic_rows_max(const sonic_moe_desc* desc) {
+  if (!valid_desc(desc)) return -1;
+  return rows_max_of(desc);
+}
+
+sonic_status sonic_routing_sizes(const sonic_moe_desc* D, size_t b[SONIC_ROUTING_NFIELDS]) {
+  if (!valid_desc(D) || !b) return SONIC_ERR_INVALID_ARG;
+  const Shape s = shape_of(D);
+  const size_t TK = (size_t)s.T * s.K;
+  b[0] = TK * 4;                              // topk_ids
+  b[1] = TK * 4;                              // topk_s
+  b[2] = (size_t)s.E * 4;                     // f
+  b[3] = (size_t)s.E * 4;                     // f_rounded
+  b[4] = (size_t)(s.E + 1) * 4;               // offsets
+  b[5] = (size_t)(s.E + 1) * 4;               // pad_offsets
+  b[6] = (size_t)s.rows_max * 4;              // row_token
+  b[7] = (size_t)s.rows_max * 4;              // row_gate
+  b[8] = (size_t)(s.T + 1) * 4;               // token_rowptr
+  b[9] = (size_t)s.rows_max * 4;              // token_rows
+  b[10] = (size_t)(s.rows_max / GEMM_M) * 4;  // tile_expert
+  b[11] = 4;                                  // num_tiles
+  return SONIC_OK;
+}
+
+size_t sonic_route_workspace_size(const sonic_moe_desc* D) { return valid_desc(D) ? route_ws(D).total : 0; }
+size_t sonic_fwd_workspace_size(const sonic_moe_desc* D) { return valid_desc(D) ? fwd_ws(D).total : 0; }
+size_t sonic_bwd_workspace_size(const sonic_moe_desc* D) { return valid_desc(D) ? bwd_ws(D).total : 0; }
+
+sonic_status sonic_workspace_offsets(const sonic_moe_desc* D, int which, size_t offs[4]) {
+  if (!valid_desc(D) || !offs) return SONIC_ERR_INVALID_ARG;
+  if (which == 0) {
+    const FwdWs w = fwd_ws(D);
+    offs[0] = w.A; offs[1] = w.Y; offs[2] = offs[3] = 0;
+  } else if (which == 1) {
+    const BwdWs w = bwd_ws(D);
+    offs[0] = w.dH; offs[1] = w.Ap; offs[2] = w.dXt; offs[3] = w.dSp;
+  } else {
+    return SONIC_ERR_INVALID_ARG;
+  }
+  return SONIC_OK;
+}
+
+const char* sonic_status_string(sonic_status s) {
+  switch (s) {
+    case SONIC_OK: return "ok";
+    case SONIC_ERR_INVALID_ARG: return "invalid argument";
+    case SONIC_ERR_UNSUPPORTED: return "unsupported shape";
+    case SONIC_ERR_WORKSPACE: return "workspace too small";
+    case SONIC_ERR_CUDA: return "CUDA launch failure";
+    case SONIC_ERR_NCCL: return "NCCL failure";
+  }
+  return "unknown status";
+}
+
+int sonic_last_launch_count(void) { return g_launches; }
+
+sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing* rt, void* ws, size_t ws_bytes,
+                         void* stream) {
+  g_launches = 0;
+  if (!valid_desc(D) || !S || !rt) return SONIC_ERR_INVALID_ARG;
+  if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
+  const RouteWs w = route_ws(D);
+  if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
+  void* ptrs[] = {rt->topk_ids, rt->topk_s, rt->f, rt->f_rounded, rt->offsets, rt->pad_offsets, rt->row_token,
+                  rt->row_gate, rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->num_tiles};
+  for (void* p : ptrs)
+    if (!p) return SONIC_ERR_INVALID_ARG;
+  if (!aligned16(S) || !aligned16(rt->row_token)) return SONIC_ERR_INVALID_ARG;
+  const Shape s = shape_of(D);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  RouteLaunch L{};
+  L.T = s.T; L.E = s.E; L.K = s.K; L.W = s.W; L.m_tile = D->m_tile;
+  L.mode = D->route_mode == SONIC_ROUTE_TR_NRF ? 1 : 0;
+  L.rescue = (D->flags & SONIC_F_NO_ORPHAN_RESCUE) ? 0 : 1;
+  L.gate_raw = (D->flags & SONIC_F_GATE_RAW) ? 1 : 0;
+  L.S = S;
+  L.topk_ids = rt->topk_ids; L.topk_s = rt->topk_s; L.f = rt->f; L.f_r = rt->f_rounded;
+  L.offsets = rt->offsets; L.pad_offsets = rt->pad_offsets; L.row_token = rt->row_token;
+  L.row_gate = rt->row_gate; L.token_rowptr = rt->token_rowptr; L.token_rows = rt->token_rows;
+  L.tile_expert = rt->tile_expert; L.num_tiles = rt->num_tiles;
+  L.bm_tc = reinterpret_cast<uint32_t*>(base + w.bm_tc);
+  L.bm_kept = reinterpret_cast<uint32_t*>(base + w.bm_kept);
+  L.wprefix = reinterpret_cast<int*>(base + w.wprefix);
+  L.tokcnt = reinterpret_cast<int*>(base + w.tokcnt);
+  L.flip = reinterpret_cast<int*>(base + w.flip);
+  L.ST = reinterpret_cast<float*>(base + w.ST);
+  g_launches = launch_route(L, static_cast<cudaStream_t>(stream));
+  return check_launch();
+}
+
+sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W1, const void* W2,
+                           const sonic_routing* rt, void* O, void* H, void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!valid_desc(D) || !X || !W1 || !W2 || !rt || !O || !H) return SONIC_ERR_INVALID_ARG;
+  if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
+  const FwdWs w = fwd_ws(D);
+  if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
+  for (const void* p : {X, W1, W2, (const void*)O, (const void*)H, (const void*)ws})
+    if (!aligned16(p)) return SONIC_ERR_INVALID_ARG;
+  const Shape s = shape_of(D);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  void* Abuf = base + w.A;
+  void* Ybuf = base + w.Y;
+  const int n = s.n, d = s.d, E = s.E;
+  const long long R = s.rows_max;
+  const int grid = num_sms();
+
+  GemmArgs g{};
+  g.num_m_tiles = rt->num_tiles; g.tile_expert = rt->tile_expert; g.row_token = rt->row_token;
+  g.row_gate = rt->row_gate; g.pad_offsets = rt->pad_offsets; g.E = E; g.n = n; g.rows_max = R;
+
+  // K1 up-proj: H = Gather(X) W1_e, SwiGLU epilogue -> H, A
+  {
+    CUtensorMap mA, mB, mC0, mC1;
+    const int Wg = n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
+    const int BN = 2 * Wg;
+    if (!map2d(&mA, X, false, s.T, d, 64, 1) || !map3d(&mB, W1, false, E, d, 2 * n, 64, 64) ||
+        !map2d(&mC0, H, false, R, 2 * n, 64, 32) || !map2d(&mC1, Abuf, false, R, n, 64, 32))
+      return SONIC_ERR_CUDA;
+    GemmArgs a = g;
+    a.n_tiles = n / Wg; a.k_blocks = d / 64; a.N_dim = 2 * n;
+    if (!launch_gemm<K_UP>(BN, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
+  }
+  // K2 down-proj: Y = gate * (A W2_e)
+  {
+    CUtensorMap mA, mB, mC0;
+    const int BN = pick_bn(d);
+    if (!map2d(&mA, Abuf, false, R, n, 64, 128) || !map3d(&mB, W2, false, E, n, d, 64, 64) ||
+        !map2d(&mC0, Ybuf, false, R, d, 64, 32))
+      return SONIC_ERR_CUDA;
+    GemmArgs a = g;
+    a.n_tiles = d / BN; a.k_blocks = (n + 63) / 64; a.N_dim = d;
+    if (!launch_gemm<K_DOWN>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
+  }
+  // K3 aggregation: O_t = sum of the token's Y rows
+  launch_aggregate(static_cast<const __nv_bfloat16*>(Ybuf), rt->token_rowptr, rt->token_rows,
+                   static_cast<__nv_bfloat16*>(O), s.T, d, st);
+  ++g_launches;
+  return check_launch();
+}
+
+sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* X, const void* H, const void* W1,
+                           const void* W2, const sonic_routing* rt, void* dX, float* dW1, float* dW2, float* dS,
+                           void* ws, size_t ws_bytes, void* stream) {
+  g_launches = 0;
+  if (!valid_desc(D) || !dO || !X || !H || !W1 || !W2 || !rt || !dX || !dW1 || !dW2 || !dS)
+    return SONIC_ERR_INVALID_ARG;
+  if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
+  const BwdWs w = bwd_ws(D);
+  if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
+  for (const void* p : {dO, X, H, W1, W2, (const void*)dX, (const void*)dW1, (const void*)dW2, (const void*)dS,
+                        (const void*)ws})
+    if (!aligned16(p)) return SONIC_ERR_INVALID_ARG;
+  const Shape s = shape_of(D);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  void* dH = base + w.dH;
+  void* Ap = base + w.Ap;
+  void* dXt = base + w.dXt;
+  float* dSp = reinterpret_cast<float*>(base + w.dSp);
+  const int n = s.n, d = s.d, E = s.E;
+  const long long R = s.rows_max;
+  const int grid = num_sms();
+
+  GemmArgs g{};
+  g.num_m_tiles = rt->num_tiles; g.tile_expert = rt->tile_expert; g.row_token = rt->row_token;
+  g.row_gate = rt->row_gate; g.pad_offsets = rt->pad_offsets; g.E = E; g.n = n; g.rows_max = R;
+
+  // K4 dH: dA' = Gather(dO) W2_e^T; epilogue dSwiGLU -> dH, A' = s A, dS = <dA', A>
+  {
+    CUtensorMap mA, mB, mC0, mC1;
+    const int BN = dh_bn(n);
+    if (!map2d(&mA, dO, false, s.T, d, 64, 1) || !map3d(&mB, W2, false, E, n, d, 64, BN) ||
+        !map2d(&mC0, dH, false, R, 2 * n, 64, 32) || !map2d(&mC1, Ap, false, R, n, 64, 32))
+      return SONIC_ERR_CUDA;
+    GemmArgs a = g;
+    a.n_tiles = n / BN; a.k_blocks = d / 64; a.N_dim = n; a.H = static_cast<const __nv_bfloat16*>(H);
+    a.dS = a.n_tiles > 1 ? dSp : dS;
+    if (!launch_gemm<K_DH>(BN, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
+    if (a.n_tiles > 1) {
+      launch_ds_reduce(dSp, a.n_tiles, R, rt->num_tiles, dS, st);
+      ++g_launches;
+    }
+  }
+  // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
+  {
+    CUtensorMap mA, mB, mC0;
+    const int BN = pick_bn(d);
+    if (!map2d(&mA, Ap, false, R, n, 64, 64) || !map2d(&mB, dO, false, s.T, d, 64, 1) ||
+        !map3d(&mC0, dW2, true, E, n, d, 32, 32))
+      return SONIC_ERR_CUDA;
+    GemmArgs a = g;
+    a.n_tiles = d / BN; a.m_tiles = (n + 127) / 128; a.M_dim = n; a.N_dim = d;
+    const int tiles = E * a.m_tiles * a.n_tiles;
+    if (!launch_gemm<K_DW2>(BN, mA, mB, mC0, mC0, a, std::min(grid, tiles), st)) return SONIC_ERR_CUDA;
+  }
+  // K6 dX~_e = dH_e W1_e^T
+  {
+    CUtensorMap mA, mB, mC0;
+    const int BN = pick_bn(d);
+    if (!map2d(&mA, dH, false, R, 2 * n, 64, 128) || !map3d(&mB, W1, false, E, d, 2 * n, 64, BN) ||
+        !map2d(&mC0, dXt, false, R, d, 64, 32))
+      return SONIC_ERR_CUDA;
+    GemmArgs a = g;
+    a.n_tiles = d / BN; a.k_blocks = (2 * n) / 64; a.N_dim = d;
+    if (!launch_gemm<K_DXT>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
+  }
+  // K7 dW1_e = Gather(X)^T dH_e   (varlen-K)
+  {
+    CUtensorMap mA, mB, mC0;
+    const int BN = pick_bn(2 * n);
+    if (!map2d(&mA, X, false, s.T, d, 64, 1) || !map2d(&mB, dH, false, R, 2 * n, 64, 64) ||
+        !map3d(&mC0, dW1, true, E, d, 2 * n, 32, 32))
+      return SONIC_ERR_CUDA;
+    GemmArgs a = g;
+    a.n_tiles = (2 * n) / BN; a.m_tiles = (d + 127) / 128; a.M_dim = d; a.N_dim = 2 * n;
+    const int tiles = E * a.m_tiles * a.n_tiles;
+    if (!launch_gemm<K_DW1>(BN, mA, mB, mC0, mC0, a, std::min(grid, tiles), st)) return SONIC_ERR_CUDA;
+  }
+  // K8 dX aggregation
+  launch_aggregate(static_cast<const __nv_bfloat16*>(dXt), rt->token_rowptr, rt->token_rows,
+                   static_cast<__nv_bfloat16*>(dX), s.T, d, st);
+  ++g_launches;
+  return check_launch();
+}
+
+}  // extern "C"

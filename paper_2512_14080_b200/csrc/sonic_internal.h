@@ -1,0 +1,34 @@
+// sonic_internal.h -- declarations shared by the libsonic translation units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+namespace sonic {
+
+constexpr int GEMM_M = 128;  // grouped-row tile (== TR m_tile, Q16)
+
+struct RouteLaunch {
+  long long T;
+  int E, K, W, m_tile, mode, rescue, gate_raw;
+  const float* S;
+  // outputs
+  int *topk_ids, *f, *f_r, *offsets, *pad_offsets, *row_token, *token_rowptr, *token_rows, *tile_expert,
+      *num_tiles;
+  float *topk_s, *row_gate;
+  // workspace
+  uint32_t *bm_tc, *bm_kept;
+  int *wprefix, *tokcnt, *flip;
+  float* ST;
+};
+
+int launch_route(const RouteLaunch& L, cudaStream_t st);
+
+// aggregation: out[t] = sum_{r in rows(t)} Y[r] (fp32 accumulation in CSR order)
+void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows, __nv_bfloat16* out, long long T,
+                      int d, cudaStream_t st);
+// dS[r] = sum_j part[j][r] for r < R_pad (device count), j < nparts
+void launch_ds_reduce(const float* part, int nparts, long long rows_max, const int* num_tiles, float* dS,
+                      cudaStream_t st);
+
+}  // namespace sonic

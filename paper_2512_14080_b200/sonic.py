@@ -1,0 +1,206 @@
+"""Thin ctypes binding of libsonic (include/sonic.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels of
+libsonic.so.  PyTorch provides device memory and the current stream.  There is no
+CPU fallback: if the library is missing or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsonic.so")
+
+SONIC_ROUTE_TC = 0
+SONIC_ROUTE_TR_NRF = 1
+SONIC_F_GATE_RAW = 1
+SONIC_F_NO_ORPHAN_RESCUE = 2
+GEMM_M = 128
+
+ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",
+                  "token_rowptr", "token_rows", "tile_expert", "num_tiles"]
+_FLOAT_FIELDS = {"topk_s", "row_gate"}
+
+
+class sonic_moe_desc(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("n", ctypes.c_int32), ("E", ctypes.c_int32),
+                ("K", ctypes.c_int32), ("m_tile", ctypes.c_int32), ("route_mode", ctypes.c_int32),
+                ("flags", ctypes.c_int32)]
+
+
+class sonic_routing(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ROUTING_FIELDS]
+
+
+class SonicError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib():
+    """Load libsonic.so (built in-tree by __graft_entry__.build()).  Fails loudly."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SonicError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        vp, sz = ctypes.c_void_p, ctypes.c_size_t
+        L.sonic_rows_max.argtypes = [P(sonic_moe_desc)]
+        L.sonic_rows_max.restype = ctypes.c_int64
+        L.sonic_routing_sizes.argtypes = [P(sonic_moe_desc), P(sz)]
+        L.sonic_routing_sizes.restype = ctypes.c_int
+        for f in ("sonic_route_workspace_size", "sonic_fwd_workspace_size", "sonic_bwd_workspace_size"):
+            getattr(L, f).argtypes = [P(sonic_moe_desc)]
+            getattr(L, f).restype = sz
+        L.sonic_workspace_offsets.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sz)]
+        L.sonic_workspace_offsets.restype = ctypes.c_int
+        L.sonic_route.argtypes = [P(sonic_moe_desc), vp, P(sonic_routing), vp, sz, vp]
+        L.sonic_route.restype = ctypes.c_int
+        L.sonic_moe_fwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, P(sonic_routing), vp, vp, vp, sz, vp]
+        L.sonic_moe_fwd.restype = ctypes.c_int
+        L.sonic_moe_bwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, vp, vp, P(sonic_routing), vp, vp, vp, vp, vp,
+                                    sz, vp]
+        L.sonic_moe_bwd.restype = ctypes.c_int
+        L.sonic_status_string.argtypes = [ctypes.c_int]
+        L.sonic_status_string.restype = ctypes.c_char_p
+        L.sonic_last_launch_count.argtypes = []
+        L.sonic_last_launch_count.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status, what):
+    if status != 0:
+        raise SonicError(f"{what}: {lib().sonic_status_string(status).decode()} ({status})")
+
+
+def make_desc(T, d, n, E, K, mode=SONIC_ROUTE_TC, m_tile=128, flags=0):
+    return sonic_moe_desc(T, d, n, E, K, m_tile, mode, flags)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def sonic_rows_max(desc):
+    return int(lib().sonic_rows_max(ctypes.byref(desc)))
+
+
+def sonic_routing_sizes(desc):
+    arr = (ctypes.c_size_t * len(ROUTING_FIELDS))()
+    _check(lib().sonic_routing_sizes(ctypes.byref(desc), arr), "sonic_routing_sizes")
+    return dict(zip(ROUTING_FIELDS, list(arr)))
+
+
+def sonic_route_workspace_size(desc):
+    return int(lib().sonic_route_workspace_size(ctypes.byref(desc)))
+
+
+def sonic_fwd_workspace_size(desc):
+    return int(lib().sonic_fwd_workspace_size(ctypes.byref(desc)))
+
+
+def sonic_bwd_workspace_size(desc):
+    return int(lib().sonic_bwd_workspace_size(ctypes.byref(desc)))
+
+
+def sonic_workspace_offsets(desc, which):
+    arr = (ctypes.c_size_t * 4)()
+    _check(lib().sonic_workspace_offsets(ctypes.byref(desc), which, arr), "sonic_workspace_offsets")
+    return list(arr)
+
+
+def sonic_last_launch_count():
+    return int(lib().sonic_last_launch_count())
+
+
+@dataclass
+class Routing:
+    """Device buffers of a sonic_routing (torch tensors, owned here) + the C struct."""
+    tensors: dict
+    c: sonic_routing
+
+    def __getattr__(self, name):
+        t = self.__dict__.get("tensors")
+        if t is not None and name in t:
+            return t[name]
+        raise AttributeError(name)
+
+
+def alloc_routing(desc, device="cuda"):
+    sizes = sonic_routing_sizes(desc)
+    tensors = {}
+    for f in ROUTING_FIELDS:
+        dt = torch.float32 if f in _FLOAT_FIELDS else torch.int32
+        tensors[f] = torch.empty(max(1, sizes[f] // 4), dtype=dt, device=device)
+    c = sonic_routing(*[t.data_ptr() for t in tensors.values()])
+    return Routing(tensors, c)
+
+
+def _ws(nbytes, device):
+    return torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+
+
+def sonic_route(desc, S, rt=None, ws=None):
+    """sonic_route: S [T,E] fp32 -> Routing (device metadata)."""
+    if rt is None:
+        rt = alloc_routing(desc, S.device)
+    if ws is None:
+        ws = _ws(sonic_route_workspace_size(desc), S.device)
+    _check(lib().sonic_route(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(ws), ws.numel(), _stream()),
+           "sonic_route")
+    return rt
+
+
+def sonic_moe_fwd(desc, X, W1, W2, rt, O=None, H=None, ws=None):
+    """sonic_moe_fwd -> (O [T,d] bf16, H_cache [rows_max,2n] bf16, ws)."""
+    rows = sonic_rows_max(desc)
+    if O is None:
+        O = torch.empty(desc.T, desc.d, dtype=torch.bfloat16, device=X.device)
+    if H is None:
+        H = torch.empty(rows, 2 * desc.n, dtype=torch.bfloat16, device=X.device)
+    if ws is None:
+        ws = _ws(sonic_fwd_workspace_size(desc), X.device)
+    _check(lib().sonic_moe_fwd(ctypes.byref(desc), _ptr(X), _ptr(W1), _ptr(W2), ctypes.byref(rt.c), _ptr(O),
+                               _ptr(H), _ptr(ws), ws.numel(), _stream()), "sonic_moe_fwd")
+    return O, H, ws
+
+
+def sonic_moe_bwd(desc, dO, X, H, W1, W2, rt, dX=None, dW1=None, dW2=None, dS=None, ws=None):
+    """sonic_moe_bwd -> (dX [T,d] bf16, dW1 [E,d,2n] f32, dW2 [E,n,d] f32, dS [rows_max] f32, ws)."""
+    rows = sonic_rows_max(desc)
+    dev = X.device
+    if dX is None:
+        dX = torch.empty(desc.T, desc.d, dtype=torch.bfloat16, device=dev)
+    if dW1 is None:
+        dW1 = torch.empty(desc.E, desc.d, 2 * desc.n, dtype=torch.float32, device=dev)
+    if dW2 is None:
+        dW2 = torch.empty(desc.E, desc.n, desc.d, dtype=torch.float32, device=dev)
+    if dS is None:
+        dS = torch.empty(rows, dtype=torch.float32, device=dev)
+    if ws is None:
+        ws = _ws(sonic_bwd_workspace_size(desc), dev)
+    _check(lib().sonic_moe_bwd(ctypes.byref(desc), _ptr(dO), _ptr(X), _ptr(H), _ptr(W1), _ptr(W2),
+                               ctypes.byref(rt.c), _ptr(dX), _ptr(dW1), _ptr(dW2), _ptr(dS), _ptr(ws), ws.numel(),
+                               _stream()), "sonic_moe_bwd")
+    return dX, dW1, dW2, dS, ws
+
+
+def ws_view(ws, offset, shape, dtype):
+    """A typed view into a workspace buffer (for inspecting transients in tests)."""
+    n = 1
+    for s in shape:
+        n *= s
+    nbytes = n * torch.empty(0, dtype=dtype).element_size()
+    return ws[offset: offset + nbytes].view(dtype).view(*shape)

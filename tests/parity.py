@@ -1,0 +1,137 @@
+"""GPU-vs-oracle parity helpers shared by the gpu tests and __graft_entry__.smoke().
+
+The GPU side runs only through the C ABI (paper_2512_14080_b200.sonic); the oracle side
+only through oracle.moe_oracle.  The two share nothing but the seeded inputs.
+
+Criteria (BASELINE.json north star):
+  * routing indices, counts, offsets, gather / scatter maps: bit-exact;
+  * bf16 outputs and gradients: relative Frobenius error <= 1e-2 AND
+    max |err| <= 2e-2 * max |ref|.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import moe_oracle as om
+from paper_2512_14080_b200 import sonic
+
+REL_F = 1e-2
+MAX_REL = 2e-2
+INT_FIELDS = ["topk_ids", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "token_rowptr", "token_rows",
+              "tile_expert", "num_tiles"]
+
+
+def err_stats(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    diff = got - ref
+    nref = np.linalg.norm(ref)
+    relf = np.linalg.norm(diff) / nref if nref > 0 else np.linalg.norm(diff)
+    mref = np.max(np.abs(ref)) if ref.size else 0.0
+    maxrel = np.max(np.abs(diff)) / mref if mref > 0 else (np.max(np.abs(diff)) if diff.size else 0.0)
+    return float(relf), float(maxrel)
+
+
+def assert_close(name, got, ref, relf_tol=REL_F, max_tol=MAX_REL):
+    relf, maxrel = err_stats(got, ref)
+    assert relf <= relf_tol and maxrel <= max_tol, f"{name}: relF={relf:.3e} max|err|/max|ref|={maxrel:.3e}"
+    return relf, maxrel
+
+
+def routing_to_numpy(rt, desc):
+    out = {}
+    for f in sonic.ROUTING_FIELDS:
+        out[f] = rt.tensors[f].cpu().numpy()
+    R_pad = int(out["pad_offsets"][desc.E])
+    R = int(out["offsets"][desc.E])
+    out["num_tiles"] = out["num_tiles"][:1]
+    out["topk_ids"] = out["topk_ids"][: desc.T * desc.K].reshape(desc.T, desc.K)
+    out["topk_s"] = out["topk_s"][: desc.T * desc.K].reshape(desc.T, desc.K)
+    out["row_token"] = out["row_token"][:R_pad]
+    out["row_gate"] = out["row_gate"][:R_pad]
+    out["token_rows"] = out["token_rows"][:R]
+    out["tile_expert"] = out["tile_expert"][: R_pad // om.GEMM_M]
+    return out
+
+
+def oracle_routing_fields(rto):
+    return {
+        "topk_ids": rto.topk_ids, "f": rto.f, "f_rounded": rto.f_rounded, "offsets": rto.offsets,
+        "pad_offsets": rto.pad_offsets, "row_token": rto.row_token, "token_rowptr": rto.token_rowptr,
+        "token_rows": rto.token_rows, "tile_expert": rto.tile_expert,
+        "num_tiles": np.array([rto.R_pad // om.GEMM_M]),
+    }
+
+
+def check_routing(g, rto):
+    """Bit-exact comparison of every integer routing field; gates to fp32 precision."""
+    o = oracle_routing_fields(rto)
+    for f in INT_FIELDS:
+        a, b = np.asarray(g[f]).astype(np.int64), np.asarray(o[f]).astype(np.int64)
+        assert a.shape == b.shape, f"{f}: shape {a.shape} vs oracle {b.shape}"
+        bad = np.nonzero(a != b)[0] if a.ndim == 1 else np.argwhere(a != b)
+        assert len(bad) == 0, f"{f}: {len(bad)} mismatches, first at {bad[:5].tolist()}"
+    assert np.allclose(g["topk_s"], rto.topk_s, rtol=0, atol=0), "topk_s"
+    assert np.allclose(g["row_gate"], rto.row_gate, rtol=2e-6, atol=1e-7), "row_gate"
+
+
+def run_gpu(desc, inp, want_ws=True):
+    """route + fwd + bwd through the C ABI; returns torch tensors (on device)."""
+    rt = sonic.sonic_route(desc, inp.S)
+    O, H, wsf = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
+    dX, dW1, dW2, dS, wsb = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+    torch.cuda.synchronize()
+    out = dict(rt=rt, O=O, H=H, dX=dX, dW1=dW1, dW2=dW2, dS=dS)
+    if want_ws:
+        offs = sonic.sonic_workspace_offsets(desc, 1)
+        rows = sonic.sonic_rows_max(desc)
+        out["dH"] = sonic.ws_view(wsb, offs[0], (rows, 2 * desc.n), torch.bfloat16)
+        out["Ap"] = sonic.ws_view(wsb, offs[1], (rows, desc.n), torch.bfloat16)
+        offs = sonic.sonic_workspace_offsets(desc, 0)
+        out["A"] = sonic.ws_view(wsf, offs[0], (rows, desc.n), torch.bfloat16)
+        out["Y"] = sonic.ws_view(wsf, offs[1], (rows, desc.d), torch.bfloat16)
+    return out
+
+
+def f64(t):
+    return t.detach().float().cpu().numpy().astype(np.float64)
+
+
+def full_parity(desc, inp, mode="tc", check_ws=True):
+    """Element-by-element parity of every output at a size the oracle finishes in seconds."""
+    g = run_gpu(desc, inp, want_ws=check_ws)
+    S = inp.S.cpu().numpy()
+    rto = om.route(S, desc.K, mode=mode, m_tile=desc.m_tile,
+                   rescue=not (desc.flags & sonic.SONIC_F_NO_ORPHAN_RESCUE),
+                   gate_raw=bool(desc.flags & sonic.SONIC_F_GATE_RAW))
+    gr = routing_to_numpy(g["rt"], desc)
+    check_routing(gr, rto)
+    X, W1, W2, dO = f64(inp.X), f64(inp.W1), f64(inp.W2), f64(inp.dO)
+    fw = om.forward(X, W1, W2, rto)
+    bw = om.backward(dO, X, W1, W2, rto)
+    stats = {}
+    stats["O"] = assert_close("O", f64(g["O"]), fw.O)
+    Hg = f64(g["H"])
+    rows = np.nonzero(rto.row_token >= 0)[0]
+    exp_of = rto.row_expert[rows]
+    Href = np.concatenate([fw.H[e] for e in range(desc.E) if e in fw.H and len(fw.H[e])], axis=0)
+    Aref = np.concatenate([fw.A[e] for e in range(desc.E) if e in fw.A and len(fw.A[e])], axis=0)
+    stats["H"] = assert_close("H", Hg[rows], Href)
+    stats["dX"] = assert_close("dX", f64(g["dX"]), bw.dX)
+    stats["dW1"] = assert_close("dW1", f64(g["dW1"]), bw.dW1)
+    stats["dW2"] = assert_close("dW2", f64(g["dW2"]), bw.dW2)
+    dSref = np.concatenate([bw.dS[e] for e in range(desc.E) if len(bw.dS[e])])
+    dSg = f64(g["dS"])
+    stats["dS"] = assert_close("dS", dSg[rows], dSref)
+    pad = np.nonzero(rto.row_token < 0)[0]
+    assert np.all(dSg[pad] == 0), "dS on pad rows must be 0"
+    if check_ws:
+        stats["A"] = assert_close("A", f64(g["A"])[rows], Aref)
+        dHref = np.concatenate([bw.dH[e] for e in range(desc.E) if len(bw.dH[e])], axis=0)
+        Apref = np.concatenate([bw.A_prime[e] for e in range(desc.E) if len(bw.A_prime[e])], axis=0)
+        stats["dH"] = assert_close("dH", f64(g["dH"])[rows], dHref)
+        stats["Ap"] = assert_close("Ap", f64(g["Ap"])[rows], Apref)
+        assert np.all(f64(g["dH"])[pad] == 0) and np.all(f64(g["Ap"])[pad] == 0), "pad rows must be exact zeros"
+    assert np.all(np.isin(exp_of, np.arange(desc.E)))
+    return stats
