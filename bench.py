@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""bench.py -- SonicMoE layer fwd+bwd on B200 through libsonic's C ABI.
+
+One step = sonic_route + sonic_moe_fwd + sonic_moe_bwd over one synthetic microbatch
+(all of SURVEY.md section 8(a)'s rows).  Default workload: BASELINE.json configs[1], the
+fine-grained 7B-class layer (T=32768, d=1536, n=256, E=128, K=8, token-choice top-K).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7b|qwen3|...] [--mode tc|tr]
+  python bench.py --impl reference ...     # the fp64 CPU oracle on the host cores
+
+N > 1 (torchrun): every rank runs its own microbatch through the full layer (data-parallel
+replicas, weak scaling, no collective on the data path); time = max over ranks.
+Prints ONE JSON line on rank 0.  See DESIGN.md section 7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE layer fwd+bwd TFLOPS (% B200 BF16 peak), tokens/s at 1/2/4/8 GPU; act. mem"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(PEAKS_FALLBACK)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+# --------------------------------------------------------------------------- FLOP / byte model
+def kernel_model(T, d, n, E, K, R, R_pad):
+    """Algorithmic FLOPs and bytes per launch.
+
+    R = routed rows (T*K under TC, sum f_r under TR).  'paper' bytes count gathered rows at
+    R*d*2; 'tight' counts each gathered tensor once.
+    """
+    b = 2
+    W1 = E * d * 2 * n * b
+    W2 = E * n * d * b
+    m = {
+        "up": dict(flops=4 * R * d * n, paper=R * d * b + W1 + R * 2 * n * b + R * n * b,
+                   tight=T * d * b + W1 + R * 2 * n * b + R * n * b),
+        "down": dict(flops=2 * R * n * d, paper=R * n * b + W2 + R * d * b, tight=R * n * b + W2 + R * d * b),
+        "agg_O": dict(flops=0, paper=R * d * b + T * d * b, tight=R * d * b + T * d * b),
+        "dH": dict(flops=2 * R * n * d, paper=R * d * b + W2 + 2 * R * 2 * n * b + R * n * b + R * 4,
+                   tight=T * d * b + W2 + 2 * R * 2 * n * b + R * n * b + R * 4),
+        "dW2": dict(flops=2 * R * n * d, paper=R * n * b + R * d * b + E * n * d * 4,
+                    tight=R * n * b + T * d * b + E * n * d * 4),
+        "dXt": dict(flops=4 * R * d * n, paper=R * 2 * n * b + W1 + R * d * b, tight=R * 2 * n * b + W1 + R * d * b),
+        "dW1": dict(flops=4 * R * d * n, paper=R * d * b + R * 2 * n * b + E * d * 2 * n * 4,
+                    tight=T * d * b + R * 2 * n * b + E * d * 2 * n * 4),
+        "agg_dX": dict(flops=0, paper=R * d * b + T * d * b, tight=R * d * b + T * d * b),
+        "route": dict(flops=0, paper=T * E * 4 + T * K * 8 + R * 12, tight=T * E * 4 + T * K * 8 + R * 12),
+        "dS_reduce": dict(flops=0, paper=R * 8, tight=R * 8),
+    }
+    return m
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+        self.path = os.path.join("/tmp", f"sonic_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.close()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sms.sort()
+        med = sms[len(sms) // 2] if sms else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# --------------------------------------------------------------------------- CPU oracle leg
+def oracle_sample(cfg, mode, seed, T_sample):
+    """The fp64 oracle as it stands on a bounded sample: the first T_sample tokens of the
+    workload (route + fwd + bwd).  Returns (model FLOPs processed, seconds, threads)."""
+    import numpy as np
+    import torch
+    from oracle import moe_oracle as om
+    from paper_2512_14080_b200.inputs import make_inputs
+    c = dict(cfg)
+    c["T"] = T_sample
+    inp = make_inputs(**c, seed=seed, device="cpu")
+    f64 = lambda t: t.float().numpy().astype(np.float64)
+    X, W1, W2, dO, S = f64(inp.X), f64(inp.W1), f64(inp.W2), f64(inp.dO), inp.S.numpy()
+    t0 = time.perf_counter()
+    rt = om.route(S, c["K"], mode=mode, m_tile=128)
+    om.forward(X, W1, W2, rt)
+    om.backward(dO, X, W1, W2, rt)
+    dt = time.perf_counter() - t0
+    flops = 18 * c["d"] * c["n"] * rt.R
+    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    return flops, dt, threads
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    T_s = args.ref_tokens
+    for _ in range(args.warmup):
+        oracle_sample(cfg, args.mode, 0, T_s)
+    tot_f, tot_t, thr = 0, 0.0, 1
+    for i in range(args.steps):
+        f, t, thr = oracle_sample(cfg, args.mode, i, T_s)
+        tot_f += f
+        tot_t += t
+    v = tot_f / tot_t / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args, cfg),
+        "cpu_baseline": {"value": v, "unit": "TFLOPS", "cores": thr, "kind": "oracle",
+                         "sample": f"first {T_s} tokens of the workload per step (route+fwd+bwd, fp64 numpy)"},
+        "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, cfg):
+    return {"workload": f"{args.config}: T={cfg['T']} d={cfg['d']} n={cfg['n']} E={cfg['E']} K={cfg['K']} "
+                        f"route={args.mode}",
+            "T": cfg["T"], "d": cfg["d"], "n": cfg["n"], "E": cfg["E"], "K": cfg["K"], "route": args.mode,
+            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "l2": "not flushed: per-step working set (X, W1, W2, H, Y, dX~, ...) is several GB >> 126 MB L2"}
+
+
+# --------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="sonic", choices=["sonic", "reference"])
+    ap.add_argument("--config", default="7b")
+    ap.add_argument("--mode", default="tc", choices=["tc", "tr"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--ref-tokens", type=int, default=1024)
+    ap.add_argument("--cpu-tokens", type=int, default=8192)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--breakdown", default="", help="write the per-kernel table to this JSON file")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    from paper_2512_14080_b200.inputs import CONFIGS
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2512_14080_b200 import sonic
+    from paper_2512_14080_b200.inputs import make_inputs
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    T, d, n, E, K = cfg["T"], cfg["d"], cfg["n"], cfg["E"], cfg["K"]
+    mode = sonic.SONIC_ROUTE_TC if args.mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
+    desc = sonic.make_desc(T, d, n, E, K, mode=mode)
+    inp = make_inputs(**cfg, seed=args.seed + rank, device=dev)
+    rows = sonic.sonic_rows_max(desc)
+    rt = sonic.alloc_routing(desc, dev)
+    ws_r = torch.empty(max(256, sonic.sonic_route_workspace_size(desc)), dtype=torch.uint8, device=dev)
+    ws_f = torch.empty(max(256, sonic.sonic_fwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
+    ws_b = torch.empty(max(256, sonic.sonic_bwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
+    O = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+    H = torch.empty(rows, 2 * n, dtype=torch.bfloat16, device=dev)
+    dX = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+    dW1 = torch.empty(E, d, 2 * n, dtype=torch.float32, device=dev)
+    dW2 = torch.empty(E, n, d, dtype=torch.float32, device=dev)
+    dS = torch.empty(rows, dtype=torch.float32, device=dev)
+    launches = [0]
+
+    def step():
+        sonic.sonic_route(desc, inp.S, rt, ws_r)
+        launches[0] += sonic.sonic_last_launch_count()
+        sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt, O, H, ws_f)
+        launches[0] += sonic.sonic_last_launch_count()
+        sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt, dX, dW1, dW2, dS, ws_b)
+        launches[0] += sonic.sonic_last_launch_count()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    R = int(rt.offsets[E].item())
+    R_pad = int(rt.pad_offsets[E].item())
+    flops_step = 18 * d * n * R
+
+    # ---- device-timed region: inputs resident in HBM
+    clocks = ClockSampler(local)
+    sonic.sonic_profile_enable(True)
+    sonic.sonic_profile_collect()
+    launches[0] = 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
+    sonic.sonic_profile_enable(False)
+    recs = sonic.sonic_profile_collect()
+    ms = ev0.elapsed_time(ev1)
+    gpu_launches = launches[0]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = flops_step * world / (ms_step * 1e-3) / 1e12
+
+    # ---- per-kernel breakdown and roofline of the dominant kernel
+    peaks = load_peaks()
+    model = kernel_model(T, d, n, E, K, R, R_pad)
+    agg = {}
+    for name, t in recs:
+        a = agg.setdefault(name, [0.0, 0])
+        a[0] += t
+        a[1] += 1
+    tf_peak = peaks["bf16_tflops_sustained"]
+    bw_peak = peaks["hbm_gbs"]
+    kernels = {}
+    for name, (tot, cnt) in agg.items():
+        avg = tot / cnt
+        mm = model.get(name, dict(flops=0, paper=0, tight=0))
+        t_tensor = mm["flops"] / (tf_peak * 1e12) * 1e3
+        t_hbm = mm["paper"] / (bw_peak * 1e9) * 1e3
+        kernels[name] = dict(avg_ms=avg, launches_per_step=cnt / args.steps, share=tot / ms if ms else None,
+                             tflops=mm["flops"] / (avg * 1e-3) / 1e12 if mm["flops"] else 0.0,
+                             gbs_paper=mm["paper"] / (avg * 1e-3) / 1e9, gbs_tight=mm["tight"] / (avg * 1e-3) / 1e9,
+                             bound="tensor" if t_tensor >= t_hbm else "hbm",
+                             roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None)
+    dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"]) if kernels else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if dom and os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{args.config}/{args.mode}/{dom}")
+    roof = None
+    if dom:
+        k = kernels[dom]
+        if k["bound"] == "tensor":
+            roof = {"kernel": dom, "bound": "tensor", "achieved": k["tflops"], "peak": tf_peak, "unit": "TFLOP/s",
+                    "frac": k["tflops"] / tf_peak, "traffic": traffic,
+                    "algorithmic_per_launch": model[dom]["flops"],
+                    "peak_source": peaks["source"] + " bf16_tflops_sustained (kernel timed inside a long step)"}
+        else:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": k["gbs_paper"], "peak": bw_peak, "unit": "GB/s",
+                    "frac": k["gbs_paper"] / bw_peak, "traffic": traffic,
+                    "algorithmic_per_launch": model[dom]["paper"], "peak_source": peaks["source"] + " hbm_gbs"}
+    layer_roof_ms = sum(kernels[k]["roofline_ms"] * kernels[k]["launches_per_step"] for k in kernels)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = inp.X.cpu().pin_memory()
+        Sh = inp.S.cpu().pin_memory()
+        dOh = inp.dO.cpu().pin_memory()
+        Oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
+        dXh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
+        Xd, Sd, dOd = torch.empty_like(inp.X), torch.empty_like(inp.S), torch.empty_like(inp.dO)
+
+        def step_e2e():
+            Xd.copy_(Xh, non_blocking=True)
+            Sd.copy_(Sh, non_blocking=True)
+            dOd.copy_(dOh, non_blocking=True)
+            sonic.sonic_route(desc, Sd, rt, ws_r)
+            sonic.sonic_moe_fwd(desc, Xd, inp.W1, inp.W2, rt, O, H, ws_f)
+            sonic.sonic_moe_bwd(desc, dOd, Xd, H, inp.W1, inp.W2, rt, dX, dW1, dW2, dS, ws_b)
+            Oh.copy_(O, non_blocking=True)
+            dXh.copy_(dX, non_blocking=True)
+
+        step_e2e()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.e2e_steps):
+            step_e2e()
+        e1.record()
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e_step = ems / args.e2e_steps
+        e2e = {"value": flops_step * world / (e_step * 1e-3) / 1e12, "unit": "TFLOPS",
+               "h2d_bytes_per_step": Xh.numel() * 2 + Sh.numel() * 4 + dOh.numel() * 2,
+               "d2h_bytes_per_step": Oh.numel() * 2 + dXh.numel() * 2, "ms_per_step": e_step}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        f, t, thr = oracle_sample(cfg, args.mode, args.seed, args.cpu_tokens)
+        cpu = {"value": f / t / 1e12, "unit": "TFLOPS", "cores": thr, "kind": "oracle",
+               "sample": f"first {args.cpu_tokens} of {T} tokens (route+fwd+bwd in fp64 numpy), {t:.1f} s"}
+
+    meta_bytes = sum(sonic.sonic_routing_sizes(desc).values())
+    act = {"X": T * d * 2, "H": R_pad * 2 * n * 2, "metadata": meta_bytes,
+           "paper_formula_2Td_4TKn": 2 * T * d + 4 * T * K * n}
+    act["total"] = act["X"] + act["H"] + act["metadata"]
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": workload_config(args, cfg),
+        "pct_peak": value / world / peaks["bf16_tflops"], "pct_peak_sustained": value / world / tf_peak,
+        "tokens_per_s": T * world / (ms_step * 1e-3),
+        "model_flops_per_step": flops_step, "rows_routed": R, "rows_padded": R_pad,
+        "layer_roofline_ms": layer_roof_ms, "layer_roofline_frac": layer_roof_ms / ms_step,
+        "act_mem_bytes": act,
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
+        "clocks": clk, "kernels": kernels, "peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops",
+                                                                                "bf16_tflops_sustained", "source")},
+    }
+    if args.breakdown:
+        json.dump(line, open(args.breakdown, "w"), indent=1)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -153,6 +153,14 @@ const char *sonic_status_string(sonic_status s);
 /* Number of kernels the last sonic_route/fwd/bwd call on this thread launched. */
 int sonic_last_launch_count(void);
 
+/* Optional timing instrumentation (per calling thread).  When enabled, every kernel (the
+ * route sequence counts as one record, "route") is bracketed by CUDA events on its stream.
+ * sonic_profile_collect synchronises on the recorded events, writes up to max_records
+ * (name, milliseconds) pairs -- names as NUL-terminated strings of name_len bytes each --
+ * clears the record list and returns the number written. */
+void sonic_profile_enable(int on);
+int sonic_profile_collect(char *names, int name_len, float *ms, int max_records);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,5 +1,5 @@
 // gemm.cuh -- the six grouped GEMMs of the SonicMoE layer as ONE warp-specialised,
-// persistent tcgen05/TMEM/TMA kernel template for sm_100a.
+// persistent tcgen05/TMEM kernel template for sm_100a.
 //
 //   kind   paper kernel (Alg.)          D = A . B per expert e                 epilogue
 //   UP     up-proj A kernel (Alg. 2)    H_e   = Gather(X) W1_e       (varlen-M) SwiGLU -> H, A
@@ -9,19 +9,21 @@
 //   DW2    dW2 kernel (Alg. 3)          dW2_e = A'_e^T Gather(dO)    (varlen-K) fp32 store
 //   DW1    dW1 kernel (Alg. 5)          dW1_e = Gather(X)^T dH_e     (varlen-K) fp32 store
 //
-// Roles (192 threads, 1 CTA per SM):
-//   warp 0     TMA producer: tile / 3-D tile / gather4 loads into a STAGES-deep smem ring
-//              (full/empty mbarriers).  Gathered rows come from row_token (the gather
-//              map) -- the paper's "gather fused with the HBM load" (sec. 4.1.1)
-//              done with TMA gather4 instead of cp.async + relay warp.
-//   warp 1     TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16 steps),
-//              two TMEM accumulator stages so the epilogue of tile i overlaps the MMA of
-//              tile i+1.
-//   warps 2-5  epilogue: tcgen05.ld -> registers -> fused math -> swizzled smem -> TMA store
-//              ("asynchronous TMA store in all Grouped GEMMs").
+// Roles (one CTA per SM, persistent static tile schedule):
+//   producers  NP warps.  Contiguous operands: TMA 2-D/3-D tile loads by one thread.
+//              Gathered operands (NP = 4): 128 threads issue 16-byte cp.async of the token
+//              rows named by the gather map straight into the 128B-swizzled operand layout
+//              -- the paper's "gather fused with the HBM load" (sec. 4.1.1).
+//              (TMA gather4 was measured at ~80 cycles per 512 B per SM on B200, too slow to
+//              feed the tensor cores.)  A producer thread signals a
+//              stage full after cp.async.wait_group + fence.proxy.async (lagged by LAG stages).
+//   MMA        one warp: TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN,
+//              K=16 steps); two TMEM accumulator stages so the epilogue of tile i overlaps
+//              the MMA of tile i+1.
+//   epilogue   4 warps: tcgen05.ld -> registers -> fused math -> swizzled smem -> TMA store
+//              (asynchronous TMA store in all GEMMs).
 // Operand smem layout: 128B-swizzled, K-major (rows of 64 K-elements) or MN-major
-// (64-element MN chunks x 64 K-rows); every stage is one A tile (128 x 64) + one B tile
-// (BN x 64).
+// (64-element MN chunks x 64 K-rows); a stage is one A tile (128 x 64) + one B tile (BN x 64).
 #pragma once
 #include "ptx.cuh"
 
@@ -35,6 +37,8 @@ struct GemmArgs {
   const int* row_token;     // gather map, -1 on pad rows
   const float* row_gate;    // gate per grouped row, 0 on pad rows
   const int* pad_offsets;   // [E+1] tile-aligned expert segments
+  const __nv_bfloat16* gsrc;  // gathered operand source (X or dO), [T, gld]
+  int gld;
   int E;
   int n_tiles;              // output tiles along N
   int m_tiles;              // varlen-K: output tiles along M per expert
@@ -55,9 +59,17 @@ template <> struct Traits<K_DXT>  { static constexpr bool vk = false, a_gather =
 template <> struct Traits<K_DW2>  { static constexpr bool vk = true,  a_gather = false, a_mn = true,  b_gather = true,  b_mn = true;  };
 template <> struct Traits<K_DW1>  { static constexpr bool vk = true,  a_gather = true,  a_mn = true,  b_gather = false, b_mn = true;  };
 
+template <int KIND>
+__host__ __device__ constexpr int num_producer_warps() {
+  return (Traits<KIND>::a_gather || Traits<KIND>::b_gather) ? 4 : 1;
+}
+template <int KIND>
+__host__ __device__ constexpr int gemm_threads() {
+  return 32 * (num_producer_warps<KIND>() + 5);
+}
+
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
-constexpr int GEMM_THREADS = 192;
 constexpr int STG_BYTES = 4096;  // one epilogue staging buffer: 32 rows x 128 B
 constexpr int SMEM_LIMIT = 232448;
 
@@ -72,6 +84,7 @@ struct GemmCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int LAG = STAGES - 2 > 0 ? STAGES - 2 : 1;  // cp.async stages in flight per producer
 };
 
 struct TileCoord {
@@ -102,74 +115,70 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile) {
   return c;
 }
 
-__device__ __forceinline__ int4 load_idx4(const int* p) {
-  int4 v = __ldg(reinterpret_cast<const int4*>(p));
-  // pad rows (-1) read token 0; their gate is 0, so every value they produce is exactly 0
-  v.x = max(v.x, 0); v.y = max(v.y, 0); v.z = max(v.z, 0); v.w = max(v.w, 0);
-  return v;
-}
-
-// Write one 32-row x 128-byte slab (thread = row) into a 128B-swizzled staging buffer.
-__device__ __forceinline__ void stage_row_bf16(uint8_t* buf, int lane, const float* v) {
-  uint32_t base = ptx::smem_u32(buf) + lane * 128;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    ptx::st_shared_v4(base + ((c ^ (lane & 7)) << 4), ptx::pack_bf16(v[8 * c + 0], v[8 * c + 1]),
-                      ptx::pack_bf16(v[8 * c + 2], v[8 * c + 3]), ptx::pack_bf16(v[8 * c + 4], v[8 * c + 5]),
-                      ptx::pack_bf16(v[8 * c + 6], v[8 * c + 7]));
-  }
-}
-__device__ __forceinline__ void stage_row_f32(uint8_t* buf, int lane, const float* v) {
-  uint32_t base = ptx::smem_u32(buf) + lane * 128;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    ptx::st_shared_v4(base + ((c ^ (lane & 7)) << 4), __float_as_uint(v[4 * c + 0]), __float_as_uint(v[4 * c + 1]),
-                      __float_as_uint(v[4 * c + 2]), __float_as_uint(v[4 * c + 3]));
-  }
-}
-
-// Per-warp double-buffered TMA store pipeline.
-struct StoreQ {
-  uint8_t* buf;  // 2 x STG_BYTES
-  int sb;
-  __device__ __forceinline__ uint8_t* acquire(int lane) {
-    if (lane == 0) ptx::bulk_wait_read<1>();
-    __syncwarp();
-    return buf + sb * STG_BYTES;
-  }
-  __device__ __forceinline__ void commit2d(int lane, const CUtensorMap* map, int c0, int c1) {
-    ptx::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      ptx::tma_store_2d(map, buf + sb * STG_BYTES, c0, c1);
-      ptx::bulk_commit();
-    }
-    sb ^= 1;
-  }
-  __device__ __forceinline__ void commit3d(int lane, const CUtensorMap* map, int c0, int c1, int c2) {
-    ptx::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      ptx::tma_store_3d(map, buf + sb * STG_BYTES, c0, c1, c2);
-      ptx::bulk_commit();
-    }
-    sb ^= 1;
-  }
-};
+// Pad rows (-1) read token 0: their gate is 0, so every value they produce is exactly 0.
+__device__ __forceinline__ int tok_of(const int* row_token, int r) { return max(__ldg(row_token + r), 0); }
 
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 __device__ __forceinline__ float sigmoidf_fast(float x) { return 1.0f / (1.0f + __expf(-x)); }
+__device__ __forceinline__ uint32_t swz(int lane, int chunk) { return (uint32_t)(lane * 128 + ((chunk ^ (lane & 7)) << 4)); }
+
+// Per-warp double-buffered TMA store pipeline (32 rows x 128 B per buffer, 128B swizzle).
+struct StoreQ {
+  uint8_t* base;
+  int sb;
+  __device__ __forceinline__ uint32_t addr(int i) const { return ptx::smem_u32(base + i * STG_BYTES); }
+  template <int N>
+  __device__ __forceinline__ void wait_reads(int lane) {
+    if (lane == 0) ptx::bulk_wait_read<N>();
+    __syncwarp();
+  }
+  // next buffer in round-robin order, waiting until the store issued from it has read smem
+  __device__ __forceinline__ int acquire(int lane) {
+    wait_reads<1>(lane);
+    return sb;
+  }
+  __device__ __forceinline__ void issue(int lane, int i, const CUtensorMap* map, int c0, int c1) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_2d(map, base + i * STG_BYTES, c0, c1);
+      ptx::bulk_commit();
+    }
+    sb = i ^ 1;
+  }
+  __device__ __forceinline__ void issue3d(int lane, int i, const CUtensorMap* map, int c0, int c1, int c2) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_3d(map, base + i * STG_BYTES, c0, c1, c2);
+      ptx::bulk_commit();
+    }
+    sb = i ^ 1;
+  }
+};
+
+__device__ __forceinline__ void write_row_bf16(uint32_t buf, int lane, const float* v /*64*/) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c)
+    ptx::st_shared_v4(buf + swz(lane, c), ptx::pack_bf16(v[8 * c], v[8 * c + 1]),
+                      ptx::pack_bf16(v[8 * c + 2], v[8 * c + 3]), ptx::pack_bf16(v[8 * c + 4], v[8 * c + 5]),
+                      ptx::pack_bf16(v[8 * c + 6], v[8 * c + 7]));
+}
 
 template <int KIND, int BN>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     sonic_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                       const __grid_constant__ CUtensorMap mC0, const __grid_constant__ CUtensorMap mC1,
                       const GemmArgs args) {
   using Tr = Traits<KIND>;
   using Cfg = GemmCfg<BN>;
+  constexpr int NP = num_producer_warps<KIND>();
+  constexpr bool GATHER = NP > 1;
   constexpr int STAGES = Cfg::STAGES;
   constexpr uint32_t A_BYTES = Cfg::A_BYTES;
   constexpr uint32_t STAGE_BYTES = Cfg::STAGE_BYTES;
+  // bytes landing through TMA per stage (the non-gathered operands)
+  constexpr uint32_t TMA_BYTES = !GATHER ? STAGE_BYTES : (Tr::a_gather ? Cfg::B_BYTES : A_BYTES);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -183,9 +192,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  if (warp == 0 && lane == 0) {
+  if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&full[s], GATHER ? NP * 32 + 1 : 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     ptx::prefetch_tmap(&mA);
     ptx::prefetch_tmap(&mB);
   }
-  if (warp == 1) {
+  if (warp == NP) {
     ptx::tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
     ptx::tmem_relinquish();
   }
@@ -207,30 +216,64 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const int total_tiles = Tr::vk ? args.E * args.m_tiles * args.n_tiles : (*args.num_m_tiles) * args.n_tiles;
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ TMA producer
+  if (warp < NP) {
+    // ============================================================ producers
     int stage = 0;
     uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const TileCoord tc = decode_tile<KIND, BN>(args, tile);
-      int4 aidx = make_int4(0, 0, 0, 0);
-      if constexpr (!Tr::vk && Tr::a_gather) aidx = load_idx4(args.row_token + tc.row0 + 4 * lane);
-      for (int kb = 0; kb < tc.nkb; ++kb) {
-        ptx::mbar_wait(&empty[stage], phase ^ 1);
-        uint8_t* sA = smem + stage * STAGE_BYTES;
-        uint8_t* sB = sA + A_BYTES;
-        uint64_t* bar = &full[stage];
-        if (lane == 0) ptx::mbar_arrive_expect_tx(bar, STAGE_BYTES);
-        __syncwarp();
-        if constexpr (!Tr::vk) {
-          // ---- A: 128 grouped rows x 64 K
-          if constexpr (Tr::a_gather) {
-            ptx::tma_gather4(sA + lane * 512, &mA, bar, kb * GEMM_BK, aidx.x, aidx.y, aidx.z, aidx.w);
-          } else if (lane == 0) {
+    if constexpr (!GATHER) {
+      if (lane == 0) {
+        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+          const TileCoord tc = decode_tile<KIND, BN>(args, tile);
+          for (int kb = 0; kb < tc.nkb; ++kb) {
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sA = smem + stage * STAGE_BYTES;
+            uint8_t* sB = sA + A_BYTES;
+            uint64_t* bar = &full[stage];
+            ptx::mbar_arrive_expect_tx(bar, STAGE_BYTES);
             ptx::tma_load_2d(sA, &mA, bar, kb * GEMM_BK, tc.row0);
+            if constexpr (KIND == K_DOWN) {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                ptx::tma_load_3d(sB + j * 8192, &mB, bar, tc.nt * BN + 64 * j, kb * GEMM_BK, tc.e);
+            } else {  // DXT: K-major weights, one box of BN rows
+              ptx::tma_load_3d(sB, &mB, bar, kb * GEMM_BK, tc.nt * BN, tc.e);
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
           }
-          // ---- B: weights of expert e (3-D tensor map [E, rows, cols])
-          if (lane == 0) {
+        }
+      }
+    } else {
+      const int pt = threadIdx.x;  // 0..127
+      const int c = pt & 7;        // 16-byte chunk within a 128-byte row
+      const int r0 = pt >> 3;      // rows r0 + 16 j
+      const uint32_t sw = (uint32_t)((c ^ (r0 & 7)) << 4);
+      int pend = 0, pstage = 0;
+      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
+        const TileCoord tc = decode_tile<KIND, BN>(args, tile);
+        const __nv_bfloat16* srcM[8];
+        if constexpr (!Tr::vk) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            srcM[j] = args.gsrc + (size_t)tok_of(args.row_token, tc.row0 + r0 + 16 * j) * args.gld + c * 8;
+        }
+        for (int kb = 0; kb < tc.nkb; ++kb) {
+          const __nv_bfloat16* srcK[4];
+          if constexpr (Tr::vk) {
+            const int krow0 = tc.seg0 + kb * GEMM_BK;
+            const int col0 = Tr::a_gather ? tc.mt * GEMM_BM : tc.nt * BN;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              srcK[j] = args.gsrc + (size_t)tok_of(args.row_token, krow0 + r0 + 16 * j) * args.gld + col0 + c * 8;
+          }
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sA = smem + stage * STAGE_BYTES;
+          uint8_t* sB = sA + A_BYTES;
+          uint64_t* bar = &full[stage];
+          if (pt == 0) {
+            ptx::mbar_arrive_expect_tx(bar, TMA_BYTES);
             if constexpr (KIND == K_UP) {
               constexpr int W = BN / 2;  // gate columns per tile; the up columns follow at +n
               if constexpr (W >= 64) {
@@ -243,48 +286,54 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               } else {  // n == 32: one 64-column box holds [gate | up]
                 ptx::tma_load_3d(sB, &mB, bar, 0, kb * GEMM_BK, tc.e);
               }
-            } else if constexpr (KIND == K_DOWN) {
-#pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                ptx::tma_load_3d(sB + j * 8192, &mB, bar, tc.nt * BN + 64 * j, kb * GEMM_BK, tc.e);
-            } else {  // DH, DXT: K-major weights, one box of BN rows
+            } else if constexpr (KIND == K_DH) {
               ptx::tma_load_3d(sB, &mB, bar, kb * GEMM_BK, tc.nt * BN, tc.e);
-            }
-          }
-        } else {
-          const int krow0 = tc.seg0 + kb * GEMM_BK;
-          const int g = lane & 15;
-          int4 kidx = make_int4(0, 0, 0, 0);
-          if constexpr (Tr::a_gather || Tr::b_gather) kidx = load_idx4(args.row_token + krow0 + 4 * g);
-          // ---- A (MN-major): 64 K-rows x 128 M-columns
-          if constexpr (Tr::a_gather) {
-            const int j = lane >> 4;
-            ptx::tma_gather4(sA + j * 8192 + g * 512, &mA, bar, tc.mt * GEMM_BM + 64 * j, kidx.x, kidx.y, kidx.z,
-                             kidx.w);
-          } else if (lane == 0) {
-            ptx::tma_load_2d(sA, &mA, bar, tc.mt * GEMM_BM, krow0);
-            ptx::tma_load_2d(sA + 8192, &mA, bar, tc.mt * GEMM_BM + 64, krow0);
-          }
-          // ---- B (MN-major): 64 K-rows x BN N-columns
-          if constexpr (Tr::b_gather) {
-            for (int it = lane; it < (BN / 64) * 16; it += 32) {
-              const int j = it >> 4;
-              ptx::tma_gather4(sB + j * 8192 + g * 512, &mB, bar, tc.nt * BN + 64 * j, kidx.x, kidx.y, kidx.z,
-                               kidx.w);
-            }
-          } else if (lane == 0) {
+            } else if constexpr (KIND == K_DW2) {  // A' tile (MN-major): 64 rows x 128 M columns
+              const int krow0 = tc.seg0 + kb * GEMM_BK;
+              ptx::tma_load_2d(sA, &mA, bar, tc.mt * GEMM_BM, krow0);
+              ptx::tma_load_2d(sA + 8192, &mA, bar, tc.mt * GEMM_BM + 64, krow0);
+            } else {  // DW1: dH tile (MN-major): 64 rows x BN columns
+              const int krow0 = tc.seg0 + kb * GEMM_BK;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sB + j * 8192, &mB, bar, tc.nt * BN + 64 * j, krow0);
+              for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sB + j * 8192, &mB, bar, tc.nt * BN + 64 * j, krow0);
+            }
           }
-        }
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+          if constexpr (!Tr::vk) {  // A: 128 gathered rows x 64 K (K-major)
+            const uint32_t dst = ptx::smem_u32(sA) + r0 * 128 + sw;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ptx::cp_async16(dst + j * 16 * 128, srcM[j] + kb * GEMM_BK);
+          } else {  // 64 gathered K-rows x (128 | BN) MN-columns (MN-major)
+            constexpr int NCH = Tr::a_gather ? 2 : BN / 64;
+            const uint32_t dst = ptx::smem_u32(Tr::a_gather ? sA : sB) + r0 * 128 + sw;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+              for (int jj = 0; jj < NCH; ++jj) ptx::cp_async16(dst + jj * 8192 + j * 16 * 128, srcK[j] + 64 * jj);
+          }
+          ptx::cp_async_commit();
+          if (++pend > Cfg::LAG) {
+            ptx::cp_async_wait<Cfg::LAG>();
+            ptx::fence_proxy_async_smem();
+            ptx::mbar_arrive(&full[pstage]);
+            if (++pstage == STAGES) pstage = 0;
+            --pend;
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
+      ptx::cp_async_wait<0>();
+      ptx::fence_proxy_async_smem();
+      while (pend > 0) {
+        ptx::mbar_arrive(&full[pstage]);
+        if (++pstage == STAGES) pstage = 0;
+        --pend;
+      }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == NP) {
+    // ============================================================ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = ptx::make_idesc(GEMM_BM, BN, Tr::a_mn ? 1 : 0, Tr::b_mn ? 1 : 0);
       int stage = 0;
@@ -322,8 +371,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ------------------------------------------------------------ epilogue (warps 2..5)
-    const int ew = warp - 2;
+    // ============================================================ epilogue (4 warps)
+    const int ew = warp - NP - 1;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     StoreQ sq{stg + ew * 2 * STG_BYTES, 0};
     int acc = 0;
@@ -341,50 +390,67 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if constexpr (W >= 64) {
 #pragma unroll 1
           for (int c = 0; c < W; c += 64) {
-            uint32_t g0[32], g1[32], u0[32], u1[32];
-            ptx::tmem_ld32(t_acc + c, g0);
-            ptx::tmem_ld32(t_acc + c + 32, g1);
-            ptx::tmem_ld32(t_acc + W + c, u0);
-            ptx::tmem_ld32(t_acc + W + c + 32, u1);
-            ptx::tmem_ld_wait();
-            float hg[64], hu[64];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              hg[j] = bf16r(__uint_as_float(g0[j]));
-              hg[32 + j] = bf16r(__uint_as_float(g1[j]));
-              hu[j] = bf16r(__uint_as_float(u0[j]));
-              hu[32 + j] = bf16r(__uint_as_float(u1[j]));
-            }
             const int col = tc.nt * W + c;
-            stage_row_bf16(sq.acquire(lane), lane, hg);
-            sq.commit2d(lane, &mC0, col, wrow);
-            stage_row_bf16(sq.acquire(lane), lane, hu);
-            sq.commit2d(lane, &mC0, args.n + col, wrow);
+            sq.wait_reads<0>(lane);
+            const uint32_t b0 = sq.addr(0), b1 = sq.addr(1);
+            uint32_t apk[32];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) hg[j] = hg[j] * sigmoidf_fast(hg[j]) * hu[j];
-            stage_row_bf16(sq.acquire(lane), lane, hg);
-            sq.commit2d(lane, &mC1, col, wrow);
+            for (int h = 0; h < 2; ++h) {
+              uint32_t g[32], u[32];
+              ptx::tmem_ld32(t_acc + c + 32 * h, g);
+              ptx::tmem_ld32(t_acc + W + c + 32 * h, u);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int q8 = 0; q8 < 4; ++q8) {
+                float hg[8], hu[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  hg[i] = bf16r(__uint_as_float(g[8 * q8 + i]));
+                  hu[i] = bf16r(__uint_as_float(u[8 * q8 + i]));
+                }
+                const int ch = 4 * h + q8;
+                ptx::st_shared_v4(b0 + swz(lane, ch), ptx::pack_bf16(hg[0], hg[1]), ptx::pack_bf16(hg[2], hg[3]),
+                                  ptx::pack_bf16(hg[4], hg[5]), ptx::pack_bf16(hg[6], hg[7]));
+                ptx::st_shared_v4(b1 + swz(lane, ch), ptx::pack_bf16(hu[0], hu[1]), ptx::pack_bf16(hu[2], hu[3]),
+                                  ptx::pack_bf16(hu[4], hu[5]), ptx::pack_bf16(hu[6], hu[7]));
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float a0 = hg[2 * i] * sigmoidf_fast(hg[2 * i]) * hu[2 * i];
+                  const float a1 = hg[2 * i + 1] * sigmoidf_fast(hg[2 * i + 1]) * hu[2 * i + 1];
+                  apk[4 * ch + i] = ptx::pack_bf16(a0, a1);
+                }
+              }
+            }
+            sq.issue(lane, 0, &mC0, col, wrow);           // H gate columns
+            sq.issue(lane, 1, &mC0, args.n + col, wrow);  // H up columns
+            sq.wait_reads<1>(lane);
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+              ptx::st_shared_v4(b0 + swz(lane, ch), apk[4 * ch], apk[4 * ch + 1], apk[4 * ch + 2], apk[4 * ch + 3]);
+            sq.issue(lane, 0, &mC1, col, wrow);           // A = SwiGLU(H)
           }
         } else {  // n == 32: accumulator columns are [gate 32 | up 32] = the whole H row
-          uint32_t g0[32], u0[32];
-          ptx::tmem_ld32(t_acc, g0);
-          ptx::tmem_ld32(t_acc + 32, u0);
+          uint32_t g[32], u[32];
+          ptx::tmem_ld32(t_acc, g);
+          ptx::tmem_ld32(t_acc + 32, u);
           ptx::tmem_ld_wait();
           float h[64], a[64];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            h[j] = bf16r(__uint_as_float(g0[j]));
-            h[32 + j] = bf16r(__uint_as_float(u0[j]));
+            h[j] = bf16r(__uint_as_float(g[j]));
+            h[32 + j] = bf16r(__uint_as_float(u[j]));
           }
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             a[j] = h[j] * sigmoidf_fast(h[j]) * h[32 + j];
             a[32 + j] = 0.f;
           }
-          stage_row_bf16(sq.acquire(lane), lane, h);
-          sq.commit2d(lane, &mC0, 0, wrow);
-          stage_row_bf16(sq.acquire(lane), lane, a);
-          sq.commit2d(lane, &mC1, 0, wrow);  // columns >= n are clipped by the tensor map
+          int i = sq.acquire(lane);
+          write_row_bf16(sq.addr(i), lane, h);
+          sq.issue(lane, i, &mC0, 0, wrow);
+          i = sq.acquire(lane);
+          write_row_bf16(sq.addr(i), lane, a);
+          sq.issue(lane, i, &mC1, 0, wrow);  // columns >= n are clipped by the tensor map
         }
       } else if constexpr (KIND == K_DOWN || KIND == K_DXT) {
         float gate = 1.f;
@@ -392,18 +458,24 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
         for (int c = 0; c < BN; c += 64) {
           if (tc.nt * BN + c >= args.N_dim) break;
-          uint32_t r0[32], r1[32];
-          ptx::tmem_ld32(t_acc + c, r0);
-          ptx::tmem_ld32(t_acc + c + 32, r1);
-          ptx::tmem_ld_wait();
-          float v[64];
+          const int i = sq.acquire(lane);
+          const uint32_t b = sq.addr(i);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            v[j] = gate * __uint_as_float(r0[j]);
-            v[32 + j] = gate * __uint_as_float(r1[j]);
+          for (int h = 0; h < 2; ++h) {
+            uint32_t r[32];
+            ptx::tmem_ld32(t_acc + c + 32 * h, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int q8 = 0; q8 < 4; ++q8) {
+              const uint32_t* v = r + 8 * q8;
+              ptx::st_shared_v4(b + swz(lane, 4 * h + q8),
+                                ptx::pack_bf16(gate * __uint_as_float(v[0]), gate * __uint_as_float(v[1])),
+                                ptx::pack_bf16(gate * __uint_as_float(v[2]), gate * __uint_as_float(v[3])),
+                                ptx::pack_bf16(gate * __uint_as_float(v[4]), gate * __uint_as_float(v[5])),
+                                ptx::pack_bf16(gate * __uint_as_float(v[6]), gate * __uint_as_float(v[7])));
+            }
           }
-          stage_row_bf16(sq.acquire(lane), lane, v);
-          sq.commit2d(lane, &mC0, tc.nt * BN + c, wrow);
+          sq.issue(lane, i, &mC0, tc.nt * BN + c, wrow);
         }
       } else if constexpr (KIND == K_DH) {
         const float s = __ldg(args.row_gate + row);
@@ -414,52 +486,71 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
           for (int c = 0; c < BN; c += 64) {
             const int col = tc.nt * BN + c;
-            uint4 hg4[8], hu4[8];
+            sq.wait_reads<0>(lane);
+            const uint32_t b0 = sq.addr(0), b1 = sq.addr(1);
+            uint32_t apk[32];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              hg4[i] = ptx::ld_nc_v4(hrow + col + 8 * i);
-              hu4[i] = ptx::ld_nc_v4(hrow + n + col + 8 * i);
-            }
-            uint32_t r0[32], r1[32];
-            ptx::tmem_ld32(t_acc + c, r0);
-            ptx::tmem_ld32(t_acc + c + 32, r1);
-            ptx::tmem_ld_wait();
-            float dg[64], du[64], ap[64];
-            const __nv_bfloat16* hgp = reinterpret_cast<const __nv_bfloat16*>(hg4);
-            const __nv_bfloat16* hup = reinterpret_cast<const __nv_bfloat16*>(hu4);
+            for (int h = 0; h < 2; ++h) {
+              uint4 hg4[4], hu4[4];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) {
-              const float dap = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
-              const float gg = __bfloat162float(hgp[j]);
-              const float uu = __bfloat162float(hup[j]);
-              const float sg = sigmoidf_fast(gg);
-              const float sl = gg * sg;
-              const float A = sl * uu;
-              const float dA = s * dap;
-              dg[j] = dA * uu * sg * (1.f + gg * (1.f - sg));
-              du[j] = dA * sl;
-              ap[j] = s * A;
-              ds = fmaf(dap, A, ds);
+              for (int i = 0; i < 4; ++i) {
+                hg4[i] = ptx::ld_nc_v4(hrow + col + 32 * h + 8 * i);
+                hu4[i] = ptx::ld_nc_v4(hrow + n + col + 32 * h + 8 * i);
+              }
+              uint32_t r[32];
+              ptx::tmem_ld32(t_acc + c + 32 * h, r);
+              ptx::tmem_ld_wait();
+              const __nv_bfloat16* hgp = reinterpret_cast<const __nv_bfloat16*>(hg4);
+              const __nv_bfloat16* hup = reinterpret_cast<const __nv_bfloat16*>(hu4);
+#pragma unroll
+              for (int q8 = 0; q8 < 4; ++q8) {
+                uint32_t pg[4], pu[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  float dg2[2], du2[2], ap2[2];
+#pragma unroll
+                  for (int k = 0; k < 2; ++k) {
+                    const int j = 8 * q8 + 2 * i + k;
+                    const float dap = __uint_as_float(r[j]);
+                    const float gg = __bfloat162float(hgp[j]);
+                    const float uu = __bfloat162float(hup[j]);
+                    const float sg = sigmoidf_fast(gg);
+                    const float sl = gg * sg;
+                    const float A = sl * uu;
+                    const float dA = s * dap;
+                    dg2[k] = dA * uu * sg * (1.f + gg * (1.f - sg));
+                    du2[k] = dA * sl;
+                    ap2[k] = s * A;
+                    ds = fmaf(dap, A, ds);
+                  }
+                  pg[i] = ptx::pack_bf16(dg2[0], dg2[1]);
+                  pu[i] = ptx::pack_bf16(du2[0], du2[1]);
+                  apk[16 * h + 4 * q8 + i] = ptx::pack_bf16(ap2[0], ap2[1]);
+                }
+                ptx::st_shared_v4(b0 + swz(lane, 4 * h + q8), pg[0], pg[1], pg[2], pg[3]);
+                ptx::st_shared_v4(b1 + swz(lane, 4 * h + q8), pu[0], pu[1], pu[2], pu[3]);
+              }
             }
-            stage_row_bf16(sq.acquire(lane), lane, dg);
-            sq.commit2d(lane, &mC0, col, wrow);
-            stage_row_bf16(sq.acquire(lane), lane, du);
-            sq.commit2d(lane, &mC0, n + col, wrow);
-            stage_row_bf16(sq.acquire(lane), lane, ap);
-            sq.commit2d(lane, &mC1, col, wrow);
+            sq.issue(lane, 0, &mC0, col, wrow);      // dH gate columns
+            sq.issue(lane, 1, &mC0, n + col, wrow);  // dH up columns
+            sq.wait_reads<1>(lane);
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch)
+              ptx::st_shared_v4(b0 + swz(lane, ch), apk[4 * ch], apk[4 * ch + 1], apk[4 * ch + 2], apk[4 * ch + 3]);
+            sq.issue(lane, 0, &mC1, col, wrow);      // A' = s A
           }
         } else {  // n == 32, BN == 32: H row = [gate 32 | up 32]
           uint4 h4[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) h4[i] = ptx::ld_nc_v4(hrow + 8 * i);
-          uint32_t r0[32];
-          ptx::tmem_ld32(t_acc, r0);
+          uint32_t r[32];
+          ptx::tmem_ld32(t_acc, r);
           ptx::tmem_ld_wait();
           const __nv_bfloat16* hp = reinterpret_cast<const __nv_bfloat16*>(h4);
           float dh[64], ap[64];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
-            const float dap = __uint_as_float(r0[j]);
+            const float dap = __uint_as_float(r[j]);
             const float gg = __bfloat162float(hp[j]);
             const float uu = __bfloat162float(hp[32 + j]);
             const float sg = sigmoidf_fast(gg);
@@ -472,10 +563,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             ap[32 + j] = 0.f;
             ds = fmaf(dap, A, ds);
           }
-          stage_row_bf16(sq.acquire(lane), lane, dh);
-          sq.commit2d(lane, &mC0, 0, wrow);
-          stage_row_bf16(sq.acquire(lane), lane, ap);
-          sq.commit2d(lane, &mC1, 0, wrow);
+          int i = sq.acquire(lane);
+          write_row_bf16(sq.addr(i), lane, dh);
+          sq.issue(lane, i, &mC0, 0, wrow);
+          i = sq.acquire(lane);
+          write_row_bf16(sq.addr(i), lane, ap);
+          sq.issue(lane, i, &mC1, 0, wrow);
         }
         if (__ldg(args.row_token + row) < 0) ds = 0.f;
         if (args.n_tiles == 1)
@@ -488,19 +581,20 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll 1
           for (int c = 0; c < BN; c += 32) {
             if (tc.nt * BN + c >= args.N_dim) break;
-            float v[32];
+            const int i = sq.acquire(lane);
+            const uint32_t b = sq.addr(i);
             if (tc.nkb > 0) {
-              uint32_t r0[32];
-              ptx::tmem_ld32(t_acc + c, r0);
+              uint32_t r[32];
+              ptx::tmem_ld32(t_acc + c, r);
               ptx::tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r0[j]);
+              for (int ch = 0; ch < 8; ++ch)
+                ptx::st_shared_v4(b + swz(lane, ch), r[4 * ch], r[4 * ch + 1], r[4 * ch + 2], r[4 * ch + 3]);
             } else {
 #pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = 0.f;
+              for (int ch = 0; ch < 8; ++ch) ptx::st_shared_v4(b + swz(lane, ch), 0u, 0u, 0u, 0u);
             }
-            stage_row_f32(sq.acquire(lane), lane, v);
-            sq.commit3d(lane, &mC0, tc.nt * BN + c, m0, tc.e);
+            sq.issue3d(lane, i, &mC0, tc.nt * BN + c, m0, tc.e);
           }
         }
       }
@@ -516,7 +610,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == NP) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }

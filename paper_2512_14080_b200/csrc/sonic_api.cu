@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <vector>
 
 #include "../../include/sonic.h"
 #include "gemm.cuh"
@@ -14,6 +15,47 @@ using namespace sonic;
 namespace {
 
 thread_local int g_launches = 0;
+
+// ---------------------------------------------------------------- optional per-kernel timing
+// When enabled (sonic_profile_enable), every launch is bracketed by CUDA events on its
+// stream; sonic_profile_collect() returns the per-name durations.  Used by bench.py to time
+// the dominant kernel live inside the timed region.
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+thread_local bool g_prof = false;
+thread_local std::vector<ProfRec> g_recs;
+thread_local std::vector<cudaEvent_t> g_pool;
+cudaEvent_t pool_get() {
+  if (!g_pool.empty()) {
+    cudaEvent_t e = g_pool.back();
+    g_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct ProfScope {
+  cudaStream_t st;
+  ProfRec r;
+  bool on;
+  ProfScope(const char* name, cudaStream_t s) : st(s), on(g_prof) {
+    if (on) {
+      r.name = name;
+      r.a = pool_get();
+      r.b = pool_get();
+      cudaEventRecord(r.a, st);
+    }
+  }
+  ~ProfScope() {
+    if (on) {
+      cudaEventRecord(r.b, st);
+      g_recs.push_back(r);
+    }
+  }
+};
 
 // ---------------------------------------------------------------- tensor maps
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -83,7 +125,7 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
       return false;
     attr = true;
   }
-  sonic_gemm_kernel<KIND, BN><<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(a, b, c0, c1, args);
+  sonic_gemm_kernel<KIND, BN><<<grid, gemm_threads<KIND>(), Cfg::SMEM, st>>>(a, b, c0, c1, args);
   ++g_launches;
   return true;
 }
@@ -254,6 +296,27 @@ const char* sonic_status_string(sonic_status s) {
 
 int sonic_last_launch_count(void) { return g_launches; }
 
+void sonic_profile_enable(int on) { g_prof = on != 0; }
+
+int sonic_profile_collect(char* names, int name_len, float* ms, int max_records) {
+  int n = 0;
+  for (auto& r : g_recs) {
+    if (n < max_records) {
+      float t = 0.f;
+      cudaEventSynchronize(r.b);
+      cudaEventElapsedTime(&t, r.a, r.b);
+      strncpy(names + (size_t)n * name_len, r.name, name_len - 1);
+      names[(size_t)n * name_len + name_len - 1] = 0;
+      ms[n] = t;
+      ++n;
+    }
+    g_pool.push_back(r.a);
+    g_pool.push_back(r.b);
+  }
+  g_recs.clear();
+  return n;
+}
+
 sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing* rt, void* ws, size_t ws_bytes,
                          void* stream) {
   g_launches = 0;
@@ -284,7 +347,10 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   L.tokcnt = reinterpret_cast<int*>(base + w.tokcnt);
   L.flip = reinterpret_cast<int*>(base + w.flip);
   L.ST = reinterpret_cast<float*>(base + w.ST);
-  g_launches = launch_route(L, static_cast<cudaStream_t>(stream));
+  {
+    ProfScope ps("route", static_cast<cudaStream_t>(stream));
+    g_launches = launch_route(L, static_cast<cudaStream_t>(stream));
+  }
   return check_launch();
 }
 
@@ -320,6 +386,8 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = n / Wg; a.k_blocks = d / 64; a.N_dim = 2 * n;
+    a.gsrc = static_cast<const __nv_bfloat16*>(X); a.gld = d;
+    ProfScope ps("up", st);
     if (!launch_gemm<K_UP>(BN, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
   }
   // K2 down-proj: Y = gate * (A W2_e)
@@ -331,9 +399,11 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = d / BN; a.k_blocks = (n + 63) / 64; a.N_dim = d;
+    ProfScope ps("down", st);
     if (!launch_gemm<K_DOWN>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
   }
   // K3 aggregation: O_t = sum of the token's Y rows
+  ProfScope ps("agg_O", st);
   launch_aggregate(static_cast<const __nv_bfloat16*>(Ybuf), rt->token_rowptr, rt->token_rows,
                    static_cast<__nv_bfloat16*>(O), s.T, d, st);
   ++g_launches;
@@ -376,9 +446,14 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = n / BN; a.k_blocks = d / 64; a.N_dim = n; a.H = static_cast<const __nv_bfloat16*>(H);
+    a.gsrc = static_cast<const __nv_bfloat16*>(dO); a.gld = d;
     a.dS = a.n_tiles > 1 ? dSp : dS;
-    if (!launch_gemm<K_DH>(BN, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
+    {
+      ProfScope ps("dH", st);
+      if (!launch_gemm<K_DH>(BN, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
+    }
     if (a.n_tiles > 1) {
+      ProfScope ps("dS_reduce", st);
       launch_ds_reduce(dSp, a.n_tiles, R, rt->num_tiles, dS, st);
       ++g_launches;
     }
@@ -392,7 +467,9 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = d / BN; a.m_tiles = (n + 127) / 128; a.M_dim = n; a.N_dim = d;
+    a.gsrc = static_cast<const __nv_bfloat16*>(dO); a.gld = d;
     const int tiles = E * a.m_tiles * a.n_tiles;
+    ProfScope ps("dW2", st);
     if (!launch_gemm<K_DW2>(BN, mA, mB, mC0, mC0, a, std::min(grid, tiles), st)) return SONIC_ERR_CUDA;
   }
   // K6 dX~_e = dH_e W1_e^T
@@ -404,6 +481,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = d / BN; a.k_blocks = (2 * n) / 64; a.N_dim = d;
+    ProfScope ps("dXt", st);
     if (!launch_gemm<K_DXT>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
   }
   // K7 dW1_e = Gather(X)^T dH_e   (varlen-K)
@@ -415,10 +493,13 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = (2 * n) / BN; a.m_tiles = (d + 127) / 128; a.M_dim = d; a.N_dim = 2 * n;
+    a.gsrc = static_cast<const __nv_bfloat16*>(X); a.gld = d;
     const int tiles = E * a.m_tiles * a.n_tiles;
+    ProfScope ps("dW1", st);
     if (!launch_gemm<K_DW1>(BN, mA, mB, mC0, mC0, a, std::min(grid, tiles), st)) return SONIC_ERR_CUDA;
   }
   // K8 dX aggregation
+  ProfScope ps("agg_dX", st);
   launch_aggregate(static_cast<const __nv_bfloat16*>(dXt), rt->token_rowptr, rt->token_rows,
                    static_cast<__nv_bfloat16*>(dX), s.T, d, st);
   ++g_launches;

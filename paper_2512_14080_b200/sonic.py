@@ -72,6 +72,11 @@ def lib():
         L.sonic_status_string.restype = ctypes.c_char_p
         L.sonic_last_launch_count.argtypes = []
         L.sonic_last_launch_count.restype = ctypes.c_int
+        L.sonic_profile_enable.argtypes = [ctypes.c_int]
+        L.sonic_profile_enable.restype = None
+        L.sonic_profile_collect.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
+                                            ctypes.c_int]
+        L.sonic_profile_collect.restype = ctypes.c_int
         _lib = L
     return _lib
 
@@ -123,6 +128,19 @@ def sonic_workspace_offsets(desc, which):
 
 def sonic_last_launch_count():
     return int(lib().sonic_last_launch_count())
+
+
+def sonic_profile_enable(on=True):
+    lib().sonic_profile_enable(1 if on else 0)
+
+
+def sonic_profile_collect(max_records=1 << 16, name_len=32):
+    """[(name, ms), ...] of the kernels launched since profiling was enabled / last collected."""
+    names = ctypes.create_string_buffer(max_records * name_len)
+    ms = (ctypes.c_float * max_records)()
+    n = lib().sonic_profile_collect(names, name_len, ms, max_records)
+    raw = names.raw
+    return [(raw[i * name_len:(i + 1) * name_len].split(b"\0", 1)[0].decode(), float(ms[i])) for i in range(n)]
 
 
 @dataclass
