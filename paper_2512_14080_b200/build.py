@@ -23,7 +23,8 @@ def up_to_date():
 def build(force=False, verbose=False):
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC] + FLAGS + ["-o", OUT] + [os.path.join(HERE, s) for s in SRCS]
+    extra = os.environ.get("SONIC_NVCC_EXTRA", "").split()
+    cmd = [NVCC] + FLAGS + extra + ["-o", OUT] + [os.path.join(HERE, s) for s in SRCS]
     r = subprocess.run(cmd, cwd=HERE, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -59,33 +59,39 @@ __device__ int block_excl_scan(int v, int* total) {
 }
 
 // ---------------------------------------------------------------- top-K
-template <int VPL>
-__global__ void k_route_topk(const float* __restrict__ S, int T, int E, int K, int W, int* __restrict__ topk_ids,
-                             float* __restrict__ topk_s, uint32_t* __restrict__ bm_tc) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
+// G lanes per token (G | 32), VPL scores per lane: lane g of a group holds experts g, g+G, ...
+// Exact 64-bit keys (ordered score << 32 | ~expert): the largest key is the largest score and,
+// among equal scores, the lower expert id -- the stable order of P:1099 without packing loss.
+template <int G, int VPL>
+__global__ void __launch_bounds__(256) k_route_topk(const float* __restrict__ S, int T, int E, int K, int W,
+                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
+                                                    uint32_t* __restrict__ bm_tc) {
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = gt / G;
+  const int g = gt % G;
+  if (t >= T) return;  // G divides 32 and T is processed in whole groups: no partial-group shuffles
   const float* row = S + (size_t)t * E;
   unsigned long long key[VPL];
 #pragma unroll
   for (int j = 0; j < VPL; ++j) {
-    const int e = lane + 32 * j;
+    const int e = g + G * j;
     key[j] = e < E ? ((unsigned long long)ord_f32(__ldg(row + e)) << 32) | (0xFFFFFFFFu - (uint32_t)e) : 0ull;
   }
+  const unsigned mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
   for (int k = 0; k < K; ++k) {
     unsigned long long best = 0;
 #pragma unroll
     for (int j = 0; j < VPL; ++j) best = key[j] > best ? key[j] : best;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const unsigned long long other = __shfl_xor_sync(mask, best, o, G);
       best = other > best ? other : best;
     }
 #pragma unroll
     for (int j = 0; j < VPL; ++j)
       if (key[j] == best) key[j] = 0ull;
     const int e = (int)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull));
-    if (lane == 0) {
+    if (g == (k % G)) {
       topk_ids[(size_t)t * K + k] = e;
       topk_s[(size_t)t * K + k] = __ldg(row + e);
       atomicOr(bm_tc + (size_t)e * W + (t >> 5), 1u << (t & 31));
@@ -93,9 +99,56 @@ __global__ void k_route_topk(const float* __restrict__ S, int T, int E, int K, i
   }
 }
 
+// TC fast path of the token CSR: every token keeps exactly its K top-K experts, so
+// rowptr[t] = t*K and the rows are the top-K experts in ascending id order.  The row of
+// (t, e) is pad_offsets[e] + (rank of t among e's tokens) = pad_offsets[e] + wprefix[e][t/32]
+// + popc(bm[e][t/32] & lanes_below(t)).  Gates renormalise the top-K scores (Q13).
+__global__ void k_token_rows_tc(const int* __restrict__ topk_ids, const float* __restrict__ topk_s,
+                                const uint32_t* __restrict__ bm, const int* __restrict__ wprefix, int T, int K, int W,
+                                const int* __restrict__ pad_offsets, int gate_raw, int* __restrict__ rowptr,
+                                int* __restrict__ token_rows, float* __restrict__ row_gate) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > T) return;
+  rowptr[t] = t * K;
+  if (t == T) return;
+  int ids[16];
+  float sc[16];
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    if (k < K) {
+      ids[k] = topk_ids[(size_t)t * K + k];
+      sc[k] = topk_s[(size_t)t * K + k];
+    }
+  }
+  // insertion sort by expert id (K <= 16)
+  for (int i = 1; i < K; ++i) {
+    const int id = ids[i];
+    const float s = sc[i];
+    int j = i - 1;
+    while (j >= 0 && ids[j] > id) {
+      ids[j + 1] = ids[j];
+      sc[j + 1] = sc[j];
+      --j;
+    }
+    ids[j + 1] = id;
+    sc[j + 1] = s;
+  }
+  for (int k = 0; k < K; ++k) sum += sc[k];
+  const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
+  const int w = t >> 5;
+  const uint32_t below = (1u << (t & 31)) - 1u;
+  for (int k = 0; k < K; ++k) {
+    const int e = ids[k];
+    const int r = pad_offsets[e] + wprefix[(size_t)e * W + w] + __popc(bm[(size_t)e * W + w] & below);
+    token_rows[(size_t)t * K + k] = r;
+    row_gate[r] = gate_raw ? sc[k] : sc[k] * inv;
+  }
+}
+
 // ---------------------------------------------------------------- per-expert popcount
 __global__ void k_expert_popc(const uint32_t* __restrict__ bm, int W, int* __restrict__ wprefix,
-                              int* __restrict__ cnt) {
+                              int* __restrict__ cnt, int* __restrict__ cnt2) {
   const int e = blockIdx.x;
   int base = 0;
   for (int w0 = 0; w0 < W; w0 += blockDim.x) {
@@ -106,7 +159,10 @@ __global__ void k_expert_popc(const uint32_t* __restrict__ bm, int W, int* __res
     if (wprefix && w < W) wprefix[(size_t)e * W + w] = base + ex;
     base += tot;
   }
-  if (threadIdx.x == 0) cnt[e] = base;
+  if (threadIdx.x == 0) {
+    cnt[e] = base;
+    if (cnt2) cnt2[e] = base;
+  }
 }
 
 // ---------------------------------------------------------------- TR decision (NR-f)
@@ -324,57 +380,77 @@ __global__ void k_build_rows(const uint32_t* __restrict__ bm_kept, const int* __
   }
 }
 
-// ---------------------------------------------------------------- token CSR
+// ---------------------------------------------------------------- token CSR (general / TR path)
+// Warp per 32-token word; the E bitmap words are read 8 at a time (independent loads in flight).
 __global__ void k_token_count(const uint32_t* __restrict__ bm_kept, int T, int E, int W, int* __restrict__ cnt) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= W) return;
   int c = 0;
-  for (int e = 0; e < E; ++e) c += (__ldg(bm_kept + (size_t)e * W + w) >> lane) & 1u;
+  int e = 0;
+  for (; e + 8 <= E; e += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldg(bm_kept + (size_t)(e + i) * W + w);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) c += (v[i] >> lane) & 1u;
+  }
+  for (; e < E; ++e) c += (__ldg(bm_kept + (size_t)e * W + w) >> lane) & 1u;
   const int t = w * 32 + lane;
   if (t < T) cnt[t] = c;
 }
 
+// One block: thread i scans the contiguous chunk [i*per, (i+1)*per) sequentially, one block
+// scan combines the chunk sums.
 __global__ void __launch_bounds__(1024) k_scan_tokens(const int* __restrict__ cnt, int T, int* __restrict__ rowptr) {
-  int base = 0;
-  for (int t0 = 0; t0 < T; t0 += blockDim.x) {
-    const int t = t0 + threadIdx.x;
-    const int c = t < T ? cnt[t] : 0;
-    int tot;
-    const int ex = block_excl_scan(c, &tot);
-    if (t < T) rowptr[t] = base + ex;
-    base += tot;
+  const int per = (T + blockDim.x - 1) / blockDim.x;
+  const int t0 = threadIdx.x * per;
+  const int t1 = min(t0 + per, T);
+  int s = 0;
+  for (int t = t0; t < t1; ++t) s += cnt[t];
+  int tot;
+  int run = block_excl_scan(s, &tot);
+  for (int t = t0; t < t1; ++t) {
+    rowptr[t] = run;
+    run += cnt[t];
   }
-  if (threadIdx.x == 0) rowptr[T] = base;
+  if (threadIdx.x == 0) rowptr[T] = tot;
 }
 
+// Rows of each token in ascending expert order + renormalised gates.  Pass 2 recovers the
+// expert of a row from the 128-row tile map (segments are tile aligned).
 __global__ void k_token_rows(const uint32_t* __restrict__ bm_kept, const int* __restrict__ wprefix, int T, int E,
-                             int W, const int* __restrict__ pad_offsets, const int* __restrict__ rowptr,
-                             const float* __restrict__ S, int gate_raw, int* __restrict__ token_rows,
-                             float* __restrict__ row_gate) {
+                             int W, const int* __restrict__ pad_offsets, const int* __restrict__ tile_expert,
+                             const int* __restrict__ rowptr, const float* __restrict__ S, int gate_raw,
+                             int* __restrict__ token_rows, float* __restrict__ row_gate) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= W) return;
   const int t = w * 32 + lane;
   const bool valid = t < T;
   const uint32_t below = (1u << lane) - 1u;
-  int j = valid ? rowptr[t] : 0;
+  const int j0 = valid ? rowptr[t] : 0;
+  int j = j0;
   float sum = 0.f;
-  for (int e = 0; e < E; ++e) {
-    const uint32_t word = __ldg(bm_kept + (size_t)e * W + w);
-    if (valid && ((word >> lane) & 1u)) {
-      token_rows[j++] = pad_offsets[e] + wprefix[(size_t)e * W + w] + __popc(word & below);
-      sum += __ldg(S + (size_t)t * E + e);
+  int e = 0;
+  for (; e < E; e += 8) {
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (e + i < E) ? __ldg(bm_kept + (size_t)(e + i) * W + w) : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (valid && ((v[i] >> lane) & 1u)) {
+        token_rows[j++] = pad_offsets[e + i] + wprefix[(size_t)(e + i) * W + w] + __popc(v[i] & below);
+        sum += __ldg(S + (size_t)t * E + e + i);
+      }
     }
   }
+  if (!valid) return;
   const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
-  j = valid ? rowptr[t] : 0;
-  for (int e = 0; e < E; ++e) {
-    const uint32_t word = __ldg(bm_kept + (size_t)e * W + w);
-    if (valid && ((word >> lane) & 1u)) {
-      const float s = __ldg(S + (size_t)t * E + e);
-      row_gate[token_rows[j++]] = gate_raw ? s : s * inv;
-    }
+  for (int k = j0; k < j; ++k) {
+    const int r = token_rows[k];
+    const float s = __ldg(S + (size_t)t * E + tile_expert[r / GEMM_M]);
+    row_gate[r] = gate_raw ? s : s * inv;
   }
 }
 
@@ -384,25 +460,24 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   const int T = (int)L.T, E = L.E, K = L.K, W = L.W;
   cudaMemsetAsync(L.bm_tc, 0, (size_t)E * W * 4, st);
   {
-    const int vpl = (E + 31) / 32;
-    const int threads = 256, blocks = (T * 32 + threads - 1) / threads;
-#define TOPK_CASE(V) \
-  k_route_topk<V><<<blocks, threads, 0, st>>>(L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
-    if (vpl <= 1) TOPK_CASE(1);
-    else if (vpl <= 2) TOPK_CASE(2);
-    else if (vpl <= 4) TOPK_CASE(4);
-    else if (vpl <= 8) TOPK_CASE(8);
-    else if (vpl <= 12) TOPK_CASE(12);
-    else if (vpl <= 16) TOPK_CASE(16);
-    else if (vpl <= 32) TOPK_CASE(32);
-    else if (vpl <= 64) TOPK_CASE(64);
-    else TOPK_CASE(128);
+    const int threads = 256;
+#define TOPK_CASE(G, V)                                                             \
+  k_route_topk<G, V><<<(int)(((long long)T * G + threads - 1) / threads), threads, 0, st>>>( \
+      L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
+    if (E <= 32) TOPK_CASE(4, 8);
+    else if (E <= 64) TOPK_CASE(8, 8);
+    else if (E <= 128) TOPK_CASE(8, 16);
+    else if (E <= 256) TOPK_CASE(16, 16);
+    else if (E <= 512) TOPK_CASE(32, 16);
+    else if (E <= 1024) TOPK_CASE(32, 32);
+    else if (E <= 2048) TOPK_CASE(32, 64);
+    else TOPK_CASE(32, 128);
 #undef TOPK_CASE
     ++nl;
   }
-  k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, nullptr, L.f); ++nl;
   const uint32_t* bm_kept = L.bm_tc;
   if (L.mode == 1) {  // token rounding
+    k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
     k_tr_decide<<<(E + 255) / 256, 256, 0, st>>>(L.f, L.f_r, E, T, L.m_tile); ++nl;
     k_transpose<<<dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st>>>(L.S, L.ST, T, E); ++nl;
     k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0); ++nl;
@@ -412,17 +487,23 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
       k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1); ++nl;
     }
     bm_kept = L.bm_kept;
-    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r); ++nl;
-  } else {
-    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r); ++nl;
+    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r, nullptr); ++nl;
+  } else {  // TC: one pass gives f, f_r (== f) and the word prefixes
+    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f, L.f_r); ++nl;
   }
   k_offsets<<<1, 1024, 0, st>>>(L.f_r, E, L.offsets, L.pad_offsets, L.tile_expert, L.num_tiles); ++nl;
   k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
                                                          L.row_gate); ++nl;
-  k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, T, E, W, L.tokcnt); ++nl;
-  k_scan_tokens<<<1, 1024, 0, st>>>(L.tokcnt, T, L.token_rowptr); ++nl;
-  k_token_rows<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, L.wprefix, T, E, W, L.pad_offsets, L.token_rowptr,
-                                                     L.S, L.gate_raw, L.token_rows, L.row_gate); ++nl;
+  if (L.mode == 0) {
+    k_token_rows_tc<<<(T + 1 + 255) / 256, 256, 0, st>>>(L.topk_ids, L.topk_s, bm_kept, L.wprefix, T, K, W,
+                                                         L.pad_offsets, L.gate_raw, L.token_rowptr, L.token_rows,
+                                                         L.row_gate); ++nl;
+  } else {
+    k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, T, E, W, L.tokcnt); ++nl;
+    k_scan_tokens<<<1, 1024, 0, st>>>(L.tokcnt, T, L.token_rowptr); ++nl;
+    k_token_rows<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, L.wprefix, T, E, W, L.pad_offsets, L.tile_expert,
+                                                       L.token_rowptr, L.S, L.gate_raw, L.token_rows, L.row_gate); ++nl;
+  }
   return nl;
 }
 

@@ -116,8 +116,8 @@ int num_sms() {
 // ---------------------------------------------------------------- GEMM launch
 template <int KIND, int BN>
 bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
-                   const GemmArgs& args, int grid, cudaStream_t st) {
-  using Cfg = GemmCfg<BN>;
+                   const CUtensorMap& dmap, const GemmArgs& args, int grid, cudaStream_t st) {
+  using Cfg = KCfg<KIND, BN>;
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(sonic_gemm_kernel<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) !=
@@ -125,20 +125,22 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
       return false;
     attr = true;
   }
-  sonic_gemm_kernel<KIND, BN><<<grid, gemm_threads<KIND>(), Cfg::SMEM, st>>>(a, b, c0, c1, args);
+  sonic_gemm_kernel<KIND, BN><<<grid, gemm_threads<KIND>(), Cfg::SMEM, st>>>(a, b, c0, c1, dmap, args);
   ++g_launches;
   return true;
 }
 
+// dmap: auxiliary tensor map (DH: the H cache, box {64, 32}); ignored by the other kinds.
 template <int KIND>
 bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
-                 const GemmArgs& args, int grid, cudaStream_t st) {
+                 const GemmArgs& args, int grid, cudaStream_t st, const CUtensorMap* dmap = nullptr) {
+  const CUtensorMap& d = dmap ? *dmap : c0;
   switch (BN) {
-    case 256: return launch_gemm_t<KIND, 256>(a, b, c0, c1, args, grid, st);
-    case 128: return launch_gemm_t<KIND, 128>(a, b, c0, c1, args, grid, st);
-    case 64: return launch_gemm_t<KIND, 64>(a, b, c0, c1, args, grid, st);
+    case 256: return launch_gemm_t<KIND, 256>(a, b, c0, c1, d, args, grid, st);
+    case 128: return launch_gemm_t<KIND, 128>(a, b, c0, c1, d, args, grid, st);
+    case 64: return launch_gemm_t<KIND, 64>(a, b, c0, c1, d, args, grid, st);
     case 32:
-      if constexpr (KIND == K_DH) return launch_gemm_t<KIND, 32>(a, b, c0, c1, args, grid, st);
+      if constexpr (KIND == K_DH) return launch_gemm_t<KIND, 32>(a, b, c0, c1, d, args, grid, st);
       return false;
     default: return false;
   }
@@ -206,7 +208,12 @@ RouteWs route_ws(const sonic_moe_desc* D) {
   return w;
 }
 
-int dh_bn(int n) { return n % 256 == 0 ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32; }
+#ifndef SONIC_DH_MAX_BN
+#define SONIC_DH_MAX_BN 128  // BN <= 128 leaves room for the TMA-loaded H buffers (gemm.cuh KCfg)
+#endif
+int dh_bn(int n) {
+  return (n % 256 == 0 && SONIC_DH_MAX_BN >= 256) ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
+}
 
 struct FwdWs { size_t A, Y, total; };
 FwdWs fwd_ws(const sonic_moe_desc* D) {
@@ -439,10 +446,11 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
 
   // K4 dH: dA' = Gather(dO) W2_e^T; epilogue dSwiGLU -> dH, A' = s A, dS = <dA', A>
   {
-    CUtensorMap mA, mB, mC0, mC1;
+    CUtensorMap mA, mB, mC0, mC1, mH;
     const int BN = dh_bn(n);
     if (!map2d(&mA, dO, false, s.T, d, 64, 1) || !map3d(&mB, W2, false, E, n, d, 64, BN) ||
-        !map2d(&mC0, dH, false, R, 2 * n, 64, 32) || !map2d(&mC1, Ap, false, R, n, 64, 32))
+        !map2d(&mC0, dH, false, R, 2 * n, 64, 32) || !map2d(&mC1, Ap, false, R, n, 64, 32) ||
+        !map2d(&mH, H, false, R, 2 * n, 64, 32))
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = n / BN; a.k_blocks = d / 64; a.N_dim = n; a.H = static_cast<const __nv_bfloat16*>(H);
@@ -450,7 +458,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     a.dS = a.n_tiles > 1 ? dSp : dS;
     {
       ProfScope ps("dH", st);
-      if (!launch_gemm<K_DH>(BN, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
+      if (!launch_gemm<K_DH>(BN, mA, mB, mC0, mC1, a, grid, st, &mH)) return SONIC_ERR_CUDA;
     }
     if (a.n_tiles > 1) {
       ProfScope ps("dS_reduce", st);
