@@ -79,14 +79,15 @@ constexpr int GEMM_BK = 64;
 constexpr int STG_BYTES = 4096;  // one epilogue staging buffer: 32 rows x 128 B
 constexpr int SMEM_LIMIT = 232448;
 
-template <int BN, bool HTMA = false>
+template <int BN, bool HTMA = false, int NB_ = 2>
 struct GemmCfg {
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int NB = NB_;  // epilogue staging buffers per epilogue warp (ring)
   // DH only: per-epilogue-warp H buffer, 32 rows x (BN gate + BN up) bf16 columns (TMA-loaded)
   static constexpr int HBUF_WARP = HTMA ? 32 * 2 * BN * 2 : 0;
-  static constexpr int FIXED = 4 * 2 * STG_BYTES + 4 * HBUF_WARP + 1024 + 256;
+  static constexpr int FIXED = 4 * NB * STG_BYTES + 4 * HBUF_WARP + 1024 + 256;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - FIXED) / (int)STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
@@ -97,8 +98,21 @@ struct GemmCfg {
 
 // DH with BN in {64, 128} reads H through TMA into per-warp smem buffers ("asynchronous
 // TMA load of H in the dH epilogue"); wider tiles would not leave room for the buffer.
+// Staging ring depth: a deeper ring lets each TMA store finish reading smem while later
+// ones are written (the epilogue was the measured limiter); at BN = 256 the
+// price is one mainloop stage (3 instead of 4).
+#ifndef SONIC_NB_WIDE
+#define SONIC_NB_WIDE 2
+#endif
+#ifndef SONIC_NB_NARROW
+#define SONIC_NB_NARROW 2
+#endif
 template <int KIND, int BN>
-using KCfg = GemmCfg<BN, KIND == K_DH && (BN == 64 || BN == 128)>;
+__host__ __device__ constexpr int staging_nb() {
+  return KIND == K_DH ? 2 : (BN == 256 ? SONIC_NB_WIDE : SONIC_NB_NARROW);
+}
+template <int KIND, int BN>
+using KCfg = GemmCfg<BN, KIND == K_DH && (BN == 64 || BN == 128), staging_nb<KIND, BN>()>;
 
 struct TileCoord {
   int e, row0, nt, mt, nkb, seg0;
@@ -141,20 +155,25 @@ __device__ __forceinline__ float tanh_approx(float x) {
 __device__ __forceinline__ float sigmoidf_fast(float x) { return fmaf(0.5f, tanh_approx(0.5f * x), 0.5f); }
 __device__ __forceinline__ uint32_t swz(int lane, int chunk) { return (uint32_t)(lane * 128 + ((chunk ^ (lane & 7)) << 4)); }
 
-// Per-warp double-buffered TMA store pipeline (32 rows x 128 B per buffer, 128B swizzle).
+// Per-warp ring of NB TMA-store staging buffers (32 rows x 128 B each, 128B swizzle).  Stores
+// are issued in ring order, one bulk group each, so the buffer k slots ahead of the head was last
+// stored from NB-k stores ago: it is free once at most NB-1-k newer groups are pending a read.
+template <int NB>
 struct StoreQ {
   uint8_t* base;
-  int sb;
+  int sb;  // ring head: the next buffer to write
   __device__ __forceinline__ uint32_t addr(int i) const { return ptx::smem_u32(base + i * STG_BYTES); }
   template <int N>
   __device__ __forceinline__ void wait_reads(int lane) {
     if (lane == 0) ptx::bulk_wait_read<N>();
     __syncwarp();
   }
-  // next buffer in round-robin order, waiting until the store issued from it has read smem
+  // the buffer k slots ahead of the head, once it is free to overwrite
+  template <int K = 0>
   __device__ __forceinline__ int acquire(int lane) {
-    wait_reads<1>(lane);
-    return sb;
+    static_assert(K < NB, "ring too shallow");
+    wait_reads<NB - 1 - K>(lane);
+    return (sb + K) % NB;
   }
   __device__ __forceinline__ void issue(int lane, int i, const CUtensorMap* map, int c0, int c1) {
     ptx::fence_proxy_async_smem();
@@ -163,7 +182,7 @@ struct StoreQ {
       ptx::tma_store_2d(map, base + i * STG_BYTES, c0, c1);
       ptx::bulk_commit();
     }
-    sb = i ^ 1;
+    sb = (i + 1) % NB;
   }
   __device__ __forceinline__ void issue3d(int lane, int i, const CUtensorMap* map, int c0, int c1, int c2) {
     ptx::fence_proxy_async_smem();
@@ -172,7 +191,7 @@ struct StoreQ {
       ptx::tma_store_3d(map, base + i * STG_BYTES, c0, c1, c2);
       ptx::bulk_commit();
     }
-    sb = i ^ 1;
+    sb = (i + 1) % NB;
   }
 };
 
@@ -212,7 +231,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + STAGES * STAGE_BYTES;
-  uint8_t* hbuf = stg + 4 * 2 * STG_BYTES;  // DH: 4 x HBUF_WARP
+  uint8_t* hbuf = stg + 4 * Cfg::NB * STG_BYTES;  // DH: 4 x HBUF_WARP
   uint64_t* full = reinterpret_cast<uint64_t*>(hbuf + 4 * Cfg::HBUF_WARP);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -433,7 +452,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     // ============================================================ epilogue (4 warps)
     const int ew = warp - NP - 1;
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    StoreQ sq{stg + ew * 2 * STG_BYTES, 0};
+    StoreQ<Cfg::NB> sq{stg + ew * Cfg::NB * STG_BYTES, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
     // DH (HTMA): each epilogue warp TMA-loads its own 32 rows of H (BN gate + BN up columns)
@@ -485,14 +504,25 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
 
+#ifdef SONIC_EXPERIMENT_NO_EPI
+      if constexpr (true) {  // ablation: mainloop only
+        if (has_next) h_issue(tile + gridDim.x);
+        if constexpr (HTMA) {
+          ptx::mbar_wait(&hfull[ew], hphase);
+          hphase ^= 1;
+        }
+      } else
+#endif
       if constexpr (KIND == K_UP) {
         constexpr int W = BN / 2;
         if constexpr (W >= 64) {
 #pragma unroll 1
           for (int c = 0; c < W; c += 64) {
             const int col = tc.nt * W + c;
-            sq.wait_reads<0>(lane);
-            const uint32_t b0 = sq.addr(0), b1 = sq.addr(1);
+            sq.acquire<1>(lane);  // the next two ring slots are both free
+            const int i0 = sq.sb;
+            const int i1 = (i0 + 1) % Cfg::NB;
+            const uint32_t b0 = sq.addr(i0), b1 = sq.addr(i1);
             uint32_t apk[32];
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -521,13 +551,14 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
                 }
               }
             }
-            sq.issue(lane, 0, &mC0, col, wrow);           // H gate columns
-            sq.issue(lane, 1, &mC0, args.n + col, wrow);  // H up columns
-            sq.wait_reads<1>(lane);
+            sq.issue(lane, i0, &mC0, col, wrow);           // H gate columns
+            sq.issue(lane, i1, &mC0, args.n + col, wrow);  // H up columns
+            const int i2 = sq.acquire(lane);
+            const uint32_t b2 = sq.addr(i2);
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch)
-              ptx::st_shared_v4(b0 + swz(lane, ch), apk[4 * ch], apk[4 * ch + 1], apk[4 * ch + 2], apk[4 * ch + 3]);
-            sq.issue(lane, 0, &mC1, col, wrow);           // A = SwiGLU(H)
+              ptx::st_shared_v4(b2 + swz(lane, ch), apk[4 * ch], apk[4 * ch + 1], apk[4 * ch + 2], apk[4 * ch + 3]);
+            sq.issue(lane, i2, &mC1, col, wrow);           // A = SwiGLU(H)
           }
         } else {  // n == 32: accumulator columns are [gate 32 | up 32] = the whole H row
           uint32_t g[32], u[32];
