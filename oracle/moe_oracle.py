@@ -386,6 +386,54 @@ def backward_reference(dO, X, W1, W2, rt: Routing):
 
 
 # --------------------------------------------------------------------------
+# Per-token evaluation for sampled parity at full size (same definitions, one token at a time)
+# --------------------------------------------------------------------------
+def forward_tokens(X, W1, W2, rt: Routing, tokens):
+    """O_t = sum_{e in kept(t)} g_te SwiGLU(X_t W1_e) W2_e for the listed tokens."""
+    out = np.zeros((len(tokens), W2.shape[2]))
+    for i, t in enumerate(tokens):
+        x = _f64(X[t])
+        for e in np.nonzero(rt.kept[t])[0]:
+            a = swiglu(x @ _f64(W1[e]))
+            out[i] += rt.gate[t, e] * (a @ _f64(W2[e]))
+    return out
+
+
+def backward_experts(dO, X, W1, W2, rt: Routing, experts):
+    """dW1_e, dW2_e and the dS of every kept row of each listed expert (Alg. 3 + Alg. 5),
+    converting only those experts' weights to fp64.  Returns {e: (dW1_e, dW2_e, dS_e)}."""
+    out = {}
+    for e in experts:
+        toks = np.nonzero(rt.kept[:, e])[0]
+        s = rt.gate[toks, e][:, None]
+        Xe, dOe = _f64(X[toks]), _f64(dO[toks])
+        W1e, W2e = _f64(W1[e]), _f64(W2[e])
+        dAp = dOe @ W2e.T                                      # dA'_e
+        Ae, dHe = dswiglu(s * dAp, Xe @ W1e)                   # dSwiGLU(dA_e, H_e)
+        out[e] = ((Xe.T @ dHe), ((s * Ae).T @ dOe), np.sum(dAp * Ae, axis=1))
+    return out
+
+
+def backward_tokens(dO, X, W1, W2, rt: Routing, tokens):
+    """dX_t and dS_(t,e) for the listed tokens, Alg. 3 + Alg. 5 row by row.
+
+    Returns (dX [len(tokens), d], {(t, e): dS}).
+    """
+    dX = np.zeros((len(tokens), X.shape[1]))
+    dS = {}
+    for i, t in enumerate(tokens):
+        x, g_o = _f64(X[t]), _f64(dO[t])
+        for e in np.nonzero(rt.kept[t])[0]:
+            s = rt.gate[t, e]
+            h = x @ _f64(W1[e])
+            dap = g_o @ _f64(W2[e]).T                          # dA' row
+            a, dh = dswiglu(s * dap, h)                        # dA = s dA'
+            dS[(t, e)] = float(np.dot(dap, a))                 # <dA', A>
+            dX[i] += dh @ _f64(W1[e]).T                        # dX~ row, summed
+    return dX, dS
+
+
+# --------------------------------------------------------------------------
 # Finite differences (S:349-361): L = sum G * O with routing held fixed
 # --------------------------------------------------------------------------
 def loss_fixed_routing(X, W1, W2, kept, gate, G):

@@ -1,0 +1,93 @@
+"""CPU-side checks of the C ABI: libsonic.so builds, loads without a GPU, exports every
+function include/sonic.h declares, and its host-side logic (sizes, validation) behaves.
+No compute call is made here (there is no GPU in CI)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "sonic.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_14080_b200 import build, sonic
+    build.build()
+    return sonic.lib()
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*[A-Za-z_][\w\s\*]*?\b(sonic_\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("sonic_route", "sonic_moe_fwd", "sonic_moe_bwd", "sonic_rows_max", "sonic_routing_sizes",
+                 "sonic_route_workspace_size", "sonic_fwd_workspace_size", "sonic_bwd_workspace_size",
+                 "sonic_status_string"):
+        assert must in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), f"libsonic.so does not export {name}"
+
+
+def test_host_side_sizes(lib):
+    from paper_2512_14080_b200 import sonic
+    from paper_2512_14080_b200.inputs import CONFIGS
+    for name, c in CONFIGS.items():
+        for mode in (sonic.SONIC_ROUTE_TC, sonic.SONIC_ROUTE_TR_NRF):
+            d = sonic.make_desc(c["T"], c["d"], c["n"], c["E"], c["K"], mode=mode)
+            rows = sonic.sonic_rows_max(d)
+            TK = c["T"] * c["K"]
+            assert rows % 128 == 0 and TK <= rows <= TK + c["E"] * 127 + 127
+            sz = sonic.sonic_routing_sizes(d)
+            assert sz["row_token"] == rows * 4 and sz["topk_ids"] == TK * 4
+            assert sz["token_rowptr"] == (c["T"] + 1) * 4
+            assert sonic.sonic_route_workspace_size(d) > 0
+            # fwd workspace holds A [rows,n] and Y [rows,d] in bf16
+            assert sonic.sonic_fwd_workspace_size(d) >= rows * (c["n"] + c["d"]) * 2
+            assert sonic.sonic_bwd_workspace_size(d) >= rows * (3 * c["n"] + c["d"]) * 2
+
+
+def test_invalid_arguments_are_rejected_before_any_launch(lib):
+    from paper_2512_14080_b200 import sonic
+    bad = [
+        sonic.make_desc(256, 64, 32, 8, 9),        # K > E
+        sonic.make_desc(256, 64, 32, 8, 0),        # K = 0
+        sonic.make_desc(256, 64, 32, 5000, 2),     # E > 4096
+        sonic.make_desc(256, 64, 32, 8, 17),       # K > 16
+        sonic.make_desc(256, 64, 32, 8, 2, m_tile=64),
+        sonic.make_desc(0, 64, 32, 8, 2),
+    ]
+    for d in bad:
+        assert lib.sonic_rows_max(ctypes.byref(d)) == -1
+        st = lib.sonic_route(ctypes.byref(d), None, None, None, 0, None)
+        assert st == -1, sonic.lib().sonic_status_string(st)
+    d = sonic.make_desc(256, 64, 32, 8, 2)
+    # null pointers -> INVALID_ARG, no CUDA call is made
+    assert lib.sonic_moe_fwd(ctypes.byref(d), None, None, None, None, None, None, None, 0, None) == -1
+    assert lib.sonic_moe_bwd(ctypes.byref(d), *([None] * 11), 0, None) == -1
+    # unsupported dims -> UNSUPPORTED (d not a multiple of 64)
+    d2 = sonic.make_desc(256, 96, 32, 8, 2)
+    rt = sonic.sonic_routing(*([1 << 20] * len(sonic.ROUTING_FIELDS)))
+    assert lib.sonic_route(ctypes.byref(d2), ctypes.c_void_p(1 << 20), ctypes.byref(rt), None, 0, None) == -2
+    # short workspace -> WORKSPACE
+    assert lib.sonic_route(ctypes.byref(d), ctypes.c_void_p(1 << 20), ctypes.byref(rt), ctypes.c_void_p(1 << 20), 1,
+                           None) == -3
+    for s in (0, -1, -2, -3, -4, -5):
+        assert lib.sonic_status_string(s)
+
+
+def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
+    from paper_2512_14080_b200 import sonic
+    monkeypatch.setattr(sonic, "LIB_PATH", str(tmp_path / "missing.so"))
+    monkeypatch.setattr(sonic, "_lib", None)
+    with pytest.raises(sonic.SonicError):
+        sonic.lib()

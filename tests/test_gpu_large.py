@@ -1,0 +1,126 @@
+"""GPU parity at BASELINE sizes (sampled), determinism, flags and routing stress cases.
+
+Full-size parity: routing metadata is compared bit-exactly in full; values are compared on
+sampled tokens (O, dX, dS, H) and sampled experts (dW1, dW2, all their rows), computed one by one
+by the oracle, with the same tolerance as the small cases.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import moe_oracle as om
+from paper_2512_14080_b200 import sonic
+from paper_2512_14080_b200.inputs import CONFIGS, make_inputs
+from tests.parity import assert_close, check_routing, f64, full_parity, routing_to_numpy, run_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+def _mode(m):
+    return sonic.SONIC_ROUTE_TC if m == "tc" else sonic.SONIC_ROUTE_TR_NRF
+
+
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+def test_bitwise_deterministic(mode):
+    T, d, n, E, K = 2048, 256, 128, 32, 4
+    inp = make_inputs(T, d, n, E, K, seed=3, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K, mode=_mode(mode))
+    a = run_gpu(desc, inp, want_ws=False)
+    b = run_gpu(desc, inp, want_ws=False)
+    ra, rb = routing_to_numpy(a["rt"], desc), routing_to_numpy(b["rt"], desc)
+    for f in ra:  # valid prefixes only (buffers are sized for rows_max)
+        assert np.array_equal(ra[f], rb[f]), f
+    R_pad = int(a["rt"].pad_offsets[E])
+    for k in ("O", "dX", "dW1", "dW2"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(a["H"][:R_pad], b["H"][:R_pad])
+    assert torch.equal(a["dS"][:R_pad], b["dS"][:R_pad])
+
+
+@pytest.mark.parametrize("flags,mode", [(sonic.SONIC_F_GATE_RAW, "tc"), (sonic.SONIC_F_GATE_RAW, "tr"),
+                                        (sonic.SONIC_F_NO_ORPHAN_RESCUE, "tr")])
+def test_flags(flags, mode):
+    T, d, n, E, K = 1024, 128, 64, 16, 2
+    inp = make_inputs(T, d, n, E, K, seed=4, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K, mode=_mode(mode), flags=flags)
+    full_parity(desc, inp, mode=mode)
+
+
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+@pytest.mark.parametrize("kind", ["skew", "ties"])
+def test_routing_stress(mode, kind):
+    """Skewed loads (empty and overfull experts) and exact score ties."""
+    T, d, n, E, K = 1536, 128, 64, 32, 4
+    kw = dict(skew=3.0) if kind == "skew" else dict(tie_levels=2)
+    inp = make_inputs(T, d, n, E, K, seed=5, device="cuda", **kw)
+    desc = sonic.make_desc(T, d, n, E, K, mode=_mode(mode))
+    full_parity(desc, inp, mode=mode)
+
+
+def test_max_K_equals_E():
+    T, d, n, E, K = 512, 64, 64, 16, 16
+    inp = make_inputs(T, d, n, E, K, seed=6, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K)
+    full_parity(desc, inp, mode="tc")
+
+
+def sampled_parity(cfg_name, mode, n_tokens=192, n_experts=3, seed=0):
+    c = CONFIGS[cfg_name]
+    T, d, n, E, K = c["T"], c["d"], c["n"], c["E"], c["K"]
+    inp = make_inputs(**c, seed=seed, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K, mode=_mode(mode))
+    g = run_gpu(desc, inp, want_ws=False)
+    S = inp.S.cpu().numpy()
+    rto = om.route(S, K, mode=mode, m_tile=128)
+    check_routing(routing_to_numpy(g["rt"], desc), rto)           # full, bit-exact
+    rng = np.random.default_rng(seed + 17)
+    toks = np.sort(rng.choice(T, size=n_tokens, replace=False))
+    exps = rng.choice(E, size=n_experts, replace=False)
+    X, dO = inp.X.float().cpu().numpy(), inp.dO.float().cpu().numpy()
+    W1c, W2c = inp.W1.cpu(), inp.W2.cpu()
+
+    class Lazy:  # per-expert fp64 views of the bf16 weights
+        def __init__(self, w):
+            self.w = w
+            self.shape = tuple(w.shape)
+            self.cache = {}
+
+        def __getitem__(self, e):
+            e = int(e)
+            if e not in self.cache:
+                self.cache[e] = self.w[e].float().numpy().astype(np.float64)
+            return self.cache[e]
+
+    W1, W2 = Lazy(W1c), Lazy(W2c)
+    Oref = om.forward_tokens(X, W1, W2, rto, toks)
+    dXref, dSref = om.backward_tokens(dO, X, W1, W2, rto, toks)
+    stats = {"O": assert_close("O", f64(g["O"][toks]), Oref),
+             "dX": assert_close("dX", f64(g["dX"][toks]), dXref)}
+    # dS and H on the sampled tokens' rows
+    rows, dsr, Hr = [], [], []
+    for t in toks:
+        for e in np.nonzero(rto.kept[t])[0]:
+            r = rto.pad_offsets[e] + int(np.searchsorted(np.nonzero(rto.kept[:, e])[0], t))
+            rows.append(r)
+            dsr.append(dSref[(t, e)])
+            Hr.append(X[t].astype(np.float64) @ W1[e])
+    rows = np.array(rows)
+    stats["dS"] = assert_close("dS", f64(g["dS"])[rows], np.array(dsr))
+    stats["H"] = assert_close("H", f64(g["H"][torch.as_tensor(rows, device="cuda")]), np.array(Hr))
+    ref = om.backward_experts(dO, X, W1, W2, rto, exps)
+    for e, (dW1e, dW2e, _) in ref.items():
+        stats[f"dW1[{e}]"] = assert_close(f"dW1[{e}]", f64(g["dW1"][int(e)]), dW1e)
+        stats[f"dW2[{e}]"] = assert_close(f"dW2[{e}]", f64(g["dW2"][int(e)]), dW2e)
+    return stats
+
+
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+def test_7b_sampled(mode):
+    stats = sampled_parity("7b", mode)
+    print({k: f"{v[0]:.2e}" for k, v in stats.items()})
+
+
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+def test_qwen3_sampled(mode):
+    stats = sampled_parity("qwen3", mode, n_tokens=96, n_experts=2)
+    print({k: f"{v[0]:.2e}" for k, v in stats.items()})

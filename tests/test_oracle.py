@@ -294,3 +294,16 @@ def test_cost_spot_values():
     assert om.arithmetic_intensity(c["T"], c["d"], c["n"], c["E"], c["K"]) == pytest.approx(c["ai"], abs=0.01)
     # iso-FLOP granularity invariance of the minimal activation set
     assert om.activation_bytes(24576, 1536, 512, 4) == om.activation_bytes(24576, 1536, 256, 8)
+
+
+def test_per_token_entry_points_match_full_passes():
+    X, W1, W2, S, dO, rt = rand_case(11, 40, 8, 4, 6, 2)
+    toks = [0, 7, 39]
+    fw = om.forward(X, W1, W2, rt)
+    assert np.allclose(om.forward_tokens(X, W1, W2, rt, toks), fw.O[toks], atol=1e-13)
+    bw = om.backward(dO, X, W1, W2, rt)
+    dXs, dSs = om.backward_tokens(dO, X, W1, W2, rt, toks)
+    assert np.allclose(dXs, bw.dX[toks], atol=1e-13)
+    for (t, e), v in dSs.items():
+        i = list(np.nonzero(rt.kept[:, e])[0]).index(t)
+        assert v == pytest.approx(bw.dS[e][i], abs=1e-13)
