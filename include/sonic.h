@@ -86,9 +86,12 @@ typedef struct {
   int32_t *token_rows;   /* [rows_max] grouped rows of each token, expert-ascending (the scatter map) */
   int32_t *tile_expert;  /* [rows_max/128] expert owning each 128-row tile */
   int32_t *num_tiles;    /* [1]    R_pad / 128 */
+  int32_t *tile_pairs;   /* [rows_max/128 + 1] 2-CTA schedule: first 128-row tile of each pair of
+                            same-expert tiles, bit 31 set when the second tile exists */
+  int32_t *num_pairs;    /* [1]    number of tile pairs */
 } sonic_routing;
 
-#define SONIC_ROUTING_NFIELDS 12
+#define SONIC_ROUTING_NFIELDS 14
 
 /* Upper bound on grouped rows (incl. pad rows): min(T*K + E*127, E*ceil(T/128)*128),
  * rounded up to a multiple of 128.  Returns -1 on an invalid descriptor. */

@@ -13,17 +13,25 @@
 //   producers  NP warps.  Contiguous operands: TMA 2-D/3-D tile loads by one thread.
 //              Gathered operands (NP = 4): 128 threads issue 16-byte cp.async of the token
 //              rows named by the gather map straight into the 128B-swizzled operand layout
-//              -- the paper's "gather fused with the HBM load" (sec. 4.1.1).
-//              (TMA gather4 was measured at ~80 cycles per 512 B per SM on B200, too slow to
-//              feed the tensor cores.)  A producer thread signals a
-//              stage full after cp.async.wait_group + fence.proxy.async (lagged by LAG stages).
-//   MMA        one warp: TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN,
-//              K=16 steps); two TMEM accumulator stages so the epilogue of tile i overlaps
-//              the MMA of tile i+1.
+//              -- the paper's "gather fused with the HBM load" (sec. 4.1.1) -- and
+//              signal with cp.async.mbarrier.arrive.noinc.  (TMA gather4 was measured at ~80
+//              cycles per 512 B per SM on B200, too slow to feed the tensor cores.)
+//   MMA        one warp: TMEM allocator + single-thread tcgen05.mma issuer (K=16 steps); two TMEM
+//              accumulator stages so the epilogue of tile i overlaps the MMA of tile i+1.
 //   epilogue   4 warps: tcgen05.ld -> registers -> fused math -> swizzled smem -> TMA store
 //              (asynchronous TMA store in all GEMMs).
-// Operand smem layout: 128B-swizzled, K-major (rows of 64 K-elements) or MN-major
-// (64-element MN chunks x 64 K-rows); a stage is one A tile (128 x 64) + one B tile (BN x 64).
+//
+// CTA2 = true: a cluster of two CTAs computes a 256 x BN tile with tcgen05.mma.cta_group::2
+// (M = 256).  Each CTA loads its own 128 A rows and HALF of B (BN/2 columns or rows); the leader
+// (rank 0) issues the MMAs and multicasts its commits to both CTAs' barriers, so each CTA's TMEM
+// holds its 128 rows of the accumulator and runs its own epilogue.  Operand traffic per FLOP drops
+// by a third.  varlen-M pairs two 128-row tiles of ONE expert (route's tile_pairs; an expert with an
+// odd tile count ends in a half pair whose second CTA computes but does not store).  For gathered
+// operands the peer CTA's MMA warp relays its local cp.async completion to the leader's barrier --
+// the paper's Blackwell relay warp.
+//
+// Operand smem layout: 128B-swizzled, K-major (rows of 64 K-elements) or MN-major (64-element MN
+// chunks x 64 K-rows); a stage is one A tile (128 x 64) + one B tile (BN or BN/2 x 64).
 #pragma once
 #include "ptx.cuh"
 
@@ -33,6 +41,8 @@ enum GemmKind { K_UP = 0, K_DOWN = 1, K_DH = 2, K_DXT = 3, K_DW2 = 4, K_DW1 = 5 
 
 struct GemmArgs {
   const int* num_m_tiles;   // varlen-M: device-resident count of 128-row tiles (R_pad / 128)
+  const int* num_pairs;     // varlen-M, CTA2: device-resident count of tile pairs
+  const int* tile_pairs;    // varlen-M, CTA2: first tile of each pair | (second exists) << 31
   const int* tile_expert;   // varlen-M: expert of each 128-row tile
   const int* row_token;     // gather map, -1 on pad rows
   const float* row_gate;    // gate per grouped row, 0 on pad rows
@@ -41,11 +51,10 @@ struct GemmArgs {
   int gld;
   int E;
   int n_tiles;              // output tiles along N
-  int m_tiles;              // varlen-K: output tiles along M per expert
+  int m_tiles;              // varlen-K: output tiles (128 rows) along M per expert
   int k_blocks;             // varlen-M: ceil(K / 64)
   int n;                    // expert intermediate dim (offset of the "up" half of H)
   int M_dim, N_dim;         // output extent along M (varlen-K) and N
-  const __nv_bfloat16* H;   // DH: cached H [rows, 2n]
   float* dS;                // DH: dS [rows] if n_tiles == 1, else partials [n_tiles][rows_max]
   long long rows_max;
 };
@@ -68,21 +77,16 @@ __host__ __device__ constexpr int gemm_threads() {
   return 32 * (num_producer_warps<KIND>() + 5);
 }
 
-// Gather producers signal a stage with cp.async.mbarrier.arrive.noinc (hardware-tracked, the
-// producer never blocks) instead of wait_group + arrive.
-#ifndef SONIC_GATHER_NOINC
-#define SONIC_GATHER_NOINC 1
-#endif
-constexpr bool GATHER_NOINC = SONIC_GATHER_NOINC != 0;
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
 constexpr int STG_BYTES = 4096;  // one epilogue staging buffer: 32 rows x 128 B
 constexpr int SMEM_LIMIT = 232448;
 
-template <int BN, bool HTMA = false, int NB_ = 2>
+template <int BN, bool CTA2, bool HTMA, int NB_>
 struct GemmCfg {
+  static constexpr int BNL = CTA2 ? BN / 2 : BN;  // B columns (or rows) held by this CTA
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
-  static constexpr uint32_t B_BYTES = BN * GEMM_BK * 2;
+  static constexpr uint32_t B_BYTES = BNL * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NB = NB_;  // epilogue staging buffers per epilogue warp (ring)
   // DH only: per-epilogue-warp H buffer, 32 rows x (BN gate + BN up) bf16 columns (TMA-loaded)
@@ -93,49 +97,53 @@ struct GemmCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                         : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int LAG = STAGES - 2 > 0 ? STAGES - 2 : 1;  // cp.async stages in flight per producer
 };
 
 // DH with BN in {64, 128} reads H through TMA into per-warp smem buffers ("asynchronous
-// TMA load of H in the dH epilogue"); wider tiles would not leave room for the buffer.
-// Staging ring depth: a deeper ring lets each TMA store finish reading smem while later
-// ones are written (the epilogue was the measured limiter); at BN = 256 the
-// price is one mainloop stage (3 instead of 4).
-#ifndef SONIC_NB_WIDE
-#define SONIC_NB_WIDE 2
-#endif
-#ifndef SONIC_NB_NARROW
-#define SONIC_NB_NARROW 2
-#endif
-template <int KIND, int BN>
-__host__ __device__ constexpr int staging_nb() {
-  return KIND == K_DH ? 2 : (BN == 256 ? SONIC_NB_WIDE : SONIC_NB_NARROW);
-}
-template <int KIND, int BN>
-using KCfg = GemmCfg<BN, KIND == K_DH && (BN == 64 || BN == 128), staging_nb<KIND, BN>()>;
+// TMA load of H in the dH epilogue").  Staging ring depth NB: 2 (a deeper ring costs a mainloop
+// stage, measured slower).
+template <int KIND, int BN, bool CTA2>
+using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128, 2>;
 
 struct TileCoord {
   int e, row0, nt, mt, nkb, seg0;
+  bool valid;  // CTA2: this CTA's half of the pair tile exists
 };
 
-template <int KIND, int BN>
-__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile) {
+template <int KIND, bool CTA2>
+__device__ __forceinline__ int total_tiles_of(const GemmArgs& a) {
+  if constexpr (Traits<KIND>::vk) return a.E * (CTA2 ? (a.m_tiles + 1) / 2 : a.m_tiles) * a.n_tiles;
+  else return (CTA2 ? *a.num_pairs : *a.num_m_tiles) * a.n_tiles;
+}
+
+template <int KIND, bool CTA2>
+__device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, int rank) {
   TileCoord c;
+  c.valid = true;
   if constexpr (Traits<KIND>::vk) {
-    int per_e = a.m_tiles * a.n_tiles;
+    const int mts = CTA2 ? (a.m_tiles + 1) / 2 : a.m_tiles;
+    const int per_e = mts * a.n_tiles;
     c.e = tile / per_e;
-    int rem = tile - c.e * per_e;
-    c.mt = rem / a.n_tiles;
-    c.nt = rem - c.mt * a.n_tiles;
+    const int rem = tile - c.e * per_e;
+    const int mp = rem / a.n_tiles;
+    c.nt = rem - mp * a.n_tiles;
+    c.mt = CTA2 ? 2 * mp + rank : mp;
+    if (CTA2) c.valid = c.mt < a.m_tiles;
     c.seg0 = __ldg(a.pad_offsets + c.e);
     c.nkb = (__ldg(a.pad_offsets + c.e + 1) - c.seg0) / GEMM_BK;
     c.row0 = 0;
   } else {
-    int m = tile / a.n_tiles;
-    c.nt = tile - m * a.n_tiles;
-    c.mt = m;
-    c.row0 = m * GEMM_BM;
-    c.e = __ldg(a.tile_expert + m);
+    const int p = tile / a.n_tiles;
+    c.nt = tile - p * a.n_tiles;
+    int first = p;
+    if constexpr (CTA2) {
+      const int pt = __ldg(a.tile_pairs + p);
+      first = pt & 0x7fffffff;
+      c.valid = rank == 0 || pt < 0;
+    }
+    c.mt = first + (CTA2 ? rank : 0);
+    c.row0 = c.mt * GEMM_BM;
+    c.e = __ldg(a.tile_expert + first);
     c.nkb = a.k_blocks;
     c.seg0 = 0;
   }
@@ -195,15 +203,6 @@ struct StoreQ {
   }
 };
 
-// 32 gate + 32 up columns of one H row (starting at column col of the gate half)
-__device__ __forceinline__ void dh_prefetch(uint4 (&g)[4], uint4 (&u)[4], const __nv_bfloat16* hrow, int n, int col) {
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    g[i] = ptx::ld_nc_v4(hrow + col + 8 * i);
-    u[i] = ptx::ld_nc_v4(hrow + n + col + 8 * i);
-  }
-}
-
 __device__ __forceinline__ void write_row_bf16(uint32_t buf, int lane, const float* v /*64*/) {
 #pragma unroll
   for (int c = 0; c < 8; ++c)
@@ -212,21 +211,35 @@ __device__ __forceinline__ void write_row_bf16(uint32_t buf, int lane, const flo
                       ptx::pack_bf16(v[8 * c + 6], v[8 * c + 7]));
 }
 
-template <int KIND, int BN>
+// TMA tile loads: 1-CTA form (own barrier) or pair form (counted on the leader's barrier).
+template <bool CTA2>
+__device__ __forceinline__ void tload2(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  if constexpr (CTA2) ptx::tma_load_2d_cg2(dst, m, bar, c0, c1);
+  else ptx::tma_load_2d(dst, m, bar, c0, c1);
+}
+template <bool CTA2>
+__device__ __forceinline__ void tload3(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  if constexpr (CTA2) ptx::tma_load_3d_cg2(dst, m, bar, c0, c1, c2);
+  else ptx::tma_load_3d(dst, m, bar, c0, c1, c2);
+}
+
+template <int KIND, int BN, bool CTA2>
 __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     sonic_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                       const __grid_constant__ CUtensorMap mC0, const __grid_constant__ CUtensorMap mC1,
                       const __grid_constant__ CUtensorMap mD, const GemmArgs args) {
   using Tr = Traits<KIND>;
-  using Cfg = KCfg<KIND, BN>;
+  using Cfg = KCfg<KIND, BN, CTA2>;
   constexpr bool HTMA = Cfg::HBUF_WARP > 0;
   constexpr int NP = num_producer_warps<KIND>();
   constexpr bool GATHER = NP > 1;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int BNL = Cfg::BNL;
   constexpr uint32_t A_BYTES = Cfg::A_BYTES;
   constexpr uint32_t STAGE_BYTES = Cfg::STAGE_BYTES;
-  // bytes landing through TMA per stage (the non-gathered operands)
+  // bytes landing through TMA per stage per CTA (the non-gathered operands)
   constexpr uint32_t TMA_BYTES = !GATHER ? STAGE_BYTES : (Tr::a_gather ? Cfg::B_BYTES : A_BYTES);
+  constexpr int MMA_M = CTA2 ? 2 * GEMM_BM : GEMM_BM;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -241,15 +254,22 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const int rank = CTA2 ? (int)ptx::cluster_ctarank() : 0;
+  const bool leader = rank == 0;
+  const int t_first = CTA2 ? blockIdx.x / 2 : blockIdx.x;
+  const int t_step = CTA2 ? gridDim.x / 2 : gridDim.x;
 
   if (threadIdx.x == 0) {
+    // full: leader counts its TMA expect_tx arrive (+ its 128 cp.async arrivals + the peer's relay
+    // for gathered kinds); a peer counts only its own cp.async arrivals.
+    const int full_cnt = GATHER ? (leader ? NP * 32 + 1 + (CTA2 ? 1 : 0) : NP * 32) : 1;
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], GATHER ? NP * 32 + 1 : 1);
+      ptx::mbar_init(&full[s], full_cnt);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], 4);
+      ptx::mbar_init(&tempty[s], CTA2 ? 8 : 4);
     }
     for (int s = 0; s < 4; ++s) ptx::mbar_init(&hfull[s], 1);
     ptx::fence_barrier_init();
@@ -257,15 +277,21 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     ptx::prefetch_tmap(&mB);
   }
   if (warp == NP) {
-    ptx::tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
-    ptx::tmem_relinquish();
+    if constexpr (CTA2) {
+      ptx::tmem_alloc2(tmem_holder, Cfg::TMEM_COLS);
+      ptx::tmem_relinquish2();
+    } else {
+      ptx::tmem_alloc(tmem_holder, Cfg::TMEM_COLS);
+      ptx::tmem_relinquish();
+    }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CTA2) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int total_tiles = Tr::vk ? args.E * args.m_tiles * args.n_tiles : (*args.num_m_tiles) * args.n_tiles;
+  const int total_tiles = total_tiles_of<KIND, CTA2>(args);
 
   if (warp < NP) {
     // ============================================================ producers
@@ -273,21 +299,21 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     uint32_t phase = 0;
     if constexpr (!GATHER) {
       if (lane == 0) {
-        for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-          const TileCoord tc = decode_tile<KIND, BN>(args, tile);
+        for (int tile = t_first; tile < total_tiles; tile += t_step) {
+          const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
+          const int n0 = tc.nt * BN + rank * BNL;  // this CTA's B columns (rows)
           for (int kb = 0; kb < tc.nkb; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sA = smem + stage * STAGE_BYTES;
             uint8_t* sB = sA + A_BYTES;
             uint64_t* bar = &full[stage];
-            ptx::mbar_arrive_expect_tx(bar, STAGE_BYTES);
-            ptx::tma_load_2d(sA, &mA, bar, kb * GEMM_BK, tc.row0);
+            if (leader) ptx::mbar_arrive_expect_tx(bar, STAGE_BYTES * (CTA2 ? 2 : 1));
+            tload2<CTA2>(sA, &mA, bar, kb * GEMM_BK, tc.row0);
             if constexpr (KIND == K_DOWN) {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j)
-                ptx::tma_load_3d(sB + j * 8192, &mB, bar, tc.nt * BN + 64 * j, kb * GEMM_BK, tc.e);
-            } else {  // DXT: K-major weights, one box of BN rows
-              ptx::tma_load_3d(sB, &mB, bar, kb * GEMM_BK, tc.nt * BN, tc.e);
+              for (int j = 0; j < BNL / 64; ++j) tload3<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, kb * GEMM_BK, tc.e);
+            } else {  // DXT: K-major weights, one box of BNL rows
+              tload3<CTA2>(sB, &mB, bar, kb * GEMM_BK, n0, tc.e);
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -301,37 +327,39 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       const int c = pt & 7;        // 16-byte chunk within a 128-byte row
       const int r0 = pt >> 3;      // rows r0 + 16 j
       const uint32_t sw = (uint32_t)((c ^ (r0 & 7)) << 4);
-      int pend = 0, pstage = 0;
       // Gather indices are prefetched one tile (varlen-M) / one stage (varlen-K) ahead so the
       // dependent cp.async addresses never wait on a global load.
       int ntok[8];
       if constexpr (!Tr::vk) {
-        if (blockIdx.x < total_tiles) {
-          const TileCoord t0 = decode_tile<KIND, BN>(args, blockIdx.x);
+        if (t_first < total_tiles) {
+          const TileCoord t0 = decode_tile<KIND, CTA2>(args, t_first, rank);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) ntok[j] = tok_of(args.row_token, t0.row0 + r0 + 16 * j);
+          for (int j = 0; j < 8; ++j) ntok[j] = t0.valid ? tok_of(args.row_token, t0.row0 + r0 + 16 * j) : 0;
         }
       }
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const TileCoord tc = decode_tile<KIND, BN>(args, tile);
+      for (int tile = t_first; tile < total_tiles; tile += t_step) {
+        const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
+        const int n0 = tc.nt * BN + rank * BNL;
         const __nv_bfloat16* srcM[8];
         int ktok[4];
         if constexpr (!Tr::vk) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) srcM[j] = args.gsrc + (size_t)ntok[j] * args.gld + c * 8;
-          if (tile + (int)gridDim.x < total_tiles) {
-            const TileCoord tn = decode_tile<KIND, BN>(args, tile + gridDim.x);
+          if (tile + t_step < total_tiles) {
+            const TileCoord tn = decode_tile<KIND, CTA2>(args, tile + t_step, rank);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ntok[j] = tok_of(args.row_token, tn.row0 + r0 + 16 * j);
+            for (int j = 0; j < 8; ++j) ntok[j] = tn.valid ? tok_of(args.row_token, tn.row0 + r0 + 16 * j) : 0;
           }
         } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j) ktok[j] = tok_of(args.row_token, tc.seg0 + r0 + 16 * j);
         }
+        // varlen-K A gather of a missing half: read column 0 (finite, never stored)
+        const int acol0 = (Tr::a_gather && tc.valid) ? tc.mt * GEMM_BM : 0;
         for (int kb = 0; kb < tc.nkb; ++kb) {
           const __nv_bfloat16* srcK[4];
           if constexpr (Tr::vk) {
-            const int col0 = Tr::a_gather ? tc.mt * GEMM_BM : tc.nt * BN;
+            const int col0 = Tr::a_gather ? acol0 : n0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) srcK[j] = args.gsrc + (size_t)ktok[j] * args.gld + col0 + c * 8;
             if (kb + 1 < tc.nkb) {
@@ -345,86 +373,77 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           uint8_t* sB = sA + A_BYTES;
           uint64_t* bar = &full[stage];
           if (pt == 0) {
-            ptx::mbar_arrive_expect_tx(bar, TMA_BYTES);
+            if (leader) ptx::mbar_arrive_expect_tx(bar, TMA_BYTES * (CTA2 ? 2 : 1));
             if constexpr (KIND == K_UP) {
               constexpr int W = BN / 2;  // gate columns per tile; the up columns follow at +n
               if constexpr (W >= 64) {
                 const int j0 = tc.nt * W;
+                if constexpr (CTA2) {  // rank 0 holds the gate half of B, rank 1 the up half
+                  const int cb = (rank ? args.n : 0) + j0;
 #pragma unroll
-                for (int j = 0; j < W / 64; ++j) {
-                  ptx::tma_load_3d(sB + j * 8192, &mB, bar, j0 + 64 * j, kb * GEMM_BK, tc.e);
-                  ptx::tma_load_3d(sB + (W / 64 + j) * 8192, &mB, bar, args.n + j0 + 64 * j, kb * GEMM_BK, tc.e);
+                  for (int j = 0; j < W / 64; ++j) tload3<true>(sB + j * 8192, &mB, bar, cb + 64 * j, kb * GEMM_BK, tc.e);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < W / 64; ++j) {
+                    tload3<false>(sB + j * 8192, &mB, bar, j0 + 64 * j, kb * GEMM_BK, tc.e);
+                    tload3<false>(sB + (W / 64 + j) * 8192, &mB, bar, args.n + j0 + 64 * j, kb * GEMM_BK, tc.e);
+                  }
                 }
-              } else {  // n == 32: one 64-column box holds [gate | up]
-                ptx::tma_load_3d(sB, &mB, bar, 0, kb * GEMM_BK, tc.e);
+              } else {  // n == 32 (1-CTA only): one 64-column box holds [gate | up]
+                tload3<CTA2>(sB, &mB, bar, 0, kb * GEMM_BK, tc.e);
               }
             } else if constexpr (KIND == K_DH) {
-              ptx::tma_load_3d(sB, &mB, bar, kb * GEMM_BK, tc.nt * BN, tc.e);
+              tload3<CTA2>(sB, &mB, bar, kb * GEMM_BK, n0, tc.e);
             } else if constexpr (KIND == K_DW2) {  // A' tile (MN-major): 64 rows x 128 M columns
               const int krow0 = tc.seg0 + kb * GEMM_BK;
-              ptx::tma_load_2d(sA, &mA, bar, tc.mt * GEMM_BM, krow0);
-              ptx::tma_load_2d(sA + 8192, &mA, bar, tc.mt * GEMM_BM + 64, krow0);
-            } else {  // DW1: dH tile (MN-major): 64 rows x BN columns
+              const int m0 = tc.valid ? tc.mt * GEMM_BM : 0;
+              tload2<CTA2>(sA, &mA, bar, m0, krow0);
+              tload2<CTA2>(sA + 8192, &mA, bar, m0 + 64, krow0);
+            } else {  // DW1: dH tile (MN-major): 64 rows x BNL columns
               const int krow0 = tc.seg0 + kb * GEMM_BK;
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sB + j * 8192, &mB, bar, tc.nt * BN + 64 * j, krow0);
+              for (int j = 0; j < BNL / 64; ++j) tload2<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, krow0);
             }
           }
           if constexpr (!Tr::vk) {  // A: 128 gathered rows x 64 K (K-major)
             const uint32_t dst = ptx::smem_u32(sA) + r0 * 128 + sw;
 #pragma unroll
             for (int j = 0; j < 8; ++j) ptx::cp_async16(dst + j * 16 * 128, srcM[j] + kb * GEMM_BK);
-          } else {  // 64 gathered K-rows x (128 | BN) MN-columns (MN-major)
-            constexpr int NCH = Tr::a_gather ? 2 : BN / 64;
+          } else {  // 64 gathered K-rows x (128 | BNL) MN-columns (MN-major)
+            constexpr int NCH = Tr::a_gather ? 2 : BNL / 64;
             const uint32_t dst = ptx::smem_u32(Tr::a_gather ? sA : sB) + r0 * 128 + sw;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
 #pragma unroll
               for (int jj = 0; jj < NCH; ++jj) ptx::cp_async16(dst + jj * 8192 + j * 16 * 128, srcK[j] + 64 * jj);
           }
-          if constexpr (GATHER_NOINC) {
-            ptx::cp_async_mbar_arrive(bar);  // arrives when this thread's copies land
-          } else {
-            ptx::cp_async_commit();
-            if (++pend > Cfg::LAG) {
-              ptx::cp_async_wait<Cfg::LAG>();
-              ptx::fence_proxy_async_smem();
-              ptx::mbar_arrive(&full[pstage]);
-              if (++pstage == STAGES) pstage = 0;
-              --pend;
-            }
-          }
+          ptx::cp_async_mbar_arrive(bar);  // arrives on this CTA's barrier when the copies land
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
       }
-      ptx::cp_async_wait<0>();
-      ptx::fence_proxy_async_smem();
-      while (pend > 0) {
-        ptx::mbar_arrive(&full[pstage]);
-        if (++pstage == STAGES) pstage = 0;
-        --pend;
-      }
     }
   } else if (warp == NP) {
-    // ============================================================ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc = ptx::make_idesc(GEMM_BM, BN, Tr::a_mn ? 1 : 0, Tr::b_mn ? 1 : 0);
+    // ============================================================ MMA issuer (leader) / relay (peer)
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = ptx::make_idesc(MMA_M, BN, Tr::a_mn ? 1 : 0, Tr::b_mn ? 1 : 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-        const TileCoord tc = decode_tile<KIND, BN>(args, tile);
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+      for (int tile = t_first; tile < total_tiles; tile += t_step) {
+        const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, 0);
+        if constexpr (CTA2) ptx::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+        else ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < tc.nkb; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
+          if constexpr (CTA2) ptx::mbar_wait_cluster(&full[stage], phase);
+          else ptx::mbar_wait(&full[stage], phase);
           // cp.async (generic proxy) data consumed by tcgen05.mma (async proxy)
-          if constexpr (GATHER && GATHER_NOINC) ptx::fence_proxy_async_smem();
+          if constexpr (GATHER) ptx::fence_proxy_async_smem();
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t b_base = a_base + A_BYTES;
@@ -434,17 +453,36 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
                                          : ptx::make_sdesc(a_base + k * 32, 16, 1024);
             const uint64_t bd = Tr::b_mn ? ptx::make_sdesc(b_base + k * 2048, 8192, 1024)
                                          : ptx::make_sdesc(b_base + k * 32, 16, 1024);
-            ptx::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (CTA2) ptx::mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            else ptx::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          ptx::mma_commit(&empty[stage]);
+          if constexpr (CTA2) ptx::mma_commit_mc(&empty[stage], 0x3);
+          else ptx::mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(&tfull[acc]);
+        if constexpr (CTA2) ptx::mma_commit_mc(&tfull[acc], 0x3);
+        else ptx::mma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
+      }
+    } else if (lane == 0 && CTA2 && GATHER) {
+      // relay: forward this CTA's cp.async completion (local barrier) to the leader's barrier
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = t_first; tile < total_tiles; tile += t_step) {
+        const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
+        for (int kb = 0; kb < tc.nkb; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::fence_proxy_async_smem();
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[stage]), 0));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
       }
     }
     __syncwarp();
@@ -455,71 +493,56 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     StoreQ<Cfg::NB> sq{stg + ew * Cfg::NB * STG_BYTES, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    // DH (HTMA): each epilogue warp TMA-loads its own 32 rows of H (BN gate + BN up columns)
-    // for its next tile into a private buffer; dH is then computed in place in that buffer
-    // and TMA-stored from it.
+    const uint32_t tempty_leader = CTA2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
+    // DH: each epilogue warp TMA-loads its own 32 rows of H (BN gate + BN up columns) for its
+    // next tile into a private buffer; dH is computed in place there and TMA-stored from it.
     uint8_t* hb = hbuf + ew * Cfg::HBUF_WARP;
     uint32_t hphase = 0;
     auto h_issue = [&](int t) {
       if constexpr (HTMA) {
         if (lane == 0) {
-          const TileCoord th = decode_tile<KIND, BN>(args, t);
+          const TileCoord th = decode_tile<KIND, CTA2>(args, t, rank);
           ptx::mbar_arrive_expect_tx(&hfull[ew], Cfg::HBUF_WARP);
+          if constexpr (BN >= 64) {
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) {
-            ptx::tma_load_2d(hb + j * STG_BYTES, &mD, &hfull[ew], th.nt * BN + 64 * j, th.row0 + 32 * q);
-            ptx::tma_load_2d(hb + (BN / 64 + j) * STG_BYTES, &mD, &hfull[ew], args.n + th.nt * BN + 64 * j,
-                             th.row0 + 32 * q);
+            for (int j = 0; j < BN / 64; ++j) {
+              ptx::tma_load_2d(hb + j * STG_BYTES, &mD, &hfull[ew], th.nt * BN + 64 * j, th.row0 + 32 * q);
+              ptx::tma_load_2d(hb + (BN / 64 + j) * STG_BYTES, &mD, &hfull[ew], args.n + th.nt * BN + 64 * j,
+                               th.row0 + 32 * q);
+            }
+          } else {  // n == 32: one box [gate | up]
+            ptx::tma_load_2d(hb, &mD, &hfull[ew], 0, th.row0 + 32 * q);
           }
         }
       }
     };
     if constexpr (HTMA) {
-      if (blockIdx.x < total_tiles) h_issue(blockIdx.x);
+      if (t_first < total_tiles) h_issue(t_first);
     }
-    // DH (BN = 256): H is read with plain loads, prefetched 32 columns ahead (across tiles too)
-    uint4 hpre_g[4], hpre_u[4];
-    if constexpr (KIND == K_DH && BN >= 64 && !HTMA) {
-      if (blockIdx.x < total_tiles) {
-        const TileCoord t0 = decode_tile<KIND, BN>(args, blockIdx.x);
-        const __nv_bfloat16* h0 = args.H + (long long)(t0.row0 + 32 * q + lane) * (2 * args.n);
-        dh_prefetch(hpre_g, hpre_u, h0, args.n, t0.nt * BN);
-      }
-    }
-    for (int tile = blockIdx.x; tile < total_tiles; tile += gridDim.x) {
-      const TileCoord tc = decode_tile<KIND, BN>(args, tile);
+    for (int tile = t_first; tile < total_tiles; tile += t_step) {
+      const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
       const int wrow = tc.row0 + 32 * q;  // first grouped row of this warp's slab
       const int row = wrow + lane;        // this thread's grouped row (varlen-M)
-      const bool has_next = tile + (int)gridDim.x < total_tiles;
-      const __nv_bfloat16* next_hrow = nullptr;
-      int next_col = 0;
-      if constexpr (KIND == K_DH) {
-        if (has_next) {
-          const TileCoord tn = decode_tile<KIND, BN>(args, tile + gridDim.x);
-          next_hrow = args.H + (long long)(tn.row0 + 32 * q + lane) * (2 * args.n);
-          next_col = tn.nt * BN;
-        }
-      }
-      ptx::mbar_wait(&tfull[acc], acc_phase);
+      const bool has_next = tile + t_step < total_tiles;
+      if constexpr (CTA2) ptx::mbar_wait_cluster(&tfull[acc], acc_phase);
+      else ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
 
-#ifdef SONIC_EXPERIMENT_NO_EPI
-      if constexpr (true) {  // ablation: mainloop only
-        if (has_next) h_issue(tile + gridDim.x);
+      if (!tc.valid) {
+        // missing half of a pair: nothing to store (keep the H-buffer protocol going)
         if constexpr (HTMA) {
           ptx::mbar_wait(&hfull[ew], hphase);
           hphase ^= 1;
+          if (has_next) h_issue(tile + t_step);
         }
-      } else
-#endif
-      if constexpr (KIND == K_UP) {
+      } else if constexpr (KIND == K_UP) {
         constexpr int W = BN / 2;
         if constexpr (W >= 64) {
 #pragma unroll 1
           for (int c = 0; c < W; c += 64) {
             const int col = tc.nt * W + c;
-            sq.acquire<1>(lane);  // the next two ring slots are both free
+            sq.template acquire<1>(lane);  // the next two ring slots are both free
             const int i0 = sq.sb;
             const int i1 = (i0 + 1) % Cfg::NB;
             const uint32_t b0 = sq.addr(i0), b1 = sq.addr(i1);
@@ -611,15 +634,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       } else if constexpr (KIND == K_DH) {
         const float s = __ldg(args.row_gate + row);
         const int n = args.n;
-        const __nv_bfloat16* hrow = args.H + (long long)row * (2 * n);
         float ds = 0.f;
-#ifdef SONIC_EXPERIMENT_DH_EPI
-        constexpr int EXP = SONIC_EXPERIMENT_DH_EPI;  // 1: skip everything, 2: no H loads, 3: no stores
-#else
-        constexpr int EXP = 0;
-#endif
-        if constexpr (EXP == 1) {
-        } else if constexpr (HTMA) {
+        if constexpr (BN >= 64) {
           ptx::mbar_wait(&hfull[ew], hphase);
           hphase ^= 1;
 #pragma unroll 1
@@ -628,7 +644,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             const uint32_t gb = ptx::smem_u32(hb + c * STG_BYTES);              // H gate -> dH gate
             const uint32_t ub = ptx::smem_u32(hb + (BN / 64 + c) * STG_BYTES);  // H up   -> dH up
             const uint32_t ab = sq.addr(c & 1);                                  // A' staging
-            sq.wait_reads<3>(lane);  // the A' store issued from this buffer 2 chunks ago has read it
+            sq.template wait_reads<3>(lane);  // the A' store issued from this buffer 2 chunks ago has read it
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               uint32_t r[32];
@@ -684,112 +700,67 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             }
           }
           if (has_next) {
-            sq.wait_reads<1>(lane);  // every dH store out of the H buffer has read it
-            h_issue(tile + gridDim.x);
+            sq.template wait_reads<1>(lane);  // every dH store out of the H buffer has read it
+            h_issue(tile + t_step);
           }
-        } else if constexpr (BN >= 64) {
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 64) {
-            const int col = tc.nt * BN + c;
-            sq.wait_reads<0>(lane);
-            const uint32_t b0 = sq.addr(0), b1 = sq.addr(1);
-            uint32_t apk[32];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              // H for this half was prefetched one half ahead (or before the tfull wait)
-              uint4 hg4[4], hu4[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                hg4[i] = hpre_g[i];
-                hu4[i] = hpre_u[i];
-              }
-              if constexpr (EXP != 2) {
-                if (c + 32 * h + 32 < BN) {
-                  dh_prefetch(hpre_g, hpre_u, hrow, n, col + 32 * h + 32);
-                } else if (has_next) {
-                  dh_prefetch(hpre_g, hpre_u, next_hrow, n, next_col);
-                }
-              }
-              uint32_t r[32];
-              ptx::tmem_ld32(t_acc + c + 32 * h, r);
-              ptx::tmem_ld_wait();
-              const __nv_bfloat16* hgp = reinterpret_cast<const __nv_bfloat16*>(hg4);
-              const __nv_bfloat16* hup = reinterpret_cast<const __nv_bfloat16*>(hu4);
-#pragma unroll
-              for (int q8 = 0; q8 < 4; ++q8) {
-                uint32_t pg[4], pu[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  float dg2[2], du2[2], ap2[2];
-#pragma unroll
-                  for (int k = 0; k < 2; ++k) {
-                    const int j = 8 * q8 + 2 * i + k;
-                    const float dap = __uint_as_float(r[j]);
-                    const float gg = __bfloat162float(hgp[j]);
-                    const float uu = __bfloat162float(hup[j]);
-                    const float sg = sigmoidf_fast(gg);
-                    const float sl = gg * sg;
-                    const float A = sl * uu;
-                    const float dA = s * dap;
-                    dg2[k] = dA * uu * sg * (1.f + gg * (1.f - sg));
-                    du2[k] = dA * sl;
-                    ap2[k] = s * A;
-                    ds = fmaf(dap, A, ds);
-                  }
-                  pg[i] = ptx::pack_bf16(dg2[0], dg2[1]);
-                  pu[i] = ptx::pack_bf16(du2[0], du2[1]);
-                  apk[16 * h + 4 * q8 + i] = ptx::pack_bf16(ap2[0], ap2[1]);
-                }
-                if constexpr (EXP != 3) {
-                  ptx::st_shared_v4(b0 + swz(lane, 4 * h + q8), pg[0], pg[1], pg[2], pg[3]);
-                  ptx::st_shared_v4(b1 + swz(lane, 4 * h + q8), pu[0], pu[1], pu[2], pu[3]);
-                } else {
-                  ds += __uint_as_float(pg[0] ^ pu[1]) * 1e-30f;
-                }
-              }
-            }
-            if constexpr (EXP != 3) {
-              sq.issue(lane, 0, &mC0, col, wrow);      // dH gate columns
-              sq.issue(lane, 1, &mC0, n + col, wrow);  // dH up columns
-              sq.wait_reads<1>(lane);
-#pragma unroll
-              for (int ch = 0; ch < 8; ++ch)
-                ptx::st_shared_v4(b0 + swz(lane, ch), apk[4 * ch], apk[4 * ch + 1], apk[4 * ch + 2], apk[4 * ch + 3]);
-              sq.issue(lane, 0, &mC1, col, wrow);      // A' = s A
-            } else {
-              ds += __uint_as_float(apk[0] ^ apk[31]) * 1e-30f;
-            }
-          }
-        } else {  // n == 32, BN == 32: H row = [gate 32 | up 32]
-          uint4 h4[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) h4[i] = ptx::ld_nc_v4(hrow + 8 * i);
+        } else {  // n == 32, BN == 32: one 64-column H box holds the whole row [gate 32 | up 32]
+          ptx::mbar_wait(&hfull[ew], hphase);
+          hphase ^= 1;
+          const uint32_t hbs = ptx::smem_u32(hb);
           uint32_t r[32];
           ptx::tmem_ld32(t_acc, r);
-          ptx::tmem_ld_wait();
-          const __nv_bfloat16* hp = reinterpret_cast<const __nv_bfloat16*>(h4);
-          float dh[64], ap[64];
+          uint4 hg4[4], hu4[4];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float dap = __uint_as_float(r[j]);
-            const float gg = __bfloat162float(hp[j]);
-            const float uu = __bfloat162float(hp[32 + j]);
-            const float sg = sigmoidf_fast(gg);
-            const float sl = gg * sg;
-            const float A = sl * uu;
-            const float dA = s * dap;
-            dh[j] = dA * uu * sg * (1.f + gg * (1.f - sg));
-            dh[32 + j] = dA * sl;
-            ap[j] = s * A;
-            ap[32 + j] = 0.f;
-            ds = fmaf(dap, A, ds);
+          for (int i = 0; i < 4; ++i) {
+            hg4[i] = ptx::ld_shared_v4(hbs + swz(lane, i));
+            hu4[i] = ptx::ld_shared_v4(hbs + swz(lane, 4 + i));
           }
-          int i = sq.acquire(lane);
-          write_row_bf16(sq.addr(i), lane, dh);
-          sq.issue(lane, i, &mC0, 0, wrow);
-          i = sq.acquire(lane);
-          write_row_bf16(sq.addr(i), lane, ap);
-          sq.issue(lane, i, &mC1, 0, wrow);
+          ptx::tmem_ld_wait();
+          const __nv_bfloat16* hgp = reinterpret_cast<const __nv_bfloat16*>(hg4);
+          const __nv_bfloat16* hup = reinterpret_cast<const __nv_bfloat16*>(hu4);
+          const int ia = sq.acquire(lane);
+          const uint32_t ab = sq.addr(ia);
+#pragma unroll
+          for (int q8 = 0; q8 < 4; ++q8) {
+            uint32_t pg[4], pu[4], pa[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              float dg2[2], du2[2], ap2[2];
+#pragma unroll
+              for (int k = 0; k < 2; ++k) {
+                const int j = 8 * q8 + 2 * i + k;
+                const float dap = __uint_as_float(r[j]);
+                const float gg = __bfloat162float(hgp[j]);
+                const float uu = __bfloat162float(hup[j]);
+                const float sg = sigmoidf_fast(gg);
+                const float sl = gg * sg;
+                const float A = sl * uu;
+                const float dA = s * dap;
+                dg2[k] = dA * uu * sg * fmaf(gg, 1.f - sg, 1.f);
+                du2[k] = dA * sl;
+                ap2[k] = s * A;
+                ds = fmaf(dap, A, ds);
+              }
+              pg[i] = ptx::pack_bf16(dg2[0], dg2[1]);
+              pu[i] = ptx::pack_bf16(du2[0], du2[1]);
+              pa[i] = ptx::pack_bf16(ap2[0], ap2[1]);
+            }
+            ptx::st_shared_v4(hbs + swz(lane, q8), pg[0], pg[1], pg[2], pg[3]);
+            ptx::st_shared_v4(hbs + swz(lane, 4 + q8), pu[0], pu[1], pu[2], pu[3]);
+            ptx::st_shared_v4(ab + swz(lane, q8), pa[0], pa[1], pa[2], pa[3]);
+            ptx::st_shared_v4(ab + swz(lane, 4 + q8), 0u, 0u, 0u, 0u);
+          }
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&mC0, hb, 0, wrow);  // dH = [d gate | d up]
+            ptx::bulk_commit();
+          }
+          sq.issue(lane, ia, &mC1, 0, wrow);  // A' (columns >= n clipped by the tensor map)
+          if (has_next) {
+            sq.template wait_reads<1>(lane);  // the dH store out of the H buffer has read it
+            h_issue(tile + t_step);
+          }
         }
         if (__ldg(args.row_token + row) < 0) ds = 0.f;
         if (args.n_tiles == 1)
@@ -821,7 +792,14 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CTA2) {
+          if (leader) ptx::mbar_arrive(&tempty[acc]);
+          else ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
+        } else {
+          ptx::mbar_arrive(&tempty[acc]);
+        }
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -830,10 +808,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CTA2) ptx::cluster_sync();
+  else __syncthreads();
   if (warp == NP) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+    if constexpr (CTA2) ptx::tmem_dealloc2(tmem_base, Cfg::TMEM_COLS);
+    else ptx::tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
   }
 }
 

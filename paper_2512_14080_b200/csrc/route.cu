@@ -317,33 +317,54 @@ __global__ void k_orphans(const uint32_t* __restrict__ bm_kept, int T, int E, in
 }
 
 // ---------------------------------------------------------------- offsets & tiles
+// Also builds the 2-CTA schedule: each expert's 128-row tiles are paired (t, t+1); an expert with
+// an odd tile count ends with a half pair (bit 31 clear).
 __global__ void __launch_bounds__(1024) k_offsets(const int* __restrict__ f_r, int E, int* __restrict__ offsets,
                                                   int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
-                                                  int* __restrict__ num_tiles) {
+                                                  int* __restrict__ num_tiles, int* __restrict__ tile_pairs,
+                                                  int* __restrict__ num_pairs) {
   __shared__ int s_pad[4097];
-  int base = 0, pbase = 0;
+  __shared__ int s_pp[4097];
+  int base = 0, pbase = 0, ppbase = 0;
   for (int e0 = 0; e0 < E; e0 += blockDim.x) {
     const int e = e0 + threadIdx.x;
     const int c = e < E ? f_r[e] : 0;
     const int pc = (c + GEMM_M - 1) / GEMM_M * GEMM_M;
-    int tot, ptot;
+    const int pp = (pc / GEMM_M + 1) / 2;
+    int tot, ptot, pptot;
     const int ex = block_excl_scan(c, &tot);
     const int pex = block_excl_scan(pc, &ptot);
+    const int ppex = block_excl_scan(pp, &pptot);
     if (e < E) {
       offsets[e] = base + ex;
       pad_offsets[e] = pbase + pex;
       s_pad[e] = pbase + pex;
+      s_pp[e] = ppbase + ppex;
     }
     base += tot;
     pbase += ptot;
+    ppbase += pptot;
   }
   if (threadIdx.x == 0) {
     offsets[E] = base;
     pad_offsets[E] = pbase;
     s_pad[E] = pbase;
+    s_pp[E] = ppbase;
     *num_tiles = pbase / GEMM_M;
+    *num_pairs = ppbase;
   }
   __syncthreads();
+  for (int i = threadIdx.x; i < ppbase; i += blockDim.x) {
+    int lo = 0, hi = E - 1;  // largest e with s_pp[e] <= i
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_pp[mid] <= i) lo = mid; else hi = mid - 1;
+    }
+    const int j = i - s_pp[lo];
+    const int tiles_e = (s_pad[lo + 1] - s_pad[lo]) / GEMM_M;
+    const int first = s_pad[lo] / GEMM_M + 2 * j;
+    tile_pairs[i] = first | ((2 * j + 1 < tiles_e) ? (int)0x80000000u : 0);
+  }
   const int nt = pbase / GEMM_M;
   for (int i = threadIdx.x; i < nt; i += blockDim.x) {
     const int r = i * GEMM_M;
@@ -491,7 +512,8 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   } else {  // TC: one pass gives f, f_r (== f) and the word prefixes
     k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f, L.f_r); ++nl;
   }
-  k_offsets<<<1, 1024, 0, st>>>(L.f_r, E, L.offsets, L.pad_offsets, L.tile_expert, L.num_tiles); ++nl;
+  k_offsets<<<1, 1024, 0, st>>>(L.f_r, E, L.offsets, L.pad_offsets, L.tile_expert, L.num_tiles, L.tile_pairs,
+                                L.num_pairs); ++nl;
   k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
                                                          L.row_gate); ++nl;
   if (L.mode == 0) {

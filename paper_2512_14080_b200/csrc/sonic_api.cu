@@ -114,39 +114,66 @@ int num_sms() {
 }
 
 // ---------------------------------------------------------------- GEMM launch
-template <int KIND, int BN>
+template <int KIND, int BN, bool CTA2>
 bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
                    const CUtensorMap& dmap, const GemmArgs& args, int grid, cudaStream_t st) {
-  using Cfg = KCfg<KIND, BN>;
+  using Cfg = KCfg<KIND, BN, CTA2>;
+  auto kern = sonic_gemm_kernel<KIND, BN, CTA2>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(sonic_gemm_kernel<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
       return false;
     attr = true;
   }
-  sonic_gemm_kernel<KIND, BN><<<grid, gemm_threads<KIND>(), Cfg::SMEM, st>>>(a, b, c0, c1, dmap, args);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(gemm_threads<KIND>());
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = CTA2 ? 2 : 1;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, a, b, c0, c1, dmap, args) != cudaSuccess) return false;
   ++g_launches;
   return true;
 }
+
+// 2-CTA (cta_group::2) tiles for every GEMM whose N tile is >= 128 (SONIC_CTA2=0 disables).
+#ifndef SONIC_CTA2
+#define SONIC_CTA2 1
+#endif
+bool use_cta2(int BN) { return SONIC_CTA2 && BN >= 128; }
 
 // dmap: auxiliary tensor map (DH: the H cache, box {64, 32}); ignored by the other kinds.
 template <int KIND>
 bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
                  const GemmArgs& args, int grid, cudaStream_t st, const CUtensorMap* dmap = nullptr) {
   const CUtensorMap& d = dmap ? *dmap : c0;
+  const bool cta2 = use_cta2(BN);
+  if (cta2) grid &= ~1;
   switch (BN) {
-    case 256: return launch_gemm_t<KIND, 256>(a, b, c0, c1, d, args, grid, st);
-    case 128: return launch_gemm_t<KIND, 128>(a, b, c0, c1, d, args, grid, st);
-    case 64: return launch_gemm_t<KIND, 64>(a, b, c0, c1, d, args, grid, st);
+    case 256:
+      if constexpr (KIND == K_DH) return false;
+      else return cta2 ? launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st)
+                       : launch_gemm_t<KIND, 256, false>(a, b, c0, c1, d, args, grid, st);
+    case 128:
+      return cta2 ? launch_gemm_t<KIND, 128, true>(a, b, c0, c1, d, args, grid, st)
+                  : launch_gemm_t<KIND, 128, false>(a, b, c0, c1, d, args, grid, st);
+    case 64: return launch_gemm_t<KIND, 64, false>(a, b, c0, c1, d, args, grid, st);
     case 32:
-      if constexpr (KIND == K_DH) return launch_gemm_t<KIND, 32>(a, b, c0, c1, d, args, grid, st);
+      if constexpr (KIND == K_DH) return launch_gemm_t<KIND, 32, false>(a, b, c0, c1, d, args, grid, st);
       return false;
     default: return false;
   }
 }
 
 int pick_bn(long long N) { return N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64; }
+// rows of the K-major weight box held by one CTA
+int bnl(int BN) { return use_cta2(BN) ? BN / 2 : BN; }
 
 // ---------------------------------------------------------------- shapes & validation
 struct Shape {
@@ -268,6 +295,8 @@ sonic_status sonic_routing_sizes(const sonic_moe_desc* D, size_t b[SONIC_ROUTING
   b[9] = (size_t)s.rows_max * 4;              // token_rows
   b[10] = (size_t)(s.rows_max / GEMM_M) * 4;  // tile_expert
   b[11] = 4;                                  // num_tiles
+  b[12] = (size_t)(s.rows_max / GEMM_M + 1) * 4;  // tile_pairs
+  b[13] = 4;                                  // num_pairs
   return SONIC_OK;
 }
 
@@ -332,7 +361,8 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   const RouteWs w = route_ws(D);
   if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
   void* ptrs[] = {rt->topk_ids, rt->topk_s, rt->f, rt->f_rounded, rt->offsets, rt->pad_offsets, rt->row_token,
-                  rt->row_gate, rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->num_tiles};
+                  rt->row_gate, rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->num_tiles,
+                  rt->tile_pairs, rt->num_pairs};
   for (void* p : ptrs)
     if (!p) return SONIC_ERR_INVALID_ARG;
   if (!aligned16(S) || !aligned16(rt->row_token)) return SONIC_ERR_INVALID_ARG;
@@ -348,6 +378,7 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   L.offsets = rt->offsets; L.pad_offsets = rt->pad_offsets; L.row_token = rt->row_token;
   L.row_gate = rt->row_gate; L.token_rowptr = rt->token_rowptr; L.token_rows = rt->token_rows;
   L.tile_expert = rt->tile_expert; L.num_tiles = rt->num_tiles;
+  L.tile_pairs = rt->tile_pairs; L.num_pairs = rt->num_pairs;
   L.bm_tc = reinterpret_cast<uint32_t*>(base + w.bm_tc);
   L.bm_kept = reinterpret_cast<uint32_t*>(base + w.bm_kept);
   L.wprefix = reinterpret_cast<int*>(base + w.wprefix);
@@ -381,6 +412,7 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
 
   GemmArgs g{};
   g.num_m_tiles = rt->num_tiles; g.tile_expert = rt->tile_expert; g.row_token = rt->row_token;
+  g.num_pairs = rt->num_pairs; g.tile_pairs = rt->tile_pairs;
   g.row_gate = rt->row_gate; g.pad_offsets = rt->pad_offsets; g.E = E; g.n = n; g.rows_max = R;
 
   // K1 up-proj: H = Gather(X) W1_e, SwiGLU epilogue -> H, A
@@ -442,18 +474,19 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
 
   GemmArgs g{};
   g.num_m_tiles = rt->num_tiles; g.tile_expert = rt->tile_expert; g.row_token = rt->row_token;
+  g.num_pairs = rt->num_pairs; g.tile_pairs = rt->tile_pairs;
   g.row_gate = rt->row_gate; g.pad_offsets = rt->pad_offsets; g.E = E; g.n = n; g.rows_max = R;
 
   // K4 dH: dA' = Gather(dO) W2_e^T; epilogue dSwiGLU -> dH, A' = s A, dS = <dA', A>
   {
     CUtensorMap mA, mB, mC0, mC1, mH;
     const int BN = dh_bn(n);
-    if (!map2d(&mA, dO, false, s.T, d, 64, 1) || !map3d(&mB, W2, false, E, n, d, 64, BN) ||
+    if (!map2d(&mA, dO, false, s.T, d, 64, 1) || !map3d(&mB, W2, false, E, n, d, 64, bnl(BN)) ||
         !map2d(&mC0, dH, false, R, 2 * n, 64, 32) || !map2d(&mC1, Ap, false, R, n, 64, 32) ||
         !map2d(&mH, H, false, R, 2 * n, 64, 32))
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
-    a.n_tiles = n / BN; a.k_blocks = d / 64; a.N_dim = n; a.H = static_cast<const __nv_bfloat16*>(H);
+    a.n_tiles = n / BN; a.k_blocks = d / 64; a.N_dim = n;
     a.gsrc = static_cast<const __nv_bfloat16*>(dO); a.gld = d;
     a.dS = a.n_tiles > 1 ? dSp : dS;
     {
@@ -484,7 +517,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   {
     CUtensorMap mA, mB, mC0;
     const int BN = pick_bn(d);
-    if (!map2d(&mA, dH, false, R, 2 * n, 64, 128) || !map3d(&mB, W1, false, E, d, 2 * n, 64, BN) ||
+    if (!map2d(&mA, dH, false, R, 2 * n, 64, 128) || !map3d(&mB, W1, false, E, d, 2 * n, 64, bnl(BN)) ||
         !map2d(&mC0, dXt, false, R, d, 64, 32))
       return SONIC_ERR_CUDA;
     GemmArgs a = g;

@@ -14,7 +14,7 @@ struct RouteLaunch {
   const float* S;
   // outputs
   int *topk_ids, *f, *f_r, *offsets, *pad_offsets, *row_token, *token_rowptr, *token_rows, *tile_expert,
-      *num_tiles;
+      *num_tiles, *tile_pairs, *num_pairs;
   float *topk_s, *row_gate;
   // workspace
   uint32_t *bm_tc, *bm_kept;

@@ -22,7 +22,7 @@ SONIC_F_NO_ORPHAN_RESCUE = 2
 GEMM_M = 128
 
 ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",
-                  "token_rowptr", "token_rows", "tile_expert", "num_tiles"]
+                  "token_rowptr", "token_rows", "tile_expert", "num_tiles", "tile_pairs", "num_pairs"]
 _FLOAT_FIELDS = {"topk_s", "row_gate"}
 
 

@@ -52,6 +52,8 @@ def routing_to_numpy(rt, desc):
     out["row_gate"] = out["row_gate"][:R_pad]
     out["token_rows"] = out["token_rows"][:R]
     out["tile_expert"] = out["tile_expert"][: R_pad // om.GEMM_M]
+    out["num_pairs"] = out["num_pairs"][:1]
+    out["tile_pairs"] = out["tile_pairs"][: int(out["num_pairs"][0])]
     return out
 
 
