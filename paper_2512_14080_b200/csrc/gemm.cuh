@@ -72,9 +72,17 @@ template <int KIND>
 __host__ __device__ constexpr int num_producer_warps() {
   return (Traits<KIND>::a_gather || Traits<KIND>::b_gather) ? 4 : 1;
 }
+// Epilogue warps: 4 (one per TMEM lane quarter).  SONIC_EPI_WARPS=8 puts two warps on each quarter,
+// each taking every other 64-column chunk; measured slower at 7B (725 vs 745 TF: fewer registers
+// and a mainloop stage less) and one small-shape test hung with it -- experimental, not validated.
+#ifndef SONIC_EPI_WARPS
+#define SONIC_EPI_WARPS 4
+#endif
+constexpr int EPI_WARPS = SONIC_EPI_WARPS;
+constexpr int EPI_HALVES = EPI_WARPS / 4;
 template <int KIND>
 __host__ __device__ constexpr int gemm_threads() {
-  return 32 * (num_producer_warps<KIND>() + 5);
+  return 32 * (num_producer_warps<KIND>() + 1 + EPI_WARPS);
 }
 
 constexpr int GEMM_BM = 128;
@@ -89,9 +97,11 @@ struct GemmCfg {
   static constexpr uint32_t B_BYTES = BNL * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NB = NB_;  // epilogue staging buffers per epilogue warp (ring)
-  // DH only: per-epilogue-warp H buffer, 32 rows x (BN gate + BN up) bf16 columns (TMA-loaded)
-  static constexpr int HBUF_WARP = HTMA ? 32 * 2 * BN * 2 : 0;
-  static constexpr int FIXED = 4 * NB * STG_BYTES + 4 * HBUF_WARP + 1024 + 256;
+  // DH only: per-epilogue-warp H buffer, 32 rows x (gate + up) bf16 columns of the warp's chunks
+  static constexpr int HCOLS_WARP = (BN / EPI_HALVES) < 64 ? 64 : BN / EPI_HALVES;
+  static constexpr int HBUF_WARP = HTMA ? 32 * 2 * HCOLS_WARP * 2 : 0;
+  // + 1 KB alignment slack + barriers / dS exchange / TMEM address (< 1 KB)
+  static constexpr int FIXED = EPI_WARPS * NB * STG_BYTES + EPI_WARPS * HBUF_WARP + 1024 + 1024;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - FIXED) / (int)STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
@@ -244,13 +254,14 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + STAGES * STAGE_BYTES;
-  uint8_t* hbuf = stg + 4 * Cfg::NB * STG_BYTES;  // DH: 4 x HBUF_WARP
-  uint64_t* full = reinterpret_cast<uint64_t*>(hbuf + 4 * Cfg::HBUF_WARP);
+  uint8_t* hbuf = stg + EPI_WARPS * Cfg::NB * STG_BYTES;  // DH: EPI_WARPS x HBUF_WARP
+  uint64_t* full = reinterpret_cast<uint64_t*>(hbuf + EPI_WARPS * Cfg::HBUF_WARP);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* hfull = tempty + 2;  // one per epilogue warp
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(hfull + 4);
+  float* ds_xchg = reinterpret_cast<float*>(hfull + EPI_WARPS);  // DH: [4][32] partial dS of half 1
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ds_xchg + 128);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -269,9 +280,9 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], CTA2 ? 8 : 4);
+      ptx::mbar_init(&tempty[s], CTA2 ? 2 * EPI_WARPS : EPI_WARPS);
     }
-    for (int s = 0; s < 4; ++s) ptx::mbar_init(&hfull[s], 1);
+    for (int s = 0; s < EPI_WARPS; ++s) ptx::mbar_init(&hfull[s], 1);
     ptx::fence_barrier_init();
     ptx::prefetch_tmap(&mA);
     ptx::prefetch_tmap(&mB);
@@ -487,9 +498,10 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     }
     __syncwarp();
   } else {
-    // ============================================================ epilogue (4 warps)
+    // ============================================================ epilogue (EPI_WARPS warps)
     const int ew = warp - NP - 1;
-    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    const int q = warp & 3;         // TMEM lane quarter this warp may access
+    const int half = ew / 4;        // which interleaved 64-column chunks (32 for fp32) it handles
     StoreQ<Cfg::NB> sq{stg + ew * Cfg::NB * STG_BYTES, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -502,16 +514,28 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       if constexpr (HTMA) {
         if (lane == 0) {
           const TileCoord th = decode_tile<KIND, CTA2>(args, t, rank);
-          ptx::mbar_arrive_expect_tx(&hfull[ew], Cfg::HBUF_WARP);
           if constexpr (BN >= 64) {
+            // this warp's chunks c = half, half + EPI_HALVES, ... (local index lc): gate box at
+            // lc * 4 KB, up box at (NLC + lc) * 4 KB
+            constexpr int NLC = (BN / 64 + EPI_HALVES - 1) / EPI_HALVES;
+            int nb = 0;
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
-              ptx::tma_load_2d(hb + j * STG_BYTES, &mD, &hfull[ew], th.nt * BN + 64 * j, th.row0 + 32 * q);
-              ptx::tma_load_2d(hb + (BN / 64 + j) * STG_BYTES, &mD, &hfull[ew], args.n + th.nt * BN + 64 * j,
+            for (int c = half, lc = 0; c < BN / 64; c += EPI_HALVES, ++lc) nb += 2;
+            ptx::mbar_arrive_expect_tx(&hfull[ew], nb * STG_BYTES);
+#pragma unroll
+            for (int c = half, lc = 0; c < BN / 64; c += EPI_HALVES, ++lc) {
+              ptx::tma_load_2d(hb + lc * STG_BYTES, &mD, &hfull[ew], th.nt * BN + 64 * c, th.row0 + 32 * q);
+              ptx::tma_load_2d(hb + (NLC + lc) * STG_BYTES, &mD, &hfull[ew], args.n + th.nt * BN + 64 * c,
                                th.row0 + 32 * q);
             }
-          } else {  // n == 32: one box [gate | up]
-            ptx::tma_load_2d(hb, &mD, &hfull[ew], 0, th.row0 + 32 * q);
+            if (nb == 0) ptx::mbar_arrive(&hfull[ew]);  // no chunk for this warp: complete the phase
+          } else {  // n == 32: one box [gate | up], handled by half 0
+            if (half == 0) {
+              ptx::mbar_arrive_expect_tx(&hfull[ew], STG_BYTES);
+              ptx::tma_load_2d(hb, &mD, &hfull[ew], 0, th.row0 + 32 * q);
+            } else {
+              ptx::mbar_arrive(&hfull[ew]);
+            }
           }
         }
       }
@@ -540,7 +564,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         constexpr int W = BN / 2;
         if constexpr (W >= 64) {
 #pragma unroll 1
-          for (int c = 0; c < W; c += 64) {
+          for (int c = 64 * half; c < W; c += 64 * EPI_HALVES) {
             const int col = tc.nt * W + c;
             sq.template acquire<1>(lane);  // the next two ring slots are both free
             const int i0 = sq.sb;
@@ -583,7 +607,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
               ptx::st_shared_v4(b2 + swz(lane, ch), apk[4 * ch], apk[4 * ch + 1], apk[4 * ch + 2], apk[4 * ch + 3]);
             sq.issue(lane, i2, &mC1, col, wrow);           // A = SwiGLU(H)
           }
-        } else {  // n == 32: accumulator columns are [gate 32 | up 32] = the whole H row
+        } else if (half == 0) {  // n == 32: accumulator columns are [gate 32 | up 32] = the whole H row
           uint32_t g[32], u[32];
           ptx::tmem_ld32(t_acc, g);
           ptx::tmem_ld32(t_acc + 32, u);
@@ -610,7 +634,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         float gate = 1.f;
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 64) {
+        for (int c = 64 * half; c < BN; c += 64 * EPI_HALVES) {
           if (tc.nt * BN + c >= args.N_dim) break;
           const int i = sq.acquire(lane);
           const uint32_t b = sq.addr(i);
@@ -639,11 +663,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           ptx::mbar_wait(&hfull[ew], hphase);
           hphase ^= 1;
 #pragma unroll 1
-          for (int c = 0; c < BN / 64; ++c) {
+          for (int c = half, lc = 0; c < BN / 64; c += EPI_HALVES, ++lc) {
+            constexpr int NLC = (BN / 64 + EPI_HALVES - 1) / EPI_HALVES;
             const int col = tc.nt * BN + 64 * c;
-            const uint32_t gb = ptx::smem_u32(hb + c * STG_BYTES);              // H gate -> dH gate
-            const uint32_t ub = ptx::smem_u32(hb + (BN / 64 + c) * STG_BYTES);  // H up   -> dH up
-            const uint32_t ab = sq.addr(c & 1);                                  // A' staging
+            const uint32_t gb = ptx::smem_u32(hb + lc * STG_BYTES);          // H gate -> dH gate
+            const uint32_t ub = ptx::smem_u32(hb + (NLC + lc) * STG_BYTES);  // H up   -> dH up
+            const uint32_t ab = sq.addr(lc & 1);                              // A' staging
             sq.template wait_reads<3>(lane);  // the A' store issued from this buffer 2 chunks ago has read it
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -691,11 +716,11 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              ptx::tma_store_2d(&mC0, hb + c * STG_BYTES, col, wrow);                      // dH gate
+              ptx::tma_store_2d(&mC0, hb + lc * STG_BYTES, col, wrow);                     // dH gate
               ptx::bulk_commit();
-              ptx::tma_store_2d(&mC0, hb + (BN / 64 + c) * STG_BYTES, n + col, wrow);      // dH up
+              ptx::tma_store_2d(&mC0, hb + (NLC + lc) * STG_BYTES, n + col, wrow);         // dH up
               ptx::bulk_commit();
-              ptx::tma_store_2d(&mC1, sq.base + (c & 1) * STG_BYTES, col, wrow);           // A' = s A
+              ptx::tma_store_2d(&mC1, sq.base + (lc & 1) * STG_BYTES, col, wrow);          // A' = s A
               ptx::bulk_commit();
             }
           }
@@ -703,6 +728,10 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             sq.template wait_reads<1>(lane);  // every dH store out of the H buffer has read it
             h_issue(tile + t_step);
           }
+        } else if (half != 0) {  // n == 32: the whole tile belongs to half 0
+          ptx::mbar_wait(&hfull[ew], hphase);
+          hphase ^= 1;
+          if (has_next) h_issue(tile + t_step);
         } else {  // n == 32, BN == 32: one 64-column H box holds the whole row [gate 32 | up 32]
           ptx::mbar_wait(&hfull[ew], hphase);
           hphase ^= 1;
@@ -762,16 +791,25 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             h_issue(tile + t_step);
           }
         }
-        if (__ldg(args.row_token + row) < 0) ds = 0.f;
-        if (args.n_tiles == 1)
-          args.dS[row] = ds;
-        else
-          args.dS[(long long)tc.nt * args.rows_max + row] = ds;
+        if constexpr (EPI_HALVES == 2) {  // combine the two halves' partial dS of each row
+          const uint32_t bar_id = 1 + q;     // named barrier per lane quarter (64 threads)
+          if (half == 1) ds_xchg[32 * q + lane] = ds;
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+          if (half == 0) ds += ds_xchg[32 * q + lane];
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        }
+        if (half == 0) {
+          if (__ldg(args.row_token + row) < 0) ds = 0.f;
+          if (args.n_tiles == 1)
+            args.dS[row] = ds;
+          else
+            args.dS[(long long)tc.nt * args.rows_max + row] = ds;
+        }
       } else {  // K_DW2 / K_DW1: fp32 weight gradient tile [128 x BN] of expert e
         const int m0 = tc.mt * GEMM_BM + 32 * q;
         if (m0 < args.M_dim) {
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
+          for (int c = 32 * half; c < BN; c += 32 * EPI_HALVES) {
             if (tc.nt * BN + c >= args.N_dim) break;
             const int i = sq.acquire(lane);
             const uint32_t b = sq.addr(i);
