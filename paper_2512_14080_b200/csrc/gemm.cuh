@@ -161,7 +161,10 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, in
 }
 
 // Pad rows (-1) read token 0: their gate is 0, so every value they produce is exactly 0.
-__device__ __forceinline__ int tok_of(const int* row_token, int r) { return max(__ldg(row_token + r), 0); }
+// tok_of loads the raw map entry; clamp() is applied only where the address is formed, so a
+// prefetched load is not consumed (and waited for) at the prefetch point.
+__device__ __forceinline__ int tok_of(const int* row_token, int r) { return __ldg(row_token + r); }
+__device__ __forceinline__ size_t clamp_tok(int t) { return (size_t)max(t, 0); }
 
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 // sigma(x) = 0.5 tanh(x/2) + 0.5 with the SFU tanh (rel. err ~2^-11, far below bf16's 2^-8)
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         int ktok[4];
         if constexpr (!Tr::vk) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) srcM[j] = args.gsrc + (size_t)ntok[j] * args.gld + c * 8;
+          for (int j = 0; j < 8; ++j) srcM[j] = args.gsrc + clamp_tok(ntok[j]) * args.gld + c * 8;
           if (tile + t_step < total_tiles) {
             const TileCoord tn = decode_tile<KIND, CTA2>(args, tile + t_step, rank);
 #pragma unroll
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           if constexpr (Tr::vk) {
             const int col0 = Tr::a_gather ? acol0 : n0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) srcK[j] = args.gsrc + (size_t)ktok[j] * args.gld + col0 + c * 8;
+            for (int j = 0; j < 4; ++j) srcK[j] = args.gsrc + clamp_tok(ktok[j]) * args.gld + col0 + c * 8;
             if (kb + 1 < tc.nkb) {
               const int krow1 = tc.seg0 + (kb + 1) * GEMM_BK;
 #pragma unroll
