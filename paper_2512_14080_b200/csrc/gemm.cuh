@@ -556,7 +556,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
 
-      if (!tc.valid) {
+#ifdef SONIC_EXPERIMENT_NO_EPI
+      constexpr bool no_epi = true;  // ablation: mainloop only, nothing stored
+#else
+      constexpr bool no_epi = false;
+#endif
+      if (!tc.valid || no_epi) {
         // missing half of a pair: nothing to store (keep the H-buffer protocol going)
         if constexpr (HTMA) {
           ptx::mbar_wait(&hfull[ew], hphase);

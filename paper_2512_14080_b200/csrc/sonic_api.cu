@@ -102,6 +102,30 @@ bool map3d(CUtensorMap* m, const void* ptr, bool f32, long long E, long long row
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#ifndef SONIC_BWD_OVERLAP
+#define SONIC_BWD_OVERLAP 1  // measured at 7B: 0 -> 784/795, 1 -> 800/801, 2 -> 792/800 TFLOPS
+#endif
+// One internal non-blocking stream (+ fork/join events) per device, for the backward's
+// weight-gradient branch.  Created on first use; calls from several host threads on the same
+// device would share it (the library is not meant for that).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool ok = false;
+};
+SideStream& side_stream() {
+  static SideStream per_dev[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStream& ss = per_dev[dev & 63];
+  if (!ss.ok) {
+    ss.ok = cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) == cudaSuccess;
+  }
+  return ss;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -499,51 +523,79 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       ++g_launches;
     }
   }
-  // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
-  {
-    CUtensorMap mA, mB, mC0;
-    const int BN = pick_bn(d);
-    if (!map2d(&mA, Ap, false, R, n, 64, 64) || !map2d(&mB, dO, false, s.T, d, 64, 1) ||
-        !map3d(&mC0, dW2, true, E, n, d, 32, 32))
-      return SONIC_ERR_CUDA;
-    GemmArgs a = g;
-    a.n_tiles = d / BN; a.m_tiles = (n + 127) / 128; a.M_dim = n; a.N_dim = d;
-    a.gsrc = static_cast<const __nv_bfloat16*>(dO); a.gld = d;
-    const int tiles = E * a.m_tiles * a.n_tiles;
-    ProfScope ps("dW2", st);
-    if (!launch_gemm<K_DW2>(BN, mA, mB, mC0, mC0, a, std::min(grid, tiles), st)) return SONIC_ERR_CUDA;
+  // Stream arrangement of the rest of the backward (SONIC_BWD_OVERLAP):
+  //   0  everything on the caller's stream;
+  //   1  the dX aggregation on an internal side stream forked after dX~, co-residing with the
+  //      dW2/dW1 CTAs on the caller's stream;
+  //   2  dW2/dW1 on the side stream forked after dH; dX~ then the aggregation on the caller's.
+  // The side stream is joined before returning.
+  const int mode = SONIC_BWD_OVERLAP;
+  SideStream& ss = side_stream();
+  if (mode != 0 && !ss.ok) return SONIC_ERR_CUDA;
+  const cudaStream_t s_dw = mode == 2 ? ss.s : st;
+  const cudaStream_t s_agg = mode == 1 ? ss.s : st;
+  if (mode == 2) {
+    cudaEventRecord(ss.fork, st);
+    cudaStreamWaitEvent(ss.s, ss.fork, 0);
   }
+  CUtensorMap mA6, mB6, mC6, mA5, mB5, mC5, mA7, mB7, mC7;
+  GemmArgs a6 = g, a5 = g, a7 = g;
+  const int BN6 = pick_bn(d), BN5 = pick_bn(d), BN7 = pick_bn(2 * n);
   // K6 dX~_e = dH_e W1_e^T
-  {
-    CUtensorMap mA, mB, mC0;
-    const int BN = pick_bn(d);
-    if (!map2d(&mA, dH, false, R, 2 * n, 64, 128) || !map3d(&mB, W1, false, E, d, 2 * n, 64, bnl(BN)) ||
-        !map2d(&mC0, dXt, false, R, d, 64, 32))
-      return SONIC_ERR_CUDA;
-    GemmArgs a = g;
-    a.n_tiles = d / BN; a.k_blocks = (2 * n) / 64; a.N_dim = d;
-    ProfScope ps("dXt", st);
-    if (!launch_gemm<K_DXT>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
-  }
+  if (!map2d(&mA6, dH, false, R, 2 * n, 64, 128) || !map3d(&mB6, W1, false, E, d, 2 * n, 64, bnl(BN6)) ||
+      !map2d(&mC6, dXt, false, R, d, 64, 32))
+    return SONIC_ERR_CUDA;
+  a6.n_tiles = d / BN6; a6.k_blocks = (2 * n) / 64; a6.N_dim = d;
+  // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
+  if (!map2d(&mA5, Ap, false, R, n, 64, 64) || !map2d(&mB5, dO, false, s.T, d, 64, 1) ||
+      !map3d(&mC5, dW2, true, E, n, d, 32, 32))
+    return SONIC_ERR_CUDA;
+  a5.n_tiles = d / BN5; a5.m_tiles = (n + 127) / 128; a5.M_dim = n; a5.N_dim = d;
+  a5.gsrc = static_cast<const __nv_bfloat16*>(dO); a5.gld = d;
+  const int tiles5 = E * a5.m_tiles * a5.n_tiles;
   // K7 dW1_e = Gather(X)^T dH_e   (varlen-K)
-  {
-    CUtensorMap mA, mB, mC0;
-    const int BN = pick_bn(2 * n);
-    if (!map2d(&mA, X, false, s.T, d, 64, 1) || !map2d(&mB, dH, false, R, 2 * n, 64, 64) ||
-        !map3d(&mC0, dW1, true, E, d, 2 * n, 32, 32))
-      return SONIC_ERR_CUDA;
-    GemmArgs a = g;
-    a.n_tiles = (2 * n) / BN; a.m_tiles = (d + 127) / 128; a.M_dim = d; a.N_dim = 2 * n;
-    a.gsrc = static_cast<const __nv_bfloat16*>(X); a.gld = d;
-    const int tiles = E * a.m_tiles * a.n_tiles;
-    ProfScope ps("dW1", st);
-    if (!launch_gemm<K_DW1>(BN, mA, mB, mC0, mC0, a, std::min(grid, tiles), st)) return SONIC_ERR_CUDA;
+  if (!map2d(&mA7, X, false, s.T, d, 64, 1) || !map2d(&mB7, dH, false, R, 2 * n, 64, 64) ||
+      !map3d(&mC7, dW1, true, E, d, 2 * n, 32, 32))
+    return SONIC_ERR_CUDA;
+  a7.n_tiles = (2 * n) / BN7; a7.m_tiles = (d + 127) / 128; a7.M_dim = d; a7.N_dim = 2 * n;
+  a7.gsrc = static_cast<const __nv_bfloat16*>(X); a7.gld = d;
+  const int tiles7 = E * a7.m_tiles * a7.n_tiles;
+
+  auto run_dxt = [&]() {
+    ProfScope ps("dXt", st);
+    return launch_gemm<K_DXT>(BN6, mA6, mB6, mC6, mC6, a6, grid, st);
+  };
+  auto run_dw2 = [&]() {
+    ProfScope ps("dW2", s_dw);
+    return launch_gemm<K_DW2>(BN5, mA5, mB5, mC5, mC5, a5, std::min(grid, tiles5), s_dw);
+  };
+  auto run_dw1 = [&]() {
+    ProfScope ps("dW1", s_dw);
+    return launch_gemm<K_DW1>(BN7, mA7, mB7, mC7, mC7, a7, std::min(grid, tiles7), s_dw);
+  };
+  auto run_agg = [&]() {  // K8 dX aggregation
+    ProfScope ps("agg_dX", s_agg);
+    launch_aggregate(static_cast<const __nv_bfloat16*>(dXt), rt->token_rowptr, rt->token_rows,
+                     static_cast<__nv_bfloat16*>(dX), s.T, d, s_agg);
+    ++g_launches;
+  };
+  if (!run_dxt()) return SONIC_ERR_CUDA;
+  if (mode == 1) {
+    cudaEventRecord(ss.fork, st);
+    cudaStreamWaitEvent(ss.s, ss.fork, 0);
+    run_agg();
+    cudaEventRecord(ss.join, ss.s);
+    if (!run_dw2() || !run_dw1()) return SONIC_ERR_CUDA;
+  } else if (mode == 2) {
+    if (!run_dw2()) return SONIC_ERR_CUDA;
+    run_agg();
+    if (!run_dw1()) return SONIC_ERR_CUDA;
+    cudaEventRecord(ss.join, ss.s);
+  } else {
+    if (!run_dw2() || !run_dw1()) return SONIC_ERR_CUDA;
+    run_agg();
   }
-  // K8 dX aggregation
-  ProfScope ps("agg_dX", st);
-  launch_aggregate(static_cast<const __nv_bfloat16*>(dXt), rt->token_rowptr, rt->token_rows,
-                   static_cast<__nv_bfloat16*>(dX), s.T, d, st);
-  ++g_launches;
+  if (mode != 0) cudaStreamWaitEvent(st, ss.join, 0);
   return check_launch();
 }
 
