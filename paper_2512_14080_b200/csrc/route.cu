@@ -63,13 +63,9 @@ __device__ int block_excl_scan(int v, int* total) {
 // Exact 64-bit keys (ordered score << 32 | ~expert): the largest key is the largest score and,
 // among equal scores, the lower expert id -- the stable order of P:1099 without packing loss.
 template <int G, int VPL>
-__global__ void __launch_bounds__(256) k_route_topk(const float* __restrict__ S, int T, int E, int K, int W,
-                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
-                                                    uint32_t* __restrict__ bm_tc) {
-  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = gt / G;
-  const int g = gt % G;
-  if (t >= T) return;  // G divides 32 and T is processed in whole groups: no partial-group shuffles
+__device__ __forceinline__ void route_topk_token(const float* __restrict__ S, int t, int E, int K, int g,
+                                                 int* __restrict__ topk_ids, float* __restrict__ topk_s,
+                                                 uint32_t* words) {
   const float* row = S + (size_t)t * E;
   unsigned long long key[VPL];
 #pragma unroll
@@ -94,9 +90,26 @@ __global__ void __launch_bounds__(256) k_route_topk(const float* __restrict__ S,
     if (g == (k % G)) {
       topk_ids[(size_t)t * K + k] = e;
       topk_s[(size_t)t * K + k] = __ldg(row + e);
-      atomicOr(bm_tc + (size_t)e * W + (t >> 5), 1u << (t & 31));
+      atomicOr(&words[e], 1u << (t & 31));  // shared memory
     }
   }
+}
+
+// One block = one 32-token bitmap word: the block's 32*G threads handle tokens 32*blockIdx.x + i;
+// the chosen experts are OR-ed into a shared-memory word per expert, then every expert's word for
+// this token block is written once (no global atomics, no memset of the bitmap).
+template <int G, int VPL>
+__global__ void __launch_bounds__(32 * G) k_route_topk(const float* __restrict__ S, int T, int E, int K, int W,
+                                                       int* __restrict__ topk_ids, float* __restrict__ topk_s,
+                                                       uint32_t* __restrict__ bm_tc) {
+  __shared__ uint32_t words[4096];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) words[e] = 0u;
+  __syncthreads();
+  const int t = blockIdx.x * 32 + threadIdx.x / G;
+  const int g = threadIdx.x % G;
+  if (t < T) route_topk_token<G, VPL>(S, t, E, K, g, topk_ids, topk_s, words);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
 }
 
 // TC fast path of the token CSR: every token keeps exactly its K top-K experts, so
@@ -479,12 +492,9 @@ __global__ void k_token_rows(const uint32_t* __restrict__ bm_kept, const int* __
 int launch_route(const RouteLaunch& L, cudaStream_t st) {
   int nl = 0;
   const int T = (int)L.T, E = L.E, K = L.K, W = L.W;
-  cudaMemsetAsync(L.bm_tc, 0, (size_t)E * W * 4, st);
   {
-    const int threads = 256;
-#define TOPK_CASE(G, V)                                                             \
-  k_route_topk<G, V><<<(int)(((long long)T * G + threads - 1) / threads), threads, 0, st>>>( \
-      L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
+#define TOPK_CASE(G, V) \
+  k_route_topk<G, V><<<W, 32 * G, 0, st>>>(L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
     if (E <= 32) TOPK_CASE(4, 8);
     else if (E <= 64) TOPK_CASE(8, 8);
     else if (E <= 128) TOPK_CASE(8, 16);
@@ -517,7 +527,7 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
                                                          L.row_gate); ++nl;
   if (L.mode == 0) {
-    k_token_rows_tc<<<(T + 1 + 255) / 256, 256, 0, st>>>(L.topk_ids, L.topk_s, bm_kept, L.wprefix, T, K, W,
+    k_token_rows_tc<<<(T + 1 + 63) / 64, 64, 0, st>>>(L.topk_ids, L.topk_s, bm_kept, L.wprefix, T, K, W,
                                                          L.pad_offsets, L.gate_raw, L.token_rowptr, L.token_rows,
                                                          L.row_gate); ++nl;
   } else {
