@@ -55,7 +55,10 @@ typedef enum {
 
 typedef enum {
   SONIC_ROUTE_TC = 0,      /* token-choice top-K */
-  SONIC_ROUTE_TR_NRF = 1   /* token rounding, Alg. 4 with NR-f */
+  SONIC_ROUTE_TR_NRF = 1,  /* token rounding, Alg. 4 with NR-f */
+  SONIC_ROUTE_GIVEN = 2    /* arbitrary routing input: S is the gate matrix, t -> e iff
+                              S[t,e] != 0, gate = S[t,e] (no renormalisation); topk_ids/topk_s are
+                              not written; K may be up to E.  Used by the expert-parallel receive side. */
 } sonic_route_mode;
 
 /* flags */
@@ -163,6 +166,49 @@ int sonic_last_launch_count(void);
  * clears the record list and returns the number written. */
 void sonic_profile_enable(int on);
 int sonic_profile_collect(char *names, int name_len, float *ms, int max_records);
+
+/*
+ * ---------------------------------------------------------------- expert parallelism
+ * G ranks; rank g owns experts [g*L, (g+1)*L), L = E/G (E % G == 0, G <= 32).  Each rank routes its
+ * own T tokens over all E experts with sonic_route; the calls below build and use the dispatch plan
+ * of one rank.  The all-to-all itself (NCCL over NVLink) is the caller's (torch.distributed):
+ * send row i of the send buffer goes to rank g for send_offsets[g] <= i < send_offsets[g+1].
+ * All pointers are device pointers; calls are asynchronous on `stream`; invalid arguments return
+ * SONIC_ERR_INVALID_ARG before any launch.
+ */
+typedef struct {
+  int32_t  *dmask;        /* [T]      bit g set when token t has a kept expert on rank g */
+  uint32_t *bm;           /* [G, W]   per-rank token bitmaps, W = ceil(T/32) */
+  int32_t  *wprefix;      /* [G, W]   exclusive popcount prefix per rank */
+  int32_t  *send_counts;  /* [G]      rows sent to each rank (one per token per rank: de-duplicated) */
+  int32_t  *send_offsets; /* [G+1]    exclusive prefix of send_counts; send_offsets[G] = rows to send */
+  int32_t  *tokcnt;       /* [T]      ranks per token */
+  int32_t  *ep_rowptr;    /* [T+1]    CSR over tokens of their send rows (ascending rank) */
+  int32_t  *ep_rows;      /* [T*G]    */
+  int32_t  *send_token;   /* [T*G]    token of each send row (ascending token within a rank) */
+  float    *send_gate;    /* [T*G, L] the token's gates for the destination's L experts, 0 = not routed */
+} sonic_ep_plan;
+#define SONIC_EP_PLAN_NFIELDS 10
+
+sonic_status sonic_ep_plan_sizes(const sonic_moe_desc *desc, int G, size_t bytes_out[SONIC_EP_PLAN_NFIELDS]);
+/* Build the plan from this rank's routing (the sonic_route output for desc). */
+sonic_status sonic_ep_build_plan(const sonic_moe_desc *desc, int G, const sonic_routing *rt, sonic_ep_plan *plan,
+                                 void *stream);
+/* send[i] = src[send_token[i]] for i < send_offsets[G] (src: [T,d] bf16 -- X forward, dO backward). */
+sonic_status sonic_ep_pack(const sonic_moe_desc *desc, int G, const sonic_ep_plan *plan, const void *src,
+                           void *send, void *stream);
+/* out[t] = sum of back[ep_rows[ep_rowptr[t] .. ep_rowptr[t+1])] in ascending rank order, fp32
+ * accumulation (back: the returned rows, laid out like the send buffer; out: [T,d] bf16). */
+sonic_status sonic_ep_combine(const sonic_moe_desc *desc, int G, const sonic_ep_plan *plan, const void *back,
+                              void *out, void *stream);
+/* Receive side: dS of the local grouped rows (local desc = GIVEN routing of the received rows over
+ * the L local experts) -> dense [rows_in, L] fp32 (zeros where not routed). */
+sonic_status sonic_ep_ds_dense(const sonic_moe_desc *local_desc, const sonic_routing *local_rt, const float *dS,
+                               float *dense, void *stream);
+/* Source side: returned dense dS rows (laid out like the send buffer, [*, L]) -> dS [rows_max] of
+ * this rank's routing. */
+sonic_status sonic_ep_ds_scatter(const sonic_moe_desc *desc, int G, const sonic_routing *rt,
+                                 const sonic_ep_plan *plan, const float *back, float *dS, void *stream);
 
 #ifdef __cplusplus
 }

@@ -488,10 +488,46 @@ __global__ void k_token_rows(const uint32_t* __restrict__ bm_kept, const int* __
   }
 }
 
+void launch_popc(const uint32_t* bm, int W, int nrows, int* wprefix, int* cnt, cudaStream_t st) {
+  k_expert_popc<<<nrows, 1024, 0, st>>>(bm, W, wprefix, cnt, nullptr);
+}
+void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st) {
+  k_scan_tokens<<<1, 1024, 0, st>>>(cnt, T, rowptr);
+}
+
+// ---------------------------------------------------------------- given routing
+// SONIC_ROUTE_GIVEN ("an interface that accepts arbitrary routing input"): S is the gate
+// matrix itself, token t is routed to e iff S[t,e] != 0.  One block per 32-token word.
+__global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W, uint32_t* __restrict__ bm) {
+  __shared__ uint32_t words[4096];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) words[e] = 0u;
+  __syncthreads();
+  for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) {
+    const int tl = i / E, e = i - tl * E;
+    const int t = blockIdx.x * 32 + tl;
+    if (t < T && S[(size_t)t * E + e] != 0.f) atomicOr(&words[e], 1u << tl);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) bm[(size_t)e * W + blockIdx.x] = words[e];
+}
+
 // ---------------------------------------------------------------- launcher
 int launch_route(const RouteLaunch& L, cudaStream_t st) {
   int nl = 0;
   const int T = (int)L.T, E = L.E, K = L.K, W = L.W;
+  if (L.mode == 2) {  // given routing: bitmap, counts, offsets, rows, CSR with raw gates
+    k_given_bitmap<<<W, 256, 0, st>>>(L.S, T, E, W, L.bm_tc); ++nl;
+    k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, L.wprefix, L.f, L.f_r); ++nl;
+    k_offsets<<<1, 1024, 0, st>>>(L.f_r, E, L.offsets, L.pad_offsets, L.tile_expert, L.num_tiles, L.tile_pairs,
+                                  L.num_pairs); ++nl;
+    k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(L.bm_tc, L.wprefix, W, L.f_r, L.pad_offsets,
+                                                           L.row_token, L.row_gate); ++nl;
+    k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_tc, T, E, W, L.tokcnt); ++nl;
+    k_scan_tokens<<<1, 1024, 0, st>>>(L.tokcnt, T, L.token_rowptr); ++nl;
+    k_token_rows<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_tc, L.wprefix, T, E, W, L.pad_offsets, L.tile_expert,
+                                                       L.token_rowptr, L.S, 1, L.token_rows, L.row_gate); ++nl;
+    return nl;
+  }
   {
 #define TOPK_CASE(G, V) \
   k_route_topk<G, V><<<W, 32 * G, 0, st>>>(L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)

@@ -208,9 +208,11 @@ struct Shape {
 bool valid_desc(const sonic_moe_desc* D) {
   if (!D) return false;
   if (D->T < 1 || D->d < 1 || D->n < 1 || D->E < 1 || D->K < 1) return false;
-  if (D->K > D->E || D->K > 16 || D->E > 4096) return false;
+  if (D->K > D->E || D->E > 4096) return false;
+  if (D->K > 16 && D->route_mode != SONIC_ROUTE_GIVEN) return false;
   if (D->m_tile != 128) return false;
-  if (D->route_mode != SONIC_ROUTE_TC && D->route_mode != SONIC_ROUTE_TR_NRF) return false;
+  if (D->route_mode != SONIC_ROUTE_TC && D->route_mode != SONIC_ROUTE_TR_NRF && D->route_mode != SONIC_ROUTE_GIVEN)
+    return false;
   return true;
 }
 bool supported_dims(const sonic_moe_desc* D) {
@@ -394,7 +396,7 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   uint8_t* base = static_cast<uint8_t*>(ws);
   RouteLaunch L{};
   L.T = s.T; L.E = s.E; L.K = s.K; L.W = s.W; L.m_tile = D->m_tile;
-  L.mode = D->route_mode == SONIC_ROUTE_TR_NRF ? 1 : 0;
+  L.mode = D->route_mode;  // 0 TC, 1 TR (NR-f), 2 given
   L.rescue = (D->flags & SONIC_F_NO_ORPHAN_RESCUE) ? 0 : 1;
   L.gate_raw = (D->flags & SONIC_F_GATE_RAW) ? 1 : 0;
   L.S = S;

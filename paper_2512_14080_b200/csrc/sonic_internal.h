@@ -23,6 +23,10 @@ struct RouteLaunch {
 };
 
 int launch_route(const RouteLaunch& L, cudaStream_t st);
+// per-row popcount + exclusive word prefix of a [nrows, W] bitmap; counts per row
+void launch_popc(const uint32_t* bm, int W, int nrows, int* wprefix, int* cnt, cudaStream_t st);
+// exclusive scan of cnt[0..T) into rowptr[0..T] (single block)
+void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st);
 
 // aggregation: out[t] = sum_{r in rows(t)} Y[r] (fp32 accumulation in CSR order)
 void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows, __nv_bfloat16* out, long long T,

@@ -1,0 +1,184 @@
+"""Expert parallelism: G ranks, rank g owns experts [g*L, (g+1)*L), L = E/G.
+
+Per layer and direction there is one exchange each way, an all-to-all-v over NVLink:
+
+  forward   route (own tokens, all E experts) -> plan -> pack X rows + gates -> a2a ->
+            GIVEN-route the received rows to the L local experts -> sonic_moe_fwd (its aggregation
+            pre-sums the local experts per received row) -> a2a back -> combine (ascending rank);
+  backward  pack dO rows -> a2a -> sonic_moe_bwd on the received rows (dW stays local) ->
+            a2a back of dX~ partial sums and of the dense per-row dS -> combine dX, scatter dS.
+
+One send row per (token, destination rank): a token whose K experts live on k ranks is sent k
+times, not K times.  Every step of the data path runs in libsonic's CUDA kernels; this module only
+moves tensors between ranks (torch.distributed all_to_all_single over NCCL -- plumbing) and sizes
+buffers (one device->host copy of the G send counts per direction: NCCL takes host split sizes).
+
+The algorithm is written for a LIST of local ranks so that the same code runs
+  * one rank per process under torchrun (DistComm, list of length 1), and
+  * G virtual ranks in one process on one GPU (SimComm) -- used by the single-GPU tests.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import sonic
+
+
+# ------------------------------------------------------------------------------- communicators
+class SimComm:
+    """G virtual ranks in one process: the all-to-all is a local shuffle of device buffers."""
+
+    def __init__(self, G):
+        self.G = G
+
+    def exchange_counts(self, send_counts):
+        """send_counts[s][g] (host ints) -> recv_counts[g][s]."""
+        return [[send_counts[s][g] for s in range(self.G)] for g in range(self.G)]
+
+    def alltoallv(self, sends, send_counts, recv_counts):
+        outs = []
+        for g in range(self.G):
+            parts = []
+            for s in range(self.G):
+                off = sum(send_counts[s][:g])
+                parts.append(sends[s][off: off + send_counts[s][g]])
+            outs.append(torch.cat(parts, 0) if parts else sends[g][:0])
+        return outs
+
+
+class DistComm:
+    """One rank per process (torch.distributed; NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.G = dist.get_world_size(group)
+
+    def exchange_counts(self, send_counts):
+        (sc,) = send_counts
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        t = torch.tensor(sc, dtype=torch.int64, device=dev)
+        r = torch.empty_like(t)
+        self.dist.all_to_all_single(r, t, group=self.group)
+        return [r.cpu().tolist()]
+
+    def alltoallv(self, sends, send_counts, recv_counts):
+        (s,), (sc,), (rc,) = sends, send_counts, recv_counts
+        out = torch.empty((sum(rc),) + tuple(s.shape[1:]), dtype=s.dtype, device=s.device)
+        self.dist.all_to_all_single(out, s[: sum(sc)].contiguous(), output_split_sizes=rc, input_split_sizes=sc,
+                                    group=self.group)
+        return [out]
+
+
+# ------------------------------------------------------------------------------- one rank
+@dataclass
+class EPRank:
+    """One rank's share of an expert-parallel MoE layer."""
+    T: int
+    d: int
+    n: int
+    E: int
+    K: int
+    G: int
+    rank: int
+    W1: torch.Tensor          # [L, d, 2n] bf16, experts [rank*L, (rank+1)*L)
+    W2: torch.Tensor          # [L, n, d]  bf16
+    mode: int = sonic.SONIC_ROUTE_TC
+    ctx: dict = field(default_factory=dict)
+
+    @property
+    def L(self):
+        return self.E // self.G
+
+    def desc(self):
+        return sonic.make_desc(self.T, self.d, self.n, self.E, self.K, mode=self.mode)
+
+    # -------------------------------------------------------------- forward
+    def dispatch_fwd(self, X, S):
+        desc = self.desc()
+        rt = sonic.sonic_route(desc, S)
+        plan = sonic.sonic_ep_build_plan(desc, self.G, rt)
+        nmax = self.T * self.G
+        send_x = torch.empty(nmax, self.d, dtype=torch.bfloat16, device=X.device)
+        sonic.sonic_ep_pack(desc, self.G, plan, X, send_x)
+        counts = plan.send_counts[: self.G].cpu().tolist()  # host split sizes (one sync)
+        self.ctx.update(rt=rt, plan=plan, counts=counts)
+        gates = plan.send_gate[: nmax * self.L].view(nmax, self.L)
+        return send_x, gates, counts
+
+    def compute_fwd(self, recv_x, recv_gate):
+        R_in = recv_x.shape[0]
+        self.ctx.update(R_in=R_in, recv_x=recv_x)
+        if R_in == 0:
+            return recv_x.new_zeros(0, self.d)
+        ld = sonic.make_desc(R_in, self.d, self.n, self.L, self.L, mode=sonic.SONIC_ROUTE_GIVEN)
+        lrt = sonic.sonic_route(ld, recv_gate.contiguous())
+        O_part, H, _ = sonic.sonic_moe_fwd(ld, recv_x, self.W1, self.W2, lrt)
+        self.ctx.update(ldesc=ld, lrt=lrt, H=H)
+        return O_part
+
+    def combine_fwd(self, back):
+        out = torch.empty(self.T, self.d, dtype=torch.bfloat16, device=back.device)
+        buf = back if back.shape[0] else back.new_zeros(1, self.d)
+        sonic.sonic_ep_combine(self.desc(), self.G, self.ctx["plan"], buf, out)
+        return out
+
+    # -------------------------------------------------------------- backward
+    def dispatch_bwd(self, dO):
+        send = torch.empty(self.T * self.G, self.d, dtype=torch.bfloat16, device=dO.device)
+        sonic.sonic_ep_pack(self.desc(), self.G, self.ctx["plan"], dO, send)
+        return send
+
+    def compute_bwd(self, recv_do):
+        R_in = self.ctx["R_in"]
+        dev = recv_do.device
+        if R_in == 0:
+            self.dW1 = torch.zeros(self.L, self.d, 2 * self.n, device=dev)
+            self.dW2 = torch.zeros(self.L, self.n, self.d, device=dev)
+            return recv_do.new_zeros(0, self.d), torch.zeros(0, self.L, device=dev)
+        ld, lrt = self.ctx["ldesc"], self.ctx["lrt"]
+        dX_part, dW1, dW2, dS, _ = sonic.sonic_moe_bwd(ld, recv_do, self.ctx["recv_x"], self.ctx["H"], self.W1,
+                                                       self.W2, lrt)
+        dense = torch.empty(R_in, self.L, dtype=torch.float32, device=dev)
+        sonic.sonic_ep_ds_dense(ld, lrt, dS, dense)
+        self.dW1, self.dW2 = dW1, dW2
+        return dX_part, dense
+
+    def combine_bwd(self, back_dx, back_ds):
+        desc, plan, rt = self.desc(), self.ctx["plan"], self.ctx["rt"]
+        dX = torch.empty(self.T, self.d, dtype=torch.bfloat16, device=back_dx.device)
+        sonic.sonic_ep_combine(desc, self.G, plan, back_dx if back_dx.shape[0] else back_dx.new_zeros(1, self.d), dX)
+        dS = torch.zeros(sonic.sonic_rows_max(desc), dtype=torch.float32, device=back_dx.device)
+        if back_ds.shape[0]:
+            sonic.sonic_ep_ds_scatter(desc, self.G, rt, plan, back_ds.contiguous(), dS)
+        return dX, dS
+
+
+# ------------------------------------------------------------------------------- the layer step
+def ep_forward(ranks, comm, Xs, Ss):
+    """Forward of the EP layer over the local ranks -> [O_r]."""
+    disp = [r.dispatch_fwd(X, S) for r, X, S in zip(ranks, Xs, Ss)]
+    send_counts = [c for _, _, c in disp]
+    recv_counts = comm.exchange_counts(send_counts)
+    recv_x = comm.alltoallv([x for x, _, _ in disp], send_counts, recv_counts)
+    recv_g = comm.alltoallv([g for _, g, _ in disp], send_counts, recv_counts)
+    parts = [r.compute_fwd(x, g) for r, x, g in zip(ranks, recv_x, recv_g)]
+    back = comm.alltoallv(parts, recv_counts, send_counts)
+    for r, rc in zip(ranks, recv_counts):
+        r.ctx["recv_counts"] = rc
+    return [r.combine_fwd(b) for r, b in zip(ranks, back)]
+
+
+def ep_backward(ranks, comm, dOs):
+    """Backward over the local ranks -> [(dX_r, dS_r)]; each rank keeps its local dW1 / dW2."""
+    send_counts = [r.ctx["counts"] for r in ranks]
+    recv_counts = [r.ctx["recv_counts"] for r in ranks]
+    sends = [r.dispatch_bwd(dO) for r, dO in zip(ranks, dOs)]
+    recv = comm.alltoallv(sends, send_counts, recv_counts)
+    outs = [r.compute_bwd(x) for r, x in zip(ranks, recv)]
+    back_dx = comm.alltoallv([o[0] for o in outs], recv_counts, send_counts)
+    back_ds = comm.alltoallv([o[1] for o in outs], recv_counts, send_counts)
+    return [r.combine_bwd(bx, bs) for r, bx, bs in zip(ranks, back_dx, back_ds)]

@@ -36,6 +36,14 @@ class sonic_routing(ctypes.Structure):
     _fields_ = [(f, ctypes.c_void_p) for f in ROUTING_FIELDS]
 
 
+EP_PLAN_FIELDS = ["dmask", "bm", "wprefix", "send_counts", "send_offsets", "tokcnt", "ep_rowptr", "ep_rows",
+                  "send_token", "send_gate"]
+
+
+class sonic_ep_plan(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in EP_PLAN_FIELDS]
+
+
 class SonicError(RuntimeError):
     pass
 
@@ -72,6 +80,18 @@ def lib():
         L.sonic_status_string.restype = ctypes.c_char_p
         L.sonic_last_launch_count.argtypes = []
         L.sonic_last_launch_count.restype = ctypes.c_int
+        L.sonic_ep_plan_sizes.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sz)]
+        L.sonic_ep_plan_sizes.restype = ctypes.c_int
+        L.sonic_ep_build_plan.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sonic_routing), P(sonic_ep_plan), vp]
+        L.sonic_ep_build_plan.restype = ctypes.c_int
+        for f in ("sonic_ep_pack", "sonic_ep_combine"):
+            getattr(L, f).argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sonic_ep_plan), vp, vp, vp]
+            getattr(L, f).restype = ctypes.c_int
+        L.sonic_ep_ds_dense.argtypes = [P(sonic_moe_desc), P(sonic_routing), vp, vp, vp]
+        L.sonic_ep_ds_dense.restype = ctypes.c_int
+        L.sonic_ep_ds_scatter.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sonic_routing), P(sonic_ep_plan), vp,
+                                          vp, vp]
+        L.sonic_ep_ds_scatter.restype = ctypes.c_int
         L.sonic_profile_enable.argtypes = [ctypes.c_int]
         L.sonic_profile_enable.restype = None
         L.sonic_profile_collect.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
@@ -222,3 +242,64 @@ def ws_view(ws, offset, shape, dtype):
         n *= s
     nbytes = n * torch.empty(0, dtype=dtype).element_size()
     return ws[offset: offset + nbytes].view(dtype).view(*shape)
+
+
+# ---------------------------------------------------------------------------- expert parallelism
+SONIC_ROUTE_GIVEN = 2
+
+
+@dataclass
+class EPPlan:
+    tensors: dict
+    c: sonic_ep_plan
+
+    def __getattr__(self, name):
+        t = self.__dict__.get("tensors")
+        if t is not None and name in t:
+            return t[name]
+        raise AttributeError(name)
+
+
+def sonic_ep_plan_sizes(desc, G):
+    arr = (ctypes.c_size_t * len(EP_PLAN_FIELDS))()
+    _check(lib().sonic_ep_plan_sizes(ctypes.byref(desc), G, arr), "sonic_ep_plan_sizes")
+    return dict(zip(EP_PLAN_FIELDS, list(arr)))
+
+
+def alloc_ep_plan(desc, G, device="cuda"):
+    sizes = sonic_ep_plan_sizes(desc, G)
+    tensors = {f: torch.empty(max(1, sizes[f] // 4), dtype=torch.float32 if f == "send_gate" else torch.int32,
+                              device=device) for f in EP_PLAN_FIELDS}
+    return EPPlan(tensors, sonic_ep_plan(*[t.data_ptr() for t in tensors.values()]))
+
+
+def sonic_ep_build_plan(desc, G, rt, plan=None):
+    if plan is None:
+        plan = alloc_ep_plan(desc, G, rt.tensors["row_token"].device)
+    _check(lib().sonic_ep_build_plan(ctypes.byref(desc), G, ctypes.byref(rt.c), ctypes.byref(plan.c), _stream()),
+           "sonic_ep_build_plan")
+    return plan
+
+
+def sonic_ep_pack(desc, G, plan, src, send):
+    _check(lib().sonic_ep_pack(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(src), _ptr(send), _stream()),
+           "sonic_ep_pack")
+    return send
+
+
+def sonic_ep_combine(desc, G, plan, back, out):
+    _check(lib().sonic_ep_combine(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(back), _ptr(out), _stream()),
+           "sonic_ep_combine")
+    return out
+
+
+def sonic_ep_ds_dense(local_desc, local_rt, dS, dense):
+    _check(lib().sonic_ep_ds_dense(ctypes.byref(local_desc), ctypes.byref(local_rt.c), _ptr(dS), _ptr(dense),
+                                   _stream()), "sonic_ep_ds_dense")
+    return dense
+
+
+def sonic_ep_ds_scatter(desc, G, rt, plan, back, dS):
+    _check(lib().sonic_ep_ds_scatter(ctypes.byref(desc), G, ctypes.byref(rt.c), ctypes.byref(plan.c), _ptr(back),
+                                     _ptr(dS), _stream()), "sonic_ep_ds_scatter")
+    return dS

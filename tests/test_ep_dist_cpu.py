@@ -1,0 +1,64 @@
+"""DistComm plumbing on CPU: world_size 2 over gloo (127.0.0.1).  Checks the count exchange and the
+variable-size all-to-all that carry the expert-parallel dispatch/combine (ep.py), including empty
+splits, against what each rank must receive."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2512_14080_b200.ep import DistComm
+        comm = DistComm()
+        # rank r sends (r+1)*(g+1) rows to rank g (rank 1 sends none to rank 0 -> empty split)
+        sc = [(rank + 1) * (g + 1) if not (rank == 1 and g == 0) else 0 for g in range(world)]
+        rc = comm.exchange_counts([sc])[0]
+        rows = []
+        for g in range(world):
+            rows += [[rank * 1000 + g * 100 + i, -1.0] for i in range(sc[g])]
+        send = torch.tensor(rows, dtype=torch.float32).view(-1, 2) if rows else torch.zeros(0, 2)
+        (recv,) = comm.alltoallv([send], [sc], [rc])
+        q.put((rank, rc, recv[:, 0].tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_distcomm_gloo_world2():
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, rc, vals = q.get(timeout=120)
+        res[r] = (rc, vals)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    # expected: rank g receives from source s the rows s*1000 + g*100 + i, i < count(s->g), sources ascending
+    for g in range(world):
+        want_counts, want_vals = [], []
+        for s in range(world):
+            c = (s + 1) * (g + 1) if not (s == 1 and g == 0) else 0
+            want_counts.append(c)
+            want_vals += [float(s * 1000 + g * 100 + i) for i in range(c)]
+        assert res[g][0] == want_counts
+        assert res[g][1] == want_vals
