@@ -8,8 +8,10 @@ fine-grained 7B-class layer (T=32768, d=1536, n=256, E=128, K=8, token-choice to
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 7b|qwen3|...] [--mode tc|tr]
   python bench.py --impl reference ...     # the fp64 CPU oracle on the host cores
 
-N > 1 (torchrun): every rank runs its own microbatch through the full layer (data-parallel
-replicas, weak scaling, no collective on the data path); time = max over ranks.
+N > 1 (torchrun): expert parallelism (paper_2512_14080_b200/ep.py) -- every rank brings its own
+T-token microbatch and owns E/N experts; tokens reach their experts' ranks through NCCL all-to-all
+(dispatch / combine, forward and backward).  Weak scaling; time = max over ranks; value = model
+FLOPs of all ranks' tokens / that time.  `--ep` runs the same EP code at N=1.
 Prints ONE JSON line on rank 0.  See DESIGN.md section 7 for every field.
 """
 from __future__ import annotations
@@ -78,16 +80,26 @@ class ClockSampler:
     def __init__(self, dev):
         self.dev = dev
         self.proc = None
+        self.skip = 0
         self.path = os.path.join("/tmp", f"sonic_clocks_{os.getpid()}.csv")
 
     def start(self):
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.fh,
+                                          "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.fh,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # nvidia-smi takes ~0.1-0.5 s to start: wait for its first sample so that the samples that
+        # follow fall inside the timed region
+        t0 = time.time()
+        while time.time() - t0 < 3.0 and self.proc.poll() is None:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.01)
+        self.skip = sum(1 for _ in open(self.path))
 
     def stop(self):
         if self.proc is None:
@@ -97,7 +109,9 @@ class ClockSampler:
         self.fh.close()
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        lines = open(self.path).readlines()
+        lines = lines[self.skip:] or lines[-1:]  # drop the idle sample(s) from before the timed region
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -165,7 +179,7 @@ def workload_config(args, cfg):
     return {"workload": f"{args.config}: T={cfg['T']} d={cfg['d']} n={cfg['n']} E={cfg['E']} K={cfg['K']} "
                         f"route={args.mode}",
             "T": cfg["T"], "d": cfg["d"], "n": cfg["n"], "E": cfg["E"], "K": cfg["K"], "route": args.mode,
-            "parallelism": f"replicas{args.gpus}" if args.gpus > 1 else "single",
+            "parallelism": f"ep{args.gpus}" if (args.gpus > 1 or getattr(args, "ep", False)) else "single",
             "l2": "not flushed: per-step working set (X, W1, W2, H, Y, dX~, ...) is several GB >> 126 MB L2"}
 
 
@@ -185,6 +199,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", default="", help="write the per-kernel table to this JSON file")
+    ap.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -210,40 +225,82 @@ def main():
     T, d, n, E, K = cfg["T"], cfg["d"], cfg["n"], cfg["E"], cfg["K"]
     mode = sonic.SONIC_ROUTE_TC if args.mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
     desc = sonic.make_desc(T, d, n, E, K, mode=mode)
-    inp = make_inputs(**cfg, seed=args.seed + rank, device=dev)
-    rows = sonic.sonic_rows_max(desc)
-    rt = sonic.alloc_routing(desc, dev)
-    ws_r = torch.empty(max(256, sonic.sonic_route_workspace_size(desc)), dtype=torch.uint8, device=dev)
-    ws_f = torch.empty(max(256, sonic.sonic_fwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
-    ws_b = torch.empty(max(256, sonic.sonic_bwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
-    O = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
-    H = torch.empty(rows, 2 * n, dtype=torch.bfloat16, device=dev)
-    dX = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
-    dW1 = torch.empty(E, d, 2 * n, dtype=torch.float32, device=dev)
-    dW2 = torch.empty(E, n, d, dtype=torch.float32, device=dev)
-    dS = torch.empty(rows, dtype=torch.float32, device=dev)
-    launches = [0]
+    use_ep = args.ep or world > 1
+    if not use_ep:
+        # ---- one GPU, all experts local: route + fwd + bwd through the C ABI
+        inp = make_inputs(**cfg, seed=args.seed + rank, device=dev)
+        X, S, dOin, W1, W2 = inp.X, inp.S, inp.dO, inp.W1, inp.W2
+        rows = sonic.sonic_rows_max(desc)
+        rt = sonic.alloc_routing(desc, dev)
+        ws_r = torch.empty(max(256, sonic.sonic_route_workspace_size(desc)), dtype=torch.uint8, device=dev)
+        ws_f = torch.empty(max(256, sonic.sonic_fwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
+        ws_b = torch.empty(max(256, sonic.sonic_bwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
+        O = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        H = torch.empty(rows, 2 * n, dtype=torch.bfloat16, device=dev)
+        dX = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        dW1 = torch.empty(E, d, 2 * n, dtype=torch.float32, device=dev)
+        dW2 = torch.empty(E, n, d, dtype=torch.float32, device=dev)
+        dS = torch.empty(rows, dtype=torch.float32, device=dev)
+
+        def run(Xa, Sa, dOa):
+            sonic.sonic_route(desc, Sa, rt, ws_r)
+            sonic.sonic_moe_fwd(desc, Xa, W1, W2, rt, O, H, ws_f)
+            sonic.sonic_moe_bwd(desc, dOa, Xa, H, W1, W2, rt, dX, dW1, dW2, dS, ws_b)
+            return O, dX
+
+        def routed_rows():
+            return int(rt.offsets[E].item()), int(rt.pad_offsets[E].item())
+
+        def local_model(R, R_pad):
+            return kernel_model(T, d, n, E, K, R, R_pad)
+    else:
+        # ---- expert parallelism over the `world` GPUs (NCCL all-to-all), weak scaling: every rank
+        #      brings its own T tokens and owns E/world experts (paper_2512_14080_b200/ep.py)
+        from paper_2512_14080_b200 import ep
+        from paper_2512_14080_b200.inputs import make_expert_weights, make_token_inputs
+        G = world
+        L = E // G
+        X, dOin, S = make_token_inputs(T, d, E, seed=args.seed + 17 * rank, device=dev)
+        W1, W2 = make_expert_weights(rank * L, (rank + 1) * L, d, n, seed=args.seed, device=dev)
+        comm = ep.DistComm() if world > 1 else ep.SimComm(1)
+        rk = ep.EPRank(T, d, n, E, K, G, rank, W1, W2, mode=mode)
+
+        def run(Xa, Sa, dOa):
+            (Oa,) = ep.ep_forward([rk], comm, [Xa], [Sa])
+            ((dXa, _),) = ep.ep_backward([rk], comm, [dOa])
+            return Oa, dXa
+
+        def routed_rows():
+            rt0 = rk.ctx["rt"]
+            return int(rt0.offsets[E].item()), int(rt0.pad_offsets[E].item())
+
+        def local_model(R, R_pad):
+            # the GEMMs run on the R_in rows this rank received, over its L experts (GIVEN routing)
+            R_in = rk.ctx["R_in"]
+            if R_in == 0:
+                return kernel_model(1, d, n, L, L, 0, 0)
+            lrt = rk.ctx["lrt"]
+            return kernel_model(R_in, d, n, L, L, int(lrt.offsets[L].item()), int(lrt.pad_offsets[L].item()))
 
     def step():
-        sonic.sonic_route(desc, inp.S, rt, ws_r)
-        launches[0] += sonic.sonic_last_launch_count()
-        sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt, O, H, ws_f)
-        launches[0] += sonic.sonic_last_launch_count()
-        sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt, dX, dW1, dW2, dS, ws_b)
-        launches[0] += sonic.sonic_last_launch_count()
+        run(X, S, dOin)
 
     for _ in range(max(args.warmup, 1)):  # >= 1 untimed step so R is known below
         step()
     torch.cuda.synchronize()
-    R = int(rt.offsets[E].item())
-    R_pad = int(rt.pad_offsets[E].item())
+    R, R_pad = routed_rows()
     flops_step = 18 * d * n * R
+    flops_all = flops_step
+    if world > 1:
+        ft = torch.tensor([float(flops_step)], device=dev, dtype=torch.float64)
+        dist.all_reduce(ft)
+        flops_all = float(ft.item())
 
     # ---- device-timed region: inputs resident in HBM
     clocks = ClockSampler(local)
     sonic.sonic_profile_enable(True)
     sonic.sonic_profile_collect()
-    launches[0] = 0
+    sonic.LAUNCHES[0] = 0
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -260,17 +317,17 @@ def main():
     sonic.sonic_profile_enable(False)
     recs = sonic.sonic_profile_collect()
     ms = ev0.elapsed_time(ev1)
-    gpu_launches = launches[0]
+    gpu_launches = sonic.LAUNCHES[0]
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = flops_step * world / (ms_step * 1e-3) / 1e12
+    value = flops_all / (ms_step * 1e-3) / 1e12
 
     # ---- per-kernel breakdown and roofline of the dominant kernel
     peaks = load_peaks()
-    model = kernel_model(T, d, n, E, K, R, R_pad)
+    model = local_model(R, R_pad)
     agg = {}
     for name, t in recs:
         a = agg.setdefault(name, [0.0, 0])
@@ -311,22 +368,20 @@ def main():
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        Xh = inp.X.cpu().pin_memory()
-        Sh = inp.S.cpu().pin_memory()
-        dOh = inp.dO.cpu().pin_memory()
+        Xh = X.cpu().pin_memory()
+        Sh = S.cpu().pin_memory()
+        dOh = dOin.cpu().pin_memory()
         Oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
         dXh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
-        Xd, Sd, dOd = torch.empty_like(inp.X), torch.empty_like(inp.S), torch.empty_like(inp.dO)
+        Xd, Sd, dOd = torch.empty_like(X), torch.empty_like(S), torch.empty_like(dOin)
 
         def step_e2e():
             Xd.copy_(Xh, non_blocking=True)
             Sd.copy_(Sh, non_blocking=True)
             dOd.copy_(dOh, non_blocking=True)
-            sonic.sonic_route(desc, Sd, rt, ws_r)
-            sonic.sonic_moe_fwd(desc, Xd, inp.W1, inp.W2, rt, O, H, ws_f)
-            sonic.sonic_moe_bwd(desc, dOd, Xd, H, inp.W1, inp.W2, rt, dX, dW1, dW2, dS, ws_b)
-            Oh.copy_(O, non_blocking=True)
-            dXh.copy_(dX, non_blocking=True)
+            Od, dXd = run(Xd, Sd, dOd)
+            Oh.copy_(Od, non_blocking=True)
+            dXh.copy_(dXd, non_blocking=True)
 
         step_e2e()
         torch.cuda.synchronize()
@@ -344,7 +399,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
         e_step = ems / args.e2e_steps
-        e2e = {"value": flops_step * world / (e_step * 1e-3) / 1e12, "unit": "TFLOPS",
+        e2e = {"value": flops_all / (e_step * 1e-3) / 1e12, "unit": "TFLOPS",
                "h2d_bytes_per_step": Xh.numel() * 2 + Sh.numel() * 4 + dOh.numel() * 2,
                "d2h_bytes_per_step": Oh.numel() * 2 + dXh.numel() * 2, "ms_per_step": e_step}
 
@@ -370,7 +425,7 @@ def main():
         "config": workload_config(args, cfg),
         "pct_peak": value / world / peaks["bf16_tflops"], "pct_peak_sustained": value / world / tf_peak,
         "tokens_per_s": T * world / (ms_step * 1e-3),
-        "model_flops_per_step": flops_step, "rows_routed": R, "rows_padded": R_pad,
+        "model_flops_per_step": flops_all, "rows_routed": R, "rows_padded": R_pad,
         "layer_roofline_ms": layer_roof_ms, "layer_roofline_frac": layer_roof_ms / ms_step,
         "act_mem_bytes": act,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,

@@ -156,7 +156,8 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc *desc, const void *dO, const voi
 
 const char *sonic_status_string(sonic_status s);
 
-/* Number of kernels the last sonic_route/fwd/bwd call on this thread launched. */
+/* Number of kernels the last sonic_route / sonic_moe_fwd / sonic_moe_bwd / sonic_ep_* compute call on
+ * this thread launched. */
 int sonic_last_launch_count(void);
 
 /* Optional timing instrumentation (per calling thread).  When enabled, every kernel (the

@@ -158,6 +158,7 @@ sonic_status sonic_ep_build_plan(const sonic_moe_desc* D, int G, const sonic_rou
   k_ep_fill<<<(T + 127) / 128, 128, 0, st>>>(rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->row_gate, T, L, W,
                                             p->dmask, p->bm, p->wprefix, p->send_offsets, p->ep_rowptr, p->ep_rows,
                                             p->send_token, p->send_gate);
+  set_last_launch_count(5);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
 }
 
@@ -168,6 +169,7 @@ sonic_status sonic_ep_pack(const sonic_moe_desc* D, int G, const sonic_ep_plan* 
   k_gather_rows<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(src), p->send_token, p->send_offsets + G, D->d,
       static_cast<__nv_bfloat16*>(send));
+  set_last_launch_count(1);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
 }
 
@@ -176,6 +178,7 @@ sonic_status sonic_ep_combine(const sonic_moe_desc* D, int G, const sonic_ep_pla
   if (!ep_ok(D, G) || !p || !back || !out) return SONIC_ERR_INVALID_ARG;
   launch_aggregate(static_cast<const __nv_bfloat16*>(back), p->ep_rowptr, p->ep_rows,
                    static_cast<__nv_bfloat16*>(out), D->T, D->d, static_cast<cudaStream_t>(stream));
+  set_last_launch_count(1);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
 }
 
@@ -188,6 +191,7 @@ sonic_status sonic_ep_ds_dense(const sonic_moe_desc* local, const sonic_routing*
   cudaMemsetAsync(dense, 0, (size_t)local->T * local->E * sizeof(float), st);
   k_ep_ds_dense<<<(unsigned)((rows_max + 255) / 256), 256, 0, st>>>(rt->row_token, rt->tile_expert, rt->num_tiles,
                                                                      dS, local->E, dense);
+  set_last_launch_count(1);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
 }
 
@@ -197,6 +201,7 @@ sonic_status sonic_ep_ds_scatter(const sonic_moe_desc* D, int G, const sonic_rou
   const int T = (int)D->T;
   k_ep_ds_scatter<<<(T + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
       rt->token_rowptr, rt->token_rows, rt->tile_expert, T, D->E / G, p->dmask, p->ep_rowptr, p->ep_rows, back, dS);
+  set_last_launch_count(1);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
 }
 

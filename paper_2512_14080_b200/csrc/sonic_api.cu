@@ -602,3 +602,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
 }
 
 }  // extern "C"
+
+namespace sonic {
+void set_last_launch_count(int n) { g_launches = n; }
+}  // namespace sonic

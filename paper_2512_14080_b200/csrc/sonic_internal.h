@@ -35,4 +35,7 @@ void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows
 void launch_ds_reduce(const float* part, int nparts, long long rows_max, const int* num_tiles, float* dS,
                       cudaStream_t st);
 
+// record the number of kernels the current C-ABI call launched (sonic_last_launch_count)
+void set_last_launch_count(int n);
+
 }  // namespace sonic

@@ -32,6 +32,30 @@ class MoEInputs:
     S: torch.Tensor    # [T,E] fp32 router scores (softmax of logits)
 
 
+def make_token_inputs(T, d, E, seed=0, device="cpu"):
+    """X, dO ~ N(0,1) bf16 and S = softmax(N(0,1) logits) fp32 for T tokens (expert-parallel runs:
+    every rank draws its own microbatch)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    X = torch.randn(T, d, generator=g, device=device).to(torch.bfloat16)
+    dO = torch.randn(T, d, generator=g, device=device).to(torch.bfloat16)
+    S = torch.softmax(torch.randn(T, E, generator=g, device=device), dim=1).contiguous()
+    return X.contiguous(), dO.contiguous(), S
+
+
+def make_expert_weights(e_lo, e_hi, d, n, seed=0, device="cpu"):
+    """W1 ~ N(0,1/d), W2 ~ N(0,1/n) (bf16) for experts [e_lo, e_hi); expert e is drawn from its own
+    seed, so any sharding of the experts over ranks yields the same weights."""
+    W1 = torch.empty(e_hi - e_lo, d, 2 * n, dtype=torch.bfloat16, device=device)
+    W2 = torch.empty(e_hi - e_lo, n, d, dtype=torch.bfloat16, device=device)
+    g = torch.Generator(device=device)
+    for i, e in enumerate(range(e_lo, e_hi)):
+        g.manual_seed(seed * 100003 + e)
+        W1[i] = (torch.randn(d, 2 * n, generator=g, device=device) / math.sqrt(d)).to(torch.bfloat16)
+        W2[i] = (torch.randn(n, d, generator=g, device=device) / math.sqrt(n)).to(torch.bfloat16)
+    return W1, W2
+
+
 def make_inputs(T, d, n, E, K=None, seed=0, device="cpu", skew=0.0, tie_levels=0):
     """X ~ N(0,1); W1 ~ N(0,1/d); W2 ~ N(0,1/n); dO ~ N(0,1); logits ~ N(0,1).
 

@@ -101,9 +101,19 @@ def lib():
     return _lib
 
 
+# cumulative count of libsonic kernel launches made through this binding (bench.py's gpu_launches)
+LAUNCHES = [0]
+
+
 def _check(status, what):
     if status != 0:
         raise SonicError(f"{what}: {lib().sonic_status_string(status).decode()} ({status})")
+
+
+def _done(status, what):
+    """_check a compute call and add the kernels it launched to LAUNCHES."""
+    _check(status, what)
+    LAUNCHES[0] += int(lib().sonic_last_launch_count())
 
 
 def make_desc(T, d, n, E, K, mode=SONIC_ROUTE_TC, m_tile=128, flags=0):
@@ -196,7 +206,7 @@ def sonic_route(desc, S, rt=None, ws=None):
         rt = alloc_routing(desc, S.device)
     if ws is None:
         ws = _ws(sonic_route_workspace_size(desc), S.device)
-    _check(lib().sonic_route(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(ws), ws.numel(), _stream()),
+    _done(lib().sonic_route(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(ws), ws.numel(), _stream()),
            "sonic_route")
     return rt
 
@@ -210,7 +220,7 @@ def sonic_moe_fwd(desc, X, W1, W2, rt, O=None, H=None, ws=None):
         H = torch.empty(rows, 2 * desc.n, dtype=torch.bfloat16, device=X.device)
     if ws is None:
         ws = _ws(sonic_fwd_workspace_size(desc), X.device)
-    _check(lib().sonic_moe_fwd(ctypes.byref(desc), _ptr(X), _ptr(W1), _ptr(W2), ctypes.byref(rt.c), _ptr(O),
+    _done(lib().sonic_moe_fwd(ctypes.byref(desc), _ptr(X), _ptr(W1), _ptr(W2), ctypes.byref(rt.c), _ptr(O),
                                _ptr(H), _ptr(ws), ws.numel(), _stream()), "sonic_moe_fwd")
     return O, H, ws
 
@@ -229,7 +239,7 @@ def sonic_moe_bwd(desc, dO, X, H, W1, W2, rt, dX=None, dW1=None, dW2=None, dS=No
         dS = torch.empty(rows, dtype=torch.float32, device=dev)
     if ws is None:
         ws = _ws(sonic_bwd_workspace_size(desc), dev)
-    _check(lib().sonic_moe_bwd(ctypes.byref(desc), _ptr(dO), _ptr(X), _ptr(H), _ptr(W1), _ptr(W2),
+    _done(lib().sonic_moe_bwd(ctypes.byref(desc), _ptr(dO), _ptr(X), _ptr(H), _ptr(W1), _ptr(W2),
                                ctypes.byref(rt.c), _ptr(dX), _ptr(dW1), _ptr(dW2), _ptr(dS), _ptr(ws), ws.numel(),
                                _stream()), "sonic_moe_bwd")
     return dX, dW1, dW2, dS, ws
@@ -276,30 +286,30 @@ def alloc_ep_plan(desc, G, device="cuda"):
 def sonic_ep_build_plan(desc, G, rt, plan=None):
     if plan is None:
         plan = alloc_ep_plan(desc, G, rt.tensors["row_token"].device)
-    _check(lib().sonic_ep_build_plan(ctypes.byref(desc), G, ctypes.byref(rt.c), ctypes.byref(plan.c), _stream()),
+    _done(lib().sonic_ep_build_plan(ctypes.byref(desc), G, ctypes.byref(rt.c), ctypes.byref(plan.c), _stream()),
            "sonic_ep_build_plan")
     return plan
 
 
 def sonic_ep_pack(desc, G, plan, src, send):
-    _check(lib().sonic_ep_pack(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(src), _ptr(send), _stream()),
+    _done(lib().sonic_ep_pack(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(src), _ptr(send), _stream()),
            "sonic_ep_pack")
     return send
 
 
 def sonic_ep_combine(desc, G, plan, back, out):
-    _check(lib().sonic_ep_combine(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(back), _ptr(out), _stream()),
+    _done(lib().sonic_ep_combine(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(back), _ptr(out), _stream()),
            "sonic_ep_combine")
     return out
 
 
 def sonic_ep_ds_dense(local_desc, local_rt, dS, dense):
-    _check(lib().sonic_ep_ds_dense(ctypes.byref(local_desc), ctypes.byref(local_rt.c), _ptr(dS), _ptr(dense),
+    _done(lib().sonic_ep_ds_dense(ctypes.byref(local_desc), ctypes.byref(local_rt.c), _ptr(dS), _ptr(dense),
                                    _stream()), "sonic_ep_ds_dense")
     return dense
 
 
 def sonic_ep_ds_scatter(desc, G, rt, plan, back, dS):
-    _check(lib().sonic_ep_ds_scatter(ctypes.byref(desc), G, ctypes.byref(rt.c), ctypes.byref(plan.c), _ptr(back),
+    _done(lib().sonic_ep_ds_scatter(ctypes.byref(desc), G, ctypes.byref(rt.c), ctypes.byref(plan.c), _ptr(back),
                                      _ptr(dS), _stream()), "sonic_ep_ds_scatter")
     return dS
