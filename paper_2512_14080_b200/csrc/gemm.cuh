@@ -88,7 +88,10 @@ __host__ __device__ constexpr int gemm_threads() {
 constexpr int GEMM_BM = 128;
 constexpr int GEMM_BK = 64;
 constexpr int STG_BYTES = 4096;  // one epilogue staging buffer: 32 rows x 128 B
-constexpr int SMEM_LIMIT = 232448;
+#ifndef SONIC_SMEM_LIMIT
+#define SONIC_SMEM_LIMIT 232448
+#endif
+constexpr int SMEM_LIMIT = SONIC_SMEM_LIMIT;
 
 template <int BN, bool CTA2, bool HTMA, int NB_>
 struct GemmCfg {
@@ -163,6 +166,9 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, in
 // Pad rows (-1) read token 0: their gate is 0, so every value they produce is exactly 0.
 // tok_of loads the raw map entry; clamp() is applied only where the address is formed, so a
 // prefetched load is not consumed (and waited for) at the prefetch point.
+#ifndef SONIC_KPD
+#define SONIC_KPD 4
+#endif
 __device__ __forceinline__ int tok_of(const int* row_token, int r) { return __ldg(row_token + r); }
 __device__ __forceinline__ size_t clamp_tok(int t) { return (size_t)max(t, 0); }
 
@@ -180,6 +186,9 @@ __device__ __forceinline__ uint32_t swz(int lane, int chunk) { return (uint32_t)
 // are issued in ring order, one bulk group each, so the buffer k slots ahead of the head was last
 // stored from NB-k stores ago: it is free once at most NB-1-k newer groups are pending a read.
 template <int NB>
+#ifndef SONIC_EXP_EPI
+#define SONIC_EXP_EPI 0  // ablation: 1 = TMEM loads only (down/dXt), 2 = no TMA stores
+#endif
 struct StoreQ {
   uint8_t* base;
   int sb;  // ring head: the next buffer to write
@@ -199,7 +208,11 @@ struct StoreQ {
   __device__ __forceinline__ void issue(int lane, int i, const CUtensorMap* map, int c0, int c1) {
     ptx::fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && SONIC_EXP_EPI == 3) {  // same traffic into L2, but L2-resident (per-warp 4 KB region)
+      ptx::tma_store_2d(map, base + i * STG_BYTES, 0, (int)(blockIdx.x * 8 + (threadIdx.x >> 5)) * 32);
+      ptx::bulk_commit();
+    }
+    if (lane == 0 && SONIC_EXP_EPI == 0) {
       ptx::tma_store_2d(map, base + i * STG_BYTES, c0, c1);
       ptx::bulk_commit();
     }
@@ -208,7 +221,7 @@ struct StoreQ {
   __device__ __forceinline__ void issue3d(int lane, int i, const CUtensorMap* map, int c0, int c1, int c2) {
     ptx::fence_proxy_async_smem();
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && (SONIC_EXP_EPI == 0 || SONIC_EXP_EPI == 3)) {
       ptx::tma_store_3d(map, base + i * STG_BYTES, c0, c1, c2);
       ptx::bulk_commit();
     }
@@ -344,6 +357,11 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       // Gather indices are prefetched one tile (varlen-M) / one stage (varlen-K) ahead so the
       // dependent cp.async addresses never wait on a global load.
       int ntok[8];
+      // varlen-K prefetch ring: KPD k-blocks of gather indices in flight (one k-block of MMA is
+      // ~700 clocks, an L2-resident index load ~800: distance 1 left the producers latency-bound)
+      constexpr int KPD = Tr::vk ? SONIC_KPD : 1;
+      constexpr int KU = Tr::vk ? KPD : 1;
+      int ktok[KPD][4];
       if constexpr (!Tr::vk) {
         if (t_first < total_tiles) {
           const TileCoord t0 = decode_tile<KIND, CTA2>(args, t_first, rank);
@@ -355,7 +373,6 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
         const int n0 = tc.nt * BN + rank * BNL;
         const __nv_bfloat16* srcM[8];
-        int ktok[4];
         if constexpr (!Tr::vk) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) srcM[j] = args.gsrc + clamp_tok(ntok[j]) * args.gld + c * 8;
@@ -366,20 +383,29 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) ktok[j] = tok_of(args.row_token, tc.seg0 + r0 + 16 * j);
+          for (int u = 0; u < KPD; ++u)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              ktok[u][j] = u < tc.nkb ? tok_of(args.row_token, tc.seg0 + u * GEMM_BK + r0 + 16 * j) : 0;
         }
         // varlen-K A gather of a missing half: read column 0 (finite, never stored)
         const int acol0 = (Tr::a_gather && tc.valid) ? tc.mt * GEMM_BM : 0;
-        for (int kb = 0; kb < tc.nkb; ++kb) {
+        // varlen-K: the k-block loop is unrolled by KPD so that ring slot u is a compile-time
+        // register set: slot u is consumed for k-block kb and refilled for kb + KPD in place.
+        for (int kb0 = 0; kb0 < tc.nkb; kb0 += KU) {
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+          const int kb = kb0 + u;
+          if (kb >= tc.nkb) break;
           const __nv_bfloat16* srcK[4];
           if constexpr (Tr::vk) {
             const int col0 = Tr::a_gather ? acol0 : n0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) srcK[j] = args.gsrc + clamp_tok(ktok[j]) * args.gld + col0 + c * 8;
-            if (kb + 1 < tc.nkb) {
-              const int krow1 = tc.seg0 + (kb + 1) * GEMM_BK;
+            for (int j = 0; j < 4; ++j) srcK[j] = args.gsrc + clamp_tok(ktok[u][j]) * args.gld + col0 + c * 8;
+            if (kb + KPD < tc.nkb) {
+              const int krow1 = tc.seg0 + (kb + KPD) * GEMM_BK;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) ktok[j] = tok_of(args.row_token, krow1 + r0 + 16 * j);
+              for (int j = 0; j < 4; ++j) ktok[u][j] = tok_of(args.row_token, krow1 + r0 + 16 * j);
             }
           }
           ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -436,6 +462,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             stage = 0;
             phase ^= 1;
           }
+        }
         }
       }
     }
@@ -654,6 +681,10 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
 #pragma unroll
             for (int q8 = 0; q8 < 4; ++q8) {
               const uint32_t* v = r + 8 * q8;
+              if constexpr (SONIC_EXP_EPI == 1) {
+                if ((v[0] ^ v[3] ^ v[5] ^ v[7]) == 0x7f7f7f7fu) args.dS[0] = 1.f;
+                continue;
+              }
               ptx::st_shared_v4(b + swz(lane, 4 * h + q8),
                                 ptx::pack_bf16(gate * __uint_as_float(v[0]), gate * __uint_as_float(v[1])),
                                 ptx::pack_bf16(gate * __uint_as_float(v[2]), gate * __uint_as_float(v[3])),

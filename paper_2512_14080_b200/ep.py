@@ -67,10 +67,14 @@ class DistComm:
 
     def alltoallv(self, sends, send_counts, recv_counts):
         (s,), (sc,), (rc,) = sends, send_counts, recv_counts
-        out = torch.empty((sum(rc),) + tuple(s.shape[1:]), dtype=s.dtype, device=s.device)
-        self.dist.all_to_all_single(out, s[: sum(sc)].contiguous(), output_split_sizes=rc, input_split_sizes=sc,
-                                    group=self.group)
-        return [out]
+        # gloo (CPU plumbing tests; several ranks sharing one GPU in the tests) exchanges host tensors
+        stage = s.is_cuda and self.dist.get_backend(self.group) != "nccl"
+        src = s[: sum(sc)].contiguous()
+        if stage:
+            src = src.cpu()
+        out = torch.empty((sum(rc),) + tuple(s.shape[1:]), dtype=s.dtype, device=src.device)
+        self.dist.all_to_all_single(out, src, output_split_sizes=rc, input_split_sizes=sc, group=self.group)
+        return [out.to(s.device) if stage else out]
 
 
 # ------------------------------------------------------------------------------- one rank

@@ -60,18 +60,19 @@ def main():
             d = dict(zip(hdr, r))
             if d.get("Metric Name") == "gpu__time_duration.sum":
                 recs.append((d["Kernel Name"], float(d["Metric Value"].replace(",", "")), d["Metric Unit"]))
+    recs = [r for r in recs if "sonic" in r[0]]  # our kernels (drop torch's input generation)
     step = recs[len(recs) // 2:]  # second (timed) step
     tot = sum(v for _, v, _ in step)
     with open(os.path.join(ROOT, "profiles", f"launches_{tag}.csv"), "w") as f:
         w = csv.writer(f)
         w.writerow(["kernel", "duration_ns", "share_of_step"])
         for k, v, u in step:
-            ns = v * (1000 if u == "usecond" else 1)
+            ns = v * (1000 if u in ("usecond", "us") else 1)
             w.writerow([k[:90], f"{ns:.0f}", f"{v / tot:.4f}"])
     lines += ["## Launch list of one step (ncu gpu__time_duration, serialised)", "",
               "| kernel | µs | share |", "|---|---|---|"]
     for k, v, u in step:
-        us = v / 1000 if u == "nsecond" else v
+        us = v / 1000 if u in ("nsecond", "ns") else v
         lines.append(f"| `{k[:70]}` | {us:.1f} | {v / tot:.3f} |")
     lines.append("")
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
@@ -90,7 +91,7 @@ def main():
         lines.append("")
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     open(os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.md"), "w").write("\n".join(lines) + "\n")
-    print("\n".join(lines))
+    print(f"wrote profiles/ncu_summary_{tag}.md")
 
 
 if __name__ == "__main__":
