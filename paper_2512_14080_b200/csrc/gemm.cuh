@@ -57,6 +57,7 @@ struct GemmArgs {
   int M_dim, N_dim;         // output extent along M (varlen-K) and N
   float* dS;                // DH: dS [rows] if n_tiles == 1, else partials [n_tiles][rows_max]
   long long rows_max;
+  __nv_bfloat16* out;       // DOWN / DXT: the output rows [rows_max, N_dim] (direct-store epilogue)
 };
 
 template <int KIND>
@@ -93,7 +94,7 @@ constexpr int STG_BYTES = 4096;  // one epilogue staging buffer: 32 rows x 128 B
 #endif
 constexpr int SMEM_LIMIT = SONIC_SMEM_LIMIT;
 
-template <int BN, bool CTA2, bool HTMA, int NB_>
+template <int BN, bool CTA2, bool HTMA, int NB_, bool HRING_ = false>
 struct GemmCfg {
   static constexpr int BNL = CTA2 ? BN / 2 : BN;  // B columns (or rows) held by this CTA
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
@@ -102,7 +103,10 @@ struct GemmCfg {
   static constexpr int NB = NB_;  // epilogue staging buffers per epilogue warp (ring)
   // DH only: per-epilogue-warp H buffer, 32 rows x (gate + up) bf16 columns of the warp's chunks
   static constexpr int HCOLS_WARP = (BN / EPI_HALVES) < 64 ? 64 : BN / EPI_HALVES;
-  static constexpr int HBUF_WARP = HTMA ? 32 * 2 * HCOLS_WARP * 2 : 0;
+  // HRING (DH, BN = 256): instead of the whole tile row, a 2-slot ring of 64-column chunks
+  // (gate 4 KB + up 4 KB per slot) streams H through each epilogue warp
+  static constexpr bool HRING = HRING_;
+  static constexpr int HBUF_WARP = HRING ? 2 * 2 * STG_BYTES : HTMA ? 32 * 2 * HCOLS_WARP * 2 : 0;
   // + 1 KB alignment slack + barriers / dS exchange / TMEM address (< 1 KB)
   static constexpr int FIXED = EPI_WARPS * NB * STG_BYTES + EPI_WARPS * HBUF_WARP + 1024 + 1024;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - FIXED) / (int)STAGE_BYTES;
@@ -116,7 +120,7 @@ struct GemmCfg {
 // TMA load of H in the dH epilogue").  Staging ring depth NB: 2 (a deeper ring costs a mainloop
 // stage, measured slower).
 template <int KIND, int BN, bool CTA2>
-using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128, 2>;
+using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128, 2, KIND == K_DH && BN == 256>;
 
 struct TileCoord {
   int e, row0, nt, mt, nkb, seg0;
@@ -256,7 +260,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
                       const __grid_constant__ CUtensorMap mD, const GemmArgs args) {
   using Tr = Traits<KIND>;
   using Cfg = KCfg<KIND, BN, CTA2>;
-  constexpr bool HTMA = Cfg::HBUF_WARP > 0;
+  constexpr bool HRING = Cfg::HRING;
+  constexpr bool HTMA = Cfg::HBUF_WARP > 0 && !HRING;
   constexpr int NP = num_producer_warps<KIND>();
   constexpr bool GATHER = NP > 1;
   constexpr int STAGES = Cfg::STAGES;
@@ -275,8 +280,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* hfull = tempty + 2;  // one per epilogue warp
-  float* ds_xchg = reinterpret_cast<float*>(hfull + EPI_WARPS);  // DH: [4][32] partial dS of half 1
+  uint64_t* hfull = tempty + 2;  // DH: one per epilogue warp (HRING: two, one per ring slot)
+  float* ds_xchg = reinterpret_cast<float*>(hfull + 2 * EPI_WARPS);  // DH: [4][32] partial dS of half 1
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ds_xchg + 128);
 
   const int warp = threadIdx.x >> 5;
@@ -298,7 +303,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], CTA2 ? 2 * EPI_WARPS : EPI_WARPS);
     }
-    for (int s = 0; s < EPI_WARPS; ++s) ptx::mbar_init(&hfull[s], 1);
+    for (int s = 0; s < 2 * EPI_WARPS; ++s) ptx::mbar_init(&hfull[s], 1);
     ptx::fence_barrier_init();
     ptx::prefetch_tmap(&mA);
     ptx::prefetch_tmap(&mB);
@@ -573,6 +578,44 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     if constexpr (HTMA) {
       if (t_first < total_tiles) h_issue(t_first);
     }
+    // HRING (DH, BN = 256): chunk c of a tile = H columns [64c, 64c + 64) of gate and of up, for
+    // this warp's 32 rows.  Chunks are loaded two ahead, in (tile, chunk) order, into the slot the
+    // consumer has just released; a slot is released once the dH stores out of it have read it.
+    constexpr int HR_NCH = BN / 64;
+    int hr_tile = t_first, hr_c = 0, hr_slot = 0;
+    uint32_t hr_phase = 0;  // bit s: parity of slot s
+    auto hr_load = [&](int slot) {
+      if constexpr (HRING) {
+        if (hr_tile >= total_tiles) return;
+        if (lane == 0) {
+          const TileCoord th = decode_tile<KIND, CTA2>(args, hr_tile, rank);
+          uint64_t* b = &hfull[2 * ew + slot];
+          uint8_t* dst = hb + slot * 2 * STG_BYTES;
+          if (th.valid) {
+            ptx::mbar_arrive_expect_tx(b, 2 * STG_BYTES);
+            ptx::tma_load_2d(dst, &mD, b, th.nt * BN + 64 * hr_c, th.row0 + 32 * q);
+            ptx::tma_load_2d(dst + STG_BYTES, &mD, b, args.n + th.nt * BN + 64 * hr_c, th.row0 + 32 * q);
+          } else {
+            ptx::mbar_arrive(b);  // missing half of a pair: an empty chunk keeps the ring in step
+          }
+        }
+        if (++hr_c == HR_NCH) {
+          hr_c = 0;
+          hr_tile += t_step;
+        }
+      }
+    };
+    auto hr_wait = [&]() -> int {
+      const int sl = hr_slot;
+      ptx::mbar_wait(&hfull[2 * ew + sl], (hr_phase >> sl) & 1u);
+      hr_phase ^= 1u << sl;
+      hr_slot ^= 1;
+      return sl;
+    };
+    if constexpr (HRING) {
+      hr_load(0);
+      hr_load(1);
+    }
     for (int tile = t_first; tile < total_tiles; tile += t_step) {
       const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
       const int wrow = tc.row0 + 32 * q;  // first grouped row of this warp's slab
@@ -590,6 +633,9 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
 #endif
       if (!tc.valid || no_epi) {
         // missing half of a pair: nothing to store (keep the H-buffer protocol going)
+        if constexpr (HRING) {
+          for (int c = 0; c < HR_NCH; ++c) hr_load(hr_wait());
+        }
         if constexpr (HTMA) {
           ptx::mbar_wait(&hfull[ew], hphase);
           hphase ^= 1;
@@ -665,6 +711,33 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           write_row_bf16(sq.addr(i), lane, a);
           sq.issue(lane, i, &mC1, 0, wrow);  // columns >= n are clipped by the tensor map
         }
+      } else if constexpr ((KIND == K_DOWN || KIND == K_DXT) && (SONIC_EXP_EPI == 4 || SONIC_EXP_EPI == 5)) {
+        // experiment: registers -> global directly (no SMEM staging); lane = row
+        float gate = 1.f;
+        if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
+        __nv_bfloat16* orow = args.out + (size_t)row * args.N_dim + tc.nt * BN;
+#pragma unroll 1
+        for (int c = 64 * half; c < BN; c += 64 * EPI_HALVES) {
+          if (tc.nt * BN + c >= args.N_dim) break;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t r[32];
+            ptx::tmem_ld32(t_acc + c + 32 * h, r);
+            ptx::tmem_ld_wait();
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              pk[i] = ptx::pack_bf16(gate * __uint_as_float(r[2 * i]), gate * __uint_as_float(r[2 * i + 1]));
+            if constexpr (SONIC_EXP_EPI == 4) {
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4)
+                ptx::st_global_v4(orow + c + 32 * h + 8 * q4, pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
+            } else {
+              ptx::st_global_v8(orow + c + 32 * h, pk);
+              ptx::st_global_v8(orow + c + 32 * h + 16, pk + 8);
+            }
+          }
+        }
       } else if constexpr (KIND == K_DOWN || KIND == K_DXT) {
         float gate = 1.f;
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
@@ -698,7 +771,72 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         const float s = __ldg(args.row_gate + row);
         const int n = args.n;
         float ds = 0.f;
-        if constexpr (BN >= 64) {
+        if constexpr (HRING) {
+#pragma unroll 1
+          for (int c = 0; c < HR_NCH; ++c) {
+            const int sl = hr_wait();
+            const int col = tc.nt * BN + 64 * c;
+            uint8_t* gbp = hb + sl * 2 * STG_BYTES;
+            const uint32_t gb = ptx::smem_u32(gbp);  // H gate -> dH gate (in place)
+            const uint32_t ub = gb + STG_BYTES;      // H up   -> dH up
+            const uint32_t ab = sq.addr(c & 1);      // A' staging (its store of chunk c-2 has read it)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t r[32];
+              ptx::tmem_ld32(t_acc + 64 * c + 32 * h, r);
+              uint4 hg4[4], hu4[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                hg4[i] = ptx::ld_shared_v4(gb + swz(lane, 4 * h + i));
+                hu4[i] = ptx::ld_shared_v4(ub + swz(lane, 4 * h + i));
+              }
+              ptx::tmem_ld_wait();
+              const __nv_bfloat16* hgp = reinterpret_cast<const __nv_bfloat16*>(hg4);
+              const __nv_bfloat16* hup = reinterpret_cast<const __nv_bfloat16*>(hu4);
+#pragma unroll
+              for (int q8 = 0; q8 < 4; ++q8) {
+                uint32_t pg[4], pu[4], pa[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  float dg2[2], du2[2], ap2[2];
+#pragma unroll
+                  for (int k = 0; k < 2; ++k) {
+                    const int j = 8 * q8 + 2 * i + k;
+                    const float dap = __uint_as_float(r[j]);
+                    const float gg = __bfloat162float(hgp[j]);
+                    const float uu = __bfloat162float(hup[j]);
+                    const float sg = sigmoidf_fast(gg);
+                    const float sl_ = gg * sg;
+                    const float A = sl_ * uu;
+                    const float dA = s * dap;
+                    dg2[k] = dA * uu * sg * fmaf(gg, 1.f - sg, 1.f);
+                    du2[k] = dA * sl_;
+                    ap2[k] = s * A;
+                    ds = fmaf(dap, A, ds);
+                  }
+                  pg[i] = ptx::pack_bf16(dg2[0], dg2[1]);
+                  pu[i] = ptx::pack_bf16(du2[0], du2[1]);
+                  pa[i] = ptx::pack_bf16(ap2[0], ap2[1]);
+                }
+                ptx::st_shared_v4(gb + swz(lane, 4 * h + q8), pg[0], pg[1], pg[2], pg[3]);
+                ptx::st_shared_v4(ub + swz(lane, 4 * h + q8), pu[0], pu[1], pu[2], pu[3]);
+                ptx::st_shared_v4(ab + swz(lane, 4 * h + q8), pa[0], pa[1], pa[2], pa[3]);
+              }
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&mC0, gbp, col, wrow);                    // dH gate
+              ptx::tma_store_2d(&mC0, gbp + STG_BYTES, n + col, wrow);    // dH up
+              ptx::bulk_commit();
+              ptx::tma_store_2d(&mC1, sq.base + (c & 1) * STG_BYTES, col, wrow);  // A' = s A
+              ptx::bulk_commit();
+              ptx::bulk_wait_read<1>();  // the dH stores have read the slot
+            }
+            __syncwarp();
+            hr_load(sl);
+          }
+        } else if constexpr (BN >= 64) {
           ptx::mbar_wait(&hfull[ew], hphase);
           hphase ^= 1;
 #pragma unroll 1

@@ -181,8 +181,7 @@ bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUten
   if (cta2) grid &= ~1;
   switch (BN) {
     case 256:
-      if constexpr (KIND == K_DH) return false;
-      else return cta2 ? launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st)
+      return cta2 ? launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st)
                        : launch_gemm_t<KIND, 256, false>(a, b, c0, c1, d, args, grid, st);
     case 128:
       return cta2 ? launch_gemm_t<KIND, 128, true>(a, b, c0, c1, d, args, grid, st)
@@ -262,7 +261,7 @@ RouteWs route_ws(const sonic_moe_desc* D) {
 }
 
 #ifndef SONIC_DH_MAX_BN
-#define SONIC_DH_MAX_BN 128  // BN <= 128 leaves room for the TMA-loaded H buffers (gemm.cuh KCfg)
+#define SONIC_DH_MAX_BN 256  // BN = 256 streams H through a chunk ring (gemm.cuh HRING)
 #endif
 int dh_bn(int n) {
   return (n % 256 == 0 && SONIC_DH_MAX_BN >= 256) ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
@@ -464,6 +463,7 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = d / BN; a.k_blocks = (n + 63) / 64; a.N_dim = d;
+    a.out = static_cast<__nv_bfloat16*>(Ybuf);
     ProfScope ps("down", st);
     if (!launch_gemm<K_DOWN>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
   }
@@ -548,6 +548,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       !map2d(&mC6, dXt, false, R, d, 64, 32))
     return SONIC_ERR_CUDA;
   a6.n_tiles = d / BN6; a6.k_blocks = (2 * n) / 64; a6.N_dim = d;
+  a6.out = static_cast<__nv_bfloat16*>(dXt);
   // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
   if (!map2d(&mA5, Ap, false, R, n, 64, 64) || !map2d(&mB5, dO, false, s.T, d, 64, 1) ||
       !map3d(&mC5, dW2, true, E, n, d, 32, 32))
