@@ -39,16 +39,22 @@ __global__ void __launch_bounds__(256) k_aggregate(const __nv_bfloat16* __restri
   for (int c = lane; c < nch; c += 32) {
     float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     int j = r0;
-    for (; j + 4 <= r1; j += 4) {
-      const int q0 = __ldg(rows + j), q1 = __ldg(rows + j + 1), q2 = __ldg(rows + j + 2), q3 = __ldg(rows + j + 3);
-      const uint4 v0 = ldg_stream(Yv + (long long)q0 * nch + c);
-      const uint4 v1 = ldg_stream(Yv + (long long)q1 * nch + c);
-      const uint4 v2 = ldg_stream(Yv + (long long)q2 * nch + c);
-      const uint4 v3 = ldg_stream(Yv + (long long)q3 * nch + c);
-      acc8(a, v0);
-      acc8(a, v1);
-      acc8(a, v2);
-      acc8(a, v3);
+#ifndef SONIC_AGG_U
+#define SONIC_AGG_U 4  // row loads in flight per lane
+#endif
+    for (; j + SONIC_AGG_U <= r1; j += SONIC_AGG_U) {
+      uint4 v[SONIC_AGG_U];
+#pragma unroll
+      for (int u = 0; u < SONIC_AGG_U; ++u) {
+#ifdef SONIC_EXP_AGG_SEQ  // ablation: sequential rows instead of the token's gathered rows
+        const long long q = j + u;
+#else
+        const long long q = __ldg(rows + j + u);
+#endif
+        v[u] = ldg_stream(Yv + q * nch + c);
+      }
+#pragma unroll
+      for (int u = 0; u < SONIC_AGG_U; ++u) acc8(a, v[u]);
     }
     for (; j < r1; ++j) acc8(a, ldg_stream(Yv + (long long)__ldg(rows + j) * nch + c));
     uint4 o;
@@ -56,6 +62,66 @@ __global__ void __launch_bounds__(256) k_aggregate(const __nv_bfloat16* __restri
 #pragma unroll
     for (int i = 0; i < 4; ++i) oh[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
     Ov[c] = o;
+  }
+}
+
+__device__ __forceinline__ void ldg_stream8(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void acc16(float (&a)[16], const uint32_t (&v)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[i]));
+    a[2 * i] += f.x;
+    a[2 * i + 1] += f.y;
+  }
+}
+
+// 32-byte variant: one warp per token, lane = 32-byte column chunk (16 bf16 columns); the row ids
+// of the token are held one per lane and broadcast by shuffle; up to 8 row loads in flight per
+// lane.  Same summation order as k_aggregate (CSR order, fp32), so identical results.
+__global__ void __launch_bounds__(256) k_aggregate32(const __nv_bfloat16* __restrict__ Y,
+                                                     const int* __restrict__ rowptr, const int* __restrict__ rows,
+                                                     __nv_bfloat16* __restrict__ out, long long T, int d) {
+  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const int r0 = __ldg(rowptr + t), r1 = __ldg(rowptr + t + 1);
+  const int nch = d >> 4;  // 32-byte chunks per row
+  const char* Yb = reinterpret_cast<const char*>(Y);
+  for (int c = lane; c - lane < nch; c += 32) {
+    const bool act = c < nch;
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = 0.f;
+    for (int b0 = r0; b0 < r1; b0 += 32) {  // row ids in batches of 32 (one per lane)
+      const int nb = min(32, r1 - b0);
+      const int myrow = lane < nb ? __ldg(rows + b0 + lane) : 0;
+      for (int j0 = 0; j0 < nb; j0 += 8) {
+        uint32_t v[8][8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int q = __shfl_sync(0xffffffffu, myrow, (j0 + u) & 31);
+          if (act && j0 + u < nb) ldg_stream8(Yb + ((long long)q * d + 16 * c) * 2, v[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (act && j0 + u < nb) acc16(a, v[u]);
+      }
+    }
+    if (act) {
+      uint32_t o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+        o[i] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out + t * d + 16 * c), "r"(o[0]),
+                   "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
+                   : "memory");
+    }
   }
 }
 
@@ -73,7 +139,13 @@ void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows
                       int d, cudaStream_t st) {
   const int threads = 256;
   const long long blocks = (T * 32 + threads - 1) / threads;
-  k_aggregate<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
+#ifndef SONIC_AGG32
+#define SONIC_AGG32 0  // 32-byte variant measured slower at 7B (180 vs 157 us)
+#endif
+  if (SONIC_AGG32 && d % 16 == 0)
+    k_aggregate32<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
+  else
+    k_aggregate<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
 }
 
 void launch_ds_reduce(const float* part, int nparts, long long rows_max, const int* num_tiles, float* dS,

@@ -173,7 +173,16 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, in
 #ifndef SONIC_KPD
 #define SONIC_KPD 4
 #endif
+// L2 prefetch distance (k-blocks) for the gathered rows (0 = off): the producers touch the lines
+// of k-block kb + SONIC_L2PF while filling kb, so the cp.async of a later stage hits L2
+#ifndef SONIC_L2PF
+#define SONIC_L2PF 0
+#endif
+#ifdef SONIC_EXP_NOGATHER  // ablation (7B only): contiguous rows instead of the gather map
+__device__ __forceinline__ int tok_of(const int* row_token, int r) { return r & 32767; }
+#else
 __device__ __forceinline__ int tok_of(const int* row_token, int r) { return __ldg(row_token + r); }
+#endif
 __device__ __forceinline__ size_t clamp_tok(int t) { return (size_t)max(t, 0); }
 
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
@@ -407,6 +416,15 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             const int col0 = Tr::a_gather ? acol0 : n0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) srcK[j] = args.gsrc + clamp_tok(ktok[u][j]) * args.gld + col0 + c * 8;
+            if constexpr (SONIC_L2PF > 0) {
+              static_assert(SONIC_L2PF < KPD, "L2 prefetch reads the index ring");
+              constexpr int NPF = Tr::a_gather ? 2 : BNL / 64;  // 128-byte lines per gathered row
+              if (c < NPF && kb + SONIC_L2PF < tc.nkb) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  ptx::prefetch_l2(args.gsrc + clamp_tok(ktok[(u + SONIC_L2PF) % KPD][j]) * args.gld + col0 + 64 * c);
+              }
+            }
             if (kb + KPD < tc.nkb) {
               const int krow1 = tc.seg0 + (kb + KPD) * GEMM_BK;
 #pragma unroll
@@ -451,6 +469,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             }
           }
           if constexpr (!Tr::vk) {  // A: 128 gathered rows x 64 K (K-major)
+            if constexpr (SONIC_L2PF > 0) {
+              if (c == 0 && kb + SONIC_L2PF < tc.nkb) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) ptx::prefetch_l2(srcM[j] + (kb + SONIC_L2PF) * GEMM_BK);
+              }
+            }
             const uint32_t dst = ptx::smem_u32(sA) + r0 * 128 + sw;
 #pragma unroll
             for (int j = 0; j < 8; ++j) ptx::cp_async16(dst + j * 16 * 128, srcM[j] + kb * GEMM_BK);
@@ -981,6 +1005,25 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             args.dS[row] = ds;
           else
             args.dS[(long long)tc.nt * args.rows_max + row] = ds;
+        }
+      } else if constexpr (SONIC_EXP_EPI == 6) {  // experiment: fp32 dW rows straight to global
+        const int m = tc.mt * GEMM_BM + 32 * q + lane;
+        float* wrow_p = reinterpret_cast<float*>(args.out) + ((size_t)tc.e * args.M_dim + m) * args.N_dim + tc.nt * BN;
+        if (m < args.M_dim) {
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            if (tc.nt * BN + c >= args.N_dim) break;
+            uint32_t r[32];
+            if (tc.nkb > 0) {
+              ptx::tmem_ld32(t_acc + c, r);
+              ptx::tmem_ld_wait();
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) r[i] = 0u;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) ptx::st_global_v8(wrow_p + c + 8 * i, r + 8 * i);
+          }
         }
       } else {  // K_DW2 / K_DW1: fp32 weight gradient tile [128 x BN] of expert e
         const int m0 = tc.mt * GEMM_BM + 32 * q;

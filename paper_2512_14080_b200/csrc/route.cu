@@ -332,16 +332,15 @@ __global__ void k_orphans(const uint32_t* __restrict__ bm_kept, int T, int E, in
 // ---------------------------------------------------------------- offsets & tiles
 // Also builds the 2-CTA schedule: each expert's 128-row tiles are paired (t, t+1); an expert with
 // an odd tile count ends with a half pair (bit 31 clear).
-__global__ void __launch_bounds__(1024) k_offsets(const int* __restrict__ f_r, int E, int* __restrict__ offsets,
-                                                  int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
-                                                  int* __restrict__ num_tiles, int* __restrict__ tile_pairs,
-                                                  int* __restrict__ num_pairs) {
+__device__ void offsets_block(const int* __restrict__ f_r, int E, int* __restrict__ offsets,
+                              int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
+                              int* __restrict__ num_tiles, int* __restrict__ tile_pairs, int* __restrict__ num_pairs) {
   __shared__ int s_pad[4097];
   __shared__ int s_pp[4097];
   int base = 0, pbase = 0, ppbase = 0;
   for (int e0 = 0; e0 < E; e0 += blockDim.x) {
     const int e = e0 + threadIdx.x;
-    const int c = e < E ? f_r[e] : 0;
+    const int c = e < E ? __ldcg(f_r + e) : 0;
     const int pc = (c + GEMM_M - 1) / GEMM_M * GEMM_M;
     const int pp = (pc / GEMM_M + 1) / 2;
     int tot, ptot, pptot;
@@ -391,6 +390,46 @@ __global__ void __launch_bounds__(1024) k_offsets(const int* __restrict__ f_r, i
 }
 
 // ---------------------------------------------------------------- gather map
+__global__ void __launch_bounds__(1024) k_offsets(const int* __restrict__ f_r, int E, int* __restrict__ offsets,
+                                                  int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
+                                                  int* __restrict__ num_tiles, int* __restrict__ tile_pairs,
+                                                  int* __restrict__ num_pairs) {
+  offsets_block(f_r, E, offsets, pad_offsets, tile_expert, num_tiles, tile_pairs, num_pairs);
+}
+
+// Per-expert popcount + word prefix (one block per expert, as k_expert_popc); the last block to
+// finish (ticket) then builds offsets / tiles / pairs from the counts (k_offsets' work) -- one
+// launch instead of two.  cnt2 (if given) receives a copy of the counts; the offsets use cnt2 if
+// given, else cnt.
+__global__ void __launch_bounds__(1024) k_popc_offsets(const uint32_t* __restrict__ bm, int W, int* __restrict__ wprefix,
+                                                       int* __restrict__ cnt, int* __restrict__ cnt2,
+                                                       unsigned* __restrict__ ticket, int* __restrict__ offsets,
+                                                       int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
+                                                       int* __restrict__ num_tiles, int* __restrict__ tile_pairs,
+                                                       int* __restrict__ num_pairs) {
+  const int e = blockIdx.x;
+  int base = 0;
+  for (int w0 = 0; w0 < W; w0 += blockDim.x) {
+    const int w = w0 + threadIdx.x;
+    const int c = w < W ? __popc(bm[(size_t)e * W + w]) : 0;
+    int tot;
+    const int ex = block_excl_scan(c, &tot);
+    if (w < W) wprefix[(size_t)e * W + w] = base + ex;
+    base += tot;
+  }
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) {
+    cnt[e] = base;
+    if (cnt2) cnt2[e] = base;
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  offsets_block(cnt2 ? cnt2 : cnt, (int)gridDim.x, offsets, pad_offsets, tile_expert, num_tiles, tile_pairs, num_pairs);
+}
+
 __global__ void k_build_rows(const uint32_t* __restrict__ bm_kept, const int* __restrict__ wprefix, int W,
                              const int* __restrict__ f_r, const int* __restrict__ pad_offsets,
                              int* __restrict__ row_token, float* __restrict__ row_gate) {
@@ -498,8 +537,10 @@ void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st) {
 // ---------------------------------------------------------------- given routing
 // SONIC_ROUTE_GIVEN ("an interface that accepts arbitrary routing input"): S is the gate
 // matrix itself, token t is routed to e iff S[t,e] != 0.  One block per 32-token word.
-__global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W, uint32_t* __restrict__ bm) {
+__global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W, uint32_t* __restrict__ bm,
+                               unsigned* __restrict__ ticket) {
   __shared__ uint32_t words[4096];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
   for (int e = threadIdx.x; e < E; e += blockDim.x) words[e] = 0u;
   __syncthreads();
   for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) {
@@ -511,15 +552,213 @@ __global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W,
   for (int e = threadIdx.x; e < E; e += blockDim.x) bm[(size_t)e * W + blockIdx.x] = words[e];
 }
 
+// ---------------------------------------------------------------- TC top-K, thread per token
+// 128 tokens per block.  Their S rows are staged through shared memory in 128-expert slabs (row
+// stride 129 words: the per-thread column walk is bank-conflict free) and each thread keeps its
+// token's top-KT ordered scores in registers by stable insertion over ascending expert ids: a
+// later expert enters only if strictly greater, so equal scores keep the lower id first -- the
+// (value desc, expert asc) order of P:1099 (Q9), exact on the ordered fp32 bits.
+constexpr int TK_TOK = 128, TK_EC = 128;
+__device__ __forceinline__ float unord_f32(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
+}
+// Four interleaved lists per thread (expert e goes to list e mod 4) give the insertion chains
+// 4-way ILP; the lists are then merged on unique 64-bit keys (ordered score << 32 | ~expert) by
+// bitonic merges, which keep the same total order.
+template <int KP>
+__device__ __forceinline__ void bitonic_merge_desc(unsigned long long (&a)[KP], const unsigned long long (&b)[KP]) {
+#pragma unroll
+  for (int i = 0; i < KP; ++i) a[i] = a[i] > b[KP - 1 - i] ? a[i] : b[KP - 1 - i];
+#pragma unroll
+  for (int d = KP / 2; d >= 1; d >>= 1) {
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      if ((i & d) == 0) {
+        const unsigned long long x = a[i], y = a[i + d];
+        a[i] = x > y ? x : y;
+        a[i + d] = x > y ? y : x;
+      }
+    }
+  }
+}
+template <int KT>
+__global__ void __launch_bounds__(TK_TOK) k_topk_tpt(const float* __restrict__ S, int T, int E, int W,
+                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
+                                                    uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket) {
+  constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;  // list length (pow2)
+  constexpr int NL = 4;
+  extern __shared__ float tk_sm[];  // [TK_TOK][TK_EC + 1] staging, then words [E][4]
+  uint32_t* words = reinterpret_cast<uint32_t*>(tk_sm + TK_TOK * (TK_EC + 1));
+  const int tid = threadIdx.x;
+  const int tok0 = blockIdx.x * TK_TOK;
+  const int ntok = min(TK_TOK, T - tok0);
+  if (blockIdx.x == 0 && tid == 0 && ticket) *ticket = 0u;
+  for (int i = tid; i < E * 4; i += TK_TOK) words[i] = 0u;
+  uint32_t top[NL][KP];
+  int id[NL][KP];
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+#pragma unroll
+    for (int i = 0; i < KP; ++i) {
+      top[l][i] = 0u;
+      id[l][i] = 0;
+    }
+  for (int e0 = 0; e0 < E; e0 += TK_EC) {
+    const int ecn = min(TK_EC, E - e0);
+    __syncthreads();
+    if (ecn == TK_EC && (E & 3) == 0) {  // 16-byte loads: 32 per token row
+#pragma unroll 8
+      for (int i = tid; i < ntok * (TK_EC / 4); i += TK_TOK) {
+        const int tl = i / (TK_EC / 4), c4 = i % (TK_EC / 4);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(S + (size_t)(tok0 + tl) * E + e0) + c4);
+        float* d = tk_sm + tl * (TK_EC + 1) + 4 * c4;
+        d[0] = v.x;
+        d[1] = v.y;
+        d[2] = v.z;
+        d[3] = v.w;
+      }
+    } else {
+      for (int tl = 0; tl < ntok; ++tl)
+        for (int ec = tid; ec < ecn; ec += TK_TOK) tk_sm[tl * (TK_EC + 1) + ec] = __ldg(S + (size_t)(tok0 + tl) * E + e0 + ec);
+    }
+    __syncthreads();
+    if (tid < ntok) {
+      const float* row = tk_sm + tid * (TK_EC + 1);
+      for (int ec = 0; ec < ecn; ec += NL) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const uint32_t v = ec + l < ecn ? ord_f32(row[ec + l]) : 0u;
+          if (v > top[l][KP - 1]) {
+            const int e = e0 + ec + l;
+#pragma unroll
+            for (int i = KP - 1; i > 0; --i) {
+              const bool gi = v > top[l][i], gp = v > top[l][i - 1];
+              top[l][i] = gi ? (gp ? top[l][i - 1] : v) : top[l][i];
+              id[l][i] = gi ? (gp ? id[l][i - 1] : e) : id[l][i];
+            }
+            if (v > top[l][0]) {
+              top[l][0] = v;
+              id[l][0] = e;
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid < ntok) {
+    unsigned long long key[NL][KP];
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+      for (int i = 0; i < KP; ++i)
+        key[l][i] = top[l][i] ? ((unsigned long long)top[l][i] << 32) | (0xFFFFFFFFu - (uint32_t)id[l][i]) : 0ull;
+    bitonic_merge_desc<KP>(key[0], key[1]);
+    bitonic_merge_desc<KP>(key[2], key[3]);
+    bitonic_merge_desc<KP>(key[0], key[2]);
+    const size_t t = (size_t)(tok0 + tid);
+#pragma unroll
+    for (int i = 0; i < KT; ++i) {
+      const int e = (int)(0xFFFFFFFFu - (uint32_t)(key[0][i] & 0xFFFFFFFFull));
+      topk_ids[t * KT + i] = e;
+      topk_s[t * KT + i] = unord_f32((uint32_t)(key[0][i] >> 32));
+      atomicOr(&words[e * 4 + (tid >> 5)], 1u << (tid & 31));
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < E * 4; i += TK_TOK) {
+    const int w = blockIdx.x * 4 + (i & 3);
+    if (w < W) bm_tc[(size_t)(i >> 2) * W + w] = words[i];
+  }
+}
+
+// TC rows in one launch: blocks [0, nb_build) build the gather map (k_build_rows' work, expert
+// e = b / nbw); the rest are one thread per (token, k): the TC token CSR (rowptr = t K, rows in
+// ascending expert order = rank of the expert among the token's K) and the renormalised gate.
+__global__ void k_rows_tc(const uint32_t* __restrict__ bm, const int* __restrict__ wprefix, int W,
+                          const int* __restrict__ f_r, const int* __restrict__ pad_offsets, int* __restrict__ row_token,
+                          float* __restrict__ row_gate, const int* __restrict__ topk_ids,
+                          const float* __restrict__ topk_s, int T, int K, int gate_raw, int* __restrict__ rowptr,
+                          int* __restrict__ token_rows, int nb_build, int nbw) {
+  if ((int)blockIdx.x < nb_build) {
+    const int e = blockIdx.x / nbw;
+    const int wb = blockIdx.x - e * nbw;
+    const int base = pad_offsets[e];
+    const int w = wb * blockDim.x + threadIdx.x;
+    if (w < W) {
+      uint32_t bits = bm[(size_t)e * W + w];
+      int r = base + wprefix[(size_t)e * W + w];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        row_token[r++] = w * 32 + b;
+        bits &= bits - 1;
+      }
+    }
+    if (wb == 0) {  // pad rows of this expert's last tile
+      for (int r = base + f_r[e] + threadIdx.x; r < pad_offsets[e + 1]; r += blockDim.x) {
+        row_token[r] = -1;
+        row_gate[r] = 0.f;
+      }
+    }
+    return;
+  }
+  const long long i = (long long)(blockIdx.x - nb_build) * blockDim.x + threadIdx.x;
+  const long long TK = (long long)T * K;
+  if (i > TK) return;
+  if (i == TK) {
+    rowptr[T] = (int)TK;
+    return;
+  }
+  const int t = (int)(i / K), k = (int)(i - (long long)t * K);
+  if (k == 0) rowptr[t] = t * K;
+  const int* ids = topk_ids + (size_t)t * K;
+  const float* sc = topk_s + (size_t)t * K;
+  const int me = ids[k];
+  const float ms = sc[k];
+  int pos = 0;
+  float sum = 0.f;
+  for (int j = 0; j < K; ++j) {
+    pos += ids[j] < me;
+    sum += sc[j];
+  }
+  const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
+  const int w = t >> 5;
+  const uint32_t below = (1u << (t & 31)) - 1u;
+  const int r = pad_offsets[me] + wprefix[(size_t)me * W + w] + __popc(bm[(size_t)me * W + w] & below);
+  token_rows[(size_t)t * K + pos] = r;
+  row_gate[r] = gate_raw ? ms : ms * inv;
+}
+
+template <int KT>
+void launch_topk_tpt(const RouteLaunch& L, cudaStream_t st) {
+  const int T = (int)L.T, E = L.E, W = L.W;
+  const int smem = (TK_TOK * (TK_EC + 1) + E * 4) * 4;
+  static int attr = 0;
+  if (attr < smem) {
+    cudaFuncSetAttribute(k_topk_tpt<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = smem;
+  }
+  k_topk_tpt<KT><<<(T + TK_TOK - 1) / TK_TOK, TK_TOK, smem, st>>>(L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc,
+                                                                 L.ticket);
+}
+void launch_topk_tpt_k(const RouteLaunch& L, cudaStream_t st) {
+  switch (L.K) {
+#define TKC(k) case k: launch_topk_tpt<k>(L, st); break;
+    TKC(1) TKC(2) TKC(3) TKC(4) TKC(5) TKC(6) TKC(7) TKC(8)
+    TKC(9) TKC(10) TKC(11) TKC(12) TKC(13) TKC(14) TKC(15) TKC(16)
+#undef TKC
+    default: break;
+  }
+}
+
 // ---------------------------------------------------------------- launcher
 int launch_route(const RouteLaunch& L, cudaStream_t st) {
   int nl = 0;
   const int T = (int)L.T, E = L.E, K = L.K, W = L.W;
   if (L.mode == 2) {  // given routing: bitmap, counts, offsets, rows, CSR with raw gates
-    k_given_bitmap<<<W, 256, 0, st>>>(L.S, T, E, W, L.bm_tc); ++nl;
-    k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, L.wprefix, L.f, L.f_r); ++nl;
-    k_offsets<<<1, 1024, 0, st>>>(L.f_r, E, L.offsets, L.pad_offsets, L.tile_expert, L.num_tiles, L.tile_pairs,
-                                  L.num_pairs); ++nl;
+    k_given_bitmap<<<W, 256, 0, st>>>(L.S, T, E, W, L.bm_tc, L.ticket); ++nl;
+    k_popc_offsets<<<E, 1024, 0, st>>>(L.bm_tc, W, L.wprefix, L.f, L.f_r, L.ticket, L.offsets, L.pad_offsets,
+                                       L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
     k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(L.bm_tc, L.wprefix, W, L.f_r, L.pad_offsets,
                                                            L.row_token, L.row_gate); ++nl;
     k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_tc, T, E, W, L.tokcnt); ++nl;
@@ -528,7 +767,14 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
                                                        L.token_rowptr, L.S, 1, L.token_rows, L.row_gate); ++nl;
     return nl;
   }
-  {
+#ifndef SONIC_TOPK_TPT
+#define SONIC_TOPK_TPT 1
+#endif
+  if (SONIC_TOPK_TPT && K <= 16 && E <= 4096) {
+    launch_topk_tpt_k(L, st);
+    ++nl;
+  } else {
+    cudaMemsetAsync(L.ticket, 0, 4, st);
 #define TOPK_CASE(G, V) \
   k_route_topk<G, V><<<W, 32 * G, 0, st>>>(L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
     if (E <= 32) TOPK_CASE(4, 8);
@@ -554,19 +800,23 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
       k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1); ++nl;
     }
     bm_kept = L.bm_kept;
-    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r, nullptr); ++nl;
-  } else {  // TC: one pass gives f, f_r (== f) and the word prefixes
-    k_expert_popc<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f, L.f_r); ++nl;
+    k_popc_offsets<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r, nullptr, L.ticket, L.offsets, L.pad_offsets,
+                                       L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
+  } else {  // TC: one pass gives f, f_r (== f), the word prefixes and the offsets
+    k_popc_offsets<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f, L.f_r, L.ticket, L.offsets, L.pad_offsets,
+                                       L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
   }
-  k_offsets<<<1, 1024, 0, st>>>(L.f_r, E, L.offsets, L.pad_offsets, L.tile_expert, L.num_tiles, L.tile_pairs,
-                                L.num_pairs); ++nl;
-  k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
-                                                         L.row_gate); ++nl;
   if (L.mode == 0) {
-    k_token_rows_tc<<<(T + 1 + 63) / 64, 64, 0, st>>>(L.topk_ids, L.topk_s, bm_kept, L.wprefix, T, K, W,
-                                                         L.pad_offsets, L.gate_raw, L.token_rowptr, L.token_rows,
-                                                         L.row_gate); ++nl;
+    const int nbw = (W + 255) / 256;
+    const int nb_build = nbw * E;
+    const long long tk = (long long)T * K + 1;
+    const int nb_tok = (int)((tk + 255) / 256);
+    k_rows_tc<<<nb_build + nb_tok, 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
+                                                 L.row_gate, L.topk_ids, L.topk_s, T, K, L.gate_raw,
+                                                 L.token_rowptr, L.token_rows, nb_build, nbw); ++nl;
   } else {
+    k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets,
+                                                           L.row_token, L.row_gate); ++nl;
     k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, T, E, W, L.tokcnt); ++nl;
     k_scan_tokens<<<1, 1024, 0, st>>>(L.tokcnt, T, L.token_rowptr); ++nl;
     k_token_rows<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, L.wprefix, T, E, W, L.pad_offsets, L.tile_expert,

@@ -243,7 +243,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 // route workspace layout
 struct RouteWs {
-  size_t bm_tc, bm_kept, wprefix, tokcnt, flip, ST, total;
+  size_t bm_tc, bm_kept, wprefix, tokcnt, flip, ticket, ST, total;
 };
 RouteWs route_ws(const sonic_moe_desc* D) {
   const Shape s = shape_of(D);
@@ -255,6 +255,7 @@ RouteWs route_ws(const sonic_moe_desc* D) {
   w.wprefix = o; o += bm;
   w.tokcnt = o; o += al((size_t)s.T * 4);
   w.flip = o; o += al((size_t)s.E * 4);
+  w.ticket = o; o += al(4);
   w.ST = o; o += (D->route_mode == SONIC_ROUTE_TR_NRF) ? al((size_t)s.T * s.E * 4) : 0;
   w.total = o;
   return w;
@@ -409,6 +410,7 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   L.wprefix = reinterpret_cast<int*>(base + w.wprefix);
   L.tokcnt = reinterpret_cast<int*>(base + w.tokcnt);
   L.flip = reinterpret_cast<int*>(base + w.flip);
+  L.ticket = reinterpret_cast<unsigned*>(base + w.ticket);
   L.ST = reinterpret_cast<float*>(base + w.ST);
   {
     ProfScope ps("route", static_cast<cudaStream_t>(stream));
@@ -555,6 +557,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     return SONIC_ERR_CUDA;
   a5.n_tiles = d / BN5; a5.m_tiles = (n + 127) / 128; a5.M_dim = n; a5.N_dim = d;
   a5.gsrc = static_cast<const __nv_bfloat16*>(dO); a5.gld = d;
+  a5.out = reinterpret_cast<__nv_bfloat16*>(dW2);
   const int tiles5 = E * a5.m_tiles * a5.n_tiles;
   // K7 dW1_e = Gather(X)^T dH_e   (varlen-K)
   if (!map2d(&mA7, X, false, s.T, d, 64, 1) || !map2d(&mB7, dH, false, R, 2 * n, 64, 64) ||
@@ -562,6 +565,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     return SONIC_ERR_CUDA;
   a7.n_tiles = (2 * n) / BN7; a7.m_tiles = (d + 127) / 128; a7.M_dim = d; a7.N_dim = 2 * n;
   a7.gsrc = static_cast<const __nv_bfloat16*>(X); a7.gld = d;
+  a7.out = reinterpret_cast<__nv_bfloat16*>(dW1);
   const int tiles7 = E * a7.m_tiles * a7.n_tiles;
 
   auto run_dxt = [&]() {

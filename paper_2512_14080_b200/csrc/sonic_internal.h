@@ -19,6 +19,7 @@ struct RouteLaunch {
   // workspace
   uint32_t *bm_tc, *bm_kept;
   int *wprefix, *tokcnt, *flip;
+  unsigned* ticket;  // last-block-done counter (zeroed by the first route kernel)
   float* ST;
 };
 
