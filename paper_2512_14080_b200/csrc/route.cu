@@ -245,12 +245,19 @@ __global__ void __launch_bounds__(1024) k_tr_select(const float* __restrict__ ST
     const int sh = shifts[p], nb = 1 << bits[p];
     for (int i = tid; i < nb; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (int t = tid; t < T; t += blockDim.x) {
-      const bool is_tc = (tcw[t >> 5] >> (t & 31)) & 1u;
-      if (is_tc != up) {
-        const uint32_t o = ord_f32(col[t]);
-        if ((o & pmask) == prefix) atomicAdd(&hist[(o >> sh) & (nb - 1)], 1);
+    for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+      const int t = t0 + tid;
+      bool act = false;
+      uint32_t bin = 0;
+      if (t < T) {
+        const bool is_tc = (tcw[t >> 5] >> (t & 31)) & 1u;
+        if (is_tc != up) {
+          const uint32_t o = ord_f32(col[t]);
+          act = (o & pmask) == prefix;
+          bin = (o >> sh) & (nb - 1);
+        }
       }
+      if (act) atomicAdd(&hist[bin], 1);
     }
     __syncthreads();
     if (tid < 32) {  // find the digit holding the k-th largest, scanning bins from the top
@@ -311,6 +318,131 @@ __global__ void __launch_bounds__(1024) k_tr_select(const float* __restrict__ ST
     __syncthreads();
     if (tid == 0) s_run = run + tot;
     __syncthreads();
+  }
+}
+
+// Word-per-thread variant: thread i owns bitmap words i, i + 1024, ...; the 32 scores of a word
+// are loaded as 8 x 16 B (one latency per word per pass), the histogram adds come from
+// registers, and the final tie pass is one block scan of per-thread equal counts instead of one
+// scan per 1024 tokens.  Same result as k_tr_select (ties at the threshold: lowest tokens first).
+__device__ __forceinline__ void load_word_keys(const float* __restrict__ col, int T, int w, uint32_t (&o)[32]) {
+  const int t0 = w * 32;
+  if (t0 + 32 <= T && (reinterpret_cast<uintptr_t>(col + t0) & 15) == 0) {
+    const float4* p = reinterpret_cast<const float4*>(col + t0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 v = __ldg(p + i);
+      o[4 * i] = ord_f32(v.x);
+      o[4 * i + 1] = ord_f32(v.y);
+      o[4 * i + 2] = ord_f32(v.z);
+      o[4 * i + 3] = ord_f32(v.w);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = t0 + i < T ? ord_f32(__ldg(col + t0 + i)) : 0u;
+  }
+}
+__global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ ST, int T, int W, int M,
+                                                      const uint32_t* __restrict__ bm_tc,
+                                                      uint32_t* __restrict__ bm_kept, const int* __restrict__ f,
+                                                      int* __restrict__ f_r, const int* __restrict__ flip,
+                                                      int rescue) {
+  __shared__ int hist[4096];
+  __shared__ int s_digit, s_above;
+  const int e = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int fc = f[e];
+  int fr;
+  if (rescue) {
+    if (!flip[e]) return;
+    fr = min((fc + M - 1) / M * M, T);
+    if (tid == 0) f_r[e] = fr;
+  } else {
+    fr = f_r[e];
+  }
+  const uint32_t* tcw = bm_tc + (size_t)e * W;
+  uint32_t* kw = bm_kept + (size_t)e * W;
+  if (fr == fc) {
+    for (int w = tid; w < W; w += blockDim.x) kw[w] = tcw[w];
+    return;
+  }
+  const bool up = fr > fc;
+  int k = up ? fr - fc : fr;
+  if (k == 0) {
+    for (int w = tid; w < W; w += blockDim.x) kw[w] = 0u;
+    return;
+  }
+  const float* col = ST + (size_t)e * T;
+  uint32_t prefix = 0, pmask = 0;
+  const int shifts[3] = {20, 8, 0};
+  const int bits[3] = {12, 12, 8};
+  for (int p = 0; p < 3; ++p) {
+    const int sh = shifts[p], nb = 1 << bits[p];
+    for (int i = tid; i < nb; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    for (int w = tid; w < W; w += blockDim.x) {
+      uint32_t o[32];
+      load_word_keys(col, T, w, o);
+      const uint32_t cand = up ? ~tcw[w] : tcw[w];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (((cand >> i) & 1u) && w * 32 + i < T && (o[i] & pmask) == prefix) atomicAdd(&hist[(o[i] >> sh) & (nb - 1)], 1);
+    }
+    __syncthreads();
+    {  // the digit holding the k-th largest: block scan over bins from the top (4 bins / thread)
+      const int bpt = (nb + blockDim.x - 1) / blockDim.x;
+      const int hi = nb - 1 - tid * bpt;  // this thread's bins: hi, hi-1, ..., hi-bpt+1
+      int sum = 0;
+      for (int b = 0; b < bpt; ++b)
+        if (hi - b >= 0) sum += hist[hi - b];
+      int tot;
+      const int ex = block_excl_scan(sum, &tot);
+      if (ex < k && k <= ex + sum) {
+        int cum = ex;
+        for (int b = 0; b < bpt; ++b) {
+          const int h = hist[hi - b];
+          if (cum + h >= k) {
+            s_digit = hi - b;
+            s_above = cum;
+            break;
+          }
+          cum += h;
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint32_t)s_digit << sh;
+    pmask |= (uint32_t)(nb - 1) << sh;
+    k -= s_above;
+    __syncthreads();
+  }
+  // threshold = prefix: keep every candidate above it and the first k equal to it (lowest tokens)
+  int run = 0;
+  for (int w0 = 0; w0 < W; w0 += blockDim.x) {
+    const int w = w0 + tid;
+    uint32_t gt = 0u, eq = 0u;
+    if (w < W) {
+      uint32_t o[32];
+      load_word_keys(col, T, w, o);
+      const uint32_t cand = up ? ~tcw[w] : tcw[w];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const bool c = ((cand >> i) & 1u) && w * 32 + i < T;
+        gt |= (uint32_t)(c && o[i] > prefix) << i;
+        eq |= (uint32_t)(c && o[i] == prefix) << i;
+      }
+    }
+    int tot;
+    const int ex = block_excl_scan(__popc(eq), &tot);
+    int take = min(max(k - run - ex, 0), __popc(eq));
+    uint32_t sel = 0u;
+    while (take-- > 0) {  // the lowest `take` equal tokens of this word
+      const uint32_t b = eq & (0u - eq);
+      sel |= b;
+      eq ^= b;
+    }
+    if (w < W) kw[w] = up ? (tcw[w] | gt | sel) : (gt | sel);
+    run += tot;
   }
 }
 
@@ -453,6 +585,112 @@ __global__ void k_build_rows(const uint32_t* __restrict__ bm_kept, const int* __
   }
 }
 
+// ---------------------------------------------------------------- token CSR via bit transposes
+// Warp per 32-token word w.  For each 32-expert chunk c, lane j loads the bitmap word of expert
+// 32c + j; a 5-stage shuffle transpose of that 32x32 bit block gives lane t the 32-bit mask of
+// token 32w + t's experts in the chunk (bit b = expert 32c + b).  Counts, an in-word shuffle scan
+// and a scan over the W word totals (done by the last block of k_csr_count) give rowptr without
+// a serial pass over T.
+__device__ __forceinline__ uint32_t transpose32(uint32_t v, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t lo = s == 16 ? 0x0000FFFFu : s == 8 ? 0x00FF00FFu : s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u
+                                                                                               : 0x55555555u;
+    const uint32_t o = __shfl_xor_sync(0xffffffffu, v, s);
+    v = (lane & s) ? ((v & ~lo) | ((o & ~lo) >> s)) : ((v & lo) | ((o & lo) << s));
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t token_mask_chunk(const uint32_t* __restrict__ bm, int E, int W, int w, int c,
+                                                     int lane) {
+  const int e = 32 * c + lane;
+  const uint32_t v = e < E ? __ldg(bm + (size_t)e * W + w) : 0u;
+  return transpose32(v, lane);
+}
+
+__global__ void k_csr_count(const uint32_t* __restrict__ bm, int T, int E, int W, int* __restrict__ word_pref,
+                            int* __restrict__ rowptr, unsigned* __restrict__ ticket) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w < W) {
+    int c = 0;
+    for (int ch = 0; ch < (E + 31) / 32; ++ch) c += __popc(token_mask_chunk(bm, E, W, w, ch, lane));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) word_pref[w] = c;  // word total for now; the last block turns it into a prefix
+  }
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // exclusive scan of the W word totals in place (blockDim.x = 256 threads, W/256 per thread)
+  int base = 0;
+  for (int w0 = 0; w0 < W; w0 += blockDim.x) {
+    const int i = w0 + threadIdx.x;
+    const int v = i < W ? __ldcg(word_pref + i) : 0;
+    int tot;
+    const int ex = block_excl_scan(v, &tot);
+    if (i < W) word_pref[i] = base + ex;
+    base += tot;
+  }
+  if (threadIdx.x == 0) rowptr[T] = base;
+}
+
+// Rows of each token in ascending expert order + gates (renormalised unless gate_raw).
+__global__ void k_csr_rows(const uint32_t* __restrict__ bm, const int* __restrict__ wprefix, int T, int E, int W,
+                           const int* __restrict__ pad_offsets, const int* __restrict__ word_pref,
+                           const float* __restrict__ S, int gate_raw, int* __restrict__ rowptr,
+                           int* __restrict__ token_rows, float* __restrict__ row_gate) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= W) return;
+  const int t = w * 32 + lane;
+  const int nch = (E + 31) / 32;
+  int c = 0;
+  for (int ch = 0; ch < nch; ++ch) c += __popc(token_mask_chunk(bm, E, W, w, ch, lane));
+  int incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int j0 = word_pref[w] + incl - c;
+  if (t < T) rowptr[t] = j0;
+  const uint32_t below = (1u << lane) - 1u;
+  const float* srow = S + (size_t)t * E;
+  float sum = 0.f;
+  int j = j0;
+  // (lanes beyond T hold empty masks; every lane stays for the transposes' shuffles)
+  for (int ch = 0; ch < nch; ++ch) {
+    uint32_t m = token_mask_chunk(bm, E, W, w, ch, lane);
+    while (m) {
+      const int e = 32 * ch + __ffs(m) - 1;
+      m &= m - 1;
+      const uint32_t word = __ldg(bm + (size_t)e * W + w);
+      token_rows[j++] = pad_offsets[e] + wprefix[(size_t)e * W + w] + __popc(word & below);
+      sum += __ldg(srow + e);
+    }
+    __syncwarp();
+  }
+  const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
+  j = j0;
+  for (int ch = 0; ch < nch; ++ch) {  // second walk: the gates
+    uint32_t m = token_mask_chunk(bm, E, W, w, ch, lane);
+    while (m) {
+      const int e = 32 * ch + __ffs(m) - 1;
+      m &= m - 1;
+      const float sv = __ldg(srow + e);
+      row_gate[token_rows[j++]] = gate_raw ? sv : sv * inv;
+    }
+    __syncwarp();
+  }
+}
+
 // ---------------------------------------------------------------- token CSR (general / TR path)
 // Warp per 32-token word; the E bitmap words are read 8 at a time (independent loads in flight).
 __global__ void k_token_count(const uint32_t* __restrict__ bm_kept, int T, int E, int W, int* __restrict__ cnt) {
@@ -540,7 +778,10 @@ void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st) {
 __global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W, uint32_t* __restrict__ bm,
                                unsigned* __restrict__ ticket) {
   __shared__ uint32_t words[4096];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    ticket[0] = 0u;
+    ticket[1] = 0u;
+  }
   for (int e = threadIdx.x; e < E; e += blockDim.x) words[e] = 0u;
   __syncthreads();
   for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) {
@@ -592,7 +833,10 @@ __global__ void __launch_bounds__(TK_TOK) k_topk_tpt(const float* __restrict__ S
   const int tid = threadIdx.x;
   const int tok0 = blockIdx.x * TK_TOK;
   const int ntok = min(TK_TOK, T - tok0);
-  if (blockIdx.x == 0 && tid == 0 && ticket) *ticket = 0u;
+  if (blockIdx.x == 0 && tid == 0 && ticket) {
+    ticket[0] = 0u;
+    ticket[1] = 0u;
+  }
   for (int i = tid; i < E * 4; i += TK_TOK) words[i] = 0u;
   uint32_t top[NL][KP];
   int id[NL][KP];
@@ -751,6 +995,15 @@ void launch_topk_tpt_k(const RouteLaunch& L, cudaStream_t st) {
   }
 }
 
+// token CSR from a kept-bitmap: counts + word scan (ticket: zeroed here), then rows and gates
+void launch_csr(const uint32_t* bm, const RouteLaunch& L, int gate_raw, cudaStream_t st) {
+  const int T = (int)L.T, E = L.E, W = L.W;
+  const int blocks = (W * 32 + 255) / 256;
+  k_csr_count<<<blocks, 256, 0, st>>>(bm, T, E, W, L.tokcnt, L.token_rowptr, L.ticket + 1);
+  k_csr_rows<<<blocks, 256, 0, st>>>(bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw, L.token_rowptr,
+                                     L.token_rows, L.row_gate);
+}
+
 // ---------------------------------------------------------------- launcher
 int launch_route(const RouteLaunch& L, cudaStream_t st) {
   int nl = 0;
@@ -761,10 +1014,8 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
                                        L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
     k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(L.bm_tc, L.wprefix, W, L.f_r, L.pad_offsets,
                                                            L.row_token, L.row_gate); ++nl;
-    k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_tc, T, E, W, L.tokcnt); ++nl;
-    k_scan_tokens<<<1, 1024, 0, st>>>(L.tokcnt, T, L.token_rowptr); ++nl;
-    k_token_rows<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_tc, L.wprefix, T, E, W, L.pad_offsets, L.tile_expert,
-                                                       L.token_rowptr, L.S, 1, L.token_rows, L.row_gate); ++nl;
+    launch_csr(L.bm_tc, L, 1, st);
+    nl += 2;
     return nl;
   }
 #ifndef SONIC_TOPK_TPT
@@ -774,7 +1025,7 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
     launch_topk_tpt_k(L, st);
     ++nl;
   } else {
-    cudaMemsetAsync(L.ticket, 0, 4, st);
+    cudaMemsetAsync(L.ticket, 0, 8, st);
 #define TOPK_CASE(G, V) \
   k_route_topk<G, V><<<W, 32 * G, 0, st>>>(L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
     if (E <= 32) TOPK_CASE(4, 8);
@@ -793,11 +1044,22 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
     k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
     k_tr_decide<<<(E + 255) / 256, 256, 0, st>>>(L.f, L.f_r, E, T, L.m_tile); ++nl;
     k_transpose<<<dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st>>>(L.S, L.ST, T, E); ++nl;
-    k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0); ++nl;
+#ifndef SONIC_TRSEL_W
+#define SONIC_TRSEL_W 1
+#endif
+    if (SONIC_TRSEL_W)
+      k_tr_select_w<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
+    else
+      k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
+    ++nl;
     if (L.rescue) {
       cudaMemsetAsync(L.flip, 0, (size_t)E * 4, st);
       k_orphans<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;
-      k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1); ++nl;
+      if (SONIC_TRSEL_W)
+        k_tr_select_w<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
+      else
+        k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
+      ++nl;
     }
     bm_kept = L.bm_kept;
     k_popc_offsets<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r, nullptr, L.ticket, L.offsets, L.pad_offsets,
@@ -817,10 +1079,8 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   } else {
     k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets,
                                                            L.row_token, L.row_gate); ++nl;
-    k_token_count<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, T, E, W, L.tokcnt); ++nl;
-    k_scan_tokens<<<1, 1024, 0, st>>>(L.tokcnt, T, L.token_rowptr); ++nl;
-    k_token_rows<<<(W * 32 + 255) / 256, 256, 0, st>>>(bm_kept, L.wprefix, T, E, W, L.pad_offsets, L.tile_expert,
-                                                       L.token_rowptr, L.S, L.gate_raw, L.token_rows, L.row_gate); ++nl;
+    launch_csr(bm_kept, L, L.gate_raw, st);
+    nl += 2;
   }
   return nl;
 }

@@ -255,7 +255,7 @@ RouteWs route_ws(const sonic_moe_desc* D) {
   w.wprefix = o; o += bm;
   w.tokcnt = o; o += al((size_t)s.T * 4);
   w.flip = o; o += al((size_t)s.E * 4);
-  w.ticket = o; o += al(4);
+  w.ticket = o; o += al(8);  // [0] offsets ticket, [1] token-CSR ticket
   w.ST = o; o += (D->route_mode == SONIC_ROUTE_TR_NRF) ? al((size_t)s.T * s.E * 4) : 0;
   w.total = o;
   return w;
