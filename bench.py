@@ -193,7 +193,7 @@ def main():
     ap.add_argument("--config", default="7b")
     ap.add_argument("--mode", default="tc", choices=["tc", "tr"])
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--ref-tokens", type=int, default=1024)
     ap.add_argument("--cpu-tokens", type=int, default=8192)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -235,14 +235,16 @@ def main():
         ws_r = torch.empty(max(256, sonic.sonic_route_workspace_size(desc)), dtype=torch.uint8, device=dev)
         ws_f = torch.empty(max(256, sonic.sonic_fwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
         ws_b = torch.empty(max(256, sonic.sonic_bwd_workspace_size(desc)), dtype=torch.uint8, device=dev)
-        O = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        # outputs double-buffered so the e2e pipeline can read step i's O/dX while step i+1 runs
+        Obuf = [torch.empty(T, d, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        dXbuf = [torch.empty(T, d, dtype=torch.bfloat16, device=dev) for _ in range(2)]
         H = torch.empty(rows, 2 * n, dtype=torch.bfloat16, device=dev)
-        dX = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
         dW1 = torch.empty(E, d, 2 * n, dtype=torch.float32, device=dev)
         dW2 = torch.empty(E, n, d, dtype=torch.float32, device=dev)
         dS = torch.empty(rows, dtype=torch.float32, device=dev)
 
-        def run(Xa, Sa, dOa):
+        def run(Xa, Sa, dOa, slot=0):
+            O, dX = Obuf[slot], dXbuf[slot]
             sonic.sonic_route(desc, Sa, rt, ws_r)
             sonic.sonic_moe_fwd(desc, Xa, W1, W2, rt, O, H, ws_f)
             sonic.sonic_moe_bwd(desc, dOa, Xa, H, W1, W2, rt, dX, dW1, dW2, dS, ws_b)
@@ -265,7 +267,7 @@ def main():
         comm = ep.DistComm() if world > 1 else ep.SimComm(1)
         rk = ep.EPRank(T, d, n, E, K, G, rank, W1, W2, mode=mode)
 
-        def run(Xa, Sa, dOa):
+        def run(Xa, Sa, dOa, slot=0):
             (Oa,) = ep.ep_forward([rk], comm, [Xa], [Sa])
             ((dXa, _),) = ep.ep_backward([rk], comm, [dOa])
             return Oa, dXa
@@ -368,30 +370,58 @@ def main():
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        # Pipelined over three streams, each step's transfers inside the timed region: the H2D of
+        # step i+1 and the D2H of step i-1 overlap the compute of step i (inputs and outputs are
+        # double-buffered; PCIe is full duplex).
         Xh = X.cpu().pin_memory()
         Sh = S.cpu().pin_memory()
         dOh = dOin.cpu().pin_memory()
-        Oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
-        dXh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
-        Xd, Sd, dOd = torch.empty_like(X), torch.empty_like(S), torch.empty_like(dOin)
+        Oh = [torch.empty(T, d, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        dXh = [torch.empty(T, d, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        Xd = [torch.empty_like(X) for _ in range(2)]
+        Sd = [torch.empty_like(S) for _ in range(2)]
+        dOd = [torch.empty_like(dOin) for _ in range(2)]
+        s_in, s_cmp, s_out = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+        ev = lambda: torch.cuda.Event()
+        ev_in = [ev(), ev()]    # inputs of slot b landed
+        ev_cmp = [ev(), ev()]   # compute of slot b done (inputs free, outputs ready)
+        ev_out = [ev(), ev()]   # D2H of slot b done (outputs free)
+        for b in range(2):      # all slots start free
+            for e_ in (ev_cmp[b], ev_out[b]):
+                e_.record(s_cmp)
 
-        def step_e2e():
-            Xd.copy_(Xh, non_blocking=True)
-            Sd.copy_(Sh, non_blocking=True)
-            dOd.copy_(dOh, non_blocking=True)
-            Od, dXd = run(Xd, Sd, dOd)
-            Oh.copy_(Od, non_blocking=True)
-            dXh.copy_(dXd, non_blocking=True)
+        def step_e2e(i):
+            b = i & 1
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(ev_cmp[b])
+                Xd[b].copy_(Xh, non_blocking=True)
+                Sd[b].copy_(Sh, non_blocking=True)
+                dOd[b].copy_(dOh, non_blocking=True)
+                ev_in[b].record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in[b])
+                s_cmp.wait_event(ev_out[b])
+                Od, dXd = run(Xd[b], Sd[b], dOd[b], b)
+                Od.record_stream(s_out)
+                dXd.record_stream(s_out)
+                ev_cmp[b].record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp[b])
+                Oh[b].copy_(Od, non_blocking=True)
+                dXh[b].copy_(dXd, non_blocking=True)
+                ev_out[b].record(s_out)
 
-        step_e2e()
+        step_e2e(0)
+        step_e2e(1)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.e2e_steps):
-            step_e2e()
-        e1.record()
+        e0.record(s_in)
+        for i in range(args.e2e_steps):
+            step_e2e(i)
+        s_in.wait_stream(s_out)
+        e1.record(s_in)
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if world > 1:
@@ -401,7 +431,8 @@ def main():
         e_step = ems / args.e2e_steps
         e2e = {"value": flops_all / (e_step * 1e-3) / 1e12, "unit": "TFLOPS",
                "h2d_bytes_per_step": Xh.numel() * 2 + Sh.numel() * 4 + dOh.numel() * 2,
-               "d2h_bytes_per_step": Oh.numel() * 2 + dXh.numel() * 2, "ms_per_step": e_step}
+               "d2h_bytes_per_step": Oh[0].numel() * 2 + dXh[0].numel() * 2, "ms_per_step": e_step,
+               "pipelined": "H2D(i+1) | compute(i) | D2H(i-1) on three streams"}
 
     if rank != 0:
         if world > 1:
