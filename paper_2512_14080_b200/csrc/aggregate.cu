@@ -65,66 +65,6 @@ __global__ void __launch_bounds__(256) k_aggregate(const __nv_bfloat16* __restri
   }
 }
 
-__device__ __forceinline__ void ldg_stream8(const void* p, uint32_t (&r)[8]) {
-  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-               : "l"(p));
-}
-__device__ __forceinline__ void acc16(float (&a)[16], const uint32_t (&v)[8]) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[i]));
-    a[2 * i] += f.x;
-    a[2 * i + 1] += f.y;
-  }
-}
-
-// 32-byte variant: one warp per token, lane = 32-byte column chunk (16 bf16 columns); the row ids
-// of the token are held one per lane and broadcast by shuffle; up to 8 row loads in flight per
-// lane.  Same summation order as k_aggregate (CSR order, fp32), so identical results.
-__global__ void __launch_bounds__(256) k_aggregate32(const __nv_bfloat16* __restrict__ Y,
-                                                     const int* __restrict__ rowptr, const int* __restrict__ rows,
-                                                     __nv_bfloat16* __restrict__ out, long long T, int d) {
-  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (t >= T) return;
-  const int r0 = __ldg(rowptr + t), r1 = __ldg(rowptr + t + 1);
-  const int nch = d >> 4;  // 32-byte chunks per row
-  const char* Yb = reinterpret_cast<const char*>(Y);
-  for (int c = lane; c - lane < nch; c += 32) {
-    const bool act = c < nch;
-    float a[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) a[i] = 0.f;
-    for (int b0 = r0; b0 < r1; b0 += 32) {  // row ids in batches of 32 (one per lane)
-      const int nb = min(32, r1 - b0);
-      const int myrow = lane < nb ? __ldg(rows + b0 + lane) : 0;
-      for (int j0 = 0; j0 < nb; j0 += 8) {
-        uint32_t v[8][8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int q = __shfl_sync(0xffffffffu, myrow, (j0 + u) & 31);
-          if (act && j0 + u < nb) ldg_stream8(Yb + ((long long)q * d + 16 * c) * 2, v[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (act && j0 + u < nb) acc16(a, v[u]);
-      }
-    }
-    if (act) {
-      uint32_t o[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const __nv_bfloat162 h = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
-        o[i] = *reinterpret_cast<const uint32_t*>(&h);
-      }
-      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(out + t * d + 16 * c), "r"(o[0]),
-                   "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(o[4]), "r"(o[5]), "r"(o[6]), "r"(o[7])
-                   : "memory");
-    }
-  }
-}
-
 __global__ void k_ds_reduce(const float* __restrict__ part, int nparts, long long rows_max,
                             const int* __restrict__ num_tiles, float* __restrict__ dS) {
   const long long R = (long long)(*num_tiles) * GEMM_M;
@@ -139,13 +79,7 @@ void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows
                       int d, cudaStream_t st) {
   const int threads = 256;
   const long long blocks = (T * 32 + threads - 1) / threads;
-#ifndef SONIC_AGG32
-#define SONIC_AGG32 0  // 32-byte variant measured slower at 7B (180 vs 157 us)
-#endif
-  if (SONIC_AGG32 && d % 16 == 0)
-    k_aggregate32<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
-  else
-    k_aggregate<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
+  k_aggregate<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
 }
 
 void launch_ds_reduce(const float* part, int nparts, long long rows_max, const int* num_tiles, float* dS,

@@ -973,6 +973,106 @@ __global__ void k_rows_tc(const uint32_t* __restrict__ bm, const int* __restrict
   row_gate[r] = gate_raw ? ms : ms * inv;
 }
 
+// Four threads per token (32 tokens per 128-thread block = one bitmap word): thread g of a token
+// scans experts g, g+4, g+8, ... (row stride 132 words: the 32 lanes of a warp hit 32 distinct
+// banks) with one stable insertion list, then two shuffle rounds of bitonic merges on the unique
+// 64-bit keys give every thread of the token its top-KT.
+constexpr int TG_TOK = 32, TG_EC = 128, TG_STRIDE = TG_EC + 4;
+template <int KT>
+__global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, int T, int E, int W,
+                                                 int* __restrict__ topk_ids, float* __restrict__ topk_s,
+                                                 uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket) {
+  constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
+  extern __shared__ float tg_sm[];  // [TG_TOK][TG_STRIDE] staging, then words [E]
+  uint32_t* words = reinterpret_cast<uint32_t*>(tg_sm + TG_TOK * TG_STRIDE);
+  const int tid = threadIdx.x, tl = tid >> 2, g = tid & 3;
+  const int tok0 = blockIdx.x * TG_TOK;
+  const int ntok = min(TG_TOK, T - tok0);
+  if (blockIdx.x == 0 && tid == 0 && ticket) {
+    ticket[0] = 0u;
+    ticket[1] = 0u;
+  }
+  for (int i = tid; i < E; i += 128) words[i] = 0u;
+  uint32_t top[KP];
+  int id[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+    top[i] = 0u;
+    id[i] = 0;
+  }
+  for (int e0 = 0; e0 < E; e0 += TG_EC) {
+    const int ecn = min(TG_EC, E - e0);
+    __syncthreads();
+    if (ecn == TG_EC && (E & 3) == 0) {
+#pragma unroll 4
+      for (int i = tid; i < ntok * (TG_EC / 4); i += 128) {
+        const int r = i / (TG_EC / 4), c4 = i % (TG_EC / 4);
+        const float4 v = __ldg(reinterpret_cast<const float4*>(S + (size_t)(tok0 + r) * E + e0) + c4);
+        *reinterpret_cast<float4*>(tg_sm + r * TG_STRIDE + 4 * c4) = v;
+      }
+    } else {
+      for (int r = 0; r < ntok; ++r)
+        for (int ec = tid; ec < ecn; ec += 128) tg_sm[r * TG_STRIDE + ec] = __ldg(S + (size_t)(tok0 + r) * E + e0 + ec);
+    }
+    __syncthreads();
+    if (tl < ntok) {
+      const float* row = tg_sm + tl * TG_STRIDE;
+      for (int ec = g; ec < ecn; ec += 4) {
+        const uint32_t v = ord_f32(row[ec]);
+        if (v > top[KP - 1]) {
+          const int e = e0 + ec;
+#pragma unroll
+          for (int i = KP - 1; i > 0; --i) {
+            const bool gi = v > top[i], gp = v > top[i - 1];
+            top[i] = gi ? (gp ? top[i - 1] : v) : top[i];
+            id[i] = gi ? (gp ? id[i - 1] : e) : id[i];
+          }
+          if (v > top[0]) {
+            top[0] = v;
+            id[0] = e;
+          }
+        }
+      }
+    }
+  }
+  unsigned long long key[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i)
+    key[i] = top[i] ? ((unsigned long long)top[i] << 32) | (0xFFFFFFFFu - (uint32_t)id[i]) : 0ull;
+#pragma unroll
+  for (int m = 1; m <= 2; m <<= 1) {
+    unsigned long long other[KP];
+#pragma unroll
+    for (int i = 0; i < KP; ++i) other[i] = __shfl_xor_sync(0xffffffffu, key[i], m);
+    bitonic_merge_desc<KP>(key, other);
+  }
+  if (tl < ntok) {
+    const size_t t = (size_t)(tok0 + tl);
+#pragma unroll
+    for (int i = 0; i < KT; ++i) {
+      if ((i & 3) != g) continue;  // the token's 4 threads share the writes
+      const int e = (int)(0xFFFFFFFFu - (uint32_t)(key[i] & 0xFFFFFFFFull));
+      topk_ids[t * KT + i] = e;
+      topk_s[t * KT + i] = unord_f32((uint32_t)(key[i] >> 32));
+      atomicOr(&words[e], 1u << tl);
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += 128) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
+}
+
+template <int KT>
+void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
+  const int T = (int)L.T, E = L.E, W = L.W;
+  const int smem = (TG_TOK * TG_STRIDE + E) * 4;
+  static int attr = 0;
+  if (attr < smem) {
+    cudaFuncSetAttribute(k_topk_g4<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = smem;
+  }
+  k_topk_g4<KT><<<W, 128, smem, st>>>(L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
+}
+
 template <int KT>
 void launch_topk_tpt(const RouteLaunch& L, cudaStream_t st) {
   const int T = (int)L.T, E = L.E, W = L.W;
@@ -987,7 +1087,10 @@ void launch_topk_tpt(const RouteLaunch& L, cudaStream_t st) {
 }
 void launch_topk_tpt_k(const RouteLaunch& L, cudaStream_t st) {
   switch (L.K) {
-#define TKC(k) case k: launch_topk_tpt<k>(L, st); break;
+#ifndef SONIC_TOPK_G4
+#define SONIC_TOPK_G4 1
+#endif
+#define TKC(k) case k: if (SONIC_TOPK_G4) launch_topk_g4<k>(L, st); else launch_topk_tpt<k>(L, st); break;
     TKC(1) TKC(2) TKC(3) TKC(4) TKC(5) TKC(6) TKC(7) TKC(8)
     TKC(9) TKC(10) TKC(11) TKC(12) TKC(13) TKC(14) TKC(15) TKC(16)
 #undef TKC
