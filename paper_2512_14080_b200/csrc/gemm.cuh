@@ -58,6 +58,7 @@ struct GemmArgs {
   float* dS;                // DH: dS [rows] if n_tiles == 1, else partials [n_tiles][rows_max]
   long long rows_max;
   __nv_bfloat16* out;       // DOWN / DXT: the output rows [rows_max, N_dim] (direct-store epilogue)
+  unsigned long long* dbg;  // SONIC_TIMING builds only: cycle counters (see sonic_api.cu)
 };
 
 template <int KIND>
@@ -503,15 +504,30 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+#ifdef SONIC_TIMING
+      unsigned long long c_te = 0, c_full = 0, c0 = clock64();
+#endif
       for (int tile = t_first; tile < total_tiles; tile += t_step) {
         const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, 0);
+#ifdef SONIC_TIMING
+        unsigned long long ca = clock64();
+#endif
         if constexpr (CTA2) ptx::mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
         else ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+#ifdef SONIC_TIMING
+        c_te += clock64() - ca;
+#endif
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < tc.nkb; ++kb) {
+#ifdef SONIC_TIMING
+          unsigned long long cb = clock64();
+#endif
           if constexpr (CTA2) ptx::mbar_wait_cluster(&full[stage], phase);
           else ptx::mbar_wait(&full[stage], phase);
+#ifdef SONIC_TIMING
+          c_full += clock64() - cb;
+#endif
           // cp.async (generic proxy) data consumed by tcgen05.mma (async proxy)
           if constexpr (GATHER) ptx::fence_proxy_async_smem();
           ptx::tc_fence_after();
@@ -538,6 +554,14 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+#ifdef SONIC_TIMING
+      if (args.dbg) {
+        atomicAdd(args.dbg + 0, clock64() - c0);
+        atomicAdd(args.dbg + 1, c_te);
+        atomicAdd(args.dbg + 2, c_full);
+        atomicAdd(args.dbg + 5, 1ull);
+      }
+#endif
     } else if (lane == 0 && CTA2 && GATHER) {
       // relay: forward this CTA's cp.async completion (local barrier) to the leader's barrier
       int stage = 0;
@@ -640,13 +664,23 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       hr_load(0);
       hr_load(1);
     }
+#ifdef SONIC_TIMING
+    unsigned long long c_tf = 0, c_epi = 0;
+#endif
     for (int tile = t_first; tile < total_tiles; tile += t_step) {
       const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
       const int wrow = tc.row0 + 32 * q;  // first grouped row of this warp's slab
       const int row = wrow + lane;        // this thread's grouped row (varlen-M)
       const bool has_next = tile + t_step < total_tiles;
+#ifdef SONIC_TIMING
+      unsigned long long cx = clock64();
+#endif
       if constexpr (CTA2) ptx::mbar_wait_cluster(&tfull[acc], acc_phase);
       else ptx::mbar_wait(&tfull[acc], acc_phase);
+#ifdef SONIC_TIMING
+      unsigned long long cy = clock64();
+      c_tf += cy - cx;
+#endif
       ptx::tc_fence_after();
       const uint32_t t_acc = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
 
@@ -1058,9 +1092,18 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           ptx::mbar_arrive(&tempty[acc]);
         }
       }
+#ifdef SONIC_TIMING
+      c_epi += clock64() - cy;
+#endif
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+#ifdef SONIC_TIMING
+    if (args.dbg && lane == 0 && ew == 0) {
+      atomicAdd(args.dbg + 3, c_tf);
+      atomicAdd(args.dbg + 4, c_epi);
+    }
+#endif
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
   }

@@ -1,3 +1,4 @@
+#include <cstdio>
 // sonic_api.cu -- the C ABI of include/sonic.h: validation, workspace layout, TMA tensor
 // maps, and the launch sequences of sonic_route / sonic_moe_fwd / sonic_moe_bwd.
 #include <cuda.h>
@@ -161,7 +162,22 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   attrs[0].val.clusterDim.z = 1;
   cfg.attrs = attrs;
   cfg.numAttrs = 1;
+#ifdef SONIC_TIMING
+  static unsigned long long* dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
+  cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st);
+  GemmArgs targs = args;
+  targs.dbg = dbg;
+  if (cudaLaunchKernelEx(&cfg, kern, a, b, c0, c1, dmap, targs) != cudaSuccess) return false;
+  unsigned long long h[16];
+  cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  const double n = h[5] ? (double)h[5] : 1.0;
+  fprintf(stderr, "TIMING kind=%d BN=%d cta2=%d: mma_total %.0f  wait_tempty %.0f  wait_full %.0f | epi_wait_tfull %.0f  epi_busy %.0f (kcycles; epilogue counters summed over the pair)\n",
+          KIND, BN, (int)CTA2, h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3, h[3] / n / 1e3, h[4] / n / 1e3);
+#else
   if (cudaLaunchKernelEx(&cfg, kern, a, b, c0, c1, dmap, args) != cudaSuccess) return false;
+#endif
   ++g_launches;
   return true;
 }
