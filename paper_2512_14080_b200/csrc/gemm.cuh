@@ -185,6 +185,10 @@ __device__ __forceinline__ int tok_of(const int* row_token, int r) { return r & 
 __device__ __forceinline__ int tok_of(const int* row_token, int r) { return __ldg(row_token + r); }
 #endif
 __device__ __forceinline__ size_t clamp_tok(int t) { return (size_t)max(t, 0); }
+__device__ __forceinline__ void gather16(uint32_t dst, const void* src, uint64_t pol) {
+  if (SONIC_L2_HINTS) ptx::cp_async16_hint(dst, src, pol);
+  else ptx::cp_async16(dst, src);
+}
 
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 // sigma(x) = 0.5 tanh(x/2) + 0.5 with the SFU tanh (rel. err ~2^-11, far below bf16's 2^-8)
@@ -367,6 +371,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     } else {
       const int pt = threadIdx.x;  // 0..127
       const int c = pt & 7;        // 16-byte chunk within a 128-byte row
+      const uint64_t gpol = ptx::policy_evict_last();  // gathered rows are re-read by K experts' tiles
       const int r0 = pt >> 3;      // rows r0 + 16 j
       const uint32_t sw = (uint32_t)((c ^ (r0 & 7)) << 4);
       // Gather indices are prefetched one tile (varlen-M) / one stage (varlen-K) ahead so the
@@ -478,14 +483,14 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             }
             const uint32_t dst = ptx::smem_u32(sA) + r0 * 128 + sw;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ptx::cp_async16(dst + j * 16 * 128, srcM[j] + kb * GEMM_BK);
+            for (int j = 0; j < 8; ++j) gather16(dst + j * 16 * 128, srcM[j] + kb * GEMM_BK, gpol);
           } else {  // 64 gathered K-rows x (128 | BNL) MN-columns (MN-major)
             constexpr int NCH = Tr::a_gather ? 2 : BNL / 64;
             const uint32_t dst = ptx::smem_u32(Tr::a_gather ? sA : sB) + r0 * 128 + sw;
 #pragma unroll
             for (int j = 0; j < 4; ++j)
 #pragma unroll
-              for (int jj = 0; jj < NCH; ++jj) ptx::cp_async16(dst + jj * 8192 + j * 16 * 128, srcK[j] + 64 * jj);
+              for (int jj = 0; jj < NCH; ++jj) gather16(dst + jj * 8192 + j * 16 * 128, srcK[j] + 64 * jj, gpol);
           }
           ptx::cp_async_mbar_arrive(bar);  // arrives on this CTA's barrier when the copies land
           if (++stage == STAGES) {
