@@ -121,7 +121,8 @@ struct GemmCfg {
 // TMA load of H in the dH epilogue").  Staging ring depth NB: 2 (a deeper ring costs a mainloop
 // stage, measured slower).
 template <int KIND, int BN, bool CTA2>
-using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128, 2, KIND == K_DH && BN == 256>;
+using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128, (KIND == K_DH && BN == 256) ? 0 : 2,
+                     KIND == K_DH && BN == 256>;
 
 struct TileCoord {
   int e, row0, nt, mt, nkb, seg0;
@@ -840,9 +841,9 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             const int sl = hr_wait();
             const int col = tc.nt * BN + 64 * c;
             uint8_t* gbp = hb + sl * 2 * STG_BYTES;
-            const uint32_t gb = ptx::smem_u32(gbp);  // H gate -> dH gate (in place)
-            const uint32_t ub = gb + STG_BYTES;      // H up   -> dH up
-            const uint32_t ab = sq.addr(c & 1);      // A' staging (its store of chunk c-2 has read it)
+            const uint32_t gb = ptx::smem_u32(gbp);  // H gate -> dH gate (in place) -> A'
+            const uint32_t ub = gb + STG_BYTES;      // H up   -> dH up (in place)
+            uint32_t pa[2][4][4];                     // A' = s A for this chunk, bf16 pairs
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               uint32_t r[32];
@@ -858,7 +859,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
               const __nv_bfloat16* hup = reinterpret_cast<const __nv_bfloat16*>(hu4);
 #pragma unroll
               for (int q8 = 0; q8 < 4; ++q8) {
-                uint32_t pg[4], pu[4], pa[4];
+                uint32_t pg[4], pu[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                   float dg2[2], du2[2], ap2[2];
@@ -879,22 +880,32 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
                   }
                   pg[i] = ptx::pack_bf16(dg2[0], dg2[1]);
                   pu[i] = ptx::pack_bf16(du2[0], du2[1]);
-                  pa[i] = ptx::pack_bf16(ap2[0], ap2[1]);
+                  pa[h][q8][i] = ptx::pack_bf16(ap2[0], ap2[1]);
                 }
                 ptx::st_shared_v4(gb + swz(lane, 4 * h + q8), pg[0], pg[1], pg[2], pg[3]);
                 ptx::st_shared_v4(ub + swz(lane, 4 * h + q8), pu[0], pu[1], pu[2], pu[3]);
-                ptx::st_shared_v4(ab + swz(lane, 4 * h + q8), pa[0], pa[1], pa[2], pa[3]);
               }
             }
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
-              ptx::tma_store_2d(&mC0, gbp, col, wrow);                    // dH gate
-              ptx::tma_store_2d(&mC0, gbp + STG_BYTES, n + col, wrow);    // dH up
+              ptx::tma_store_2d(&mC0, gbp, col, wrow);                  // dH gate
+              ptx::tma_store_2d(&mC0, gbp + STG_BYTES, n + col, wrow);  // dH up
               ptx::bulk_commit();
-              ptx::tma_store_2d(&mC1, sq.base + (c & 1) * STG_BYTES, col, wrow);  // A' = s A
+              ptx::bulk_wait_read<0>();  // the gate slot is free for A'
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int q8 = 0; q8 < 4; ++q8)
+                ptx::st_shared_v4(gb + swz(lane, 4 * h + q8), pa[h][q8][0], pa[h][q8][1], pa[h][q8][2], pa[h][q8][3]);
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&mC1, gbp, col, wrow);  // A' = s A
               ptx::bulk_commit();
-              ptx::bulk_wait_read<1>();  // the dH stores have read the slot
+              ptx::bulk_wait_read<0>();  // the slot is free for the next H chunk
             }
             __syncwarp();
             hr_load(sl);
