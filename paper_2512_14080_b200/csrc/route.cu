@@ -342,6 +342,7 @@ __device__ __forceinline__ void load_word_keys(const float* __restrict__ col, in
     for (int i = 0; i < 32; ++i) o[i] = t0 + i < T ? ord_f32(__ldg(col + t0 + i)) : 0u;
   }
 }
+template <bool ONE>  // ONE: W <= blockDim.x, so each thread's single word of keys stays in registers
 __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ ST, int T, int W, int M,
                                                       const uint32_t* __restrict__ bm_tc,
                                                       uint32_t* __restrict__ bm_kept, const int* __restrict__ f,
@@ -373,6 +374,18 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
     return;
   }
   const float* col = ST + (size_t)e * T;
+  uint32_t okeep[ONE ? 32 : 1];
+  uint32_t cand1 = 0u;
+  if constexpr (ONE) {
+    if (tid < W) {
+      uint32_t o[32];
+      load_word_keys(col, T, tid, o);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) okeep[i] = o[i];
+      cand1 = (up ? ~tcw[tid] : tcw[tid]);
+      if (tid * 32 + 32 > T) cand1 &= (T - tid * 32 >= 32) ? ~0u : ((1u << (T - tid * 32)) - 1u);
+    }
+  }
   uint32_t prefix = 0, pmask = 0;
   const int shifts[3] = {20, 8, 0};
   const int bits[3] = {12, 12, 8};
@@ -380,13 +393,22 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
     const int sh = shifts[p], nb = 1 << bits[p];
     for (int i = tid; i < nb; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (int w = tid; w < W; w += blockDim.x) {
-      uint32_t o[32];
-      load_word_keys(col, T, w, o);
-      const uint32_t cand = up ? ~tcw[w] : tcw[w];
+    if constexpr (ONE) {
+      if (tid < W) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i)
-        if (((cand >> i) & 1u) && w * 32 + i < T && (o[i] & pmask) == prefix) atomicAdd(&hist[(o[i] >> sh) & (nb - 1)], 1);
+        for (int i = 0; i < 32; ++i)
+          if (((cand1 >> i) & 1u) && (okeep[i] & pmask) == prefix) atomicAdd(&hist[(okeep[i] >> sh) & (nb - 1)], 1);
+      }
+    } else {
+      for (int w = tid; w < W; w += blockDim.x) {
+        uint32_t o[32];
+        load_word_keys(col, T, w, o);
+        const uint32_t cand = up ? ~tcw[w] : tcw[w];
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (((cand >> i) & 1u) && w * 32 + i < T && (o[i] & pmask) == prefix)
+            atomicAdd(&hist[(o[i] >> sh) & (nb - 1)], 1);
+      }
     }
     __syncthreads();
     {  // the digit holding the k-th largest: block scan over bins from the top (4 bins / thread)
@@ -422,14 +444,23 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
     const int w = w0 + tid;
     uint32_t gt = 0u, eq = 0u;
     if (w < W) {
-      uint32_t o[32];
-      load_word_keys(col, T, w, o);
-      const uint32_t cand = up ? ~tcw[w] : tcw[w];
+      if constexpr (ONE) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const bool c = ((cand >> i) & 1u) && w * 32 + i < T;
-        gt |= (uint32_t)(c && o[i] > prefix) << i;
-        eq |= (uint32_t)(c && o[i] == prefix) << i;
+        for (int i = 0; i < 32; ++i) {
+          const bool c = (cand1 >> i) & 1u;
+          gt |= (uint32_t)(c && okeep[i] > prefix) << i;
+          eq |= (uint32_t)(c && okeep[i] == prefix) << i;
+        }
+      } else {
+        uint32_t o[32];
+        load_word_keys(col, T, w, o);
+        const uint32_t cand = up ? ~tcw[w] : tcw[w];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const bool c = ((cand >> i) & 1u) && w * 32 + i < T;
+          gt |= (uint32_t)(c && o[i] > prefix) << i;
+          eq |= (uint32_t)(c && o[i] == prefix) << i;
+        }
       }
     }
     int tot;
@@ -688,6 +719,60 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ bm, const int* __restric
       row_gate[token_rows[j++]] = gate_raw ? sv : sv * inv;
     }
     __syncwarp();
+  }
+}
+
+// One block per word, one warp per 32-expert chunk (E <= 1024): the chunk masks, per-chunk counts
+// and partial gate sums go through shared memory; warp 0 forms rowptr and the gate scale; then each
+// warp writes its chunk's rows at base + (counts of the lower chunks).
+__global__ void k_csr_rows_chunked(const uint32_t* __restrict__ bm, const int* __restrict__ wprefix, int T, int E,
+                                   int W, const int* __restrict__ pad_offsets, const int* __restrict__ word_pref,
+                                   const float* __restrict__ S, int gate_raw, int* __restrict__ rowptr,
+                                   int* __restrict__ token_rows, float* __restrict__ row_gate) {
+  __shared__ int s_cnt[32][33];
+  __shared__ float s_sum[32][33];
+  __shared__ int s_base[32];
+  __shared__ float s_inv[32];
+  const int w = blockIdx.x, ch = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nch = blockDim.x >> 5;
+  const int t = w * 32 + lane;
+  const float* srow = S + (size_t)t * E;
+  const uint32_t m = token_mask_chunk(bm, E, W, w, ch, lane);
+  float ps = 0.f;
+  for (uint32_t mm = m; mm; mm &= mm - 1) ps += __ldg(srow + 32 * ch + __ffs(mm) - 1);
+  s_cnt[ch][lane] = __popc(m);
+  s_sum[ch][lane] = ps;
+  __syncthreads();
+  if (ch == 0) {
+    int tot = 0;
+    float sum = 0.f;
+    for (int c = 0; c < nch; ++c) {
+      tot += s_cnt[c][lane];
+      sum += s_sum[c][lane];
+    }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int base = word_pref[w] + incl - tot;
+    if (t < T) rowptr[t] = base;
+    s_base[lane] = base;
+    s_inv[lane] = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
+  }
+  __syncthreads();
+  int j = s_base[lane];
+  for (int c = 0; c < ch; ++c) j += s_cnt[c][lane];
+  const float inv = s_inv[lane];
+  const uint32_t below = (1u << lane) - 1u;
+  for (uint32_t mm = m; mm; mm &= mm - 1) {
+    const int e = 32 * ch + __ffs(mm) - 1;
+    const uint32_t word = __ldg(bm + (size_t)e * W + w);
+    const int r = pad_offsets[e] + wprefix[(size_t)e * W + w] + __popc(word & below);
+    token_rows[j++] = r;
+    const float sv = __ldg(srow + e);
+    row_gate[r] = gate_raw ? sv : sv * inv;
   }
 }
 
@@ -1103,8 +1188,13 @@ void launch_csr(const uint32_t* bm, const RouteLaunch& L, int gate_raw, cudaStre
   const int T = (int)L.T, E = L.E, W = L.W;
   const int blocks = (W * 32 + 255) / 256;
   k_csr_count<<<blocks, 256, 0, st>>>(bm, T, E, W, L.tokcnt, L.token_rowptr, L.ticket + 1);
-  k_csr_rows<<<blocks, 256, 0, st>>>(bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw, L.token_rowptr,
-                                     L.token_rows, L.row_gate);
+  const int nch = (E + 31) / 32;
+  if (nch <= 32)
+    k_csr_rows_chunked<<<W, 32 * nch, 0, st>>>(bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw,
+                                               L.token_rowptr, L.token_rows, L.row_gate);
+  else
+    k_csr_rows<<<blocks, 256, 0, st>>>(bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw,
+                                       L.token_rowptr, L.token_rows, L.row_gate);
 }
 
 // ---------------------------------------------------------------- launcher
@@ -1150,16 +1240,20 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
 #ifndef SONIC_TRSEL_W
 #define SONIC_TRSEL_W 1
 #endif
-    if (SONIC_TRSEL_W)
-      k_tr_select_w<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
+    if (SONIC_TRSEL_W && W <= 1024)
+      k_tr_select_w<true><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
+    else if (SONIC_TRSEL_W)
+      k_tr_select_w<false><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
     else
       k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
     ++nl;
     if (L.rescue) {
       cudaMemsetAsync(L.flip, 0, (size_t)E * 4, st);
       k_orphans<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;
-      if (SONIC_TRSEL_W)
-        k_tr_select_w<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
+      if (SONIC_TRSEL_W && W <= 1024)
+        k_tr_select_w<true><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
+      else if (SONIC_TRSEL_W)
+        k_tr_select_w<false><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
       else
         k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
       ++nl;
