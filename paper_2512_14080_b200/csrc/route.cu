@@ -6,17 +6,20 @@
 // hold tokens in ascending order (popcount prefix over words), the token CSR lists
 // experts in ascending order.
 //
-//   k_route_topk     TC top-K per token (warp per token, exact 64-bit keys: ordered fp32
-//                    score, ties -> lower expert id, Q9) -> topk, TC bitmap
+//   k_topk_g4        TC top-K per token (4 threads per token, stable insertion on ordered fp32
+//                    scores, bitonic merges on exact 64-bit keys; ties -> lower expert id;
+//                    P:1072-1099, Q9) -> topk, TC bitmap
 //   k_expert_popc    per-expert popcount + exclusive word prefix (histogram f_e)
 //   k_tr_decide      NR-f rounding decision
 //   k_transpose      S -> S^T so expert columns are contiguous (TR only)
-//   k_tr_select      Alg. 4 step (4): per expert, keep the top f_r of the ranking
+//   k_tr_select_w    Alg. 4 step (4): per expert, keep the top f_r of the ranking
 //                    (in-TC, S, -t) via radix select on the ordered score + token tie pass
 //   k_orphans        tokens with no kept expert flag their top-1 expert (Q14 rescue)
-//   k_offsets        offsets, tile-aligned pad_offsets, tile -> expert map
+//   k_popc_offsets   counts + word prefixes; last block: offsets, tile-aligned pad_offsets,
+//                    tile -> expert map, 2-CTA pair schedule
 //   k_build_rows     gather map row_token (+ pad rows)
-//   k_token_count / k_scan_tokens / k_token_rows   token CSR and renormalised gates
+//   k_rows_tc        TC: gather map + token CSR + renormalised gates in one launch
+//   k_csr_count / k_csr_rows_chunked   general token CSR (TR, GIVEN) via 32x32 bit transposes
 #include "sonic_internal.h"
 
 namespace sonic {
@@ -58,106 +61,6 @@ __device__ int block_excl_scan(int v, int* total) {
   return base + x - v;
 }
 
-// ---------------------------------------------------------------- top-K
-// G lanes per token (G | 32), VPL scores per lane: lane g of a group holds experts g, g+G, ...
-// Exact 64-bit keys (ordered score << 32 | ~expert): the largest key is the largest score and,
-// among equal scores, the lower expert id -- the stable order of P:1099 without packing loss.
-template <int G, int VPL>
-__device__ __forceinline__ void route_topk_token(const float* __restrict__ S, int t, int E, int K, int g,
-                                                 int* __restrict__ topk_ids, float* __restrict__ topk_s,
-                                                 uint32_t* words) {
-  const float* row = S + (size_t)t * E;
-  unsigned long long key[VPL];
-#pragma unroll
-  for (int j = 0; j < VPL; ++j) {
-    const int e = g + G * j;
-    key[j] = e < E ? ((unsigned long long)ord_f32(__ldg(row + e)) << 32) | (0xFFFFFFFFu - (uint32_t)e) : 0ull;
-  }
-  const unsigned mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
-  for (int k = 0; k < K; ++k) {
-    unsigned long long best = 0;
-#pragma unroll
-    for (int j = 0; j < VPL; ++j) best = key[j] > best ? key[j] : best;
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) {
-      const unsigned long long other = __shfl_xor_sync(mask, best, o, G);
-      best = other > best ? other : best;
-    }
-#pragma unroll
-    for (int j = 0; j < VPL; ++j)
-      if (key[j] == best) key[j] = 0ull;
-    const int e = (int)(0xFFFFFFFFu - (uint32_t)(best & 0xFFFFFFFFull));
-    if (g == (k % G)) {
-      topk_ids[(size_t)t * K + k] = e;
-      topk_s[(size_t)t * K + k] = __ldg(row + e);
-      atomicOr(&words[e], 1u << (t & 31));  // shared memory
-    }
-  }
-}
-
-// One block = one 32-token bitmap word: the block's 32*G threads handle tokens 32*blockIdx.x + i;
-// the chosen experts are OR-ed into a shared-memory word per expert, then every expert's word for
-// this token block is written once (no global atomics, no memset of the bitmap).
-template <int G, int VPL>
-__global__ void __launch_bounds__(32 * G) k_route_topk(const float* __restrict__ S, int T, int E, int K, int W,
-                                                       int* __restrict__ topk_ids, float* __restrict__ topk_s,
-                                                       uint32_t* __restrict__ bm_tc) {
-  __shared__ uint32_t words[4096];
-  for (int e = threadIdx.x; e < E; e += blockDim.x) words[e] = 0u;
-  __syncthreads();
-  const int t = blockIdx.x * 32 + threadIdx.x / G;
-  const int g = threadIdx.x % G;
-  if (t < T) route_topk_token<G, VPL>(S, t, E, K, g, topk_ids, topk_s, words);
-  __syncthreads();
-  for (int e = threadIdx.x; e < E; e += blockDim.x) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
-}
-
-// TC fast path of the token CSR: every token keeps exactly its K top-K experts, so
-// rowptr[t] = t*K and the rows are the top-K experts in ascending id order.  The row of
-// (t, e) is pad_offsets[e] + (rank of t among e's tokens) = pad_offsets[e] + wprefix[e][t/32]
-// + popc(bm[e][t/32] & lanes_below(t)).  Gates renormalise the top-K scores (Q13).
-__global__ void k_token_rows_tc(const int* __restrict__ topk_ids, const float* __restrict__ topk_s,
-                                const uint32_t* __restrict__ bm, const int* __restrict__ wprefix, int T, int K, int W,
-                                const int* __restrict__ pad_offsets, int gate_raw, int* __restrict__ rowptr,
-                                int* __restrict__ token_rows, float* __restrict__ row_gate) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > T) return;
-  rowptr[t] = t * K;
-  if (t == T) return;
-  int ids[16];
-  float sc[16];
-  float sum = 0.f;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    if (k < K) {
-      ids[k] = topk_ids[(size_t)t * K + k];
-      sc[k] = topk_s[(size_t)t * K + k];
-    }
-  }
-  // insertion sort by expert id (K <= 16)
-  for (int i = 1; i < K; ++i) {
-    const int id = ids[i];
-    const float s = sc[i];
-    int j = i - 1;
-    while (j >= 0 && ids[j] > id) {
-      ids[j + 1] = ids[j];
-      sc[j + 1] = sc[j];
-      --j;
-    }
-    ids[j + 1] = id;
-    sc[j + 1] = s;
-  }
-  for (int k = 0; k < K; ++k) sum += sc[k];
-  const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
-  const int w = t >> 5;
-  const uint32_t below = (1u << (t & 31)) - 1u;
-  for (int k = 0; k < K; ++k) {
-    const int e = ids[k];
-    const int r = pad_offsets[e] + wprefix[(size_t)e * W + w] + __popc(bm[(size_t)e * W + w] & below);
-    token_rows[(size_t)t * K + k] = r;
-    row_gate[r] = gate_raw ? sc[k] : sc[k] * inv;
-  }
-}
 
 // ---------------------------------------------------------------- per-expert popcount
 __global__ void k_expert_popc(const uint32_t* __restrict__ bm, int W, int* __restrict__ wprefix,
@@ -208,118 +111,6 @@ __global__ void k_transpose(const float* __restrict__ S, float* __restrict__ ST,
 // rescue == 1: only experts flagged by k_orphans; they round up (f_r = min(ceil, T)).
 // Selects the k largest candidates by (ordered S desc, token asc): down -> candidates are the
 // TC tokens, k = f_r; up -> candidates are the non-TC tokens, k = f_r - f (Alg. 4, Q10).
-__global__ void __launch_bounds__(1024) k_tr_select(const float* __restrict__ ST, int T, int W, int M,
-                                                    const uint32_t* __restrict__ bm_tc,
-                                                    uint32_t* __restrict__ bm_kept, const int* __restrict__ f,
-                                                    int* __restrict__ f_r, const int* __restrict__ flip, int rescue) {
-  __shared__ int hist[4096];
-  __shared__ int s_digit, s_above, s_run;
-  const int e = blockIdx.x;
-  const int tid = threadIdx.x;
-  const int fc = f[e];
-  int fr;
-  if (rescue) {
-    if (!flip[e]) return;
-    fr = min((fc + M - 1) / M * M, T);
-    if (tid == 0) f_r[e] = fr;
-  } else {
-    fr = f_r[e];
-  }
-  const uint32_t* tcw = bm_tc + (size_t)e * W;
-  uint32_t* kw = bm_kept + (size_t)e * W;
-  if (fr == fc) {
-    for (int w = tid; w < W; w += blockDim.x) kw[w] = tcw[w];
-    return;
-  }
-  const bool up = fr > fc;
-  int k = up ? fr - fc : fr;
-  if (k == 0) {  // down to zero: drop every token
-    for (int w = tid; w < W; w += blockDim.x) kw[w] = 0u;
-    return;
-  }
-  const float* col = ST + (size_t)e * T;
-  uint32_t prefix = 0, pmask = 0;
-  const int shifts[3] = {20, 8, 0};
-  const int bits[3] = {12, 12, 8};
-  for (int p = 0; p < 3; ++p) {
-    const int sh = shifts[p], nb = 1 << bits[p];
-    for (int i = tid; i < nb; i += blockDim.x) hist[i] = 0;
-    __syncthreads();
-    for (int t0 = 0; t0 < T; t0 += blockDim.x) {
-      const int t = t0 + tid;
-      bool act = false;
-      uint32_t bin = 0;
-      if (t < T) {
-        const bool is_tc = (tcw[t >> 5] >> (t & 31)) & 1u;
-        if (is_tc != up) {
-          const uint32_t o = ord_f32(col[t]);
-          act = (o & pmask) == prefix;
-          bin = (o >> sh) & (nb - 1);
-        }
-      }
-      if (act) atomicAdd(&hist[bin], 1);
-    }
-    __syncthreads();
-    if (tid < 32) {  // find the digit holding the k-th largest, scanning bins from the top
-      const int per = nb / 32;
-      const int hi = nb - 1 - tid * per;  // this lane's bins: hi, hi-1, ..., hi-per+1
-      int s = 0;
-      for (int b = 0; b < per; ++b) s += hist[hi - b];
-      int incl = s;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tid >= o) incl += y;
-      }
-      const unsigned ball = __ballot_sync(0xffffffffu, incl >= k);
-      const int L = __ffs(ball) - 1;
-      if (tid == L) {
-        int cum = incl - s;
-        for (int b = 0; b < per; ++b) {
-          const int h = hist[hi - b];
-          if (cum + h >= k) {
-            s_digit = hi - b;
-            s_above = cum;
-            break;
-          }
-          cum += h;
-        }
-      }
-    }
-    __syncthreads();
-    prefix |= (uint32_t)s_digit << sh;
-    pmask |= (uint32_t)(nb - 1) << sh;
-    k -= s_above;
-    __syncthreads();
-  }
-  // threshold = prefix; keep all candidates above it and the first k (lowest token ids) equal to it
-  if (tid == 0) s_run = 0;
-  __syncthreads();
-  const int Tpad = (T + blockDim.x - 1) / blockDim.x * blockDim.x;
-  for (int t0 = 0; t0 < Tpad; t0 += blockDim.x) {
-    const int t = t0 + tid;
-    bool cand = false;
-    uint32_t o = 0;
-    if (t < T) {
-      const bool is_tc = (tcw[t >> 5] >> (t & 31)) & 1u;
-      cand = is_tc != up;
-      if (cand) o = ord_f32(col[t]);
-    }
-    const int eq = (cand && o == prefix) ? 1 : 0;
-    int tot;
-    const int ex = block_excl_scan(eq, &tot);
-    const int run = s_run;
-    const bool sel = cand && (o > prefix || (eq && run + ex < k));
-    const unsigned word = __ballot_sync(0xffffffffu, sel);
-    if ((tid & 31) == 0 && t < T) {
-      const int w = t >> 5;
-      kw[w] = up ? (tcw[w] | word) : word;
-    }
-    __syncthreads();
-    if (tid == 0) s_run = run + tot;
-    __syncthreads();
-  }
-}
 
 // Word-per-thread variant: thread i owns bitmap words i, i + 1024, ...; the 32 scores of a word
 // are loaded as 8 x 16 B (one latency per word per pass), the histogram adds come from
@@ -553,12 +344,6 @@ __device__ void offsets_block(const int* __restrict__ f_r, int E, int* __restric
 }
 
 // ---------------------------------------------------------------- gather map
-__global__ void __launch_bounds__(1024) k_offsets(const int* __restrict__ f_r, int E, int* __restrict__ offsets,
-                                                  int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
-                                                  int* __restrict__ num_tiles, int* __restrict__ tile_pairs,
-                                                  int* __restrict__ num_pairs) {
-  offsets_block(f_r, E, offsets, pad_offsets, tile_expert, num_tiles, tile_pairs, num_pairs);
-}
 
 // Per-expert popcount + word prefix (one block per expert, as k_expert_popc); the last block to
 // finish (ticket) then builds offsets / tiles / pairs from the counts (k_offsets' work) -- one
@@ -776,25 +561,6 @@ __global__ void k_csr_rows_chunked(const uint32_t* __restrict__ bm, const int* _
   }
 }
 
-// ---------------------------------------------------------------- token CSR (general / TR path)
-// Warp per 32-token word; the E bitmap words are read 8 at a time (independent loads in flight).
-__global__ void k_token_count(const uint32_t* __restrict__ bm_kept, int T, int E, int W, int* __restrict__ cnt) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= W) return;
-  int c = 0;
-  int e = 0;
-  for (; e + 8 <= E; e += 8) {
-    uint32_t v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = __ldg(bm_kept + (size_t)(e + i) * W + w);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) c += (v[i] >> lane) & 1u;
-  }
-  for (; e < E; ++e) c += (__ldg(bm_kept + (size_t)e * W + w) >> lane) & 1u;
-  const int t = w * 32 + lane;
-  if (t < T) cnt[t] = c;
-}
 
 // One block: thread i scans the contiguous chunk [i*per, (i+1)*per) sequentially, one block
 // scan combines the chunk sums.
@@ -813,42 +579,6 @@ __global__ void __launch_bounds__(1024) k_scan_tokens(const int* __restrict__ cn
   if (threadIdx.x == 0) rowptr[T] = tot;
 }
 
-// Rows of each token in ascending expert order + renormalised gates.  Pass 2 recovers the
-// expert of a row from the 128-row tile map (segments are tile aligned).
-__global__ void k_token_rows(const uint32_t* __restrict__ bm_kept, const int* __restrict__ wprefix, int T, int E,
-                             int W, const int* __restrict__ pad_offsets, const int* __restrict__ tile_expert,
-                             const int* __restrict__ rowptr, const float* __restrict__ S, int gate_raw,
-                             int* __restrict__ token_rows, float* __restrict__ row_gate) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= W) return;
-  const int t = w * 32 + lane;
-  const bool valid = t < T;
-  const uint32_t below = (1u << lane) - 1u;
-  const int j0 = valid ? rowptr[t] : 0;
-  int j = j0;
-  float sum = 0.f;
-  int e = 0;
-  for (; e < E; e += 8) {
-    uint32_t v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = (e + i < E) ? __ldg(bm_kept + (size_t)(e + i) * W + w) : 0u;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (valid && ((v[i] >> lane) & 1u)) {
-        token_rows[j++] = pad_offsets[e + i] + wprefix[(size_t)(e + i) * W + w] + __popc(v[i] & below);
-        sum += __ldg(S + (size_t)t * E + e + i);
-      }
-    }
-  }
-  if (!valid) return;
-  const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
-  for (int k = j0; k < j; ++k) {
-    const int r = token_rows[k];
-    const float s = __ldg(S + (size_t)t * E + tile_expert[r / GEMM_M]);
-    row_gate[r] = gate_raw ? s : s * inv;
-  }
-}
 
 void launch_popc(const uint32_t* bm, int W, int nrows, int* wprefix, int* cnt, cudaStream_t st) {
   k_expert_popc<<<nrows, 1024, 0, st>>>(bm, W, wprefix, cnt, nullptr);
@@ -878,13 +608,8 @@ __global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W,
   for (int e = threadIdx.x; e < E; e += blockDim.x) bm[(size_t)e * W + blockIdx.x] = words[e];
 }
 
-// ---------------------------------------------------------------- TC top-K, thread per token
-// 128 tokens per block.  Their S rows are staged through shared memory in 128-expert slabs (row
-// stride 129 words: the per-thread column walk is bank-conflict free) and each thread keeps its
-// token's top-KT ordered scores in registers by stable insertion over ascending expert ids: a
-// later expert enters only if strictly greater, so equal scores keep the lower id first -- the
-// (value desc, expert asc) order of P:1099 (Q9), exact on the ordered fp32 bits.
-constexpr int TK_TOK = 128, TK_EC = 128;
+// ---------------------------------------------------------------- TC top-K helpers
+// Inverse of ord_f32 (the ordered key of a non-negative-zero float gives the float back).
 __device__ __forceinline__ float unord_f32(uint32_t k) {
   return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
 }
@@ -905,99 +630,6 @@ __device__ __forceinline__ void bitonic_merge_desc(unsigned long long (&a)[KP], 
         a[i + d] = x > y ? y : x;
       }
     }
-  }
-}
-template <int KT>
-__global__ void __launch_bounds__(TK_TOK) k_topk_tpt(const float* __restrict__ S, int T, int E, int W,
-                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
-                                                    uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket) {
-  constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;  // list length (pow2)
-  constexpr int NL = 4;
-  extern __shared__ float tk_sm[];  // [TK_TOK][TK_EC + 1] staging, then words [E][4]
-  uint32_t* words = reinterpret_cast<uint32_t*>(tk_sm + TK_TOK * (TK_EC + 1));
-  const int tid = threadIdx.x;
-  const int tok0 = blockIdx.x * TK_TOK;
-  const int ntok = min(TK_TOK, T - tok0);
-  if (blockIdx.x == 0 && tid == 0 && ticket) {
-    ticket[0] = 0u;
-    ticket[1] = 0u;
-  }
-  for (int i = tid; i < E * 4; i += TK_TOK) words[i] = 0u;
-  uint32_t top[NL][KP];
-  int id[NL][KP];
-#pragma unroll
-  for (int l = 0; l < NL; ++l)
-#pragma unroll
-    for (int i = 0; i < KP; ++i) {
-      top[l][i] = 0u;
-      id[l][i] = 0;
-    }
-  for (int e0 = 0; e0 < E; e0 += TK_EC) {
-    const int ecn = min(TK_EC, E - e0);
-    __syncthreads();
-    if (ecn == TK_EC && (E & 3) == 0) {  // 16-byte loads: 32 per token row
-#pragma unroll 8
-      for (int i = tid; i < ntok * (TK_EC / 4); i += TK_TOK) {
-        const int tl = i / (TK_EC / 4), c4 = i % (TK_EC / 4);
-        const float4 v = __ldg(reinterpret_cast<const float4*>(S + (size_t)(tok0 + tl) * E + e0) + c4);
-        float* d = tk_sm + tl * (TK_EC + 1) + 4 * c4;
-        d[0] = v.x;
-        d[1] = v.y;
-        d[2] = v.z;
-        d[3] = v.w;
-      }
-    } else {
-      for (int tl = 0; tl < ntok; ++tl)
-        for (int ec = tid; ec < ecn; ec += TK_TOK) tk_sm[tl * (TK_EC + 1) + ec] = __ldg(S + (size_t)(tok0 + tl) * E + e0 + ec);
-    }
-    __syncthreads();
-    if (tid < ntok) {
-      const float* row = tk_sm + tid * (TK_EC + 1);
-      for (int ec = 0; ec < ecn; ec += NL) {
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          const uint32_t v = ec + l < ecn ? ord_f32(row[ec + l]) : 0u;
-          if (v > top[l][KP - 1]) {
-            const int e = e0 + ec + l;
-#pragma unroll
-            for (int i = KP - 1; i > 0; --i) {
-              const bool gi = v > top[l][i], gp = v > top[l][i - 1];
-              top[l][i] = gi ? (gp ? top[l][i - 1] : v) : top[l][i];
-              id[l][i] = gi ? (gp ? id[l][i - 1] : e) : id[l][i];
-            }
-            if (v > top[l][0]) {
-              top[l][0] = v;
-              id[l][0] = e;
-            }
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (tid < ntok) {
-    unsigned long long key[NL][KP];
-#pragma unroll
-    for (int l = 0; l < NL; ++l)
-#pragma unroll
-      for (int i = 0; i < KP; ++i)
-        key[l][i] = top[l][i] ? ((unsigned long long)top[l][i] << 32) | (0xFFFFFFFFu - (uint32_t)id[l][i]) : 0ull;
-    bitonic_merge_desc<KP>(key[0], key[1]);
-    bitonic_merge_desc<KP>(key[2], key[3]);
-    bitonic_merge_desc<KP>(key[0], key[2]);
-    const size_t t = (size_t)(tok0 + tid);
-#pragma unroll
-    for (int i = 0; i < KT; ++i) {
-      const int e = (int)(0xFFFFFFFFu - (uint32_t)(key[0][i] & 0xFFFFFFFFull));
-      topk_ids[t * KT + i] = e;
-      topk_s[t * KT + i] = unord_f32((uint32_t)(key[0][i] >> 32));
-      atomicOr(&words[e * 4 + (tid >> 5)], 1u << (tid & 31));
-    }
-  }
-  __syncthreads();
-  for (int i = tid; i < E * 4; i += TK_TOK) {
-    const int w = blockIdx.x * 4 + (i & 3);
-    if (w < W) bm_tc[(size_t)(i >> 2) * W + w] = words[i];
   }
 }
 
@@ -1158,24 +790,9 @@ void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   k_topk_g4<KT><<<W, 128, smem, st>>>(L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
 }
 
-template <int KT>
-void launch_topk_tpt(const RouteLaunch& L, cudaStream_t st) {
-  const int T = (int)L.T, E = L.E, W = L.W;
-  const int smem = (TK_TOK * (TK_EC + 1) + E * 4) * 4;
-  static int attr = 0;
-  if (attr < smem) {
-    cudaFuncSetAttribute(k_topk_tpt<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = smem;
-  }
-  k_topk_tpt<KT><<<(T + TK_TOK - 1) / TK_TOK, TK_TOK, smem, st>>>(L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc,
-                                                                 L.ticket);
-}
-void launch_topk_tpt_k(const RouteLaunch& L, cudaStream_t st) {
+void launch_topk(const RouteLaunch& L, cudaStream_t st) {
   switch (L.K) {
-#ifndef SONIC_TOPK_G4
-#define SONIC_TOPK_G4 1
-#endif
-#define TKC(k) case k: if (SONIC_TOPK_G4) launch_topk_g4<k>(L, st); else launch_topk_tpt<k>(L, st); break;
+#define TKC(k) case k: launch_topk_g4<k>(L, st); break;
     TKC(1) TKC(2) TKC(3) TKC(4) TKC(5) TKC(6) TKC(7) TKC(8)
     TKC(9) TKC(10) TKC(11) TKC(12) TKC(13) TKC(14) TKC(15) TKC(16)
 #undef TKC
@@ -1211,51 +828,26 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
     nl += 2;
     return nl;
   }
-#ifndef SONIC_TOPK_TPT
-#define SONIC_TOPK_TPT 1
-#endif
-  if (SONIC_TOPK_TPT && K <= 16 && E <= 4096) {
-    launch_topk_tpt_k(L, st);
-    ++nl;
-  } else {
-    cudaMemsetAsync(L.ticket, 0, 8, st);
-#define TOPK_CASE(G, V) \
-  k_route_topk<G, V><<<W, 32 * G, 0, st>>>(L.S, T, E, K, W, L.topk_ids, L.topk_s, L.bm_tc)
-    if (E <= 32) TOPK_CASE(4, 8);
-    else if (E <= 64) TOPK_CASE(8, 8);
-    else if (E <= 128) TOPK_CASE(8, 16);
-    else if (E <= 256) TOPK_CASE(16, 16);
-    else if (E <= 512) TOPK_CASE(32, 16);
-    else if (E <= 1024) TOPK_CASE(32, 32);
-    else if (E <= 2048) TOPK_CASE(32, 64);
-    else TOPK_CASE(32, 128);
-#undef TOPK_CASE
-    ++nl;
-  }
+  launch_topk(L, st);  // K <= 16 (validated for TC / TR)
+  ++nl;
   const uint32_t* bm_kept = L.bm_tc;
   if (L.mode == 1) {  // token rounding
     k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
     k_tr_decide<<<(E + 255) / 256, 256, 0, st>>>(L.f, L.f_r, E, T, L.m_tile); ++nl;
     k_transpose<<<dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st>>>(L.S, L.ST, T, E); ++nl;
-#ifndef SONIC_TRSEL_W
-#define SONIC_TRSEL_W 1
-#endif
-    if (SONIC_TRSEL_W && W <= 1024)
-      k_tr_select_w<true><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
-    else if (SONIC_TRSEL_W)
-      k_tr_select_w<false><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
-    else
-      k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 0);
+    auto select = [&](int rescue) {
+      if (W <= 1024)
+        k_tr_select_w<true><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, rescue);
+      else
+        k_tr_select_w<false><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip,
+                                                 rescue);
+    };
+    select(0);
     ++nl;
     if (L.rescue) {
       cudaMemsetAsync(L.flip, 0, (size_t)E * 4, st);
       k_orphans<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;
-      if (SONIC_TRSEL_W && W <= 1024)
-        k_tr_select_w<true><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
-      else if (SONIC_TRSEL_W)
-        k_tr_select_w<false><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
-      else
-        k_tr_select<<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, 1);
+      select(1);
       ++nl;
     }
     bm_kept = L.bm_kept;
