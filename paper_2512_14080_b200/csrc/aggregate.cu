@@ -4,6 +4,7 @@
 // The gate is already applied in the down-proj epilogue (Q2), so one unweighted kernel
 // serves O and dX.  HBM-bound: reads R*d*2 B, writes T*d*2 B.
 #include "sonic_internal.h"
+#include "ptx.cuh"
 
 namespace sonic {
 
@@ -29,6 +30,8 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
 __global__ void __launch_bounds__(256) k_aggregate(const __nv_bfloat16* __restrict__ Y, const int* __restrict__ rowptr,
                                                    const int* __restrict__ rows, __nv_bfloat16* __restrict__ out,
                                                    long long T, int d) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (t >= T) return;
@@ -67,6 +70,8 @@ __global__ void __launch_bounds__(256) k_aggregate(const __nv_bfloat16* __restri
 
 __global__ void k_ds_reduce(const float* __restrict__ part, int nparts, long long rows_max,
                             const int* __restrict__ num_tiles, float* __restrict__ dS) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const long long R = (long long)(*num_tiles) * GEMM_M;
   for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < R; r += (long long)gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -79,12 +84,12 @@ void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows
                       int d, cudaStream_t st) {
   const int threads = 256;
   const long long blocks = (T * 32 + threads - 1) / threads;
-  k_aggregate<<<(unsigned)blocks, threads, 0, st>>>(Y, rowptr, rows, out, T, d);
+  launch_k(k_aggregate, (unsigned)blocks, threads, 0, st, Y, rowptr, rows, out, T, d);
 }
 
 void launch_ds_reduce(const float* part, int nparts, long long rows_max, const int* num_tiles, float* dS,
                       cudaStream_t st) {
-  k_ds_reduce<<<148 * 4, 256, 0, st>>>(part, nparts, rows_max, num_tiles, dS);
+  launch_k(k_ds_reduce, 148 * 4, 256, 0, st, part, nparts, rows_max, num_tiles, dS);
 }
 
 }  // namespace sonic

@@ -16,6 +16,7 @@
 //            returned and scattered into the source's grouped-row dS.
 #include "../../include/sonic.h"
 #include "sonic_internal.h"
+#include "ptx.cuh"
 
 namespace sonic {
 
@@ -23,6 +24,8 @@ namespace sonic {
 __global__ void k_ep_mask(const int* __restrict__ rowptr, const int* __restrict__ rows,
                           const int* __restrict__ tile_expert, int T, int L, int G, int W, int* __restrict__ dmask,
                           int* __restrict__ tokcnt, uint32_t* __restrict__ bm) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ uint32_t words[32];
   if (threadIdx.x < 32) words[threadIdx.x] = 0u;
   __syncthreads();
@@ -39,6 +42,8 @@ __global__ void k_ep_mask(const int* __restrict__ rowptr, const int* __restrict_
 }
 
 __global__ void k_ep_offsets(const int* __restrict__ cnt, int G, int* __restrict__ off) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   if (threadIdx.x == 0) {
     int s = 0;
     for (int g = 0; g < G; ++g) {
@@ -56,6 +61,8 @@ __global__ void k_ep_fill(const int* __restrict__ rowptr, const int* __restrict_
                           const int* __restrict__ wprefix, const int* __restrict__ off,
                           const int* __restrict__ ep_rowptr, int* __restrict__ ep_rows, int* __restrict__ send_token,
                           float* __restrict__ send_gate) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const uint32_t mask = (uint32_t)dmask[t];
@@ -81,6 +88,8 @@ __global__ void k_ep_fill(const int* __restrict__ rowptr, const int* __restrict_
 // dst[i] = src[map[i]] for i < *count (bf16 rows of d elements, 16-byte vectors, warp per row)
 __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ src, const int* __restrict__ map,
                               const int* __restrict__ count, int d, __nv_bfloat16* __restrict__ dst) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (i >= *count) return;
@@ -93,6 +102,8 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ src, const int* 
 __global__ void k_ep_ds_dense(const int* __restrict__ row_token, const int* __restrict__ tile_expert,
                               const int* __restrict__ num_tiles, const float* __restrict__ dS, int L,
                               float* __restrict__ dense) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= (*num_tiles) * GEMM_M) return;
   const int t = row_token[r];
@@ -104,6 +115,8 @@ __global__ void k_ep_ds_scatter(const int* __restrict__ rowptr, const int* __res
                                 const int* __restrict__ tile_expert, int T, int L, const int* __restrict__ dmask,
                                 const int* __restrict__ ep_rowptr, const int* __restrict__ ep_rows,
                                 const float* __restrict__ back, float* __restrict__ dS) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= T) return;
   const uint32_t mask = (uint32_t)dmask[t];
@@ -150,12 +163,12 @@ sonic_status sonic_ep_build_plan(const sonic_moe_desc* D, int G, const sonic_rou
   if (!ep_ok(D, G) || !rt || !p) return SONIC_ERR_INVALID_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int T = (int)D->T, L = D->E / G, W = words_of(D->T);
-  k_ep_mask<<<W, 32, 0, st>>>(rt->token_rowptr, rt->token_rows, rt->tile_expert, T, L, G, W, p->dmask, p->tokcnt,
+  launch_k(k_ep_mask, W, 32, 0, st, rt->token_rowptr, rt->token_rows, rt->tile_expert, T, L, G, W, p->dmask, p->tokcnt,
                               p->bm);
   launch_popc(p->bm, W, G, p->wprefix, p->send_counts, st);
-  k_ep_offsets<<<1, 32, 0, st>>>(p->send_counts, G, p->send_offsets);
+  launch_k(k_ep_offsets, 1, 32, 0, st, p->send_counts, G, p->send_offsets);
   launch_scan_tokens(p->tokcnt, T, p->ep_rowptr, st);
-  k_ep_fill<<<(T + 127) / 128, 128, 0, st>>>(rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->row_gate, T, L, W,
+  launch_k(k_ep_fill, (T + 127) / 128, 128, 0, st, rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->row_gate, T, L, W,
                                             p->dmask, p->bm, p->wprefix, p->send_offsets, p->ep_rowptr, p->ep_rows,
                                             p->send_token, p->send_gate);
   set_last_launch_count(5);
@@ -166,7 +179,7 @@ sonic_status sonic_ep_pack(const sonic_moe_desc* D, int G, const sonic_ep_plan* 
                            void* stream) {
   if (!ep_ok(D, G) || !p || !src || !send) return SONIC_ERR_INVALID_ARG;
   const long long rows = D->T * G;
-  k_gather_rows<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  launch_k(k_gather_rows, (unsigned)((rows * 32 + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream), 
       static_cast<const __nv_bfloat16*>(src), p->send_token, p->send_offsets + G, D->d,
       static_cast<__nv_bfloat16*>(send));
   set_last_launch_count(1);
@@ -189,7 +202,7 @@ sonic_status sonic_ep_ds_dense(const sonic_moe_desc* local, const sonic_routing*
   const long long rows_max = sonic_rows_max(local);
   if (rows_max < 0) return SONIC_ERR_INVALID_ARG;
   cudaMemsetAsync(dense, 0, (size_t)local->T * local->E * sizeof(float), st);
-  k_ep_ds_dense<<<(unsigned)((rows_max + 255) / 256), 256, 0, st>>>(rt->row_token, rt->tile_expert, rt->num_tiles,
+  launch_k(k_ep_ds_dense, (unsigned)((rows_max + 255) / 256), 256, 0, st, rt->row_token, rt->tile_expert, rt->num_tiles,
                                                                      dS, local->E, dense);
   set_last_launch_count(1);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
@@ -199,7 +212,7 @@ sonic_status sonic_ep_ds_scatter(const sonic_moe_desc* D, int G, const sonic_rou
                                  const float* back, float* dS, void* stream) {
   if (!ep_ok(D, G) || !rt || !p || !back || !dS) return SONIC_ERR_INVALID_ARG;
   const int T = (int)D->T;
-  k_ep_ds_scatter<<<(T + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+  launch_k(k_ep_ds_scatter, (T + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream), 
       rt->token_rowptr, rt->token_rows, rt->tile_expert, T, D->E / G, p->dmask, p->ep_rowptr, p->ep_rows, back, dS);
   set_last_launch_count(1);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;

@@ -306,6 +306,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   const int t_first = CTA2 ? blockIdx.x / 2 : blockIdx.x;
   const int t_step = CTA2 ? gridDim.x / 2 : gridDim.x;
 
+  ptx::pdl_trigger();
   if (threadIdx.x == 0) {
     // full: leader counts its TMA expect_tx arrive (+ its 128 cp.async arrivals + the peer's relay
     // for gathered kinds); a peer counts only its own cp.async arrivals.
@@ -337,6 +338,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  ptx::pdl_wait();  // everything above is local setup; the routing / operand data come after
 
   const int total_tiles = total_tiles_of<KIND, CTA2>(args);
 

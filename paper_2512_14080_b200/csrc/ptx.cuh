@@ -13,6 +13,15 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Every libsonic kernel is launched with programmatic stream serialization (launch_k /
+// launch_gemm_t): it lets the next kernel in the stream launch as soon as all of its blocks are
+// running (pdl_trigger) and waits for the previous kernel's completion and memory (pdl_wait)
+// before touching anything that kernel produced.  Kernels call pdl_trigger(); pdl_wait(); first
+// (the GEMMs after their shared-memory / TMEM setup), so only launch latency and prologues overlap.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

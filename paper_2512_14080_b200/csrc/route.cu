@@ -21,6 +21,7 @@
 //   k_rows_tc        TC: gather map + token CSR + renormalised gates in one launch
 //   k_csr_count / k_csr_rows_chunked   general token CSR (TR, GIVEN) via 32x32 bit transposes
 #include "sonic_internal.h"
+#include "ptx.cuh"
 
 namespace sonic {
 
@@ -65,6 +66,8 @@ __device__ int block_excl_scan(int v, int* total) {
 // ---------------------------------------------------------------- per-expert popcount
 __global__ void k_expert_popc(const uint32_t* __restrict__ bm, int W, int* __restrict__ wprefix,
                               int* __restrict__ cnt, int* __restrict__ cnt2) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int e = blockIdx.x;
   int base = 0;
   for (int w0 = 0; w0 < W; w0 += blockDim.x) {
@@ -83,6 +86,8 @@ __global__ void k_expert_popc(const uint32_t* __restrict__ bm, int W, int* __res
 
 // ---------------------------------------------------------------- TR decision (NR-f)
 __global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, int E, int T, int M) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
     const int fe = f[e];
     const int up = min((fe + M - 1) / M * M, T);
@@ -93,6 +98,8 @@ __global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, in
 
 // ---------------------------------------------------------------- S -> S^T
 __global__ void k_transpose(const float* __restrict__ S, float* __restrict__ ST, int T, int E) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ float tile[32][33];
   const int e0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -139,6 +146,8 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
                                                       uint32_t* __restrict__ bm_kept, const int* __restrict__ f,
                                                       int* __restrict__ f_r, const int* __restrict__ flip,
                                                       int rescue) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ int hist[4096];
   __shared__ int s_digit, s_above;
   const int e = blockIdx.x;
@@ -272,6 +281,8 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
 // Warp per 32-token word.  A token kept by no expert flags its top-1 TC expert.
 __global__ void k_orphans(const uint32_t* __restrict__ bm_kept, int T, int E, int W, int K,
                           const int* __restrict__ topk_ids, int* __restrict__ flip) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= W) return;
@@ -355,6 +366,8 @@ __global__ void __launch_bounds__(1024) k_popc_offsets(const uint32_t* __restric
                                                        int* __restrict__ pad_offsets, int* __restrict__ tile_expert,
                                                        int* __restrict__ num_tiles, int* __restrict__ tile_pairs,
                                                        int* __restrict__ num_pairs) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int e = blockIdx.x;
   int base = 0;
   for (int w0 = 0; w0 < W; w0 += blockDim.x) {
@@ -381,6 +394,8 @@ __global__ void __launch_bounds__(1024) k_popc_offsets(const uint32_t* __restric
 __global__ void k_build_rows(const uint32_t* __restrict__ bm_kept, const int* __restrict__ wprefix, int W,
                              const int* __restrict__ f_r, const int* __restrict__ pad_offsets,
                              int* __restrict__ row_token, float* __restrict__ row_gate) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int e = blockIdx.y;
   const int base = pad_offsets[e];
   const int w = blockIdx.x * blockDim.x + threadIdx.x;
@@ -426,6 +441,8 @@ __device__ __forceinline__ uint32_t token_mask_chunk(const uint32_t* __restrict_
 
 __global__ void k_csr_count(const uint32_t* __restrict__ bm, int T, int E, int W, int* __restrict__ word_pref,
                             int* __restrict__ rowptr, unsigned* __restrict__ ticket) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w < W) {
@@ -462,6 +479,8 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ bm, const int* __restric
                            const int* __restrict__ pad_offsets, const int* __restrict__ word_pref,
                            const float* __restrict__ S, int gate_raw, int* __restrict__ rowptr,
                            int* __restrict__ token_rows, float* __restrict__ row_gate) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= W) return;
@@ -514,6 +533,8 @@ __global__ void k_csr_rows_chunked(const uint32_t* __restrict__ bm, const int* _
                                    int W, const int* __restrict__ pad_offsets, const int* __restrict__ word_pref,
                                    const float* __restrict__ S, int gate_raw, int* __restrict__ rowptr,
                                    int* __restrict__ token_rows, float* __restrict__ row_gate) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ int s_cnt[32][33];
   __shared__ float s_sum[32][33];
   __shared__ int s_base[32];
@@ -565,6 +586,8 @@ __global__ void k_csr_rows_chunked(const uint32_t* __restrict__ bm, const int* _
 // One block: thread i scans the contiguous chunk [i*per, (i+1)*per) sequentially, one block
 // scan combines the chunk sums.
 __global__ void __launch_bounds__(1024) k_scan_tokens(const int* __restrict__ cnt, int T, int* __restrict__ rowptr) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int per = (T + blockDim.x - 1) / blockDim.x;
   const int t0 = threadIdx.x * per;
   const int t1 = min(t0 + per, T);
@@ -581,10 +604,10 @@ __global__ void __launch_bounds__(1024) k_scan_tokens(const int* __restrict__ cn
 
 
 void launch_popc(const uint32_t* bm, int W, int nrows, int* wprefix, int* cnt, cudaStream_t st) {
-  k_expert_popc<<<nrows, 1024, 0, st>>>(bm, W, wprefix, cnt, nullptr);
+  launch_k(k_expert_popc, nrows, 1024, 0, st, bm, W, wprefix, cnt, nullptr);
 }
 void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st) {
-  k_scan_tokens<<<1, 1024, 0, st>>>(cnt, T, rowptr);
+  launch_k(k_scan_tokens, 1, 1024, 0, st, cnt, T, rowptr);
 }
 
 // ---------------------------------------------------------------- given routing
@@ -592,6 +615,8 @@ void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st) {
 // matrix itself, token t is routed to e iff S[t,e] != 0.  One block per 32-token word.
 __global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W, uint32_t* __restrict__ bm,
                                unsigned* __restrict__ ticket) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   __shared__ uint32_t words[4096];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     ticket[0] = 0u;
@@ -641,6 +666,8 @@ __global__ void k_rows_tc(const uint32_t* __restrict__ bm, const int* __restrict
                           float* __restrict__ row_gate, const int* __restrict__ topk_ids,
                           const float* __restrict__ topk_s, int T, int K, int gate_raw, int* __restrict__ rowptr,
                           int* __restrict__ token_rows, int nb_build, int nbw) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   if ((int)blockIdx.x < nb_build) {
     const int e = blockIdx.x / nbw;
     const int wb = blockIdx.x - e * nbw;
@@ -699,6 +726,8 @@ template <int KT>
 __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, int T, int E, int W,
                                                  int* __restrict__ topk_ids, float* __restrict__ topk_s,
                                                  uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
   extern __shared__ float tg_sm[];  // [TG_TOK][TG_STRIDE] staging, then words [E]
   uint32_t* words = reinterpret_cast<uint32_t*>(tg_sm + TG_TOK * TG_STRIDE);
@@ -787,7 +816,7 @@ void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
     cudaFuncSetAttribute(k_topk_g4<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = smem;
   }
-  k_topk_g4<KT><<<W, 128, smem, st>>>(L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
+  launch_k(k_topk_g4<KT>, W, 128, smem, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
 }
 
 void launch_topk(const RouteLaunch& L, cudaStream_t st) {
@@ -804,13 +833,13 @@ void launch_topk(const RouteLaunch& L, cudaStream_t st) {
 void launch_csr(const uint32_t* bm, const RouteLaunch& L, int gate_raw, cudaStream_t st) {
   const int T = (int)L.T, E = L.E, W = L.W;
   const int blocks = (W * 32 + 255) / 256;
-  k_csr_count<<<blocks, 256, 0, st>>>(bm, T, E, W, L.tokcnt, L.token_rowptr, L.ticket + 1);
+  launch_k(k_csr_count, blocks, 256, 0, st, bm, T, E, W, L.tokcnt, L.token_rowptr, L.ticket + 1);
   const int nch = (E + 31) / 32;
   if (nch <= 32)
-    k_csr_rows_chunked<<<W, 32 * nch, 0, st>>>(bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw,
+    launch_k(k_csr_rows_chunked, W, 32 * nch, 0, st, bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw,
                                                L.token_rowptr, L.token_rows, L.row_gate);
   else
-    k_csr_rows<<<blocks, 256, 0, st>>>(bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw,
+    launch_k(k_csr_rows, blocks, 256, 0, st, bm, L.wprefix, T, E, W, L.pad_offsets, L.tokcnt, L.S, gate_raw,
                                        L.token_rowptr, L.token_rows, L.row_gate);
 }
 
@@ -819,10 +848,10 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   int nl = 0;
   const int T = (int)L.T, E = L.E, K = L.K, W = L.W;
   if (L.mode == 2) {  // given routing: bitmap, counts, offsets, rows, CSR with raw gates
-    k_given_bitmap<<<W, 256, 0, st>>>(L.S, T, E, W, L.bm_tc, L.ticket); ++nl;
-    k_popc_offsets<<<E, 1024, 0, st>>>(L.bm_tc, W, L.wprefix, L.f, L.f_r, L.ticket, L.offsets, L.pad_offsets,
+    launch_k(k_given_bitmap, W, 256, 0, st, L.S, T, E, W, L.bm_tc, L.ticket); ++nl;
+    launch_k(k_popc_offsets, E, 1024, 0, st, L.bm_tc, W, L.wprefix, L.f, L.f_r, L.ticket, L.offsets, L.pad_offsets,
                                        L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
-    k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(L.bm_tc, L.wprefix, W, L.f_r, L.pad_offsets,
+    launch_k(k_build_rows, dim3((W + 255) / 256, E), 256, 0, st, L.bm_tc, L.wprefix, W, L.f_r, L.pad_offsets,
                                                            L.row_token, L.row_gate); ++nl;
     launch_csr(L.bm_tc, L, 1, st);
     nl += 2;
@@ -832,29 +861,29 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   ++nl;
   const uint32_t* bm_kept = L.bm_tc;
   if (L.mode == 1) {  // token rounding
-    k_expert_popc<<<E, 1024, 0, st>>>(L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
-    k_tr_decide<<<(E + 255) / 256, 256, 0, st>>>(L.f, L.f_r, E, T, L.m_tile); ++nl;
-    k_transpose<<<dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st>>>(L.S, L.ST, T, E); ++nl;
+    launch_k(k_expert_popc, E, 1024, 0, st, L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
+    launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile); ++nl;
+    launch_k(k_transpose, dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st, L.S, L.ST, T, E); ++nl;
     auto select = [&](int rescue) {
       if (W <= 1024)
-        k_tr_select_w<true><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, rescue);
+        launch_k(k_tr_select_w<true>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, rescue);
       else
-        k_tr_select_w<false><<<E, 1024, 0, st>>>(L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip,
+        launch_k(k_tr_select_w<false>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip,
                                                  rescue);
     };
     select(0);
     ++nl;
     if (L.rescue) {
       cudaMemsetAsync(L.flip, 0, (size_t)E * 4, st);
-      k_orphans<<<(W * 32 + 255) / 256, 256, 0, st>>>(L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;
+      launch_k(k_orphans, (W * 32 + 255) / 256, 256, 0, st, L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;
       select(1);
       ++nl;
     }
     bm_kept = L.bm_kept;
-    k_popc_offsets<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f_r, nullptr, L.ticket, L.offsets, L.pad_offsets,
+    launch_k(k_popc_offsets, E, 1024, 0, st, bm_kept, W, L.wprefix, L.f_r, nullptr, L.ticket, L.offsets, L.pad_offsets,
                                        L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
   } else {  // TC: one pass gives f, f_r (== f), the word prefixes and the offsets
-    k_popc_offsets<<<E, 1024, 0, st>>>(bm_kept, W, L.wprefix, L.f, L.f_r, L.ticket, L.offsets, L.pad_offsets,
+    launch_k(k_popc_offsets, E, 1024, 0, st, bm_kept, W, L.wprefix, L.f, L.f_r, L.ticket, L.offsets, L.pad_offsets,
                                        L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
   }
   if (L.mode == 0) {
@@ -862,11 +891,11 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
     const int nb_build = nbw * E;
     const long long tk = (long long)T * K + 1;
     const int nb_tok = (int)((tk + 255) / 256);
-    k_rows_tc<<<nb_build + nb_tok, 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
+    launch_k(k_rows_tc, nb_build + nb_tok, 256, 0, st, bm_kept, L.wprefix, W, L.f_r, L.pad_offsets, L.row_token,
                                                  L.row_gate, L.topk_ids, L.topk_s, T, K, L.gate_raw,
                                                  L.token_rowptr, L.token_rows, nb_build, nbw); ++nl;
   } else {
-    k_build_rows<<<dim3((W + 255) / 256, E), 256, 0, st>>>(bm_kept, L.wprefix, W, L.f_r, L.pad_offsets,
+    launch_k(k_build_rows, dim3((W + 255) / 256, E), 256, 0, st, bm_kept, L.wprefix, W, L.f_r, L.pad_offsets,
                                                            L.row_token, L.row_gate); ++nl;
     launch_csr(bm_kept, L, L.gate_raw, st);
     nl += 2;

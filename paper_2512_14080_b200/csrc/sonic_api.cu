@@ -155,13 +155,15 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   cfg.blockDim = dim3(gemm_threads<KIND>());
   cfg.dynamicSmemBytes = Cfg::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attrs[1];
+  cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
   attrs[0].val.clusterDim.x = CTA2 ? 2 : 1;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = SONIC_PDL ? 1 : 0;
   cfg.attrs = attrs;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
 #ifdef SONIC_TIMING
   static unsigned long long* dbg = nullptr;
   if (!dbg) cudaMalloc(&dbg, 16 * sizeof(unsigned long long));

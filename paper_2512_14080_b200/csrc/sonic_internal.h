@@ -6,6 +6,26 @@
 
 namespace sonic {
 
+#ifndef SONIC_PDL
+#define SONIC_PDL 1  // programmatic dependent launch between consecutive libsonic kernels
+#endif
+// Kernel launch with the programmatic-stream-serialization attribute (see ptx.cuh pdl_*).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = SONIC_PDL ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 constexpr int GEMM_M = 128;  // grouped-row tile (== TR m_tile, Q16)
 
 struct RouteLaunch {
