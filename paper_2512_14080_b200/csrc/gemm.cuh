@@ -81,10 +81,19 @@ __host__ __device__ constexpr int num_producer_warps() {
 #define SONIC_EPI_WARPS 4
 #endif
 constexpr int EPI_WARPS = SONIC_EPI_WARPS;
-constexpr int EPI_HALVES = EPI_WARPS / 4;
+// Per-kind epilogue warp count (8 = two warps per TMEM lane quarter, each taking every other
+// 64-column chunk).  The down-proj (K = n: few k-blocks per tile) waits on its epilogue, but
+// 8 warps did not help it; all kinds use SONIC_EPI_WARPS = 4.
+#ifndef SONIC_EPI_WARPS_DOWN
+#define SONIC_EPI_WARPS_DOWN 4  // 8 measured slower at 7B (247 vs 239 us)
+#endif
+template <int KIND>
+__host__ __device__ constexpr int epi_warps() {
+  return KIND == K_DOWN ? SONIC_EPI_WARPS_DOWN : EPI_WARPS;
+}
 template <int KIND>
 __host__ __device__ constexpr int gemm_threads() {
-  return 32 * (num_producer_warps<KIND>() + 1 + EPI_WARPS);
+  return 32 * (num_producer_warps<KIND>() + 1 + epi_warps<KIND>());
 }
 
 constexpr int GEMM_BM = 128;
@@ -95,21 +104,23 @@ constexpr int STG_BYTES = 4096;  // one epilogue staging buffer: 32 rows x 128 B
 #endif
 constexpr int SMEM_LIMIT = SONIC_SMEM_LIMIT;
 
-template <int BN, bool CTA2, bool HTMA, int NB_, bool HRING_ = false>
+template <int BN, bool CTA2, bool HTMA, int NB_, bool HRING_ = false, int EPW_ = EPI_WARPS>
 struct GemmCfg {
+  static constexpr int EPW = EPW_;       // epilogue warps
+  static constexpr int EPH = EPW_ / 4;   // warps per TMEM lane quarter
   static constexpr int BNL = CTA2 ? BN / 2 : BN;  // B columns (or rows) held by this CTA
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;
   static constexpr uint32_t B_BYTES = BNL * GEMM_BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int NB = NB_;  // epilogue staging buffers per epilogue warp (ring)
   // DH only: per-epilogue-warp H buffer, 32 rows x (gate + up) bf16 columns of the warp's chunks
-  static constexpr int HCOLS_WARP = (BN / EPI_HALVES) < 64 ? 64 : BN / EPI_HALVES;
+  static constexpr int HCOLS_WARP = (BN / EPH) < 64 ? 64 : BN / EPH;
   // HRING (DH, BN = 256): instead of the whole tile row, a 2-slot ring of 64-column chunks
   // (gate 4 KB + up 4 KB per slot) streams H through each epilogue warp
   static constexpr bool HRING = HRING_;
   static constexpr int HBUF_WARP = HRING ? 2 * 2 * STG_BYTES : HTMA ? 32 * 2 * HCOLS_WARP * 2 : 0;
   // + 1 KB alignment slack + barriers / dS exchange / TMEM address (< 1 KB)
-  static constexpr int FIXED = EPI_WARPS * NB * STG_BYTES + EPI_WARPS * HBUF_WARP + 1024 + 1024;
+  static constexpr int FIXED = EPW * NB * STG_BYTES + EPW * HBUF_WARP + 1024 + 1024;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - FIXED) / (int)STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
@@ -122,7 +133,7 @@ struct GemmCfg {
 // stage, measured slower).
 template <int KIND, int BN, bool CTA2>
 using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128, (KIND == K_DH && BN == 256) ? 0 : 2,
-                     KIND == K_DH && BN == 256>;
+                     KIND == K_DH && BN == 256, epi_warps<KIND>()>;
 
 struct TileCoord {
   int e, row0, nt, mt, nkb, seg0;
@@ -290,13 +301,13 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stg = smem + STAGES * STAGE_BYTES;
-  uint8_t* hbuf = stg + EPI_WARPS * Cfg::NB * STG_BYTES;  // DH: EPI_WARPS x HBUF_WARP
-  uint64_t* full = reinterpret_cast<uint64_t*>(hbuf + EPI_WARPS * Cfg::HBUF_WARP);
+  uint8_t* hbuf = stg + Cfg::EPW * Cfg::NB * STG_BYTES;  // DH: Cfg::EPW x HBUF_WARP
+  uint64_t* full = reinterpret_cast<uint64_t*>(hbuf + Cfg::EPW * Cfg::HBUF_WARP);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* hfull = tempty + 2;  // DH: one per epilogue warp (HRING: two, one per ring slot)
-  float* ds_xchg = reinterpret_cast<float*>(hfull + 2 * EPI_WARPS);  // DH: [4][32] partial dS of half 1
+  float* ds_xchg = reinterpret_cast<float*>(hfull + 2 * Cfg::EPW);  // DH: [4][32] partial dS of half 1
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(ds_xchg + 128);
 
   const int warp = threadIdx.x >> 5;
@@ -317,9 +328,9 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
-      ptx::mbar_init(&tempty[s], CTA2 ? 2 * EPI_WARPS : EPI_WARPS);
+      ptx::mbar_init(&tempty[s], CTA2 ? 2 * Cfg::EPW : Cfg::EPW);
     }
-    for (int s = 0; s < 2 * EPI_WARPS; ++s) ptx::mbar_init(&hfull[s], 1);
+    for (int s = 0; s < 2 * Cfg::EPW; ++s) ptx::mbar_init(&hfull[s], 1);
     ptx::fence_barrier_init();
     ptx::prefetch_tmap(&mA);
     ptx::prefetch_tmap(&mB);
@@ -589,7 +600,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     }
     __syncwarp();
   } else {
-    // ============================================================ epilogue (EPI_WARPS warps)
+    // ============================================================ epilogue (Cfg::EPW warps)
     const int ew = warp - NP - 1;
     const int q = warp & 3;         // TMEM lane quarter this warp may access
     const int half = ew / 4;        // which interleaved 64-column chunks (32 for fp32) it handles
@@ -606,15 +617,15 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         if (lane == 0) {
           const TileCoord th = decode_tile<KIND, CTA2>(args, t, rank);
           if constexpr (BN >= 64) {
-            // this warp's chunks c = half, half + EPI_HALVES, ... (local index lc): gate box at
+            // this warp's chunks c = half, half + Cfg::EPH, ... (local index lc): gate box at
             // lc * 4 KB, up box at (NLC + lc) * 4 KB
-            constexpr int NLC = (BN / 64 + EPI_HALVES - 1) / EPI_HALVES;
+            constexpr int NLC = (BN / 64 + Cfg::EPH - 1) / Cfg::EPH;
             int nb = 0;
 #pragma unroll
-            for (int c = half, lc = 0; c < BN / 64; c += EPI_HALVES, ++lc) nb += 2;
+            for (int c = half, lc = 0; c < BN / 64; c += Cfg::EPH, ++lc) nb += 2;
             ptx::mbar_arrive_expect_tx(&hfull[ew], nb * STG_BYTES);
 #pragma unroll
-            for (int c = half, lc = 0; c < BN / 64; c += EPI_HALVES, ++lc) {
+            for (int c = half, lc = 0; c < BN / 64; c += Cfg::EPH, ++lc) {
               ptx::tma_load_2d(hb + lc * STG_BYTES, &mD, &hfull[ew], th.nt * BN + 64 * c, th.row0 + 32 * q);
               ptx::tma_load_2d(hb + (NLC + lc) * STG_BYTES, &mD, &hfull[ew], args.n + th.nt * BN + 64 * c,
                                th.row0 + 32 * q);
@@ -711,7 +722,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         constexpr int W = BN / 2;
         if constexpr (W >= 64) {
 #pragma unroll 1
-          for (int c = 64 * half; c < W; c += 64 * EPI_HALVES) {
+          for (int c = 64 * half; c < W; c += 64 * Cfg::EPH) {
             const int col = tc.nt * W + c;
             sq.template acquire<1>(lane);  // the next two ring slots are both free
             const int i0 = sq.sb;
@@ -783,7 +794,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
         __nv_bfloat16* orow = args.out + (size_t)row * args.N_dim + tc.nt * BN;
 #pragma unroll 1
-        for (int c = 64 * half; c < BN; c += 64 * EPI_HALVES) {
+        for (int c = 64 * half; c < BN; c += 64 * Cfg::EPH) {
           if (tc.nt * BN + c >= args.N_dim) break;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
@@ -808,7 +819,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         float gate = 1.f;
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
 #pragma unroll 1
-        for (int c = 64 * half; c < BN; c += 64 * EPI_HALVES) {
+        for (int c = 64 * half; c < BN; c += 64 * Cfg::EPH) {
           if (tc.nt * BN + c >= args.N_dim) break;
           const int i = sq.acquire(lane);
           const uint32_t b = sq.addr(i);
@@ -916,8 +927,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           ptx::mbar_wait(&hfull[ew], hphase);
           hphase ^= 1;
 #pragma unroll 1
-          for (int c = half, lc = 0; c < BN / 64; c += EPI_HALVES, ++lc) {
-            constexpr int NLC = (BN / 64 + EPI_HALVES - 1) / EPI_HALVES;
+          for (int c = half, lc = 0; c < BN / 64; c += Cfg::EPH, ++lc) {
+            constexpr int NLC = (BN / 64 + Cfg::EPH - 1) / Cfg::EPH;
             const int col = tc.nt * BN + 64 * c;
             const uint32_t gb = ptx::smem_u32(hb + lc * STG_BYTES);          // H gate -> dH gate
             const uint32_t ub = ptx::smem_u32(hb + (NLC + lc) * STG_BYTES);  // H up   -> dH up
@@ -1044,7 +1055,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             h_issue(tile + t_step);
           }
         }
-        if constexpr (EPI_HALVES == 2) {  // combine the two halves' partial dS of each row
+        if constexpr (Cfg::EPH == 2) {  // combine the two halves' partial dS of each row
           const uint32_t bar_id = 1 + q;     // named barrier per lane quarter (64 threads)
           if (half == 1) ds_xchg[32 * q + lane] = ds;
           asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
@@ -1081,7 +1092,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         const int m0 = tc.mt * GEMM_BM + 32 * q;
         if (m0 < args.M_dim) {
 #pragma unroll 1
-          for (int c = 32 * half; c < BN; c += 32 * EPI_HALVES) {
+          for (int c = 32 * half; c < BN; c += 32 * Cfg::EPH) {
             if (tc.nt * BN + c >= args.N_dim) break;
             const int i = sq.acquire(lane);
             const uint32_t b = sq.addr(i);
