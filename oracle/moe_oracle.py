@@ -118,6 +118,64 @@ def round_nrf(f, M):
     return np.where((up - f) < (f - dn), up, dn)
 
 
+def round_balance(f, M, T=None):
+    """Balance-f (Alg. 6): one pass over the experts in index order with the
+    accumulator z of the residuals chosen so far; expert e pads (rounds up) iff
+    |r_up + z| < |r_down + z| (strict, as printed), else it drops (rounds down).  The up option is
+    capped at T first (Q15), so r_up uses the capped count."""
+    f = np.asarray(f, dtype=np.int64)
+    out = np.empty_like(f)
+    z = 0
+    for e, fe in enumerate(f):
+        up = int(round_up(fe, M))
+        if T is not None:
+            up = min(up, T)
+        dn = int(round_down(fe, M))
+        r_up, r_dn = up - int(fe), dn - int(fe)
+        if abs(r_up + z) < abs(r_dn + z):
+            out[e] = up
+            z += r_up
+        else:
+            out[e] = dn
+            z += r_dn
+    return out
+
+
+_MASK64 = (1 << 64) - 1
+
+
+def sr_u64(seed, e):
+    """The counter-based generator of SR-f (Q21): SplitMix64's output function applied to
+    the state (seed << 32 | e) + 0x9E3779B97F4A7C15 (one step of SplitMix64 from that state)."""
+    x = (((int(seed) & 0xFFFFFFFF) << 32) | (int(e) & 0xFFFFFFFF)) + 0x9E3779B97F4A7C15
+    x &= _MASK64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _MASK64
+    return x ^ (x >> 31)
+
+
+def round_sr(f, M, seed, T=None):
+    """SR-f: expert e pads with probability (f_e - floor(f_e)) / M.  The draw is
+    u_e = sr_u64(seed, e) >> 40, uniform on [0, 2^24); pad iff u_e / 2^24 < (f_e - floor) / M,
+    i.e. u_e * M < (f_e - floor) * 2^24 (exact integer comparison)."""
+    f = np.asarray(f, dtype=np.int64)
+    out = np.empty_like(f)
+    for e, fe in enumerate(f):
+        up = int(round_up(fe, M))
+        if T is not None:
+            up = min(up, T)
+        dn = int(round_down(fe, M))
+        u = sr_u64(seed, e) >> 40
+        out[e] = up if u * M < (int(fe) - dn) * (1 << 24) else dn
+    return out
+
+
+def ec_capacity(T, K, E, M):
+    """Expert-choice capacity (Q22): the average TC load ceil(T K / E), rounded up to a multiple of
+    M_tile and capped at T."""
+    return min(int(round_up(-(-T * K // E), M)), T)
+
+
 def _rank_expert_column(S_col, tc_col):
     """Alg. 4 steps (3)-(4) for one expert: pi_e = sort(S'_e) descending.
 
@@ -173,10 +231,18 @@ class Routing:
         return int(self.pad_offsets[-1])
 
 
-def route(S, K, mode="tc", m_tile=128, rescue=True, gate_raw=False):
-    """Routing per Alg. 4 or plain TC.
+TR_ROUNDINGS = ("nrf", "up", "down", "balance", "sr")
 
-    mode "tc": kept = TC top-K set.  mode "tr": token rounding with NR-f.
+
+def route(S, K, mode="tc", m_tile=128, rescue=True, gate_raw=False, rounding="nrf", seed=0):
+    """Routing per Alg. 4, plain TC or expert choice.
+
+    mode "tc": kept = TC top-K set.
+    mode "tr": token rounding; ``rounding`` picks the subroutine of App.: "nrf"
+      (default, P:2174), "up" (P:2194), "down" (P:2196), "balance" (Alg. 6), "sr" (P:2176, the
+      draws from ``sr_u64(seed, e)``).  The orphan rescue (Q14) applies to every subroutine.
+    mode "ec": expert choice (NEXT-3, Q22): every expert keeps the ``ec_capacity`` highest-scoring
+      tokens (S desc, token asc); no rescue -- tokens no expert chose have no rows.
     """
     S = np.asarray(S, dtype=np.float64)
     T, E = S.shape
@@ -188,9 +254,27 @@ def route(S, K, mode="tc", m_tile=128, rescue=True, gate_raw=False):
     if mode == "tc":
         f_r = f.copy()
         kept = tc.copy()
+    elif mode == "ec":
+        C = ec_capacity(T, K, E, m_tile)
+        f_r = np.full(E, C, dtype=np.int64)
+        kept = np.zeros((T, E), dtype=bool)
+        for e in range(E):
+            order = np.lexsort((np.arange(T), -S[:, e]))       # S desc, token asc
+            kept[order[:C], e] = True
     elif mode == "tr":
         f_up = np.minimum(round_up(f, m_tile), T)              # Q15: cap at T
-        f_r = np.minimum(round_nrf(f, m_tile), T)              # round_and_sparsify (NR-f)
+        if rounding == "nrf":
+            f_r = np.minimum(round_nrf(f, m_tile), T)          # round_and_sparsify (NR-f)
+        elif rounding == "up":
+            f_r = f_up.copy()
+        elif rounding == "down":
+            f_r = round_down(f, m_tile).astype(np.int64)
+        elif rounding == "balance":
+            f_r = round_balance(f, m_tile, T)
+        elif rounding == "sr":
+            f_r = round_sr(f, m_tile, seed, T)
+        else:
+            raise ValueError(rounding)
         kept = np.zeros((T, E), dtype=bool)
 
         def select(e):                                         # step (4), one expert

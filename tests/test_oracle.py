@@ -307,3 +307,91 @@ def test_per_token_entry_points_match_full_passes():
     for (t, e), v in dSs.items():
         i = list(np.nonzero(rt.kept[:, e])[0]).index(t)
         assert v == pytest.approx(bw.dS[e][i], abs=1e-13)
+
+
+# ---------------------------------------------------------------- NEXT-3 rounding subroutines, EC
+def test_round_up_down_golden():
+    """UP / DOWN: the M-multiples above / below f, by hand."""
+    f = np.array([0, 1, 63, 64, 65, 127, 128, 200])
+    assert om.round_up(f, 64).tolist() == [0, 64, 64, 64, 128, 128, 128, 256]
+    assert om.round_down(f, 64).tolist() == [0, 0, 0, 64, 64, 64, 128, 192]
+
+
+def test_balance_hand_traced():
+    """Alg. 6 traced by hand.  M=4, f=(1,1,1,1): z: -1 (|3-0|<|-1-0| no), -2 (2<2 no),
+    +1 (1<3 yes), 0 (4<0 no) -> (0,0,4,0).  f=(3,3,3): up z=1; |2|<|-2| no -> down z=-2; up z=-1."""
+    assert om.round_balance([1, 1, 1, 1], 4).tolist() == [0, 0, 4, 0]
+    assert om.round_balance([3, 3, 3], 4).tolist() == [4, 0, 4]
+    assert om.round_balance([4, 8, 0], 4).tolist() == [4, 8, 0]  # multiples are kept
+
+
+@pytest.mark.parametrize("M", [4, 16, 128])
+def test_balance_invariants(M):
+    """Alg. 6's guarantee |sum_e f_r - sum_e f| <= M/2, each f_r one of the two
+    neighbouring multiples."""
+    rng = np.random.default_rng(M)
+    for _ in range(200):
+        f = rng.integers(0, 5 * M, size=rng.integers(1, 40))
+        fr = om.round_balance(f, M)
+        assert abs(int(fr.sum()) - int(f.sum())) <= M // 2
+        assert np.all((fr == om.round_up(f, M)) | (fr == om.round_down(f, M)))
+
+
+def test_sr_generator_is_splitmix64():
+    """sr_u64(0, 0) is one SplitMix64 step from state 0: the generator's published first output
+    for seed 0, 0xE220A8397B1DCDAF."""
+    assert om.sr_u64(0, 0) == 0xE220A8397B1DCDAF
+
+
+def test_sr_rounding_probabilities():
+    """SR-f: pad with probability (f - floor f)/M; multiples never move."""
+    M = 128
+    f = np.array([128 + 32, 256 + 96, 384, 7])  # p = 0.25, 0.75, 0 (multiple), 7/128
+    ups = np.zeros(len(f))
+    n = 3000
+    for seed in range(n):
+        fr = om.round_sr(f, M, seed)
+        assert np.all((fr == om.round_up(f, M)) | (fr == om.round_down(f, M)))
+        ups += fr > f
+    rate = ups / n
+    assert abs(rate[0] - 0.25) < 0.03 and abs(rate[1] - 0.75) < 0.03
+    assert rate[2] == 0.0 and abs(rate[3] - 7 / 128) < 0.02
+
+
+def test_ec_brute_force():
+    """Expert choice: every expert keeps the C highest scores (ties to the lower token), C from
+    ec_capacity; brute force with Python's sort on tiny inputs, including exact ties."""
+    rng = np.random.default_rng(3)
+    T, E, K, M = 40, 6, 2, 4
+    S = np.round(rng.random((T, E)) * 8) / 8  # quantised: exact ties
+    C = om.ec_capacity(T, K, E, M)
+    assert C == 16  # ceil(80/6) = 14 -> 16
+    rt = om.route(S, K, mode="ec", m_tile=M)
+    for e in range(E):
+        want = sorted(range(T), key=lambda t: (-S[t, e], t))[:C]
+        assert set(np.nonzero(rt.kept[:, e])[0].tolist()) == set(want)
+    assert np.all(rt.f_rounded == C)
+
+
+@pytest.mark.parametrize("rounding", ["up", "down", "balance", "sr"])
+def test_tr_subroutine_route_invariants(rounding):
+    """Every subroutine: f_r is a multiple of M (or T), the kept set of an expert is its TC set
+    plus / minus the best / worst-ranked tokens (up: TC subset of kept; down: kept subset of TC),
+    kept counts equal f_r, and the rescue leaves no orphan."""
+    rng = np.random.default_rng(11)
+    T, E, K, M = 200, 8, 2, 16
+    S = rng.random((T, E))
+    rt = om.route(S, K, mode="tr", m_tile=M, rounding=rounding, seed=5)
+    tc = np.zeros((T, E), bool)
+    tc[np.arange(T)[:, None], rt.topk_ids] = True
+    for e in range(E):
+        fr, fe = int(rt.f_rounded[e]), int(rt.f[e])
+        assert fr % M == 0 or fr == T
+        assert rt.kept[:, e].sum() == fr
+        if fr >= fe:
+            assert np.all(rt.kept[tc[:, e], e])
+        else:
+            assert not np.any(rt.kept[~tc[:, e], e])
+    assert rt.kept.any(axis=1).all()
+    if rounding == "up":
+        assert np.all(rt.f_rounded == np.minimum(om.round_up(rt.f, M), T))
