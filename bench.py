@@ -27,6 +27,9 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# --mode -> (sonic route mode, oracle mode, oracle rounding); tr = NR-f (the paper's default)
+ROUTE_MODES = {"tc": (0, "tc", "nrf"), "tr": (1, "tr", "nrf"), "tr_up": (3, "tr", "up"), "tr_down": (4, "tr", "down"),
+               "tr_balance": (5, "tr", "balance"), "tr_sr": (6, "tr", "sr"), "ec": (7, "ec", "nrf")}
 METRIC = "MoE layer fwd+bwd TFLOPS (% B200 BF16 peak), tokens/s at 1/2/4/8 GPU; act. mem"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
@@ -142,7 +145,8 @@ def oracle_sample(cfg, mode, seed, T_sample):
     f64 = lambda t: t.float().numpy().astype(np.float64)
     X, W1, W2, dO, S = f64(inp.X), f64(inp.W1), f64(inp.W2), f64(inp.dO), inp.S.numpy()
     t0 = time.perf_counter()
-    rt = om.route(S, c["K"], mode=mode, m_tile=128)
+    _, omode, rounding = ROUTE_MODES[mode]
+    rt = om.route(S, c["K"], mode=omode, m_tile=128, rounding=rounding)
     om.forward(X, W1, W2, rt)
     om.backward(dO, X, W1, W2, rt)
     dt = time.perf_counter() - t0
@@ -191,7 +195,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="sonic", choices=["sonic", "reference"])
     ap.add_argument("--config", default="7b")
-    ap.add_argument("--mode", default="tc", choices=["tc", "tr"])
+    ap.add_argument("--mode", default="tc", choices=list(ROUTE_MODES))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--ref-tokens", type=int, default=1024)
@@ -223,7 +227,7 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     T, d, n, E, K = cfg["T"], cfg["d"], cfg["n"], cfg["E"], cfg["K"]
-    mode = sonic.SONIC_ROUTE_TC if args.mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
+    mode = ROUTE_MODES[args.mode][0]
     desc = sonic.make_desc(T, d, n, E, K, mode=mode)
     use_ep = args.ep or world > 1
     if not use_ep:

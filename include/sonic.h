@@ -56,9 +56,19 @@ typedef enum {
 typedef enum {
   SONIC_ROUTE_TC = 0,      /* token-choice top-K */
   SONIC_ROUTE_TR_NRF = 1,  /* token rounding, Alg. 4 with NR-f */
-  SONIC_ROUTE_GIVEN = 2    /* arbitrary routing input: S is the gate matrix, t -> e iff
+  SONIC_ROUTE_GIVEN = 2,   /* arbitrary routing input: S is the gate matrix, t -> e iff
                               S[t,e] != 0, gate = S[t,e] (no renormalisation); topk_ids/topk_s are
                               not written; K may be up to E.  Used by the expert-parallel receive side. */
+  /* Token rounding with the other subroutines of the ablation; selection, rescue and
+   * gates as for SONIC_ROUTE_TR_NRF. */
+  SONIC_ROUTE_TR_UP = 3,       /* always pad: f_r = min(ceil_M(f), T) */
+  SONIC_ROUTE_TR_DOWN = 4,     /* always drop: f_r = floor_M(f) */
+  SONIC_ROUTE_TR_BALANCE = 5,  /* Balance-f, Alg. 6: sequential residual accumulator */
+  SONIC_ROUTE_TR_SR = 6,       /* SR-f: pad with probability (f - floor_M f)/M; the draw of
+                                  expert e is SplitMix64 from state (seed << 32 | e), top 24 bits (Q21) */
+  SONIC_ROUTE_EC = 7           /* expert choice (NEXT-3, Q22): each expert keeps its C best tokens,
+                                  C = min(ceil_M(ceil(T K / E)), T); no orphan rescue (tokens no expert
+                                  chose have no rows and get O = dX = 0) */
 } sonic_route_mode;
 
 /* flags */
@@ -72,6 +82,7 @@ typedef struct {
   int32_t m_tile;      /* TR rounding tile; must be 128 (the GEMM M tile) */
   int32_t route_mode;  /* sonic_route_mode */
   int32_t flags;       /* SONIC_F_* */
+  uint32_t seed;       /* SONIC_ROUTE_TR_SR: seed of the rounding draws (ignored otherwise) */
 } sonic_moe_desc;
 
 /* Routing metadata: written by sonic_route, read by sonic_moe_fwd/bwd.

@@ -10,7 +10,8 @@
 //                    scores, bitonic merges on exact 64-bit keys; ties -> lower expert id;
 //                    P:1072-1099, Q9) -> topk, TC bitmap
 //   k_expert_popc    per-expert popcount + exclusive word prefix (histogram f_e)
-//   k_tr_decide      NR-f rounding decision
+//   k_tr_decide      rounding decision: NR-f, UP, DOWN, Balance-f, SR-f
+//                    (P:2116-2198); expert choice capacity (Q22)
 //   k_transpose      S -> S^T so expert columns are contiguous (TR only)
 //   k_tr_select_w    Alg. 4 step (4): per expert, keep the top f_r of the ranking
 //                    (in-TC, S, -t) via radix select on the ordered score + token tie pass
@@ -20,6 +21,7 @@
 //   k_build_rows     gather map row_token (+ pad rows)
 //   k_rows_tc        TC: gather map + token CSR + renormalised gates in one launch
 //   k_csr_count / k_csr_rows_chunked   general token CSR (TR, GIVEN) via 32x32 bit transposes
+#include <algorithm>
 #include "sonic_internal.h"
 #include "ptx.cuh"
 
@@ -85,14 +87,54 @@ __global__ void k_expert_popc(const uint32_t* __restrict__ bm, int W, int* __res
 }
 
 // ---------------------------------------------------------------- TR decision (NR-f)
-__global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, int E, int T, int M) {
+// SR-f draw of expert e (Q21): one SplitMix64 step from state (seed << 32 | e), top 24 bits.
+__device__ __forceinline__ uint32_t sr_draw24(uint32_t seed, uint32_t e) {
+  unsigned long long x = (((unsigned long long)seed << 32) | e) + 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return (uint32_t)(x >> 40);
+}
+
+// Rounding decision per expert.  rounding: 0 NR-f (strict '<': an exact M/2 tie
+// rounds down, Q11), 1 up, 2 down, 3 Balance-f (Alg. 6: sequential, one thread), 4 SR-f.
+// ec_cap >= 0: expert choice, every expert takes ec_cap tokens.
+__global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, int E, int T, int M, int rounding,
+                            uint32_t seed, int ec_cap) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  if (rounding == 3 && ec_cap < 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      long long z = 0;
+      for (int e = 0; e < E; ++e) {
+        const int fe = f[e];
+        const int up = min((fe + M - 1) / M * M, T);
+        const int dn = fe / M * M;
+        const long long ru = up - fe, rd = dn - fe;
+        const bool pick_up = llabs(ru + z) < llabs(rd + z);
+        f_r[e] = pick_up ? up : dn;
+        z += pick_up ? ru : rd;
+      }
+    }
+    return;
+  }
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    if (ec_cap >= 0) {
+      f_r[e] = ec_cap;
+      continue;
+    }
     const int fe = f[e];
     const int up = min((fe + M - 1) / M * M, T);
     const int dn = fe / M * M;
-    f_r[e] = (up - fe) < (fe - dn) ? up : dn;  // strict '<': exact M/2 ties round down (Q11)
+    int r;
+    switch (rounding) {
+      case 1: r = up; break;
+      case 2: r = dn; break;
+      case 4: r = (unsigned long long)sr_draw24(seed, (uint32_t)e) * (unsigned)M <
+                          ((unsigned long long)(fe - dn) << 24) ? up : dn; break;
+      default: r = (up - fe) < (fe - dn) ? up : dn; break;
+    }
+    f_r[e] = r;
   }
 }
 
@@ -145,14 +187,15 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
                                                       const uint32_t* __restrict__ bm_tc,
                                                       uint32_t* __restrict__ bm_kept, const int* __restrict__ f,
                                                       int* __restrict__ f_r, const int* __restrict__ flip,
-                                                      int rescue) {
+                                                      int rescue, int ec) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   __shared__ int hist[4096];
   __shared__ int s_digit, s_above;
   const int e = blockIdx.x;
   const int tid = threadIdx.x;
-  const int fc = f[e];
+  // expert choice: no TC set -- every token is a candidate and the kept set is the selection
+  const int fc = ec ? 0 : f[e];
   int fr;
   if (rescue) {
     if (!flip[e]) return;
@@ -161,10 +204,11 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
   } else {
     fr = f_r[e];
   }
-  const uint32_t* tcw = bm_tc + (size_t)e * W;
+  const uint32_t* tcw_p = bm_tc + (size_t)e * W;
+  auto tcw = [&](int w) -> uint32_t { return ec ? 0u : tcw_p[w]; };
   uint32_t* kw = bm_kept + (size_t)e * W;
   if (fr == fc) {
-    for (int w = tid; w < W; w += blockDim.x) kw[w] = tcw[w];
+    for (int w = tid; w < W; w += blockDim.x) kw[w] = tcw(w);
     return;
   }
   const bool up = fr > fc;
@@ -182,7 +226,7 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
       load_word_keys(col, T, tid, o);
 #pragma unroll
       for (int i = 0; i < 32; ++i) okeep[i] = o[i];
-      cand1 = (up ? ~tcw[tid] : tcw[tid]);
+      cand1 = (up ? ~tcw(tid) : tcw(tid));
       if (tid * 32 + 32 > T) cand1 &= (T - tid * 32 >= 32) ? ~0u : ((1u << (T - tid * 32)) - 1u);
     }
   }
@@ -203,7 +247,7 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
       for (int w = tid; w < W; w += blockDim.x) {
         uint32_t o[32];
         load_word_keys(col, T, w, o);
-        const uint32_t cand = up ? ~tcw[w] : tcw[w];
+        const uint32_t cand = up ? ~tcw(w) : tcw(w);
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           if (((cand >> i) & 1u) && w * 32 + i < T && (o[i] & pmask) == prefix)
@@ -254,7 +298,7 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
       } else {
         uint32_t o[32];
         load_word_keys(col, T, w, o);
-        const uint32_t cand = up ? ~tcw[w] : tcw[w];
+        const uint32_t cand = up ? ~tcw(w) : tcw(w);
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const bool c = ((cand >> i) & 1u) && w * 32 + i < T;
@@ -272,7 +316,7 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
       sel |= b;
       eq ^= b;
     }
-    if (w < W) kw[w] = up ? (tcw[w] | gt | sel) : (gt | sel);
+    if (w < W) kw[w] = up ? (tcw(w) | gt | sel) : (gt | sel);
     run += tot;
   }
 }
@@ -860,20 +904,27 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   launch_topk(L, st);  // K <= 16 (validated for TC / TR)
   ++nl;
   const uint32_t* bm_kept = L.bm_tc;
-  if (L.mode == 1) {  // token rounding
+  if (L.mode == 1 || L.mode == 3) {  // token rounding (any subroutine) or expert choice
+    const bool ec = L.mode == 3;
+    int ec_cap = -1;
+    if (ec) {  // Q22: ceil(T K / E) rounded up to a tile, capped at T
+      const long long avg = ((long long)T * K + E - 1) / E;
+      ec_cap = (int)std::min<long long>((avg + L.m_tile - 1) / L.m_tile * L.m_tile, T);
+    }
     launch_k(k_expert_popc, E, 1024, 0, st, L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
-    launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile); ++nl;
+    launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile, L.rounding, L.seed, ec_cap); ++nl;
     launch_k(k_transpose, dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st, L.S, L.ST, T, E); ++nl;
     auto select = [&](int rescue) {
       if (W <= 1024)
-        launch_k(k_tr_select_w<true>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip, rescue);
+        launch_k(k_tr_select_w<true>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip,
+                 rescue, ec ? 1 : 0);
       else
         launch_k(k_tr_select_w<false>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip,
-                                                 rescue);
+                 rescue, ec ? 1 : 0);
     };
     select(0);
     ++nl;
-    if (L.rescue) {
+    if (L.rescue && !ec) {
       cudaMemsetAsync(L.flip, 0, (size_t)E * 4, st);
       launch_k(k_orphans, (W * 32 + 255) / 256, 256, 0, st, L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;
       select(1);

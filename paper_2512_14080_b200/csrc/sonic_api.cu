@@ -228,8 +228,7 @@ bool valid_desc(const sonic_moe_desc* D) {
   if (D->K > D->E || D->E > 4096) return false;
   if (D->K > 16 && D->route_mode != SONIC_ROUTE_GIVEN) return false;
   if (D->m_tile != 128) return false;
-  if (D->route_mode != SONIC_ROUTE_TC && D->route_mode != SONIC_ROUTE_TR_NRF && D->route_mode != SONIC_ROUTE_GIVEN)
-    return false;
+  if (D->route_mode < SONIC_ROUTE_TC || D->route_mode > SONIC_ROUTE_EC) return false;
   return true;
 }
 bool supported_dims(const sonic_moe_desc* D) {
@@ -274,7 +273,8 @@ RouteWs route_ws(const sonic_moe_desc* D) {
   w.tokcnt = o; o += al((size_t)s.T * 4);
   w.flip = o; o += al((size_t)s.E * 4);
   w.ticket = o; o += al(8);  // [0] offsets ticket, [1] token-CSR ticket
-  w.ST = o; o += (D->route_mode == SONIC_ROUTE_TR_NRF) ? al((size_t)s.T * s.E * 4) : 0;
+  const bool needs_st = D->route_mode != SONIC_ROUTE_TC && D->route_mode != SONIC_ROUTE_GIVEN;
+  w.ST = o; o += needs_st ? al((size_t)s.T * s.E * 4) : 0;
   w.total = o;
   return w;
 }
@@ -414,7 +414,17 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   uint8_t* base = static_cast<uint8_t*>(ws);
   RouteLaunch L{};
   L.T = s.T; L.E = s.E; L.K = s.K; L.W = s.W; L.m_tile = D->m_tile;
-  L.mode = D->route_mode;  // 0 TC, 1 TR (NR-f), 2 given
+  // launcher modes: 0 TC, 1 TR (rounding subroutine in L.rounding), 2 given, 3 expert choice
+  switch (D->route_mode) {
+    case SONIC_ROUTE_TC: L.mode = 0; break;
+    case SONIC_ROUTE_GIVEN: L.mode = 2; break;
+    case SONIC_ROUTE_EC: L.mode = 3; break;
+    default:
+      L.mode = 1;
+      L.rounding = D->route_mode == SONIC_ROUTE_TR_NRF ? 0 : D->route_mode - SONIC_ROUTE_TR_UP + 1;
+      break;
+  }
+  L.seed = D->seed;
   L.rescue = (D->flags & SONIC_F_NO_ORPHAN_RESCUE) ? 0 : 1;
   L.gate_raw = (D->flags & SONIC_F_GATE_RAW) ? 1 : 0;
   L.S = S;

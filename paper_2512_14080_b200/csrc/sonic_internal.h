@@ -31,6 +31,8 @@ constexpr int GEMM_M = 128;  // grouped-row tile (== TR m_tile, Q16)
 struct RouteLaunch {
   long long T;
   int E, K, W, m_tile, mode, rescue, gate_raw;
+  int rounding;   // mode 1 (TR): 0 NR-f, 1 up, 2 down, 3 Balance-f, 4 SR-f; mode 3 = expert choice
+  uint32_t seed;  // SR-f draws
   const float* S;
   // outputs
   int *topk_ids, *f, *f_r, *offsets, *pad_offsets, *row_token, *token_rowptr, *token_rows, *tile_expert,

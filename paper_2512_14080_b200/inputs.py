@@ -20,6 +20,9 @@ CONFIGS = {
     "qwen3": dict(T=32768, d=2048, n=768, E=128, K=8),
     "dsv3": dict(T=65536, d=7168, n=2048, E=256, K=8),
     "kimi": dict(T=65536, d=7168, n=2048, E=384, K=8),
+    # the paper's token-rounding speed study (Table 14 / Fig. 12: T, d, n, K = 16384, 1536,
+    # 1024, 2 at E = 128): TC vs TR context, not a BASELINE.json config
+    "tr_study": dict(T=16384, d=1536, n=1024, E=128, K=2),
 }
 
 

@@ -17,6 +17,14 @@ LIB_PATH = os.path.join(_HERE, "libsonic.so")
 
 SONIC_ROUTE_TC = 0
 SONIC_ROUTE_TR_NRF = 1
+SONIC_ROUTE_TR_UP = 3
+SONIC_ROUTE_TR_DOWN = 4
+SONIC_ROUTE_TR_BALANCE = 5
+SONIC_ROUTE_TR_SR = 6
+SONIC_ROUTE_EC = 7
+# oracle route(mode, rounding) of each TR-family mode
+ROUTE_MODE_NAMES = {0: ("tc", "nrf"), 1: ("tr", "nrf"), 3: ("tr", "up"), 4: ("tr", "down"), 5: ("tr", "balance"),
+                    6: ("tr", "sr"), 7: ("ec", "nrf")}
 SONIC_F_GATE_RAW = 1
 SONIC_F_NO_ORPHAN_RESCUE = 2
 GEMM_M = 128
@@ -29,7 +37,7 @@ _FLOAT_FIELDS = {"topk_s", "row_gate"}
 class sonic_moe_desc(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("n", ctypes.c_int32), ("E", ctypes.c_int32),
                 ("K", ctypes.c_int32), ("m_tile", ctypes.c_int32), ("route_mode", ctypes.c_int32),
-                ("flags", ctypes.c_int32)]
+                ("flags", ctypes.c_int32), ("seed", ctypes.c_uint32)]
 
 
 class sonic_routing(ctypes.Structure):
@@ -116,8 +124,8 @@ def _done(status, what):
     LAUNCHES[0] += int(lib().sonic_last_launch_count())
 
 
-def make_desc(T, d, n, E, K, mode=SONIC_ROUTE_TC, m_tile=128, flags=0):
-    return sonic_moe_desc(T, d, n, E, K, m_tile, mode, flags)
+def make_desc(T, d, n, E, K, mode=SONIC_ROUTE_TC, m_tile=128, flags=0, seed=0):
+    return sonic_moe_desc(T, d, n, E, K, m_tile, mode, flags, seed)
 
 
 def _ptr(t):

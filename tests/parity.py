@@ -100,13 +100,13 @@ def f64(t):
     return t.detach().float().cpu().numpy().astype(np.float64)
 
 
-def full_parity(desc, inp, mode="tc", check_ws=True):
+def full_parity(desc, inp, mode="tc", check_ws=True, rounding="nrf"):
     """Element-by-element parity of every output at a size the oracle finishes in seconds."""
     g = run_gpu(desc, inp, want_ws=check_ws)
     S = inp.S.cpu().numpy()
     rto = om.route(S, desc.K, mode=mode, m_tile=desc.m_tile,
                    rescue=not (desc.flags & sonic.SONIC_F_NO_ORPHAN_RESCUE),
-                   gate_raw=bool(desc.flags & sonic.SONIC_F_GATE_RAW))
+                   gate_raw=bool(desc.flags & sonic.SONIC_F_GATE_RAW), rounding=rounding, seed=desc.seed)
     gr = routing_to_numpy(g["rt"], desc)
     check_routing(gr, rto)
     X, W1, W2, dO = f64(inp.X), f64(inp.W1), f64(inp.W2), f64(inp.dO)

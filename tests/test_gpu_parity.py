@@ -28,3 +28,38 @@ def test_small_parity(case):
     desc = sonic.make_desc(T, d, n, E, K, mode=m)
     stats = full_parity(desc, inp, mode=mode)
     print(name, {k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
+
+
+# NEXT-3: the other token-rounding subroutines and expert choice, against the oracle
+VARIANTS = [
+    ("up", sonic.SONIC_ROUTE_TR_UP), ("down", sonic.SONIC_ROUTE_TR_DOWN),
+    ("balance", sonic.SONIC_ROUTE_TR_BALANCE), ("sr", sonic.SONIC_ROUTE_TR_SR), ("ec", sonic.SONIC_ROUTE_EC),
+]
+
+
+@pytest.mark.parametrize("shape", [(1000, 128, 64, 16, 4), (2048, 256, 128, 16, 4)], ids=["ragged", "multi"])
+@pytest.mark.parametrize("name,m", VARIANTS, ids=[v[0] for v in VARIANTS])
+def test_routing_variants_parity(name, m, shape):
+    T, d, n, E, K = shape
+    inp = make_inputs(T, d, n, E, K, seed=2, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K, mode=m, seed=12345)
+    mode, rounding = sonic.ROUTE_MODE_NAMES[m]
+    stats = full_parity(desc, inp, mode=mode, rounding=rounding)
+    print(name, {k: f"{v[0]:.2e}" for k, v in stats.items()})
+
+
+def test_sr_seed_changes_decisions():
+    """SR-f draws depend on the descriptor's seed (and match the oracle for each)."""
+    from tests.parity import check_routing, routing_to_numpy
+    from oracle import moe_oracle as om
+    T, d, n, E, K = 4096, 64, 64, 64, 8
+    inp = make_inputs(T, d, n, E, K, seed=4, device="cuda")
+    frs = []
+    for seed in (1, 2, 3):
+        desc = sonic.make_desc(T, d, n, E, K, mode=sonic.SONIC_ROUTE_TR_SR, seed=seed)
+        rt = sonic.sonic_route(desc, inp.S)
+        torch.cuda.synchronize()
+        g = routing_to_numpy(rt, desc)
+        check_routing(g, om.route(inp.S.cpu().numpy(), K, mode="tr", rounding="sr", seed=seed))
+        frs.append(tuple(g["f_rounded"].tolist()))
+    assert len(set(frs)) > 1
