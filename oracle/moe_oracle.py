@@ -558,3 +558,47 @@ def arithmetic_intensity(T, d, n, E, K):
     """Eq. 4: 3 / ((2+2G)/d + 3/(T rho)), G = d/n, rho = K/E."""
     G, rho = d / n, K / E
     return 3.0 / ((2 + 2 * G) / d + 3.0 / (T * rho))
+
+
+# --------------------------------------------------------------------------
+# Router backward (NEXT-4): dS -> d logits through the renormalisation and the softmax
+# --------------------------------------------------------------------------
+def router_backward(S, rt: Routing, dS_te, gate_raw=False):
+    """d logits of the router for a fixed routing (the top-K / rounding choice is piecewise
+    constant and has no gradient).
+
+    Gates (P:1488, Q13): g_te = S_te / Z_t with Z_t = sum_{e' kept for t} S_te' (or g = S with
+    ``gate_raw``).  Chain rule, written per token:
+      dS_full_te = (dS_te - sum_{e' kept} dS_te' g_te') / Z_t   for kept e, 0 otherwise
+      (gate_raw: dS_full_te = dS_te for kept e);
+      d logit_tj = S_tj (dS_full_tj - sum_i S_ti dS_full_ti)      (softmax Jacobian, S = softmax).
+    ``dS_te`` is a dense [T, E] array holding dL/dg_te on kept (t, e) and zeros elsewhere.
+    """
+    S = np.asarray(S, dtype=np.float64)
+    dS_te = np.asarray(dS_te, dtype=np.float64)
+    kept = rt.kept
+    T, E = S.shape
+    dfull = np.zeros((T, E))
+    for t in range(T):
+        ks = np.nonzero(kept[t])[0]
+        if len(ks) == 0:
+            continue
+        if gate_raw:
+            dfull[t, ks] = dS_te[t, ks]
+        else:
+            Z = S[t, ks].sum()
+            g = S[t, ks] / Z
+            dfull[t, ks] = (dS_te[t, ks] - np.dot(dS_te[t, ks], g)) / Z
+    dot = (S * dfull).sum(axis=1, keepdims=True)
+    return S * (dfull - dot)
+
+
+def dS_dense(rt: Routing, dS_by_expert):
+    """The per-expert dS lists of ``backward`` as a dense [T, E] array (zeros off the kept set)."""
+    T, E = rt.kept.shape
+    out = np.zeros((T, E))
+    for e in range(E):
+        toks = np.nonzero(rt.kept[:, e])[0]
+        if len(toks):
+            out[toks, e] = dS_by_expert[e]
+    return out

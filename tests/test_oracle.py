@@ -395,3 +395,49 @@ def test_tr_subroutine_route_invariants(rounding):
     assert rt.kept.any(axis=1).all()
     if rounding == "up":
         assert np.all(rt.f_rounded == np.minimum(om.round_up(rt.f, M), T))
+
+
+# ---------------------------------------------------------------- NEXT-4 router backward
+@pytest.mark.parametrize("gate_raw", [False, True])
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+def test_router_backward_finite_differences(mode, gate_raw):
+    """d logits from router_backward equals central finite differences of
+    L(logits) = sum_{kept (t,e)} g_te(softmax(logits)) c_te with the routing (kept sets) frozen."""
+    rng = np.random.default_rng(21 if gate_raw else 22)
+    T, E, K, M = 12, 6, 2, 4
+    logits = rng.normal(size=(T, E))
+    S = np.exp(logits - logits.max(1, keepdims=True))
+    S /= S.sum(1, keepdims=True)
+    rt = om.route(S, K, mode=mode, m_tile=M, gate_raw=gate_raw)
+    c = rng.normal(size=(T, E)) * rt.kept
+
+    def loss(lg):
+        s = np.exp(lg - lg.max(1, keepdims=True))
+        s /= s.sum(1, keepdims=True)
+        if gate_raw:
+            g = np.where(rt.kept, s, 0.0)
+        else:
+            z = np.where(rt.kept, s, 0.0).sum(1, keepdims=True)
+            g = np.where(rt.kept, s / np.where(z == 0, 1.0, z), 0.0)
+        return float((g * c).sum())
+
+    got = om.router_backward(S, rt, c, gate_raw=gate_raw)
+    h = 1e-6
+    fd = np.zeros_like(logits)
+    for t in range(T):
+        for j in range(E):
+            lp, lm = logits.copy(), logits.copy()
+            lp[t, j] += h
+            lm[t, j] -= h
+            fd[t, j] = (loss(lp) - loss(lm)) / (2 * h)
+    np.testing.assert_allclose(got, fd, rtol=1e-6, atol=1e-8)
+
+
+def test_router_backward_rows_sum_to_zero():
+    """softmax Jacobian: every row of d logits sums to 0 (shifting all logits changes nothing)."""
+    rng = np.random.default_rng(5)
+    S = rng.random((30, 8))
+    S /= S.sum(1, keepdims=True)
+    rt = om.route(S, 3, mode="tc")
+    d = om.router_backward(S, rt, rng.normal(size=S.shape) * rt.kept)
+    np.testing.assert_allclose(d.sum(1), 0.0, atol=1e-12)
