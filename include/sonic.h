@@ -165,6 +165,19 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc *desc, const void *dO, const voi
                            void *dX, float *dW1, float *dW2, float *dS,
                            void *ws, size_t ws_bytes, void *stream);
 
+/*
+ * sonic_router_bwd -- NEXT-4: the router's backward from dS to d logits for the routing in rt
+ * (the top-K / rounding choice is piecewise constant: no gradient through it).
+ *   g_te = S_te / Z_t, Z_t = sum of S over t's kept experts (Q13; g = S with
+ *   SONIC_F_GATE_RAW).  dS_full_te = (dS_te - sum_e' dS_te' g_te') / Z_t on kept (t,e), 0 elsewhere;
+ *   d logit_tj = S_tj (dS_full_tj - sum_i S_ti dS_full_ti)  (S = softmax(logits) row-wise).
+ *   S [T,E] fp32 (the scores sonic_route used); dS [rows_max] fp32 from sonic_moe_bwd;
+ *   dlogits [T,E] fp32 output (every entry written; tokens with no expert get 0).
+ * Not valid for SONIC_ROUTE_GIVEN (no softmax there): returns SONIC_ERR_INVALID_ARG.
+ */
+sonic_status sonic_router_bwd(const sonic_moe_desc *desc, const float *S, const sonic_routing *rt,
+                              const float *dS, float *dlogits, void *stream);
+
 const char *sonic_status_string(sonic_status s);
 
 /* Number of kernels the last sonic_route / sonic_moe_fwd / sonic_moe_bwd / sonic_ep_* compute call on

@@ -80,6 +80,62 @@ __global__ void k_ds_reduce(const float* __restrict__ part, int nparts, long lon
   }
 }
 
+// Router backward (NEXT-4): warp per token.  The token's kept rows come from the CSR, the expert of
+// a row from the 128-row tile map; lanes then write the E-wide d logits row.
+__global__ void k_router_bwd(const float* __restrict__ S, const int* __restrict__ rowptr,
+                             const int* __restrict__ rows, const int* __restrict__ tile_expert,
+                             const float* __restrict__ dS, long long T, int E, int gate_raw,
+                             float* __restrict__ dlogits) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const long long t = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= T) return;
+  const float* st = S + t * E;
+  const int r0 = __ldg(rowptr + t), r1 = __ldg(rowptr + t + 1);
+  // pass 1 over the kept rows (lanes stride): Z = sum S, c = sum dS * S (so sum dS g = c / Z)
+  float z = 0.f, c = 0.f;
+  for (int j = r0 + lane; j < r1; j += 32) {
+    const int r = __ldg(rows + j);
+    const int e = __ldg(tile_expert + r / GEMM_M);
+    const float s = __ldg(st + e);
+    z += s;
+    c += __ldg(dS + r) * s;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    z += __shfl_xor_sync(0xffffffffu, z, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  // dS_full on kept experts; dot = sum S dS_full
+  const float invz = (z == 0.f) ? 0.f : 1.f / z;
+  const float cg = c * invz;  // sum_e dS_e g_e
+  float dot = 0.f;
+  for (int j = r0 + lane; j < r1; j += 32) {
+    const int r = __ldg(rows + j);
+    const int e = __ldg(tile_expert + r / GEMM_M);
+    const float full = gate_raw ? __ldg(dS + r) : (__ldg(dS + r) - cg) * invz;
+    dot += __ldg(st + e) * full;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  float* out = dlogits + t * E;
+  for (int e = lane; e < E; e += 32) out[e] = -__ldg(st + e) * dot;
+  __syncwarp();
+  for (int j = r0 + lane; j < r1; j += 32) {  // kept experts: S_e (dS_full_e - dot)
+    const int r = __ldg(rows + j);
+    const int e = __ldg(tile_expert + r / GEMM_M);
+    const float full = gate_raw ? __ldg(dS + r) : (__ldg(dS + r) - cg) * invz;
+    out[e] = __ldg(st + e) * (full - dot);
+  }
+}
+
+void launch_router_bwd(const float* S, const int* rowptr, const int* rows, const int* tile_expert, const float* dS,
+                       long long T, int E, int gate_raw, float* dlogits, cudaStream_t st) {
+  const long long blocks = (T * 32 + 255) / 256;
+  launch_k(k_router_bwd, (unsigned)blocks, 256, 0, st, S, rowptr, rows, tile_expert, dS, T, E, gate_raw, dlogits);
+}
+
 void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows, __nv_bfloat16* out, long long T,
                       int d, cudaStream_t st) {
   const int threads = 256;

@@ -374,6 +374,20 @@ const char* sonic_status_string(sonic_status s) {
   return "unknown status";
 }
 
+sonic_status sonic_router_bwd(const sonic_moe_desc* D, const float* S, const sonic_routing* rt, const float* dS,
+                              float* dlogits, void* stream) {
+  g_launches = 0;
+  if (!valid_desc(D) || D->route_mode == SONIC_ROUTE_GIVEN || !S || !rt || !dS || !dlogits) return SONIC_ERR_INVALID_ARG;
+  if (!rt->token_rowptr || !rt->token_rows || !rt->tile_expert) return SONIC_ERR_INVALID_ARG;
+  {
+    ProfScope ps("router_bwd", static_cast<cudaStream_t>(stream));
+    launch_router_bwd(S, rt->token_rowptr, rt->token_rows, rt->tile_expert, dS, D->T, D->E,
+                      (D->flags & SONIC_F_GATE_RAW) ? 1 : 0, dlogits, static_cast<cudaStream_t>(stream));
+    ++g_launches;
+  }
+  return check_launch();
+}
+
 int sonic_last_launch_count(void) { return g_launches; }
 
 void sonic_profile_enable(int on) { g_prof = on != 0; }

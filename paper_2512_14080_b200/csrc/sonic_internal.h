@@ -51,6 +51,9 @@ void launch_popc(const uint32_t* bm, int W, int nrows, int* wprefix, int* cnt, c
 // exclusive scan of cnt[0..T) into rowptr[0..T] (single block)
 void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st);
 
+// router backward (sonic_router_bwd)
+void launch_router_bwd(const float* S, const int* rowptr, const int* rows, const int* tile_expert, const float* dS,
+                       long long T, int E, int gate_raw, float* dlogits, cudaStream_t st);
 // aggregation: out[t] = sum_{r in rows(t)} Y[r] (fp32 accumulation in CSR order)
 void launch_aggregate(const __nv_bfloat16* Y, const int* rowptr, const int* rows, __nv_bfloat16* out, long long T,
                       int d, cudaStream_t st);

@@ -84,6 +84,8 @@ def lib():
         L.sonic_moe_bwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, vp, vp, P(sonic_routing), vp, vp, vp, vp, vp,
                                     sz, vp]
         L.sonic_moe_bwd.restype = ctypes.c_int
+        L.sonic_router_bwd.argtypes = [P(sonic_moe_desc), vp, P(sonic_routing), vp, vp, vp]
+        L.sonic_router_bwd.restype = ctypes.c_int
         L.sonic_status_string.argtypes = [ctypes.c_int]
         L.sonic_status_string.restype = ctypes.c_char_p
         L.sonic_last_launch_count.argtypes = []
@@ -251,6 +253,15 @@ def sonic_moe_bwd(desc, dO, X, H, W1, W2, rt, dX=None, dW1=None, dW2=None, dS=No
                                ctypes.byref(rt.c), _ptr(dX), _ptr(dW1), _ptr(dW2), _ptr(dS), _ptr(ws), ws.numel(),
                                _stream()), "sonic_moe_bwd")
     return dX, dW1, dW2, dS, ws
+
+
+def sonic_router_bwd(desc, S, rt, dS, dlogits=None):
+    """sonic_router_bwd: dS [rows_max] fp32 -> d logits [T,E] fp32 (NEXT-4)."""
+    if dlogits is None:
+        dlogits = torch.empty(desc.T, desc.E, dtype=torch.float32, device=S.device)
+    _done(lib().sonic_router_bwd(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(dS), _ptr(dlogits),
+                                 _stream()), "sonic_router_bwd")
+    return dlogits
 
 
 def ws_view(ws, offset, shape, dtype):

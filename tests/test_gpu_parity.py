@@ -63,3 +63,33 @@ def test_sr_seed_changes_decisions():
         check_routing(g, om.route(inp.S.cpu().numpy(), K, mode="tr", rounding="sr", seed=seed))
         frs.append(tuple(g["f_rounded"].tolist()))
     assert len(set(frs)) > 1
+
+
+@pytest.mark.parametrize("mode,m,flags", [("tc", sonic.SONIC_ROUTE_TC, 0), ("tr", sonic.SONIC_ROUTE_TR_NRF, 0),
+                                          ("tc", sonic.SONIC_ROUTE_TC, sonic.SONIC_F_GATE_RAW),
+                                          ("ec", sonic.SONIC_ROUTE_EC, 0)], ids=["tc", "tr", "tc_raw", "ec"])
+def test_router_bwd_parity(mode, m, flags):
+    """NEXT-4: sonic_router_bwd on the GPU's own dS equals the oracle's router_backward (fp64) on that
+    same dS (fp32 arithmetic: 1e-5 relative)."""
+    import numpy as np
+    from oracle import moe_oracle as om
+    from tests.parity import routing_to_numpy, check_routing
+    T, d, n, E, K = 1000, 128, 64, 16, 4
+    inp = make_inputs(T, d, n, E, K, seed=9, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K, mode=m, flags=flags)
+    rt = sonic.sonic_route(desc, inp.S)
+    O, H, _ = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
+    _, _, _, dS, _ = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+    dl = sonic.sonic_router_bwd(desc, inp.S, rt, dS)
+    torch.cuda.synchronize()
+    S = inp.S.cpu().numpy()
+    rto = om.route(S, K, mode=mode, m_tile=128, gate_raw=bool(flags & sonic.SONIC_F_GATE_RAW))
+    check_routing(routing_to_numpy(rt, desc), rto)
+    dSg = dS.cpu().numpy().astype(np.float64)
+    dense = np.zeros((T, E))
+    rows = np.nonzero(rto.row_token >= 0)[0]
+    dense[rto.row_token[rows], rto.row_expert[rows]] = dSg[rows]
+    ref = om.router_backward(S, rto, dense, gate_raw=bool(flags & sonic.SONIC_F_GATE_RAW))
+    got = dl.cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < 1e-5, err
