@@ -462,6 +462,9 @@ def main():
         "tokens_per_s": T * world / (ms_step * 1e-3),
         "model_flops_per_step": flops_all, "rows_routed": R, "rows_padded": R_pad,
         "layer_roofline_ms": layer_roof_ms, "layer_roofline_frac": layer_roof_ms / ms_step,
+        # the same metric without sonic_route (the paper's bounds exclude the router)
+        "value_excl_route": (flops_all / ((ms_step - kernels["route"]["avg_ms"] * kernels["route"]["launches_per_step"])
+                                          * 1e-3) / 1e12) if "route" in kernels else None,
         "act_mem_bytes": act,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
         "clocks": clk, "kernels": kernels, "peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops",
