@@ -104,7 +104,7 @@ bool map3d(CUtensorMap* m, const void* ptr, bool f32, long long E, long long row
 }
 
 #ifndef SONIC_BWD_OVERLAP
-#define SONIC_BWD_OVERLAP 1  // measured at 7B: 0 -> 784/795, 1 -> 800/801, 2 -> 792/800 TFLOPS
+#define SONIC_BWD_OVERLAP 3  // 7B, same run: 0 -> 2.186 ms, 1 -> 2.180, 3 -> 2.183 / 2.141 (dW1 then runs alone)
 #endif
 // One internal non-blocking stream (+ fork/join events) per device, for the backward's
 // weight-gradient branch.  Created on first use; calls from several host threads on the same
@@ -573,13 +573,14 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   //   0  everything on the caller's stream;
   //   1  the dX aggregation on an internal side stream forked after dX~, co-residing with the
   //      dW2/dW1 CTAs on the caller's stream;
-  //   2  dW2/dW1 on the side stream forked after dH; dX~ then the aggregation on the caller's.
+  //   2  dW2/dW1 on the side stream forked after dH; dX~ then the aggregation on the caller's;
+  //   3  the dX aggregation on the side stream overlapping dW2 only, joined before dW1.
   // The side stream is joined before returning.
   const int mode = SONIC_BWD_OVERLAP;
   SideStream& ss = side_stream();
   if (mode != 0 && !ss.ok) return SONIC_ERR_CUDA;
   const cudaStream_t s_dw = mode == 2 ? ss.s : st;
-  const cudaStream_t s_agg = mode == 1 ? ss.s : st;
+  const cudaStream_t s_agg = (mode == 1 || mode == 3) ? ss.s : st;
   if (mode == 2) {
     cudaEventRecord(ss.fork, st);
     cudaStreamWaitEvent(ss.s, ss.fork, 0);
@@ -640,6 +641,14 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     run_agg();
     if (!run_dw1()) return SONIC_ERR_CUDA;
     cudaEventRecord(ss.join, ss.s);
+  } else if (mode == 3) {  // the aggregation overlaps dW2 only; dW1 runs alone
+    cudaEventRecord(ss.fork, st);
+    cudaStreamWaitEvent(ss.s, ss.fork, 0);
+    run_agg();
+    cudaEventRecord(ss.join, ss.s);
+    if (!run_dw2()) return SONIC_ERR_CUDA;
+    cudaStreamWaitEvent(st, ss.join, 0);
+    if (!run_dw1()) return SONIC_ERR_CUDA;
   } else {
     if (!run_dw2() || !run_dw1()) return SONIC_ERR_CUDA;
     run_agg();
