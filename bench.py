@@ -151,7 +151,11 @@ def oracle_sample(cfg, mode, seed, T_sample):
     om.backward(dO, X, W1, W2, rt)
     dt = time.perf_counter() - t0
     flops = 18 * c["d"] * c["n"] * rt.R
-    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    try:  # the BLAS pool numpy actually used
+        from threadpoolctl import threadpool_info
+        threads = max([p.get("num_threads", 1) for p in threadpool_info() if p.get("user_api") == "blas"] or [1])
+    except Exception:
+        threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
     return flops, dt, threads
 
 
