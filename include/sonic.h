@@ -74,6 +74,9 @@ typedef enum {
 /* flags */
 #define SONIC_F_GATE_RAW         1  /* gate = S_te (no renormalisation over the kept set, Q13) */
 #define SONIC_F_NO_ORPHAN_RESCUE 2  /* TR: skip the orphan rescue (Q14) */
+#define SONIC_F_DW_ACCUMULATE    4  /* sonic_moe_bwd: dW1 += ..., dW2 += ... (fp32 element-wise adds done by
+                                       the TMA store unit; one add per element per call, so deterministic)
+                                       instead of overwriting -- gradient accumulation over microbatches */
 
 typedef struct {
   int64_t T;           /* tokens in the microbatch */
@@ -156,7 +159,8 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc *desc, const void *X, const void
  * dX aggregation.
  *   dO [T,d] bf16; X, H_cache, W1, W2, rt as in the forward.
  *   dX  [T,d] bf16 output.
- *   dW1 [E,d,2n] fp32, dW2 [E,n,d] fp32 outputs, overwritten (experts with no rows get 0).
+ *   dW1 [E,d,2n] fp32, dW2 [E,n,d] fp32 outputs, overwritten (experts with no rows get 0), or
+ *       accumulated into with SONIC_F_DW_ACCUMULATE (experts with no rows unchanged).
  *   dS  [rows_max] fp32 output: dL/dg for each grouped row (0 on pad rows).  The router
  *       backward (renormalisation/softmax Jacobian) is outside the boundary.
  */

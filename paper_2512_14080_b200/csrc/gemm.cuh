@@ -59,6 +59,7 @@ struct GemmArgs {
   long long rows_max;
   __nv_bfloat16* out;       // DOWN / DXT: the output rows [rows_max, N_dim] (direct-store epilogue)
   unsigned long long* dbg;  // SONIC_TIMING builds only: cycle counters (see sonic_api.cu)
+  int accumulate;           // DW1 / DW2: add into the existing dW (SONIC_F_DW_ACCUMULATE) instead of overwriting
 };
 
 template <int KIND>
@@ -248,11 +249,13 @@ struct StoreQ {
     }
     sb = (i + 1) % NB;
   }
-  __device__ __forceinline__ void issue3d(int lane, int i, const CUtensorMap* map, int c0, int c1, int c2) {
+  __device__ __forceinline__ void issue3d(int lane, int i, const CUtensorMap* map, int c0, int c1, int c2,
+                                          bool add = false) {
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0 && (SONIC_EXP_EPI == 0 || SONIC_EXP_EPI == 3)) {
-      ptx::tma_store_3d(map, base + i * STG_BYTES, c0, c1, c2);
+      if (add) ptx::tma_reduce_add_3d(map, base + i * STG_BYTES, c0, c1, c2);
+      else ptx::tma_store_3d(map, base + i * STG_BYTES, c0, c1, c2);
       ptx::bulk_commit();
     }
     sb = (i + 1) % NB;
@@ -1090,7 +1093,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         }
       } else {  // K_DW2 / K_DW1: fp32 weight gradient tile [128 x BN] of expert e
         const int m0 = tc.mt * GEMM_BM + 32 * q;
-        if (m0 < args.M_dim) {
+        // accumulate (dW += tile, TMA reduce-add): an expert with no rows adds nothing
+        if (m0 < args.M_dim && !(args.accumulate && tc.nkb == 0)) {
 #pragma unroll 1
           for (int c = 32 * half; c < BN; c += 32 * Cfg::EPH) {
             if (tc.nt * BN + c >= args.N_dim) break;
@@ -1107,7 +1111,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
 #pragma unroll
               for (int ch = 0; ch < 8; ++ch) ptx::st_shared_v4(b + swz(lane, ch), 0u, 0u, 0u, 0u);
             }
-            sq.issue3d(lane, i, &mC0, tc.nt * BN + c, m0, tc.e);
+            sq.issue3d(lane, i, &mC0, tc.nt * BN + c, m0, tc.e, args.accumulate != 0);
           }
         }
       }

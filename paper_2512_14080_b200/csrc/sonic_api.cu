@@ -600,6 +600,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     return SONIC_ERR_CUDA;
   a5.n_tiles = d / BN5; a5.m_tiles = (n + 127) / 128; a5.M_dim = n; a5.N_dim = d;
   a5.gsrc = static_cast<const __nv_bfloat16*>(dO); a5.gld = d;
+  a5.accumulate = (D->flags & SONIC_F_DW_ACCUMULATE) ? 1 : 0;
   a5.out = reinterpret_cast<__nv_bfloat16*>(dW2);
   const int tiles5 = E * a5.m_tiles * a5.n_tiles;
   // K7 dW1_e = Gather(X)^T dH_e   (varlen-K)
@@ -608,6 +609,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     return SONIC_ERR_CUDA;
   a7.n_tiles = (2 * n) / BN7; a7.m_tiles = (d + 127) / 128; a7.M_dim = d; a7.N_dim = 2 * n;
   a7.gsrc = static_cast<const __nv_bfloat16*>(X); a7.gld = d;
+  a7.accumulate = (D->flags & SONIC_F_DW_ACCUMULATE) ? 1 : 0;
   a7.out = reinterpret_cast<__nv_bfloat16*>(dW1);
   const int tiles7 = E * a7.m_tiles * a7.n_tiles;
 

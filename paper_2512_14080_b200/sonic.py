@@ -27,6 +27,7 @@ ROUTE_MODE_NAMES = {0: ("tc", "nrf"), 1: ("tr", "nrf"), 3: ("tr", "up"), 4: ("tr
                     6: ("tr", "sr"), 7: ("ec", "nrf")}
 SONIC_F_GATE_RAW = 1
 SONIC_F_NO_ORPHAN_RESCUE = 2
+SONIC_F_DW_ACCUMULATE = 4
 GEMM_M = 128
 
 ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",

@@ -93,3 +93,27 @@ def test_router_bwd_parity(mode, m, flags):
     got = dl.cpu().numpy().astype(np.float64)
     err = np.abs(got - ref).max() / np.abs(ref).max()
     assert err < 1e-5, err
+
+
+def test_dw_accumulate():
+    """SONIC_F_DW_ACCUMULATE: dW += (the overwrite result), bit-exactly (one fp32 add per element);
+    experts with no rows keep their initial values."""
+    T, d, n, E, K = 64, 128, 64, 64, 2  # 64 experts, 128 rows: some experts have no rows
+    inp = make_inputs(T, d, n, E, K, seed=13, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K)
+    rt = sonic.sonic_route(desc, inp.S)
+    O, H, _ = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
+    _, dW1, dW2, _, _ = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(0)
+    init1 = torch.randn(dW1.shape, generator=g, device="cuda")
+    init2 = torch.randn(dW2.shape, generator=g, device="cuda")
+    acc1, acc2 = init1.clone(), init2.clone()
+    dacc = sonic.make_desc(T, d, n, E, K, flags=sonic.SONIC_F_DW_ACCUMULATE)
+    rt2 = sonic.sonic_route(dacc, inp.S)
+    sonic.sonic_moe_bwd(dacc, inp.dO, inp.X, H, inp.W1, inp.W2, rt2, dW1=acc1, dW2=acc2)
+    torch.cuda.synchronize()
+    assert torch.equal(acc1, init1 + dW1)
+    assert torch.equal(acc2, init2 + dW2)
+    empty = (rt.f[:E] == 0).nonzero().flatten()
+    assert len(empty) > 0 and torch.equal(acc1[empty], init1[empty])
