@@ -133,7 +133,11 @@ struct GemmCfg {
 // TMA load of H in the dH epilogue").  Staging ring depth NB: 2 (a deeper ring costs a mainloop
 // stage, measured slower).
 template <int KIND, int BN, bool CTA2>
-using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128, (KIND == K_DH && BN == 256) ? 0 : 2,
+#ifndef SONIC_NB_DOWN
+#define SONIC_NB_DOWN 2  // staging ring depth of the down-proj (4 measured the same at 7B)
+#endif
+using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128,
+                     (KIND == K_DH && BN == 256) ? 0 : (KIND == K_DOWN ? SONIC_NB_DOWN : 2),
                      KIND == K_DH && BN == 256, epi_warps<KIND>()>;
 
 struct TileCoord {
