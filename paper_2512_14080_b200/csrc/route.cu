@@ -124,7 +124,8 @@ __global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, in
       continue;
     }
     const int fe = f[e];
-    const int up = min((fe + M - 1) / M * M, T);
+    const int up_m = (fe + M - 1) / M * M;  // the M-multiple above f (uncapped: the NR-f comparison)
+    const int up = min(up_m, T);            // Q15: a chosen "up" is capped at T
     const int dn = fe / M * M;
     int r;
     switch (rounding) {
@@ -132,7 +133,7 @@ __global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, in
       case 2: r = dn; break;
       case 4: r = (unsigned long long)sr_draw24(seed, (uint32_t)e) * (unsigned)M <
                           ((unsigned long long)(fe - dn) << 24) ? up : dn; break;
-      default: r = (up - fe) < (fe - dn) ? up : dn; break;
+      default: r = (up_m - fe) < (fe - dn) ? up : dn; break;  // strict '<': M/2 ties round down (Q11)
     }
     f_r[e] = r;
   }

@@ -117,3 +117,27 @@ def test_dw_accumulate():
     assert torch.equal(acc2, init2 + dW2)
     empty = (rt.f[:E] == 0).nonzero().flatten()
     assert len(empty) > 0 and torch.equal(acc1[empty], init1[empty])
+
+
+# Shape sweep over the edge cases of the routing and GEMM paths: E not a multiple of 4 or 32
+# (scalar S staging, partial expert chunks), E > 128 (several S slabs), K = 1, tiny / ragged T,
+# n = 32 and 64, d = 64.
+FUZZ = [
+    # (T, d, n, E, K, mode)
+    (33, 64, 32, 5, 1, "tc"),
+    (97, 64, 64, 33, 3, "tr"),
+    (300, 128, 64, 200, 6, "tc"),
+    (300, 128, 64, 200, 6, "tr"),
+    (777, 64, 32, 7, 7, "tr"),
+    (129, 192, 128, 130, 2, "ec"),
+    (1500, 64, 64, 260, 8, "tc"),
+]
+
+
+@pytest.mark.parametrize("case", FUZZ, ids=[f"T{c[0]}_d{c[1]}_n{c[2]}_E{c[3]}_K{c[4]}_{c[5]}" for c in FUZZ])
+def test_shape_sweep(case):
+    T, d, n, E, K, mode = case
+    inp = make_inputs(T, d, n, E, K, seed=T + E, device="cuda")
+    m = {"tc": sonic.SONIC_ROUTE_TC, "tr": sonic.SONIC_ROUTE_TR_NRF, "ec": sonic.SONIC_ROUTE_EC}[mode]
+    desc = sonic.make_desc(T, d, n, E, K, mode=m)
+    full_parity(desc, inp, mode=mode)
