@@ -14,9 +14,11 @@ from tests.parity import assert_close, f64
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("G,mode", [(1, "tc"), (2, "tc"), (4, "tc"), (2, "tr"), (4, "tr")])
-def test_ep_matches_oracle(G, mode):
-    T, d, n, E, K = 768, 128, 64, 16, 4
+@pytest.mark.parametrize("G,mode,E", [(1, "tc", 16), (2, "tc", 16), (4, "tc", 16), (2, "tr", 16), (4, "tr", 16),
+                                      (2, "tc", 64)])
+def test_ep_matches_oracle(G, mode, E):
+    """E = 64 over 2 ranks: 32 local experts, so the receive side's GIVEN routing has K = 32 > 16."""
+    T, d, n, K = 768, 128, 64, 4
     m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
     base = make_inputs(T, d, n, E, K, seed=40, device="cuda")
     W1, W2 = base.W1, base.W2
