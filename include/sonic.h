@@ -74,6 +74,11 @@ typedef enum {
 /* flags */
 #define SONIC_F_GATE_RAW         1  /* gate = S_te (no renormalisation over the kept set, Q13) */
 #define SONIC_F_NO_ORPHAN_RESCUE 2  /* TR: skip the orphan rescue (Q14) */
+#define SONIC_F_BWD_NO_DW        8  /* sonic_moe_bwd part 1: dH, dS, dX only (dW1/dW2 may be NULL);
+                                       dH and A' are left in ws */
+#define SONIC_F_BWD_DW_ONLY     16  /* sonic_moe_bwd part 2: dW2, dW1 from the dH / A' a preceding
+                                       SONIC_F_BWD_NO_DW call left in the same ws (dX/dS may be NULL).
+                                       Lets a caller overlap the dX exchange with the weight gradients. */
 #define SONIC_F_DW_ACCUMULATE    4  /* sonic_moe_bwd: dW1 += ..., dW2 += ... (fp32 element-wise adds done by
                                        the TMA store unit; one add per element per call, so deterministic)
                                        instead of overwriting -- gradient accumulation over microbatches */

@@ -523,14 +523,17 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
                            const void* W2, const sonic_routing* rt, void* dX, float* dW1, float* dW2, float* dS,
                            void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
-  if (!valid_desc(D) || !dO || !X || !H || !W1 || !W2 || !rt || !dX || !dW1 || !dW2 || !dS)
+  if (!valid_desc(D)) return SONIC_ERR_INVALID_ARG;
+  const bool no_dw = D->flags & SONIC_F_BWD_NO_DW, dw_only = D->flags & SONIC_F_BWD_DW_ONLY;
+  if (no_dw && dw_only) return SONIC_ERR_INVALID_ARG;
+  if (!dO || !X || !H || !W1 || !W2 || !rt || (!dw_only && (!dX || !dS)) || (!no_dw && (!dW1 || !dW2)))
     return SONIC_ERR_INVALID_ARG;
   if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
   const BwdWs w = bwd_ws(D);
   if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
   for (const void* p : {dO, X, H, W1, W2, (const void*)dX, (const void*)dW1, (const void*)dW2, (const void*)dS,
                         (const void*)ws})
-    if (!aligned16(p)) return SONIC_ERR_INVALID_ARG;
+    if (p && !aligned16(p)) return SONIC_ERR_INVALID_ARG;
   const Shape s = shape_of(D);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t* base = static_cast<uint8_t*>(ws);
@@ -548,7 +551,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   g.row_gate = rt->row_gate; g.pad_offsets = rt->pad_offsets; g.E = E; g.n = n; g.rows_max = R;
 
   // K4 dH: dA' = Gather(dO) W2_e^T; epilogue dSwiGLU -> dH, A' = s A, dS = <dA', A>
-  {
+  if (!dw_only) {
     CUtensorMap mA, mB, mC0, mC1, mH;
     const int BN = dh_bn(n);
     if (!map2d(&mA, dO, false, s.T, d, 64, 1) || !map3d(&mB, W2, false, E, n, d, 64, bnl(BN)) ||
@@ -631,6 +634,17 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
                      static_cast<__nv_bfloat16*>(dX), s.T, d, s_agg);
     ++g_launches;
   };
+  if (no_dw) {  // split backward, part 1: dX (and dS); dH / A' stay in ws for part 2
+    if (!run_dxt()) return SONIC_ERR_CUDA;
+    launch_aggregate(static_cast<const __nv_bfloat16*>(dXt), rt->token_rowptr, rt->token_rows,
+                     static_cast<__nv_bfloat16*>(dX), s.T, d, st);
+    ++g_launches;
+    return check_launch();
+  }
+  if (dw_only) {  // split backward, part 2: dW2, dW1 from the dH / A' of part 1 (same ws)
+    if (!run_dw2() || !run_dw1()) return SONIC_ERR_CUDA;
+    return check_launch();
+  }
   if (!run_dxt()) return SONIC_ERR_CUDA;
   if (mode == 1) {
     cudaEventRecord(ss.fork, st);

@@ -5,8 +5,9 @@ Per layer and direction there is one exchange each way, an all-to-all-v over NVL
   forward   route (own tokens, all E experts) -> plan -> pack X rows + gates -> a2a ->
             GIVEN-route the received rows to the L local experts -> sonic_moe_fwd (its aggregation
             pre-sums the local experts per received row) -> a2a back -> combine (ascending rank);
-  backward  pack dO rows -> a2a -> sonic_moe_bwd on the received rows (dW stays local) ->
-            a2a back of dX~ partial sums and of the dense per-row dS -> combine dX, scatter dS.
+  backward  pack dO rows -> a2a -> sonic_moe_bwd part 1 (dH, dS, dX~) on the received rows ->
+            a2a back of dX~ partial sums and of the dense per-row dS, overlapped with part 2 (the local
+            dW2 / dW1, SONIC_F_BWD_DW_ONLY) -> combine dX, scatter dS.
 
 One send row per (token, destination rank): a token whose K experts live on k ranks is sent k
 times, not K times.  Every step of the data path runs in libsonic's CUDA kernels; this module only
@@ -47,6 +48,12 @@ class SimComm:
             outs.append(torch.cat(parts, 0) if parts else sends[g][:0])
         return outs
 
+    def alltoallv_start(self, sends, send_counts, recv_counts):
+        return self.alltoallv(sends, send_counts, recv_counts)
+
+    def alltoallv_finish(self, pending):
+        return pending
+
 
 class DistComm:
     """One rank per process (torch.distributed; NCCL on GPUs, gloo on CPU)."""
@@ -66,6 +73,11 @@ class DistComm:
         return [r.cpu().tolist()]
 
     def alltoallv(self, sends, send_counts, recv_counts):
+        return self.alltoallv_finish(self.alltoallv_start(sends, send_counts, recv_counts))
+
+    def alltoallv_start(self, sends, send_counts, recv_counts):
+        """Issue the exchange asynchronously (NCCL runs it on its own stream after the work already
+        queued on the current stream); alltoallv_finish makes the current stream wait for it."""
         (s,), (sc,), (rc,) = sends, send_counts, recv_counts
         # gloo (CPU plumbing tests; several ranks sharing one GPU in the tests) exchanges host tensors
         stage = s.is_cuda and self.dist.get_backend(self.group) != "nccl"
@@ -73,8 +85,14 @@ class DistComm:
         if stage:
             src = src.cpu()
         out = torch.empty((sum(rc),) + tuple(s.shape[1:]), dtype=s.dtype, device=src.device)
-        self.dist.all_to_all_single(out, src, output_split_sizes=rc, input_split_sizes=sc, group=self.group)
-        return [out.to(s.device) if stage else out]
+        work = self.dist.all_to_all_single(out, src, output_split_sizes=rc, input_split_sizes=sc, group=self.group,
+                                           async_op=True)
+        return (out, work, s.device if stage else None, src)
+
+    def alltoallv_finish(self, pending):
+        out, work, dev, _src = pending
+        work.wait()
+        return [out.to(dev) if dev is not None else out]
 
 
 # ------------------------------------------------------------------------------- one rank
@@ -136,20 +154,38 @@ class EPRank:
         sonic.sonic_ep_pack(self.desc(), self.G, self.ctx["plan"], dO, send)
         return send
 
+    def _ldesc(self, extra_flags):
+        ld = self.ctx["ldesc"]
+        return sonic.make_desc(ld.T, ld.d, ld.n, ld.E, ld.K, mode=ld.route_mode, flags=ld.flags | extra_flags)
+
     def compute_bwd(self, recv_do):
+        """Backward part 1 on the received rows: dH, dS, dX~ partial sums (the dW come later, in
+        compute_bwd_dw, so that they overlap the exchange of these results)."""
         R_in = self.ctx["R_in"]
         dev = recv_do.device
         if R_in == 0:
-            self.dW1 = torch.zeros(self.L, self.d, 2 * self.n, device=dev)
-            self.dW2 = torch.zeros(self.L, self.n, self.d, device=dev)
+            self.ctx["bws"] = None
             return recv_do.new_zeros(0, self.d), torch.zeros(0, self.L, device=dev)
-        ld, lrt = self.ctx["ldesc"], self.ctx["lrt"]
-        dX_part, dW1, dW2, dS, _ = sonic.sonic_moe_bwd(ld, recv_do, self.ctx["recv_x"], self.ctx["H"], self.W1,
-                                                       self.W2, lrt)
+        lrt = self.ctx["lrt"]
+        ld = self._ldesc(sonic.SONIC_F_BWD_NO_DW)
+        dX_part, _, _, dS, ws = sonic.sonic_moe_bwd(ld, recv_do, self.ctx["recv_x"], self.ctx["H"], self.W1, self.W2,
+                                                    lrt)
+        self.ctx.update(bws=ws, recv_do=recv_do)
         dense = torch.empty(R_in, self.L, dtype=torch.float32, device=dev)
         sonic.sonic_ep_ds_dense(ld, lrt, dS, dense)
-        self.dW1, self.dW2 = dW1, dW2
         return dX_part, dense
+
+    def compute_bwd_dw(self):
+        """Backward part 2: dW2, dW1 of the local experts from part 1's dH / A' (same workspace)."""
+        dev = self.W1.device
+        if self.ctx.get("bws") is None:
+            self.dW1 = torch.zeros(self.L, self.d, 2 * self.n, device=dev)
+            self.dW2 = torch.zeros(self.L, self.n, self.d, device=dev)
+            return
+        ld = self._ldesc(sonic.SONIC_F_BWD_DW_ONLY)
+        _, dW1, dW2, _, _ = sonic.sonic_moe_bwd(ld, self.ctx["recv_do"], self.ctx["recv_x"], self.ctx["H"], self.W1,
+                                                self.W2, self.ctx["lrt"], ws=self.ctx["bws"])
+        self.dW1, self.dW2 = dW1, dW2
 
     def combine_bwd(self, back_dx, back_ds):
         desc, plan, rt = self.desc(), self.ctx["plan"], self.ctx["rt"]
@@ -183,6 +219,11 @@ def ep_backward(ranks, comm, dOs):
     sends = [r.dispatch_bwd(dO) for r, dO in zip(ranks, dOs)]
     recv = comm.alltoallv(sends, send_counts, recv_counts)
     outs = [r.compute_bwd(x) for r, x in zip(ranks, recv)]
-    back_dx = comm.alltoallv([o[0] for o in outs], recv_counts, send_counts)
-    back_ds = comm.alltoallv([o[1] for o in outs], recv_counts, send_counts)
+    # the dX~ / dS exchange runs while the local weight gradients are computed
+    p_dx = comm.alltoallv_start([o[0] for o in outs], recv_counts, send_counts)
+    p_ds = comm.alltoallv_start([o[1] for o in outs], recv_counts, send_counts)
+    for r in ranks:
+        r.compute_bwd_dw()
+    back_dx = comm.alltoallv_finish(p_dx)
+    back_ds = comm.alltoallv_finish(p_ds)
     return [r.combine_bwd(bx, bs) for r, bx, bs in zip(ranks, back_dx, back_ds)]

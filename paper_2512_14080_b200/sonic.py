@@ -28,6 +28,8 @@ ROUTE_MODE_NAMES = {0: ("tc", "nrf"), 1: ("tr", "nrf"), 3: ("tr", "up"), 4: ("tr
 SONIC_F_GATE_RAW = 1
 SONIC_F_NO_ORPHAN_RESCUE = 2
 SONIC_F_DW_ACCUMULATE = 4
+SONIC_F_BWD_NO_DW = 8
+SONIC_F_BWD_DW_ONLY = 16
 GEMM_M = 128
 
 ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",
@@ -240,13 +242,15 @@ def sonic_moe_bwd(desc, dO, X, H, W1, W2, rt, dX=None, dW1=None, dW2=None, dS=No
     """sonic_moe_bwd -> (dX [T,d] bf16, dW1 [E,d,2n] f32, dW2 [E,n,d] f32, dS [rows_max] f32, ws)."""
     rows = sonic_rows_max(desc)
     dev = X.device
-    if dX is None:
+    want_dx = not (desc.flags & SONIC_F_BWD_DW_ONLY)
+    want_dw = not (desc.flags & SONIC_F_BWD_NO_DW)
+    if dX is None and want_dx:
         dX = torch.empty(desc.T, desc.d, dtype=torch.bfloat16, device=dev)
-    if dW1 is None:
+    if dW1 is None and want_dw:
         dW1 = torch.empty(desc.E, desc.d, 2 * desc.n, dtype=torch.float32, device=dev)
-    if dW2 is None:
+    if dW2 is None and want_dw:
         dW2 = torch.empty(desc.E, desc.n, desc.d, dtype=torch.float32, device=dev)
-    if dS is None:
+    if dS is None and want_dx:
         dS = torch.empty(rows, dtype=torch.float32, device=dev)
     if ws is None:
         ws = _ws(sonic_bwd_workspace_size(desc), dev)

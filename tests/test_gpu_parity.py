@@ -141,3 +141,23 @@ def test_shape_sweep(case):
     m = {"tc": sonic.SONIC_ROUTE_TC, "tr": sonic.SONIC_ROUTE_TR_NRF, "ec": sonic.SONIC_ROUTE_EC}[mode]
     desc = sonic.make_desc(T, d, n, E, K, mode=m)
     full_parity(desc, inp, mode=mode)
+
+
+def test_split_backward_matches_monolithic():
+    """SONIC_F_BWD_NO_DW then SONIC_F_BWD_DW_ONLY (same workspace) give exactly the one-call result."""
+    T, d, n, E, K = 1000, 128, 64, 16, 4
+    inp = make_inputs(T, d, n, E, K, seed=17, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K)
+    rt = sonic.sonic_route(desc, inp.S)
+    O, H, _ = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
+    dX, dW1, dW2, dS, _ = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+    d1 = sonic.make_desc(T, d, n, E, K, flags=sonic.SONIC_F_BWD_NO_DW)
+    d2 = sonic.make_desc(T, d, n, E, K, flags=sonic.SONIC_F_BWD_DW_ONLY)
+    dXa, w1a, w2a, dSa, ws = sonic.sonic_moe_bwd(d1, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+    assert w1a is None and w2a is None
+    dXb, w1b, w2b, dSb, _ = sonic.sonic_moe_bwd(d2, inp.dO, inp.X, H, inp.W1, inp.W2, rt, ws=ws)
+    assert dXb is None and dSb is None
+    torch.cuda.synchronize()
+    R = int(rt.offsets[E].item())
+    assert torch.equal(dXa, dX) and torch.equal(w1b, dW1) and torch.equal(w2b, dW2)
+    assert torch.equal(dSa[:R], dS[:R])
