@@ -38,6 +38,11 @@ class SimComm:
         """send_counts[s][g] (host ints) -> recv_counts[g][s]."""
         return [[send_counts[s][g] for s in range(self.G)] for g in range(self.G)]
 
+    def exchange_counts_dev(self, send_dev):
+        """Device count tensors [G] per local rank -> (send, recv) host lists, one host read."""
+        host = torch.stack([c[: self.G] for c in send_dev]).cpu().tolist()
+        return host, self.exchange_counts(host)
+
     def alltoallv(self, sends, send_counts, recv_counts):
         outs = []
         for g in range(self.G):
@@ -71,6 +76,19 @@ class DistComm:
         r = torch.empty_like(t)
         self.dist.all_to_all_single(r, t, group=self.group)
         return [r.cpu().tolist()]
+
+    def exchange_counts_dev(self, send_dev):
+        """The G send counts of this rank (device int32) -> (send, recv) host lists.  Under NCCL the
+        count all-to-all runs on the device and one host read fetches both directions."""
+        (c,) = send_dev
+        if self.dist.get_backend(self.group) != "nccl":
+            sc = c[: self.G].cpu().tolist()
+            return [sc], self.exchange_counts([sc])
+        t = c[: self.G].to(torch.int64)
+        r = torch.empty_like(t)
+        self.dist.all_to_all_single(r, t, group=self.group)
+        both = torch.stack([t, r]).cpu().tolist()
+        return [both[0]], [both[1]]
 
     def alltoallv(self, sends, send_counts, recv_counts):
         return self.alltoallv_finish(self.alltoallv_start(sends, send_counts, recv_counts))
@@ -126,10 +144,9 @@ class EPRank:
         nmax = self.T * self.G
         send_x = torch.empty(nmax, self.d, dtype=torch.bfloat16, device=X.device)
         sonic.sonic_ep_pack(desc, self.G, plan, X, send_x)
-        counts = plan.send_counts[: self.G].cpu().tolist()  # host split sizes (one sync)
-        self.ctx.update(rt=rt, plan=plan, counts=counts)
+        self.ctx.update(rt=rt, plan=plan)
         gates = plan.send_gate[: nmax * self.L].view(nmax, self.L)
-        return send_x, gates, counts
+        return send_x, gates, plan.send_counts  # device counts: read once, with the exchange
 
     def compute_fwd(self, recv_x, recv_gate):
         R_in = recv_x.shape[0]
@@ -164,13 +181,19 @@ class EPRank:
         R_in = self.ctx["R_in"]
         dev = recv_do.device
         if R_in == 0:
-            self.ctx["bws"] = None
+            self.ctx.update(bws=None, dw_done=False)
             return recv_do.new_zeros(0, self.d), torch.zeros(0, self.L, device=dev)
         lrt = self.ctx["lrt"]
-        ld = self._ldesc(sonic.SONIC_F_BWD_NO_DW)
-        dX_part, _, _, dS, ws = sonic.sonic_moe_bwd(ld, recv_do, self.ctx["recv_x"], self.ctx["H"], self.W1, self.W2,
-                                                    lrt)
-        self.ctx.update(bws=ws, recv_do=recv_do)
+        if self.G == 1:  # nothing to overlap: one call (the dX aggregation then overlaps dW2 inside)
+            ld = self._ldesc(0)
+            dX_part, self.dW1, self.dW2, dS, _ = sonic.sonic_moe_bwd(ld, recv_do, self.ctx["recv_x"], self.ctx["H"],
+                                                                     self.W1, self.W2, lrt)
+            self.ctx.update(bws=None, dw_done=True)
+        else:
+            ld = self._ldesc(sonic.SONIC_F_BWD_NO_DW)
+            dX_part, _, _, dS, ws = sonic.sonic_moe_bwd(ld, recv_do, self.ctx["recv_x"], self.ctx["H"], self.W1,
+                                                        self.W2, lrt)
+            self.ctx.update(bws=ws, recv_do=recv_do, dw_done=False)
         dense = torch.empty(R_in, self.L, dtype=torch.float32, device=dev)
         sonic.sonic_ep_ds_dense(ld, lrt, dS, dense)
         return dX_part, dense
@@ -178,6 +201,8 @@ class EPRank:
     def compute_bwd_dw(self):
         """Backward part 2: dW2, dW1 of the local experts from part 1's dH / A' (same workspace)."""
         dev = self.W1.device
+        if self.ctx.get("dw_done"):
+            return
         if self.ctx.get("bws") is None:
             self.dW1 = torch.zeros(self.L, self.d, 2 * self.n, device=dev)
             self.dW2 = torch.zeros(self.L, self.n, self.d, device=dev)
@@ -201,8 +226,10 @@ class EPRank:
 def ep_forward(ranks, comm, Xs, Ss):
     """Forward of the EP layer over the local ranks -> [O_r]."""
     disp = [r.dispatch_fwd(X, S) for r, X, S in zip(ranks, Xs, Ss)]
-    send_counts = [c for _, _, c in disp]
-    recv_counts = comm.exchange_counts(send_counts)
+    # NCCL takes host split sizes: the only host synchronisation of the layer step
+    send_counts, recv_counts = comm.exchange_counts_dev([c for _, _, c in disp])
+    for r, sc in zip(ranks, send_counts):
+        r.ctx["counts"] = sc
     recv_x = comm.alltoallv([x for x, _, _ in disp], send_counts, recv_counts)
     recv_g = comm.alltoallv([g for _, g, _ in disp], send_counts, recv_counts)
     parts = [r.compute_fwd(x, g) for r, x, g in zip(ranks, recv_x, recv_g)]
