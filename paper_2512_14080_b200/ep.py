@@ -50,7 +50,7 @@ class SimComm:
             for s in range(self.G):
                 off = sum(send_counts[s][:g])
                 parts.append(sends[s][off: off + send_counts[s][g]])
-            outs.append(torch.cat(parts, 0) if parts else sends[g][:0])
+            outs.append(parts[0] if len(parts) == 1 else torch.cat(parts, 0))  # G = 1: a view, no copy
         return outs
 
     def alltoallv_start(self, sends, send_counts, recv_counts):
