@@ -199,6 +199,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="sonic", choices=["sonic", "reference"])
     ap.add_argument("--config", default="7b")
+    ap.add_argument("--shape", default="", help="T,d,n,E,K: a custom workload instead of --config (sweeps)")
     ap.add_argument("--mode", default="tc", choices=list(ROUTE_MODES))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=20)
@@ -215,7 +216,12 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
 
     from paper_2512_14080_b200.inputs import CONFIGS
-    cfg = CONFIGS[args.config]
+    if args.shape:
+        T_, d_, n_, E_, K_ = (int(v) for v in args.shape.split(","))
+        cfg = dict(T=T_, d=d_, n=n_, E=E_, K=K_)
+        args.config = f"custom_{args.shape.replace(',', 'x')}"
+    else:
+        cfg = CONFIGS[args.config]
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
