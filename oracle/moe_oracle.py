@@ -170,6 +170,32 @@ def round_sr(f, M, seed, T=None):
     return out
 
 
+def round_nrs(S, tc, f, M, seed, T):
+    """NR-s: pad expert e with probability
+        p_e = (sum_t s_e,t - sum_t floor(s)_e,t) / (sum_t ceil(s)_e,t - sum_t floor(s)_e,t),
+    s_e the scores of e's TC tokens, floor(s)_e those of pi_e[:floor(f_e)], ceil(s)_e those of
+    pi_e[:ceil(f_e)] (pi_e = Alg. 4's ranking, _rank_expert_column).  The sums are fp64 sums of the
+    fp32 scores; the draw is SR-f's (u_e = sr_u64(seed, e) >> 40, Q21): pad iff u_e < p_e 2^24."""
+    f = np.asarray(f, dtype=np.int64)
+    out = np.empty_like(f)
+    for e, fe in enumerate(f):
+        fe = int(fe)
+        dn = int(round_down(fe, M))
+        up = min(int(round_up(fe, M)), T)
+        if dn == fe:
+            out[e] = fe
+            continue
+        order = _rank_expert_column(S[:, e], tc[:, e])
+        s_tc = float(np.sum(S[order[:fe], e]))
+        s_dn = float(np.sum(S[order[:dn], e]))
+        s_up = float(np.sum(S[order[:up], e]))
+        with np.errstate(divide="ignore", invalid="ignore"):
+            p = np.float64(s_tc - s_dn) / np.float64(s_up - s_dn)
+        u = sr_u64(seed, e) >> 40
+        out[e] = up if float(u) < float(p) * 16777216.0 else dn
+    return out
+
+
 def ec_capacity(T, K, E, M):
     """Expert-choice capacity (Q22): the average TC load ceil(T K / E), rounded up to a multiple of
     M_tile and capped at T."""
@@ -231,7 +257,7 @@ class Routing:
         return int(self.pad_offsets[-1])
 
 
-TR_ROUNDINGS = ("nrf", "up", "down", "balance", "sr")
+TR_ROUNDINGS = ("nrf", "up", "down", "balance", "sr", "nrs")
 
 
 def route(S, K, mode="tc", m_tile=128, rescue=True, gate_raw=False, rounding="nrf", seed=0):
@@ -240,7 +266,7 @@ def route(S, K, mode="tc", m_tile=128, rescue=True, gate_raw=False, rounding="nr
     mode "tc": kept = TC top-K set.
     mode "tr": token rounding; ``rounding`` picks the subroutine of App.: "nrf"
       (default, P:2174), "up" (P:2194), "down" (P:2196), "balance" (Alg. 6), "sr" (P:2176, the
-      draws from ``sr_u64(seed, e)``).  The orphan rescue (Q14) applies to every subroutine.
+      draws from ``sr_u64(seed, e)``), "nrs" (score-weighted, same draws).  The orphan rescue (Q14) applies to every subroutine.
     mode "ec": expert choice (NEXT-3, Q22): every expert keeps the ``ec_capacity`` highest-scoring
       tokens (S desc, token asc); no rescue -- tokens no expert chose have no rows.
     """
@@ -273,6 +299,8 @@ def route(S, K, mode="tc", m_tile=128, rescue=True, gate_raw=False, rounding="nr
             f_r = round_balance(f, m_tile, T)
         elif rounding == "sr":
             f_r = round_sr(f, m_tile, seed, T)
+        elif rounding == "nrs":
+            f_r = round_nrs(S, tc, f, m_tile, seed, T)
         else:
             raise ValueError(rounding)
         kept = np.zeros((T, E), dtype=bool)

@@ -441,3 +441,47 @@ def test_router_backward_rows_sum_to_zero():
     rt = om.route(S, 3, mode="tc")
     d = om.router_backward(S, rt, rng.normal(size=S.shape) * rt.kept)
     np.testing.assert_allclose(d.sum(1), 0.0, atol=1e-12)
+
+
+def test_nrs_probability_by_brute_force():
+    """NR-s: over many seeds the pad frequency of each expert matches the probability
+    computed independently with Python's sort of (not-in-TC, -S, t) -- pi_e of Alg. 4 -- and
+    plain Python sums; tile multiples never move."""
+    rng = np.random.default_rng(31)
+    T, E, K, M = 60, 5, 2, 8
+    S = rng.random((T, E))
+    ids, _ = om.topk_tc(S, K)
+    tc = np.zeros((T, E), bool)
+    tc[np.arange(T)[:, None], ids] = True
+    f = tc.sum(0)
+    p_ref = []
+    for e in range(E):
+        pi = sorted(range(T), key=lambda t: (not tc[t, e], -S[t, e], t))
+        fe = int(f[e])
+        dn, up = fe // M * M, min(-(-fe // M) * M, T)
+        s_tc = sum(S[t, e] for t in pi[:fe])
+        s_dn = sum(S[t, e] for t in pi[:dn])
+        s_up = sum(S[t, e] for t in pi[:up])
+        p_ref.append(None if dn == fe else (s_tc - s_dn) / (s_up - s_dn))
+    n = 3000
+    ups = np.zeros(E)
+    for seed in range(n):
+        fr = om.round_nrs(S, tc, f, M, seed, T)
+        for e in range(E):
+            if p_ref[e] is None:
+                assert fr[e] == f[e]
+        ups += fr > f
+    for e in range(E):
+        if p_ref[e] is not None:
+            sd = (p_ref[e] * (1 - p_ref[e]) / n) ** 0.5
+            assert abs(ups[e] / n - p_ref[e]) < 4 * sd + 1e-3, (e, ups[e] / n, p_ref[e])
+
+
+def test_nrs_route_invariants():
+    rng = np.random.default_rng(12)
+    T, E, K, M = 200, 8, 2, 16
+    S = rng.random((T, E)).astype(np.float32).astype(np.float64)
+    rt = om.route(S, K, mode="tr", m_tile=M, rounding="nrs", seed=9)
+    assert np.all((rt.f_rounded % M == 0) | (rt.f_rounded == T))
+    assert rt.kept.any(axis=1).all()
+    assert np.all(rt.kept.sum(0) == rt.f_rounded)
