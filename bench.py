@@ -29,7 +29,8 @@ sys.path.insert(0, ROOT)
 
 # --mode -> (sonic route mode, oracle mode, oracle rounding); tr = NR-f (the paper's default)
 ROUTE_MODES = {"tc": (0, "tc", "nrf"), "tr": (1, "tr", "nrf"), "tr_up": (3, "tr", "up"), "tr_down": (4, "tr", "down"),
-               "tr_balance": (5, "tr", "balance"), "tr_sr": (6, "tr", "sr"), "ec": (7, "ec", "nrf")}
+               "tr_balance": (5, "tr", "balance"), "tr_sr": (6, "tr", "sr"), "ec": (7, "ec", "nrf"),
+               "tr_nrs": (8, "tr", "nrs")}
 METRIC = "MoE layer fwd+bwd TFLOPS (% B200 BF16 peak), tokens/s at 1/2/4/8 GPU; act. mem"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 

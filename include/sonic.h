@@ -66,9 +66,11 @@ typedef enum {
   SONIC_ROUTE_TR_BALANCE = 5,  /* Balance-f, Alg. 6: sequential residual accumulator */
   SONIC_ROUTE_TR_SR = 6,       /* SR-f: pad with probability (f - floor_M f)/M; the draw of
                                   expert e is SplitMix64 from state (seed << 32 | e), top 24 bits (Q21) */
-  SONIC_ROUTE_EC = 7           /* expert choice (NEXT-3, Q22): each expert keeps its C best tokens,
+  SONIC_ROUTE_EC = 7,          /* expert choice (NEXT-3, Q22): each expert keeps its C best tokens,
                                   C = min(ceil_M(ceil(T K / E)), T); no orphan rescue (tokens no expert
                                   chose have no rows and get O = dX = 0) */
+  SONIC_ROUTE_TR_NRS = 8       /* NR-s (Q25): pad with probability (sum s - sum floor s) /
+                                  (sum ceil s - sum floor s) over Alg. 4's ranking; SR-f's draws (seed) */
 } sonic_route_mode;
 
 /* flags */

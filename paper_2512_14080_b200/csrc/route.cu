@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
                                                       const uint32_t* __restrict__ bm_tc,
                                                       uint32_t* __restrict__ bm_kept, const int* __restrict__ f,
                                                       int* __restrict__ f_r, const int* __restrict__ flip,
-                                                      int rescue, int ec) {
+                                                      int rescue, int ec, const int* __restrict__ fr_src) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   __shared__ int hist[4096];
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
     fr = min((fc + M - 1) / M * M, T);
     if (tid == 0) f_r[e] = fr;
   } else {
-    fr = f_r[e];
+    fr = fr_src ? fr_src[e] : f_r[e];  // NR-s runs the selection for both candidate counts
   }
   const uint32_t* tcw_p = bm_tc + (size_t)e * W;
   auto tcw = [&](int w) -> uint32_t { return ec ? 0u : tcw_p[w]; };
@@ -320,6 +320,73 @@ __global__ void __launch_bounds__(1024) k_tr_select_w(const float* __restrict__ 
     if (w < W) kw[w] = up ? (tcw(w) | gt | sel) : (gt | sel);
     run += tot;
   }
+}
+
+// ---------------------------------------------------------------- NR-s (Q25)
+// the two candidate counts of every expert: floor_M(f) and min(ceil_M(f), T)
+__global__ void k_nrs_counts(const int* __restrict__ f, int E, int T, int M, int* __restrict__ f_dn,
+                             int* __restrict__ f_up) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
+    const int fe = f[e];
+    f_dn[e] = fe / M * M;
+    f_up[e] = min((fe + M - 1) / M * M, T);
+  }
+}
+
+// sums[e] = sum of S over the tokens set in expert e's bitmap, in fp64 (exact for fp32 scores
+// of one expert: order-independent).  One block per expert.
+__global__ void k_bitmap_sums(const float* __restrict__ ST, const uint32_t* __restrict__ bm, int T, int W,
+                              double* __restrict__ sums) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int e = blockIdx.x;
+  const float* col = ST + (size_t)e * T;
+  double acc = 0.0;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    uint32_t bits = bm[(size_t)e * W + w];
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      acc += (double)col[w * 32 + b];
+    }
+  }
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) sums[e] = v;
+  }
+}
+
+// the decision (p = (s_tc - s_dn) / (s_up - s_dn), pad iff u < p 2^24) and the chosen kept words
+__global__ void k_nrs_decide(const int* __restrict__ f, const int* __restrict__ f_dn, const int* __restrict__ f_up,
+                             const double* __restrict__ s_tc, const double* __restrict__ s_dn,
+                             const double* __restrict__ s_up, const uint32_t* __restrict__ bm_dn,
+                             const uint32_t* __restrict__ bm_up, int W, uint32_t seed, int* __restrict__ f_r,
+                             uint32_t* __restrict__ bm_kept) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int e = blockIdx.x;
+  __shared__ int s_up_chosen;
+  if (threadIdx.x == 0) {
+    bool go_up = false;
+    if (f_dn[e] != f[e]) {
+      const double p = (s_tc[e] - s_dn[e]) / (s_up[e] - s_dn[e]);
+      go_up = (double)sr_draw24(seed, (uint32_t)e) < p * 16777216.0;
+    }
+    s_up_chosen = go_up;
+    f_r[e] = go_up ? f_up[e] : f_dn[e];
+  }
+  __syncthreads();
+  const uint32_t* src = (s_up_chosen ? bm_up : bm_dn) + (size_t)e * W;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) bm_kept[(size_t)e * W + w] = src[w];
 }
 
 // ---------------------------------------------------------------- orphan detection
@@ -912,19 +979,35 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
       const long long avg = ((long long)T * K + E - 1) / E;
       ec_cap = (int)std::min<long long>((avg + L.m_tile - 1) / L.m_tile * L.m_tile, T);
     }
+    const bool nrs = !ec && L.rounding == 5;
     launch_k(k_expert_popc, E, 1024, 0, st, L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
-    launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile, L.rounding, L.seed, ec_cap); ++nl;
+    if (!nrs) {
+      launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile, L.rounding, L.seed, ec_cap);
+      ++nl;
+    }
     launch_k(k_transpose, dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st, L.S, L.ST, T, E); ++nl;
-    auto select = [&](int rescue) {
+    auto select_into = [&](int rescue, uint32_t* out, const int* fr_src) {
       if (W <= 1024)
-        launch_k(k_tr_select_w<true>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip,
-                 rescue, ec ? 1 : 0);
+        launch_k(k_tr_select_w<true>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, out, L.f, L.f_r, L.flip,
+                 rescue, ec ? 1 : 0, fr_src);
       else
-        launch_k(k_tr_select_w<false>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, L.bm_kept, L.f, L.f_r, L.flip,
-                 rescue, ec ? 1 : 0);
+        launch_k(k_tr_select_w<false>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, out, L.f, L.f_r, L.flip,
+                 rescue, ec ? 1 : 0, fr_src);
     };
-    select(0);
-    ++nl;
+    auto select = [&](int rescue) { select_into(rescue, L.bm_kept, nullptr); };
+    if (nrs) {  // NR-s: both candidate selections, their score sums, then the draw
+      launch_k(k_nrs_counts, (E + 255) / 256, 256, 0, st, L.f, E, T, L.m_tile, L.f_dn, L.f_up); ++nl;
+      select_into(0, L.bm_dn, L.f_dn); ++nl;
+      select_into(0, L.bm_up, L.f_up); ++nl;
+      launch_k(k_bitmap_sums, E, 256, 0, st, L.ST, L.bm_tc, T, W, L.nrs_sums); ++nl;
+      launch_k(k_bitmap_sums, E, 256, 0, st, L.ST, L.bm_dn, T, W, L.nrs_sums + E); ++nl;
+      launch_k(k_bitmap_sums, E, 256, 0, st, L.ST, L.bm_up, T, W, L.nrs_sums + 2 * E); ++nl;
+      launch_k(k_nrs_decide, E, 256, 0, st, L.f, L.f_dn, L.f_up, L.nrs_sums, L.nrs_sums + E, L.nrs_sums + 2 * E,
+               L.bm_dn, L.bm_up, W, L.seed, L.f_r, L.bm_kept); ++nl;
+    } else {
+      select(0);
+      ++nl;
+    }
     if (L.rescue && !ec) {
       cudaMemsetAsync(L.flip, 0, (size_t)E * 4, st);
       launch_k(k_orphans, (W * 32 + 255) / 256, 256, 0, st, L.bm_kept, T, E, W, K, L.topk_ids, L.flip); ++nl;

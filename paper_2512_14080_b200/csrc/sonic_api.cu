@@ -228,7 +228,7 @@ bool valid_desc(const sonic_moe_desc* D) {
   if (D->K > D->E || D->E > 4096) return false;
   if (D->K > 16 && D->route_mode != SONIC_ROUTE_GIVEN) return false;
   if (D->m_tile != 128) return false;
-  if (D->route_mode < SONIC_ROUTE_TC || D->route_mode > SONIC_ROUTE_EC) return false;
+  if (D->route_mode < SONIC_ROUTE_TC || D->route_mode > SONIC_ROUTE_TR_NRS) return false;
   return true;
 }
 bool supported_dims(const sonic_moe_desc* D) {
@@ -260,7 +260,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 // route workspace layout
 struct RouteWs {
-  size_t bm_tc, bm_kept, wprefix, tokcnt, flip, ticket, ST, total;
+  size_t bm_tc, bm_kept, wprefix, tokcnt, flip, ticket, ST, nrs, total;
 };
 RouteWs route_ws(const sonic_moe_desc* D) {
   const Shape s = shape_of(D);
@@ -275,6 +275,8 @@ RouteWs route_ws(const sonic_moe_desc* D) {
   w.ticket = o; o += al(8);  // [0] offsets ticket, [1] token-CSR ticket
   const bool needs_st = D->route_mode != SONIC_ROUTE_TC && D->route_mode != SONIC_ROUTE_GIVEN;
   w.ST = o; o += needs_st ? al((size_t)s.T * s.E * 4) : 0;
+  // NR-s: two candidate bitmaps, two count arrays, three score-sum arrays
+  w.nrs = o; o += (D->route_mode == SONIC_ROUTE_TR_NRS) ? 2 * bm + 2 * al((size_t)s.E * 4) + al((size_t)s.E * 24) : 0;
   w.total = o;
   return w;
 }
@@ -433,6 +435,7 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
     case SONIC_ROUTE_TC: L.mode = 0; break;
     case SONIC_ROUTE_GIVEN: L.mode = 2; break;
     case SONIC_ROUTE_EC: L.mode = 3; break;
+    case SONIC_ROUTE_TR_NRS: L.mode = 1; L.rounding = 5; break;
     default:
       L.mode = 1;
       L.rounding = D->route_mode == SONIC_ROUTE_TR_NRF ? 0 : D->route_mode - SONIC_ROUTE_TR_UP + 1;
@@ -453,6 +456,15 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   L.tokcnt = reinterpret_cast<int*>(base + w.tokcnt);
   L.flip = reinterpret_cast<int*>(base + w.flip);
   L.ticket = reinterpret_cast<unsigned*>(base + w.ticket);
+  if (D->route_mode == SONIC_ROUTE_TR_NRS) {
+    const size_t bmb = al((size_t)s.E * s.W * 4);
+    uint8_t* q = base + w.nrs;
+    L.bm_dn = reinterpret_cast<uint32_t*>(q); q += bmb;
+    L.bm_up = reinterpret_cast<uint32_t*>(q); q += bmb;
+    L.f_dn = reinterpret_cast<int*>(q); q += al((size_t)s.E * 4);
+    L.f_up = reinterpret_cast<int*>(q); q += al((size_t)s.E * 4);
+    L.nrs_sums = reinterpret_cast<double*>(q);
+  }
   L.ST = reinterpret_cast<float*>(base + w.ST);
   {
     ProfScope ps("route", static_cast<cudaStream_t>(stream));

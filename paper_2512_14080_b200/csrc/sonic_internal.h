@@ -31,7 +31,7 @@ constexpr int GEMM_M = 128;  // grouped-row tile (== TR m_tile, Q16)
 struct RouteLaunch {
   long long T;
   int E, K, W, m_tile, mode, rescue, gate_raw;
-  int rounding;   // mode 1 (TR): 0 NR-f, 1 up, 2 down, 3 Balance-f, 4 SR-f; mode 3 = expert choice
+  int rounding;   // mode 1 (TR): 0 NR-f, 1 up, 2 down, 3 Balance-f, 4 SR-f, 5 NR-s; mode 3 = expert choice
   uint32_t seed;  // SR-f draws
   const float* S;
   // outputs
@@ -42,6 +42,10 @@ struct RouteLaunch {
   uint32_t *bm_tc, *bm_kept;
   int *wprefix, *tokcnt, *flip;
   unsigned* ticket;  // last-block-done counter (zeroed by the first route kernel)
+  // NR-s scratch (route mode SONIC_ROUTE_TR_NRS only)
+  uint32_t *bm_dn, *bm_up;
+  int *f_dn, *f_up;
+  double* nrs_sums;  // [3E]: TC, floor, ceil score sums
   float* ST;
 };
 

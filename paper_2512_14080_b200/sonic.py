@@ -22,9 +22,10 @@ SONIC_ROUTE_TR_DOWN = 4
 SONIC_ROUTE_TR_BALANCE = 5
 SONIC_ROUTE_TR_SR = 6
 SONIC_ROUTE_EC = 7
+SONIC_ROUTE_TR_NRS = 8
 # oracle route(mode, rounding) of each TR-family mode
 ROUTE_MODE_NAMES = {0: ("tc", "nrf"), 1: ("tr", "nrf"), 3: ("tr", "up"), 4: ("tr", "down"), 5: ("tr", "balance"),
-                    6: ("tr", "sr"), 7: ("ec", "nrf")}
+                    6: ("tr", "sr"), 7: ("ec", "nrf"), 8: ("tr", "nrs")}
 SONIC_F_GATE_RAW = 1
 SONIC_F_NO_ORPHAN_RESCUE = 2
 SONIC_F_DW_ACCUMULATE = 4

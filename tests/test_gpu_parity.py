@@ -34,6 +34,7 @@ def test_small_parity(case):
 VARIANTS = [
     ("up", sonic.SONIC_ROUTE_TR_UP), ("down", sonic.SONIC_ROUTE_TR_DOWN),
     ("balance", sonic.SONIC_ROUTE_TR_BALANCE), ("sr", sonic.SONIC_ROUTE_TR_SR), ("ec", sonic.SONIC_ROUTE_EC),
+    ("nrs", sonic.SONIC_ROUTE_TR_NRS),
 ]
 
 
