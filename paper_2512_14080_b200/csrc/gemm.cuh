@@ -57,7 +57,6 @@ struct GemmArgs {
   int M_dim, N_dim;         // output extent along M (varlen-K) and N
   float* dS;                // DH: dS [rows] if n_tiles == 1, else partials [n_tiles][rows_max]
   long long rows_max;
-  __nv_bfloat16* out;       // DOWN / DXT: the output rows [rows_max, N_dim] (direct-store epilogue)
   unsigned long long* dbg;  // SONIC_TIMING builds only: cycle counters (see sonic_api.cu)
   int accumulate;           // DW1 / DW2: add into the existing dW (SONIC_F_DW_ACCUMULATE) instead of overwriting
 };
@@ -222,7 +221,7 @@ __device__ __forceinline__ uint32_t swz(int lane, int chunk) { return (uint32_t)
 // stored from NB-k stores ago: it is free once at most NB-1-k newer groups are pending a read.
 template <int NB>
 #ifndef SONIC_EXP_EPI
-#define SONIC_EXP_EPI 0  // ablation: 1 = TMEM loads only (down/dXt), 2 = no TMA stores
+#define SONIC_EXP_EPI 0  // ablation: 1 = TMEM loads only (down/dXt), 2 = no TMA stores, 3 = L2-resident stores
 #endif
 struct StoreQ {
   uint8_t* base;
@@ -795,33 +794,6 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           write_row_bf16(sq.addr(i), lane, a);
           sq.issue(lane, i, &mC1, 0, wrow);  // columns >= n are clipped by the tensor map
         }
-      } else if constexpr ((KIND == K_DOWN || KIND == K_DXT) && (SONIC_EXP_EPI == 4 || SONIC_EXP_EPI == 5)) {
-        // experiment: registers -> global directly (no SMEM staging); lane = row
-        float gate = 1.f;
-        if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
-        __nv_bfloat16* orow = args.out + (size_t)row * args.N_dim + tc.nt * BN;
-#pragma unroll 1
-        for (int c = 64 * half; c < BN; c += 64 * Cfg::EPH) {
-          if (tc.nt * BN + c >= args.N_dim) break;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t r[32];
-            ptx::tmem_ld32(t_acc + c + 32 * h, r);
-            ptx::tmem_ld_wait();
-            uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              pk[i] = ptx::pack_bf16(gate * __uint_as_float(r[2 * i]), gate * __uint_as_float(r[2 * i + 1]));
-            if constexpr (SONIC_EXP_EPI == 4) {
-#pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4)
-                ptx::st_global_v4(orow + c + 32 * h + 8 * q4, pk[4 * q4], pk[4 * q4 + 1], pk[4 * q4 + 2], pk[4 * q4 + 3]);
-            } else {
-              ptx::st_global_v8(orow + c + 32 * h, pk);
-              ptx::st_global_v8(orow + c + 32 * h + 16, pk + 8);
-            }
-          }
-        }
       } else if constexpr (KIND == K_DOWN || KIND == K_DXT) {
         float gate = 1.f;
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
@@ -1075,25 +1047,6 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             args.dS[row] = ds;
           else
             args.dS[(long long)tc.nt * args.rows_max + row] = ds;
-        }
-      } else if constexpr (SONIC_EXP_EPI == 6) {  // experiment: fp32 dW rows straight to global
-        const int m = tc.mt * GEMM_BM + 32 * q + lane;
-        float* wrow_p = reinterpret_cast<float*>(args.out) + ((size_t)tc.e * args.M_dim + m) * args.N_dim + tc.nt * BN;
-        if (m < args.M_dim) {
-#pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            if (tc.nt * BN + c >= args.N_dim) break;
-            uint32_t r[32];
-            if (tc.nkb > 0) {
-              ptx::tmem_ld32(t_acc + c, r);
-              ptx::tmem_ld_wait();
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) r[i] = 0u;
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i) ptx::st_global_v8(wrow_p + c + 8 * i, r + 8 * i);
-          }
         }
       } else {  // K_DW2 / K_DW1: fp32 weight gradient tile [128 x BN] of expert e
         const int m0 = tc.mt * GEMM_BM + 32 * q;

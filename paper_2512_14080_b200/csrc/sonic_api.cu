@@ -519,7 +519,6 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = d / BN; a.k_blocks = (n + 63) / 64; a.N_dim = d;
-    a.out = static_cast<__nv_bfloat16*>(Ybuf);
     ProfScope ps("down", st);
     if (!launch_gemm<K_DOWN>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
   }
@@ -608,7 +607,6 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       !map2d(&mC6, dXt, false, R, d, 64, 32))
     return SONIC_ERR_CUDA;
   a6.n_tiles = d / BN6; a6.k_blocks = (2 * n) / 64; a6.N_dim = d;
-  a6.out = static_cast<__nv_bfloat16*>(dXt);
   // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
   if (!map2d(&mA5, Ap, false, R, n, 64, 64) || !map2d(&mB5, dO, false, s.T, d, 64, 1) ||
       !map3d(&mC5, dW2, true, E, n, d, 32, 32))
@@ -616,7 +614,6 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   a5.n_tiles = d / BN5; a5.m_tiles = (n + 127) / 128; a5.M_dim = n; a5.N_dim = d;
   a5.gsrc = static_cast<const __nv_bfloat16*>(dO); a5.gld = d;
   a5.accumulate = (D->flags & SONIC_F_DW_ACCUMULATE) ? 1 : 0;
-  a5.out = reinterpret_cast<__nv_bfloat16*>(dW2);
   const int tiles5 = E * a5.m_tiles * a5.n_tiles;
   // K7 dW1_e = Gather(X)^T dH_e   (varlen-K)
   if (!map2d(&mA7, X, false, s.T, d, 64, 1) || !map2d(&mB7, dH, false, R, 2 * n, 64, 64) ||
@@ -625,7 +622,6 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   a7.n_tiles = (2 * n) / BN7; a7.m_tiles = (d + 127) / 128; a7.M_dim = d; a7.N_dim = 2 * n;
   a7.gsrc = static_cast<const __nv_bfloat16*>(X); a7.gld = d;
   a7.accumulate = (D->flags & SONIC_F_DW_ACCUMULATE) ? 1 : 0;
-  a7.out = reinterpret_cast<__nv_bfloat16*>(dW1);
   const int tiles7 = E * a7.m_tiles * a7.n_tiles;
 
   auto run_dxt = [&]() {
