@@ -234,6 +234,18 @@ def main():
     from paper_2512_14080_b200.inputs import make_inputs
 
     torch.cuda.set_device(local)
+    if os.environ.get("SONIC_L2_PERSIST_MB"):  # experiment: L2 set-aside for evict_last lines
+        import ctypes
+        rt_ = ctypes.CDLL("libcudart.so.12") if os.path.exists("/usr/local/cuda/lib64/libcudart.so.12") else None
+        if rt_ is not None:
+            mb = int(os.environ["SONIC_L2_PERSIST_MB"])
+            st = rt_.cudaDeviceSetLimit(ctypes.c_int(6), ctypes.c_size_t(mb << 20))  # cudaLimitPersistingL2CacheSize
+            got = ctypes.c_size_t(0)
+            rt_.cudaDeviceGetLimit(ctypes.byref(got), ctypes.c_int(6))
+            mx = ctypes.c_int(0)
+            rt_.cudaDeviceGetAttribute(ctypes.byref(mx), ctypes.c_int(108), ctypes.c_int(local))  # MaxPersistingL2CacheSize
+            print(f"[l2 persist] set {mb} MB -> status {st}, limit {got.value >> 20} MB (max {mx.value >> 20} MB)",
+                  file=sys.stderr)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)

@@ -202,7 +202,7 @@ __device__ __forceinline__ int tok_of(const int* row_token, int r) { return __ld
 #endif
 __device__ __forceinline__ size_t clamp_tok(int t) { return (size_t)max(t, 0); }
 __device__ __forceinline__ void gather16(uint32_t dst, const void* src, uint64_t pol) {
-  if (SONIC_L2_HINTS) ptx::cp_async16_hint(dst, src, pol);
+  if (SONIC_L2_HINTS & 1) ptx::cp_async16_hint(dst, src, pol);
   else ptx::cp_async16(dst, src);
 }
 

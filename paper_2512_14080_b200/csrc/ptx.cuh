@@ -104,9 +104,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 }
 // L2 cache policies: the streamed epilogue outputs are marked evict-first and the gathered
 // activation rows (X / dO, read by K experts' tiles) evict-last, so the outputs do not push the
-// gather sources out of L2 (SONIC_L2_HINTS; 0 disables).
+// gather sources out of L2 (SONIC_L2_HINTS bit mask: 1 = gathered rows evict-last, 2 = stores
+// evict-first; 0 disables).
 #ifndef SONIC_L2_HINTS
-#define SONIC_L2_HINTS 1
+#define SONIC_L2_HINTS 3
 #endif
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
@@ -119,7 +120,7 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
-  if (SONIC_L2_HINTS) {
+  if (SONIC_L2_HINTS & 2) {
     asm volatile(
         "cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
             map),
@@ -132,7 +133,7 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
   }
 }
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
-  if (SONIC_L2_HINTS) {
+  if (SONIC_L2_HINTS & 2) {
     asm volatile(
         "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(
             map),

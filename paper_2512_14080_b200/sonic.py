@@ -13,7 +13,8 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsonic.so")
+# SONIC_LIB: experiment builds only (tools/ab.sh); the product path is the in-tree libsonic.so
+LIB_PATH = os.environ.get("SONIC_LIB") or os.path.join(_HERE, "libsonic.so")
 
 SONIC_ROUTE_TC = 0
 SONIC_ROUTE_TR_NRF = 1
