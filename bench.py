@@ -189,6 +189,8 @@ def workload_config(args, cfg):
                         f"route={args.mode}",
             "T": cfg["T"], "d": cfg["d"], "n": cfg["n"], "E": cfg["E"], "K": cfg["K"], "route": args.mode,
             "parallelism": f"ep{args.gpus}" if (args.gpus > 1 or getattr(args, "ep", False)) else "single",
+            **({"ep_exchange": "peer-memory kernels (CUDA IPC)" if args.comm == "peer" else "NCCL all-to-all-v"}
+               if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             "l2": "not flushed: per-step working set (X, W1, W2, H, Y, dX~, ...) is several GB >> 126 MB L2"}
 
 
@@ -210,6 +212,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", default="", help="write the per-kernel table to this JSON file")
     ap.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
+                    help="EP exchange: NCCL all-to-all-v, or libsonic's peer-memory kernels (CUDA IPC / NVLink)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -291,7 +295,10 @@ def main():
         L = E // G
         X, dOin, S = make_token_inputs(T, d, E, seed=args.seed + 17 * rank, device=dev)
         W1, W2 = make_expert_weights(rank * L, (rank + 1) * L, d, n, seed=args.seed, device=dev)
-        comm = ep.DistComm() if world > 1 else ep.SimComm(1)
+        if args.comm == "peer":
+            comm = ep.PeerComm(G, T, d, L, [rank])
+        else:
+            comm = ep.DistComm() if world > 1 else ep.SimComm(1)
         rk = ep.EPRank(T, d, n, E, K, G, rank, W1, W2, mode=mode)
 
         def run(Xa, Sa, dOa, slot=0):

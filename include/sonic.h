@@ -246,6 +246,48 @@ sonic_status sonic_ep_ds_dense(const sonic_moe_desc *local_desc, const sonic_rou
 sonic_status sonic_ep_ds_scatter(const sonic_moe_desc *desc, int G, const sonic_routing *rt,
                                  const sonic_ep_plan *plan, const float *back, float *dS, void *stream);
 
+/*
+ * ---------------------------------------------------------------- peer-memory exchange (NEXT-2)
+ * The EP all-to-all-v without NCCL (the paper's future work on
+ * communication).  Each rank of the group allocates one symmetric region of `bytes` and maps
+ * every other rank's region over CUDA IPC (NVLink peer memory on an NVSwitch box).  Kernels store
+ * rows straight into the destination rank's region; sonic_peer_barrier orders the phases on the
+ * stream (system-scope release/acquire flags), with no host synchronisation.
+ * Ownership: sonic_peer_create allocates the region and the flags (cudaMalloc on the current
+ * device) and sonic_peer_destroy frees them (it synchronises the device first).  Every rank must
+ * issue the same sequence of sonic_peer_barrier calls.  All calls return SONIC_ERR_INVALID_ARG on
+ * bad arguments (before any launch) and SONIC_ERR_CUDA on a CUDA failure.
+ */
+#define SONIC_PEER_MAX 32
+#define SONIC_PEER_HANDLE_BYTES 256
+typedef struct sonic_peer sonic_peer;
+/* Allocate this rank's region and flags; write the exportable handle blob (SONIC_PEER_HANDLE_BYTES
+ * bytes) to `handle` -- the caller exchanges the blobs (e.g. all_gather) and passes all of them,
+ * rank-ordered, to sonic_peer_open.  Ranks created in the same process (virtual ranks on one GPU,
+ * each driving its own stream) are mapped by their raw pointers instead of CUDA IPC. */
+sonic_status sonic_peer_create(int rank, int world, size_t bytes, sonic_peer **out, void *handle);
+sonic_status sonic_peer_open(sonic_peer *peer, const void *handles /* [world][SONIC_PEER_HANDLE_BYTES] */);
+/* Device address of rank r's region as mapped in this process (r == own rank: the own region). */
+void        *sonic_peer_base(const sonic_peer *peer, int r);
+sonic_status sonic_peer_destroy(sonic_peer *peer);
+/* Stream-ordered barrier over the group: the work queued before it on `stream` on every rank
+ * (its peer stores) is visible to the work queued after it on every rank. */
+sonic_status sonic_peer_barrier(sonic_peer *peer, void *stream);
+/* Fused dispatch: send row i of the plan (destination g: send_offsets[g] <= i < send_offsets[g+1])
+ * = src[send_token[i]] ([T,d] bf16) is stored as row dst_row0[g] + (i - send_offsets[g]) of the
+ * [*, d] bf16 array at byte offset region_off of rank g's region.  dst_row0: HOST array [G] (the
+ * rows the lower source ranks put there, from the count matrix).  The caller sizes the regions
+ * (capacity T*G rows per source block is always enough). */
+sonic_status sonic_ep_pack_peer(const sonic_moe_desc *desc, int G, const sonic_ep_plan *plan, const void *src,
+                                const sonic_peer *peer, size_t region_off, const int32_t *dst_row0, void *stream);
+/* Block put: rows [src_row0[g], src_row0[g] + cnt[g]) of the device array src (row_bytes each, a
+ * multiple of 4; 16-byte vectors when row_bytes, src and region_off allow) to rows [dst_row0[g], ...) of the array at byte offset region_off of rank g's
+ * region, for every g < G (= world).  src_row0 / cnt / dst_row0: HOST arrays [G].  Returns
+ * SONIC_ERR_INVALID_ARG if a block would end past the region. */
+sonic_status sonic_peer_put_rows(const sonic_peer *peer, int G, const void *src, size_t row_bytes,
+                                 const int32_t *src_row0, const int32_t *cnt, const int32_t *dst_row0,
+                                 size_t region_off, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

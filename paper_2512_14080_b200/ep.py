@@ -20,6 +20,7 @@ The algorithm is written for a LIST of local ranks so that the same code runs
 """
 from __future__ import annotations
 
+import contextlib
 from dataclasses import dataclass, field
 
 import torch
@@ -43,7 +44,10 @@ class SimComm:
         host = torch.stack([c[: self.G] for c in send_dev]).cpu().tolist()
         return host, self.exchange_counts(host)
 
-    def alltoallv(self, sends, send_counts, recv_counts):
+    def rank_stream(self, i):
+        return contextlib.nullcontext()
+
+    def alltoallv(self, sends, send_counts, recv_counts, tag=None):
         outs = []
         for g in range(self.G):
             parts = []
@@ -53,7 +57,7 @@ class SimComm:
             outs.append(parts[0] if len(parts) == 1 else torch.cat(parts, 0))  # G = 1: a view, no copy
         return outs
 
-    def alltoallv_start(self, sends, send_counts, recv_counts):
+    def alltoallv_start(self, sends, send_counts, recv_counts, tag=None):
         return self.alltoallv(sends, send_counts, recv_counts)
 
     def alltoallv_finish(self, pending):
@@ -90,10 +94,13 @@ class DistComm:
         both = torch.stack([t, r]).cpu().tolist()
         return [both[0]], [both[1]]
 
-    def alltoallv(self, sends, send_counts, recv_counts):
+    def rank_stream(self, i):
+        return contextlib.nullcontext()
+
+    def alltoallv(self, sends, send_counts, recv_counts, tag=None):
         return self.alltoallv_finish(self.alltoallv_start(sends, send_counts, recv_counts))
 
-    def alltoallv_start(self, sends, send_counts, recv_counts):
+    def alltoallv_start(self, sends, send_counts, recv_counts, tag=None):
         """Issue the exchange asynchronously (NCCL runs it on its own stream after the work already
         queued on the current stream); alltoallv_finish makes the current stream wait for it."""
         (s,), (sc,), (rc,) = sends, send_counts, recv_counts
@@ -111,6 +118,159 @@ class DistComm:
         out, work, dev, _src = pending
         work.wait()
         return [out.to(dev) if dev is not None else out]
+
+
+class PeerComm:
+    """The exchange through peer memory (libsonic sonic_peer_*; NEXT-2): no NCCL on the data path.
+
+    Each local rank owns one symmetric region (CUDA IPC across processes -- NVLink peer memory on an
+    NVSwitch box -- or raw pointers between virtual ranks of one process).  Region layout, rows of
+    capacity NS = T*G (a destination receives at most T rows from each source, a source gets back at
+    most its T*G send rows):
+
+      counts [G, G] i32 | x [NS, d] bf16 | gate [NS, L] f32 | do [NS, d] bf16 | back [NS, d] bf16 |
+      ds [NS, L] f32
+
+    `back` serves the forward return (Y partial sums) and the backward return (dX~ partial sums):
+    the pre-exchange barrier orders the backward's stores after the forward's combine on every rank.
+    Each exchange is barrier -> stores into the peers -> barrier on the rank's stream; the dispatch
+    stores come straight from the gather (sonic_ep_pack_peer), the returns are block puts.  The only
+    host synchronisation is the read of the count matrix (received-row counts size the local GEMMs).
+
+    ranks: the local ranks (one per process under torchrun, or G virtual ranks in one process, each
+    on its own CUDA stream so their barriers can meet).
+    """
+
+    def __init__(self, G, T, d, L, local_ranks, group=None, device=None):
+        self.G, self.T, self.d, self.L = G, T, d, L
+        self.local = list(local_ranks)
+        ns = T * G
+        off, lay = 0, {}
+        for name, nbytes in (("counts", G * G * 4), ("x", ns * d * 2), ("gate", ns * L * 4), ("do", ns * d * 2),
+                             ("back", ns * d * 2), ("ds", ns * L * 4)):
+            lay[name] = off
+            off += (nbytes + 255) // 256 * 256
+        self.lay, self.nbytes = lay, off
+        self.regions = [sonic.PeerRegion(r, G, off) for r in self.local]
+        blobs = [rg.handle() for rg in self.regions]
+        if len(self.local) < G:  # one rank per process: exchange the handle blobs (setup only)
+            import torch.distributed as dist
+            allb = [None] * G
+            dist.all_gather_object(allb, blobs[0], group=group)
+            blobs = allb
+        for rg in self.regions:
+            rg.open(blobs)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.streams = [torch.cuda.Stream(device=dev) for _ in self.local] if len(self.local) > 1 else [None]
+        self.M = None
+
+    def close(self):
+        torch.cuda.synchronize()
+        for rg in self.regions:
+            rg.close()
+        self.regions = []
+
+    # ---------------------------------------------------------------- streams
+    @contextlib.contextmanager
+    def rank_stream(self, i):
+        st = self.streams[i]
+        if st is None:
+            yield
+            return
+        st.wait_stream(torch.cuda.default_stream(st.device))
+        with torch.cuda.stream(st):
+            yield
+
+    def join(self):
+        """Make the default stream wait for the virtual ranks' streams."""
+        cur = torch.cuda.current_stream()
+        for st in self.streams:
+            if st is not None:
+                cur.wait_stream(st)
+
+    # ---------------------------------------------------------------- counts
+    def exchange_counts_dev(self, send_dev):
+        """Every rank stores its G send counts into row `rank` of every rank's count matrix; one host
+        read of the own matrix gives M[s][g] = rows s sends to g."""
+        G = self.G
+        for i, (rg, c) in enumerate(zip(self.regions, send_dev)):
+            with self.rank_stream(i):
+                rg.barrier()
+                rg.put_rows(c[:G].contiguous(), G * 4, [0] * G, [1] * G, [rg.rank] * G, self.lay["counts"])
+                rg.barrier()
+        Ms = []
+        for i, rg in enumerate(self.regions):
+            with self.rank_stream(i):
+                Ms.append(rg.view(self.lay["counts"], (G, G), torch.int32).cpu().tolist())
+        self.M = Ms[0]
+        assert all(m == self.M for m in Ms)
+        send = [self.M[rg.rank] for rg in self.regions]
+        recv = [[self.M[s][rg.rank] for s in range(G)] for rg in self.regions]
+        return send, recv
+
+    # ---------------------------------------------------------------- block offsets (from M)
+    def _dispatch_rows(self, me):
+        """dst_row0[g] = rows the lower sources put into g; my block i -> g is my send rows."""
+        G, M = self.G, self.M
+        return [sum(M[s][g] for s in range(me)) for g in range(G)]
+
+    def _return_rows(self, me):
+        """As a destination, the block received from source s (rows [recv_off[s], +M[s][me])) goes back
+        to rows [send_off_s[me], ...) of s's return area (s's send-buffer order)."""
+        G, M = self.G, self.M
+        src0 = [sum(M[s2][me] for s2 in range(s)) for s in range(G)]
+        cnt = [M[s][me] for s in range(G)]
+        dst0 = [sum(M[s][g2] for g2 in range(me)) for s in range(G)]
+        return src0, cnt, dst0
+
+    # ---------------------------------------------------------------- exchanges
+    def dispatch_packed(self, ranks, srcs, tag):
+        """Fused pack + dispatch: each rank's kernel gathers src[send_token] straight into the
+        destination ranks' `tag` area.  Returns the received rows of each local rank."""
+        outs = []
+        for i, (rk, rg, src) in enumerate(zip(ranks, self.regions, srcs)):
+            with self.rank_stream(i):
+                rg.barrier()
+                rg.pack(rk.desc(), self.G, rk.ctx["plan"], src, self.lay[tag], self._dispatch_rows(rg.rank))
+                rg.barrier()
+        for i, rg in enumerate(self.regions):
+            n_in = sum(self.M[s][rg.rank] for s in range(self.G))
+            outs.append(rg.view(self.lay[tag], (n_in, self.d), torch.bfloat16))
+        return outs
+
+    _RETURN = {"y": "back", "dx": "back", "ds": "ds"}
+
+    def alltoallv(self, sends, send_counts, recv_counts, tag=None):
+        """Block exchange of per-destination-contiguous rows: dispatch direction for tag "gate",
+        return direction (back to the sources, send-buffer order) for "y", "dx", "ds"."""
+        outs = []
+        ret = tag in self._RETURN
+        area = self._RETURN.get(tag, tag)
+        for i, (rg, snd) in enumerate(zip(self.regions, sends)):
+            with self.rank_stream(i):
+                row_bytes = snd[0].numel() * snd.element_size() if snd.dim() > 1 else snd.element_size()
+                if ret:
+                    src0, cnt, dst0 = self._return_rows(rg.rank)
+                else:
+                    me = rg.rank
+                    cnt = list(self.M[me])
+                    src0 = [sum(cnt[:g]) for g in range(self.G)]
+                    dst0 = self._dispatch_rows(me)
+                rg.barrier()
+                if sum(cnt) and snd.numel():
+                    rg.put_rows(snd.contiguous(), row_bytes, src0, cnt, dst0, self.lay[area])
+                rg.barrier()
+        for i, (rg, snd) in enumerate(zip(self.regions, sends)):
+            me = rg.rank
+            n = sum(self.M[me]) if ret else sum(self.M[s][me] for s in range(self.G))
+            outs.append(rg.view(self.lay[area], (n,) + tuple(snd.shape[1:]), snd.dtype))
+        return outs
+
+    def alltoallv_start(self, sends, send_counts, recv_counts, tag=None):
+        return self.alltoallv(sends, send_counts, recv_counts, tag=tag)
+
+    def alltoallv_finish(self, pending):
+        return pending
 
 
 # ------------------------------------------------------------------------------- one rank
@@ -137,16 +297,22 @@ class EPRank:
         return sonic.make_desc(self.T, self.d, self.n, self.E, self.K, mode=self.mode)
 
     # -------------------------------------------------------------- forward
-    def dispatch_fwd(self, X, S):
+    def plan_fwd(self, S):
+        """Route the own tokens over all E experts and build the dispatch plan -> (gates of the send
+        rows [T*G, L], device send counts [G])."""
         desc = self.desc()
         rt = sonic.sonic_route(desc, S)
         plan = sonic.sonic_ep_build_plan(desc, self.G, rt)
         nmax = self.T * self.G
-        send_x = torch.empty(nmax, self.d, dtype=torch.bfloat16, device=X.device)
-        sonic.sonic_ep_pack(desc, self.G, plan, X, send_x)
         self.ctx.update(rt=rt, plan=plan)
         gates = plan.send_gate[: nmax * self.L].view(nmax, self.L)
-        return send_x, gates, plan.send_counts  # device counts: read once, with the exchange
+        return gates, plan.send_counts  # device counts: read once, with the exchange
+
+    def pack(self, src):
+        """Send rows (X forward, dO backward) into a staging buffer (the NCCL / SimComm path)."""
+        send = torch.empty(self.T * self.G, self.d, dtype=torch.bfloat16, device=src.device)
+        sonic.sonic_ep_pack(self.desc(), self.G, self.ctx["plan"], src, send)
+        return send
 
     def compute_fwd(self, recv_x, recv_gate):
         R_in = recv_x.shape[0]
@@ -166,11 +332,6 @@ class EPRank:
         return out
 
     # -------------------------------------------------------------- backward
-    def dispatch_bwd(self, dO):
-        send = torch.empty(self.T * self.G, self.d, dtype=torch.bfloat16, device=dO.device)
-        sonic.sonic_ep_pack(self.desc(), self.G, self.ctx["plan"], dO, send)
-        return send
-
     def _ldesc(self, extra_flags):
         ld = self.ctx["ldesc"]
         return sonic.make_desc(ld.T, ld.d, ld.n, ld.E, ld.K, mode=ld.route_mode, flags=ld.flags | extra_flags)
@@ -223,34 +384,65 @@ class EPRank:
 
 
 # ------------------------------------------------------------------------------- the layer step
+def _dispatch(ranks, comm, srcs, send_counts, recv_counts, tag):
+    """Rows src[send_token] of every local rank to their destination ranks."""
+    if hasattr(comm, "dispatch_packed"):  # peer memory: the gather stores into the destinations
+        return comm.dispatch_packed(ranks, srcs, tag)
+    sends = []
+    for i, (r, src) in enumerate(zip(ranks, srcs)):
+        with comm.rank_stream(i):
+            sends.append(r.pack(src))
+    return comm.alltoallv(sends, send_counts, recv_counts, tag=tag)
+
+
 def ep_forward(ranks, comm, Xs, Ss):
     """Forward of the EP layer over the local ranks -> [O_r]."""
-    disp = [r.dispatch_fwd(X, S) for r, X, S in zip(ranks, Xs, Ss)]
-    # NCCL takes host split sizes: the only host synchronisation of the layer step
-    send_counts, recv_counts = comm.exchange_counts_dev([c for _, _, c in disp])
+    disp = []
+    for i, (r, S) in enumerate(zip(ranks, Ss)):
+        with comm.rank_stream(i):
+            disp.append(r.plan_fwd(S))
+    # the send counts are host arguments of the exchange: the only host synchronisation of the step
+    send_counts, recv_counts = comm.exchange_counts_dev([c for _, c in disp])
     for r, sc in zip(ranks, send_counts):
         r.ctx["counts"] = sc
-    recv_x = comm.alltoallv([x for x, _, _ in disp], send_counts, recv_counts)
-    recv_g = comm.alltoallv([g for _, g, _ in disp], send_counts, recv_counts)
-    parts = [r.compute_fwd(x, g) for r, x, g in zip(ranks, recv_x, recv_g)]
-    back = comm.alltoallv(parts, recv_counts, send_counts)
-    for r, rc in zip(ranks, recv_counts):
+    recv_x = _dispatch(ranks, comm, Xs, send_counts, recv_counts, "x")
+    recv_g = comm.alltoallv([g for g, _ in disp], send_counts, recv_counts, tag="gate")
+    parts = []
+    for i, (r, x, g) in enumerate(zip(ranks, recv_x, recv_g)):
+        with comm.rank_stream(i):
+            parts.append(r.compute_fwd(x, g))
+    back = comm.alltoallv(parts, recv_counts, send_counts, tag="y")
+    outs = []
+    for i, (r, rc, b) in enumerate(zip(ranks, recv_counts, back)):
         r.ctx["recv_counts"] = rc
-    return [r.combine_fwd(b) for r, b in zip(ranks, back)]
+        with comm.rank_stream(i):
+            outs.append(r.combine_fwd(b))
+    if hasattr(comm, "join"):
+        comm.join()
+    return outs
 
 
 def ep_backward(ranks, comm, dOs):
     """Backward over the local ranks -> [(dX_r, dS_r)]; each rank keeps its local dW1 / dW2."""
     send_counts = [r.ctx["counts"] for r in ranks]
     recv_counts = [r.ctx["recv_counts"] for r in ranks]
-    sends = [r.dispatch_bwd(dO) for r, dO in zip(ranks, dOs)]
-    recv = comm.alltoallv(sends, send_counts, recv_counts)
-    outs = [r.compute_bwd(x) for r, x in zip(ranks, recv)]
-    # the dX~ / dS exchange runs while the local weight gradients are computed
-    p_dx = comm.alltoallv_start([o[0] for o in outs], recv_counts, send_counts)
-    p_ds = comm.alltoallv_start([o[1] for o in outs], recv_counts, send_counts)
-    for r in ranks:
-        r.compute_bwd_dw()
+    recv = _dispatch(ranks, comm, dOs, send_counts, recv_counts, "do")
+    outs = []
+    for i, (r, x) in enumerate(zip(ranks, recv)):
+        with comm.rank_stream(i):
+            outs.append(r.compute_bwd(x))
+    # the dX~ / dS exchange runs while the local weight gradients are computed (NCCL path)
+    p_dx = comm.alltoallv_start([o[0] for o in outs], recv_counts, send_counts, tag="dx")
+    p_ds = comm.alltoallv_start([o[1] for o in outs], recv_counts, send_counts, tag="ds")
+    for i, r in enumerate(ranks):
+        with comm.rank_stream(i):
+            r.compute_bwd_dw()
     back_dx = comm.alltoallv_finish(p_dx)
     back_ds = comm.alltoallv_finish(p_ds)
-    return [r.combine_bwd(bx, bs) for r, bx, bs in zip(ranks, back_dx, back_ds)]
+    res = []
+    for i, (r, bx, bs) in enumerate(zip(ranks, back_dx, back_ds)):
+        with comm.rank_stream(i):
+            res.append(r.combine_bwd(bx, bs))
+    if hasattr(comm, "join"):
+        comm.join()
+    return res

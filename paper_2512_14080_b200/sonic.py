@@ -107,6 +107,22 @@ def lib():
         L.sonic_ep_ds_scatter.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sonic_routing), P(sonic_ep_plan), vp,
                                           vp, vp]
         L.sonic_ep_ds_scatter.restype = ctypes.c_int
+        L.sonic_peer_create.argtypes = [ctypes.c_int, ctypes.c_int, sz, P(vp), vp]
+        L.sonic_peer_create.restype = ctypes.c_int
+        L.sonic_peer_open.argtypes = [vp, vp]
+        L.sonic_peer_open.restype = ctypes.c_int
+        L.sonic_peer_base.argtypes = [vp, ctypes.c_int]
+        L.sonic_peer_base.restype = vp
+        L.sonic_peer_destroy.argtypes = [vp]
+        L.sonic_peer_destroy.restype = ctypes.c_int
+        L.sonic_peer_barrier.argtypes = [vp, vp]
+        L.sonic_peer_barrier.restype = ctypes.c_int
+        L.sonic_ep_pack_peer.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sonic_ep_plan), vp, vp, sz,
+                                         P(ctypes.c_int32), vp]
+        L.sonic_ep_pack_peer.restype = ctypes.c_int
+        L.sonic_peer_put_rows.argtypes = [vp, ctypes.c_int, vp, sz, P(ctypes.c_int32), P(ctypes.c_int32),
+                                          P(ctypes.c_int32), sz, vp]
+        L.sonic_peer_put_rows.restype = ctypes.c_int
         L.sonic_profile_enable.argtypes = [ctypes.c_int]
         L.sonic_profile_enable.restype = None
         L.sonic_profile_collect.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
@@ -339,3 +355,70 @@ def sonic_ep_ds_scatter(desc, G, rt, plan, back, dS):
     _done(lib().sonic_ep_ds_scatter(ctypes.byref(desc), G, ctypes.byref(rt.c), ctypes.byref(plan.c), _ptr(back),
                                      _ptr(dS), _stream()), "sonic_ep_ds_scatter")
     return dS
+
+
+# ---------------------------------------------------------------- peer-memory exchange (NEXT-2)
+SONIC_PEER_HANDLE_BYTES = 256
+
+
+def _i32(vals):
+    return (ctypes.c_int32 * len(vals))(*[int(v) for v in vals])
+
+
+class PeerRegion:
+    """One rank's symmetric region, mapped into every rank of the group (sonic_peer_*)."""
+
+    def __init__(self, rank, world, nbytes):
+        self.rank, self.world, self.nbytes = rank, world, int(nbytes)
+        self.h = ctypes.c_void_p()
+        self.blob = ctypes.create_string_buffer(SONIC_PEER_HANDLE_BYTES)
+        _check(lib().sonic_peer_create(rank, world, self.nbytes, ctypes.byref(self.h), self.blob),
+               "sonic_peer_create")
+
+    def handle(self):
+        """The exportable handle blob (bytes) of this rank."""
+        return self.blob.raw
+
+    def open(self, blobs):
+        """blobs: the handle blobs of all ranks, rank-ordered."""
+        assert len(blobs) == self.world and all(len(b) == SONIC_PEER_HANDLE_BYTES for b in blobs)
+        buf = ctypes.create_string_buffer(b"".join(blobs), SONIC_PEER_HANDLE_BYTES * self.world)
+        _check(lib().sonic_peer_open(self.h, buf), "sonic_peer_open")
+
+    def view(self, offset, shape, dtype):
+        """A torch tensor over the OWN region at byte offset `offset` (no copy)."""
+        base = lib().sonic_peer_base(self.h, self.rank)
+        numel = 1
+        for v in shape:
+            numel *= int(v)
+        es = torch.empty(0, dtype=dtype).element_size()
+        assert offset % 16 == 0 and offset + numel * es <= self.nbytes
+        return _wrap_device_ptr(base + offset, numel * es).view(dtype)[:numel].view(*shape)
+
+    def barrier(self):
+        _done(lib().sonic_peer_barrier(self.h, _stream()), "sonic_peer_barrier")
+
+    def pack(self, desc, G, plan, src, region_off, dst_row0):
+        _done(lib().sonic_ep_pack_peer(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(src), self.h,
+                                       int(region_off), _i32(dst_row0), _stream()), "sonic_ep_pack_peer")
+
+    def put_rows(self, src, row_bytes, src_row0, cnt, dst_row0, region_off):
+        _done(lib().sonic_peer_put_rows(self.h, self.world, _ptr(src), int(row_bytes), _i32(src_row0), _i32(cnt),
+                                        _i32(dst_row0), int(region_off), _stream()), "sonic_peer_put_rows")
+
+    def close(self):
+        if self.h:
+            _check(lib().sonic_peer_destroy(self.h), "sonic_peer_destroy")
+            self.h = ctypes.c_void_p()
+
+
+class _DevBuf:
+    """__cuda_array_interface__ over a raw device pointer owned by libsonic (the peer region)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _wrap_device_ptr(ptr, nbytes):
+    return torch.as_tensor(_DevBuf(ptr, nbytes), device="cuda")

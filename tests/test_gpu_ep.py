@@ -1,5 +1,7 @@
-"""Expert-parallel layer on one GPU: G virtual ranks exchange through SimComm (the same ep.py code
-runs one rank per process over NCCL).  Every rank's outputs are compared with the fp64 oracle run
+"""Expert-parallel layer on one GPU: G virtual ranks exchange through SimComm or through peer memory
+(PeerComm: each virtual rank drives its own stream, the dispatch kernels store into the other
+ranks' regions and the flag barriers order the phases; the same ep.py code runs one rank per process
+over NCCL or CUDA IPC).  Every rank's outputs are compared with the fp64 oracle run
 on that rank's own microbatch with the full expert set; dW shards with the oracle's dW summed over
 all ranks' tokens."""
 import numpy as np
@@ -14,9 +16,40 @@ from tests.parity import assert_close, f64
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("G,mode,E", [(1, "tc", 16), (2, "tc", 16), (4, "tc", 16), (2, "tr", 16), (4, "tr", 16),
-                                      (2, "tc", 64)])
-def test_ep_matches_oracle(G, mode, E):
+def _run_ep(G, mode, E, comm_kind, T=768, d=128, n=64, K=4):
+    m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
+    base = make_inputs(T, d, n, E, K, seed=40, device="cuda")
+    W1, W2 = base.W1, base.W2
+    L = E // G
+    ins = [make_inputs(T, d, n, E, K, seed=41 + r, device="cuda") for r in range(G)]
+    ranks = [ep.EPRank(T, d, n, E, K, G, r, W1[r * L:(r + 1) * L].contiguous(), W2[r * L:(r + 1) * L].contiguous(),
+                       mode=m) for r in range(G)]
+    comm = ep.SimComm(G) if comm_kind == "sim" else ep.PeerComm(G, T, d, L, range(G))
+    Os = ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins])
+    outs = ep.ep_backward(ranks, comm, [i.dO for i in ins])
+    torch.cuda.synchronize()
+    res = [(Os[r].clone(), outs[r][0].clone(), outs[r][1].clone(), ranks[r].dW1.clone(), ranks[r].dW2.clone())
+           for r in range(G)]
+    if comm_kind == "peer":
+        comm.close()
+    return res
+
+
+@pytest.mark.parametrize("G,mode,E", [(2, "tc", 16), (4, "tr", 16), (2, "tc", 64)])
+def test_ep_peer_equals_sim(G, mode, E):
+    """The peer-memory exchange moves the same rows to the same places as the staged exchange: every
+    output of every rank is bit-identical."""
+    a = _run_ep(G, mode, E, "sim")
+    b = _run_ep(G, mode, E, "peer")
+    for r in range(G):
+        for name, x, y in zip(("O", "dX", "dS", "dW1", "dW2"), a[r], b[r]):
+            assert torch.equal(x, y), f"rank {r} {name} differs between SimComm and PeerComm"
+
+
+@pytest.mark.parametrize("G,mode,E,comm_kind", [(1, "tc", 16, "sim"), (2, "tc", 16, "sim"), (4, "tc", 16, "sim"),
+                                                (2, "tr", 16, "sim"), (4, "tr", 16, "sim"), (2, "tc", 64, "sim"),
+                                                (2, "tc", 16, "peer"), (4, "tr", 16, "peer")])
+def test_ep_matches_oracle(G, mode, E, comm_kind):
     """E = 64 over 2 ranks: 32 local experts, so the receive side's GIVEN routing has K = 32 > 16."""
     T, d, n, K = 768, 128, 64, 4
     m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
@@ -26,7 +59,7 @@ def test_ep_matches_oracle(G, mode, E):
     ins = [make_inputs(T, d, n, E, K, seed=41 + r, device="cuda") for r in range(G)]
     ranks = [ep.EPRank(T, d, n, E, K, G, r, W1[r * L:(r + 1) * L].contiguous(), W2[r * L:(r + 1) * L].contiguous(),
                        mode=m) for r in range(G)]
-    comm = ep.SimComm(G)
+    comm = ep.SimComm(G) if comm_kind == "sim" else ep.PeerComm(G, T, d, L, range(G))
     Os = ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins])
     outs = ep.ep_backward(ranks, comm, [i.dO for i in ins])
     torch.cuda.synchronize()
@@ -49,6 +82,8 @@ def test_ep_matches_oracle(G, mode, E):
     dW2 = np.concatenate([f64(rk.dW2) for rk in ranks], 0)
     assert_close("dW1", dW1, dW1_ref)
     assert_close("dW2", dW2, dW2_ref)
+    if comm_kind == "peer":
+        comm.close()
 
 
 def test_ep_plan_dedup():

@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mode, q):
+def _worker(rank, world, port, mode, q, comm_kind="dist"):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -38,18 +38,24 @@ def _worker(rank, world, port, mode, q):
         W1, W2 = (t.cuda() for t in make_expert_weights(rank * L, (rank + 1) * L, d, n, seed=5))
         m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
         rk = ep.EPRank(T, d, n, E, K, world, rank, W1, W2, mode=m)
-        comm = ep.DistComm()
+        # dist: host-staged all-to-all over gloo; peer: CUDA IPC regions (handles exchanged over gloo),
+        # the dispatch/return kernels store into the other process's region, flag barriers order them
+        comm = ep.DistComm() if comm_kind == "dist" else ep.PeerComm(world, T, d, L, [rank])
         (O,) = ep.ep_forward([rk], comm, [X], [S])
         ((dX, dS),) = ep.ep_backward([rk], comm, [dO])
         torch.cuda.synchronize()
+        if comm_kind == "peer":
+            O, dX, dS = O.clone(), dX.clone(), dS.clone()
+            dist.barrier()  # no rank unmaps its region while a peer may still store into it
+            comm.close()
         # numpy by value: torch CPU tensors would travel as shared-memory handles that die with this process
         q.put((rank,) + tuple(t.float().cpu().numpy() for t in (O, dX, dS, rk.dW1, rk.dW2)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["tc", "tr"])
-def test_ep_two_processes(mode):
+@pytest.mark.parametrize("mode,comm_kind", [("tc", "dist"), ("tr", "dist"), ("tc", "peer"), ("tr", "peer")])
+def test_ep_two_processes(mode, comm_kind):
     from oracle import moe_oracle as om
     from paper_2512_14080_b200.inputs import make_expert_weights, make_token_inputs
     from tests.parity import assert_close, f64
@@ -58,7 +64,7 @@ def test_ep_two_processes(mode):
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, port, mode, q, comm_kind)) for r in range(world)]
     for p in ps:
         p.start()
     res = {}
