@@ -119,6 +119,16 @@ bool fill_rows(const sonic_peer* p, int G, const int32_t* a, const int32_t* b, c
   }
   return true;
 }
+
+// CUDA lazy loading loads a kernel at its first launch and may wait for the device to go idle to
+// do so; a first launch queued behind a spinning barrier whose partner has not been queued yet (virtual
+// ranks of one process, queued rank by rank) would then deadlock.  Load every peer kernel up front.
+bool preload_peer_kernels() {
+  cudaFuncAttributes a;
+  return cudaFuncGetAttributes(&a, k_peer_barrier) == cudaSuccess && cudaFuncGetAttributes(&a, k_pack_peer) == cudaSuccess &&
+         cudaFuncGetAttributes(&a, k_put_rows<uint4>) == cudaSuccess &&
+         cudaFuncGetAttributes(&a, k_put_rows<uint32_t>) == cudaSuccess;
+}
 }  // namespace
 
 extern "C" {
@@ -127,6 +137,7 @@ sonic_status sonic_peer_create(int rank, int world, size_t bytes, sonic_peer** o
   if (!out || !handle || world < 1 || world > SONIC_PEER_MAX || rank < 0 || rank >= world || bytes == 0)
     return SONIC_ERR_INVALID_ARG;
   *out = nullptr;
+  if (!preload_peer_kernels()) return SONIC_ERR_CUDA;
   sonic_peer* p = new sonic_peer;
   p->rank = rank;
   p->world = world;
