@@ -483,6 +483,13 @@ def main():
     act = {"X": T * d * 2, "H": R_pad * 2 * n * 2, "metadata": meta_bytes,
            "paper_formula_2Td_4TKn": 2 * T * d + 4 * T * K * n}
     act["total"] = act["X"] + act["H"] + act["metadata"]
+    if not use_ep:
+        # the allocations the step actually holds from the forward to the backward (routing tensors +
+        # the H cache; X is the caller's), and the transient workspaces (A, Y in fwd; dH, A', dX~ in bwd)
+        held = sum(t.numel() * t.element_size() for t in rt.tensors.values()) + H.numel() * H.element_size()
+        act["measured"] = {"held_fwd_to_bwd": held + X.numel() * X.element_size(),
+                           "fwd_workspace": ws_f.numel(), "bwd_workspace": ws_b.numel(),
+                           "peak_allocated": torch.cuda.max_memory_allocated(dev)}
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",

@@ -74,11 +74,20 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 // 16-byte Ampere-style async copy global -> shared (LDGSTS), L1 bypass.
+// L2 prefetch size of the gather copies (SONIC_CPA_L2: 128 or 256 bytes)
+#ifndef SONIC_CPA_L2
+#define SONIC_CPA_L2 128
+#endif
+#if SONIC_CPA_L2 == 256
+#define SONIC_CPA_PF ".L2::256B"
+#else
+#define SONIC_CPA_PF ".L2::128B"
+#endif
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  asm volatile("cp.async.cg.shared.global" SONIC_CPA_PF " [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async16_hint(uint32_t dst, const void* src, uint64_t policy) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint.L2::128B [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint" SONIC_CPA_PF " [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
                "l"(policy)
                : "memory");
 }
