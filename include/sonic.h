@@ -93,6 +93,11 @@ typedef struct {
   int32_t route_mode;  /* sonic_route_mode */
   int32_t flags;       /* SONIC_F_* */
   uint32_t seed;       /* SONIC_ROUTE_TR_SR: seed of the rounding draws (ignored otherwise) */
+  int64_t rows_cap;    /* SONIC_ROUTE_GIVEN: upper bound on the routed (token, expert) pairs, i.e. the
+                          nonzero gates of S (0 = T*K).  Sizes rows_max = rows_cap + E*(m_tile-1) rounded
+                          up to m_tile, so the expert-parallel receive side (K = L local experts) does not
+                          reserve T*L rows.  The caller guarantees it (more nonzero gates than rows_cap
+                          is undefined behaviour); must be 0 for the other modes. */
 } sonic_moe_desc;
 
 /* Routing metadata: written by sonic_route, read by sonic_moe_fwd/bwd.

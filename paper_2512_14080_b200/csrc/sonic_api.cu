@@ -229,17 +229,21 @@ bool valid_desc(const sonic_moe_desc* D) {
   if (D->K > 16 && D->route_mode != SONIC_ROUTE_GIVEN) return false;
   if (D->m_tile != 128) return false;
   if (D->route_mode < SONIC_ROUTE_TC || D->route_mode > SONIC_ROUTE_TR_NRS) return false;
+  if (D->rows_cap < 0 || (D->rows_cap != 0 && D->route_mode != SONIC_ROUTE_GIVEN)) return false;
   return true;
 }
+long long rows_max_of(const sonic_moe_desc* D);
 bool supported_dims(const sonic_moe_desc* D) {
   if (D->d % 64 != 0) return false;
   if (!(D->n == 32 || D->n % 64 == 0)) return false;
-  if (D->T * (long long)D->K + (long long)D->E * 127 >= (1ll << 31)) return false;
+  if (rows_max_of(D) >= (1ll << 31)) return false;
   if ((long long)D->E * D->T >= (1ll << 40)) return false;
   return true;
 }
 long long rows_max_of(const sonic_moe_desc* D) {
-  const long long a = D->T * D->K + (long long)D->E * (GEMM_M - 1);
+  const long long pairs = (D->route_mode == SONIC_ROUTE_GIVEN && D->rows_cap > 0) ? std::min(D->rows_cap, D->T * D->K)
+                                                                                   : D->T * D->K;
+  const long long a = pairs + (long long)D->E * (GEMM_M - 1);
   const long long b = (long long)D->E * ((D->T + GEMM_M - 1) / GEMM_M) * GEMM_M;
   const long long r = std::min(a, b);
   return (r + GEMM_M - 1) / GEMM_M * GEMM_M;

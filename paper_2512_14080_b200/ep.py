@@ -36,12 +36,15 @@ class SimComm:
         self.G = G
 
     def exchange_counts(self, send_counts):
-        """send_counts[s][g] (host ints) -> recv_counts[g][s]."""
-        return [[send_counts[s][g] for s in range(self.G)] for g in range(self.G)]
+        """send_counts[s] (host ints, n blocks of G: block j, entry g = what s sends to g) ->
+        recv[g] (n blocks of G: block j, entry s = what g gets from s)."""
+        G = self.G
+        nb = len(send_counts[0]) // G
+        return [[send_counts[s][j * G + g] for j in range(nb) for s in range(G)] for g in range(G)]
 
     def exchange_counts_dev(self, send_dev):
-        """Device count tensors [G] per local rank -> (send, recv) host lists, one host read."""
-        host = torch.stack([c[: self.G] for c in send_dev]).cpu().tolist()
+        """Device count tensors [n*G] per local rank -> (send, recv) host lists, one host read."""
+        host = torch.stack(list(send_dev)).cpu().tolist()
         return host, self.exchange_counts(host)
 
     def rank_stream(self, i):
@@ -74,24 +77,29 @@ class DistComm:
         self.G = dist.get_world_size(group)
 
     def exchange_counts(self, send_counts):
+        """send_counts: [one host list of n blocks of G] -> [recv list, n blocks of G (entry s)]."""
         (sc,) = send_counts
+        G = self.G
+        nb = len(sc) // G
         dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
-        t = torch.tensor(sc, dtype=torch.int64, device=dev)
+        t = torch.tensor(sc, dtype=torch.int64, device=dev).view(nb, G).t().contiguous()  # row g -> rank g
         r = torch.empty_like(t)
         self.dist.all_to_all_single(r, t, group=self.group)
-        return [r.cpu().tolist()]
+        return [r.t().reshape(-1).cpu().tolist()]  # row s of r came from s
 
     def exchange_counts_dev(self, send_dev):
         """The G send counts of this rank (device int32) -> (send, recv) host lists.  Under NCCL the
         count all-to-all runs on the device and one host read fetches both directions."""
         (c,) = send_dev
+        G = self.G
+        nb = c.numel() // G
         if self.dist.get_backend(self.group) != "nccl":
-            sc = c[: self.G].cpu().tolist()
+            sc = c.cpu().tolist()
             return [sc], self.exchange_counts([sc])
-        t = c[: self.G].to(torch.int64)
+        t = c.to(torch.int64).view(nb, G).t().contiguous()
         r = torch.empty_like(t)
         self.dist.all_to_all_single(r, t, group=self.group)
-        both = torch.stack([t, r]).cpu().tolist()
+        both = torch.stack([t.t().reshape(-1), r.t().reshape(-1)]).cpu().tolist()
         return [both[0]], [both[1]]
 
     def rank_stream(self, i):
@@ -141,12 +149,14 @@ class PeerComm:
     on its own CUDA stream so their barriers can meet).
     """
 
+    NB = 2  # count blocks exchanged per rank: send rows per destination, routed pairs per destination
+
     def __init__(self, G, T, d, L, local_ranks, group=None, device=None):
         self.G, self.T, self.d, self.L = G, T, d, L
         self.local = list(local_ranks)
         ns = T * G
         off, lay = 0, {}
-        for name, nbytes in (("counts", G * G * 4), ("x", ns * d * 2), ("gate", ns * L * 4), ("do", ns * d * 2),
+        for name, nbytes in (("counts", G * self.NB * G * 4), ("x", ns * d * 2), ("gate", ns * L * 4), ("do", ns * d * 2),
                              ("back", ns * d * 2), ("ds", ns * L * 4)):
             lay[name] = off
             off += (nbytes + 255) // 256 * 256
@@ -192,20 +202,23 @@ class PeerComm:
     def exchange_counts_dev(self, send_dev):
         """Every rank stores its G send counts into row `rank` of every rank's count matrix; one host
         read of the own matrix gives M[s][g] = rows s sends to g."""
-        G = self.G
+        G, nb = self.G, self.NB
         for i, (rg, c) in enumerate(zip(self.regions, send_dev)):
+            assert c.numel() == nb * G
             with self.rank_stream(i):
                 rg.barrier()
-                rg.put_rows(c[:G].contiguous(), G * 4, [0] * G, [1] * G, [rg.rank] * G, self.lay["counts"])
+                rg.put_rows(c.to(torch.int32).contiguous(), nb * G * 4, [0] * G, [1] * G, [rg.rank] * G,
+                            self.lay["counts"])
                 rg.barrier()
         Ms = []
         for i, rg in enumerate(self.regions):
             with self.rank_stream(i):
-                Ms.append(rg.view(self.lay["counts"], (G, G), torch.int32).cpu().tolist())
-        self.M = Ms[0]
-        assert all(m == self.M for m in Ms)
-        send = [self.M[rg.rank] for rg in self.regions]
-        recv = [[self.M[s][rg.rank] for s in range(G)] for rg in self.regions]
+                Ms.append(rg.view(self.lay["counts"], (G, nb * G), torch.int32).cpu().tolist())
+        full = Ms[0]
+        assert all(m == full for m in Ms)
+        self.M = [row[:G] for row in full]  # M[s][g]: send rows s -> g (block 0)
+        send = [full[rg.rank] for rg in self.regions]
+        recv = [[full[s][j * G + rg.rank] for j in range(nb) for s in range(G)] for rg in self.regions]
         return send, recv
 
     # ---------------------------------------------------------------- block offsets (from M)
@@ -306,7 +319,10 @@ class EPRank:
         nmax = self.T * self.G
         self.ctx.update(rt=rt, plan=plan)
         gates = plan.send_gate[: nmax * self.L].view(nmax, self.L)
-        return gates, plan.send_counts  # device counts: read once, with the exchange
+        # routed (token, expert) pairs per destination rank: sizes the receiver's GIVEN routing
+        pairs = rt.f_rounded[: self.E].view(self.G, self.L).sum(1, dtype=torch.int32)
+        # device counts [send rows per rank | routed pairs per rank]: read once, with the exchange
+        return gates, torch.cat([plan.send_counts[: self.G], pairs])
 
     def pack(self, src):
         """Send rows (X forward, dO backward) into a staging buffer (the NCCL / SimComm path)."""
@@ -314,12 +330,15 @@ class EPRank:
         sonic.sonic_ep_pack(self.desc(), self.G, self.ctx["plan"], src, send)
         return send
 
-    def compute_fwd(self, recv_x, recv_gate):
+    def compute_fwd(self, recv_x, recv_gate, pairs_in=0):
+        """pairs_in: routed (token, local expert) pairs in the received rows (0 = unknown: bound by
+        R_in * L) -- sizes H and the workspaces instead of R_in * L rows."""
         R_in = recv_x.shape[0]
         self.ctx.update(R_in=R_in, recv_x=recv_x)
         if R_in == 0:
             return recv_x.new_zeros(0, self.d)
-        ld = sonic.make_desc(R_in, self.d, self.n, self.L, self.L, mode=sonic.SONIC_ROUTE_GIVEN)
+        ld = sonic.make_desc(R_in, self.d, self.n, self.L, self.L, mode=sonic.SONIC_ROUTE_GIVEN,
+                             rows_cap=max(0, int(pairs_in)))
         lrt = sonic.sonic_route(ld, recv_gate.contiguous())
         O_part, H, _ = sonic.sonic_moe_fwd(ld, recv_x, self.W1, self.W2, lrt)
         self.ctx.update(ldesc=ld, lrt=lrt, H=H)
@@ -334,7 +353,8 @@ class EPRank:
     # -------------------------------------------------------------- backward
     def _ldesc(self, extra_flags):
         ld = self.ctx["ldesc"]
-        return sonic.make_desc(ld.T, ld.d, ld.n, ld.E, ld.K, mode=ld.route_mode, flags=ld.flags | extra_flags)
+        return sonic.make_desc(ld.T, ld.d, ld.n, ld.E, ld.K, mode=ld.route_mode, flags=ld.flags | extra_flags,
+                               rows_cap=ld.rows_cap)
 
     def compute_bwd(self, recv_do):
         """Backward part 1 on the received rows: dH, dS, dX~ partial sums (the dW come later, in
@@ -402,15 +422,19 @@ def ep_forward(ranks, comm, Xs, Ss):
         with comm.rank_stream(i):
             disp.append(r.plan_fwd(S))
     # the send counts are host arguments of the exchange: the only host synchronisation of the step
-    send_counts, recv_counts = comm.exchange_counts_dev([c for _, c in disp])
+    send_both, recv_both = comm.exchange_counts_dev([c for _, c in disp])
+    G = ranks[0].G
+    send_counts = [sb[:G] for sb in send_both]
+    recv_counts = [rb[:G] for rb in recv_both]
+    pairs_in = [sum(rb[G:2 * G]) for rb in recv_both]
     for r, sc in zip(ranks, send_counts):
         r.ctx["counts"] = sc
     recv_x = _dispatch(ranks, comm, Xs, send_counts, recv_counts, "x")
     recv_g = comm.alltoallv([g for g, _ in disp], send_counts, recv_counts, tag="gate")
     parts = []
-    for i, (r, x, g) in enumerate(zip(ranks, recv_x, recv_g)):
+    for i, (r, x, g, pin) in enumerate(zip(ranks, recv_x, recv_g, pairs_in)):
         with comm.rank_stream(i):
-            parts.append(r.compute_fwd(x, g))
+            parts.append(r.compute_fwd(x, g, pin))
     back = comm.alltoallv(parts, recv_counts, send_counts, tag="y")
     outs = []
     for i, (r, rc, b) in enumerate(zip(ranks, recv_counts, back)):

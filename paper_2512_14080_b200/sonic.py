@@ -42,7 +42,7 @@ _FLOAT_FIELDS = {"topk_s", "row_gate"}
 class sonic_moe_desc(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int64), ("d", ctypes.c_int32), ("n", ctypes.c_int32), ("E", ctypes.c_int32),
                 ("K", ctypes.c_int32), ("m_tile", ctypes.c_int32), ("route_mode", ctypes.c_int32),
-                ("flags", ctypes.c_int32), ("seed", ctypes.c_uint32)]
+                ("flags", ctypes.c_int32), ("seed", ctypes.c_uint32), ("rows_cap", ctypes.c_int64)]
 
 
 class sonic_routing(ctypes.Structure):
@@ -147,8 +147,8 @@ def _done(status, what):
     LAUNCHES[0] += int(lib().sonic_last_launch_count())
 
 
-def make_desc(T, d, n, E, K, mode=SONIC_ROUTE_TC, m_tile=128, flags=0, seed=0):
-    return sonic_moe_desc(T, d, n, E, K, m_tile, mode, flags, seed)
+def make_desc(T, d, n, E, K, mode=SONIC_ROUTE_TC, m_tile=128, flags=0, seed=0, rows_cap=0):
+    return sonic_moe_desc(T, d, n, E, K, m_tile, mode, flags, seed, rows_cap)
 
 
 def _ptr(t):

@@ -91,3 +91,17 @@ def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(sonic, "_lib", None)
     with pytest.raises(sonic.SonicError):
         sonic.lib()
+
+
+def test_given_rows_cap(lib):
+    """SONIC_ROUTE_GIVEN with rows_cap: rows_max = round_128(rows_cap + E*127) (capped by the T*K
+    bound); rows_cap on another mode, or negative, is rejected."""
+    from paper_2512_14080_b200 import sonic
+    d = sonic.make_desc(1000, 64, 64, 32, 32, mode=sonic.SONIC_ROUTE_GIVEN, rows_cap=5000)
+    assert sonic.sonic_rows_max(d) == (5000 + 32 * 127 + 127) // 128 * 128
+    d0 = sonic.make_desc(1000, 64, 64, 32, 32, mode=sonic.SONIC_ROUTE_GIVEN)
+    assert sonic.sonic_rows_max(d0) == min(1000 * 32 + 32 * 127, 32 * 1024)  # E * ceil_128(T) bound
+    assert sonic.sonic_rows_max(d) < sonic.sonic_rows_max(d0)
+    assert sonic.sonic_rows_max(sonic.make_desc(1000, 64, 64, 32, 8, rows_cap=5000)) == -1
+    assert sonic.sonic_rows_max(sonic.make_desc(1000, 64, 64, 32, 32, mode=sonic.SONIC_ROUTE_GIVEN,
+                                                rows_cap=-1)) == -1

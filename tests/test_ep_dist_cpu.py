@@ -28,6 +28,9 @@ def _worker(rank, world, port, q):
         # rank r sends (r+1)*(g+1) rows to rank g (rank 1 sends none to rank 0 -> empty split)
         sc = [(rank + 1) * (g + 1) if not (rank == 1 and g == 0) else 0 for g in range(world)]
         rc = comm.exchange_counts([sc])[0]
+        # two count blocks in one exchange (send rows | routed pairs per destination)
+        rc2 = comm.exchange_counts([sc + [10 * rank + g for g in range(world)]])[0]
+        assert rc2 == rc + [10 * s + rank for s in range(world)], rc2
         rows = []
         for g in range(world):
             rows += [[rank * 1000 + g * 100 + i, -1.0] for i in range(sc[g])]
@@ -62,3 +65,12 @@ def test_distcomm_gloo_world2():
             want_vals += [float(s * 1000 + g * 100 + i) for i in range(c)]
         assert res[g][0] == want_counts
         assert res[g][1] == want_vals
+
+
+def test_simcomm_count_blocks():
+    from paper_2512_14080_b200.ep import SimComm
+    G = 3
+    send = [[100 * s + g for g in range(G)] + [1000 * s + g for g in range(G)] for s in range(G)]
+    recv = SimComm(G).exchange_counts(send)
+    for g in range(G):
+        assert recv[g] == [100 * s + g for s in range(G)] + [1000 * s + g for s in range(G)]

@@ -63,6 +63,9 @@ def test_ep_matches_oracle(G, mode, E, comm_kind):
     Os = ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins])
     outs = ep.ep_backward(ranks, comm, [i.dO for i in ins])
     torch.cuda.synchronize()
+    for rk in ranks:  # the receive side is sized by the routed pairs, not R_in * L
+        ld, lrt = rk.ctx["ldesc"], rk.ctx["lrt"]
+        assert ld.rows_cap > 0 and sonic.sonic_rows_max(ld) <= int(lrt.offsets[L]) + L * 127 + 127
     W1n, W2n = f64(W1), f64(W2)
     dW1_ref = np.zeros_like(W1n)
     dW2_ref = np.zeros_like(W2n)
