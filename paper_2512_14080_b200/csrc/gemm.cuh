@@ -187,6 +187,10 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, in
 // Pad rows (-1) read token 0: their gate is 0, so every value they produce is exactly 0.
 // tok_of loads the raw map entry; clamp() is applied only where the address is formed, so a
 // prefetched load is not consumed (and waited for) at the prefetch point.
+// DOWN / DXT epilogue: TMEM loads pipelined one chunk ahead (1) or load-wait per 32 columns (0)
+#ifndef SONIC_EPI_PIPE
+#define SONIC_EPI_PIPE 1
+#endif
 #ifndef SONIC_KPD
 #define SONIC_KPD 4
 #endif
@@ -793,6 +797,50 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           i = sq.acquire(lane);
           write_row_bf16(sq.addr(i), lane, a);
           sq.issue(lane, i, &mC1, 0, wrow);  // columns >= n are clipped by the tensor map
+        }
+      } else if constexpr ((KIND == K_DOWN || KIND == K_DXT) && SONIC_EPI_PIPE) {
+        // TMEM loads run one 64-column chunk ahead of the convert + store of the current chunk, so
+        // the tcgen05.ld latency is paid once per tile instead of twice per chunk.
+        float gate = 1.f;
+        if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
+        constexpr int NCH = BN / (64 * Cfg::EPH);
+        uint32_t r[2][2][32];
+        auto col_of = [&](int j) { return 64 * half + j * 64 * Cfg::EPH; };
+        auto live = [&](int j) { return j < NCH && tc.nt * BN + col_of(j) < args.N_dim; };
+        if (live(0)) {
+          ptx::tmem_ld32(t_acc + col_of(0), r[0][0]);
+          ptx::tmem_ld32(t_acc + col_of(0) + 32, r[0][1]);
+          ptx::tmem_ld_wait();
+          ptx::tmem_regs_ready(r[0][0]);
+          ptx::tmem_regs_ready(r[0][1]);
+        }
+#pragma unroll
+        for (int j = 0; j < NCH; ++j) {
+          if (!live(j)) break;
+          const int sl = j & 1;
+          if (live(j + 1)) {
+            ptx::tmem_ld32(t_acc + col_of(j + 1), r[sl ^ 1][0]);
+            ptx::tmem_ld32(t_acc + col_of(j + 1) + 32, r[sl ^ 1][1]);
+          }
+          const int i = sq.acquire(lane);
+          const uint32_t b = sq.addr(i);
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q8 = 0; q8 < 4; ++q8) {
+              const uint32_t* v = r[sl][h] + 8 * q8;
+              ptx::st_shared_v4(b + swz(lane, 4 * h + q8),
+                                ptx::pack_bf16(gate * __uint_as_float(v[0]), gate * __uint_as_float(v[1])),
+                                ptx::pack_bf16(gate * __uint_as_float(v[2]), gate * __uint_as_float(v[3])),
+                                ptx::pack_bf16(gate * __uint_as_float(v[4]), gate * __uint_as_float(v[5])),
+                                ptx::pack_bf16(gate * __uint_as_float(v[6]), gate * __uint_as_float(v[7])));
+            }
+          sq.issue(lane, i, &mC0, tc.nt * BN + col_of(j), wrow);
+          if (live(j + 1)) {
+            ptx::tmem_ld_wait();
+            ptx::tmem_regs_ready(r[sl ^ 1][0]);
+            ptx::tmem_regs_ready(r[sl ^ 1][1]);
+          }
         }
       } else if constexpr (KIND == K_DOWN || KIND == K_DXT) {
         float gate = 1.f;
