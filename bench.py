@@ -237,6 +237,11 @@ def main():
     from paper_2512_14080_b200 import sonic
     from paper_2512_14080_b200.inputs import make_inputs
 
+    # test-only: several ranks sharing one GPU (the single-GPU box) exercise the N > 1 code path over
+    # gloo; the exchange is then the host-staged DistComm or the peer-memory kernels, never NCCL
+    share_gpu = os.environ.get("SONIC_BENCH_SHARE_GPU") == "1"
+    if share_gpu:
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if os.environ.get("SONIC_L2_PERSIST_MB"):  # experiment: L2 set-aside for evict_last lines
         import ctypes
@@ -251,7 +256,10 @@ def main():
             print(f"[l2 persist] set {mb} MB -> status {st}, limit {got.value >> 20} MB (max {mx.value >> 20} MB)",
                   file=sys.stderr)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     T, d, n, E, K = cfg["T"], cfg["d"], cfg["n"], cfg["E"], cfg["K"]
     mode = ROUTE_MODES[args.mode][0]

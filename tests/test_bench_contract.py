@@ -42,3 +42,28 @@ def test_default_arm_line_tiny():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["act_mem_bytes"]["measured"]["held_fwd_to_bwd"] >= d["act_mem_bytes"]["X"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("comm", ["nccl", "peer"])
+def test_two_rank_bench_line(comm):
+    """The N > 1 path of bench.py (expert parallel, barriers, max-over-ranks timing, rank-0 line) with
+    two ranks sharing the one GPU over gloo (SONIC_BENCH_SHARE_GPU; "nccl" then means the
+    host-staged DistComm, "peer" the peer-memory kernels over CUDA IPC)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, SONIC_BENCH_SHARE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", "tiny", "--steps", "3", "--warmup", "3", "--e2e-steps", "2",
+                        "--comm", comm], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert BASE_KEYS <= set(d)
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "ep2"
+    assert d["scaling"] == "weak"
