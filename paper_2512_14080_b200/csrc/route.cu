@@ -12,7 +12,7 @@
 //   k_expert_popc    per-expert popcount + exclusive word prefix (histogram f_e)
 //   k_tr_decide      rounding decision: NR-f, UP, DOWN, Balance-f, SR-f
 //                    (P:2116-2198); expert choice capacity (Q22)
-//   k_transpose      S -> S^T so expert columns are contiguous (TR only)
+//   (S^T for TR, expert columns contiguous, is written by k_topk_g4 from its staged slab)
 //   k_tr_select_w    Alg. 4 step (4): per expert, keep the top f_r of the ranking
 //                    (in-TC, S, -t) via radix select on the ordered score + token tie pass
 //   k_orphans        tokens with no kept expert flag their top-1 expert (Q14 rescue)
@@ -136,23 +136,6 @@ __global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, in
       default: r = (up_m - fe) < (fe - dn) ? up : dn; break;  // strict '<': M/2 ties round down (Q11)
     }
     f_r[e] = r;
-  }
-}
-
-// ---------------------------------------------------------------- S -> S^T
-__global__ void k_transpose(const float* __restrict__ S, float* __restrict__ ST, int T, int E) {
-  ptx::pdl_trigger();
-  ptx::pdl_wait();
-  __shared__ float tile[32][33];
-  const int e0 = blockIdx.x * 32, t0 = blockIdx.y * 32;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int t = t0 + i, e = e0 + threadIdx.x;
-    tile[i][threadIdx.x] = (t < T && e < E) ? S[(size_t)t * E + e] : 0.f;
-  }
-  __syncthreads();
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int e = e0 + i, t = t0 + threadIdx.x;
-    if (e < E && t < T) ST[(size_t)e * T + t] = tile[threadIdx.x][i];
   }
 }
 
@@ -837,7 +820,8 @@ constexpr int TG_TOK = 32, TG_EC = 128, TG_STRIDE = TG_EC + 4;
 template <int KT>
 __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, int T, int E, int W,
                                                  int* __restrict__ topk_ids, float* __restrict__ topk_s,
-                                                 uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket) {
+                                                 uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket,
+                                                 float* __restrict__ ST) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
@@ -873,6 +857,11 @@ __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, in
         for (int ec = tid; ec < ecn; ec += 128) tg_sm[r * TG_STRIDE + ec] = __ldg(S + (size_t)(tok0 + r) * E + e0 + ec);
     }
     __syncthreads();
+    if (ST) {  // TR: the transposed scores S^T [E, T] for the per-expert selection, from the same slab
+      const int wp = tid >> 5, ln = tid & 31;
+      for (int ec = wp; ec < ecn; ec += 4)
+        if (ln < ntok) ST[(size_t)(e0 + ec) * T + tok0 + ln] = tg_sm[ln * TG_STRIDE + ec];
+    }
     if (tl < ntok) {
       const float* row = tg_sm + tl * TG_STRIDE;
       for (int ec = g; ec < ecn; ec += 4) {
@@ -928,7 +917,9 @@ void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
     cudaFuncSetAttribute(k_topk_g4<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = smem;
   }
-  launch_k(k_topk_g4<KT>, W, 128, smem, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
+  // token rounding / expert choice read S^T: written here from the staged slab (no separate transpose)
+  float* st_out = (L.mode == 1 || L.mode == 3) ? L.ST : nullptr;
+  launch_k(k_topk_g4<KT>, W, 128, smem, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, st_out);
 }
 
 void launch_topk(const RouteLaunch& L, cudaStream_t st) {
@@ -985,7 +976,6 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
       launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile, L.rounding, L.seed, ec_cap);
       ++nl;
     }
-    launch_k(k_transpose, dim3((E + 31) / 32, (T + 31) / 32), dim3(32, 8), 0, st, L.S, L.ST, T, E); ++nl;
     auto select_into = [&](int rescue, uint32_t* out, const int* fr_src) {
       if (W <= 1024)
         launch_k(k_tr_select_w<true>, E, 1024, 0, st, L.ST, T, W, L.m_tile, L.bm_tc, out, L.f, L.f_r, L.flip,
