@@ -192,7 +192,7 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, in
 #define SONIC_EPI_PIPE 1
 #endif
 #ifndef SONIC_KPD
-#define SONIC_KPD 4
+#define SONIC_KPD 16  // 2 -> 4 -> 8 -> 16: dW2 261 -> 255 -> 245 -> 221 us, dW1 410 -> 402 -> 389 -> 375 us (7B); 24+ spills
 #endif
 // L2 prefetch distance (k-blocks) for the gathered rows (0 = off): the producers touch the lines
 // of k-block kb + SONIC_L2PF while filling kb, so the cp.async of a later stage hits L2
@@ -401,8 +401,10 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       // Gather indices are prefetched one tile (varlen-M) / one stage (varlen-K) ahead so the
       // dependent cp.async addresses never wait on a global load.
       int ntok[8];
-      // varlen-K prefetch ring: KPD k-blocks of gather indices in flight (one k-block of MMA is
-      // ~700 clocks, an L2-resident index load ~800: distance 1 left the producers latency-bound)
+      // varlen-K prefetch ring: KPD k-blocks of gather indices in flight.  The index loads share
+      // the LSU queue with the producers' own outstanding cp.async gathers, so their effective
+      // latency is the gathers' (often HBM) latency: the deeper the ring the better until the
+      // registers run out (16: 4 indices x 16 k-blocks per thread, no spills)
       constexpr int KPD = Tr::vk ? SONIC_KPD : 1;
       constexpr int KU = Tr::vk ? KPD : 1;
       int ktok[KPD][4];
