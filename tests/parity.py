@@ -33,9 +33,16 @@ def err_stats(got, ref):
     return float(relf), float(maxrel)
 
 
+# Below this many elements the relative Frobenius error is the relative error of one or a few
+# single dot products, which cancellation can push past 1e-2 with bf16 operands however exact the
+# kernel is; there only the north star's per-element bound (|err| <= 2e-2 max|ref|) applies.
+MIN_FROB_ELEMS = 16
+
+
 def assert_close(name, got, ref, relf_tol=REL_F, max_tol=MAX_REL):
     relf, maxrel = err_stats(got, ref)
-    assert relf <= relf_tol and maxrel <= max_tol, f"{name}: relF={relf:.3e} max|err|/max|ref|={maxrel:.3e}"
+    frob_ok = relf <= relf_tol or np.asarray(ref).size < MIN_FROB_ELEMS
+    assert frob_ok and maxrel <= max_tol, f"{name}: relF={relf:.3e} max|err|/max|ref|={maxrel:.3e}"
     return relf, maxrel
 
 

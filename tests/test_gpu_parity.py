@@ -132,6 +132,9 @@ FUZZ = [
     (777, 64, 32, 7, 7, "tr"),
     (129, 192, 128, 130, 2, "ec"),
     (1500, 64, 64, 260, 8, "tc"),
+    (1, 64, 32, 1, 1, "tc"),      # a single token, a single expert
+    (1, 64, 32, 4, 2, "tr"),      # TR with T < m_tile: every chosen "up" is capped at T (Q15)
+    (2, 64, 64, 3, 3, "tr"),      # K = E with two tokens
 ]
 
 
