@@ -72,7 +72,31 @@ def kernel_model(T, d, n, E, K, R, R_pad):
         "route": dict(flops=0, paper=T * E * 4 + T * K * 8 + R * 12, tight=T * E * 4 + T * K * 8 + R * 12),
         "dS_reduce": dict(flops=0, paper=R * 8, tight=R * 8),
     }
+    # bytes written (part of the totals above): HBM writes alone run at ~3.9 TB/s on B200, well
+    # below the copy rate, so a store-heavy kernel is also bounded by write_bytes / write bandwidth
+    writes = {"up": R * 2 * n * b + R * n * b, "down": R * d * b, "agg_O": T * d * b,
+              "dH": R * 2 * n * b + R * n * b + R * 4, "dW2": E * n * d * 4, "dXt": R * d * b,
+              "dW1": E * d * 2 * n * 4, "agg_dX": T * d * b, "route": T * K * 8 + R * 12, "dS_reduce": R * 4}
+    for k, w in writes.items():
+        m[k]["write"] = w
     return m
+
+
+def measure_write_gbs(dev):
+    """HBM write-only bandwidth of this device, measured now: a 1 GiB memset, best of 5."""
+    import torch
+    buf = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    best = None
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        buf.zero_()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1)
+        best = t if best is None else min(best, t)
+    del buf
+    return (1 << 30) / (best * 1e-3) / 1e9
 
 
 # --------------------------------------------------------------------------- clocks
@@ -379,12 +403,15 @@ def main():
         a[1] += 1
     tf_peak = peaks["bf16_tflops_sustained"]
     bw_peak = peaks["hbm_gbs"]
+    peaks["hbm_write_gbs"] = wr_peak = measure_write_gbs(dev)
+    peaks["hbm_write_source"] = "measured in this run (1 GiB memset, best of 5)"
     kernels = {}
     for name, (tot, cnt) in agg.items():
         avg = tot / cnt
-        mm = model.get(name, dict(flops=0, paper=0, tight=0))
+        mm = model.get(name, dict(flops=0, paper=0, tight=0, write=0))
         t_tensor = mm["flops"] / (tf_peak * 1e12) * 1e3
-        t_hbm = mm["paper"] / (bw_peak * 1e9) * 1e3
+        # bytes bound: all bytes at the copy rate, or the written bytes alone at the write rate
+        t_hbm = max(mm["paper"] / (bw_peak * 1e9), mm.get("write", 0) / (wr_peak * 1e9)) * 1e3
         kernels[name] = dict(avg_ms=avg, launches_per_step=cnt / args.steps, share=tot / ms if ms else None,
                              tflops=mm["flops"] / (avg * 1e-3) / 1e12 if mm["flops"] else 0.0,
                              gbs_paper=mm["paper"] / (avg * 1e-3) / 1e9, gbs_tight=mm["tight"] / (avg * 1e-3) / 1e9,
@@ -513,7 +540,8 @@ def main():
         "act_mem_bytes": act,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
         "clocks": clk, "kernels": kernels, "peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops",
-                                                                                "bf16_tflops_sustained", "source")},
+                                                                                "bf16_tflops_sustained", "source",
+                                                                                "hbm_write_gbs", "hbm_write_source")},
     }
     if args.breakdown:
         json.dump(line, open(args.breakdown, "w"), indent=1)
