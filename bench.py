@@ -47,7 +47,7 @@ def load_peaks():
 
 
 # --------------------------------------------------------------------------- FLOP / byte model
-def kernel_model(T, d, n, E, K, R, R_pad):
+def kernel_model(T, d, n, E, K, R, R_pad, dw=4):
     """Algorithmic FLOPs and bytes per launch.
 
     R = routed rows (T*K under TC, sum f_r under TR).  'paper' bytes count gathered rows at
@@ -63,11 +63,11 @@ def kernel_model(T, d, n, E, K, R, R_pad):
         "agg_O": dict(flops=0, paper=R * d * b + T * d * b, tight=R * d * b + T * d * b),
         "dH": dict(flops=2 * R * n * d, paper=R * d * b + W2 + 2 * R * 2 * n * b + R * n * b + R * 4,
                    tight=T * d * b + W2 + 2 * R * 2 * n * b + R * n * b + R * 4),
-        "dW2": dict(flops=2 * R * n * d, paper=R * n * b + R * d * b + E * n * d * 4,
-                    tight=R * n * b + T * d * b + E * n * d * 4),
+        "dW2": dict(flops=2 * R * n * d, paper=R * n * b + R * d * b + E * n * d * dw,
+                    tight=R * n * b + T * d * b + E * n * d * dw),
         "dXt": dict(flops=4 * R * d * n, paper=R * 2 * n * b + W1 + R * d * b, tight=R * 2 * n * b + W1 + R * d * b),
-        "dW1": dict(flops=4 * R * d * n, paper=R * d * b + R * 2 * n * b + E * d * 2 * n * 4,
-                    tight=T * d * b + R * 2 * n * b + E * d * 2 * n * 4),
+        "dW1": dict(flops=4 * R * d * n, paper=R * d * b + R * 2 * n * b + E * d * 2 * n * dw,
+                    tight=T * d * b + R * 2 * n * b + E * d * 2 * n * dw),
         "agg_dX": dict(flops=0, paper=R * d * b + T * d * b, tight=R * d * b + T * d * b),
         "route": dict(flops=0, paper=T * E * 4 + T * K * 8 + R * 12, tight=T * E * 4 + T * K * 8 + R * 12),
         "dS_reduce": dict(flops=0, paper=R * 8, tight=R * 8),
@@ -75,8 +75,8 @@ def kernel_model(T, d, n, E, K, R, R_pad):
     # bytes written (part of the totals above): HBM writes alone run at ~3.9 TB/s on B200, well
     # below the copy rate, so a store-heavy kernel is also bounded by write_bytes / write bandwidth
     writes = {"up": R * 2 * n * b + R * n * b, "down": R * d * b, "agg_O": T * d * b,
-              "dH": R * 2 * n * b + R * n * b + R * 4, "dW2": E * n * d * 4, "dXt": R * d * b,
-              "dW1": E * d * 2 * n * 4, "agg_dX": T * d * b, "route": T * K * 8 + R * 12, "dS_reduce": R * 4}
+              "dH": R * 2 * n * b + R * n * b + R * 4, "dW2": E * n * d * dw, "dXt": R * d * b,
+              "dW1": E * d * 2 * n * dw, "agg_dX": T * d * b, "route": T * K * 8 + R * 12, "dS_reduce": R * 4}
     for k, w in writes.items():
         m[k]["write"] = w
     return m
@@ -215,6 +215,7 @@ def workload_config(args, cfg):
             "parallelism": f"ep{args.gpus}" if (args.gpus > 1 or getattr(args, "ep", False)) else "single",
             **({"ep_exchange": "peer-memory kernels (CUDA IPC)" if args.comm == "peer" else "NCCL all-to-all-v"}
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
+            **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
             "l2": "not flushed: per-step working set (X, W1, W2, H, Y, dX~, ...) is several GB >> 126 MB L2"}
 
 
@@ -236,6 +237,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", default="", help="write the per-kernel table to this JSON file")
     ap.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
+    ap.add_argument("--dw-bf16", action="store_true", help="SONIC_F_DW_BF16: weight gradients stored as bf16")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
                     help="EP exchange: NCCL all-to-all-v, or libsonic's peer-memory kernels (CUDA IPC / NVLink)")
     args = ap.parse_args()
@@ -287,7 +289,7 @@ def main():
     dev = torch.device("cuda", local)
     T, d, n, E, K = cfg["T"], cfg["d"], cfg["n"], cfg["E"], cfg["K"]
     mode = ROUTE_MODES[args.mode][0]
-    desc = sonic.make_desc(T, d, n, E, K, mode=mode)
+    desc = sonic.make_desc(T, d, n, E, K, mode=mode, flags=sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0)
     use_ep = args.ep or world > 1
     if not use_ep:
         # ---- one GPU, all experts local: route + fwd + bwd through the C ABI
@@ -302,8 +304,9 @@ def main():
         Obuf = [torch.empty(T, d, dtype=torch.bfloat16, device=dev) for _ in range(2)]
         dXbuf = [torch.empty(T, d, dtype=torch.bfloat16, device=dev) for _ in range(2)]
         H = torch.empty(rows, 2 * n, dtype=torch.bfloat16, device=dev)
-        dW1 = torch.empty(E, d, 2 * n, dtype=torch.float32, device=dev)
-        dW2 = torch.empty(E, n, d, dtype=torch.float32, device=dev)
+        wdt = torch.bfloat16 if args.dw_bf16 else torch.float32
+        dW1 = torch.empty(E, d, 2 * n, dtype=wdt, device=dev)
+        dW2 = torch.empty(E, n, d, dtype=wdt, device=dev)
         dS = torch.empty(rows, dtype=torch.float32, device=dev)
 
         def run(Xa, Sa, dOa, slot=0):
@@ -317,7 +320,7 @@ def main():
             return int(rt.offsets[E].item()), int(rt.pad_offsets[E].item())
 
         def local_model(R, R_pad):
-            return kernel_model(T, d, n, E, K, R, R_pad)
+            return kernel_model(T, d, n, E, K, R, R_pad, dw=2 if args.dw_bf16 else 4)
     else:
         # ---- expert parallelism over the `world` GPUs (NCCL all-to-all), weak scaling: every rank
         #      brings its own T tokens and owns E/world experts (paper_2512_14080_b200/ep.py)

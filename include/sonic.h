@@ -81,6 +81,9 @@ typedef enum {
 #define SONIC_F_BWD_DW_ONLY     16  /* sonic_moe_bwd part 2: dW2, dW1 from the dH / A' a preceding
                                        SONIC_F_BWD_NO_DW call left in the same ws (dX/dS may be NULL).
                                        Lets a caller overlap the dX exchange with the weight gradients. */
+#define SONIC_F_DW_BF16         32  /* sonic_moe_bwd: dW1 / dW2 are written as bf16 (the float* arguments point
+                                       at bf16 [E,d,2n] / [E,n,d] buffers): half the weight-gradient store
+                                       traffic; fp32 accumulation as always.  Not with SONIC_F_DW_ACCUMULATE. */
 #define SONIC_F_DW_ACCUMULATE    4  /* sonic_moe_bwd: dW1 += ..., dW2 += ... (fp32 element-wise adds done by
                                        the TMA store unit; one add per element per call, so deterministic)
                                        instead of overwriting -- gradient accumulation over microbatches */

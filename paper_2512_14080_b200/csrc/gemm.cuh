@@ -59,6 +59,7 @@ struct GemmArgs {
   long long rows_max;
   unsigned long long* dbg;  // SONIC_TIMING builds only: cycle counters (see sonic_api.cu)
   int accumulate;           // DW1 / DW2: add into the existing dW (SONIC_F_DW_ACCUMULATE) instead of overwriting
+  int dw_bf16;              // DW1 / DW2: store dW as bf16 (SONIC_F_DW_BF16; the store map is then bf16)
 };
 
 template <int KIND>
@@ -1101,7 +1102,35 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       } else {  // K_DW2 / K_DW1: fp32 weight gradient tile [128 x BN] of expert e
         const int m0 = tc.mt * GEMM_BM + 32 * q;
         // accumulate (dW += tile, TMA reduce-add): an expert with no rows adds nothing
-        if (m0 < args.M_dim && !(args.accumulate && tc.nkb == 0)) {
+        if (args.dw_bf16 && m0 < args.M_dim) {  // bf16 dW: 64 columns (128 B) per staging buffer
+#pragma unroll 1
+          for (int c = 64 * half; c < BN; c += 64 * Cfg::EPH) {
+            if (tc.nt * BN + c >= args.N_dim) break;
+            const int i = sq.acquire(lane);
+            const uint32_t b = sq.addr(i);
+            if (tc.nkb > 0) {
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                uint32_t r[32];
+                ptx::tmem_ld32(t_acc + c + 32 * h, r);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int q8 = 0; q8 < 4; ++q8) {
+                  const uint32_t* v = r + 8 * q8;
+                  ptx::st_shared_v4(b + swz(lane, 4 * h + q8),
+                                    ptx::pack_bf16(__uint_as_float(v[0]), __uint_as_float(v[1])),
+                                    ptx::pack_bf16(__uint_as_float(v[2]), __uint_as_float(v[3])),
+                                    ptx::pack_bf16(__uint_as_float(v[4]), __uint_as_float(v[5])),
+                                    ptx::pack_bf16(__uint_as_float(v[6]), __uint_as_float(v[7])));
+                }
+              }
+            } else {
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch) ptx::st_shared_v4(b + swz(lane, ch), 0u, 0u, 0u, 0u);
+            }
+            sq.issue3d(lane, i, &mC0, tc.nt * BN + c, m0, tc.e, false);
+          }
+        } else if (m0 < args.M_dim && !(args.accumulate && tc.nkb == 0)) {
 #pragma unroll 1
           for (int c = 32 * half; c < BN; c += 32 * Cfg::EPH) {
             if (tc.nt * BN + c >= args.N_dim) break;

@@ -541,6 +541,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   if (!valid_desc(D)) return SONIC_ERR_INVALID_ARG;
   const bool no_dw = D->flags & SONIC_F_BWD_NO_DW, dw_only = D->flags & SONIC_F_BWD_DW_ONLY;
   if (no_dw && dw_only) return SONIC_ERR_INVALID_ARG;
+  if ((D->flags & SONIC_F_DW_BF16) && (D->flags & SONIC_F_DW_ACCUMULATE)) return SONIC_ERR_INVALID_ARG;
   if (!dO || !X || !H || !W1 || !W2 || !rt || (!dw_only && (!dX || !dS)) || (!no_dw && (!dW1 || !dW2)))
     return SONIC_ERR_INVALID_ARG;
   if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
@@ -612,20 +613,23 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     return SONIC_ERR_CUDA;
   a6.n_tiles = d / BN6; a6.k_blocks = (2 * n) / 64; a6.N_dim = d;
   // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
+  const bool dw_bf16 = (D->flags & SONIC_F_DW_BF16) != 0;
   if (!map2d(&mA5, Ap, false, R, n, 64, 64) || !map2d(&mB5, dO, false, s.T, d, 64, 1) ||
-      !map3d(&mC5, dW2, true, E, n, d, 32, 32))
+      !map3d(&mC5, dW2, !dw_bf16, E, n, d, dw_bf16 ? 64 : 32, 32))
     return SONIC_ERR_CUDA;
   a5.n_tiles = d / BN5; a5.m_tiles = (n + 127) / 128; a5.M_dim = n; a5.N_dim = d;
   a5.gsrc = static_cast<const __nv_bfloat16*>(dO); a5.gld = d;
   a5.accumulate = (D->flags & SONIC_F_DW_ACCUMULATE) ? 1 : 0;
+  a5.dw_bf16 = dw_bf16 ? 1 : 0;
   const int tiles5 = E * a5.m_tiles * a5.n_tiles;
   // K7 dW1_e = Gather(X)^T dH_e   (varlen-K)
   if (!map2d(&mA7, X, false, s.T, d, 64, 1) || !map2d(&mB7, dH, false, R, 2 * n, 64, 64) ||
-      !map3d(&mC7, dW1, true, E, d, 2 * n, 32, 32))
+      !map3d(&mC7, dW1, !dw_bf16, E, d, 2 * n, dw_bf16 ? 64 : 32, 32))
     return SONIC_ERR_CUDA;
   a7.n_tiles = (2 * n) / BN7; a7.m_tiles = (d + 127) / 128; a7.M_dim = d; a7.N_dim = 2 * n;
   a7.gsrc = static_cast<const __nv_bfloat16*>(X); a7.gld = d;
   a7.accumulate = (D->flags & SONIC_F_DW_ACCUMULATE) ? 1 : 0;
+  a7.dw_bf16 = dw_bf16 ? 1 : 0;
   const int tiles7 = E * a7.m_tiles * a7.n_tiles;
 
   auto run_dxt = [&]() {

@@ -32,6 +32,7 @@ SONIC_F_NO_ORPHAN_RESCUE = 2
 SONIC_F_DW_ACCUMULATE = 4
 SONIC_F_BWD_NO_DW = 8
 SONIC_F_BWD_DW_ONLY = 16
+SONIC_F_DW_BF16 = 32
 GEMM_M = 128
 
 ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",
@@ -257,17 +258,19 @@ def sonic_moe_fwd(desc, X, W1, W2, rt, O=None, H=None, ws=None):
 
 
 def sonic_moe_bwd(desc, dO, X, H, W1, W2, rt, dX=None, dW1=None, dW2=None, dS=None, ws=None):
-    """sonic_moe_bwd -> (dX [T,d] bf16, dW1 [E,d,2n] f32, dW2 [E,n,d] f32, dS [rows_max] f32, ws)."""
+    """sonic_moe_bwd -> (dX [T,d] bf16, dW1 [E,d,2n], dW2 [E,n,d] (f32, or bf16 with SONIC_F_DW_BF16),
+    dS [rows_max] f32, ws)."""
     rows = sonic_rows_max(desc)
     dev = X.device
     want_dx = not (desc.flags & SONIC_F_BWD_DW_ONLY)
     want_dw = not (desc.flags & SONIC_F_BWD_NO_DW)
     if dX is None and want_dx:
         dX = torch.empty(desc.T, desc.d, dtype=torch.bfloat16, device=dev)
+    wdt = torch.bfloat16 if desc.flags & SONIC_F_DW_BF16 else torch.float32
     if dW1 is None and want_dw:
-        dW1 = torch.empty(desc.E, desc.d, 2 * desc.n, dtype=torch.float32, device=dev)
+        dW1 = torch.empty(desc.E, desc.d, 2 * desc.n, dtype=wdt, device=dev)
     if dW2 is None and want_dw:
-        dW2 = torch.empty(desc.E, desc.n, desc.d, dtype=torch.float32, device=dev)
+        dW2 = torch.empty(desc.E, desc.n, desc.d, dtype=wdt, device=dev)
     if dS is None and want_dx:
         dS = torch.empty(rows, dtype=torch.float32, device=dev)
     if ws is None:

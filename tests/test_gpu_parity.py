@@ -120,6 +120,28 @@ def test_dw_accumulate():
     assert len(empty) > 0 and torch.equal(acc1[empty], init1[empty])
 
 
+@pytest.mark.parametrize("shape", [(64, 128, 64, 64, 2), (2048, 256, 128, 16, 4), (1000, 192, 384, 8, 2)],
+                         ids=["empty_experts", "multi", "wide_n"])
+def test_dw_bf16(shape):
+    """SONIC_F_DW_BF16: dW1 / dW2 stored as bf16 are the fp32 results rounded to nearest even, bit for bit
+    (same fp32 accumulation; experts with no rows get zeros); with DW_ACCUMULATE the call is rejected."""
+    T, d, n, E, K = shape
+    inp = make_inputs(T, d, n, E, K, seed=17, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K)
+    rt = sonic.sonic_route(desc, inp.S)
+    O, H, _ = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
+    _, dW1, dW2, _, _ = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+    db = sonic.make_desc(T, d, n, E, K, flags=sonic.SONIC_F_DW_BF16)
+    rtb = sonic.sonic_route(db, inp.S)
+    _, b1, b2, _, _ = sonic.sonic_moe_bwd(db, inp.dO, inp.X, H, inp.W1, inp.W2, rtb)
+    torch.cuda.synchronize()
+    assert b1.dtype == torch.bfloat16 and b2.dtype == torch.bfloat16
+    assert torch.equal(b1, dW1.to(torch.bfloat16)) and torch.equal(b2, dW2.to(torch.bfloat16))
+    bad = sonic.make_desc(T, d, n, E, K, flags=sonic.SONIC_F_DW_BF16 | sonic.SONIC_F_DW_ACCUMULATE)
+    with pytest.raises(sonic.SonicError):
+        sonic.sonic_moe_bwd(bad, inp.dO, inp.X, H, inp.W1, inp.W2, rtb)
+
+
 # Shape sweep over the edge cases of the routing and GEMM paths: E not a multiple of 4 or 32
 # (scalar S staging, partial expert chunks), E > 128 (several S slabs), K = 1, tiny / ragged T,
 # n = 32 and 64, d = 64.
