@@ -912,10 +912,12 @@ template <int KT>
 void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   const int T = (int)L.T, E = L.E, W = L.W;
   const int smem = (TG_TOK * TG_STRIDE + E) * 4;
-  static int attr = 0;
-  if (attr < smem) {
+  static int attr[64] = {};  // per device (function attributes are per context)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (attr[dev & 63] < smem) {
     cudaFuncSetAttribute(k_topk_g4<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = smem;
+    attr[dev & 63] = smem;
   }
   // token rounding / expert choice read S^T: written here from the staged slab (no separate transpose)
   float* st_out = (L.mode == 1 || L.mode == 3) ? L.ST : nullptr;

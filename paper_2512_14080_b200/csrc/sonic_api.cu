@@ -128,10 +128,11 @@ SideStream& side_stream() {
 }
 
 int num_sms() {
-  static int n = 0;
+  static int per_dev[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = per_dev[dev & 63];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
   }
@@ -144,11 +145,13 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
                    const CUtensorMap& dmap, const GemmArgs& args, int grid, cudaStream_t st) {
   using Cfg = KCfg<KIND, BN, CTA2>;
   auto kern = sonic_gemm_kernel<KIND, BN, CTA2>;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[64] = {};  // function attributes are per device (context)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
       return false;
-    attr = true;
+    attr[dev & 63] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
