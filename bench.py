@@ -438,6 +438,22 @@ def main():
                     "frac": k["gbs_paper"] / bw_peak, "traffic": traffic,
                     "algorithmic_per_launch": model[dom]["paper"], "peak_source": peaks["source"] + " hbm_gbs"}
     layer_roof_ms = sum(kernels[k]["roofline_ms"] * kernels[k]["launches_per_step"] for k in kernels)
+    exchange = None
+    if use_ep:
+        # NVLink bytes this rank moves per step (rows to / from the OTHER ranks): forward X rows +
+        # gates out, Y partial sums back; backward dO rows out, dX~ partial sums + dS back
+        G_ = world
+        sc, rc = rk.ctx["counts"], rk.ctx["recv_counts"]
+        s_off = sum(c for g, c in enumerate(sc) if g != rank)
+        r_off = sum(c for g, c in enumerate(rc) if g != rank)
+        L_ = E // G_
+        out_b = s_off * (2 * d * 2 + L_ * 4) + r_off * (2 * d * 2 + L_ * 4)
+        in_b = r_off * (2 * d * 2 + L_ * 4) + s_off * (2 * d * 2 + L_ * 4)
+        nvl_gbs = 900.0  # NVLink 5 per direction per GPU (nominal)
+        nvl_ms = max(out_b, in_b) / (nvl_gbs * 1e9) * 1e3
+        exchange = {"bytes_out_per_step": out_b, "bytes_in_per_step": in_b, "nvlink_gbs_nominal": nvl_gbs,
+                    "nvlink_roofline_ms": nvl_ms,
+                    "layer_roofline_ms_with_exchange": layer_roof_ms + nvl_ms}
 
     # ---- end to end through the public API with host buffers
     e2e = None
@@ -542,7 +558,7 @@ def main():
                                           * 1e-3) / 1e12) if "route" in kernels else None,
         "act_mem_bytes": act,
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
-        "clocks": clk, "kernels": kernels, "peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops",
+        "clocks": clk, "kernels": kernels, "exchange": exchange, "peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops",
                                                                                 "bf16_tflops_sustained", "source",
                                                                                 "hbm_write_gbs", "hbm_write_source")},
     }
