@@ -24,7 +24,7 @@
  *  - Supported shapes: 1 <= K <= min(E, 16), E <= 4096 (the paper's top-K range,
  *    P:1076), d % 64 == 0, n == 32 or n % 64 == 0, m_tile == 128 (the GEMM M
  *    tile, P:1238 footnote "M_tile is GPU-dependent", Q16),
- *    T*K + E*127 < 2^31.  All pointers 16-byte aligned.
+ *    rows_max (sonic_rows_max) < 2^31.  All pointers 16-byte aligned.
  *
  * Grouped-row layout.  Expert e owns the grouped rows
  * [pad_offsets[e], pad_offsets[e+1]); the first f_rounded[e] of them hold e's
@@ -175,7 +175,13 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc *desc, const void *X, const void
  *   dO [T,d] bf16; X, H_cache, W1, W2, rt as in the forward.
  *   dX  [T,d] bf16 output.
  *   dW1 [E,d,2n] fp32, dW2 [E,n,d] fp32 outputs, overwritten (experts with no rows get 0), or
- *       accumulated into with SONIC_F_DW_ACCUMULATE (experts with no rows unchanged).
+ *       accumulated into with SONIC_F_DW_ACCUMULATE (experts with no rows unchanged), or bf16
+ *       buffers of the same shapes with SONIC_F_DW_BF16 (the fp32 result rounded to nearest even).
+ *   Split form: SONIC_F_BWD_NO_DW computes dH, dS, dX only (dW1/dW2 may be NULL) and leaves dH, A'
+ *       in ws; a following SONIC_F_BWD_DW_ONLY call with the same ws computes dW2, dW1 (dX/dS may
+ *       be NULL) -- the expert-parallel path overlaps its dX~ exchange with the second call.
+ *   Streams: the dX aggregation may run on an internal side stream forked from and joined back
+ *       into `stream` before return (SONIC_BWD_OVERLAP); callers see ordinary stream semantics.
  *   dS  [rows_max] fp32 output: dL/dg for each grouped row (0 on pad rows).  The router
  *       backward (renormalisation/softmax Jacobian) is outside the boundary.
  */
