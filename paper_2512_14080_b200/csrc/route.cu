@@ -817,8 +817,13 @@ __global__ void k_rows_tc(const uint32_t* __restrict__ bm, const int* __restrict
 // banks) with one stable insertion list, then two shuffle rounds of bitonic merges on the unique
 // 64-bit keys give every thread of the token its top-KT.
 constexpr int TG_TOK = 32, TG_EC = 128, TG_STRIDE = TG_EC + 4;
+// threads per token of the top-K (4 or 8): each scans every TPT-th expert into its own sorted list,
+// then log2(TPT) shuffle rounds of bitonic merges
+#ifndef SONIC_TOPK_TPT
+#define SONIC_TOPK_TPT 4
+#endif
 template <int KT>
-__global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, int T, int E, int W,
+__global__ void __launch_bounds__(32 * SONIC_TOPK_TPT) k_topk_g4(const float* __restrict__ S, int T, int E, int W,
                                                  int* __restrict__ topk_ids, float* __restrict__ topk_s,
                                                  uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket,
                                                  float* __restrict__ ST) {
@@ -827,14 +832,15 @@ __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, in
   constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
   extern __shared__ float tg_sm[];  // [TG_TOK][TG_STRIDE] staging, then words [E]
   uint32_t* words = reinterpret_cast<uint32_t*>(tg_sm + TG_TOK * TG_STRIDE);
-  const int tid = threadIdx.x, tl = tid >> 2, g = tid & 3;
+  constexpr int TPT = SONIC_TOPK_TPT, NT = 32 * TPT;  // threads per token, per block
+  const int tid = threadIdx.x, tl = tid / TPT, g = tid % TPT;
   const int tok0 = blockIdx.x * TG_TOK;
   const int ntok = min(TG_TOK, T - tok0);
   if (blockIdx.x == 0 && tid == 0 && ticket) {
     ticket[0] = 0u;
     ticket[1] = 0u;
   }
-  for (int i = tid; i < E; i += 128) words[i] = 0u;
+  for (int i = tid; i < E; i += NT) words[i] = 0u;
   uint32_t top[KP];
   int id[KP];
 #pragma unroll
@@ -847,24 +853,24 @@ __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, in
     __syncthreads();
     if (ecn == TG_EC && (E & 3) == 0) {
 #pragma unroll 4
-      for (int i = tid; i < ntok * (TG_EC / 4); i += 128) {
+      for (int i = tid; i < ntok * (TG_EC / 4); i += NT) {
         const int r = i / (TG_EC / 4), c4 = i % (TG_EC / 4);
         const float4 v = __ldg(reinterpret_cast<const float4*>(S + (size_t)(tok0 + r) * E + e0) + c4);
         *reinterpret_cast<float4*>(tg_sm + r * TG_STRIDE + 4 * c4) = v;
       }
     } else {
       for (int r = 0; r < ntok; ++r)
-        for (int ec = tid; ec < ecn; ec += 128) tg_sm[r * TG_STRIDE + ec] = __ldg(S + (size_t)(tok0 + r) * E + e0 + ec);
+        for (int ec = tid; ec < ecn; ec += NT) tg_sm[r * TG_STRIDE + ec] = __ldg(S + (size_t)(tok0 + r) * E + e0 + ec);
     }
     __syncthreads();
     if (ST) {  // TR: the transposed scores S^T [E, T] for the per-expert selection, from the same slab
       const int wp = tid >> 5, ln = tid & 31;
-      for (int ec = wp; ec < ecn; ec += 4)
+      for (int ec = wp; ec < ecn; ec += NT / 32)
         if (ln < ntok) ST[(size_t)(e0 + ec) * T + tok0 + ln] = tg_sm[ln * TG_STRIDE + ec];
     }
     if (tl < ntok) {
       const float* row = tg_sm + tl * TG_STRIDE;
-      for (int ec = g; ec < ecn; ec += 4) {
+      for (int ec = g; ec < ecn; ec += TPT) {
         const uint32_t v = ord_f32(row[ec]);
         if (v > top[KP - 1]) {
           const int e = e0 + ec;
@@ -887,7 +893,7 @@ __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, in
   for (int i = 0; i < KP; ++i)
     key[i] = top[i] ? ((unsigned long long)top[i] << 32) | (0xFFFFFFFFu - (uint32_t)id[i]) : 0ull;
 #pragma unroll
-  for (int m = 1; m <= 2; m <<= 1) {
+  for (int m = 1; m < TPT; m <<= 1) {
     unsigned long long other[KP];
 #pragma unroll
     for (int i = 0; i < KP; ++i) other[i] = __shfl_xor_sync(0xffffffffu, key[i], m);
@@ -897,7 +903,7 @@ __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, in
     const size_t t = (size_t)(tok0 + tl);
 #pragma unroll
     for (int i = 0; i < KT; ++i) {
-      if ((i & 3) != g) continue;  // the token's 4 threads share the writes
+      if (i % TPT != g) continue;  // the token's TPT threads share the writes
       const int e = (int)(0xFFFFFFFFu - (uint32_t)(key[i] & 0xFFFFFFFFull));
       topk_ids[t * KT + i] = e;
       topk_s[t * KT + i] = unord_f32((uint32_t)(key[i] >> 32));
@@ -905,7 +911,7 @@ __global__ void __launch_bounds__(128) k_topk_g4(const float* __restrict__ S, in
     }
   }
   __syncthreads();
-  for (int e = tid; e < E; e += 128) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
+  for (int e = tid; e < E; e += NT) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
 }
 
 template <int KT>
@@ -921,7 +927,8 @@ void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   }
   // token rounding / expert choice read S^T: written here from the staged slab (no separate transpose)
   float* st_out = (L.mode == 1 || L.mode == 3) ? L.ST : nullptr;
-  launch_k(k_topk_g4<KT>, W, 128, smem, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, st_out);
+  launch_k(k_topk_g4<KT>, W, 32 * SONIC_TOPK_TPT, smem, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket,
+           st_out);
 }
 
 void launch_topk(const RouteLaunch& L, cudaStream_t st) {
