@@ -157,7 +157,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- CPU oracle leg
-def oracle_sample(cfg, mode, seed, T_sample):
+def oracle_sample(cfg, mode, seed, T_sample, m_tile=128):
     """The fp64 oracle as it stands on a bounded sample: the first T_sample tokens of the
     workload (route + fwd + bwd).  Returns (model FLOPs processed, seconds, threads)."""
     import numpy as np
@@ -171,7 +171,7 @@ def oracle_sample(cfg, mode, seed, T_sample):
     X, W1, W2, dO, S = f64(inp.X), f64(inp.W1), f64(inp.W2), f64(inp.dO), inp.S.numpy()
     t0 = time.perf_counter()
     _, omode, rounding = ROUTE_MODES[mode]
-    rt = om.route(S, c["K"], mode=omode, m_tile=128, rounding=rounding)
+    rt = om.route(S, c["K"], mode=omode, m_tile=m_tile, rounding=rounding)
     om.forward(X, W1, W2, rt)
     om.backward(dO, X, W1, W2, rt)
     dt = time.perf_counter() - t0
@@ -189,10 +189,10 @@ def run_reference(args, cfg, rank, world):
         return
     T_s = args.ref_tokens
     for _ in range(args.warmup):
-        oracle_sample(cfg, args.mode, 0, T_s)
+        oracle_sample(cfg, args.mode, 0, T_s, args.m_tile)
     tot_f, tot_t, thr = 0, 0.0, 1
     for i in range(args.steps):
-        f, t, thr = oracle_sample(cfg, args.mode, i, T_s)
+        f, t, thr = oracle_sample(cfg, args.mode, i, T_s, args.m_tile)
         tot_f += f
         tot_t += t
     v = tot_f / tot_t / 1e12
@@ -216,6 +216,7 @@ def workload_config(args, cfg):
             **({"ep_exchange": "peer-memory kernels (CUDA IPC)" if args.comm == "peer" else "NCCL all-to-all-v"}
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
+            **({"m_tile": args.m_tile} if getattr(args, "m_tile", 128) != 128 else {}),
             "l2": "not flushed: per-step working set (X, W1, W2, H, Y, dX~, ...) is several GB >> 126 MB L2"}
 
 
@@ -237,6 +238,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--breakdown", default="", help="write the per-kernel table to this JSON file")
     ap.add_argument("--ep", action="store_true", help="expert-parallel path even at N=1 (always on for N>1)")
+    ap.add_argument("--m-tile", type=int, default=128, choices=[128, 256],
+                    help="token-rounding tile (256 = the 2-CTA pair's M tile: no half-empty pairs)")
     ap.add_argument("--dw-bf16", action="store_true", help="SONIC_F_DW_BF16: weight gradients stored as bf16")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
                     help="EP exchange: NCCL all-to-all-v, or libsonic's peer-memory kernels (CUDA IPC / NVLink)")
@@ -289,7 +292,8 @@ def main():
     dev = torch.device("cuda", local)
     T, d, n, E, K = cfg["T"], cfg["d"], cfg["n"], cfg["E"], cfg["K"]
     mode = ROUTE_MODES[args.mode][0]
-    desc = sonic.make_desc(T, d, n, E, K, mode=mode, flags=sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0)
+    desc = sonic.make_desc(T, d, n, E, K, mode=mode, m_tile=args.m_tile,
+                           flags=sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0)
     use_ep = args.ep or world > 1
     if not use_ep:
         # ---- one GPU, all experts local: route + fwd + bwd through the C ABI
@@ -533,7 +537,7 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        f, t, thr = oracle_sample(cfg, args.mode, args.seed, args.cpu_tokens)
+        f, t, thr = oracle_sample(cfg, args.mode, args.seed, args.cpu_tokens, args.m_tile)
         cpu = {"value": f / t / 1e12, "unit": "TFLOPS", "cores": thr, "kind": "oracle",
                "sample": f"first {args.cpu_tokens} of {T} tokens (route+fwd+bwd in fp64 numpy), {t:.1f} s"}
 

@@ -22,8 +22,8 @@
  *    index checks do not exist in release builds.  No C++ exception crosses
  *    the ABI.
  *  - Supported shapes: 1 <= K <= min(E, 16), E <= 4096 (the paper's top-K range,
- *    P:1076), d % 64 == 0, n == 32 or n % 64 == 0, m_tile == 128 (the GEMM M
- *    tile, P:1238 footnote "M_tile is GPU-dependent", Q16),
+ *    P:1076), d % 64 == 0, n == 32 or n % 64 == 0, m_tile 128 or 256 (the GEMM M
+ *    tile of one CTA or of a 2-CTA pair, P:1238 footnote "M_tile is GPU-dependent", Q16),
  *    rows_max (sonic_rows_max) < 2^31.  All pointers 16-byte aligned.
  *
  * Grouped-row layout.  Expert e owns the grouped rows
@@ -92,7 +92,9 @@ typedef struct {
   int64_t T;           /* tokens in the microbatch */
   int32_t d, n;        /* embedding dim, expert intermediate dim (H has 2n columns: [gate | up], Q1) */
   int32_t E, K;        /* experts, experts per token */
-  int32_t m_tile;      /* TR rounding tile; must be 128 (the GEMM M tile) */
+  int32_t m_tile;      /* TR / EC rounding tile: 128 (one CTA's M tile) or 256 (a 2-CTA pair's M tile,
+                          Q16): with 256 every expert gets an even number of 128-row tiles, so no
+                          pair is half empty (the grouped-row layout stays in 128-row tiles) */
   int32_t route_mode;  /* sonic_route_mode */
   int32_t flags;       /* SONIC_F_* */
   uint32_t seed;       /* SONIC_ROUTE_TR_SR: seed of the rounding draws (ignored otherwise) */
@@ -125,7 +127,7 @@ typedef struct {
 
 #define SONIC_ROUTING_NFIELDS 14
 
-/* Upper bound on grouped rows (incl. pad rows): min(T*K + E*127, E*ceil(T/128)*128),
+/* Upper bound on grouped rows (incl. pad rows): min(T*K + E*(max(m_tile,128)-1), E*ceil(T/128)*128),
  * rounded up to a multiple of 128.  Returns -1 on an invalid descriptor. */
 int64_t sonic_rows_max(const sonic_moe_desc *desc);
 

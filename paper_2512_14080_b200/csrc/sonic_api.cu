@@ -230,7 +230,7 @@ bool valid_desc(const sonic_moe_desc* D) {
   if (D->T < 1 || D->d < 1 || D->n < 1 || D->E < 1 || D->K < 1) return false;
   if (D->K > D->E || D->E > 4096) return false;
   if (D->K > 16 && D->route_mode != SONIC_ROUTE_GIVEN) return false;
-  if (D->m_tile != 128) return false;
+  if (D->m_tile != 128 && D->m_tile != 256) return false;  // one CTA's M tile or a 2-CTA pair's (Q16)
   if (D->route_mode < SONIC_ROUTE_TC || D->route_mode > SONIC_ROUTE_TR_NRS) return false;
   if (D->rows_cap < 0 || (D->rows_cap != 0 && D->route_mode != SONIC_ROUTE_GIVEN)) return false;
   return true;
@@ -246,7 +246,8 @@ bool supported_dims(const sonic_moe_desc* D) {
 long long rows_max_of(const sonic_moe_desc* D) {
   const long long pairs = (D->route_mode == SONIC_ROUTE_GIVEN && D->rows_cap > 0) ? std::min(D->rows_cap, D->T * D->K)
                                                                                    : D->T * D->K;
-  const long long a = pairs + (long long)D->E * (GEMM_M - 1);
+  // token rounding moves an expert's count by less than one rounding tile; TC pads to 128-row tiles
+  const long long a = pairs + (long long)D->E * (std::max(D->m_tile, GEMM_M) - 1);
   const long long b = (long long)D->E * ((D->T + GEMM_M - 1) / GEMM_M) * GEMM_M;
   const long long r = std::min(a, b);
   return (r + GEMM_M - 1) / GEMM_M * GEMM_M;

@@ -93,6 +93,14 @@ def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
         sonic.lib()
 
 
+def test_m_tile_256_rows_bound(lib):
+    """m_tile 256 is accepted and widens the rows bound to E*255 of rounding slack; 64 is rejected."""
+    from paper_2512_14080_b200 import sonic
+    d = sonic.make_desc(32768, 1536, 256, 128, 8, mode=sonic.SONIC_ROUTE_TR_NRF, m_tile=256)
+    assert sonic.sonic_rows_max(d) == (32768 * 8 + 128 * 255 + 127) // 128 * 128
+    assert sonic.sonic_rows_max(sonic.make_desc(256, 64, 32, 8, 2, m_tile=64)) == -1
+
+
 def test_given_rows_cap(lib):
     """SONIC_ROUTE_GIVEN with rows_cap: rows_max = round_128(rows_cap + E*127) (capped by the T*K
     bound); rows_cap on another mode, or negative, is rejected."""

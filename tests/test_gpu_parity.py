@@ -120,6 +120,32 @@ def test_dw_accumulate():
     assert len(empty) > 0 and torch.equal(acc1[empty], init1[empty])
 
 
+M256 = [
+    # (T, d, n, E, K, mode, rounding): token rounding / expert choice to 256-row multiples (Q16)
+    (4096, 128, 64, 16, 4, "tr", "nrf"),
+    (3000, 128, 64, 16, 4, "tr", "nrf"),     # T not a multiple of 256: capped ups (Q15)
+    (4096, 128, 64, 16, 4, "tr", "up"),
+    (4096, 128, 64, 16, 4, "tr", "down"),
+    (4096, 128, 64, 16, 4, "tr", "balance"),
+    (4096, 128, 64, 16, 4, "ec", "nrf"),
+]
+_M256_MODE = {("tr", "nrf"): sonic.SONIC_ROUTE_TR_NRF, ("tr", "up"): 3, ("tr", "down"): 4, ("tr", "balance"): 5,
+              ("ec", "nrf"): 7}
+
+
+@pytest.mark.parametrize("case", M256, ids=[f"T{c[0]}_{c[5]}_{c[6]}" for c in M256])
+def test_m_tile_256(case):
+    """m_tile = 256 (a 2-CTA pair's M tile): routing bit-exact vs the oracle at M = 256, every
+    kept count a multiple of 256 (or capped at T), values within tolerance."""
+    T, d, n, E, K, mode, rounding = case
+    inp = make_inputs(T, d, n, E, K, seed=23, device="cuda")
+    desc = sonic.make_desc(T, d, n, E, K, mode=_M256_MODE[(mode, rounding)], m_tile=256)
+    full_parity(desc, inp, mode=mode, rounding=rounding)
+    rt = sonic.sonic_route(desc, inp.S)
+    fr = rt.f_rounded[:E].cpu()
+    assert bool(((fr % 256 == 0) | (fr == T)).all())
+
+
 @pytest.mark.parametrize("shape", [(64, 128, 64, 64, 2), (2048, 256, 128, 16, 4), (1000, 192, 384, 8, 2)],
                          ids=["empty_experts", "multi", "wide_n"])
 def test_dw_bf16(shape):
