@@ -55,6 +55,8 @@ __global__ void k_ep_offsets(const int* __restrict__ cnt, int G, int* __restrict
 }
 
 // Send-row positions, the token CSR over send rows, the row -> token map and the gates.
+// One warp per token: the send rows of the token (ascending rank) get their positions, the token id
+// and zeroed gate rows (lanes over the L gates), then lanes over the token's routed rows write its gates.
 __global__ void k_ep_fill(const int* __restrict__ rowptr, const int* __restrict__ rows,
                           const int* __restrict__ tile_expert, const float* __restrict__ row_gate, int T, int L, int W,
                           const int* __restrict__ dmask, const uint32_t* __restrict__ bm,
@@ -63,29 +65,33 @@ __global__ void k_ep_fill(const int* __restrict__ rowptr, const int* __restrict_
                           float* __restrict__ send_gate) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
   if (t >= T) return;
   const uint32_t mask = (uint32_t)dmask[t];
   const int w = t >> 5;
   const uint32_t below = (1u << (t & 31)) - 1u;
-  int j = ep_rowptr[t];
-  for (uint32_t m = mask; m; m &= m - 1) {
+  const int j0 = ep_rowptr[t];
+  int j = j0;
+  for (uint32_t m = mask; m; m &= m - 1, ++j) {  // warp-uniform
     const int g = __ffs(m) - 1;
     const int pos = off[g] + wprefix[(size_t)g * W + w] + __popc(bm[(size_t)g * W + w] & below);
-    ep_rows[j++] = pos;
-    send_token[pos] = t;
-    for (int i = 0; i < L; ++i) send_gate[(size_t)pos * L + i] = 0.f;
+    if (lane == 0) {
+      ep_rows[j] = pos;
+      send_token[pos] = t;
+    }
+    for (int i = lane; i < L; i += 32) send_gate[(size_t)pos * L + i] = 0.f;
   }
-  for (int k = rowptr[t]; k < rowptr[t + 1]; ++k) {
+  __syncwarp();
+  for (int k = rowptr[t] + lane; k < rowptr[t + 1]; k += 32) {
     const int r = rows[k];
     const int e = tile_expert[r / GEMM_M];
     const int g = e / L;
-    const int pos = ep_rows[ep_rowptr[t] + __popc(mask & ((1u << g) - 1u))];
+    const int pos = ep_rows[j0 + __popc(mask & ((1u << g) - 1u))];
     send_gate[(size_t)pos * L + (e - g * L)] = row_gate[r];
   }
 }
 
-// dst[i] = src[map[i]] for i < *count (bf16 rows of d elements, 16-byte vectors, warp per row)
 __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ src, const int* __restrict__ map,
                               const int* __restrict__ count, int d, __nv_bfloat16* __restrict__ dst) {
   ptx::pdl_trigger();
@@ -168,7 +174,7 @@ sonic_status sonic_ep_build_plan(const sonic_moe_desc* D, int G, const sonic_rou
   launch_popc(p->bm, W, G, p->wprefix, p->send_counts, st);
   launch_k(k_ep_offsets, 1, 32, 0, st, p->send_counts, G, p->send_offsets);
   launch_scan_tokens(p->tokcnt, T, p->ep_rowptr, st);
-  launch_k(k_ep_fill, (T + 127) / 128, 128, 0, st, rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->row_gate, T, L, W,
+  launch_k(k_ep_fill, (unsigned)(((size_t)T * 32 + 255) / 256), 256, 0, st, rt->token_rowptr, rt->token_rows, rt->tile_expert, rt->row_gate, T, L, W,
                                             p->dmask, p->bm, p->wprefix, p->send_offsets, p->ep_rowptr, p->ep_rows,
                                             p->send_token, p->send_gate);
   set_last_launch_count(5);

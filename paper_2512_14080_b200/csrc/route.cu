@@ -678,25 +678,29 @@ __global__ void k_csr_rows_chunked(const uint32_t* __restrict__ bm, const int* _
 }
 
 
-// One block: thread i scans the contiguous chunk [i*per, (i+1)*per) sequentially, one block
-// scan combines the chunk sums.
+// One block, tiles of 4 x 1024 values: thread i holds values [4i, 4i+4) of the tile (coalesced
+// loads), a block scan of the per-thread sums plus the running carry gives the exclusive prefix.
 __global__ void __launch_bounds__(1024) k_scan_tokens(const int* __restrict__ cnt, int T, int* __restrict__ rowptr) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const int per = (T + blockDim.x - 1) / blockDim.x;
-  const int t0 = threadIdx.x * per;
-  const int t1 = min(t0 + per, T);
-  int s = 0;
-  for (int t = t0; t < t1; ++t) s += cnt[t];
-  int tot;
-  int run = block_excl_scan(s, &tot);
-  for (int t = t0; t < t1; ++t) {
-    rowptr[t] = run;
-    run += cnt[t];
+  int carry = 0;
+  for (int base = 0; base < T; base += 4 * (int)blockDim.x) {
+    const int i0 = base + 4 * (int)threadIdx.x;
+    int v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = i0 + k < T ? __ldg(cnt + i0 + k) : 0;
+    int tot;
+    int run = carry + block_excl_scan(v[0] + v[1] + v[2] + v[3], &tot);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (i0 + k < T) rowptr[i0 + k] = run;
+      run += v[k];
+    }
+    carry += tot;
+    __syncthreads();  // block_excl_scan's shared partials are reused by the next tile
   }
-  if (threadIdx.x == 0) rowptr[T] = tot;
+  if (threadIdx.x == 0) rowptr[T] = carry;
 }
-
 
 void launch_popc(const uint32_t* bm, int W, int nrows, int* wprefix, int* cnt, cudaStream_t st) {
   launch_k(k_expert_popc, nrows, 1024, 0, st, bm, W, wprefix, cnt, nullptr);
