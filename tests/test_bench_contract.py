@@ -66,4 +66,6 @@ def test_two_rank_bench_line(comm):
     d = json.loads(lines[0])
     assert BASE_KEYS <= set(d)
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["parallelism"] == "ep2"
+    ex = d["exchange"]
+    assert ex["bytes_out_per_step"] > 0 and ex["layer_roofline_ms_with_exchange"] > ex["nvlink_roofline_ms"] > 0
     assert d["scaling"] == "weak"

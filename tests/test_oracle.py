@@ -119,7 +119,7 @@ def test_rank_matches_paper_S_prime_form():
             assert np.array_equal(paper, om._rank_expert_column(S[:, e], tc[:, e]))
 
 
-@pytest.mark.parametrize("M", [4, 16, 128])
+@pytest.mark.parametrize("M", [4, 16, 128, 256])  # 256: the 2-CTA pair's M tile (Q16)
 def test_token_rounding_invariants(M):
     """North-star TR invariants + P:1236/P:1243 locality, over 100 seeds."""
     for seed in range(100 if M < 128 else 20):
