@@ -217,7 +217,9 @@ def workload_config(args, cfg):
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
             **({"m_tile": args.m_tile} if getattr(args, "m_tile", 128) != 128 else {}),
-            "l2": "not flushed: per-step working set (X, W1, W2, H, Y, dX~, ...) is several GB >> 126 MB L2"}
+            "l2": ("flushed before every timed step (memset of 2x L2 outside the step's event pair); warm "
+                   "back-to-back number in `warm`") if getattr(args, "l2_flush", False) else
+                  "not flushed: per-step working set (X, W1, W2, H, Y, dX~, ...) is several GB >> 126 MB L2"}
 
 
 # --------------------------------------------------------------------------- main
@@ -241,6 +243,10 @@ def main():
     ap.add_argument("--m-tile", type=int, default=128, choices=[128, 256],
                     help="token-rounding tile (256 = the 2-CTA pair's M tile: no half-empty pairs)")
     ap.add_argument("--dw-bf16", action="store_true", help="SONIC_F_DW_BF16: weight gradients stored as bf16")
+    ap.add_argument("--no-l2-flush", dest="l2_flush", action="store_false",
+                    help="time the K steps back to back without flushing L2 (the primary number flushes)")
+    ap.add_argument("--sustain-s", type=float, default=0.0,
+                    help="also run the step back to back for this many seconds (sustained / power-capped regime)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
                     help="EP exchange: NCCL all-to-all-v, or libsonic's peer-memory kernels (CUDA IPC / NVLink)")
     args = ap.parse_args()
@@ -375,34 +381,81 @@ def main():
         dist.all_reduce(ft)
         flops_all = float(ft.item())
 
-    # ---- device-timed region: inputs resident in HBM
-    clocks = ClockSampler(local)
-    sonic.sonic_profile_enable(True)
-    sonic.sonic_profile_collect()
-    sonic.LAUNCHES[0] = 0
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        step()
-    ev1.record()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    if world > 1:
-        dist.barrier()
-    sonic.sonic_profile_enable(False)
-    recs = sonic.sonic_profile_collect()
-    ms = ev0.elapsed_time(ev1)
-    gpu_launches = sonic.LAUNCHES[0]
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    # ---- device-timed region: inputs resident in HBM, no instrumentation inside it
+    # Primary number: L2 flushed before every step (a write of 2x the L2 size, outside
+    # the step's own event pair); `warm` beside it: the same K steps back to back, L2 not flushed.
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_buf = torch.empty(max(2 * l2_bytes, 1 << 20), dtype=torch.uint8, device=dev) if args.l2_flush else None
+
+    def timed_pass(flush, profile=False):
+        clocks = ClockSampler(local)
+        sonic.sonic_profile_enable(profile)
+        sonic.sonic_profile_collect()
+        sonic.LAUNCHES[0] = 0
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clocks.start()
+        if flush:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for a, b in evs:
+                flush_buf.zero_()
+                a.record()
+                step()
+                b.record()
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in evs)
+        else:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for _ in range(args.steps):
+                step()
+            ev1.record()
+            torch.cuda.synchronize()
+            ms = ev0.elapsed_time(ev1)
+        clk = clocks.stop()
+        if world > 1:
+            dist.barrier()
+        sonic.sonic_profile_enable(False)
+        recs = sonic.sonic_profile_collect()
+        launches = sonic.LAUNCHES[0]
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, clk, recs, launches
+
+    ms, clk, _, gpu_launches = timed_pass(args.l2_flush)
     ms_step = ms / args.steps
     value = flops_all / (ms_step * 1e-3) / 1e12
+    ms_w, clk_w, _, _ = timed_pass(False) if args.l2_flush else (ms, clk, None, None)
+    warm = {"ms_per_step": ms_w / args.steps, "value": flops_all / (ms_w / args.steps * 1e-3) / 1e12,
+            "clocks": clk_w, "l2": "not flushed (steps back to back)"}
+    # per-kernel breakdown: a second pass of the same K steps with every launch bracketed by CUDA
+    # events on its own stream (sonic_profile_*), so the headline above carries no instrumentation
+    ms_p, clk_p, recs, _ = timed_pass(False, profile=True)
+    sustained = None
+    if args.sustain_s > 0:
+        # seconds-long back-to-back run: the regime the sustained (power-capped) peak describes
+        n_sus = 0
+        clocks = ClockSampler(local)
+        torch.cuda.synchronize()
+        clocks.start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        t0 = time.time()
+        while time.time() - t0 < args.sustain_s:
+            for _ in range(20):
+                step()
+            n_sus += 20
+            e1.record()
+            e1.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        sus_ms = e0.elapsed_time(e1) / n_sus
+        sustained = {"seconds": args.sustain_s, "steps": n_sus, "ms_per_step": sus_ms,
+                     "value": flops_all / (sus_ms * 1e-3) / 1e12, "clocks": clocks.stop()}
 
     # ---- per-kernel breakdown and roofline of the dominant kernel
     peaks = load_peaks()
@@ -412,22 +465,30 @@ def main():
         a = agg.setdefault(name, [0.0, 0])
         a[0] += t
         a[1] += 1
-    tf_peak = peaks["bf16_tflops_sustained"]
+    # Tensor peak for the roofline: the burst figure when the breakdown pass ran at (near) max SM clock
+    # without a power cap, the sustained one otherwise (MEASURED_PEAKS.json either way)
+    capped = ("sw_power_cap" in (clk_p.get("reasons") or [])) or (
+        clk_p.get("sm_mhz") and clk_p.get("sm_max_mhz") and clk_p["sm_mhz"] < 0.95 * clk_p["sm_max_mhz"])
+    tf_peak = peaks["bf16_tflops_sustained"] if capped else peaks["bf16_tflops"]
+    peak_choice = ("bf16_tflops_sustained: the breakdown pass saw sw_power_cap or SM clock < 0.95 max" if capped
+                   else "bf16_tflops (burst): the breakdown pass ran at max SM clock, no power cap")
     bw_peak = peaks["hbm_gbs"]
     peaks["hbm_write_gbs"] = wr_peak = wr_gbs
-    peaks["hbm_write_source"] = "measured in this run before the warm-up (1 GiB memset, best of 10)"
+    peaks["hbm_write_source"] = "measured in this run before the warm-up (1 GiB memset, best of 10); label only"
     kernels = {}
     for name, (tot, cnt) in agg.items():
         avg = tot / cnt
         mm = model.get(name, dict(flops=0, paper=0, tight=0, write=0))
         t_tensor = mm["flops"] / (tf_peak * 1e12) * 1e3
-        # bytes bound: all bytes at the copy rate, or the written bytes alone at the write rate
-        t_hbm = max(mm["paper"] / (bw_peak * 1e9), mm.get("write", 0) / (wr_peak * 1e9)) * 1e3
-        kernels[name] = dict(avg_ms=avg, launches_per_step=cnt / args.steps, share=tot / ms if ms else None,
+        t_hbm = mm["paper"] / (bw_peak * 1e9) * 1e3  # all algorithmic bytes at the measured copy rate
+        t_write = mm.get("write", 0) / (wr_peak * 1e9) * 1e3
+        kernels[name] = dict(avg_ms=avg, launches_per_step=cnt / args.steps, share=tot / ms_p if ms_p else None,
                              tflops=mm["flops"] / (avg * 1e-3) / 1e12 if mm["flops"] else 0.0,
                              gbs_paper=mm["paper"] / (avg * 1e-3) / 1e9, gbs_tight=mm["tight"] / (avg * 1e-3) / 1e9,
                              bound="tensor" if t_tensor >= t_hbm else "hbm",
-                             roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None)
+                             roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None,
+                             # label only, not a roofline: the written bytes at this run's memset rate
+                             write_aware_ms=max(t_tensor, t_hbm, t_write))
     dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"]) if kernels else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -439,8 +500,7 @@ def main():
         if k["bound"] == "tensor":
             roof = {"kernel": dom, "bound": "tensor", "achieved": k["tflops"], "peak": tf_peak, "unit": "TFLOP/s",
                     "frac": k["tflops"] / tf_peak, "traffic": traffic,
-                    "algorithmic_per_launch": model[dom]["flops"],
-                    "peak_source": peaks["source"] + " bf16_tflops_sustained (kernel timed inside a long step)"}
+                    "algorithmic_per_launch": model[dom]["flops"], "peak_source": peaks["source"] + " " + peak_choice}
         else:
             roof = {"kernel": dom, "bound": "hbm", "achieved": k["gbs_paper"], "peak": bw_peak, "unit": "GB/s",
                     "frac": k["gbs_paper"] / bw_peak, "traffic": traffic,
@@ -557,14 +617,17 @@ def main():
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": workload_config(args, cfg),
-        "pct_peak": value / world / peaks["bf16_tflops"], "pct_peak_sustained": value / world / tf_peak,
+        "pct_peak": value / world / peaks["bf16_tflops"],
+        "pct_peak_sustained": value / world / peaks["bf16_tflops_sustained"],
         "tokens_per_s": T * world / (ms_step * 1e-3),
         "model_flops_per_step": flops_all, "rows_routed": R, "rows_padded": R_pad,
         "layer_roofline_ms": layer_roof_ms, "layer_roofline_frac": layer_roof_ms / ms_step,
         # the same metric without sonic_route (the paper's bounds exclude the router)
         "value_excl_route": (flops_all / ((ms_step - kernels["route"]["avg_ms"] * kernels["route"]["launches_per_step"])
                                           * 1e-3) / 1e12) if "route" in kernels else None,
-        "act_mem_bytes": act,
+        "act_mem_bytes": act, "warm": warm, "sustained": sustained,
+        "breakdown_pass": {"ms_per_step": ms_p / args.steps, "clocks": clk_p,
+                           "note": "per-kernel events on (sonic_profile_enable); kernels/roofline come from it"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
         "clocks": clk, "kernels": kernels, "exchange": exchange, "peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops",
                                                                                 "bf16_tflops_sustained", "source",

@@ -57,7 +57,9 @@ typedef enum {
   SONIC_ROUTE_TC = 0,      /* token-choice top-K */
   SONIC_ROUTE_TR_NRF = 1,  /* token rounding, Alg. 4 with NR-f */
   SONIC_ROUTE_GIVEN = 2,   /* arbitrary routing input: S is the gate matrix, t -> e iff
-                              S[t,e] != 0, gate = S[t,e] (no renormalisation); topk_ids/topk_s are
+                              the bits of S[t,e] are not +0.0 (a routed pair with a zero gate is
+                              passed as -0.0, which sonic_ep_build_plan does), gate = S[t,e] (no
+                              renormalisation); topk_ids/topk_s are
                               not written; K may be up to E.  Used by the expert-parallel receive side. */
   /* Token rounding with the other subroutines of the ablation; selection, rescue and
    * gates as for SONIC_ROUTE_TR_NRF. */
@@ -128,7 +130,8 @@ typedef struct {
 #define SONIC_ROUTING_NFIELDS 14
 
 /* Upper bound on grouped rows (incl. pad rows): min(T*K + E*(max(m_tile,128)-1), E*ceil(T/128)*128),
- * rounded up to a multiple of 128.  Returns -1 on an invalid descriptor. */
+ * rounded up to a multiple of 128; for SONIC_ROUTE_EC exactly E*ceil_128(C) with the capacity
+ * C = min(ceil_m_tile(ceil(T*K/E)), T) (Q22).  Returns -1 on an invalid descriptor. */
 int64_t sonic_rows_max(const sonic_moe_desc *desc);
 
 /* Byte size of each sonic_routing field, in declaration order. */

@@ -384,6 +384,16 @@ def _f64(a):
     return np.asarray(a, dtype=np.float64)
 
 
+def expert_forward(Xe, W1e, W2e, ge):
+    """One expert's forward on its gathered rows (Alg. 2):
+    H_e = X_e W1_e;  A_e = act(H_e) (SwiGLU);  Y_e = g_e * (A_e W2_e) (gate before
+    aggregation, Q2 / P:1774 option (1)).  ``Xe`` = Gather(X, pi_:,e) [f_e, d], ``ge`` [f_e]."""
+    He = Xe @ W1e                                              # H_e = X_e W1_e
+    Ae = swiglu(He)                                            # A_e = act(H_e)
+    Ye = np.asarray(ge)[:, None] * (Ae @ W2e)                  # Y_e scaled by g (Q2)
+    return He, Ae, Ye
+
+
 def forward(X, W1, W2, rt: Routing, experts=None):
     """O_t = sum_e pi_te g_te Y_{e,t},  Y_e = SwiGLU(X_e W1_e) W2_e.
 
@@ -397,10 +407,7 @@ def forward(X, W1, W2, rt: Routing, experts=None):
     H, A, Y, tokens = {}, {}, {}, {}
     for e in (range(E) if experts is None else experts):
         toks = np.nonzero(rt.kept[:, e])[0]
-        Xe = X[toks]                                           # X_e = Gather(X, pi_:,e)
-        He = Xe @ W1[e]                                        # H_e = X_e W1_e
-        Ae = swiglu(He)                                        # A_e = act(H_e)
-        Ye = rt.gate[toks, e][:, None] * (Ae @ W2[e])          # Y_e scaled by g (Q2)
+        He, Ae, Ye = expert_forward(X[toks], W1[e], W2[e], rt.gate[toks, e])  # X_e = Gather(X, pi_:,e)
         np.add.at(O, toks, Ye)                                 # O_t = sum_e ...
         H[e], A[e], Y[e], tokens[e] = He, Ae, Ye, toks
     return ForwardResult(O, H, A, Y, tokens)
@@ -430,14 +437,43 @@ class BackwardResult:
     dXt: dict                # e -> [f_e,d]  dX~ rows
 
 
-def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None):
-    """Alg. 3 then Alg. 5, row by row in the paper's notation.
+@dataclass
+class ExpertGrads:
+    """One expert's backward outputs (Alg. 3 + Alg. 5), rows in ascending token order."""
+    dAp: np.ndarray          # [f_e,n]   dA' = Gather(dO) W2_e^T
+    A: np.ndarray            # [f_e,n]   A = SwiGLU(H)
+    dH: np.ndarray           # [f_e,2n]
+    A_prime: np.ndarray      # [f_e,n]   A' = s A
+    dS: np.ndarray           # [f_e]     <dA', A>
+    dW1: np.ndarray          # [d,2n]
+    dW2: np.ndarray          # [n,d]
+    dXt: np.ndarray          # [f_e,d]   dX~ rows
+
+
+def expert_backward(dOe, Xe, W1e, W2e, ge, He=None):
+    """One expert's backward on its gathered rows, Alg. 3 then Alg. 5:
 
     dA'_e = Gather(dO) W2_e^T;  dA_e = s_e dA'_e;  (A_e, dH_e) = dSwiGLU(dA_e, H_e);
     A'_e = s_e A_e;  dS_e,t = <dA'_e,t, A_e,t> (boxed eq. P:1752);
-    dW2_e = A'_e^T dO_e (Q4, P:1768);  dX~_e = dH_e W1_e^T;  dW1_e = X_e^T dH_e;
-    dX_t = sum_e pi_te dX~_e,t.
-    H is recomputed from X unless a cache is given (only X and H are cached, §3.2).
+    dW2_e = A'_e^T dO_e (Q4);  dX~_e = dH_e W1_e^T;  dW1_e = X_e^T dH_e.
+    H_e is recomputed from X_e unless given (only X and H are cached, sec. 3.2)."""
+    s = np.asarray(ge)[:, None]                                # s_e = Gather(S, pi_:,e)
+    if He is None:
+        He = Xe @ W1e
+    dAp = dOe @ W2e.T                                          # dA'_e
+    dA = s * dAp                                               # dA_e
+    Ae, dHe = dswiglu(dA, He)                                  # A_e, dH_e
+    Ape = s * Ae                                               # A'_e
+    return ExpertGrads(dAp=dAp, A=Ae, dH=dHe, A_prime=Ape,
+                       dS=np.sum(dAp * Ae, axis=1),            # <dA'_e,t, A_e,t>
+                       dW1=Xe.T @ dHe,                         # dW1_e = X_e^T dH_e
+                       dW2=Ape.T @ dOe,                        # dW2_e = A'^T dO_e
+                       dXt=dHe @ W1e.T)                        # dX~_e = dH_e W1_e^T
+
+
+def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None):
+    """Alg. 3 then Alg. 5 for every expert (``expert_backward``), then
+    dX_t = sum_e pi_te dX~_e,t (Alg. 5's aggregation).
     ``experts`` restricts the work (dX then holds only those experts' terms).
     """
     dO, X, W1, W2 = _f64(dO), _f64(X), _f64(W1), _f64(W2)
@@ -450,19 +486,11 @@ def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None):
     dS, dH, Ap, dXt = {}, {}, {}, {}
     for e in (range(E) if experts is None else experts):
         toks = np.nonzero(rt.kept[:, e])[0]
-        s = rt.gate[toks, e][:, None]                          # s_e = Gather(S, pi_:,e)
-        He = X[toks] @ W1[e] if H_cache is None else _f64(H_cache[e])
-        dOe = dO[toks]                                         # Gather(dO, pi_:,e)
-        dAp = dOe @ W2[e].T                                    # dA'_e
-        dA = s * dAp                                           # dA_e
-        Ae, dHe = dswiglu(dA, He)                              # A_e, dH_e
-        Ape = s * Ae                                           # A'_e
-        dS[e] = np.sum(dAp * Ae, axis=1)                       # <dA'_e,t, A_e,t>
-        dW2[e] = Ape.T @ dOe                                   # dW2_e = A'^T dO_e
-        dXt[e] = dHe @ W1[e].T                                 # dX~_e = dH_e W1_e^T
-        dW1[e] = X[toks].T @ dHe                               # dW1_e = X_e^T dH_e
-        np.add.at(dX, toks, dXt[e])                            # dX_t = sum_e dX~_e,t
-        dH[e], Ap[e] = dHe, Ape
+        g = expert_backward(dO[toks], X[toks], W1[e], W2[e], rt.gate[toks, e],
+                            None if H_cache is None else _f64(H_cache[e]))
+        dW1[e], dW2[e] = g.dW1, g.dW2
+        np.add.at(dX, toks, g.dXt)                             # dX_t = sum_e dX~_e,t
+        dS[e], dH[e], Ap[e], dXt[e] = g.dS, g.dH, g.A_prime, g.dXt
     return BackwardResult(dX, dW1, dW2, dS, dH, Ap, dXt)
 
 
@@ -512,17 +540,14 @@ def forward_tokens(X, W1, W2, rt: Routing, tokens):
 
 
 def backward_experts(dO, X, W1, W2, rt: Routing, experts):
-    """dW1_e, dW2_e and the dS of every kept row of each listed expert (Alg. 3 + Alg. 5),
-    converting only those experts' weights to fp64.  Returns {e: (dW1_e, dW2_e, dS_e)}."""
+    """dW1_e, dW2_e and the dS of every kept row of each listed expert (``expert_backward``),
+    converting only those experts' weights to fp64 (W1 / W2 may be lazy per-expert views).
+    Returns {e: (dW1_e, dW2_e, dS_e)}.  Pinned against ``backward`` in tests/test_oracle.py."""
     out = {}
     for e in experts:
         toks = np.nonzero(rt.kept[:, e])[0]
-        s = rt.gate[toks, e][:, None]
-        Xe, dOe = _f64(X[toks]), _f64(dO[toks])
-        W1e, W2e = _f64(W1[e]), _f64(W2[e])
-        dAp = dOe @ W2e.T                                      # dA'_e
-        Ae, dHe = dswiglu(s * dAp, Xe @ W1e)                   # dSwiGLU(dA_e, H_e)
-        out[e] = ((Xe.T @ dHe), ((s * Ae).T @ dOe), np.sum(dAp * Ae, axis=1))
+        g = expert_backward(_f64(dO[toks]), _f64(X[toks]), _f64(W1[e]), _f64(W2[e]), rt.gate[toks, e])
+        out[e] = (g.dW1, g.dW2, g.dS)
     return out
 
 

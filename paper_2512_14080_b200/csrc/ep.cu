@@ -88,7 +88,8 @@ __global__ void k_ep_fill(const int* __restrict__ rowptr, const int* __restrict_
     const int e = tile_expert[r / GEMM_M];
     const int g = e / L;
     const int pos = ep_rows[j0 + __popc(mask & ((1u << g) - 1u))];
-    send_gate[(size_t)pos * L + (e - g * L)] = row_gate[r];
+    const float gv = row_gate[r];  // a routed pair with a zero gate is sent as -0.0 (GIVEN membership)
+    send_gate[(size_t)pos * L + (e - g * L)] = __float_as_uint(gv) == 0u ? -0.f : gv;
   }
 }
 

@@ -711,7 +711,8 @@ void launch_scan_tokens(const int* cnt, int T, int* rowptr, cudaStream_t st) {
 
 // ---------------------------------------------------------------- given routing
 // SONIC_ROUTE_GIVEN ("an interface that accepts arbitrary routing input"): S is the gate
-// matrix itself, token t is routed to e iff S[t,e] != 0.  One block per 32-token word.
+// matrix itself, token t is routed to e iff S[t,e] is not +0.0 (so a routed pair whose gate is exactly
+// zero travels as -0.0 and keeps its row: its dS = <dA', A> is not zero).  One block per 32-token word.
 __global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W, uint32_t* __restrict__ bm,
                                unsigned* __restrict__ ticket) {
   ptx::pdl_trigger();
@@ -726,7 +727,7 @@ __global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W,
   for (int i = threadIdx.x; i < 32 * E; i += blockDim.x) {
     const int tl = i / E, e = i - tl * E;
     const int t = blockIdx.x * 32 + tl;
-    if (t < T && S[(size_t)t * E + e] != 0.f) atomicOr(&words[e], 1u << tl);
+    if (t < T && __float_as_uint(S[(size_t)t * E + e]) != 0u) atomicOr(&words[e], 1u << tl);
   }
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) bm[(size_t)e * W + blockIdx.x] = words[e];

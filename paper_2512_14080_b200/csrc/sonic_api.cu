@@ -199,7 +199,7 @@ bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUten
                  const GemmArgs& args, int grid, cudaStream_t st, const CUtensorMap* dmap = nullptr) {
   const CUtensorMap& d = dmap ? *dmap : c0;
   const bool cta2 = use_cta2(BN);
-  if (cta2) grid &= ~1;
+  if (cta2) grid = std::max(2, grid & ~1);  // a pair needs both CTAs, even for a single pair tile
   switch (BN) {
     case 256:
       return cta2 ? launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st)
@@ -246,9 +246,16 @@ bool supported_dims(const sonic_moe_desc* D) {
 long long rows_max_of(const sonic_moe_desc* D) {
   const long long pairs = (D->route_mode == SONIC_ROUTE_GIVEN && D->rows_cap > 0) ? std::min(D->rows_cap, D->T * D->K)
                                                                                    : D->T * D->K;
+  const long long b = (long long)D->E * ((D->T + GEMM_M - 1) / GEMM_M) * GEMM_M;
+  if (D->route_mode == SONIC_ROUTE_EC) {
+    // expert choice (Q22): every expert keeps exactly C = min(ceil_M(ceil(T K / E)), T) rows, padded
+    // to a 128-row tile; E * C can exceed T K by up to E * (m_tile - 1) + E - 1 (same C as launch_route)
+    const long long avg = (D->T * D->K + D->E - 1) / D->E;
+    const long long C = std::min<long long>((avg + D->m_tile - 1) / D->m_tile * D->m_tile, D->T);
+    return std::min((long long)D->E * ((C + GEMM_M - 1) / GEMM_M) * GEMM_M, b);
+  }
   // token rounding moves an expert's count by less than one rounding tile; TC pads to 128-row tiles
   const long long a = pairs + (long long)D->E * (std::max(D->m_tile, GEMM_M) - 1);
-  const long long b = (long long)D->E * ((D->T + GEMM_M - 1) / GEMM_M) * GEMM_M;
   const long long r = std::min(a, b);
   return (r + GEMM_M - 1) / GEMM_M * GEMM_M;
 }

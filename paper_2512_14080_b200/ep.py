@@ -147,6 +147,11 @@ class PeerComm:
 
     ranks: the local ranks (one per process under torchrun, or G virtual ranks in one process, each
     on its own CUDA stream so their barriers can meet).
+
+    Lifetime: one PeerComm serves ONE MoE layer with one training step in flight.  The received x
+    and dO rows stay views into the region and the backward's dW1 / dW2 read them, so a second
+    layer's dispatch through the same PeerComm would overwrite them before the first layer's
+    backward (silently wrong weight gradients).  Stack layers with one PeerComm each.
     """
 
     NB = 2  # count blocks exchanged per rank: send rows per destination, routed pairs per destination

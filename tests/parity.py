@@ -33,17 +33,68 @@ def err_stats(got, ref):
     return float(relf), float(maxrel)
 
 
-# Below this many elements the relative Frobenius error is the relative error of one or a few
-# single dot products, which cancellation can push past 1e-2 with bf16 operands however exact the
-# kernel is; there only the north star's per-element bound (|err| <= 2e-2 max|ref|) applies.
-MIN_FROB_ELEMS = 16
-
-
 def assert_close(name, got, ref, relf_tol=REL_F, max_tol=MAX_REL):
     relf, maxrel = err_stats(got, ref)
-    frob_ok = relf <= relf_tol or np.asarray(ref).size < MIN_FROB_ELEMS
-    assert frob_ok and maxrel <= max_tol, f"{name}: relF={relf:.3e} max|err|/max|ref|={maxrel:.3e}"
+    assert relf <= relf_tol and maxrel <= max_tol, f"{name}: relF={relf:.3e} max|err|/max|ref|={maxrel:.3e}"
     return relf, maxrel
+
+
+# bf16 unit roundoff (8-bit significand, round to nearest even)
+U_BF16 = 2.0 ** -8
+
+
+def ds_storage_bound(dAp, H):
+    """First-order bound on |dS_gpu - dS_ref| per row from the one rounding the method itself
+    prescribes before dS: H is stored (and re-read) as bf16 (the cached activation), so the
+    kernel's A = silu(g) u is formed from g(1+d1), u(1+d2) with |d1|, |d2| <= u_bf16, giving
+      |dA_j| <= u_bf16 (|g silu'(g)| + |silu(g)|) |u|   and   |d dS| <= sum_j |dA'_j| |dA_j|.
+    Twice that (second-order terms, the fp32 accumulations, the SFU sigmoid at ~2^-11) is the
+    tolerance (tolerance reading).  dS = <dA', A> is a single dot product whose
+    terms can cancel, so its relative error is not bounded by the element-wise roundoff: this bound
+    is what a correct kernel guarantees for it when the Frobenius criterion does not apply."""
+    n = H.shape[1] // 2
+    g, u = H[:, :n], H[:, n:]
+    sens = (np.abs(g * om.dsilu(g)) + np.abs(om.silu(g))) * np.abs(u)
+    return 2.0 * U_BF16 * np.sum(np.abs(dAp) * sens, axis=1)
+
+
+class ErrAcc:
+    """Streaming version of err_stats / assert_close over a tensor compared in slices: the same
+    relative Frobenius error (sqrt of summed squares) and the same max|err| / max|ref|."""
+
+    def __init__(self, name):
+        self.name, self.sd, self.sr, self.md, self.mr, self.n = name, 0.0, 0.0, 0.0, 0.0, 0
+        self.cond_ok = None  # per-element storage bound (dS only): None = not supplied
+
+    def add(self, got, ref, cond=None):
+        got = np.asarray(got, np.float64)
+        ref = np.asarray(ref, np.float64)
+        assert got.shape == ref.shape, f"{self.name}: shape {got.shape} vs oracle {ref.shape}"
+        diff = got - ref
+        self.sd += float(np.sum(diff * diff))
+        self.sr += float(np.sum(ref * ref))
+        if diff.size:
+            self.md = max(self.md, float(np.max(np.abs(diff))))
+            self.mr = max(self.mr, float(np.max(np.abs(ref))))
+        self.n += ref.size
+        if cond is not None:
+            ok = bool(np.all(np.abs(diff) <= cond))
+            self.cond_ok = ok if self.cond_ok is None else (self.cond_ok and ok)
+
+    def stats(self):
+        relf = np.sqrt(self.sd) / np.sqrt(self.sr) if self.sr > 0 else np.sqrt(self.sd)
+        maxrel = self.md / self.mr if self.mr > 0 else self.md
+        return float(relf), float(maxrel)
+
+    def check(self, relf_tol=REL_F, max_tol=MAX_REL):
+        relf, maxrel = self.stats()
+        ok = relf <= relf_tol and maxrel <= max_tol
+        # dS only: a few elements whose dot products cancel may pass on the derived storage bound
+        # (every element within it); the per-element criterion still applies to them.
+        if not ok and self.cond_ok and maxrel <= max_tol:
+            ok = True
+        assert ok, f"{self.name}: relF={relf:.3e} max|err|/max|ref|={maxrel:.3e} (n={self.n}, bound_ok={self.cond_ok})"
+        return relf, maxrel
 
 
 def routing_to_numpy(rt, desc):
@@ -107,8 +158,69 @@ def f64(t):
     return t.detach().float().cpu().numpy().astype(np.float64)
 
 
+class _Lazy:
+    """Per-expert fp64 copies of a device weight tensor, converted on first use."""
+
+    def __init__(self, w):
+        self.w, self.shape, self.cache = w, tuple(w.shape), {}
+
+    def __getitem__(self, e):
+        e = int(e)
+        if e not in self.cache:
+            self.cache = {e: f64(self.w[e])}  # keep one expert: the full-size weights are GBs in fp64
+        return self.cache[e]
+
+
+def stream_parity(desc, inp, g, rto, check_ws=True):
+    """Element-by-element parity of every output, one expert at a time (the oracle's per-expert
+    stages ``expert_forward`` / ``expert_backward``, pinned in tests/test_oracle.py), so that the
+    full BASELINE sizes fit in host memory.  Every routed row, token and weight element is compared;
+    the criteria are applied to each whole tensor (streamed sums, ErrAcc)."""
+    E = desc.E
+    X, dO = f64(inp.X), f64(inp.dO)
+    W1, W2 = _Lazy(inp.W1), _Lazy(inp.W2)
+    T, d = X.shape
+    O_ref = np.zeros((T, d))
+    dX_ref = np.zeros((T, d))
+    names = ["H", "dW1", "dW2", "dS"] + (["A", "dH", "Ap"] if check_ws else [])
+    acc = {k: ErrAcc(k) for k in names}
+    have_A = check_ws and g.get("A") is not None
+    for e in range(E):
+        lo = int(rto.pad_offsets[e])
+        fe = int(rto.f_rounded[e])
+        hi_pad = int(rto.pad_offsets[e + 1])
+        toks = rto.row_token[lo: lo + fe]
+        ge = rto.row_gate[lo: lo + fe]
+        Xe, dOe = X[toks], dO[toks]
+        He, Ae, Ye = om.expert_forward(Xe, W1[e], W2[e], ge)
+        gr = om.expert_backward(dOe, Xe, W1[e], W2[e], ge, He)
+        np.add.at(O_ref, toks, Ye)
+        np.add.at(dX_ref, toks, gr.dXt)
+        acc["H"].add(f64(g["H"][lo: lo + fe]), He)
+        acc["dS"].add(f64(g["dS"][lo: lo + fe]), gr.dS, cond=ds_storage_bound(gr.dAp, He))
+        acc["dW1"].add(f64(g["dW1"][e]), gr.dW1)
+        acc["dW2"].add(f64(g["dW2"][e]), gr.dW2)
+        if hi_pad > lo + fe:
+            assert torch.all(g["dS"][lo + fe: hi_pad] == 0), f"dS on pad rows of expert {e} must be 0"
+        if check_ws:
+            if have_A:
+                acc["A"].add(f64(g["A"][lo: lo + fe]), Ae)
+            acc["dH"].add(f64(g["dH"][lo: lo + fe]), gr.dH)
+            acc["Ap"].add(f64(g["Ap"][lo: lo + fe]), gr.A_prime)
+            if hi_pad > lo + fe:
+                assert torch.all(g["dH"][lo + fe: hi_pad] == 0) and torch.all(g["Ap"][lo + fe: hi_pad] == 0), \
+                    f"pad rows of expert {e} must be exact zeros"
+    stats = {}
+    stats["O"] = assert_close("O", f64(g["O"]), O_ref)
+    stats["dX"] = assert_close("dX", f64(g["dX"]), dX_ref)
+    for k, a in acc.items():
+        if a.n or k in ("dW1", "dW2"):
+            stats[k] = a.check()
+    return stats
+
+
 def full_parity(desc, inp, mode="tc", check_ws=True, rounding="nrf"):
-    """Element-by-element parity of every output at a size the oracle finishes in seconds."""
+    """Routing bit-exact in full, then every value output element by element (stream_parity)."""
     g = run_gpu(desc, inp, want_ws=check_ws)
     S = inp.S.cpu().numpy()
     rto = om.route(S, desc.K, mode=mode, m_tile=desc.m_tile,
@@ -116,31 +228,4 @@ def full_parity(desc, inp, mode="tc", check_ws=True, rounding="nrf"):
                    gate_raw=bool(desc.flags & sonic.SONIC_F_GATE_RAW), rounding=rounding, seed=desc.seed)
     gr = routing_to_numpy(g["rt"], desc)
     check_routing(gr, rto)
-    X, W1, W2, dO = f64(inp.X), f64(inp.W1), f64(inp.W2), f64(inp.dO)
-    fw = om.forward(X, W1, W2, rto)
-    bw = om.backward(dO, X, W1, W2, rto)
-    stats = {}
-    stats["O"] = assert_close("O", f64(g["O"]), fw.O)
-    Hg = f64(g["H"])
-    rows = np.nonzero(rto.row_token >= 0)[0]
-    exp_of = rto.row_expert[rows]
-    Href = np.concatenate([fw.H[e] for e in range(desc.E) if e in fw.H and len(fw.H[e])], axis=0)
-    Aref = np.concatenate([fw.A[e] for e in range(desc.E) if e in fw.A and len(fw.A[e])], axis=0)
-    stats["H"] = assert_close("H", Hg[rows], Href)
-    stats["dX"] = assert_close("dX", f64(g["dX"]), bw.dX)
-    stats["dW1"] = assert_close("dW1", f64(g["dW1"]), bw.dW1)
-    stats["dW2"] = assert_close("dW2", f64(g["dW2"]), bw.dW2)
-    dSref = np.concatenate([bw.dS[e] for e in range(desc.E) if len(bw.dS[e])])
-    dSg = f64(g["dS"])
-    stats["dS"] = assert_close("dS", dSg[rows], dSref)
-    pad = np.nonzero(rto.row_token < 0)[0]
-    assert np.all(dSg[pad] == 0), "dS on pad rows must be 0"
-    if check_ws:
-        stats["A"] = assert_close("A", f64(g["A"])[rows], Aref)
-        dHref = np.concatenate([bw.dH[e] for e in range(desc.E) if len(bw.dH[e])], axis=0)
-        Apref = np.concatenate([bw.A_prime[e] for e in range(desc.E) if len(bw.A_prime[e])], axis=0)
-        stats["dH"] = assert_close("dH", f64(g["dH"])[rows], dHref)
-        stats["Ap"] = assert_close("Ap", f64(g["Ap"])[rows], Apref)
-        assert np.all(f64(g["dH"])[pad] == 0) and np.all(f64(g["Ap"])[pad] == 0), "pad rows must be exact zeros"
-    assert np.all(np.isin(exp_of, np.arange(desc.E)))
-    return stats
+    return stream_parity(desc, inp, g, rto, check_ws=check_ws)

@@ -56,6 +56,19 @@ def test_host_side_sizes(lib):
             assert sonic.sonic_bwd_workspace_size(d) >= rows * (3 * c["n"] + c["d"]) * 2
 
 
+@pytest.mark.parametrize("T,E,K", [(4097, 256, 8), (8193, 256, 8), (16385, 256, 8), (300, 200, 6), (100, 1, 1),
+                                   (4096, 128, 8)])
+def test_ec_rows_bound_covers_capacity(lib, T, E, K):
+    """Expert choice keeps C = min(ceil_M(ceil(T K / E)), T) rows per expert (Q22); rows_max must hold
+    E tiles-rounded copies of C (E*C can exceed T K + E*127 once E > 128)."""
+    from paper_2512_14080_b200 import sonic
+    for m_tile in (128, 256):
+        d = sonic.make_desc(T, 128, 64, E, K, mode=sonic.SONIC_ROUTE_EC, m_tile=m_tile)
+        C = min(-(-(-(-T * K // E)) // m_tile) * m_tile, T)
+        need = E * (-(-C // 128) * 128)
+        assert sonic.sonic_rows_max(d) >= need
+
+
 def test_invalid_arguments_are_rejected_before_any_launch(lib):
     from paper_2512_14080_b200 import sonic
     bad = [

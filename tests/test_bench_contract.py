@@ -42,6 +42,15 @@ def test_default_arm_line_tiny():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
     assert d["act_mem_bytes"]["measured"]["held_fwd_to_bwd"] >= d["act_mem_bytes"]["X"]
+    # the headline is flushed and uninstrumented; warm and the instrumented breakdown pass sit beside it
+    assert d["config"]["l2"].startswith("flushed") and d["warm"]["ms_per_step"] > 0
+    assert d["breakdown_pass"]["ms_per_step"] > 0
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
+    if peaks and r["bound"] == "tensor":
+        assert r["peak"] in (peaks["bf16_tflops"], peaks["bf16_tflops_sustained"])
+    if peaks and r["bound"] == "hbm":
+        assert r["peak"] == peaks["hbm_gbs"]
 
 
 @pytest.mark.gpu

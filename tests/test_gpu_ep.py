@@ -111,3 +111,40 @@ def test_ep_plan_dedup():
         seg = tok[off[g]: off[g + 1]]
         assert np.all(np.diff(seg) > 0)
         assert set(seg.tolist()) == {t for t in range(T) if g in set((ids[t] // L).tolist())}
+
+
+@pytest.mark.parametrize("comm_kind", ["sim", "peer"])
+def test_ep_zero_gate_pairs_keep_their_rows(comm_kind):
+    """A routed (token, expert) pair whose gate is exactly 0 (K = E picks zero scores) contributes
+    nothing to O but has dS = <dA', A> != 0.  The dispatch sends it as -0.0 so the receiving rank's
+    GIVEN routing keeps the row: dS matches the single-GPU oracle on every kept pair."""
+    G, T, d, n, E, K = 2, 256, 128, 64, 8, 8
+    base = make_inputs(T, d, n, E, K, seed=50, device="cuda")
+    L = E // G
+    ins = [make_inputs(T, d, n, E, K, seed=51 + r, device="cuda") for r in range(G)]
+    for r, i in enumerate(ins):  # zero scores on two experts (one per rank) for every other token
+        S = i.S.clone()
+        S[::2, 1] = 0.0
+        S[1::2, 6] = 0.0
+        i.S = (S / S.sum(1, keepdim=True)).contiguous()
+        i.S[::2, 1] = 0.0
+        i.S[1::2, 6] = 0.0
+    ranks = [ep.EPRank(T, d, n, E, K, G, r, base.W1[r * L:(r + 1) * L].contiguous(),
+                       base.W2[r * L:(r + 1) * L].contiguous(), mode=sonic.SONIC_ROUTE_TC) for r in range(G)]
+    comm = ep.SimComm(G) if comm_kind == "sim" else ep.PeerComm(G, T, d, L, range(G))
+    ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins])
+    outs = ep.ep_backward(ranks, comm, [i.dO for i in ins])
+    torch.cuda.synchronize()
+    W1n, W2n = f64(base.W1), f64(base.W2)
+    for r in range(G):
+        S = ins[r].S.cpu().numpy()
+        rto = om.route(S, K, mode="tc", m_tile=128)
+        assert (rto.kept & (S == 0)).sum() == T  # the zero-score pairs are routed
+        bw = om.backward(f64(ins[r].dO), f64(ins[r].X), W1n, W2n, rto)
+        rows = np.nonzero(rto.row_token >= 0)[0]
+        dSref = np.concatenate([bw.dS[e] for e in range(E) if len(bw.dS[e])])
+        zero_rows = rows[rto.row_gate[rows] == 0]
+        assert np.all(np.abs(dSref[np.isin(rows, zero_rows)]) > 0)
+        assert_close(f"dS[{r}]", f64(outs[r][1])[rows], dSref)
+    if comm_kind == "peer":
+        comm.close()

@@ -17,6 +17,13 @@ SMALL = [
     ("multi_tr", 2048, 256, 128, 16, 4, "tr"),
     ("wide_n_tc", 1024, 256, 384, 8, 2, "tc"),       # dH with 3 N-tiles (dS partials)
     ("many_e_tc", 512, 128, 64, 64, 8, "tc"),         # empty / tiny experts
+    # n = 256: the dH kernel's BN = 256 H-chunk ring (the 7B production path); 2048 rows per expert:
+    # 32 k-blocks in the varlen-K dW kernels, past the 16-deep gather-index ring (ring refill)
+    ("n256_tc", 8192, 256, 256, 8, 2, "tc"),
+    ("n256_tr", 8192, 256, 256, 8, 2, "tr"),
+    # the 7B layer's d and n (every 7B kernel configuration) with 8 experts of ~2048 rows
+    ("7b_dims_tc", 8192, 1536, 256, 8, 2, "tc"),
+    ("7b_dims_tr", 8191, 1536, 256, 8, 2, "tr"),
 ]
 
 
@@ -183,6 +190,9 @@ FUZZ = [
     (1, 64, 32, 1, 1, "tc"),      # a single token, a single expert
     (1, 64, 32, 4, 2, "tr"),      # TR with T < m_tile: every chosen "up" is capped at T (Q15)
     (2, 64, 64, 3, 3, "tr"),      # K = E with two tokens
+    (4097, 128, 64, 256, 8, "ec"),  # EC with E > 128 and T K not divisible by E (rows bound)
+    (300, 128, 64, 1, 1, "tc"),   # E = 1 with 2-CTA dW tiles: a single varlen-K pair tile
+    (64, 128, 128, 1, 1, "tr"),
 ]
 
 

@@ -286,6 +286,77 @@ def test_backward_uses_cached_H():
     assert np.allclose(a.dW1, b.dW1, atol=1e-13)
 
 
+def _lazy(W):
+    """Per-expert views the way the full-size GPU tests hand weights to the oracle."""
+    class Lazy:
+        shape = W.shape
+
+        def __getitem__(self, e):
+            return W[int(e)].copy()
+    return Lazy()
+
+
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+def test_backward_experts_matches_full_backward(mode):
+    """backward_experts (the dW1 / dW2 / dS checker of the sampled and streamed full-size GPU tests)
+    equals backward (FD- and dual-path-pinned above) on every expert, including empty ones, with the
+    weights passed as lazy per-expert views."""
+    for seed in range(4):
+        X, W1, W2, S, dO, rt = rand_case(60 + seed, 48, 8, 4, 10, 3, mode=mode, m_tile=4)
+        bw = om.backward(dO, X, W1, W2, rt)
+        E = W1.shape[0]
+        got = om.backward_experts(dO, X, _lazy(W1), _lazy(W2), rt, range(E))
+        for e in range(E):
+            dW1e, dW2e, dSe = got[e]
+            assert np.array_equal(dW1e, bw.dW1[e]) and np.array_equal(dW2e, bw.dW2[e])
+            assert np.array_equal(dSe, bw.dS[e])
+        # an independent spot check of one expert's dW2 / dW1 written out as sums over its rows
+        e = int(np.argmax(rt.f_rounded))
+        toks = np.nonzero(rt.kept[:, e])[0]
+        dW2_sum = np.zeros_like(W2[e])
+        dW1_sum = np.zeros_like(W1[e])
+        for t in toks:
+            g = rt.gate[t, e]
+            h = X[t] @ W1[e]
+            dap = W2[e] @ dO[t]                                  # dA' row = dO_t W2_e^T
+            a, dh = om.dswiglu(g * dap, h)
+            dW2_sum += np.outer(g * a, dO[t])
+            dW1_sum += np.outer(X[t], dh)
+        assert np.allclose(got[e][1], dW2_sum, rtol=0, atol=1e-12)
+        assert np.allclose(got[e][0], dW1_sum, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("mode", ["tc", "tr"])
+def test_metadata_brute_force(mode):
+    """build_metadata against an independent construction: the grouped rows are the kept (expert,
+    token) pairs sorted lexicographically, each expert's segment padded to a GEMM_M multiple; the
+    token CSR is the same pairs sorted by (token, expert)."""
+    X, W1, W2, S, dO, rt = rand_case(8, 300, 4, 2, 9, 3, mode=mode, m_tile=16)
+    T, E = rt.kept.shape
+    pairs = sorted((e, t) for t in range(T) for e in range(E) if rt.kept[t, e])
+    row_token, row_expert, row_gate, row_of = [], [], [], {}
+    for e in range(E):
+        mine = [t for (ee, t) in pairs if ee == e]
+        for t in mine:
+            row_of[(t, e)] = len(row_token)
+            row_token.append(t)
+            row_expert.append(e)
+            row_gate.append(rt.gate[t, e])
+        while len(row_token) % om.GEMM_M:
+            row_token.append(-1)
+            row_expert.append(e)
+            row_gate.append(0.0)
+    assert rt.row_token.tolist() == row_token
+    assert rt.row_expert.tolist() == row_expert
+    assert rt.row_gate.tolist() == row_gate
+    by_token = sorted((t, e) for (e, t) in pairs)
+    assert rt.token_rows.tolist() == [row_of[p] for p in by_token]
+    counts = [sum(1 for (t, _) in by_token if t == tt) for tt in range(T)]
+    assert rt.token_rowptr.tolist() == [0] + np.cumsum(counts).tolist()
+    assert rt.offsets.tolist() == [0] + np.cumsum([sum(1 for (e, _) in pairs if e == ee) for ee in range(E)]).tolist()
+    assert rt.tile_expert.tolist() == row_expert[:: om.GEMM_M]
+
+
 # ------------------------------------------------------------------ closed forms
 def test_cost_spot_values():
     c = GOLD["cost"]
