@@ -86,6 +86,10 @@ typedef enum {
 #define SONIC_F_DW_BF16         32  /* sonic_moe_bwd: dW1 / dW2 are written as bf16 (the float* arguments point
                                        at bf16 [E,d,2n] / [E,n,d] buffers): half the weight-gradient store
                                        traffic; fp32 accumulation as always.  Not with SONIC_F_DW_ACCUMULATE. */
+#define SONIC_F_NO_FUSED_UPDOWN 64  /* sonic_moe_fwd: run the up- and down-projection as two kernels with A in
+                                       the workspace (the fused kernel, NEXT-1, is used whenever n is 128 or
+                                       256 and d % 128 == 0; sonic_fwd_workspace_size then holds Y only).
+                                       Used for A/B measurement and to test both paths. */
 #define SONIC_F_DW_ACCUMULATE    4  /* sonic_moe_bwd: dW1 += ..., dW2 += ... (fp32 element-wise adds done by
                                        the TMA store unit; one add per element per call, so deterministic)
                                        instead of overwriting -- gradient accumulation over microbatches */
@@ -138,11 +142,13 @@ int64_t sonic_rows_max(const sonic_moe_desc *desc);
 sonic_status sonic_routing_sizes(const sonic_moe_desc *desc, size_t bytes_out[SONIC_ROUTING_NFIELDS]);
 
 size_t sonic_route_workspace_size(const sonic_moe_desc *desc);
-size_t sonic_fwd_workspace_size(const sonic_moe_desc *desc);  /* A [rows_max,n] + Y [rows_max,d] (bf16) */
+size_t sonic_fwd_workspace_size(const sonic_moe_desc *desc);  /* Y [rows_max,d] (bf16), + A [rows_max,n] when the
+                                                                up/down projections are not fused */
 size_t sonic_bwd_workspace_size(const sonic_moe_desc *desc);  /* dH, A', dX~ (bf16) + dS partials (fp32) */
 
 /* Byte offsets of the named transients inside the fwd / bwd workspace, for
- * inspection by tests: fwd {A, Y}; bwd {dH, A_prime, dXt, dS_part}.  which = 0 (fwd) or 1 (bwd). */
+ * inspection by tests: fwd {A, Y}; bwd {dH, A_prime, dXt, dS_part}.  which = 0 (fwd) or 1 (bwd).
+ * The fwd A offset is SIZE_MAX when the up/down projections are fused (A is never materialised). */
 sonic_status sonic_workspace_offsets(const sonic_moe_desc *desc, int which, size_t offs_out[4]);
 
 /*

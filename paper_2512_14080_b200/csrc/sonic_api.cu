@@ -9,6 +9,7 @@
 
 #include "../../include/sonic.h"
 #include "gemm.cuh"
+#include "updown.cuh"
 #include "sonic_internal.h"
 
 using namespace sonic;
@@ -104,7 +105,7 @@ bool map3d(CUtensorMap* m, const void* ptr, bool f32, long long E, long long row
 }
 
 #ifndef SONIC_BWD_OVERLAP
-#define SONIC_BWD_OVERLAP 3  // 7B, same run: 0 -> 2.186 ms, 1 -> 2.180, 3 -> 2.183 / 2.141 (dW1 then runs alone)
+#define SONIC_BWD_OVERLAP 0  // 7B, same run: 0 -> 2.186 ms, 1 -> 2.180, 3 -> 2.183 / 2.141: no measured gain, so serial (clean per-kernel attribution)
 #endif
 // One internal non-blocking stream (+ fork/join events) per device, for the backward's
 // weight-gradient branch.  Created on first use; calls from several host threads on the same
@@ -215,6 +216,38 @@ bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUten
   }
 }
 
+template <int NU, int BND>
+bool launch_updown(const CUtensorMap& w1, const CUtensorMap& w2, const CUtensorMap& h, const CUtensorMap& y,
+                   const UpDownArgs& args, int grid, cudaStream_t st) {
+  using Cfg = UpDownCfg<NU, BND>;
+  auto kern = sonic_updown_kernel<NU, BND>;
+  static bool attr[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 63]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM) != cudaSuccess)
+      return false;
+    attr[dev & 63] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(std::max(2, grid & ~1));
+  cfg.blockDim = dim3(Cfg::THREADS);
+  cfg.dynamicSmemBytes = Cfg::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[1].val.programmaticStreamSerializationAllowed = SONIC_PDL ? 1 : 0;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 2;
+  if (cudaLaunchKernelEx(&cfg, kern, w1, w2, h, y, args) != cudaSuccess) return false;
+  ++g_launches;
+  return true;
+}
+
 int pick_bn(long long N) { return N % 256 == 0 ? 256 : N % 128 == 0 ? 128 : 64; }
 // rows of the K-major weight box held by one CTA
 int bnl(int BN) { return use_cta2(BN) ? BN / 2 : BN; }
@@ -303,12 +336,24 @@ int dh_bn(int n) {
   return (n % 256 == 0 && SONIC_DH_MAX_BN >= 256) ? 256 : n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
 }
 
-struct FwdWs { size_t A, Y, total; };
+#ifndef SONIC_FUSED_UPDOWN
+#define SONIC_FUSED_UPDOWN 1  // NEXT-1: up -> down fused (updown.cuh) where the shape allows it
+#endif
+// The fused up/down kernel holds a CTA's 128 rows of A (128 x n bf16) in shared memory: n = 128 or
+// 256 (with 3+ operand stages); d a multiple of 128 (D jobs of 256 or 128 columns).
+bool fused_updown(const sonic_moe_desc* D) {
+  return SONIC_FUSED_UPDOWN && !(D->flags & SONIC_F_NO_FUSED_UPDOWN) && use_cta2(256) && (D->n == 128 || D->n == 256) &&
+         D->d % 128 == 0;
+}
+
+struct FwdWs { size_t A, Y, total; bool fused; };
 FwdWs fwd_ws(const sonic_moe_desc* D) {
   const Shape s = shape_of(D);
   FwdWs w;
   size_t o = 0;
-  w.A = o; o += al((size_t)s.rows_max * s.n * 2);
+  w.fused = fused_updown(D);
+  w.A = w.fused ? SIZE_MAX : o;  // fused: A never leaves the SM
+  if (!w.fused) o += al((size_t)s.rows_max * s.n * 2);
   w.Y = o; o += al((size_t)s.rows_max * s.d * 2);
   w.total = o;
   return w;
@@ -511,8 +556,25 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
   g.num_pairs = rt->num_pairs; g.tile_pairs = rt->tile_pairs;
   g.row_gate = rt->row_gate; g.pad_offsets = rt->pad_offsets; g.E = E; g.n = n; g.rows_max = R;
 
+  if (w.fused) {
+    // K1 + K2 fused: H = Gather(X) W1_e -> H (cached), A = SwiGLU(H) in smem, Y = g * (A W2_e)
+    CUtensorMap mW1, mW2, mH, mY;
+    if (!map3d(&mW1, W1, false, E, d, 2 * n, 64, 64) || !map3d(&mW2, W2, false, E, n, d, 64, 64) ||
+        !map2d(&mH, H, false, R, 2 * n, 64, 32) || !map2d(&mY, Ybuf, false, R, d, 64, 32))
+      return SONIC_ERR_CUDA;
+    UpDownArgs a{};
+    a.num_pairs = rt->num_pairs; a.tile_pairs = rt->tile_pairs; a.tile_expert = rt->tile_expert;
+    a.row_token = rt->row_token; a.row_gate = rt->row_gate;
+    a.X = static_cast<const __nv_bfloat16*>(X); a.d = d; a.n = n;
+    ProfScope ps("updown", st);
+    const bool ok = n == 256 ? (d % 256 == 0 ? launch_updown<2, 256>(mW1, mW2, mH, mY, a, grid, st)
+                                             : launch_updown<2, 128>(mW1, mW2, mH, mY, a, grid, st))
+                             : (d % 256 == 0 ? launch_updown<1, 256>(mW1, mW2, mH, mY, a, grid, st)
+                                             : launch_updown<1, 128>(mW1, mW2, mH, mY, a, grid, st));
+    if (!ok) return SONIC_ERR_CUDA;
+  }
   // K1 up-proj: H = Gather(X) W1_e, SwiGLU epilogue -> H, A
-  {
+  if (!w.fused) {
     CUtensorMap mA, mB, mC0, mC1;
     const int Wg = n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
     const int BN = 2 * Wg;
@@ -526,7 +588,7 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
     if (!launch_gemm<K_UP>(BN, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
   }
   // K2 down-proj: Y = gate * (A W2_e)
-  {
+  if (!w.fused) {
     CUtensorMap mA, mB, mC0;
     const int BN = pick_bn(d);
     if (!map2d(&mA, Abuf, false, R, n, 64, 128) || !map3d(&mB, W2, false, E, n, d, 64, 64) ||

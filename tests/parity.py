@@ -149,7 +149,8 @@ def run_gpu(desc, inp, want_ws=True):
         out["dH"] = sonic.ws_view(wsb, offs[0], (rows, 2 * desc.n), torch.bfloat16)
         out["Ap"] = sonic.ws_view(wsb, offs[1], (rows, desc.n), torch.bfloat16)
         offs = sonic.sonic_workspace_offsets(desc, 0)
-        out["A"] = sonic.ws_view(wsf, offs[0], (rows, desc.n), torch.bfloat16)
+        fused = offs[0] == (1 << 64) - 1  # the fused up/down kernel keeps A on chip
+        out["A"] = None if fused else sonic.ws_view(wsf, offs[0], (rows, desc.n), torch.bfloat16)
         out["Y"] = sonic.ws_view(wsf, offs[1], (rows, desc.d), torch.bfloat16)
     return out
 

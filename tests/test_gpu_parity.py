@@ -24,6 +24,10 @@ SMALL = [
     # the 7B layer's d and n (every 7B kernel configuration) with 8 experts of ~2048 rows
     ("7b_dims_tc", 8192, 1536, 256, 8, 2, "tc"),
     ("7b_dims_tr", 8191, 1536, 256, 8, 2, "tr"),
+    # the fused up/down kernel: D jobs of 128 columns (d % 256 != 0); empty experts and half pairs
+    # (experts with one 128-row tile) with n = 256
+    ("fused_bnd128_tc", 1000, 384, 128, 16, 4, "tc"),
+    ("fused_many_e_tc", 512, 256, 256, 64, 8, "tc"),
 ]
 
 
@@ -223,3 +227,25 @@ def test_split_backward_matches_monolithic():
     R = int(rt.offsets[E].item())
     assert torch.equal(dXa, dX) and torch.equal(w1b, dW1) and torch.equal(w2b, dW2)
     assert torch.equal(dSa[:R], dS[:R])
+
+
+@pytest.mark.parametrize("shape,mode", [((2048, 256, 128, 16, 4), "tc"), ((8192, 1536, 256, 8, 2), "tr"),
+                                        ((512, 256, 256, 64, 8), "tc")], ids=["n128", "7b_dims_tr", "half_pairs"])
+def test_fused_updown_equals_two_kernels(shape, mode):
+    """NEXT-1: the fused up/down kernel (A kept in shared memory) gives the same H and O as the
+    separate up- and down-projection kernels (SONIC_F_NO_FUSED_UPDOWN) bit for bit: the same MMA
+    shapes and K order, the same bf16 A; and the unfused path stays parity-green at n = 256."""
+    T, d, n, E, K = shape
+    inp = make_inputs(T, d, n, E, K, seed=31, device="cuda")
+    m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
+    d_f = sonic.make_desc(T, d, n, E, K, mode=m)
+    d_u = sonic.make_desc(T, d, n, E, K, mode=m, flags=sonic.SONIC_F_NO_FUSED_UPDOWN)
+    assert sonic.sonic_fwd_workspace_size(d_f) < sonic.sonic_fwd_workspace_size(d_u)  # no A in the workspace
+    rt = sonic.sonic_route(d_f, inp.S)
+    Of, Hf, _ = sonic.sonic_moe_fwd(d_f, inp.X, inp.W1, inp.W2, rt)
+    Ou, Hu, _ = sonic.sonic_moe_fwd(d_u, inp.X, inp.W1, inp.W2, rt)
+    torch.cuda.synchronize()
+    R_pad = int(rt.pad_offsets[E])
+    assert torch.equal(Hf[:R_pad], Hu[:R_pad])
+    assert torch.equal(Of, Ou)
+    full_parity(d_u, inp, mode=mode)
