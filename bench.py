@@ -60,6 +60,9 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4):
         "up": dict(flops=4 * R * d * n, paper=R * d * b + W1 + R * 2 * n * b + R * n * b,
                    tight=T * d * b + W1 + R * 2 * n * b + R * n * b),
         "down": dict(flops=2 * R * n * d, paper=R * n * b + W2 + R * d * b, tight=R * n * b + W2 + R * d * b),
+        # fused up + down (NEXT-1): A stays on chip, so neither its write nor its read is counted
+        "updown": dict(flops=6 * R * d * n, paper=R * d * b + W1 + W2 + R * 2 * n * b + R * d * b,
+                       tight=T * d * b + W1 + W2 + R * 2 * n * b + R * d * b),
         "agg_O": dict(flops=0, paper=R * d * b + T * d * b, tight=R * d * b + T * d * b),
         "dH": dict(flops=2 * R * n * d, paper=R * d * b + W2 + 2 * R * 2 * n * b + R * n * b + R * 4,
                    tight=T * d * b + W2 + 2 * R * 2 * n * b + R * n * b + R * 4),
@@ -74,7 +77,7 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4):
     }
     # bytes written (part of the totals above): HBM writes alone run at ~3.9 TB/s on B200, well
     # below the copy rate, so a store-heavy kernel is also bounded by write_bytes / write bandwidth
-    writes = {"up": R * 2 * n * b + R * n * b, "down": R * d * b, "agg_O": T * d * b,
+    writes = {"up": R * 2 * n * b + R * n * b, "down": R * d * b, "updown": R * 2 * n * b + R * d * b, "agg_O": T * d * b,
               "dH": R * 2 * n * b + R * n * b + R * 4, "dW2": E * n * d * dw, "dXt": R * d * b,
               "dW1": E * d * 2 * n * dw, "agg_dX": T * d * b, "route": T * K * 8 + R * 12, "dS_reduce": R * 4}
     for k, w in writes.items():
@@ -216,6 +219,7 @@ def workload_config(args, cfg):
             **({"ep_exchange": "peer-memory kernels (CUDA IPC)" if args.comm == "peer" else "NCCL all-to-all-v"}
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
+            **({"updown": "two kernels (SONIC_F_NO_FUSED_UPDOWN)"} if getattr(args, "no_fuse", False) else {}),
             **({"m_tile": args.m_tile} if getattr(args, "m_tile", 128) != 128 else {}),
             "l2": ("flushed before every timed step (memset of 2x L2 outside the step's event pair); warm "
                    "back-to-back number in `warm`") if getattr(args, "l2_flush", False) else
@@ -243,6 +247,8 @@ def main():
     ap.add_argument("--m-tile", type=int, default=128, choices=[128, 256],
                     help="token-rounding tile (256 = the 2-CTA pair's M tile: no half-empty pairs)")
     ap.add_argument("--dw-bf16", action="store_true", help="SONIC_F_DW_BF16: weight gradients stored as bf16")
+    ap.add_argument("--no-fuse", action="store_true",
+                    help="SONIC_F_NO_FUSED_UPDOWN: separate up- and down-projection kernels (A through HBM)")
     ap.add_argument("--no-l2-flush", dest="l2_flush", action="store_false",
                     help="time the K steps back to back without flushing L2 (the primary number flushes)")
     ap.add_argument("--sustain-s", type=float, default=0.0,
@@ -299,7 +305,8 @@ def main():
     T, d, n, E, K = cfg["T"], cfg["d"], cfg["n"], cfg["E"], cfg["K"]
     mode = ROUTE_MODES[args.mode][0]
     desc = sonic.make_desc(T, d, n, E, K, mode=mode, m_tile=args.m_tile,
-                           flags=sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0)
+                           flags=(sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0) |
+                           (sonic.SONIC_F_NO_FUSED_UPDOWN if args.no_fuse else 0))
     use_ep = args.ep or world > 1
     if not use_ep:
         # ---- one GPU, all experts local: route + fwd + bwd through the C ABI

@@ -182,7 +182,12 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   fprintf(stderr, "TIMING kind=%d BN=%d cta2=%d: mma_total %.0f  wait_tempty %.0f  wait_full %.0f | epi_wait_tfull %.0f  epi_busy %.0f (kcycles; epilogue counters summed over the pair)\n",
           KIND, BN, (int)CTA2, h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3, h[3] / n / 1e3, h[4] / n / 1e3);
 #else
-  if (cudaLaunchKernelEx(&cfg, kern, a, b, c0, c1, dmap, args) != cudaSuccess) return false;
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, kern, a, b, c0, c1, dmap, args);
+  if (err != cudaSuccess) {
+    fprintf(stderr, "libsonic: sonic_gemm_kernel<%d,%d,%d> launch failed: %s\n", KIND, BN, (int)CTA2,
+            cudaGetErrorString(err));
+    return false;
+  }
 #endif
   ++g_launches;
   return true;
@@ -243,7 +248,28 @@ bool launch_updown(const CUtensorMap& w1, const CUtensorMap& w2, const CUtensorM
   attrs[1].val.programmaticStreamSerializationAllowed = SONIC_PDL ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
-  if (cudaLaunchKernelEx(&cfg, kern, w1, w2, h, y, args) != cudaSuccess) return false;
+#ifdef SONIC_TIMING
+  static unsigned long long* dbg = nullptr;
+  if (!dbg) cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
+  cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), st);
+  UpDownArgs targs = args;
+  targs.dbg = dbg;
+  if (cudaLaunchKernelEx(&cfg, kern, w1, w2, h, y, targs) != cudaSuccess) return false;
+  unsigned long long hc[16];
+  cudaMemcpyAsync(hc, dbg, sizeof(hc), cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  const double nn = hc[8] ? (double)hc[8] : 1.0;
+  fprintf(stderr, "TIMING updown NU=%d BND=%d (kcycles per pair): total %.0f | mma tempty U %.0f D %.0f | full U %.0f D %.0f | "
+          "aready %.0f | job span U %.0f D %.0f || epi(w0) wait_tfull %.0f busy U %.0f D %.0f\n",
+          NU, BND, hc[0] / nn / 1e3, hc[1] / nn / 1e3, hc[2] / nn / 1e3, hc[3] / nn / 1e3, hc[4] / nn / 1e3,
+          hc[5] / nn / 1e3, hc[6] / nn / 1e3, hc[7] / nn / 1e3, hc[9] / nn / 1e3, hc[10] / nn / 1e3, hc[11] / nn / 1e3);
+#else
+  const cudaError_t err = cudaLaunchKernelEx(&cfg, kern, w1, w2, h, y, args);
+  if (err != cudaSuccess) {
+    fprintf(stderr, "libsonic: sonic_updown_kernel<%d,%d> launch failed: %s\n", NU, BND, cudaGetErrorString(err));
+    return false;
+  }
+#endif
   ++g_launches;
   return true;
 }

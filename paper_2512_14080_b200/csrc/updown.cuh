@@ -40,21 +40,33 @@ struct UpDownArgs {
   const float* row_gate;   // gate per grouped row (0 on pad rows)
   const __nv_bfloat16* X;  // [T, d]
   int d, n;
+  unsigned long long* dbg;  // SONIC_TIMING builds only: cycle counters (sonic_api.cu prints them)
 };
 
-template <int NU_, int BND_>
+#ifndef SONIC_UD_EPW
+#define SONIC_UD_EPW 8  // epilogue warps of the fused kernel (4: one per TMEM lane quarter; 8: two)
+#endif
+#ifndef SONIC_UD_L2PF
+#define SONIC_UD_L2PF 8  // L2 prefetch distance (k-blocks) of the gathered X rows (0 = off)
+#endif
+
+template <int NU_, int BND_, int EPW_ = SONIC_UD_EPW>
 struct UpDownCfg {
   static constexpr int NU = NU_;                       // U jobs per tile (n / 128)
   static constexpr int BND = BND_;                     // D job N width (256 or 128)
-  static constexpr int NP = 4;                         // producer warps
-  static constexpr int EPW = 4;                        // epilogue warps
-  static constexpr int THREADS = 32 * (NP + 1 + EPW);  // 288
+  static constexpr int NP = EPW_ == 8 ? 2 : 4;         // producer warps (11 or 9 warps: <= 3 per SM
+                                                       // sub-partition, so 168 registers fit)
+  static constexpr int EPW = EPW_;                     // epilogue warps (4 or 8)
+  static constexpr int EPH = EPW / 4;                  // epilogue warps per TMEM lane quarter
+  static constexpr int THREADS = 32 * (NP + 1 + EPW);  // 288 / 352
+  static constexpr int RS = NP * 4;                    // gather: row stride between a thread's rows
+  static constexpr int RPT = GEMM_BM / RS;             // gather: rows per producer thread
   static constexpr uint32_t A_BYTES = GEMM_BM * GEMM_BK * 2;        // gathered X tile, 16 KB
   static constexpr uint32_t BU_BYTES = 128 * GEMM_BK * 2;           // this CTA's W1 half: 128 cols
   static constexpr uint32_t BD_BYTES = (BND / 2) * GEMM_BK * 2;     // this CTA's W2 half
   static constexpr uint32_t STAGE_BYTES = A_BYTES + BU_BYTES;       // 32 KB
   static constexpr int ABUF = NU * 2 * 16384;                       // A buffer: 128 x n bf16
-  static constexpr int NB = 2;                                      // staging ring per epilogue warp
+  static constexpr int NB = EPW == 4 ? 2 : 1;                       // staging ring per epilogue warp
   static constexpr int FIXED = ABUF + EPW * NB * STG_BYTES + 1024 + 1024;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - FIXED) / (int)STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -62,8 +74,10 @@ struct UpDownCfg {
   static_assert(STAGES >= 3, "fused up/down: not enough shared memory for the operand ring");
 };
 
+// Registers are allocated per SM sub-partition (16K each; warp w runs on sub-partition w % 4): with
+// at most 3 warps per sub-partition (9 or 11 warps) every thread may hold 168
 template <int NU, int BND>
-__global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
+__global__ void __maxnreg__(168)
     sonic_updown_kernel(const __grid_constant__ CUtensorMap mW1, const __grid_constant__ CUtensorMap mW2,
                         const __grid_constant__ CUtensorMap mH, const __grid_constant__ CUtensorMap mY,
                         const UpDownArgs args) {
@@ -81,8 +95,8 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* aready = tempty + 2;  // [NU]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aready + 2);
+  uint64_t* aready = tempty + 2;  // [2 NU]: one per 64-column k-block of A
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(aready + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -104,8 +118,8 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
       ptx::mbar_init(&tempty[s], 2 * Cfg::EPW);
-      ptx::mbar_init(&aready[s], 2 * Cfg::EPW);
     }
+    for (int s = 0; s < 2 * NU; ++s) ptx::mbar_init(&aready[s], 2 * 4);  // 4 lane-quarter warps x 2 CTAs
     ptx::fence_barrier_init();
     ptx::prefetch_tmap(&mW1);
     ptx::prefetch_tmap(&mW2);
@@ -134,32 +148,33 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
     // ============================================================ producers
     int stage = 0;
     uint32_t phase = 0;
-    const int pt = threadIdx.x;  // 0..127
+    constexpr int RS = Cfg::RS, RPT = Cfg::RPT;
+    const int pt = threadIdx.x;  // 0 .. 32 NP - 1
     const int c = pt & 7;        // 16-byte chunk within a 128-byte row
-    const int r0 = pt >> 3;      // rows r0 + 16 j
+    const int r0 = pt >> 3;      // rows r0 + RS j
     const uint32_t sw = (uint32_t)((c ^ (r0 & 7)) << 4);
     const uint64_t gpol = ptx::policy_evict_last();
-    int ntok[8];
+    int ntok[RPT];
     if (t_first < total) {
       int mt, e;
       bool v;
       decode(t_first, mt, v, e);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) ntok[j] = v ? tok_of(args.row_token, mt * GEMM_BM + r0 + 16 * j) : 0;
+      for (int j = 0; j < RPT; ++j) ntok[j] = v ? tok_of(args.row_token, mt * GEMM_BM + r0 + RS * j) : 0;
     }
     for (int tile = t_first; tile < total; tile += t_step) {
       int mt, e;
       bool valid;
       decode(tile, mt, valid, e);
-      const __nv_bfloat16* srcM[8];
+      const __nv_bfloat16* srcM[RPT];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) srcM[j] = args.X + clamp_tok(ntok[j]) * d + c * 8;
+      for (int j = 0; j < RPT; ++j) srcM[j] = args.X + clamp_tok(ntok[j]) * d + c * 8;
       if (tile + t_step < total) {  // the next tile's gather indices, one tile ahead
         int mt2, e2;
         bool v2;
         decode(tile + t_step, mt2, v2, e2);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) ntok[j] = v2 ? tok_of(args.row_token, mt2 * GEMM_BM + r0 + 16 * j) : 0;
+        for (int j = 0; j < RPT; ++j) ntok[j] = v2 ? tok_of(args.row_token, mt2 * GEMM_BM + r0 + RS * j) : 0;
       }
       // U jobs: gathered X rows + this CTA's 128 W1 columns (rank 0: gate, rank 1: up)
       for (int uj = 0; uj < NU; ++uj) {
@@ -176,13 +191,25 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
           }
           const uint32_t dst = ptx::smem_u32(sA) + r0 * 128 + sw;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) gather16(dst + j * 16 * 128, srcM[j] + kb * GEMM_BK, gpol);
+          for (int j = 0; j < RPT; ++j) gather16(dst + j * RS * 128, srcM[j] + kb * GEMM_BK, gpol);
           ptx::cp_async_mbar_arrive(bar);
+          // the first U job reads the tile's X rows from HBM: pull the lines SONIC_UD_L2PF k-blocks ahead
+          // into L2 (the 4-stage smem ring alone is ~2k cycles of lookahead); U_1.. re-read them from L2
+          if (SONIC_UD_L2PF > 0 && uj == 0 && c == 0 && kb + SONIC_UD_L2PF < KB_U) {
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) ptx::prefetch_l2(srcM[j] + (kb + SONIC_UD_L2PF) * GEMM_BK);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
+      }
+      // while the D jobs run, pull the next tile's first SONIC_UD_L2PF k-blocks of X rows into L2
+      // (thread c takes k-block c of its rows; ntok already holds the next tile's tokens)
+      if (SONIC_UD_L2PF > 0 && tile + t_step < total && c < SONIC_UD_L2PF && c < KB_U) {
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) ptx::prefetch_l2(args.X + clamp_tok(ntok[j]) * d + c * GEMM_BK);
       }
       // D jobs: this CTA's BND/2 columns of the W2 N-tile (A is resident in the A buffer)
       for (int di = 0; di < ND; ++di) {
@@ -216,18 +243,37 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
       uint32_t acc_phase = 0;
       uint32_t a_phase = 0;
       const uint32_t abase = ptx::smem_u32(abuf);
+#ifdef SONIC_TIMING
+      unsigned long long c0 = clock64(), c_te[2] = {0, 0}, c_full[2] = {0, 0}, c_ar = 0, c_busy[2] = {0, 0};
+#define TSTAMP(x) const unsigned long long x = clock64()
+#else
+#define TSTAMP(x)
+#endif
       for (int tile = t_first; tile < total; tile += t_step) {
         for (int job = 0; job < NU + ND; ++job) {
           const bool is_u = job < NU;
+          TSTAMP(ta);
           ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+#ifdef SONIC_TIMING
+          TSTAMP(tb);
+          c_te[is_u ? 0 : 1] += tb - ta;
+#endif
           ptx::tc_fence_after();
           const uint32_t d_tmem = tmem_base + acc * 256;
           const int nkb = is_u ? KB_U : KB_D;
           for (int kb = 0; kb < nkb; ++kb) {
-            if (job == NU && (kb & 1) == 0) {  // D_0: A columns [64 kb, 64 kb + 128) written by U_{kb/2}
-              ptx::mbar_wait(&aready[kb >> 1], a_phase);
+            if (job == NU) {  // D_0: A columns [64 kb, 64 kb + 64) written by U_{kb/2}'s epilogue
+              TSTAMP(tc);
+              ptx::mbar_wait(&aready[kb], a_phase);
+#ifdef SONIC_TIMING
+              c_ar += clock64() - tc;
+#endif
             }
+            TSTAMP(td);
             ptx::mbar_wait(&full[stage], phase);
+#ifdef SONIC_TIMING
+            c_full[is_u ? 0 : 1] += clock64() - td;
+#endif
             if (is_u) ptx::fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05.mma
             ptx::tc_fence_after();
             const uint32_t s_base = ptx::smem_u32(smem + stage * STAGE_BYTES);
@@ -246,11 +292,27 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
             }
           }
           ptx::mma_commit_mc(&tfull[acc], 0x3);
+#ifdef SONIC_TIMING
+          c_busy[is_u ? 0 : 1] += clock64() - ta;
+#endif
           acc ^= 1;
           if (acc == 0) acc_phase ^= 1;
         }
         a_phase ^= 1;
       }
+#ifdef SONIC_TIMING
+      if (args.dbg) {
+        atomicAdd(args.dbg + 0, clock64() - c0);
+        atomicAdd(args.dbg + 1, c_te[0]);
+        atomicAdd(args.dbg + 2, c_te[1]);
+        atomicAdd(args.dbg + 3, c_full[0]);
+        atomicAdd(args.dbg + 4, c_full[1]);
+        atomicAdd(args.dbg + 5, c_ar);
+        atomicAdd(args.dbg + 6, c_busy[0]);
+        atomicAdd(args.dbg + 7, c_busy[1]);
+        atomicAdd(args.dbg + 8, 1ull);
+      }
+#endif
     } else if (lane == 0 && !leader) {
       // relay: this CTA's producer arrivals (cp.async completions) -> the leader's full barrier
       int stage = 0;
@@ -269,15 +331,22 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
     }
     __syncwarp();
   } else {
-    // ============================================================ epilogue (4 warps)
+    // ============================================================ epilogue (EPW warps)
+    // Warp ew works on TMEM lane quarter q = warp % 4 (its 32 rows) and, with EPW = 8, on every other
+    // 64-column chunk (half = ew / 4).
+    constexpr int EPH = Cfg::EPH;
     const int ew = warp - NP - 1;
-    const int q = warp & 3;  // TMEM lane quarter
+    const int q = warp & 3;
+    const int half = ew / 4;
     StoreQ<Cfg::NB> sq{stg + ew * Cfg::NB * STG_BYTES, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
     const uint32_t tempty_leader = ptx::mapa(ptx::smem_u32(&tempty[0]), 0);
     const uint32_t aready_leader = ptx::mapa(ptx::smem_u32(&aready[0]), 0);
     const uint32_t arow = ptx::smem_u32(abuf) + (uint32_t)(32 * q) * 128;  // this warp's 32 rows of A
+#ifdef SONIC_TIMING
+    unsigned long long e_wait = 0, e_busy[2] = {0, 0};
+#endif
     for (int tile = t_first; tile < total; tile += t_step) {
       int mt, e;
       bool valid;
@@ -286,25 +355,35 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
       const int row = wrow + lane;
       const float gate = valid ? __ldg(args.row_gate + row) : 0.f;
       for (int job = 0; job < NU + ND; ++job) {
+#ifdef SONIC_TIMING
+        const unsigned long long ea = clock64();
+#endif
         ptx::mbar_wait(&tfull[acc], acc_phase);
+#ifdef SONIC_TIMING
+        const unsigned long long eb = clock64();
+        e_wait += eb - ea;
+#endif
         ptx::tc_fence_after();
         const uint32_t t_acc = tmem_base + ((uint32_t)(32 * q) << 16) + acc * 256;
         if (job < NU) {
-          // ---- U job: accumulator cols [0,128) = gate, [128,256) = up of H cols 128 job + [0,128)
-          if (valid) {
+          // ---- U job: accumulator cols [0,128) = gate, [128,256) = up of H cols 128 job + [0,128).
+          // Per 64-column chunk: A first (into the A buffer; then the MMA thread may start on that
+          // k-block of D_0), then the H gate / up columns through the staging ring by TMA store.
 #pragma unroll 1
-            for (int c = 0; c < 128; c += 64) {
-              const int col = 128 * job + c;
-              sq.template acquire<1>(lane);
-              const int i0 = sq.sb;
-              const int i1 = (i0 + 1) % Cfg::NB;
-              const uint32_t b0 = sq.addr(i0), b1 = sq.addr(i1);
-              const uint32_t ab = arow + (uint32_t)(col / 64) * 16384;  // A k-block col/64
+          for (int cc = half; cc < 2; cc += EPH) {
+            const int col = 128 * job + 64 * cc;
+            const int akb = 2 * job + cc;  // A k-block written by this chunk
+            uint32_t pu[2][16];            // up half of H, bf16 pairs, stored after the gate half
+            int ig = 0;
+            uint32_t bg = 0;
+            if (valid) {
+              ig = sq.acquire(lane);
+              bg = sq.addr(ig);
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 uint32_t g[32], u[32];
-                ptx::tmem_ld32(t_acc + c + 32 * h, g);
-                ptx::tmem_ld32(t_acc + 128 + c + 32 * h, u);
+                ptx::tmem_ld32(t_acc + 64 * cc + 32 * h, g);
+                ptx::tmem_ld32(t_acc + 128 + 64 * cc + 32 * h, u);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int q8 = 0; q8 < 4; ++q8) {
@@ -315,56 +394,58 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
                     hu[i] = bf16r(__uint_as_float(u[8 * q8 + i]));
                   }
                   const int ch = 4 * h + q8;
-                  ptx::st_shared_v4(b0 + swz(lane, ch), ptx::pack_bf16(hg[0], hg[1]), ptx::pack_bf16(hg[2], hg[3]),
-                                    ptx::pack_bf16(hg[4], hg[5]), ptx::pack_bf16(hg[6], hg[7]));
-                  ptx::st_shared_v4(b1 + swz(lane, ch), ptx::pack_bf16(hu[0], hu[1]), ptx::pack_bf16(hu[2], hu[3]),
-                                    ptx::pack_bf16(hu[4], hu[5]), ptx::pack_bf16(hu[6], hu[7]));
                   uint32_t apk[4];
 #pragma unroll
                   for (int i = 0; i < 4; ++i) {
                     const float a0 = hg[2 * i] * sigmoidf_fast(hg[2 * i]) * hu[2 * i];
                     const float a1 = hg[2 * i + 1] * sigmoidf_fast(hg[2 * i + 1]) * hu[2 * i + 1];
                     apk[i] = ptx::pack_bf16(a0, a1);
+                    pu[h][4 * q8 + i] = ptx::pack_bf16(hu[2 * i], hu[2 * i + 1]);
                   }
-                  ptx::st_shared_v4(ab + swz(lane, ch), apk[0], apk[1], apk[2], apk[3]);
+                  ptx::st_shared_v4(arow + (uint32_t)akb * 16384 + swz(lane, ch), apk[0], apk[1], apk[2], apk[3]);
+                  ptx::st_shared_v4(bg + swz(lane, ch), ptx::pack_bf16(hg[0], hg[1]), ptx::pack_bf16(hg[2], hg[3]),
+                                    ptx::pack_bf16(hg[4], hg[5]), ptx::pack_bf16(hg[6], hg[7]));
                 }
               }
-              sq.issue(lane, i0, &mH, col, wrow);      // H gate columns
-              sq.issue(lane, i1, &mH, n + col, wrow);  // H up columns
             }
-          }
-          // A columns [128 job, 128 job + 128) of this warp's rows are in place: make them visible to
-          // the tensor core (async proxy) and tell the leader's MMA thread
-          ptx::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            if (leader) ptx::mbar_arrive(&aready[job]);
-            else ptx::mbar_arrive_cluster(aready_leader + job * 8);
+            // A k-block akb of this warp's rows is in place: make it visible to the tensor core (async
+            // proxy) and tell the leader's MMA thread
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              if (leader) ptx::mbar_arrive(&aready[akb]);
+              else ptx::mbar_arrive_cluster(aready_leader + akb * 8);
+            }
+            if (valid) {
+              sq.issue(lane, ig, &mH, col, wrow);  // H gate columns
+              const int iu = sq.acquire(lane);
+              const uint32_t bu = sq.addr(iu);
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int q8 = 0; q8 < 4; ++q8)
+                  ptx::st_shared_v4(bu + swz(lane, 4 * h + q8), pu[h][4 * q8], pu[h][4 * q8 + 1], pu[h][4 * q8 + 2],
+                                    pu[h][4 * q8 + 3]);
+              sq.issue(lane, iu, &mH, n + col, wrow);  // H up columns
+            }
           }
         } else if (valid) {
-          // ---- D job: Y[:, BND i .. ] = gate * acc, bf16, TMA store (loads one 64-col chunk ahead)
+          // ---- D job: Y[:, BND i .. ] = gate * acc, bf16, TMA store; chunks j = half, half + EPH, ..
           const int di = job - NU;
           constexpr int NCH = BND / 64;
-          uint32_t r[2][2][32];
-          ptx::tmem_ld32(t_acc, r[0][0]);
-          ptx::tmem_ld32(t_acc + 32, r[0][1]);
-          ptx::tmem_ld_wait();
-          ptx::tmem_regs_ready(r[0][0]);
-          ptx::tmem_regs_ready(r[0][1]);
-#pragma unroll
-          for (int j = 0; j < NCH; ++j) {
-            const int sl = j & 1;
-            if (j + 1 < NCH) {
-              ptx::tmem_ld32(t_acc + 64 * (j + 1), r[sl ^ 1][0]);
-              ptx::tmem_ld32(t_acc + 64 * (j + 1) + 32, r[sl ^ 1][1]);
-            }
+#pragma unroll 1
+          for (int j = half; j < NCH; j += EPH) {
+            uint32_t r[2][32];
+            ptx::tmem_ld32(t_acc + 64 * j, r[0]);
+            ptx::tmem_ld32(t_acc + 64 * j + 32, r[1]);
             const int i = sq.acquire(lane);
             const uint32_t b = sq.addr(i);
+            ptx::tmem_ld_wait();
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
               for (int q8 = 0; q8 < 4; ++q8) {
-                const uint32_t* v = r[sl][h] + 8 * q8;
+                const uint32_t* v = r[h] + 8 * q8;
                 ptx::st_shared_v4(b + swz(lane, 4 * h + q8),
                                   ptx::pack_bf16(gate * __uint_as_float(v[0]), gate * __uint_as_float(v[1])),
                                   ptx::pack_bf16(gate * __uint_as_float(v[2]), gate * __uint_as_float(v[3])),
@@ -372,11 +453,6 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
                                   ptx::pack_bf16(gate * __uint_as_float(v[6]), gate * __uint_as_float(v[7])));
               }
             sq.issue(lane, i, &mY, di * BND + 64 * j, wrow);
-            if (j + 1 < NCH) {
-              ptx::tmem_ld_wait();
-              ptx::tmem_regs_ready(r[sl ^ 1][0]);
-              ptx::tmem_regs_ready(r[sl ^ 1][1]);
-            }
           }
         }
         ptx::tc_fence_before();
@@ -385,12 +461,22 @@ __global__ void __launch_bounds__(UpDownCfg<NU, BND>::THREADS, 1)
           if (leader) ptx::mbar_arrive(&tempty[acc]);
           else ptx::mbar_arrive_cluster(tempty_leader + acc * 8);
         }
+#ifdef SONIC_TIMING
+        e_busy[job < NU ? 0 : 1] += clock64() - eb;
+#endif
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
     }
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
+#ifdef SONIC_TIMING
+    if (args.dbg && lane == 0 && ew == 0 && leader) {
+      atomicAdd(args.dbg + 9, e_wait);
+      atomicAdd(args.dbg + 10, e_busy[0]);
+      atomicAdd(args.dbg + 11, e_busy[1]);
+    }
+#endif
   }
 
   ptx::tc_fence_before();

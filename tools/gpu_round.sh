@@ -1,7 +1,5 @@
 set -x
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
-python -c "import os;print(os.cpu_count())"
-timeout 2400 python -m pytest tests -m gpu -x -q -rA --durations=25 > gpurun_out/r2a_pytest.log 2>&1; echo "pytest rc=$?"
-tail -5 gpurun_out/r2a_pytest.log
-timeout 600 python bench.py --steps 20 --warmup 5 --sustain-s 5 > gpurun_out/r2a_bench.json 2> gpurun_out/r2a_bench.err; echo "bench rc=$?"
-tail -c 3000 gpurun_out/r2a_bench.json
+timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "fused or tiny or multi or n256 or 7b_dims" 2>&1 | tail -3
+SONIC_LIB=$PWD/exp_libs/timing.so timeout 300 python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline 2>&1 | grep "TIMING updown" | tail -2
+LIBS="epw4 nopf base" REPS=2 STEPS=30 SHOW="^value|^updown|^up |^down" bash tools/ab.sh
+BENCH_ARGS="--no-fuse" LIBS="base" REPS=2 STEPS=30 SHOW="^value|^updown|^up |^down" bash tools/ab.sh
