@@ -136,11 +136,38 @@ def check_routing(g, rto):
     assert np.allclose(g["row_gate"], rto.row_gate, rtol=2e-6, atol=1e-7), "row_gate"
 
 
-def run_gpu(desc, inp, want_ws=True):
-    """route + fwd + bwd through the C ABI; returns torch tensors (on device)."""
-    rt = sonic.sonic_route(desc, inp.S)
-    O, H, wsf = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
-    dX, dW1, dW2, dS, wsb = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+def _poisoned(shape, dtype):
+    """A buffer whose every byte is 0xFF: NaN as bf16 / fp32, -1 as int32."""
+    t = torch.empty(shape, dtype=dtype, device="cuda")
+    t.view(torch.uint8).fill_(0xFF)
+    return t
+
+
+def run_gpu(desc, inp, want_ws=True, poison=False):
+    """route + fwd + bwd through the C ABI; returns torch tensors (on device).
+
+    poison: every output, routing and workspace buffer starts as 0xFF bytes (NaN / -1), so a kernel
+    that read a location its producer never wrote would turn the compared outputs NaN (the check the
+    sanitizer's initcheck cannot make across TMA bulk stores)."""
+    if poison:
+        T, d, n, E = desc.T, desc.d, desc.n, desc.E
+        rows = sonic.sonic_rows_max(desc)
+        rt = sonic.alloc_routing(desc, "cuda")
+        for t in rt.tensors.values():
+            t.view(torch.uint8).fill_(0xFF)
+        u8 = torch.uint8
+        rt = sonic.sonic_route(desc, inp.S, rt, _poisoned(max(256, sonic.sonic_route_workspace_size(desc)), u8))
+        H = _poisoned((rows, 2 * n), torch.bfloat16)
+        O, H, wsf = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt, _poisoned((T, d), torch.bfloat16), H,
+                                        _poisoned(max(256, sonic.sonic_fwd_workspace_size(desc)), u8))
+        dX, dW1, dW2, dS, wsb = sonic.sonic_moe_bwd(
+            desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt, _poisoned((T, d), torch.bfloat16),
+            _poisoned((E, d, 2 * n), torch.float32), _poisoned((E, n, d), torch.float32),
+            _poisoned((rows,), torch.float32), _poisoned(max(256, sonic.sonic_bwd_workspace_size(desc)), u8))
+    else:
+        rt = sonic.sonic_route(desc, inp.S)
+        O, H, wsf = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
+        dX, dW1, dW2, dS, wsb = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
     torch.cuda.synchronize()
     out = dict(rt=rt, O=O, H=H, dX=dX, dW1=dW1, dW2=dW2, dS=dS)
     if want_ws:
@@ -220,9 +247,9 @@ def stream_parity(desc, inp, g, rto, check_ws=True):
     return stats
 
 
-def full_parity(desc, inp, mode="tc", check_ws=True, rounding="nrf"):
+def full_parity(desc, inp, mode="tc", check_ws=True, rounding="nrf", poison=False):
     """Routing bit-exact in full, then every value output element by element (stream_parity)."""
-    g = run_gpu(desc, inp, want_ws=check_ws)
+    g = run_gpu(desc, inp, want_ws=check_ws, poison=poison)
     S = inp.S.cpu().numpy()
     rto = om.route(S, desc.K, mode=mode, m_tile=desc.m_tile,
                    rescue=not (desc.flags & sonic.SONIC_F_NO_ORPHAN_RESCUE),

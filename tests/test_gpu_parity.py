@@ -249,3 +249,26 @@ def test_fused_updown_equals_two_kernels(shape, mode):
     assert torch.equal(Hf[:R_pad], Hu[:R_pad])
     assert torch.equal(Of, Ou)
     full_parity(d_u, inp, mode=mode)
+
+
+POISON = [
+    # every GEMM template instance (1-CTA and 2-CTA kinds, fused and unfused up/down, the dH ring and
+    # dS partials), TC and TR, with pad rows, half pairs and empty experts
+    ("tiny_tc", 256, 64, 32, 8, 2, "tc", 0),
+    ("ragged_tc", 1000, 128, 64, 16, 4, "tc", 0),
+    ("multi_tr", 2048, 256, 128, 16, 4, "tr", 0),
+    ("n256_half_pairs", 512, 256, 256, 64, 8, "tc", 0),
+    ("n256_unfused", 512, 256, 256, 64, 8, "tc", sonic.SONIC_F_NO_FUSED_UPDOWN),
+    ("wide_n_tr", 1024, 256, 384, 8, 2, "tr", 0),
+]
+
+
+@pytest.mark.parametrize("case", POISON, ids=[c[0] for c in POISON])
+def test_poisoned_buffers(case):
+    """Outputs, routing and workspaces start as NaN / -1 bytes: parity (which rejects NaN) holds, so no
+    kernel reads a location that its producer did not write -- including rows written by TMA bulk
+    stores, which compute-sanitizer's initcheck does not track (sanitizers)."""
+    name, T, d, n, E, K, mode, flags = case
+    inp = make_inputs(T, d, n, E, K, seed=5, device="cuda")
+    m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
+    full_parity(sonic.make_desc(T, d, n, E, K, mode=m, flags=flags), inp, mode=mode, poison=True)
