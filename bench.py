@@ -75,31 +75,14 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4):
         "route": dict(flops=0, paper=T * E * 4 + T * K * 8 + R * 12, tight=T * E * 4 + T * K * 8 + R * 12),
         "dS_reduce": dict(flops=0, paper=R * 8, tight=R * 8),
     }
-    # bytes written (part of the totals above): HBM writes alone run at ~3.9 TB/s on B200, well
-    # below the copy rate, so a store-heavy kernel is also bounded by write_bytes / write bandwidth
+    # bytes written (part of the totals above; reported, not a separate bound: write-only HBM traffic
+    # reaches 6.2-7.0 TB/s on B200 with 16/32-byte or TMA stores, tools/hbm_write_probe.cu)
     writes = {"up": R * 2 * n * b + R * n * b, "down": R * d * b, "updown": R * 2 * n * b + R * d * b, "agg_O": T * d * b,
               "dH": R * 2 * n * b + R * n * b + R * 4, "dW2": E * n * d * dw, "dXt": R * d * b,
               "dW1": E * d * 2 * n * dw, "agg_dX": T * d * b, "route": T * K * 8 + R * 12, "dS_reduce": R * 4}
     for k, w in writes.items():
         m[k]["write"] = w
     return m
-
-
-def measure_write_gbs(dev):
-    """HBM write-only bandwidth of this device, measured now: a 1 GiB memset, best of 10 (+1 warm-up)."""
-    import torch
-    buf = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
-    best = None
-    for _ in range(11):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        buf.zero_()
-        e1.record()
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1)
-        best = t if best is None else min(best, t)
-    del buf
-    return (1 << 30) / (best * 1e-3) / 1e9
 
 
 # --------------------------------------------------------------------------- clocks
@@ -219,7 +202,7 @@ def workload_config(args, cfg):
             **({"ep_exchange": "peer-memory kernels (CUDA IPC)" if args.comm == "peer" else "NCCL all-to-all-v"}
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
-            **({"updown": "two kernels (SONIC_F_NO_FUSED_UPDOWN)"} if getattr(args, "no_fuse", False) else {}),
+            **({"updown": "fused kernel (SONIC_F_FUSED_UPDOWN)"} if getattr(args, "fuse", False) else {}),
             **({"m_tile": args.m_tile} if getattr(args, "m_tile", 128) != 128 else {}),
             "l2": ("flushed before every timed step (memset of 2x L2 outside the step's event pair); warm "
                    "back-to-back number in `warm`") if getattr(args, "l2_flush", False) else
@@ -247,8 +230,8 @@ def main():
     ap.add_argument("--m-tile", type=int, default=128, choices=[128, 256],
                     help="token-rounding tile (256 = the 2-CTA pair's M tile: no half-empty pairs)")
     ap.add_argument("--dw-bf16", action="store_true", help="SONIC_F_DW_BF16: weight gradients stored as bf16")
-    ap.add_argument("--no-fuse", action="store_true",
-                    help="SONIC_F_NO_FUSED_UPDOWN: separate up- and down-projection kernels (A through HBM)")
+    ap.add_argument("--fuse", action="store_true",
+                    help="SONIC_F_FUSED_UPDOWN: the fused up/down kernel (A kept on chip) instead of two kernels")
     ap.add_argument("--no-l2-flush", dest="l2_flush", action="store_false",
                     help="time the K steps back to back without flushing L2 (the primary number flushes)")
     ap.add_argument("--sustain-s", type=float, default=0.0,
@@ -306,7 +289,7 @@ def main():
     mode = ROUTE_MODES[args.mode][0]
     desc = sonic.make_desc(T, d, n, E, K, mode=mode, m_tile=args.m_tile,
                            flags=(sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0) |
-                           (sonic.SONIC_F_NO_FUSED_UPDOWN if args.no_fuse else 0))
+                           (sonic.SONIC_F_FUSED_UPDOWN if args.fuse else 0))
     use_ep = args.ep or world > 1
     if not use_ep:
         # ---- one GPU, all experts local: route + fwd + bwd through the C ABI
@@ -369,10 +352,6 @@ def main():
                 return kernel_model(1, d, n, L, L, 0, 0)
             lrt = rk.ctx["lrt"]
             return kernel_model(R_in, d, n, L, L, int(lrt.offsets[L].item()), int(lrt.pad_offsets[L].item()))
-
-    # HBM write-only bandwidth, measured before any step runs (a power-capped GPU after the timed
-    # region measures low); best of 10 memsets of 1 GiB
-    wr_gbs = measure_write_gbs(dev)
 
     def step():
         run(X, S, dOin)
@@ -479,22 +458,17 @@ def main():
     tf_sus = peaks["bf16_tflops_sustained"]
     peak_choice = "bf16_tflops (burst): K-step timed region; frac_vs_sustained uses bf16_tflops_sustained"
     bw_peak = peaks["hbm_gbs"]
-    peaks["hbm_write_gbs"] = wr_peak = wr_gbs
-    peaks["hbm_write_source"] = "measured in this run before the warm-up (1 GiB memset, best of 10); label only"
     kernels = {}
     for name, (tot, cnt) in agg.items():
         avg = tot / cnt
         mm = model.get(name, dict(flops=0, paper=0, tight=0, write=0))
         t_tensor = mm["flops"] / (tf_peak * 1e12) * 1e3
         t_hbm = mm["paper"] / (bw_peak * 1e9) * 1e3  # all algorithmic bytes at the measured copy rate
-        t_write = mm.get("write", 0) / (wr_peak * 1e9) * 1e3
         kernels[name] = dict(avg_ms=avg, launches_per_step=cnt / args.steps, share=tot / ms_p if ms_p else None,
                              tflops=mm["flops"] / (avg * 1e-3) / 1e12 if mm["flops"] else 0.0,
                              gbs_paper=mm["paper"] / (avg * 1e-3) / 1e9, gbs_tight=mm["tight"] / (avg * 1e-3) / 1e9,
                              bound="tensor" if t_tensor >= t_hbm else "hbm",
-                             roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None,
-                             # label only, not a roofline: the written bytes at this run's memset rate
-                             write_aware_ms=max(t_tensor, t_hbm, t_write))
+                             roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None)
     dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"]) if kernels else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -636,8 +610,7 @@ def main():
                            "note": "per-kernel events on (sonic_profile_enable); kernels/roofline come from it"},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": gpu_launches,
         "clocks": clk, "kernels": kernels, "exchange": exchange, "peaks": {k: peaks.get(k) for k in ("hbm_gbs", "bf16_tflops",
-                                                                                "bf16_tflops_sustained", "source",
-                                                                                "hbm_write_gbs", "hbm_write_source")},
+                                                                                "bf16_tflops_sustained", "source")},
     }
     if args.breakdown:
         json.dump(line, open(args.breakdown, "w"), indent=1)

@@ -86,10 +86,12 @@ typedef enum {
 #define SONIC_F_DW_BF16         32  /* sonic_moe_bwd: dW1 / dW2 are written as bf16 (the float* arguments point
                                        at bf16 [E,d,2n] / [E,n,d] buffers): half the weight-gradient store
                                        traffic; fp32 accumulation as always.  Not with SONIC_F_DW_ACCUMULATE. */
-#define SONIC_F_NO_FUSED_UPDOWN 64  /* sonic_moe_fwd: run the up- and down-projection as two kernels with A in
-                                       the workspace (the fused kernel, NEXT-1, is used whenever n is 128 or
-                                       256 and d % 128 == 0; sonic_fwd_workspace_size then holds Y only).
-                                       Used for A/B measurement and to test both paths. */
+#define SONIC_F_NO_FUSED_UPDOWN 64  /* sonic_moe_fwd: force the up- and down-projection to run as two kernels
+                                       with A in the workspace (the default). */
+#define SONIC_F_FUSED_UPDOWN   128  /* sonic_moe_fwd: the fused up/down kernel (NEXT-1: A = SwiGLU(H) stays in
+                                       shared memory, never written to HBM) where n is 128 or 256 and
+                                       d % 128 == 0; sonic_fwd_workspace_size then holds Y only.  Opt-in:
+                                       measured slower than the two kernels at 7B. */
 #define SONIC_F_DW_ACCUMULATE    4  /* sonic_moe_bwd: dW1 += ..., dW2 += ... (fp32 element-wise adds done by
                                        the TMA store unit; one add per element per call, so deterministic)
                                        instead of overwriting -- gradient accumulation over microbatches */

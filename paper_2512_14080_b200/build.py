@@ -6,7 +6,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRCS = ["csrc/sonic_api.cu", "csrc/route.cu", "csrc/aggregate.cu", "csrc/ep.cu", "csrc/peer.cu"]
-DEPS = SRCS + ["csrc/gemm.cuh", "csrc/ptx.cuh", "csrc/sonic_internal.h", "../include/sonic.h"]
+DEPS = SRCS + ["csrc/gemm.cuh", "csrc/updown.cuh", "csrc/ptx.cuh", "csrc/sonic_internal.h", "../include/sonic.h"]
 OUT = os.path.join(HERE, "libsonic.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-shared",

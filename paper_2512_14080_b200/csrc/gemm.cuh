@@ -151,7 +151,9 @@ __device__ __forceinline__ int total_tiles_of(const GemmArgs& a) {
   else return (CTA2 ? *a.num_pairs : *a.num_m_tiles) * a.n_tiles;
 }
 
-template <int KIND, bool CTA2>
+// MFAST (varlen-K under MC, the dW1 order): the M-pair index runs fastest, so tiles 2k and 2k+1
+// -- the two pairs of a 4-CTA cluster -- share the expert and the N tile (and so the B operand)
+template <int KIND, bool CTA2, bool MFAST = false>
 __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, int rank) {
   TileCoord c;
   c.valid = true;
@@ -160,8 +162,14 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, in
     const int per_e = mts * a.n_tiles;
     c.e = tile / per_e;
     const int rem = tile - c.e * per_e;
-    const int mp = rem / a.n_tiles;
-    c.nt = rem - mp * a.n_tiles;
+    int mp;
+    if constexpr (MFAST) {
+      c.nt = rem / mts;
+      mp = rem - c.nt * mts;
+    } else {
+      mp = rem / a.n_tiles;
+      c.nt = rem - mp * a.n_tiles;
+    }
     c.mt = CTA2 ? 2 * mp + rank : mp;
     if (CTA2) c.valid = c.mt < a.m_tiles;
     c.seg0 = __ldg(a.pad_offsets + c.e);
@@ -290,7 +298,13 @@ __device__ __forceinline__ void tload3(void* dst, const CUtensorMap* m, uint64_t
   else ptx::tma_load_3d(dst, m, bar, c0, c1, c2);
 }
 
-template <int KIND, int BN, bool CTA2>
+// MC (CTA2 only): a cluster of FOUR CTAs = two pairs.  The static schedule gives the two pairs the
+// consecutive pair tiles 2k and 2k+1, which share one operand (DOWN, DXT, DW2: the A tile -- same
+// rows, the next N tile; DW1 with the MFAST order: the B tile -- same expert and N tile, the next M
+// pair).  Each pair TMA-loads half of the shared tile and multicasts it into both pairs' stage, so
+// the L2 -> SM operand traffic per MMA drops by a quarter; a stage is refilled once BOTH pairs' MMAs
+// have released it (empty barriers count the two pair leaders' commits).
+template <int KIND, int BN, bool CTA2, bool MC = false>
 __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     sonic_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
                       const __grid_constant__ CUtensorMap mC0, const __grid_constant__ CUtensorMap mC1,
@@ -323,7 +337,15 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int rank = CTA2 ? (int)ptx::cluster_ctarank() : 0;
+  static_assert(!MC || CTA2, "multicast clusters are built from 2-CTA pairs");
+  constexpr bool MFAST = MC && KIND == K_DW1;
+  const int crank = CTA2 ? (int)ptx::cluster_ctarank() : 0;
+  const int rank = crank & 1;                                  // rank within the pair
+  const int pidx = MC ? crank >> 1 : 0;                        // pair within the cluster
+  const uint32_t lead = (uint32_t)(crank & ~1);                // this pair's leader (cluster rank)
+  const uint16_t pmask = (uint16_t)(0x3u << (2 * pidx));      // this pair's two CTAs
+  const uint16_t smask = (uint16_t)((1u << rank) | (1u << (2 + rank)));  // MC: same-rank CTAs of both pairs
+  (void)smask;
   const bool leader = rank == 0;
   const int t_first = CTA2 ? blockIdx.x / 2 : blockIdx.x;
   const int t_step = CTA2 ? gridDim.x / 2 : gridDim.x;
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     const int full_cnt = GATHER ? (leader ? NP * 32 + 1 + (CTA2 ? 1 : 0) : NP * 32) : 1;
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], full_cnt);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], MC ? 2 : 1);
     }
     for (int s = 0; s < 2; ++s) {
       ptx::mbar_init(&tfull[s], 1);
@@ -371,7 +393,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     if constexpr (!GATHER) {
       if (lane == 0) {
         for (int tile = t_first; tile < total_tiles; tile += t_step) {
-          const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
+          const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);
           const int n0 = tc.nt * BN + rank * BNL;  // this CTA's B columns (rows)
           for (int kb = 0; kb < tc.nkb; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -379,7 +401,10 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             uint8_t* sB = sA + A_BYTES;
             uint64_t* bar = &full[stage];
             if (leader) ptx::mbar_arrive_expect_tx(bar, STAGE_BYTES * (CTA2 ? 2 : 1));
-            tload2<CTA2>(sA, &mA, bar, kb * GEMM_BK, tc.row0);
+            if constexpr (MC)  // half of the shared A tile (64 rows, box map mD) into both pairs
+              ptx::tma_load_2d_cg2_mc(sA + pidx * 8192, &mD, bar, kb * GEMM_BK, tc.row0 + 64 * pidx, smask);
+            else
+              tload2<CTA2>(sA, &mA, bar, kb * GEMM_BK, tc.row0);
             if constexpr (KIND == K_DOWN) {
 #pragma unroll
               for (int j = 0; j < BNL / 64; ++j) tload3<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, kb * GEMM_BK, tc.e);
@@ -411,20 +436,20 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       int ktok[KPD][4];
       if constexpr (!Tr::vk) {
         if (t_first < total_tiles) {
-          const TileCoord t0 = decode_tile<KIND, CTA2>(args, t_first, rank);
+          const TileCoord t0 = decode_tile<KIND, CTA2, MFAST>(args, t_first, rank);
 #pragma unroll
           for (int j = 0; j < 8; ++j) ntok[j] = t0.valid ? tok_of(args.row_token, t0.row0 + r0 + 16 * j) : 0;
         }
       }
       for (int tile = t_first; tile < total_tiles; tile += t_step) {
-        const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
+        const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);
         const int n0 = tc.nt * BN + rank * BNL;
         const __nv_bfloat16* srcM[8];
         if constexpr (!Tr::vk) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) srcM[j] = args.gsrc + clamp_tok(ntok[j]) * args.gld + c * 8;
           if (tile + t_step < total_tiles) {
-            const TileCoord tn = decode_tile<KIND, CTA2>(args, tile + t_step, rank);
+            const TileCoord tn = decode_tile<KIND, CTA2, MFAST>(args, tile + t_step, rank);
 #pragma unroll
             for (int j = 0; j < 8; ++j) ntok[j] = tn.valid ? tok_of(args.row_token, tn.row0 + r0 + 16 * j) : 0;
           }
@@ -493,12 +518,21 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             } else if constexpr (KIND == K_DW2) {  // A' tile (MN-major): 64 rows x 128 M columns
               const int krow0 = tc.seg0 + kb * GEMM_BK;
               const int m0 = tc.valid ? tc.mt * GEMM_BM : 0;
-              tload2<CTA2>(sA, &mA, bar, m0, krow0);
-              tload2<CTA2>(sA + 8192, &mA, bar, m0 + 64, krow0);
+              if constexpr (MC) {  // one of the two 64-column boxes, into both pairs
+                ptx::tma_load_2d_cg2_mc(sA + 8192 * pidx, &mA, bar, m0 + 64 * pidx, krow0, smask);
+              } else {
+                tload2<CTA2>(sA, &mA, bar, m0, krow0);
+                tload2<CTA2>(sA + 8192, &mA, bar, m0 + 64, krow0);
+              }
             } else {  // DW1: dH tile (MN-major): 64 rows x BNL columns
               const int krow0 = tc.seg0 + kb * GEMM_BK;
+              if constexpr (MC) {  // MFAST: both pairs hold the same B columns; one box each, into both
+                static_assert(!MC || BNL == 128, "DW1 multicast splits the B half into two 64-column boxes");
+                ptx::tma_load_2d_cg2_mc(sB + 8192 * pidx, &mB, bar, n0 + 64 * pidx, krow0, smask);
+              } else {
 #pragma unroll
-              for (int j = 0; j < BNL / 64; ++j) tload2<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, krow0);
+                for (int j = 0; j < BNL / 64; ++j) tload2<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, krow0);
+              }
             }
           }
           if constexpr (!Tr::vk) {  // A: 128 gathered rows x 64 K (K-major)
@@ -540,7 +574,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       unsigned long long c_te = 0, c_full = 0, c0 = clock64();
 #endif
       for (int tile = t_first; tile < total_tiles; tile += t_step) {
-        const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, 0);
+        const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, 0);
 #ifdef SONIC_TIMING
         unsigned long long ca = clock64();
 #endif
@@ -574,14 +608,14 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             if constexpr (CTA2) ptx::mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
             else ptx::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          if constexpr (CTA2) ptx::mma_commit_mc(&empty[stage], 0x3);
+          if constexpr (CTA2) ptx::mma_commit_mc(&empty[stage], MC ? (uint16_t)0xF : pmask);
           else ptx::mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        if constexpr (CTA2) ptx::mma_commit_mc(&tfull[acc], 0x3);
+        if constexpr (CTA2) ptx::mma_commit_mc(&tfull[acc], pmask);
         else ptx::mma_commit(&tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
@@ -599,11 +633,11 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = t_first; tile < total_tiles; tile += t_step) {
-        const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
+        const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);
         for (int kb = 0; kb < tc.nkb; ++kb) {
           ptx::mbar_wait(&full[stage], phase);
           ptx::fence_proxy_async_smem();
-          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[stage]), 0));
+          ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&full[stage]), lead));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -620,7 +654,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     StoreQ<Cfg::NB> sq{stg + ew * Cfg::NB * STG_BYTES, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    const uint32_t tempty_leader = CTA2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), 0) : 0u;
+    const uint32_t tempty_leader = CTA2 ? ptx::mapa(ptx::smem_u32(&tempty[0]), lead) : 0u;
     // DH: each epilogue warp TMA-loads its own 32 rows of H (BN gate + BN up columns) for its
     // next tile into a private buffer; dH is computed in place there and TMA-stored from it.
     uint8_t* hb = hbuf + ew * Cfg::HBUF_WARP;
@@ -628,7 +662,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     auto h_issue = [&](int t) {
       if constexpr (HTMA) {
         if (lane == 0) {
-          const TileCoord th = decode_tile<KIND, CTA2>(args, t, rank);
+          const TileCoord th = decode_tile<KIND, CTA2, MFAST>(args, t, rank);
           if constexpr (BN >= 64) {
             // this warp's chunks c = half, half + Cfg::EPH, ... (local index lc): gate box at
             // lc * 4 KB, up box at (NLC + lc) * 4 KB
@@ -668,7 +702,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       if constexpr (HRING) {
         if (hr_tile >= total_tiles) return;
         if (lane == 0) {
-          const TileCoord th = decode_tile<KIND, CTA2>(args, hr_tile, rank);
+          const TileCoord th = decode_tile<KIND, CTA2, MFAST>(args, hr_tile, rank);
           uint64_t* b = &hfull[2 * ew + slot];
           uint8_t* dst = hb + slot * 2 * STG_BYTES;
           if (th.valid) {
@@ -700,7 +734,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     unsigned long long c_tf = 0, c_epi = 0;
 #endif
     for (int tile = t_first; tile < total_tiles; tile += t_step) {
-      const TileCoord tc = decode_tile<KIND, CTA2>(args, tile, rank);
+      const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);
       const int wrow = tc.row0 + 32 * q;  // first grouped row of this warp's slab
       const int row = wrow + lane;        // this thread's grouped row (varlen-M)
       const bool has_next = tile + t_step < total_tiles;

@@ -297,6 +297,16 @@ __device__ __forceinline__ void tma_load_3d_cg2(void* dst, const CUtensorMap* ma
       "l"(map), "r"(leader_bar(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// Pair-form TMA load multicast to every CTA in `mask` (same smem offset in each); the bytes are
+// counted on the mbarrier at the same offset in each destination CTA's pair leader.
+__device__ __forceinline__ void tma_load_2d_cg2_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                   uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(leader_bar(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)

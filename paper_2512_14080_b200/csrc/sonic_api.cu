@@ -141,11 +141,11 @@ int num_sms() {
 }
 
 // ---------------------------------------------------------------- GEMM launch
-template <int KIND, int BN, bool CTA2>
+template <int KIND, int BN, bool CTA2, bool MC = false>
 bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
                    const CUtensorMap& dmap, const GemmArgs& args, int grid, cudaStream_t st) {
   using Cfg = KCfg<KIND, BN, CTA2>;
-  auto kern = sonic_gemm_kernel<KIND, BN, CTA2>;
+  auto kern = sonic_gemm_kernel<KIND, BN, CTA2, MC>;
   static bool attr[64] = {};  // function attributes are per device (context)
   int dev = 0;
   cudaGetDevice(&dev);
@@ -161,13 +161,25 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   cfg.stream = st;
   cudaLaunchAttribute attrs[2];
   attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = CTA2 ? 2 : 1;
+  attrs[0].val.clusterDim.x = MC ? 4 : CTA2 ? 2 : 1;
   attrs[0].val.clusterDim.y = 1;
   attrs[0].val.clusterDim.z = 1;
   attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attrs[1].val.programmaticStreamSerializationAllowed = SONIC_PDL ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = 2;
+  if constexpr (MC) {
+    // 4-CTA clusters must fit in a GPC: launch at most as many as can be co-resident (a multiple
+    // of 4 CTAs: the two pairs of a cluster run the same number of pair tiles)
+    static int max_cl[64] = {};
+    if (!max_cl[dev & 63]) {
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) != cudaSuccess || ncl <= 0) ncl = grid / 4;
+      max_cl[dev & 63] = std::max(1, ncl);
+    }
+    grid = std::max(4, std::min(grid & ~3, 4 * max_cl[dev & 63]));
+    cfg.gridDim = dim3(grid);
+  }
 #ifdef SONIC_TIMING
   static unsigned long long* dbg = nullptr;
   if (!dbg) cudaMalloc(&dbg, 16 * sizeof(unsigned long long));
@@ -199,13 +211,22 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
 #endif
 bool use_cta2(int BN) { return SONIC_CTA2 && BN >= 128; }
 
-// dmap: auxiliary tensor map (DH: the H cache, box {64, 32}); ignored by the other kinds.
+// 4-CTA multicast clusters (MC, gemm.cuh) for DOWN / DXT / DW2 / DW1 at BN = 256 when the shared
+// operand's partner tiles exist (an even tile count along the sharing dimension).  SONIC_MC4=0: pairs only.
+#ifndef SONIC_MC4
+#define SONIC_MC4 0  // measured slower at 7B (dXt 331 -> 354 us, dW1 376 -> 387, dW2 217 -> 226): DESIGN.md 6.8
+#endif
+// dmap: auxiliary tensor map (DH: the H cache, box {64, 32}; DOWN / DXT with mc: the A operand with
+// a 64-row box, the half tile each pair multicasts); ignored by the other kinds.
 template <int KIND>
 bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c0, const CUtensorMap& c1,
-                 const GemmArgs& args, int grid, cudaStream_t st, const CUtensorMap* dmap = nullptr) {
+                 const GemmArgs& args, int grid, cudaStream_t st, const CUtensorMap* dmap = nullptr, bool mc = false) {
   const CUtensorMap& d = dmap ? *dmap : c0;
   const bool cta2 = use_cta2(BN);
   if (cta2) grid = std::max(2, grid & ~1);  // a pair needs both CTAs, even for a single pair tile
+  if constexpr (KIND == K_DOWN || KIND == K_DXT || KIND == K_DW2 || KIND == K_DW1) {
+    if (SONIC_MC4 && mc && cta2 && BN == 256) return launch_gemm_t<KIND, 256, true, true>(a, b, c0, c1, d, args, grid, st);
+  }
   switch (BN) {
     case 256:
       return cta2 ? launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st)
@@ -363,12 +384,14 @@ int dh_bn(int n) {
 }
 
 #ifndef SONIC_FUSED_UPDOWN
-#define SONIC_FUSED_UPDOWN 1  // NEXT-1: up -> down fused (updown.cuh) where the shape allows it
+#define SONIC_FUSED_UPDOWN 0  // NEXT-1 fused up/down (updown.cuh): opt-in per call (SONIC_F_FUSED_UPDOWN);
+                              // measured slower than the two kernels at 7B
 #endif
 // The fused up/down kernel holds a CTA's 128 rows of A (128 x n bf16) in shared memory: n = 128 or
 // 256 (with 3+ operand stages); d a multiple of 128 (D jobs of 256 or 128 columns).
 bool fused_updown(const sonic_moe_desc* D) {
-  return SONIC_FUSED_UPDOWN && !(D->flags & SONIC_F_NO_FUSED_UPDOWN) && use_cta2(256) && (D->n == 128 || D->n == 256) &&
+  return (SONIC_FUSED_UPDOWN || (D->flags & SONIC_F_FUSED_UPDOWN)) && !(D->flags & SONIC_F_NO_FUSED_UPDOWN) &&
+         use_cta2(256) && (D->n == 128 || D->n == 256) &&
          D->d % 128 == 0;
 }
 
@@ -615,15 +638,16 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
   }
   // K2 down-proj: Y = gate * (A W2_e)
   if (!w.fused) {
-    CUtensorMap mA, mB, mC0;
+    CUtensorMap mA, mB, mC0, mA64;
     const int BN = pick_bn(d);
     if (!map2d(&mA, Abuf, false, R, n, 64, 128) || !map3d(&mB, W2, false, E, n, d, 64, 64) ||
-        !map2d(&mC0, Ybuf, false, R, d, 64, 32))
+        !map2d(&mC0, Ybuf, false, R, d, 64, 32) || !map2d(&mA64, Abuf, false, R, n, 64, 64))
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = d / BN; a.k_blocks = (n + 63) / 64; a.N_dim = d;
     ProfScope ps("down", st);
-    if (!launch_gemm<K_DOWN>(BN, mA, mB, mC0, mC0, a, grid, st)) return SONIC_ERR_CUDA;
+    // multicast cluster: the pair tiles (m, 2j) and (m, 2j+1) share the A rows
+    if (!launch_gemm<K_DOWN>(BN, mA, mB, mC0, mC0, a, grid, st, &mA64, a.n_tiles % 2 == 0)) return SONIC_ERR_CUDA;
   }
   // K3 aggregation: O_t = sum of the token's Y rows
   ProfScope ps("agg_O", st);
@@ -703,12 +727,12 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     cudaEventRecord(ss.fork, st);
     cudaStreamWaitEvent(ss.s, ss.fork, 0);
   }
-  CUtensorMap mA6, mB6, mC6, mA5, mB5, mC5, mA7, mB7, mC7;
+  CUtensorMap mA6, mB6, mC6, mA5, mB5, mC5, mA7, mB7, mC7, mA6h;
   GemmArgs a6 = g, a5 = g, a7 = g;
   const int BN6 = pick_bn(d), BN5 = pick_bn(d), BN7 = pick_bn(2 * n);
   // K6 dX~_e = dH_e W1_e^T
   if (!map2d(&mA6, dH, false, R, 2 * n, 64, 128) || !map3d(&mB6, W1, false, E, d, 2 * n, 64, bnl(BN6)) ||
-      !map2d(&mC6, dXt, false, R, d, 64, 32))
+      !map2d(&mC6, dXt, false, R, d, 64, 32) || !map2d(&mA6h, dH, false, R, 2 * n, 64, 64))
     return SONIC_ERR_CUDA;
   a6.n_tiles = d / BN6; a6.k_blocks = (2 * n) / 64; a6.N_dim = d;
   // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
@@ -733,15 +757,16 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
 
   auto run_dxt = [&]() {
     ProfScope ps("dXt", st);
-    return launch_gemm<K_DXT>(BN6, mA6, mB6, mC6, mC6, a6, grid, st);
+    return launch_gemm<K_DXT>(BN6, mA6, mB6, mC6, mC6, a6, grid, st, &mA6h, a6.n_tiles % 2 == 0);
   };
   auto run_dw2 = [&]() {
     ProfScope ps("dW2", s_dw);
-    return launch_gemm<K_DW2>(BN5, mA5, mB5, mC5, mC5, a5, std::min(grid, tiles5), s_dw);
+    return launch_gemm<K_DW2>(BN5, mA5, mB5, mC5, mC5, a5, std::min(grid, tiles5), s_dw, nullptr, a5.n_tiles % 2 == 0);
   };
   auto run_dw1 = [&]() {
     ProfScope ps("dW1", s_dw);
-    return launch_gemm<K_DW1>(BN7, mA7, mB7, mC7, mC7, a7, std::min(grid, tiles7), s_dw);
+    return launch_gemm<K_DW1>(BN7, mA7, mB7, mC7, mC7, a7, std::min(grid, tiles7), s_dw, nullptr,
+                              ((a7.m_tiles + 1) / 2) % 2 == 0);
   };
   auto run_agg = [&]() {  // K8 dX aggregation
     ProfScope ps("agg_dX", s_agg);

@@ -34,6 +34,7 @@ SONIC_F_BWD_NO_DW = 8
 SONIC_F_BWD_DW_ONLY = 16
 SONIC_F_DW_BF16 = 32
 SONIC_F_NO_FUSED_UPDOWN = 64
+SONIC_F_FUSED_UPDOWN = 128
 GEMM_M = 128
 
 ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",

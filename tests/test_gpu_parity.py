@@ -36,7 +36,8 @@ def test_small_parity(case):
     name, T, d, n, E, K, mode = case
     inp = make_inputs(T, d, n, E, K, seed=1, device="cuda")
     m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
-    desc = sonic.make_desc(T, d, n, E, K, mode=m)
+    # the fused up/down kernel is opt-in (SONIC_F_FUSED_UPDOWN); the fused_* shapes exercise it
+    desc = sonic.make_desc(T, d, n, E, K, mode=m, flags=sonic.SONIC_F_FUSED_UPDOWN if name.startswith("fused") else 0)
     stats = full_parity(desc, inp, mode=mode)
     print(name, {k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
 
@@ -233,13 +234,13 @@ def test_split_backward_matches_monolithic():
                                         ((512, 256, 256, 64, 8), "tc")], ids=["n128", "7b_dims_tr", "half_pairs"])
 def test_fused_updown_equals_two_kernels(shape, mode):
     """NEXT-1: the fused up/down kernel (A kept in shared memory) gives the same H and O as the
-    separate up- and down-projection kernels (SONIC_F_NO_FUSED_UPDOWN) bit for bit: the same MMA
-    shapes and K order, the same bf16 A; and the unfused path stays parity-green at n = 256."""
+    separate up- and down-projection kernels (the default) bit for bit: the same MMA shapes and K
+    order, the same bf16 A; and the fused path is parity-green against the oracle."""
     T, d, n, E, K = shape
     inp = make_inputs(T, d, n, E, K, seed=31, device="cuda")
     m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
-    d_f = sonic.make_desc(T, d, n, E, K, mode=m)
-    d_u = sonic.make_desc(T, d, n, E, K, mode=m, flags=sonic.SONIC_F_NO_FUSED_UPDOWN)
+    d_f = sonic.make_desc(T, d, n, E, K, mode=m, flags=sonic.SONIC_F_FUSED_UPDOWN)
+    d_u = sonic.make_desc(T, d, n, E, K, mode=m)
     assert sonic.sonic_fwd_workspace_size(d_f) < sonic.sonic_fwd_workspace_size(d_u)  # no A in the workspace
     rt = sonic.sonic_route(d_f, inp.S)
     Of, Hf, _ = sonic.sonic_moe_fwd(d_f, inp.X, inp.W1, inp.W2, rt)
@@ -248,7 +249,7 @@ def test_fused_updown_equals_two_kernels(shape, mode):
     R_pad = int(rt.pad_offsets[E])
     assert torch.equal(Hf[:R_pad], Hu[:R_pad])
     assert torch.equal(Of, Ou)
-    full_parity(d_u, inp, mode=mode)
+    full_parity(d_f, inp, mode=mode)
 
 
 POISON = [
@@ -258,7 +259,8 @@ POISON = [
     ("ragged_tc", 1000, 128, 64, 16, 4, "tc", 0),
     ("multi_tr", 2048, 256, 128, 16, 4, "tr", 0),
     ("n256_half_pairs", 512, 256, 256, 64, 8, "tc", 0),
-    ("n256_unfused", 512, 256, 256, 64, 8, "tc", sonic.SONIC_F_NO_FUSED_UPDOWN),
+    ("n256_fused", 512, 256, 256, 64, 8, "tc", sonic.SONIC_F_FUSED_UPDOWN),
+    ("n128_fused_tr", 2048, 256, 128, 16, 4, "tr", sonic.SONIC_F_FUSED_UPDOWN),
     ("wide_n_tr", 1024, 256, 384, 8, 2, "tr", 0),
 ]
 

@@ -22,10 +22,10 @@ CASES = [
     ("tiny_tc n32 (1-CTA kinds, dH BN=32)", 256, 64, 32, 8, 2, R.SONIC_ROUTE_TC, 0),
     ("tiny_tr n32", 256, 64, 32, 8, 2, R.SONIC_ROUTE_TR_NRF, 0),
     ("ragged_tc n64 (BN 128 2-CTA + 64 1-CTA)", 1000, 128, 64, 16, 4, R.SONIC_ROUTE_TC, 0),
-    ("multi_tr n128 (fused up/down NU=1)", 2048, 256, 128, 16, 4, R.SONIC_ROUTE_TR_NRF, 0),
-    ("n256 fused NU=2, dH ring, half pairs", 512, 256, 256, 64, 8, R.SONIC_ROUTE_TC, 0),
-    ("n256 unfused up/down kernels", 512, 256, 256, 64, 8, R.SONIC_ROUTE_TC, R.SONIC_F_NO_FUSED_UPDOWN),
-    ("fused D jobs of 128 columns", 1000, 384, 128, 16, 4, R.SONIC_ROUTE_TC, 0),
+    ("multi_tr n128 (fused up/down NU=1)", 2048, 256, 128, 16, 4, R.SONIC_ROUTE_TR_NRF, R.SONIC_F_FUSED_UPDOWN),
+    ("n256 fused NU=2, dH ring, half pairs", 512, 256, 256, 64, 8, R.SONIC_ROUTE_TC, R.SONIC_F_FUSED_UPDOWN),
+    ("n256 unfused up/down kernels", 512, 256, 256, 64, 8, R.SONIC_ROUTE_TC, 0),
+    ("fused D jobs of 128 columns", 1000, 384, 128, 16, 4, R.SONIC_ROUTE_TC, R.SONIC_F_FUSED_UPDOWN),
     ("wide n384 (dH 3 N-tiles + dS reduce)", 1024, 256, 384, 8, 2, R.SONIC_ROUTE_TC, 0),
     ("bf16 dW", 1000, 192, 384, 8, 2, R.SONIC_ROUTE_TC, R.SONIC_F_DW_BF16),
     ("dW accumulate, empty experts", 64, 128, 64, 64, 2, R.SONIC_ROUTE_TC, R.SONIC_F_DW_ACCUMULATE),
