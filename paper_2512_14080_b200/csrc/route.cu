@@ -919,6 +919,95 @@ __global__ void __launch_bounds__(32 * SONIC_TOPK_TPT) k_topk_g4(const float* __
   for (int e = tid; e < E; e += NT) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
 }
 
+// TC top-K with one warp per token (E % 32 == 0, E <= 32 * EPLMAX; no S^T output): lane l holds
+// experts l, l + 32, ... (coalesced 128-byte loads), keeps its own top min(E/32, KP) keys sorted
+// (key = ordered score << 32 | ~expert: unique, so the order is the exact (S desc, expert asc) order
+// of Q9), then KT rounds of a two-step warp max (redux.sync on the score half, then on the expert
+// half among the lanes holding that score) pop the winners in order.  A block of 8 warps routes 32
+// consecutive tokens, i.e. one word of the per-expert bitmaps.
+template <int KT, int EPLMAX>
+__global__ void __launch_bounds__(256) k_topk_warp(const float* __restrict__ S, int T, int E, int W,
+                                                   int* __restrict__ topk_ids, float* __restrict__ topk_s,
+                                                   uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
+  constexpr int LL = EPLMAX < KP ? EPLMAX : KP;  // lane list length
+  __shared__ uint32_t words[32 * EPLMAX];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int tok0 = blockIdx.x * 32;
+  const int epl = E >> 5;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && ticket) {
+    ticket[0] = 0u;
+    ticket[1] = 0u;
+  }
+  for (int i = threadIdx.x; i < E; i += 256) words[i] = 0u;
+  // the warp's 4 tokens: all loads first (4 x epl in flight per lane)
+  float v[4][EPLMAX];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int t = tok0 + wp + 8 * u;
+#pragma unroll
+    for (int j = 0; j < EPLMAX; ++j)
+      v[u][j] = (t < T && j < epl) ? __ldg(S + (size_t)t * E + 32 * j + lane) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int t = tok0 + wp + 8 * u;
+    if (t >= T) continue;  // (uniform per warp)
+    unsigned long long lst[LL];
+#pragma unroll
+    for (int i = 0; i < LL; ++i) lst[i] = 0ull;
+#pragma unroll
+    for (int j = 0; j < EPLMAX; ++j) {
+      if (j >= epl) break;
+      const unsigned long long k =
+          ((unsigned long long)ord_f32(v[u][j]) << 32) | (0xFFFFFFFFu - (uint32_t)(32 * j + lane));
+      if (k > lst[LL - 1]) {
+#pragma unroll
+        for (int i = LL - 1; i > 0; --i) {
+          const bool gi = k > lst[i], gp = k > lst[i - 1];
+          lst[i] = gi ? (gp ? lst[i - 1] : k) : lst[i];
+        }
+        if (k > lst[0]) lst[0] = k;
+      }
+    }
+    int my_e = 0;
+    uint32_t my_s = 0;
+#pragma unroll
+    for (int r = 0; r < KT; ++r) {
+      const uint32_t hi = (uint32_t)(lst[0] >> 32);
+      const uint32_t m = __reduce_max_sync(0xffffffffu, hi);
+      const uint32_t lo = hi == m ? (uint32_t)lst[0] : 0u;
+      const uint32_t ml = __reduce_max_sync(0xffffffffu, lo);
+      if (hi == m && lo == ml) {  // the winner pops its head
+#pragma unroll
+        for (int i = 0; i < LL - 1; ++i) lst[i] = lst[i + 1];
+        lst[LL - 1] = 0ull;
+      }
+      if (lane == r) {
+        my_e = (int)(0xFFFFFFFFu - ml);
+        my_s = m;
+      }
+    }
+    if (lane < KT) {
+      topk_ids[(size_t)t * KT + lane] = my_e;
+      topk_s[(size_t)t * KT + lane] = unord_f32(my_s);
+      atomicOr(&words[my_e], 1u << (t - tok0));
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += 256) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
+}
+
+#ifndef SONIC_TOPK_WARP
+#define SONIC_TOPK_WARP 1  // TC: the warp-per-token top-K (E % 32 == 0, E <= SONIC_TOPK_WARP_EMAX); 0 = k_topk_g4 always
+#endif
+#ifndef SONIC_TOPK_WARP_EMAX
+#define SONIC_TOPK_WARP_EMAX 128
+#endif
+
 template <int KT>
 void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   const int T = (int)L.T, E = L.E, W = L.W;
@@ -932,6 +1021,13 @@ void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   }
   // token rounding / expert choice read S^T: written here from the staged slab (no separate transpose)
   float* st_out = (L.mode == 1 || L.mode == 3) ? L.ST : nullptr;
+  // warp per token: 7B / Qwen3 (E = 128) route 32.7 -> 27.3 us; at E = 384 (Kimi) slower than the
+  // four-threads-per-token kernel (92.7 -> 106.3 us), so only for E <= SONIC_TOPK_WARP_EMAX
+  if (SONIC_TOPK_WARP && !st_out && E % 32 == 0 && E <= SONIC_TOPK_WARP_EMAX) {
+    if (E <= 128) launch_k(k_topk_warp<KT, 4>, W, 256, 0, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
+    else launch_k(k_topk_warp<KT, 8>, W, 256, 0, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
+    return;
+  }
   launch_k(k_topk_g4<KT>, W, 32 * SONIC_TOPK_TPT, smem, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket,
            st_out);
 }
