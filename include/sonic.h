@@ -168,6 +168,22 @@ sonic_status sonic_route(const sonic_moe_desc *desc, const float *S, sonic_routi
                          void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * sonic_route_logits -- sonic_route with the router softmax fused in ("an optional softmax
+ * fusion ... within the top-K kernel"; SURVEY 8(b) SONIC_F_FUSED_SOFTMAX).
+ *   logits [T,E] fp32 router logits (finite, Q24), read once.
+ *   S_out  [T,E] fp32 output: S_t = softmax(logits_t) per token, computed in fp32 -- max-subtracted
+ *          expf, the sum over each lane's experts in order then a fixed butterfly across the warp,
+ *          IEEE division (deterministic; within (E + 64) * 2^-24 relative of the exact softmax).
+ *          It is the S of sonic_route / sonic_router_bwd: keep it for the backward.
+ *   out    as sonic_route; the routing is exactly sonic_route(desc, S_out) (bit for bit).
+ * Under TC with E % 32 == 0 and E <= 128 the softmax runs inside the warp-per-token top-K kernel
+ * (logits in, S out, no extra pass); otherwise a row-softmax kernel writes S_out first (same
+ * arithmetic).  Not for SONIC_ROUTE_GIVEN (SONIC_ERR_INVALID_ARG).  logits and S_out must not alias.
+ */
+sonic_status sonic_route_logits(const sonic_moe_desc *desc, const float *logits, float *S_out,
+                                sonic_routing *out, void *ws, size_t ws_bytes, void *stream);
+
+/*
  * sonic_moe_fwd -- Alg. 2: up-proj A kernel (gather fused, SwiGLU
  * epilogue), down-proj Y kernel (gate applied in the epilogue, Q2), expert
  * aggregation O kernel (gather-and-sum, no atomics).

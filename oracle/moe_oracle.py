@@ -614,6 +614,18 @@ def arithmetic_intensity(T, d, n, E, K):
 
 
 # --------------------------------------------------------------------------
+# Router softmax (NEXT-4; "optional softmax fusion on top-K values")
+# --------------------------------------------------------------------------
+def softmax(logits):
+    """S_te = exp(l_te) / sum_e' exp(l_te'), per token (row), in fp64; the max-subtraction is the
+    textbook overflow guard (it cancels exactly in the ratio).  The scores S that ``route`` takes
+    (S = softmax of the router logits)."""
+    lg = np.asarray(logits, dtype=np.float64)
+    z = np.exp(lg - lg.max(axis=1, keepdims=True))
+    return z / z.sum(axis=1, keepdims=True)
+
+
+# --------------------------------------------------------------------------
 # Router backward (NEXT-4): dS -> d logits through the renormalisation and the softmax
 # --------------------------------------------------------------------------
 def router_backward(S, rt: Routing, dS_te, gate_raw=False):

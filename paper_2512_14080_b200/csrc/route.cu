@@ -919,6 +919,71 @@ __global__ void __launch_bounds__(32 * SONIC_TOPK_TPT) k_topk_g4(const float* __
   for (int e = tid; e < E; e += NT) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
 }
 
+// ---------------------------------------------------------------- fused router softmax
+// S_t = softmax(logits_t) in fp32 for one token held by a warp, lane l owning experts l, l + 32, ...
+// (epl per lane): max via the exact ordered-key warp max, e_j = expf(l_j - max), the sum lane-local
+// in j order then a fixed xor-butterfly across lanes (deterministic, and the same order in every
+// kernel that calls this), S_j = e_j / sum (IEEE division).
+template <int EPLMAX>
+__device__ __forceinline__ void warp_softmax_row(float (&v)[EPLMAX], int epl) {
+  uint32_t mk = 0u;
+#pragma unroll
+  for (int j = 0; j < EPLMAX; ++j)
+    if (j < epl) mk = max(mk, ord_f32(v[j]));
+  const float mx = unord_f32(__reduce_max_sync(0xffffffffu, mk));
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < EPLMAX; ++j) {
+    if (j < epl) {
+      v[j] = expf(v[j] - mx);
+      sum += v[j];
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+#pragma unroll
+  for (int j = 0; j < EPLMAX; ++j)
+    if (j < epl) v[j] = __fdiv_rn(v[j], sum);
+}
+
+// Row softmax for the paths that cannot fuse it into the top-K (token rounding / expert choice,
+// E > SONIC_TOPK_WARP_EMAX or E % 32 != 0): one warp per token, the same arithmetic as the fused
+// top-K (E % 32 == 0, E <= 512: bit-identical S); larger or ragged E go through the same
+// lane-strided order with the values re-read from global memory.
+template <int EPLMAX>
+__global__ void __launch_bounds__(256) k_softmax_rows(const float* __restrict__ logits, long long T, int E,
+                                                      float* __restrict__ S) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const long long t = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (t >= T) return;
+  const float* row = logits + t * E;
+  float* out = S + t * E;
+  const int epl = (E + 31) >> 5;
+  if (epl <= EPLMAX && E % 32 == 0) {
+    float v[EPLMAX];
+#pragma unroll
+    for (int j = 0; j < EPLMAX; ++j) v[j] = j < epl ? __ldg(row + 32 * j + lane) : 0.f;
+    warp_softmax_row<EPLMAX>(v, epl);
+#pragma unroll
+    for (int j = 0; j < EPLMAX; ++j)
+      if (j < epl) out[32 * j + lane] = v[j];
+    return;
+  }
+  uint32_t mk = 0u;
+  for (int j = 0; j < epl; ++j)
+    if (32 * j + lane < E) mk = max(mk, ord_f32(__ldg(row + 32 * j + lane)));
+  const float mx = unord_f32(__reduce_max_sync(0xffffffffu, mk));
+  float sum = 0.f;
+  for (int j = 0; j < epl; ++j)
+    if (32 * j + lane < E) sum += expf(__ldg(row + 32 * j + lane) - mx);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  for (int j = 0; j < epl; ++j)
+    if (32 * j + lane < E) out[32 * j + lane] = __fdiv_rn(expf(__ldg(row + 32 * j + lane) - mx), sum);
+}
+
 // TC top-K with one warp per token (E % 32 == 0, E <= 32 * EPLMAX; no S^T output): lane l holds
 // experts l, l + 32, ... (coalesced 128-byte loads), keeps its own top min(E/32, KP) keys sorted
 // (key = ordered score << 32 | ~expert: unique, so the order is the exact (S desc, expert asc) order
@@ -928,7 +993,8 @@ __global__ void __launch_bounds__(32 * SONIC_TOPK_TPT) k_topk_g4(const float* __
 template <int KT, int EPLMAX>
 __global__ void __launch_bounds__(256) k_topk_warp(const float* __restrict__ S, int T, int E, int W,
                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
-                                                   uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket) {
+                                                   uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket,
+                                                   float* __restrict__ S_out) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
@@ -956,6 +1022,12 @@ __global__ void __launch_bounds__(256) k_topk_warp(const float* __restrict__ S, 
   for (int u = 0; u < 4; ++u) {
     const int t = tok0 + wp + 8 * u;
     if (t >= T) continue;  // (uniform per warp)
+    if (S_out) {  // softmax fusion: the loaded values are logits; S is written and routed on
+      warp_softmax_row<EPLMAX>(v[u], epl);
+#pragma unroll
+      for (int j = 0; j < EPLMAX; ++j)
+        if (j < epl) S_out[(size_t)t * E + 32 * j + lane] = v[u][j];
+    }
     unsigned long long lst[LL];
 #pragma unroll
     for (int i = 0; i < LL; ++i) lst[i] = 0ull;
@@ -1009,7 +1081,7 @@ __global__ void __launch_bounds__(256) k_topk_warp(const float* __restrict__ S, 
 #endif
 
 template <int KT>
-void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
+int launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   const int T = (int)L.T, E = L.E, W = L.W;
   const int smem = (TG_TOK * TG_STRIDE + E) * 4;
   static int attr[64] = {};  // per device (function attributes are per context)
@@ -1024,21 +1096,30 @@ void launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   // warp per token: 7B / Qwen3 (E = 128) route 32.7 -> 27.3 us; at E = 384 (Kimi) slower than the
   // four-threads-per-token kernel (92.7 -> 106.3 us), so only for E <= SONIC_TOPK_WARP_EMAX
   if (SONIC_TOPK_WARP && !st_out && E % 32 == 0 && E <= SONIC_TOPK_WARP_EMAX) {
-    if (E <= 128) launch_k(k_topk_warp<KT, 4>, W, 256, 0, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
-    else launch_k(k_topk_warp<KT, 8>, W, 256, 0, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket);
-    return;
+    // with logits (sonic_route_logits) the softmax is fused here: reads logits, writes S, routes on S
+    const float* in = L.logits ? L.logits : L.S;
+    float* s_out = L.logits ? const_cast<float*>(L.S) : nullptr;
+    if (E <= 128) launch_k(k_topk_warp<KT, 4>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out);
+    else launch_k(k_topk_warp<KT, 8>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out);
+    return 1;
+  }
+  int nl = 1;
+  if (L.logits) {  // no fused top-K for this mode / E: the row softmax first, then the top-K on S
+    launch_k(k_softmax_rows<16>, (int)((L.T + 7) / 8), 256, 0, st, L.logits, L.T, E, const_cast<float*>(L.S));
+    ++nl;
   }
   launch_k(k_topk_g4<KT>, W, 32 * SONIC_TOPK_TPT, smem, st, L.S, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket,
            st_out);
+  return nl;
 }
 
-void launch_topk(const RouteLaunch& L, cudaStream_t st) {
+int launch_topk(const RouteLaunch& L, cudaStream_t st) {
   switch (L.K) {
-#define TKC(k) case k: launch_topk_g4<k>(L, st); break;
+#define TKC(k) case k: return launch_topk_g4<k>(L, st);
     TKC(1) TKC(2) TKC(3) TKC(4) TKC(5) TKC(6) TKC(7) TKC(8)
     TKC(9) TKC(10) TKC(11) TKC(12) TKC(13) TKC(14) TKC(15) TKC(16)
 #undef TKC
-    default: break;
+    default: return 0;
   }
 }
 
@@ -1070,8 +1151,7 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
     nl += 2;
     return nl;
   }
-  launch_topk(L, st);  // K <= 16 (validated for TC / TR)
-  ++nl;
+  nl += launch_topk(L, st);  // K <= 16 (validated for TC / TR); + the row softmax with logits
   const uint32_t* bm_kept = L.bm_tc;
   if (L.mode == 1 || L.mode == 3) {  // token rounding (any subroutine) or expert choice
     const bool ec = L.mode == 3;

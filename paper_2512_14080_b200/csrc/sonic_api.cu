@@ -522,10 +522,11 @@ int sonic_profile_collect(char* names, int name_len, float* ms, int max_records)
   return n;
 }
 
-sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing* rt, void* ws, size_t ws_bytes,
-                         void* stream) {
+static sonic_status route_impl(const sonic_moe_desc* D, const float* S, const float* logits, sonic_routing* rt,
+                               void* ws, size_t ws_bytes, void* stream) {
   g_launches = 0;
   if (!valid_desc(D) || !S || !rt) return SONIC_ERR_INVALID_ARG;
+  if (logits && (D->route_mode == SONIC_ROUTE_GIVEN || !aligned16(logits))) return SONIC_ERR_INVALID_ARG;
   if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
   const RouteWs w = route_ws(D);
   if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
@@ -554,6 +555,7 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
   L.rescue = (D->flags & SONIC_F_NO_ORPHAN_RESCUE) ? 0 : 1;
   L.gate_raw = (D->flags & SONIC_F_GATE_RAW) ? 1 : 0;
   L.S = S;
+  L.logits = logits;
   L.topk_ids = rt->topk_ids; L.topk_s = rt->topk_s; L.f = rt->f; L.f_r = rt->f_rounded;
   L.offsets = rt->offsets; L.pad_offsets = rt->pad_offsets; L.row_token = rt->row_token;
   L.row_gate = rt->row_gate; L.token_rowptr = rt->token_rowptr; L.token_rows = rt->token_rows;
@@ -580,6 +582,17 @@ sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing*
     g_launches = launch_route(L, static_cast<cudaStream_t>(stream));
   }
   return check_launch();
+}
+
+sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing* rt, void* ws, size_t ws_bytes,
+                         void* stream) {
+  return route_impl(D, S, nullptr, rt, ws, ws_bytes, stream);
+}
+
+sonic_status sonic_route_logits(const sonic_moe_desc* D, const float* logits, float* S_out, sonic_routing* rt,
+                                void* ws, size_t ws_bytes, void* stream) {
+  if (!logits) return SONIC_ERR_INVALID_ARG;
+  return route_impl(D, S_out, logits, rt, ws, ws_bytes, stream);
 }
 
 sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W1, const void* W2,

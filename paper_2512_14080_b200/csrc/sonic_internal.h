@@ -33,7 +33,8 @@ struct RouteLaunch {
   int E, K, W, m_tile, mode, rescue, gate_raw;
   int rounding;   // mode 1 (TR): 0 NR-f, 1 up, 2 down, 3 Balance-f, 4 SR-f, 5 NR-s; mode 3 = expert choice
   uint32_t seed;  // SR-f draws
-  const float* S;
+  const float* S;        // scores; with `logits` set, the S output buffer the fused softmax writes
+  const float* logits;   // sonic_route_logits: router logits [T,E] (softmax fused), else null
   // outputs
   int *topk_ids, *f, *f_r, *offsets, *pad_offsets, *row_token, *token_rowptr, *token_rows, *tile_expert,
       *num_tiles, *tile_pairs, *num_pairs;

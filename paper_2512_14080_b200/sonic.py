@@ -87,6 +87,8 @@ def lib():
         L.sonic_workspace_offsets.restype = ctypes.c_int
         L.sonic_route.argtypes = [P(sonic_moe_desc), vp, P(sonic_routing), vp, sz, vp]
         L.sonic_route.restype = ctypes.c_int
+        L.sonic_route_logits.argtypes = [P(sonic_moe_desc), vp, vp, P(sonic_routing), vp, sz, vp]
+        L.sonic_route_logits.restype = ctypes.c_int
         L.sonic_moe_fwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, P(sonic_routing), vp, vp, vp, sz, vp]
         L.sonic_moe_fwd.restype = ctypes.c_int
         L.sonic_moe_bwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, vp, vp, P(sonic_routing), vp, vp, vp, vp, vp,
@@ -243,6 +245,20 @@ def sonic_route(desc, S, rt=None, ws=None):
     _done(lib().sonic_route(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(ws), ws.numel(), _stream()),
            "sonic_route")
     return rt
+
+
+def sonic_route_logits(desc, logits, S=None, rt=None, ws=None):
+    """sonic_route_logits: router logits [T,E] fp32 -> (S = softmax(logits) [T,E] fp32, Routing); the
+    softmax is fused into the routing."""
+    if S is None:
+        S = torch.empty_like(logits)
+    if rt is None:
+        rt = alloc_routing(desc, logits.device)
+    if ws is None:
+        ws = _ws(sonic_route_workspace_size(desc), logits.device)
+    _done(lib().sonic_route_logits(ctypes.byref(desc), _ptr(logits), _ptr(S), ctypes.byref(rt.c), _ptr(ws), ws.numel(),
+                                   _stream()), "sonic_route_logits")
+    return S, rt
 
 
 def sonic_moe_fwd(desc, X, W1, W2, rt, O=None, H=None, ws=None):

@@ -274,3 +274,43 @@ def test_poisoned_buffers(case):
     inp = make_inputs(T, d, n, E, K, seed=5, device="cuda")
     m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
     full_parity(sonic.make_desc(T, d, n, E, K, mode=m, flags=flags), inp, mode=mode, poison=True)
+
+
+# NEXT-4: router softmax fused into the routing, sonic_route_logits
+LOGIT_CASES = [
+    # (name, T, E, K, route mode): TC with E <= 128 fuses the softmax into the warp top-K; the others
+    # run the row-softmax kernel first (TR / EC need S^T; E = 384 > 128; E = 40 is not a multiple of 32)
+    ("tc_e128", 4096, 128, 8, sonic.SONIC_ROUTE_TC),
+    ("tc_e64_ragged_T", 1000, 64, 4, sonic.SONIC_ROUTE_TC),
+    ("tr_e128", 4096, 128, 8, sonic.SONIC_ROUTE_TR_NRF),
+    ("ec_e64", 2048, 64, 4, sonic.SONIC_ROUTE_EC),
+    ("tc_e384", 2048, 384, 8, sonic.SONIC_ROUTE_TC),
+    ("tc_e40", 999, 40, 3, sonic.SONIC_ROUTE_TC),
+    ("tc_e1000", 300, 1000, 16, sonic.SONIC_ROUTE_TC),
+]
+
+
+@pytest.mark.parametrize("case", LOGIT_CASES, ids=[c[0] for c in LOGIT_CASES])
+def test_route_logits_fused_softmax(case):
+    """S = softmax(logits) within the fp32 bound of the arithmetic stated in include/sonic.h
+    ((E + 64) * 2^-24 relative per element: max-subtracted expf, an E-term fp32 sum, one division),
+    the routing bit-exact against the oracle's route on that S, and identical to sonic_route(S)."""
+    import numpy as np
+    from oracle import moe_oracle as om
+    from tests.parity import check_routing, routing_to_numpy
+    name, T, E, K, m = case
+    g = torch.Generator(device="cuda").manual_seed(77)
+    logits = torch.randn(T, E, device="cuda", generator=g) * 2.0
+    desc = sonic.make_desc(T, 64, 64, E, K, mode=m)
+    S, rt = sonic.sonic_route_logits(desc, logits)
+    rt2 = sonic.sonic_route(desc, S.clone())
+    torch.cuda.synchronize()
+    S_ref = om.softmax(logits.double().cpu().numpy())
+    Sg = S.double().cpu().numpy()
+    bound = (E + 64) * 2.0 ** -24 * S_ref + 1e-40
+    assert np.all(np.abs(Sg - S_ref) <= bound), f"{name}: max rel err {np.max(np.abs(Sg - S_ref) / S_ref):.3e}"
+    ga, gb = routing_to_numpy(rt, desc), routing_to_numpy(rt2, desc)  # the written extents
+    for f in ga:
+        assert np.array_equal(ga[f], gb[f]), f"{name}: {f} differs from sonic_route(S)"
+    mode, rounding = sonic.ROUTE_MODE_NAMES[m]
+    check_routing(ga, om.route(S.cpu().numpy(), K, mode=mode, rounding=rounding))

@@ -468,6 +468,29 @@ def test_tr_subroutine_route_invariants(rounding):
         assert np.all(rt.f_rounded == np.minimum(om.round_up(rt.f, M), T))
 
 
+# ---------------------------------------------------------------- NEXT-4 router softmax
+def test_softmax_closed_forms():
+    """Pins of om.softmax against the mathematics: two experts reduce to the logistic sigmoid of the
+    logit difference; equal logits give 1/E; rows sum to 1; adding a constant per row changes nothing;
+    a large negative offset of one logit sends its probability to ~0; order is preserved."""
+    rng = np.random.default_rng(3)
+    a = rng.normal(size=50) * 4
+    b = rng.normal(size=50) * 4
+    S2 = om.softmax(np.stack([a, b], axis=1))
+    np.testing.assert_allclose(S2[:, 0], 1.0 / (1.0 + np.exp(b - a)), rtol=1e-15, atol=1e-300)
+    np.testing.assert_allclose(om.softmax(np.full((3, 7), 2.5)), 1.0 / 7, rtol=1e-15)
+    lg = rng.normal(size=(40, 96)) * 3
+    S = om.softmax(lg)
+    np.testing.assert_allclose(S.sum(1), 1.0, rtol=0, atol=1e-14)
+    np.testing.assert_allclose(om.softmax(lg + rng.normal(size=(40, 1)) * 50), S, rtol=1e-12)
+    assert np.all(np.argsort(-S, axis=1, kind="stable")[:, :5] == np.argsort(-lg, axis=1, kind="stable")[:, :5])
+    lg2 = lg.copy()
+    lg2[:, 0] -= 1000.0
+    assert np.all(om.softmax(lg2)[:, 0] < 1e-300)
+    # a worked value: softmax([0, ln 2, ln 3]) = [1, 2, 3] / 6
+    np.testing.assert_allclose(om.softmax(np.log([[1.0, 2.0, 3.0]])), [[1 / 6, 2 / 6, 3 / 6]], rtol=1e-15)
+
+
 # ---------------------------------------------------------------- NEXT-4 router backward
 @pytest.mark.parametrize("gate_raw", [False, True])
 @pytest.mark.parametrize("mode", ["tc", "tr"])
