@@ -234,6 +234,33 @@ sonic_status sonic_router_bwd(const sonic_moe_desc *desc, const float *S, const 
 
 const char *sonic_status_string(sonic_status s);
 
+/*
+ * sonic_router_fwd -- the router GEMM before the routing (NEXT-4; the router "computes" the scores,
+ * P:284 footnote): logits = X W_r.
+ *   X      [T,d] bf16 row-major (the layer input, as sonic_moe_fwd's X)
+ *   Wr     [d,E] bf16 row-major router weight
+ *   logits [T,E] fp32 output (fp32 accumulation), the input of sonic_route_logits.
+ * A plain dense GEMM, run by cuBLAS (cublasGemmEx), loaded with dlopen at first use:
+ * SONIC_ERR_UNSUPPORTED if libcublas.so.12 cannot be loaded.  Asynchronous on `stream`.
+ */
+sonic_status sonic_router_fwd(const sonic_moe_desc *desc, const void *X, const void *Wr, float *logits,
+                              void *stream);
+
+/*
+ * sonic_router_grad -- the router's share of the input and weight gradients (NEXT-4), from the
+ * d logits of sonic_router_bwd (which carries dS through the gate renormalisation and softmax):
+ *   dlogits [T,E] fp32; rounded to bf16 in ws for the tensor-core GEMMs (the operand precision
+ *           of every GEMM of the layer)
+ *   dX      [T,d] bf16 in/out, may be NULL: dX += dlogits W_r^T (pass sonic_moe_bwd's dX to get
+ *           the layer's full input gradient; fp32 accumulation, one bf16 rounding)
+ *   dWr     [d,E] fp32 out, may be NULL: dWr = X^T dlogits (overwritten)
+ *   ws      >= sonic_router_grad_workspace_size(desc) bytes, 16-byte aligned.
+ * Both NULL is SONIC_ERR_INVALID_ARG.  cuBLAS as sonic_router_fwd.
+ */
+size_t sonic_router_grad_workspace_size(const sonic_moe_desc *desc);
+sonic_status sonic_router_grad(const sonic_moe_desc *desc, const void *X, const void *Wr, const float *dlogits,
+                               void *dX, float *dWr, void *ws, size_t ws_bytes, void *stream);
+
 /* Number of kernels the last sonic_route / sonic_moe_fwd / sonic_moe_bwd / sonic_ep_* compute call on
  * this thread launched. */
 int sonic_last_launch_count(void);

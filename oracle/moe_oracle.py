@@ -625,6 +625,20 @@ def softmax(logits):
     return z / z.sum(axis=1, keepdims=True)
 
 
+def router_logits(X, Wr):
+    """The router GEMM (scores S = softmax(X W_r)): logits = X W_r, [T, d] x [d, E]."""
+    return np.asarray(X, dtype=np.float64) @ np.asarray(Wr, dtype=np.float64)
+
+
+def router_input_grads(X, Wr, dlogits):
+    """Gradients of the router GEMM given d logits (chain rule of logits = X W_r):
+    dX_router = dlogits W_r^T (added to the MoE layer's dX), dW_r = X^T dlogits."""
+    X = np.asarray(X, dtype=np.float64)
+    Wr = np.asarray(Wr, dtype=np.float64)
+    dl = np.asarray(dlogits, dtype=np.float64)
+    return dl @ Wr.T, X.T @ dl
+
+
 # --------------------------------------------------------------------------
 # Router backward (NEXT-4): dS -> d logits through the renormalisation and the softmax
 # --------------------------------------------------------------------------

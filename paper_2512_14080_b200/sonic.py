@@ -89,6 +89,12 @@ def lib():
         L.sonic_route.restype = ctypes.c_int
         L.sonic_route_logits.argtypes = [P(sonic_moe_desc), vp, vp, P(sonic_routing), vp, sz, vp]
         L.sonic_route_logits.restype = ctypes.c_int
+        L.sonic_router_fwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, vp]
+        L.sonic_router_fwd.restype = ctypes.c_int
+        L.sonic_router_grad_workspace_size.argtypes = [P(sonic_moe_desc)]
+        L.sonic_router_grad_workspace_size.restype = sz
+        L.sonic_router_grad.argtypes = [P(sonic_moe_desc), vp, vp, vp, vp, vp, vp, sz, vp]
+        L.sonic_router_grad.restype = ctypes.c_int
         L.sonic_moe_fwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, P(sonic_routing), vp, vp, vp, sz, vp]
         L.sonic_moe_fwd.restype = ctypes.c_int
         L.sonic_moe_bwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, vp, vp, P(sonic_routing), vp, vp, vp, vp, vp,
@@ -306,6 +312,26 @@ def sonic_router_bwd(desc, S, rt, dS, dlogits=None):
     _done(lib().sonic_router_bwd(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(dS), _ptr(dlogits),
                                  _stream()), "sonic_router_bwd")
     return dlogits
+
+
+def sonic_router_fwd(desc, X, Wr, logits=None):
+    """sonic_router_fwd: logits [T,E] fp32 = X [T,d] bf16 . Wr [d,E] bf16 (NEXT-4)."""
+    if logits is None:
+        logits = torch.empty(desc.T, desc.E, dtype=torch.float32, device=X.device)
+    _done(lib().sonic_router_fwd(ctypes.byref(desc), _ptr(X), _ptr(Wr), _ptr(logits), _stream()), "sonic_router_fwd")
+    return logits
+
+
+def sonic_router_grad(desc, X, Wr, dlogits, dX=None, dWr=None, want_dWr=True, ws=None):
+    """sonic_router_grad: dX += dlogits Wr^T (in place, if dX is given), dWr = X^T dlogits -> (dX, dWr)."""
+    if dWr is None and want_dWr:
+        dWr = torch.empty(desc.d, desc.E, dtype=torch.float32, device=X.device)
+    if ws is None:
+        ws = _ws(int(lib().sonic_router_grad_workspace_size(ctypes.byref(desc))), X.device)
+    _done(lib().sonic_router_grad(ctypes.byref(desc), _ptr(X), _ptr(Wr), _ptr(dlogits), _ptr(dX) if dX is not None
+                                  else None, _ptr(dWr) if dWr is not None else None, _ptr(ws), ws.numel(), _stream()),
+          "sonic_router_grad")
+    return dX, dWr
 
 
 def ws_view(ws, offset, shape, dtype):

@@ -314,3 +314,62 @@ def test_route_logits_fused_softmax(case):
         assert np.array_equal(ga[f], gb[f]), f"{name}: {f} differs from sonic_route(S)"
     mode, rounding = sonic.ROUTE_MODE_NAMES[m]
     check_routing(ga, om.route(S.cpu().numpy(), K, mode=mode, rounding=rounding))
+
+
+@pytest.mark.parametrize("shape", [(4096, 256, 128), (1000, 1536, 128), (777, 384, 40)], ids=["7bE", "7bd", "ragged"])
+def test_router_gemms(shape):
+    """NEXT-4 router GEMMs: logits = X W_r within the fp32-accumulation bound (bf16 products are
+    exact in fp32, so |err| <= d 2^-24 sum_k |X_tk W_ke|); dX += dlogits W_r^T and dW_r = X^T dlogits
+    (d logits rounded to bf16 for the tensor cores, by design) within the north-star criterion."""
+    import numpy as np
+    from oracle import moe_oracle as om
+    from tests.parity import assert_close
+    T, d, E = shape
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    Wr = (torch.randn(d, E, device="cuda", generator=g) / d ** 0.5).bfloat16()
+    dl = torch.randn(T, E, device="cuda", generator=g) * 1e-2
+    dX0 = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+    desc = sonic.make_desc(T, d, 64, E, min(2, E))
+    logits = sonic.sonic_router_fwd(desc, X, Wr)
+    dX = dX0.clone()
+    dX, dWr = sonic.sonic_router_grad(desc, X, Wr, dl, dX=dX)
+    torch.cuda.synchronize()
+    Xn, Wn = X.double().cpu().numpy(), Wr.double().cpu().numpy()
+    ref = om.router_logits(Xn, Wn)
+    bound = d * 2.0 ** -24 * (np.abs(Xn) @ np.abs(Wn)) + 1e-30
+    assert np.all(np.abs(logits.double().cpu().numpy() - ref) <= bound)
+    dX_r, dW_r = om.router_input_grads(Xn, Wn, dl.double().cpu().numpy())
+    assert_close("dX", dX.double().cpu().numpy(), dX0.double().cpu().numpy() + dX_r)
+    assert_close("dWr", dWr.double().cpu().numpy(), dW_r)
+
+
+def test_router_full_chain():
+    """The training step around the expert layer, all through the C ABI: router GEMM -> fused
+    softmax + routing -> MoE fwd/bwd -> router backward (dS -> d logits) -> router GEMM grads;
+    dX (expert path + router path) and dW_r against the oracle chain on the same inputs."""
+    import numpy as np
+    from oracle import moe_oracle as om
+    from tests.parity import assert_close
+    T, d, n, E, K = 2048, 256, 128, 32, 4
+    inp = make_inputs(T, d, n, E, K, seed=8, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(6)
+    Wr = (torch.randn(d, E, device="cuda", generator=g) / d ** 0.5).bfloat16()
+    desc = sonic.make_desc(T, d, n, E, K)
+    logits = sonic.sonic_router_fwd(desc, inp.X, Wr)
+    S, rt = sonic.sonic_route_logits(desc, logits)
+    O, H, _ = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
+    dX, dW1, dW2, dS, _ = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
+    dlog = sonic.sonic_router_bwd(desc, S, rt, dS)
+    dX, dWr = sonic.sonic_router_grad(desc, inp.X, Wr, dlog, dX=dX)
+    torch.cuda.synchronize()
+    f = lambda t: t.double().cpu().numpy()
+    Xn, Wn = f(inp.X), f(Wr)
+    Sn = S.cpu().numpy()  # the S the GPU routed on (its own parity: test_route_logits_fused_softmax)
+    rto = om.route(Sn, K, mode="tc")
+    bw = om.backward(f(inp.dO), Xn, f(inp.W1), f(inp.W2), rto)
+    dlog_ref = om.router_backward(Sn, rto, om.dS_dense(rto, bw.dS))
+    dXr, dWr_ref = om.router_input_grads(Xn, Wn, dlog_ref)
+    assert_close("dlogits", f(dlog), dlog_ref)
+    assert_close("dX (experts + router)", f(dX), bw.dX + dXr)
+    assert_close("dWr", f(dWr), dWr_ref)

@@ -491,6 +491,35 @@ def test_softmax_closed_forms():
     np.testing.assert_allclose(om.softmax(np.log([[1.0, 2.0, 3.0]])), [[1 / 6, 2 / 6, 3 / 6]], rtol=1e-15)
 
 
+def test_router_chain_finite_differences():
+    """The whole router chain -- logits = X W_r, S = softmax, gates renormalised over the frozen kept
+    sets -- differentiated by router_backward then router_input_grads equals central finite
+    differences of L(X, W_r) = sum_{kept (t,e)} c_te g_te, for every coordinate of X and W_r."""
+    rng = np.random.default_rng(9)
+    T, d, E, K = 10, 5, 6, 2
+    X = rng.normal(size=(T, d))
+    Wr = rng.normal(size=(d, E))
+    S = om.softmax(om.router_logits(X, Wr))
+    rt = om.route(S, K, mode="tc")
+    c = rng.normal(size=(T, E)) * rt.kept
+
+    def loss(Xv, Wv):
+        s = om.softmax(Xv @ Wv)
+        z = np.where(rt.kept, s, 0.0).sum(1, keepdims=True)
+        return float((np.where(rt.kept, s / z, 0.0) * c).sum())
+
+    dX, dW = om.router_input_grads(X, Wr, om.router_backward(S, rt, c))
+    h = 1e-6
+    for arr, got, which in ((X, dX, 0), (Wr, dW, 1)):
+        fd = np.zeros_like(arr)
+        for idx in np.ndindex(*arr.shape):
+            p_, m_ = arr.copy(), arr.copy()
+            p_[idx] += h
+            m_[idx] -= h
+            fd[idx] = ((loss(p_, Wr) - loss(m_, Wr)) if which == 0 else (loss(X, p_) - loss(X, m_))) / (2 * h)
+        np.testing.assert_allclose(got, fd, rtol=1e-6, atol=1e-9)
+
+
 # ---------------------------------------------------------------- NEXT-4 router backward
 @pytest.mark.parametrize("gate_raw", [False, True])
 @pytest.mark.parametrize("mode", ["tc", "tr"])
