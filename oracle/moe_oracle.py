@@ -394,7 +394,54 @@ def expert_forward(Xe, W1e, W2e, ge):
     return He, Ae, Ye
 
 
-def forward(X, W1, W2, rt: Routing, experts=None):
+# --------------------------------------------------------------------------
+# FP8 up-projection (NEXT-4; the paper's future work): e4m3 operands with one scale per
+# token row of X and one per output column of W1_e, fp32 accumulation, the scales applied to the sum
+# --------------------------------------------------------------------------
+E4M3_MAX = 448.0
+
+
+def e4m3_round(x):
+    """Round to the nearest OCP FP8 E4M3 value, ties to even, finite values beyond the largest
+    (448) saturated to +-448 (cvt.rn.satfinite).  E4M3: bias 7, 3 mantissa bits: normals
+    m * 2^e with m in [1, 2) on a grid of 2^(e-3) for e >= -6, subnormals on the grid 2^-9."""
+    x = np.asarray(x, dtype=np.float64)
+    a = np.abs(x)
+    _, ex = np.frexp(np.where(a > 0, a, 1.0))       # a = m 2^ex, m in [0.5, 1): floor(log2 a) = ex - 1
+    e = np.maximum(ex - 1, -6)                      # below 2^-6 the spacing stays 2^-9 (subnormals)
+    q = np.ldexp(1.0, e - 3)                        # spacing of the grid around a
+    r = np.minimum(np.rint(a / q) * q, E4M3_MAX)    # a / q and the product are exact; rint: ties to even
+    return np.copysign(r, x)
+
+
+def quantize_e4m3(M, axis):
+    """Per-slice e4m3 quantisation along `axis` (the reduction dimension K): scale = amax / 448 in
+    fp32 (1 where amax = 0), q = e4m3_round(fl32(M / scale)).  Returns (q, scale) with
+    M ~= q * scale; q and scale are exactly what the GPU's quantisation kernels produce."""
+    M32 = np.asarray(M, dtype=np.float32)
+    amax = np.max(np.abs(M32), axis=axis, keepdims=True).astype(np.float32)
+    scale = np.where(amax > 0, amax / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
+    q = e4m3_round((M32 / scale).astype(np.float32))
+    return q, np.squeeze(scale, axis=axis).astype(np.float64)
+
+
+def fp8_up_operands(X, W1):
+    """X [T,d] -> (Xq, sx [T]) per token row; W1 [E,d,2n] -> (W1q, sw [E,2n]) per output column."""
+    Xq, sx = quantize_e4m3(X, axis=1)
+    W1q, sw = quantize_e4m3(W1, axis=1)
+    return Xq, sx, W1q, sw
+
+
+def expert_forward_fp8(Xq_e, sx_e, W1q_e, sw_e, W2e, ge):
+    """expert_forward with the up-projection on the quantised operands:
+    H_e = (Xq_e W1q_e) * sx_e[:, None] * sw_e[None, :]; the rest as expert_forward."""
+    He = (_f64(Xq_e) @ _f64(W1q_e)) * _f64(sx_e)[:, None] * _f64(sw_e)[None, :]
+    Ae = swiglu(He)
+    Ye = np.asarray(ge)[:, None] * (Ae @ _f64(W2e))
+    return He, Ae, Ye
+
+
+def forward(X, W1, W2, rt: Routing, experts=None, fp8_up=False):
     """O_t = sum_e pi_te g_te Y_{e,t},  Y_e = SwiGLU(X_e W1_e) W2_e.
 
     The gate multiplies Y before aggregation (Q2, P:1774 option (1)); the
@@ -405,9 +452,14 @@ def forward(X, W1, W2, rt: Routing, experts=None):
     E = W1.shape[0]
     O = np.zeros((T, d))
     H, A, Y, tokens = {}, {}, {}, {}
+    if fp8_up:
+        Xq, sx, W1q, sw = fp8_up_operands(X, W1)
     for e in (range(E) if experts is None else experts):
         toks = np.nonzero(rt.kept[:, e])[0]
-        He, Ae, Ye = expert_forward(X[toks], W1[e], W2[e], rt.gate[toks, e])  # X_e = Gather(X, pi_:,e)
+        if fp8_up:
+            He, Ae, Ye = expert_forward_fp8(Xq[toks], sx[toks], W1q[e], sw[e], W2[e], rt.gate[toks, e])
+        else:
+            He, Ae, Ye = expert_forward(X[toks], W1[e], W2[e], rt.gate[toks, e])  # X_e = Gather(X, pi_:,e)
         np.add.at(O, toks, Ye)                                 # O_t = sum_e ...
         H[e], A[e], Y[e], tokens[e] = He, Ae, Ye, toks
     return ForwardResult(O, H, A, Y, tokens)

@@ -304,6 +304,9 @@ __device__ __forceinline__ void tload3(void* dst, const CUtensorMap* m, uint64_t
 // pair).  Each pair TMA-loads half of the shared tile and multicasts it into both pairs' stage, so
 // the L2 -> SM operand traffic per MMA drops by a quarter; a stage is refilled once BOTH pairs' MMAs
 // have released it (empty barriers count the two pair leaders' commits).
+#ifndef SONIC_DW1_MFAST
+#define SONIC_DW1_MFAST 0  // experiment: dW1 tiles in M-pair-fastest order without the multicast
+#endif
 template <int KIND, int BN, bool CTA2, bool MC = false>
 __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     sonic_gemm_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mB,
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   static_assert(!MC || CTA2, "multicast clusters are built from 2-CTA pairs");
-  constexpr bool MFAST = MC && KIND == K_DW1;
+  constexpr bool MFAST = (MC || SONIC_DW1_MFAST) && KIND == K_DW1;
   const int crank = CTA2 ? (int)ptx::cluster_ctarank() : 0;
   const int rank = crank & 1;                                  // rank within the pair
   const int pidx = MC ? crank >> 1 : 0;                        // pair within the cluster

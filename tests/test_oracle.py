@@ -608,3 +608,63 @@ def test_nrs_route_invariants():
     assert np.all((rt.f_rounded % M == 0) | (rt.f_rounded == T))
     assert rt.kept.any(axis=1).all()
     assert np.all(rt.kept.sum(0) == rt.f_rounded)
+
+
+# ---------------------------------------------------------------- NEXT-4 FP8 up-projection
+def test_e4m3_round_against_the_format():
+    """om.e4m3_round against torch's float8_e4m3fn cast (an independent library rounding, ties to
+    even) on every finite code, every midpoint between neighbouring codes and random values; and
+    saturation of finite values beyond 448 (the satfinite cvt; torch's cast has no saturation)."""
+    import torch
+    codes = torch.arange(256, dtype=torch.uint8).view(torch.float8_e4m3fn).float().numpy().astype(np.float64)
+    fin = np.unique(codes[np.isfinite(codes)])
+    np.testing.assert_array_equal(om.e4m3_round(fin), fin)
+    mids = (fin[1:] + fin[:-1]) / 2
+    rng = np.random.default_rng(1)
+    vals = np.concatenate([mids, rng.normal(size=20000) * 30, rng.normal(size=5000) * 1e-2,
+                           rng.normal(size=2000) * 1e-3])
+    vals = vals[np.abs(vals) <= 448].astype(np.float32)
+    ref = torch.tensor(vals).to(torch.float8_e4m3fn).float().numpy()
+    np.testing.assert_array_equal(om.e4m3_round(vals), ref)
+    np.testing.assert_array_equal(om.e4m3_round(np.array([449.0, 464.0, 1e6, -500.0])), [448, 448, 448, -448])
+    # the grid: spacing 2^-9 below 2^-6 (subnormals), 2^(e-3) above
+    assert om.e4m3_round(np.array([2.0 ** -9 * 1.4]))[0] == 2.0 ** -9
+    assert om.e4m3_round(np.array([1.0 + 2.0 ** -4]))[0] == 1.0  # tie -> even (1.0 vs 1.125)
+
+
+def test_quantize_e4m3_properties():
+    """Per-slice scales: amax / 448 in fp32; every slice's largest |q| is exactly 448; q * scale
+    is within half an e4m3 step of the input (2^-4 relative, or 2^-10 * scale in the subnormal range)."""
+    rng = np.random.default_rng(2)
+    M = (rng.normal(size=(64, 96)) * np.exp(rng.normal(size=(64, 1)))).astype(np.float32)
+    M[5] = 0.0
+    q, s = om.quantize_e4m3(M, axis=1)
+    assert s[5] == 1.0 and np.all(q[5] == 0)
+    nz = np.arange(64) != 5
+    np.testing.assert_array_equal(np.max(np.abs(q[nz]), axis=1), 448.0)
+    np.testing.assert_array_equal(s.astype(np.float32), (np.max(np.abs(M), axis=1) / np.float32(448)).astype(np.float32)
+                                  * nz + (~nz))
+    err = np.abs(q * s[:, None] - M)
+    assert np.all(err <= 2.0 ** -4 * np.abs(M) * (1 + 1e-6) + 2.0 ** -10 * s[:, None] * (1 + 1e-6))
+
+
+def test_forward_fp8_up_is_the_quantised_definition():
+    """forward(fp8_up=True) equals the dense definition on the dequantised operands
+    (Xq sx) (W1q sw): the scales factor out of the K sum exactly; and it stays within the
+    quantisation error of the bf16 forward."""
+    rng = np.random.default_rng(4)
+    T, d, n, E, K = 48, 32, 16, 4, 2
+    X = rng.normal(size=(T, d))
+    W1 = rng.normal(size=(E, d, 2 * n)) / np.sqrt(d)
+    W2 = rng.normal(size=(E, n, d)) / np.sqrt(n)
+    S = rng.random((T, E))
+    S /= S.sum(1, keepdims=True)
+    rt = om.route(S, K, mode="tc")
+    Xq, sx, W1q, sw = om.fp8_up_operands(X, W1)
+    Xdq = Xq * sx[:, None]
+    W1dq = W1q * sw[:, None, :]
+    f8 = om.forward(X, W1, W2, rt, fp8_up=True)
+    ref = om.forward(Xdq, W1dq, W2, rt)
+    np.testing.assert_allclose(f8.O, ref.O, rtol=1e-12, atol=1e-12)
+    full = om.forward(X, W1, W2, rt)
+    assert np.linalg.norm(f8.O - full.O) / np.linalg.norm(full.O) < 0.1
