@@ -47,7 +47,7 @@ def load_peaks():
 
 
 # --------------------------------------------------------------------------- FLOP / byte model
-def kernel_model(T, d, n, E, K, R, R_pad, dw=4):
+def kernel_model(T, d, n, E, K, R, R_pad, dw=4, fp8_up=False, w1_cached=False):
     """Algorithmic FLOPs and bytes per launch.
 
     R = routed rows (T*K under TC, sum f_r under TR).  'paper' bytes count gathered rows at
@@ -56,9 +56,10 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4):
     b = 2
     W1 = E * d * 2 * n * b
     W2 = E * n * d * b
+    ab = 1 if fp8_up else b  # bytes per up-projection operand element (e4m3 with SONIC_F_FP8_UP)
     m = {
-        "up": dict(flops=4 * R * d * n, paper=R * d * b + W1 + R * 2 * n * b + R * n * b,
-                   tight=T * d * b + W1 + R * 2 * n * b + R * n * b),
+        "up": dict(flops=4 * R * d * n, paper=R * d * ab + W1 * ab // b + R * 2 * n * b + R * n * b,
+                   tight=T * d * ab + W1 * ab // b + R * 2 * n * b + R * n * b),
         "down": dict(flops=2 * R * n * d, paper=R * n * b + W2 + R * d * b, tight=R * n * b + W2 + R * d * b),
         # fused up + down (NEXT-1): A stays on chip, so neither its write nor its read is counted
         "updown": dict(flops=6 * R * d * n, paper=R * d * b + W1 + W2 + R * 2 * n * b + R * d * b,
@@ -73,6 +74,9 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4):
                     tight=T * d * b + R * 2 * n * b + E * d * 2 * n * dw),
         "agg_dX": dict(flops=0, paper=R * d * b + T * d * b, tight=R * d * b + T * d * b),
         "route": dict(flops=0, paper=T * E * 4 + T * K * 8 + R * 12, tight=T * E * 4 + T * K * 8 + R * 12),
+        # SONIC_F_FP8_UP: X and W1 read once, their e4m3 copies written (+ scales)
+        "quant_fp8": dict(flops=0, paper=T * d * 3 + (0 if w1_cached else E * d * 2 * n * 3),
+                          tight=T * d * 3 + (0 if w1_cached else E * d * 2 * n * 3)),
         "dS_reduce": dict(flops=0, paper=R * 8, tight=R * 8),
     }
     # bytes written (part of the totals above; reported, not a separate bound: write-only HBM traffic
@@ -203,6 +207,10 @@ def workload_config(args, cfg):
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
             **({"updown": "fused kernel (SONIC_F_FUSED_UPDOWN)"} if getattr(args, "fuse", False) else {}),
+            **({"up_proj": "e4m3 operands (SONIC_F_FP8_UP), everything else bf16" +
+                          ("; W1's e4m3 copy cached across steps (SONIC_F_FP8_W1_CACHED)"
+                           if getattr(args, "fp8_w1_cached", False) else "")} if getattr(args, "fp8_up", False)
+               else {}),
             **({"m_tile": args.m_tile} if getattr(args, "m_tile", 128) != 128 else {}),
             "l2": ("flushed before every timed step (memset of 2x L2 outside the step's event pair); warm "
                    "back-to-back number in `warm`") if getattr(args, "l2_flush", False) else
@@ -230,6 +238,11 @@ def main():
     ap.add_argument("--m-tile", type=int, default=128, choices=[128, 256],
                     help="token-rounding tile (256 = the 2-CTA pair's M tile: no half-empty pairs)")
     ap.add_argument("--dw-bf16", action="store_true", help="SONIC_F_DW_BF16: weight gradients stored as bf16")
+    ap.add_argument("--fp8-up", action="store_true",
+                    help="SONIC_F_FP8_UP: the up-projection on e4m3 operands (NEXT-4; not the bf16 headline)")
+    ap.add_argument("--fp8-w1-cached", action="store_true",
+                    help="with --fp8-up: SONIC_F_FP8_W1_CACHED after the first step (W1's e4m3 copy reused, as in the "
+                         "micro-batches of a gradient-accumulation step)")
     ap.add_argument("--fuse", action="store_true",
                     help="SONIC_F_FUSED_UPDOWN: the fused up/down kernel (A kept on chip) instead of two kernels")
     ap.add_argument("--no-l2-flush", dest="l2_flush", action="store_false",
@@ -289,7 +302,8 @@ def main():
     mode = ROUTE_MODES[args.mode][0]
     desc = sonic.make_desc(T, d, n, E, K, mode=mode, m_tile=args.m_tile,
                            flags=(sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0) |
-                           (sonic.SONIC_F_FUSED_UPDOWN if args.fuse else 0))
+                           (sonic.SONIC_F_FUSED_UPDOWN if args.fuse else 0) |
+                           (sonic.SONIC_F_FP8_UP if args.fp8_up else 0))
     use_ep = args.ep or world > 1
     if not use_ep:
         # ---- one GPU, all experts local: route + fwd + bwd through the C ABI
@@ -309,10 +323,16 @@ def main():
         dW2 = torch.empty(E, n, d, dtype=wdt, device=dev)
         dS = torch.empty(rows, dtype=torch.float32, device=dev)
 
+        # --fp8-w1-cached: the first forward quantises W1 into ws_f, later ones reuse it
+        desc_f = [desc]
+
         def run(Xa, Sa, dOa, slot=0):
             O, dX = Obuf[slot], dXbuf[slot]
             sonic.sonic_route(desc, Sa, rt, ws_r)
-            sonic.sonic_moe_fwd(desc, Xa, W1, W2, rt, O, H, ws_f)
+            sonic.sonic_moe_fwd(desc_f[0], Xa, W1, W2, rt, O, H, ws_f)
+            if args.fp8_w1_cached and not (desc_f[0].flags & sonic.SONIC_F_FP8_W1_CACHED):
+                desc_f[0] = sonic.make_desc(T, d, n, E, K, mode=mode, m_tile=args.m_tile,
+                                            flags=desc.flags | sonic.SONIC_F_FP8_W1_CACHED)
             sonic.sonic_moe_bwd(desc, dOa, Xa, H, W1, W2, rt, dX, dW1, dW2, dS, ws_b)
             return O, dX
 
@@ -320,7 +340,8 @@ def main():
             return int(rt.offsets[E].item()), int(rt.pad_offsets[E].item())
 
         def local_model(R, R_pad):
-            return kernel_model(T, d, n, E, K, R, R_pad, dw=2 if args.dw_bf16 else 4)
+            return kernel_model(T, d, n, E, K, R, R_pad, dw=2 if args.dw_bf16 else 4, fp8_up=args.fp8_up,
+                                w1_cached=args.fp8_w1_cached)
     else:
         # ---- expert parallelism over the `world` GPUs (NCCL all-to-all), weak scaling: every rank
         #      brings its own T tokens and owns E/world experts (paper_2512_14080_b200/ep.py)
@@ -462,13 +483,17 @@ def main():
     for name, (tot, cnt) in agg.items():
         avg = tot / cnt
         mm = model.get(name, dict(flops=0, paper=0, tight=0, write=0))
-        t_tensor = mm["flops"] / (tf_peak * 1e12) * 1e3
+        # the e4m3 up-projection is held to the fp8 peak: the measured bf16 peak x 2 (the guide's nominal
+        # dense fp8 : bf16 ratio, 4.5 : 2.25 PFLOP/s)
+        kpeak = tf_peak * (2.0 if (args.fp8_up and name == "up") else 1.0)
+        t_tensor = mm["flops"] / (kpeak * 1e12) * 1e3
         t_hbm = mm["paper"] / (bw_peak * 1e9) * 1e3  # all algorithmic bytes at the measured copy rate
         kernels[name] = dict(avg_ms=avg, launches_per_step=cnt / args.steps, share=tot / ms_p if ms_p else None,
                              tflops=mm["flops"] / (avg * 1e-3) / 1e12 if mm["flops"] else 0.0,
                              gbs_paper=mm["paper"] / (avg * 1e-3) / 1e9, gbs_tight=mm["tight"] / (avg * 1e-3) / 1e9,
                              bound="tensor" if t_tensor >= t_hbm else "hbm",
-                             roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None)
+                             roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None,
+                             tensor_peak=kpeak)
     dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"]) if kernels else None
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
@@ -478,8 +503,9 @@ def main():
     if dom:
         k = kernels[dom]
         if k["bound"] == "tensor":
-            roof = {"kernel": dom, "bound": "tensor", "achieved": k["tflops"], "peak": tf_peak, "unit": "TFLOP/s",
-                    "frac": k["tflops"] / tf_peak, "frac_vs_sustained": k["tflops"] / tf_sus, "traffic": traffic,
+            kp = k["tensor_peak"]
+            roof = {"kernel": dom, "bound": "tensor", "achieved": k["tflops"], "peak": kp, "unit": "TFLOP/s",
+                    "frac": k["tflops"] / kp, "frac_vs_sustained": k["tflops"] / (tf_sus * kp / tf_peak), "traffic": traffic,
                     "algorithmic_per_launch": model[dom]["flops"], "peak_source": peaks["source"] + " " + peak_choice}
         else:
             roof = {"kernel": dom, "bound": "hbm", "achieved": k["gbs_paper"], "peak": bw_peak, "unit": "GB/s",
@@ -595,7 +621,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "vs_baseline": None, "dtype": "bf16+e4m3(up-proj)" if args.fp8_up else "bf16", "data": "synthetic",
         "config": workload_config(args, cfg),
         "pct_peak": value / world / peaks["bf16_tflops"],
         "pct_peak_sustained": value / world / peaks["bf16_tflops_sustained"],

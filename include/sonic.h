@@ -92,6 +92,21 @@ typedef enum {
                                        shared memory, never written to HBM) where n is 128 or 256 and
                                        d % 128 == 0; sonic_fwd_workspace_size then holds Y only.  Opt-in:
                                        measured slower than the two kernels at 7B. */
+#define SONIC_F_FP8_UP         256  /* sonic_moe_fwd: the up-projection on e4m3 operands (NEXT-4, the paper's
+                                       FP8 future work P:1553-1556): X quantised per token row and W1 per
+                                       output column (sonic_quantize_e4m3_rows / _cols: scale = amax/448 in
+                                       fp32, round to nearest even, satfinite), e4m3 x e4m3 -> fp32 tensor-core
+                                       sums (tcgen05 kind::f8f6f4), H = sum * sx[t] * sw[e][c], then the
+                                       usual SwiGLU epilogue (H, A in bf16).  Everything else stays bf16;
+                                       the backward differentiates the quantised forward through the
+                                       cached H.  Needs n % 128 == 0 and d % 128 == 0 (else
+                                       SONIC_ERR_UNSUPPORTED); the fwd workspace then also holds the e4m3
+                                       copies and scales.  Not with the fused up/down kernel. */
+#define SONIC_F_FP8_W1_CACHED  512  /* with SONIC_F_FP8_UP: the e4m3 copy of W1 and its scales in the fwd
+                                       workspace are still valid (a previous sonic_moe_fwd with the same W1
+                                       and this workspace wrote them, e.g. the earlier micro-batches of a
+                                       gradient-accumulation step): only X is quantised.  The caller
+                                       guarantees it; stale weights are not detected. */
 #define SONIC_F_DW_ACCUMULATE    4  /* sonic_moe_bwd: dW1 += ..., dW2 += ... (fp32 element-wise adds done by
                                        the TMA store unit; one add per element per call, so deterministic)
                                        instead of overwriting -- gradient accumulation over microbatches */
@@ -233,6 +248,19 @@ sonic_status sonic_router_bwd(const sonic_moe_desc *desc, const float *S, const 
                               const float *dS, float *dlogits, void *stream);
 
 const char *sonic_status_string(sonic_status s);
+
+/*
+ * e4m3 quantisation (NEXT-4, SONIC_F_FP8_UP): one fp32 scale per slice along the reduction dim,
+ * scale = amax / 448 (1 where amax = 0), q = cvt.rn.satfinite.e4m3(fl32(x / scale)).
+ *   _rows: X [rows, cols] bf16 (cols % 8 == 0, 16-byte aligned) -> q [rows, cols] e4m3, scale [rows]
+ *   _cols: W [batch, K, N] bf16 (N % 8 == 0, 16-byte aligned) -> q [batch, K, N] e4m3 (same layout),
+ *          scale [batch, N] (per column)
+ * Caller-owned device buffers; asynchronous on `stream`.
+ */
+sonic_status sonic_quantize_e4m3_rows(const void *X, int64_t rows, int32_t cols, void *q, float *scale,
+                                      void *stream);
+sonic_status sonic_quantize_e4m3_cols(const void *W, int32_t batch, int32_t K, int32_t N, void *q, float *scale,
+                                      void *stream);
 
 /*
  * sonic_router_fwd -- the router GEMM before the routing (NEXT-4; the router "computes" the scores,

@@ -5,7 +5,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRCS = ["csrc/sonic_api.cu", "csrc/route.cu", "csrc/aggregate.cu", "csrc/ep.cu", "csrc/peer.cu", "csrc/router.cu"]
+SRCS = ["csrc/sonic_api.cu", "csrc/route.cu", "csrc/aggregate.cu", "csrc/ep.cu", "csrc/peer.cu", "csrc/router.cu", "csrc/fp8.cu"]
 DEPS = SRCS + ["csrc/gemm.cuh", "csrc/updown.cuh", "csrc/ptx.cuh", "csrc/sonic_internal.h", "../include/sonic.h"]
 OUT = os.path.join(HERE, "libsonic.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

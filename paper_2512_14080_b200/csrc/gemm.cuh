@@ -37,7 +37,11 @@
 
 namespace sonic {
 
-enum GemmKind { K_UP = 0, K_DOWN = 1, K_DH = 2, K_DXT = 3, K_DW2 = 4, K_DW1 = 5 };
+enum GemmKind { K_UP = 0, K_DOWN = 1, K_DH = 2, K_DXT = 3, K_DW2 = 4, K_DW1 = 5, K_UP8 = 6 };
+// K_UP8: the up-projection with e4m3 operands (SONIC_F_FP8_UP, NEXT-4): Gather(Xq) W1q_e with the
+// per-token scale sx and per-column scale sw applied to the fp32 sum in the epilogue, which is then
+// K_UP's (H, A in bf16).  A k-block is 128 e4m3 values: the same 128-byte rows, stages and
+// descriptors as bf16's 64; the MMA is kind::f8f6f4 (K = 32).
 
 struct GemmArgs {
   const int* num_m_tiles;   // varlen-M: device-resident count of 128-row tiles (R_pad / 128)
@@ -60,11 +64,14 @@ struct GemmArgs {
   unsigned long long* dbg;  // SONIC_TIMING builds only: cycle counters (see sonic_api.cu)
   int accumulate;           // DW1 / DW2: add into the existing dW (SONIC_F_DW_ACCUMULATE) instead of overwriting
   int dw_bf16;              // DW1 / DW2: store dW as bf16 (SONIC_F_DW_BF16; the store map is then bf16)
+  const float* sx;          // UP8: per-token scale of the e4m3 X rows [T]
+  const float* sw;          // UP8: per-column scale of the e4m3 W1 [E, 2n]
 };
 
 template <int KIND>
 struct Traits;
 template <> struct Traits<K_UP>   { static constexpr bool vk = false, a_gather = true,  a_mn = false, b_gather = false, b_mn = true;  };
+template <> struct Traits<K_UP8>  { static constexpr bool vk = false, a_gather = true,  a_mn = false, b_gather = false, b_mn = true;  };
 template <> struct Traits<K_DOWN> { static constexpr bool vk = false, a_gather = false, a_mn = false, b_gather = false, b_mn = true;  };
 template <> struct Traits<K_DH>   { static constexpr bool vk = false, a_gather = true,  a_mn = false, b_gather = false, b_mn = false; };
 template <> struct Traits<K_DXT>  { static constexpr bool vk = false, a_gather = false, a_mn = false, b_gather = false, b_mn = false; };
@@ -325,6 +332,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   // bytes landing through TMA per stage per CTA (the non-gathered operands)
   constexpr uint32_t TMA_BYTES = !GATHER ? STAGE_BYTES : (Tr::a_gather ? Cfg::B_BYTES : A_BYTES);
   constexpr int MMA_M = CTA2 ? 2 * GEMM_BM : GEMM_BM;
+  constexpr bool F8 = KIND == K_UP8;  // e4m3 operands (kind::f8f6f4)
+  constexpr int ESZ = F8 ? 1 : 2;     // bytes per operand element
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -447,10 +456,11 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       for (int tile = t_first; tile < total_tiles; tile += t_step) {
         const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);
         const int n0 = tc.nt * BN + rank * BNL;
-        const __nv_bfloat16* srcM[8];
+        const uint8_t* srcM[8];  // byte addresses: a k-block is 128 bytes of a row (64 bf16 / 128 e4m3)
         if constexpr (!Tr::vk) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) srcM[j] = args.gsrc + clamp_tok(ntok[j]) * args.gld + c * 8;
+          for (int j = 0; j < 8; ++j)
+            srcM[j] = reinterpret_cast<const uint8_t*>(args.gsrc) + clamp_tok(ntok[j]) * args.gld * ESZ + c * 16;
           if (tile + t_step < total_tiles) {
             const TileCoord tn = decode_tile<KIND, CTA2, MFAST>(args, tile + t_step, rank);
 #pragma unroll
@@ -498,7 +508,10 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           uint64_t* bar = &full[stage];
           if (pt == 0) {
             if (leader) ptx::mbar_arrive_expect_tx(bar, TMA_BYTES * (CTA2 ? 2 : 1));
-            if constexpr (KIND == K_UP) {
+            if constexpr (KIND == K_UP8) {  // one e4m3 box: 128 columns (128 B) x 128 K-rows, MN-major
+              static_assert(BN == 256 && CTA2, "the e4m3 up-projection runs as 2-CTA pairs of 256 columns");
+              tload3<true>(sB, &mB, bar, (rank ? args.n : 0) + tc.nt * (BN / 2), kb * 128, tc.e);
+            } else if constexpr (KIND == K_UP) {
               constexpr int W = BN / 2;  // gate columns per tile; the up columns follow at +n
               if constexpr (W >= 64) {
                 const int j0 = tc.nt * W;
@@ -542,12 +555,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             if constexpr (SONIC_L2PF > 0) {
               if (c == 0 && kb + SONIC_L2PF < tc.nkb) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) ptx::prefetch_l2(srcM[j] + (kb + SONIC_L2PF) * GEMM_BK);
+                for (int j = 0; j < 8; ++j) ptx::prefetch_l2(srcM[j] + (kb + SONIC_L2PF) * 128);
               }
             }
             const uint32_t dst = ptx::smem_u32(sA) + r0 * 128 + sw;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) gather16(dst + j * 16 * 128, srcM[j] + kb * GEMM_BK, gpol);
+            for (int j = 0; j < 8; ++j) gather16(dst + j * 16 * 128, srcM[j] + kb * 128, gpol);
           } else {  // 64 gathered K-rows x (128 | BNL) MN-columns (MN-major)
             constexpr int NCH = Tr::a_gather ? 2 : BNL / 64;
             const uint32_t dst = ptx::smem_u32(Tr::a_gather ? sA : sB) + r0 * 128 + sw;
@@ -568,7 +581,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   } else if (warp == NP) {
     // ============================================================ MMA issuer (leader) / relay (peer)
     if (lane == 0 && leader) {
-      constexpr uint32_t idesc = ptx::make_idesc(MMA_M, BN, Tr::a_mn ? 1 : 0, Tr::b_mn ? 1 : 0);
+      constexpr uint32_t idesc = F8 ? ptx::make_idesc_e4m3(MMA_M, BN, Tr::a_mn ? 1 : 0, Tr::b_mn ? 1 : 0)
+                                    : ptx::make_idesc(MMA_M, BN, Tr::a_mn ? 1 : 0, Tr::b_mn ? 1 : 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -606,10 +620,18 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           for (int k = 0; k < GEMM_BK / 16; ++k) {
             const uint64_t ad = Tr::a_mn ? ptx::make_sdesc(a_base + k * 2048, 8192, 1024)
                                          : ptx::make_sdesc(a_base + k * 32, 16, 1024);
-            const uint64_t bd = Tr::b_mn ? ptx::make_sdesc(b_base + k * 2048, 8192, 1024)
+            // MN-major B: one MMA step is 16 (bf16) or 32 (e4m3) K-rows of 128 bytes; a 128-byte MN
+            // chunk spans 64 (bf16) K-rows x ... or, for e4m3, the whole 128-row k-block
+            const uint64_t bd = Tr::b_mn ? (F8 ? ptx::make_sdesc(b_base + k * 4096, 16384, 1024)
+                                               : ptx::make_sdesc(b_base + k * 2048, 8192, 1024))
                                          : ptx::make_sdesc(b_base + k * 32, 16, 1024);
-            if constexpr (CTA2) ptx::mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
-            else ptx::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            if constexpr (F8) {
+              if constexpr (CTA2) ptx::mma_f8_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              else ptx::mma_f8(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            } else {
+              if constexpr (CTA2) ptx::mma_bf16_cg2(d_tmem, ad, bd, idesc, (kb | k) != 0);
+              else ptx::mma_bf16(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            }
           }
           if constexpr (CTA2) ptx::mma_commit_mc(&empty[stage], MC ? (uint16_t)0xF : pmask);
           else ptx::mma_commit(&empty[stage]);
@@ -768,12 +790,24 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           hphase ^= 1;
           if (has_next) h_issue(tile + t_step);
         }
-      } else if constexpr (KIND == K_UP) {
+      } else if constexpr (KIND == K_UP || KIND == K_UP8) {
         constexpr int W = BN / 2;
+        // UP8: H = acc * sx[token] * sw[e][column] (the scales of the e4m3 operands, NEXT-4)
+        float sxr = 1.f;
+        if constexpr (F8) sxr = __ldg(args.sx + clamp_tok(__ldg(args.row_token + row)));
         if constexpr (W >= 64) {
 #pragma unroll 1
           for (int c = 64 * half; c < W; c += 64 * Cfg::EPH) {
             const int col = tc.nt * W + c;
+            float swg[2] = {1.f, 1.f}, swu[2] = {1.f, 1.f};  // lane j holds the scales of columns j, 32 + j
+            if constexpr (F8) {
+              const float* swe = args.sw + (size_t)tc.e * 2 * args.n;
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                swg[h] = __ldg(swe + col + 32 * h + lane);
+                swu[h] = __ldg(swe + args.n + col + 32 * h + lane);
+              }
+            }
             sq.template acquire<1>(lane);  // the next two ring slots are both free
             const int i0 = sq.sb;
             const int i1 = (i0 + 1) % Cfg::NB;
@@ -790,8 +824,13 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
                 float hg[8], hu[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                  hg[i] = bf16r(__uint_as_float(g[8 * q8 + i]));
-                  hu[i] = bf16r(__uint_as_float(u[8 * q8 + i]));
+                  float vg = __uint_as_float(g[8 * q8 + i]), vu = __uint_as_float(u[8 * q8 + i]);
+                  if constexpr (F8) {
+                    vg *= sxr * __shfl_sync(0xffffffffu, swg[h], 8 * q8 + i);
+                    vu *= sxr * __shfl_sync(0xffffffffu, swu[h], 8 * q8 + i);
+                  }
+                  hg[i] = bf16r(vg);
+                  hu[i] = bf16r(vu);
                 }
                 const int ch = 4 * h + q8;
                 ptx::st_shared_v4(b0 + swz(lane, ch), ptx::pack_bf16(hg[0], hg[1]), ptx::pack_bf16(hg[2], hg[3]),

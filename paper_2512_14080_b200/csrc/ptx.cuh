@@ -248,6 +248,14 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo_byte
   return d;
 }
 // Instruction descriptor, kind::f16: bf16 x bf16 -> fp32, M x N, majors (0 = K, 1 = MN).
+// kind::f8f6f4 with A, B = E4M3 (format 0), D = f32
+__host__ __device__ constexpr uint32_t make_idesc_e4m3(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4)                      // D format f32
+         | ((uint32_t)a_mn << 15)       // A major (A / B format 0 = E4M3)
+         | ((uint32_t)b_mn << 16)       // B major
+         | ((uint32_t)(N >> 3) << 17)   // N / 8
+         | ((uint32_t)(M >> 4) << 24);  // M / 16
+}
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N, int a_mn, int b_mn) {
   return (1u << 4)                      // D format f32
          | (1u << 7)                    // A format bf16
@@ -326,6 +334,30 @@ __device__ __forceinline__ void mma_bf16_cg2(uint32_t tmem_d, uint64_t adesc, ui
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// FP8 (e4m3 x e4m3 -> fp32, K = 32 per instruction), pair form; the descriptors are laid out as
+// for bf16 (a 128-byte K-major row holds 128 e4m3 values instead of 64 bf16).
+__device__ __forceinline__ void mma_f8_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_f8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");

@@ -89,6 +89,18 @@ bool map2d(CUtensorMap* m, const void* ptr, bool f32, long long rows, long long 
              gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// 3-D row-major [E, rows, cols] bytes (e4m3); box {box_cols, box_rows, 1}; 128B swizzle.
+bool map3d_u8(CUtensorMap* m, const void* ptr, long long E, long long rows, long long cols, int box_cols, int box_rows) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t gdim[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)E};
+  cuuint64_t gstride[2] = {(cuuint64_t)cols, (cuuint64_t)(rows * cols)};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(ptr), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 // 3-D row-major [E, rows, cols] tensor; box {box_cols, box_rows, 1}; 128B swizzle.
 bool map3d(CUtensorMap* m, const void* ptr, bool f32, long long E, long long rows, long long cols, int box_cols,
            int box_rows) {
@@ -224,21 +236,26 @@ bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUten
   const CUtensorMap& d = dmap ? *dmap : c0;
   const bool cta2 = use_cta2(BN);
   if (cta2) grid = std::max(2, grid & ~1);  // a pair needs both CTAs, even for a single pair tile
-  if constexpr (KIND == K_DOWN || KIND == K_DXT || KIND == K_DW2 || KIND == K_DW1) {
-    if (SONIC_MC4 && mc && cta2 && BN == 256) return launch_gemm_t<KIND, 256, true, true>(a, b, c0, c1, d, args, grid, st);
-  }
-  switch (BN) {
-    case 256:
-      return cta2 ? launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st)
-                       : launch_gemm_t<KIND, 256, false>(a, b, c0, c1, d, args, grid, st);
-    case 128:
-      return cta2 ? launch_gemm_t<KIND, 128, true>(a, b, c0, c1, d, args, grid, st)
-                  : launch_gemm_t<KIND, 128, false>(a, b, c0, c1, d, args, grid, st);
-    case 64: return launch_gemm_t<KIND, 64, false>(a, b, c0, c1, d, args, grid, st);
-    case 32:
-      if constexpr (KIND == K_DH) return launch_gemm_t<KIND, 32, false>(a, b, c0, c1, d, args, grid, st);
-      return false;
-    default: return false;
+  if constexpr (KIND == K_UP8) {  // e4m3: 2-CTA pairs of 256 columns only (fp8_up_ok)
+    return cta2 && BN == 256 && launch_gemm_t<K_UP8, 256, true>(a, b, c0, c1, d, args, grid, st);
+  } else {
+    if constexpr (KIND == K_DOWN || KIND == K_DXT || KIND == K_DW2 || KIND == K_DW1) {
+      if (SONIC_MC4 && mc && cta2 && BN == 256)
+        return launch_gemm_t<KIND, 256, true, true>(a, b, c0, c1, d, args, grid, st);
+    }
+    switch (BN) {
+      case 256:
+        return cta2 ? launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st)
+                    : launch_gemm_t<KIND, 256, false>(a, b, c0, c1, d, args, grid, st);
+      case 128:
+        return cta2 ? launch_gemm_t<KIND, 128, true>(a, b, c0, c1, d, args, grid, st)
+                    : launch_gemm_t<KIND, 128, false>(a, b, c0, c1, d, args, grid, st);
+      case 64: return launch_gemm_t<KIND, 64, false>(a, b, c0, c1, d, args, grid, st);
+      case 32:
+        if constexpr (KIND == K_DH) return launch_gemm_t<KIND, 32, false>(a, b, c0, c1, d, args, grid, st);
+        return false;
+      default: return false;
+    }
   }
 }
 
@@ -395,15 +412,26 @@ bool fused_updown(const sonic_moe_desc* D) {
          D->d % 128 == 0;
 }
 
-struct FwdWs { size_t A, Y, total; bool fused; };
+// SONIC_F_FP8_UP (NEXT-4): the up-projection on e4m3 operands; needs the 2-CTA 256-column UP tile
+// (n % 128 == 0) and whole 128-element k-blocks (d % 128 == 0); not with the fused up/down kernel
+bool fp8_up(const sonic_moe_desc* D) { return (D->flags & SONIC_F_FP8_UP) != 0; }
+bool fp8_up_ok(const sonic_moe_desc* D) { return use_cta2(256) && D->n % 128 == 0 && D->d % 128 == 0; }
+struct FwdWs { size_t A, Y, Xq, sx, W1q, sw, total; bool fused; };
 FwdWs fwd_ws(const sonic_moe_desc* D) {
   const Shape s = shape_of(D);
   FwdWs w;
   size_t o = 0;
-  w.fused = fused_updown(D);
+  w.fused = fused_updown(D) && !fp8_up(D);
   w.A = w.fused ? SIZE_MAX : o;  // fused: A never leaves the SM
   if (!w.fused) o += al((size_t)s.rows_max * s.n * 2);
   w.Y = o; o += al((size_t)s.rows_max * s.d * 2);
+  w.Xq = w.sx = w.W1q = w.sw = SIZE_MAX;
+  if (fp8_up(D)) {  // e4m3 copies of X and W1 and their scales
+    w.Xq = o; o += al((size_t)s.T * s.d);
+    w.sx = o; o += al((size_t)s.T * 4);
+    w.W1q = o; o += al((size_t)s.E * s.d * 2 * s.n);
+    w.sw = o; o += al((size_t)s.E * 2 * s.n * 4);
+  }
   w.total = o;
   return w;
 }
@@ -600,6 +628,7 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
   g_launches = 0;
   if (!valid_desc(D) || !X || !W1 || !W2 || !rt || !O || !H) return SONIC_ERR_INVALID_ARG;
   if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
+  if (fp8_up(D) && !fp8_up_ok(D)) return SONIC_ERR_UNSUPPORTED;
   const FwdWs w = fwd_ws(D);
   if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
   for (const void* p : {X, W1, W2, (const void*)O, (const void*)H, (const void*)ws})
@@ -635,8 +664,35 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
                                              : launch_updown<1, 128>(mW1, mW2, mH, mY, a, grid, st));
     if (!ok) return SONIC_ERR_CUDA;
   }
+  // K1 up-proj on e4m3 operands (SONIC_F_FP8_UP): quantise X per token and W1 per output column,
+  // then H = (Gather(Xq) W1q_e) * sx * sw in the epilogue (NEXT-4)
+  if (fp8_up(D)) {
+    uint8_t* Xq = base + w.Xq;
+    float* sx = reinterpret_cast<float*>(base + w.sx);
+    uint8_t* W1q = base + w.W1q;
+    float* sw = reinterpret_cast<float*>(base + w.sw);
+    {
+      ProfScope ps("quant_fp8", st);
+      launch_quant_rows_e4m3(X, s.T, d, Xq, sx, st);
+      ++g_launches;
+      if (!(D->flags & SONIC_F_FP8_W1_CACHED)) {
+        launch_quant_cols_e4m3(W1, E, d, 2 * n, W1q, sw, st);
+        g_launches += 3;  // columns: amax, quantise, amax -> scale
+      }
+    }
+    CUtensorMap mA, mB, mC0, mC1;
+    if (!map2d(&mA, X, false, s.T, d, 64, 1) || !map3d_u8(&mB, W1q, E, d, 2 * n, 128, 128) ||
+        !map2d(&mC0, H, false, R, 2 * n, 64, 32) || !map2d(&mC1, Abuf, false, R, n, 64, 32))
+      return SONIC_ERR_CUDA;
+    GemmArgs a = g;
+    a.n_tiles = n / 128; a.k_blocks = d / 128; a.N_dim = 2 * n;
+    a.gsrc = reinterpret_cast<const __nv_bfloat16*>(Xq); a.gld = d;  // e4m3 rows (gathered by byte address)
+    a.sx = sx; a.sw = sw;
+    ProfScope ps("up", st);
+    if (!launch_gemm<K_UP8>(256, mA, mB, mC0, mC1, a, grid, st)) return SONIC_ERR_CUDA;
+  }
   // K1 up-proj: H = Gather(X) W1_e, SwiGLU epilogue -> H, A
-  if (!w.fused) {
+  if (!w.fused && !fp8_up(D)) {
     CUtensorMap mA, mB, mC0, mC1;
     const int Wg = n % 128 == 0 ? 128 : n % 64 == 0 ? 64 : 32;
     const int BN = 2 * Wg;

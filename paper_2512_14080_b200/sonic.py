@@ -35,6 +35,8 @@ SONIC_F_BWD_DW_ONLY = 16
 SONIC_F_DW_BF16 = 32
 SONIC_F_NO_FUSED_UPDOWN = 64
 SONIC_F_FUSED_UPDOWN = 128
+SONIC_F_FP8_UP = 256
+SONIC_F_FP8_W1_CACHED = 512
 GEMM_M = 128
 
 ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",
@@ -89,6 +91,10 @@ def lib():
         L.sonic_route.restype = ctypes.c_int
         L.sonic_route_logits.argtypes = [P(sonic_moe_desc), vp, vp, P(sonic_routing), vp, sz, vp]
         L.sonic_route_logits.restype = ctypes.c_int
+        L.sonic_quantize_e4m3_rows.argtypes = [vp, ctypes.c_int64, ctypes.c_int32, vp, vp, vp]
+        L.sonic_quantize_e4m3_rows.restype = ctypes.c_int
+        L.sonic_quantize_e4m3_cols.argtypes = [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp, vp]
+        L.sonic_quantize_e4m3_cols.restype = ctypes.c_int
         L.sonic_router_fwd.argtypes = [P(sonic_moe_desc), vp, vp, vp, vp]
         L.sonic_router_fwd.restype = ctypes.c_int
         L.sonic_router_grad_workspace_size.argtypes = [P(sonic_moe_desc)]
@@ -312,6 +318,24 @@ def sonic_router_bwd(desc, S, rt, dS, dlogits=None):
     _done(lib().sonic_router_bwd(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(dS), _ptr(dlogits),
                                  _stream()), "sonic_router_bwd")
     return dlogits
+
+
+def sonic_quantize_e4m3_rows(X):
+    """X [rows, cols] bf16 -> (q [rows, cols] uint8 e4m3 codes, scale [rows] fp32)."""
+    q = torch.empty(X.shape, dtype=torch.uint8, device=X.device)
+    s = torch.empty(X.shape[0], dtype=torch.float32, device=X.device)
+    _done(lib().sonic_quantize_e4m3_rows(_ptr(X), X.shape[0], X.shape[1], _ptr(q), _ptr(s), _stream()),
+          "sonic_quantize_e4m3_rows")
+    return q, s
+
+
+def sonic_quantize_e4m3_cols(W):
+    """W [batch, K, N] bf16 -> (q [batch, K, N] uint8 e4m3 codes, scale [batch, N] fp32)."""
+    q = torch.empty(W.shape, dtype=torch.uint8, device=W.device)
+    s = torch.empty(W.shape[0], W.shape[2], dtype=torch.float32, device=W.device)
+    _done(lib().sonic_quantize_e4m3_cols(_ptr(W), W.shape[0], W.shape[1], W.shape[2], _ptr(q), _ptr(s), _stream()),
+          "sonic_quantize_e4m3_cols")
+    return q, s
 
 
 def sonic_router_fwd(desc, X, Wr, logits=None):

@@ -200,6 +200,12 @@ class _Lazy:
 
 
 def stream_parity(desc, inp, g, rto, check_ws=True):
+    """(see _stream_parity)"""
+    return _stream_parity(desc, inp, g, rto, check_ws=check_ws,
+                          fp8_up=bool(desc.flags & getattr(sonic, "SONIC_F_FP8_UP", 0)))
+
+
+def _stream_parity(desc, inp, g, rto, check_ws=True, fp8_up=False):
     """Element-by-element parity of every output, one expert at a time (the oracle's per-expert
     stages ``expert_forward`` / ``expert_backward``, pinned in tests/test_oracle.py), so that the
     full BASELINE sizes fit in host memory.  Every routed row, token and weight element is compared;
@@ -213,6 +219,8 @@ def stream_parity(desc, inp, g, rto, check_ws=True):
     names = ["H", "dW1", "dW2", "dS"] + (["A", "dH", "Ap"] if check_ws else [])
     acc = {k: ErrAcc(k) for k in names}
     have_A = check_ws and g.get("A") is not None
+    if fp8_up:  # SONIC_F_FP8_UP: the oracle's e4m3 operands (per token row of X, per column of W1_e)
+        Xq, sx = om.quantize_e4m3(X, axis=1)
     for e in range(E):
         lo = int(rto.pad_offsets[e])
         fe = int(rto.f_rounded[e])
@@ -220,7 +228,11 @@ def stream_parity(desc, inp, g, rto, check_ws=True):
         toks = rto.row_token[lo: lo + fe]
         ge = rto.row_gate[lo: lo + fe]
         Xe, dOe = X[toks], dO[toks]
-        He, Ae, Ye = om.expert_forward(Xe, W1[e], W2[e], ge)
+        if fp8_up:
+            W1q_e, sw_e = om.quantize_e4m3(W1[e], axis=0)
+            He, Ae, Ye = om.expert_forward_fp8(Xq[toks], sx[toks], W1q_e, sw_e, W2[e], ge)
+        else:
+            He, Ae, Ye = om.expert_forward(Xe, W1[e], W2[e], ge)
         gr = om.expert_backward(dOe, Xe, W1[e], W2[e], ge, He)
         np.add.at(O_ref, toks, Ye)
         np.add.at(dX_ref, toks, gr.dXt)

@@ -373,3 +373,66 @@ def test_router_full_chain():
     assert_close("dlogits", f(dlog), dlog_ref)
     assert_close("dX (experts + router)", f(dX), bw.dX + dXr)
     assert_close("dWr", f(dWr), dWr_ref)
+
+
+# NEXT-4: FP8 (e4m3) up-projection, SONIC_F_FP8_UP
+def test_quantize_e4m3_bit_exact():
+    """The library's e4m3 quantisation equals the oracle's bit for bit: the codes (through torch's
+    float8_e4m3fn view) and the fp32 scales, per token row of X and per output column of W1_e
+    (zero rows / columns get scale 1 and zero codes)."""
+    import numpy as np
+    from oracle import moe_oracle as om
+    g = torch.Generator(device="cuda").manual_seed(3)
+    X = (torch.randn(1000, 1536, device="cuda", generator=g) * torch.exp(torch.randn(1000, 1, device="cuda",
+                                                                                      generator=g))).bfloat16()
+    X[7] = 0
+    W = (torch.randn(8, 256, 512, device="cuda", generator=g) * 0.05).bfloat16()
+    W[2, :, 17] = 0
+    xq, sx = sonic.sonic_quantize_e4m3_rows(X)
+    wq, sw = sonic.sonic_quantize_e4m3_cols(W)
+    torch.cuda.synchronize()
+    to_f = lambda q: q.view(torch.float8_e4m3fn).float().cpu().numpy()
+    oq, osx = om.quantize_e4m3(X.float().cpu().numpy(), axis=1)
+    np.testing.assert_array_equal(to_f(xq), oq)
+    np.testing.assert_array_equal(sx.cpu().numpy(), osx.astype(np.float32))
+    oq, osw = om.quantize_e4m3(W.float().cpu().numpy(), axis=1)
+    np.testing.assert_array_equal(to_f(wq), oq)
+    np.testing.assert_array_equal(sw.cpu().numpy(), osw.astype(np.float32))
+
+
+FP8_CASES = [
+    ("fp8_tc", 2048, 256, 128, 16, 4, "tc"),
+    ("fp8_tr", 2048, 256, 128, 16, 4, "tr"),
+    ("fp8_n256_ragged", 1000, 384, 256, 8, 2, "tc"),
+    ("fp8_7b_dims", 4096, 1536, 256, 8, 2, "tc"),
+]
+
+
+@pytest.mark.parametrize("case", FP8_CASES, ids=[c[0] for c in FP8_CASES])
+def test_fp8_up_parity(case):
+    """SONIC_F_FP8_UP: every output of route + fwd + bwd against the oracle whose up-projection
+    runs on the same e4m3 operands (forward(fp8_up=True); the backward through the cached H), within
+    the north-star criterion; the bf16 layer is only a quantisation error away (checked loosely)."""
+    name, T, d, n, E, K, mode = case
+    inp = make_inputs(T, d, n, E, K, seed=11, device="cuda")
+    m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
+    desc = sonic.make_desc(T, d, n, E, K, mode=m, flags=sonic.SONIC_F_FP8_UP)
+    stats = full_parity(desc, inp, mode=mode)
+    print(name, {k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
+
+
+def test_fp8_w1_cached_reuses_the_copy():
+    """SONIC_F_FP8_W1_CACHED reuses the e4m3 W1 left in the workspace by the previous call: the same
+    outputs as quantising again (same W1), and different from a call whose cached copy is stale."""
+    T, d, n, E, K = 2048, 256, 128, 16, 4
+    inp = make_inputs(T, d, n, E, K, seed=12, device="cuda")
+    d8 = sonic.make_desc(T, d, n, E, K, flags=sonic.SONIC_F_FP8_UP)
+    dc = sonic.make_desc(T, d, n, E, K, flags=sonic.SONIC_F_FP8_UP | sonic.SONIC_F_FP8_W1_CACHED)
+    rt = sonic.sonic_route(d8, inp.S)
+    O1, H1, ws = sonic.sonic_moe_fwd(d8, inp.X, inp.W1, inp.W2, rt)
+    O2, H2, _ = sonic.sonic_moe_fwd(dc, inp.X, inp.W1, inp.W2, rt, ws=ws)
+    O3, _, _ = sonic.sonic_moe_fwd(dc, inp.X, (inp.W1 * 2).contiguous(), inp.W2, rt, ws=ws)  # stale copy used
+    torch.cuda.synchronize()
+    R_pad = int(rt.pad_offsets[E])  # H rows past R_pad are never written
+    assert torch.equal(O1, O2) and torch.equal(H1[:R_pad], H2[:R_pad])
+    assert torch.equal(O1, O3)
