@@ -312,7 +312,7 @@ __device__ __forceinline__ void tload3(void* dst, const CUtensorMap* m, uint64_t
 // the L2 -> SM operand traffic per MMA drops by a quarter; a stage is refilled once BOTH pairs' MMAs
 // have released it (empty barriers count the two pair leaders' commits).
 #ifndef SONIC_DW1_MFAST
-#define SONIC_DW1_MFAST 1  // dW1 tiles in M-pair-fastest order (the 2 N tiles of an expert's dH slice run on neighbouring pairs): 372.7/373.9 -> 369.7/370.1 us at 7B
+#define SONIC_DW1_MFAST 1  // dW1 tiles M-pair-fastest: the d-slices of one (expert, N tile) run on neighbouring pairs, which read the same dH columns at the same time (7B: 372.7/373.9 -> 369.7/370.1 us)
 #endif
 template <int KIND, int BN, bool CTA2, bool MC = false>
 __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
