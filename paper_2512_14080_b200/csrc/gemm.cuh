@@ -311,6 +311,9 @@ __device__ __forceinline__ void tload3(void* dst, const CUtensorMap* m, uint64_t
 // pair).  Each pair TMA-loads half of the shared tile and multicasts it into both pairs' stage, so
 // the L2 -> SM operand traffic per MMA drops by a quarter; a stage is refilled once BOTH pairs' MMAs
 // have released it (empty barriers count the two pair leaders' commits).
+#ifndef SONIC_STREAM_EF
+#define SONIC_STREAM_EF 2  // evict-first hint on the streamed TMA operand of dW1 (1) / dW2 (2): dW2 213 -> 209 us, dW1 unchanged (7B, 3 reps)
+#endif
 #ifndef SONIC_DW1_MFAST
 #define SONIC_DW1_MFAST 1  // dW1 tiles M-pair-fastest: the d-slices of one (expert, N tile) run on neighbouring pairs, which read the same dH columns at the same time (7B: 372.7/373.9 -> 369.7/370.1 us)
 #endif
@@ -536,6 +539,9 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
               const int m0 = tc.valid ? tc.mt * GEMM_BM : 0;
               if constexpr (MC) {  // one of the two 64-column boxes, into both pairs
                 ptx::tma_load_2d_cg2_mc(sA + 8192 * pidx, &mA, bar, m0 + 64 * pidx, krow0, smask);
+              } else if constexpr (CTA2 && (SONIC_STREAM_EF & 2)) {  // A' streamed evict-first: keep dO's rows in L2
+                ptx::tma_load_2d_cg2_hint(sA, &mA, bar, m0, krow0, ptx::policy_evict_first());
+                ptx::tma_load_2d_cg2_hint(sA + 8192, &mA, bar, m0 + 64, krow0, ptx::policy_evict_first());
               } else {
                 tload2<CTA2>(sA, &mA, bar, m0, krow0);
                 tload2<CTA2>(sA + 8192, &mA, bar, m0 + 64, krow0);
@@ -547,7 +553,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
                 ptx::tma_load_2d_cg2_mc(sB + 8192 * pidx, &mB, bar, n0 + 64 * pidx, krow0, smask);
               } else {
 #pragma unroll
-                for (int j = 0; j < BNL / 64; ++j) tload2<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, krow0);
+                for (int j = 0; j < BNL / 64; ++j) {
+                  if constexpr (CTA2 && (SONIC_STREAM_EF & 1))  // dH streamed evict-first: keep X's rows in L2
+                    ptx::tma_load_2d_cg2_hint(sB + j * 8192, &mB, bar, n0 + 64 * j, krow0, ptx::policy_evict_first());
+                  else
+                    tload2<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, krow0);
+                }
               }
             }
           }

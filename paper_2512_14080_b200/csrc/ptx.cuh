@@ -305,6 +305,16 @@ __device__ __forceinline__ void tma_load_3d_cg2(void* dst, const CUtensorMap* ma
       "l"(map), "r"(leader_bar(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// Pair-form TMA load with an L2 eviction-priority hint (streamed operands marked evict-first so they
+// do not push the gathered rows out of L2)
+__device__ __forceinline__ void tma_load_2d_cg2_hint(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                     uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(leader_bar(bar)), "r"(c0), "r"(c1), "l"(policy)
+      : "memory");
+}
 // Pair-form TMA load multicast to every CTA in `mask` (same smem offset in each); the bytes are
 // counted on the mbarrier at the same offset in each destination CTA's pair leader.
 __device__ __forceinline__ void tma_load_2d_cg2_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
