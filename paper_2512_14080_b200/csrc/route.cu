@@ -994,7 +994,7 @@ template <int KT, int EPLMAX>
 __global__ void __launch_bounds__(256) k_topk_warp(const float* __restrict__ S, int T, int E, int W,
                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
                                                    uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket,
-                                                   float* __restrict__ S_out) {
+                                                   float* __restrict__ S_out, int* __restrict__ cnt_acc) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
@@ -1070,7 +1070,131 @@ __global__ void __launch_bounds__(256) k_topk_warp(const float* __restrict__ S, 
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < E; e += 256) bm_tc[(size_t)e * W + blockIdx.x] = words[e];
+  for (int e = threadIdx.x; e < E; e += 256) {
+    const uint32_t wd = words[e];
+    bm_tc[(size_t)e * W + blockIdx.x] = wd;
+    if (cnt_acc && wd) atomicAdd(cnt_acc + e, __popc(wd));  // f_e, for the one-pass TC build
+  }
+}
+
+// TC index build in ONE launch after k_topk_warp (whose count atomics give every f_e): block e
+// (1024 threads) takes the exclusive prefixes of f, of the 128-row padded counts and of the 2-CTA
+// pair counts over all experts (so each block knows its own offsets: no second grid-wide pass), then
+// builds its segment -- the gather map from a popcount scan of its bitmap words, its pad rows, its
+// tiles and tile pairs -- and, for every token of the segment, the token-CSR entry (the expert's
+// rank among the token's K, ascending) and the renormalised gate.  Same outputs as k_popc_offsets +
+// k_rows_tc.
+constexpr int TCB_THREADS = 256;  // k_tc_build: threads per block = bitmap words per block
+// SONIC_TC_BUILD1=1: the TC route in two launches (k_topk_warp with count atomics + k_tc_build instead of
+// k_popc_offsets + k_rows_tc).  Parity green, but measured slower at 7B (route 27.3 -> 35.0 us with one
+// block per expert, 39.0 us with 256-word blocks: the memset before the top-K breaks the PDL chain and
+// 1024 blocks' count atomics contend on E addresses), so the three-launch build stays the default.
+#ifndef SONIC_TC_BUILD1
+#define SONIC_TC_BUILD1 0
+#endif
+__global__ void __launch_bounds__(TCB_THREADS) k_tc_build(const uint32_t* __restrict__ bm, int W, const int* __restrict__ cnt_in,
+                                                   int E, int K, long long T, const int* __restrict__ topk_ids,
+                                                   const float* __restrict__ topk_s, int gate_raw, int* __restrict__ f,
+                                                   int* __restrict__ f_r, int* __restrict__ offsets,
+                                                   int* __restrict__ pad_offsets, int* __restrict__ row_token,
+                                                   float* __restrict__ row_gate, int* __restrict__ rowptr,
+                                                   int* __restrict__ token_rows, int* __restrict__ tile_expert,
+                                                   int* __restrict__ num_tiles, int* __restrict__ tile_pairs,
+                                                   int* __restrict__ num_pairs) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  __shared__ int s_off, s_pad, s_pair, s_tot_off, s_tot_pad, s_tot_pair;
+  const int e = blockIdx.x;
+  const int chunk = blockIdx.y;  // this block's words: [chunk * TCB_THREADS, +TCB_THREADS)
+  // prefixes over the experts (E <= TCB_THREADS here: one block scan)
+  {
+    const int x = threadIdx.x;
+    const int c = x < E ? __ldcg(cnt_in + x) : 0;
+    const int pc = (c + GEMM_M - 1) / GEMM_M * GEMM_M;
+    const int pp = (pc / GEMM_M + 1) / 2;
+    int t0, t1, t2;
+    const int ex = block_excl_scan(c, &t0);
+    const int pex = block_excl_scan(pc, &t1);
+    const int ppx = block_excl_scan(pp, &t2);
+    if (x == e) {
+      s_off = ex;
+      s_pad = pex;
+      s_pair = ppx;
+    }
+    if (x == 0) {
+      s_tot_off = t0;
+      s_tot_pad = t1;
+      s_tot_pair = t2;
+    }
+  }
+  __syncthreads();
+  const int cnt = __ldcg(cnt_in + e);
+  const int pad0 = s_pad, pc = (cnt + GEMM_M - 1) / GEMM_M * GEMM_M;
+  // rows of this expert before this block's words: popcount of the words [0, chunk * TCB_THREADS)
+  int before = 0;
+  {
+    int c = 0;
+    for (int w = threadIdx.x; w < chunk * TCB_THREADS; w += blockDim.x) c += __popc(bm[(size_t)e * W + w]);
+    int tot;
+    block_excl_scan(c, &tot);
+    before = tot;
+  }
+  if (threadIdx.x == 0 && chunk == 0) {
+    f[e] = cnt;
+    f_r[e] = cnt;
+    offsets[e] = s_off;
+    pad_offsets[e] = pad0;
+    if (e == E - 1) {
+      offsets[E] = s_tot_off;
+      pad_offsets[E] = s_tot_pad;
+      *num_tiles = s_tot_pad / GEMM_M;
+      *num_pairs = s_tot_pair;
+    }
+  }
+  if (chunk == 0) {
+    const int tiles_e = pc / GEMM_M, tile0 = pad0 / GEMM_M;
+    for (int i = threadIdx.x; i < tiles_e; i += blockDim.x) tile_expert[tile0 + i] = e;
+    for (int j = threadIdx.x; 2 * j < tiles_e; j += blockDim.x)
+      tile_pairs[s_pair + j] = (tile0 + 2 * j) | ((2 * j + 1 < tiles_e) ? (int)0x80000000u : 0);
+    for (int r = pad0 + cnt + threadIdx.x; r < pad0 + pc; r += blockDim.x) {  // pad rows of the last tile
+      row_token[r] = -1;
+      row_gate[r] = 0.f;
+    }
+  }
+  {
+    const long long nb = (long long)E * gridDim.y, b = (long long)chunk * E + e;
+    for (long long t = b + (long long)threadIdx.x * nb; t <= T; t += (long long)blockDim.x * nb)
+      rowptr[t] = (int)(t * K);  // TC: every token has K rows
+  }
+  // this block's part of the segment: ascending tokens from a popcount scan of its words
+  int base = pad0 + before;
+  {
+    const int w0 = chunk * TCB_THREADS;
+    const int w = w0 + threadIdx.x;
+    uint32_t bits = w < W ? bm[(size_t)e * W + w] : 0u;
+    int tot;
+    int r = base + block_excl_scan(__popc(bits), &tot);
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int t = w * 32 + b;
+      row_token[r] = t;
+      const int* ids = topk_ids + (size_t)t * K;
+      const float* sc = topk_s + (size_t)t * K;
+      int pos = 0;
+      float sum = 0.f, ms = 0.f;
+      for (int j = 0; j < K; ++j) {
+        const int id = ids[j];
+        pos += id < e;
+        sum += sc[j];
+        if (id == e) ms = sc[j];
+      }
+      const float inv = (gate_raw || sum == 0.f) ? 1.f : 1.f / sum;
+      token_rows[(size_t)t * K + pos] = r;
+      row_gate[r] = gate_raw ? ms : ms * inv;
+      ++r;
+    }
+  }
 }
 
 #ifndef SONIC_TOPK_WARP
@@ -1099,8 +1223,11 @@ int launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
     // with logits (sonic_route_logits) the softmax is fused here: reads logits, writes S, routes on S
     const float* in = L.logits ? L.logits : L.S;
     float* s_out = L.logits ? const_cast<float*>(L.S) : nullptr;
-    if (E <= 128) launch_k(k_topk_warp<KT, 4>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out);
-    else launch_k(k_topk_warp<KT, 8>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out);
+    // TC: the per-expert counts accumulate here (zeroed first) for the one-launch build, k_tc_build
+    int* acc = (SONIC_TC_BUILD1 && L.mode == 0 && E <= TCB_THREADS) ? L.tokcnt : nullptr;
+    if (acc) cudaMemsetAsync(acc, 0, (size_t)E * 4, st);
+    if (E <= 128) launch_k(k_topk_warp<KT, 4>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out, acc);
+    else launch_k(k_topk_warp<KT, 8>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out, acc);
     return 1;
   }
   int nl = 1;
@@ -1152,6 +1279,15 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
     return nl;
   }
   nl += launch_topk(L, st);  // K <= 16 (validated for TC / TR); + the row softmax with logits
+  if (SONIC_TC_BUILD1 && L.mode == 0 && SONIC_TOPK_WARP && E % 32 == 0 && E <= SONIC_TOPK_WARP_EMAX &&
+      E <= TCB_THREADS) {
+    // TC after the warp top-K: the whole index build in one launch (counts from the top-K's atomics)
+    launch_k(k_tc_build, dim3(E, (W + TCB_THREADS - 1) / TCB_THREADS), TCB_THREADS, 0, st, L.bm_tc, W,
+             (const int*)L.tokcnt, E, K, L.T, L.topk_ids, L.topk_s,
+             L.gate_raw, L.f, L.f_r, L.offsets, L.pad_offsets, L.row_token, L.row_gate, L.token_rowptr, L.token_rows,
+             L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs);
+    return nl + 1;
+  }
   const uint32_t* bm_kept = L.bm_tc;
   if (L.mode == 1 || L.mode == 3) {  // token rounding (any subroutine) or expert choice
     const bool ec = L.mode == 3;

@@ -382,7 +382,7 @@ RouteWs route_ws(const sonic_moe_desc* D) {
   w.bm_tc = o; o += bm;
   w.bm_kept = o; o += bm;
   w.wprefix = o; o += bm;
-  w.tokcnt = o; o += al((size_t)s.T * 4);
+  w.tokcnt = o; o += al((size_t)std::max<long long>(s.T, s.E) * 4);  // token counts (TR CSR) / expert counts (TC)
   w.flip = o; o += al((size_t)s.E * 4);
   w.ticket = o; o += al(8);  // [0] offsets ticket, [1] token-CSR ticket
   const bool needs_st = D->route_mode != SONIC_ROUTE_TC && D->route_mode != SONIC_ROUTE_GIVEN;
