@@ -203,7 +203,11 @@ def workload_config(args, cfg):
                         f"route={args.mode}",
             "T": cfg["T"], "d": cfg["d"], "n": cfg["n"], "E": cfg["E"], "K": cfg["K"], "route": args.mode,
             "parallelism": f"ep{args.gpus}" if (args.gpus > 1 or getattr(args, "ep", False)) else "single",
-            **({"ep_exchange": "peer-memory kernels (CUDA IPC)" if args.comm == "peer" else "NCCL all-to-all-v"}
+            **({"cuda_graph": "one step captured and replayed"} if getattr(args, "graph", False) else {}),
+            **({"ep_exchange": ("peer-memory kernels (CUDA IPC)" + (", host-sync-free (device offsets, capacity "
+                                                                    "2*T*K pairs)" if getattr(args, "sync_free", False)
+                                                                    else "")) if args.comm == "peer"
+                else "NCCL all-to-all-v"}
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
             **({"updown": "fused kernel (SONIC_F_FUSED_UPDOWN)"} if getattr(args, "fuse", False) else {}),
@@ -249,6 +253,11 @@ def main():
                     help="time the K steps back to back without flushing L2 (the primary number flushes)")
     ap.add_argument("--sustain-s", type=float, default=0.0,
                     help="also run the step back to back for this many seconds (sustained / power-capped regime)")
+    ap.add_argument("--sync-free", action="store_true",
+                    help="with --comm peer: the host-sync-free exchange (offsets read on the device, NEXT-2)")
+    ap.add_argument("--graph", action="store_true",
+                    help="capture one step in a CUDA graph and replay it in the timed passes (needs a step "
+                         "without host synchronisation: the single-GPU path, or --comm peer --sync-free)")
     ap.add_argument("--comm", default="nccl", choices=["nccl", "peer"],
                     help="EP exchange: NCCL all-to-all-v, or libsonic's peer-memory kernels (CUDA IPC / NVLink)")
     args = ap.parse_args()
@@ -352,7 +361,7 @@ def main():
         X, dOin, S = make_token_inputs(T, d, E, seed=args.seed + 17 * rank, device=dev)
         W1, W2 = make_expert_weights(rank * L, (rank + 1) * L, d, n, seed=args.seed, device=dev)
         if args.comm == "peer":
-            comm = ep.PeerComm(G, T, d, L, [rank])
+            comm = ep.PeerComm(G, T, d, L, [rank], sync_free=args.sync_free)
         else:
             comm = ep.DistComm() if world > 1 else ep.SimComm(1)
         rk = ep.EPRank(T, d, n, E, K, G, rank, W1, W2, mode=mode)
@@ -374,12 +383,24 @@ def main():
             lrt = rk.ctx["lrt"]
             return kernel_model(R_in, d, n, L, L, int(lrt.offsets[L].item()), int(lrt.pad_offsets[L].item()))
 
-    def step():
+    def step_eager():
         run(X, S, dOin)
 
+    step = step_eager
     for _ in range(max(args.warmup, 1)):  # >= 1 untimed step so R is known below
         step()
     torch.cuda.synchronize()
+    graph = None
+    if args.graph:
+        # the whole step as one CUDA graph (launch overhead and Python out of the timed region); the
+        # per-kernel breakdown pass below stays eager (its events are recorded by the library calls)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step_eager()
+        torch.cuda.synchronize()
+        step = graph.replay
+        step()
+        torch.cuda.synchronize()
     R, R_pad = routed_rows()
     flops_step = 18 * d * n * R
     flops_all = flops_step
@@ -441,7 +462,9 @@ def main():
             "clocks": clk_w, "l2": "not flushed (steps back to back)"}
     # per-kernel breakdown: a second pass of the same K steps with every launch bracketed by CUDA
     # events on its own stream (sonic_profile_*), so the headline above carries no instrumentation
+    step = step_eager  # the breakdown pass: per-launch events need the eager calls
     ms_p, clk_p, recs, _ = timed_pass(False, profile=True)
+    step = graph.replay if graph is not None else step_eager
     sustained = None
     if args.sustain_s > 0:
         # seconds-long back-to-back run: the regime the sustained (power-capped) peak describes
@@ -518,6 +541,10 @@ def main():
         # gates out, Y partial sums back; backward dO rows out, dX~ partial sums + dS back
         G_ = world
         sc, rc = rk.ctx["counts"], rk.ctx["recv_counts"]
+        if sc is None:  # host-sync-free exchange: read the count matrix now, outside the timed region
+            Mfull = comm.regions[0].view(comm.lay["counts"], (G_, comm.NB * G_), torch.int32).cpu().tolist()
+            sc = Mfull[rank][:G_]
+            rc = [Mfull[s_][rank] for s_ in range(G_)]
         s_off = sum(c for g, c in enumerate(sc) if g != rank)
         r_off = sum(c for g, c in enumerate(rc) if g != rank)
         L_ = E // G_

@@ -183,6 +183,17 @@ sonic_status sonic_route(const sonic_moe_desc *desc, const float *S, sonic_routi
                          void *ws, size_t ws_bytes, void *stream);
 
 /*
+ * sonic_route_given_capped -- SONIC_ROUTE_GIVEN routing whose routed pairs may exceed the descriptor's
+ * rows_cap (the host-sync-free expert-parallel receive side, NEXT-2, sizes its buffers from a
+ * capacity instead of the exact received count).  Counts the pairs first; within rows_cap it is
+ * exactly sonic_route and *overflow = 0; beyond it the routing is made EMPTY (no rows: nothing is
+ * written out of bounds and the GEMMs / aggregation of that step do nothing) and *overflow = 1 --
+ * the caller must treat the step as invalid (re-run it with exact sizing).  overflow: device int.
+ */
+sonic_status sonic_route_given_capped(const sonic_moe_desc *desc, const float *S, sonic_routing *out, void *ws,
+                                      size_t ws_bytes, int *overflow, void *stream);
+
+/*
  * sonic_route_logits -- sonic_route with the router softmax fused in ("an optional softmax
  * fusion ... within the top-K kernel"; SURVEY 8(b) SONIC_F_FUSED_SOFTMAX).
  *   logits [T,E] fp32 router logits (finite, Q24), read once.
@@ -385,6 +396,29 @@ sonic_status sonic_ep_pack_peer(const sonic_moe_desc *desc, int G, const sonic_e
 sonic_status sonic_peer_put_rows(const sonic_peer *peer, int G, const void *src, size_t row_bytes,
                                  const int32_t *src_row0, const int32_t *cnt, const int32_t *dst_row0,
                                  size_t region_off, void *stream);
+
+/*
+ * Host-sync-free variants (NEXT-2): the block offsets are read on the device from the count matrix
+ * at byte offset counts_off of the rank's OWN region (row s = the vector rank s stored in the count
+ * exchange; M[s][g] = rows s sends g = the first G of its count_cols int32), so no host read of the
+ * counts is needed and the calls can be captured in a CUDA graph.  Same stores as the host-offset
+ * versions.
+ *   sonic_ep_pack_peer_dev:  dispatch, dst_row0[g] = sum_{s < rank} M[s][g].
+ *   sonic_peer_put_rows_dev: direction 0 (dispatch, rank -> g): rows [sum_{g'<g} M[rank][g'],
+ *       +M[rank][g]) of src to rows [sum_{s<rank} M[s][g], ...) of rank g; direction 1 (return,
+ *       rank = destination, g = source): rows [sum_{s<g} M[s][rank], +M[g][rank]) to rows
+ *       [sum_{g'<rank} M[g][g'], ...) of rank g.  The caller sizes the regions for the worst case
+ *       (T*G rows per array, as PeerComm does); blocks are not bounds-checked on the host.
+ *   sonic_peer_zero_tail: zero rows [R_in, cap_rows) of the own-region array at region_off, R_in =
+ *       sum_s M[s][rank] (stale rows of an earlier step past this step's received rows).
+ */
+sonic_status sonic_ep_pack_peer_dev(const sonic_moe_desc *desc, int G, const sonic_ep_plan *plan, const void *src,
+                                    const sonic_peer *peer, size_t region_off, size_t counts_off, int count_cols,
+                                    void *stream);
+sonic_status sonic_peer_put_rows_dev(const sonic_peer *peer, int G, const void *src, size_t row_bytes, int direction,
+                                     size_t counts_off, int count_cols, size_t region_off, void *stream);
+sonic_status sonic_peer_zero_tail(const sonic_peer *peer, int G, size_t row_bytes, size_t counts_off, int count_cols,
+                                  size_t region_off, long long cap_rows, void *stream);
 
 #ifdef __cplusplus
 }

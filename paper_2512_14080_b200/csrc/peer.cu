@@ -92,6 +92,68 @@ __global__ void k_put_rows(const char* __restrict__ src, size_t row_bytes, PeerP
   __threadfence_system();
 }
 
+// ---------------------------------------------------------------- host-sync-free variants (NEXT-2)
+// The block offsets come from the count matrix M in the rank's OWN region (every rank stored its
+// row there in the count exchange): M[s][g] = rows s sends g = cnt[s * cols + g].
+__device__ __forceinline__ int cm(const int* cnt, int cols, int s, int g) { return __ldcg(cnt + (size_t)s * cols + g); }
+
+// Dispatch as k_pack_peer; destination row dst_row0[g] = sum_{s < me} M[s][g], computed here.
+__global__ void k_pack_peer_dev(const __nv_bfloat16* __restrict__ src, const int* __restrict__ send_token,
+                                const int* __restrict__ send_offsets, int G, int d, PeerPtrs P, size_t off,
+                                const int* __restrict__ cnt, int cols, int me) {
+  const long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i < __ldg(send_offsets + G)) {
+    int g = 0;
+    while (g + 1 < G && i >= __ldg(send_offsets + g + 1)) ++g;
+    long long dst0 = 0;
+    for (int s = 0; s < me; ++s) dst0 += cm(cnt, cols, s, g);
+    const long long drow = dst0 + (i - __ldg(send_offsets + g));
+    const uint4* sp = reinterpret_cast<const uint4*>(src + (size_t)__ldg(send_token + i) * d);
+    uint4* o = reinterpret_cast<uint4*>(P.base[g] + off + (size_t)drow * d * 2);
+    for (int c = lane; c < d / 8; c += 32) o[c] = sp[c];
+  }
+  __threadfence_system();
+}
+
+// Block put with the blocks from M (blockIdx.y = g): dir 0 (dispatch, me -> g): rows
+// [sum_{g'<g} M[me][g'], +M[me][g]) of src to rows [sum_{s<me} M[s][g], ...) of rank g; dir 1 (return,
+// me is the destination, g the source): rows [sum_{s<g} M[s][me], +M[g][me]) to rows
+// [sum_{g'<me} M[g][g'], ...) of rank g.
+template <typename V>
+__global__ void k_put_rows_dev(const char* __restrict__ src, size_t row_bytes, PeerPtrs P, size_t off,
+                               const int* __restrict__ cnt, int cols, int me, int G, int dir) {
+  const int g = blockIdx.y;
+  long long src0 = 0, dst0 = 0;
+  int n;
+  if (dir == 0) {
+    n = cm(cnt, cols, me, g);
+    for (int j = 0; j < g; ++j) src0 += cm(cnt, cols, me, j);
+    for (int s = 0; s < me; ++s) dst0 += cm(cnt, cols, s, g);
+  } else {
+    n = cm(cnt, cols, g, me);
+    for (int s = 0; s < g; ++s) src0 += cm(cnt, cols, s, me);
+    for (int j = 0; j < me; ++j) dst0 += cm(cnt, cols, g, j);
+  }
+  const size_t nv = (size_t)n * row_bytes / sizeof(V);
+  const V* sp = reinterpret_cast<const V*>(src + (size_t)src0 * row_bytes);
+  V* o = reinterpret_cast<V*>(P.base[g] + off + (size_t)dst0 * row_bytes);
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += (size_t)gridDim.x * blockDim.x)
+    o[j] = sp[j];
+  __threadfence_system();
+}
+
+// Zero rows [R_in, cap_rows) of an own-region array, R_in = sum_s M[s][me] (the rows received this
+// step): stale rows of an earlier step must not look routed to the capacity-sized receive side.
+__global__ void k_zero_tail(char* __restrict__ base, size_t row_bytes, const int* __restrict__ cnt, int cols, int me,
+                            int G, long long cap_rows) {
+  long long r_in = 0;
+  for (int s = 0; s < G; ++s) r_in += cm(cnt, cols, s, me);
+  const size_t b0 = (size_t)r_in * row_bytes, b1 = (size_t)cap_rows * row_bytes;
+  for (size_t j = b0 / 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < b1 / 4; j += (size_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint32_t*>(base)[j] = 0u;
+}
+
 }  // namespace sonic
 
 using namespace sonic;
@@ -127,7 +189,11 @@ bool preload_peer_kernels() {
   cudaFuncAttributes a;
   return cudaFuncGetAttributes(&a, k_peer_barrier) == cudaSuccess && cudaFuncGetAttributes(&a, k_pack_peer) == cudaSuccess &&
          cudaFuncGetAttributes(&a, k_put_rows<uint4>) == cudaSuccess &&
-         cudaFuncGetAttributes(&a, k_put_rows<uint32_t>) == cudaSuccess;
+         cudaFuncGetAttributes(&a, k_put_rows<uint32_t>) == cudaSuccess &&
+         cudaFuncGetAttributes(&a, k_pack_peer_dev) == cudaSuccess &&
+         cudaFuncGetAttributes(&a, k_put_rows_dev<uint4>) == cudaSuccess &&
+         cudaFuncGetAttributes(&a, k_put_rows_dev<uint32_t>) == cudaSuccess &&
+         cudaFuncGetAttributes(&a, k_zero_tail) == cudaSuccess;
 }
 }  // namespace
 
@@ -234,6 +300,55 @@ sonic_status sonic_ep_pack_peer(const sonic_moe_desc* D, int G, const sonic_ep_p
   const long long rows = D->T * G;
   k_pack_peer<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const __nv_bfloat16*>(src), plan->send_token, plan->send_offsets, G, D->d, P, region_off, R);
+  set_last_launch_count(1);
+  return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
+}
+
+sonic_status sonic_ep_pack_peer_dev(const sonic_moe_desc* D, int G, const sonic_ep_plan* plan, const void* src,
+                                    const sonic_peer* p, size_t region_off, size_t counts_off, int count_cols,
+                                    void* stream) {
+  if (!D || !plan || !src || D->d % 8 != 0 || count_cols < G) return SONIC_ERR_INVALID_ARG;
+  PeerRows R{};
+  PeerPtrs P{};
+  if (!fill_rows(p, G, nullptr, nullptr, nullptr, &R, &P)) return SONIC_ERR_INVALID_ARG;
+  const int* cnt = reinterpret_cast<const int*>(static_cast<const char*>(p->region) + counts_off);
+  const long long rows = D->T * G;
+  k_pack_peer_dev<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(src), plan->send_token, plan->send_offsets, G, D->d, P, region_off, cnt,
+      count_cols, p->rank);
+  set_last_launch_count(1);
+  return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
+}
+
+sonic_status sonic_peer_put_rows_dev(const sonic_peer* p, int G, const void* src, size_t row_bytes, int direction,
+                                     size_t counts_off, int count_cols, size_t region_off, void* stream) {
+  if (!src || row_bytes == 0 || row_bytes % 4 != 0 || region_off % 4 != 0 || count_cols < G ||
+      (direction != 0 && direction != 1))
+    return SONIC_ERR_INVALID_ARG;
+  PeerRows R{};
+  PeerPtrs P{};
+  if (!fill_rows(p, G, nullptr, nullptr, nullptr, &R, &P)) return SONIC_ERR_INVALID_ARG;
+  const int* cnt = reinterpret_cast<const int*>(static_cast<const char*>(p->region) + counts_off);
+  dim3 grid((unsigned)std::max(1, 296 / G), G);
+  const bool v16 = row_bytes % 16 == 0 && region_off % 16 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0;
+  if (v16)
+    k_put_rows_dev<uint4><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const char*>(src), row_bytes, P, region_off, cnt, count_cols, p->rank, G, direction);
+  else
+    k_put_rows_dev<uint32_t><<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const char*>(src), row_bytes, P, region_off, cnt, count_cols, p->rank, G, direction);
+  set_last_launch_count(1);
+  return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
+}
+
+sonic_status sonic_peer_zero_tail(const sonic_peer* p, int G, size_t row_bytes, size_t counts_off, int count_cols,
+                                  size_t region_off, long long cap_rows, void* stream) {
+  if (!p || G != p->world || row_bytes == 0 || row_bytes % 4 != 0 || region_off % 4 != 0 || count_cols < G ||
+      cap_rows < 0 || region_off + (size_t)cap_rows * row_bytes > p->bytes)
+    return SONIC_ERR_INVALID_ARG;
+  const int* cnt = reinterpret_cast<const int*>(static_cast<const char*>(p->region) + counts_off);
+  k_zero_tail<<<296, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<char*>(p->region) + region_off, row_bytes,
+                                                                  cnt, count_cols, p->rank, G, cap_rows);
   set_last_launch_count(1);
   return cudaGetLastError() == cudaSuccess ? SONIC_OK : SONIC_ERR_CUDA;
 }

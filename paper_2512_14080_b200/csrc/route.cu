@@ -733,6 +733,27 @@ __global__ void k_given_bitmap(const float* __restrict__ S, int T, int E, int W,
   for (int e = threadIdx.x; e < E; e += blockDim.x) bm[(size_t)e * W + blockIdx.x] = words[e];
 }
 
+// GIVEN routing with a capacity (the host-sync-free EP receive side, NEXT-2): one block counts the
+// routed pairs in the bitmap; more than `cap` would overflow the rows sized from rows_cap, so the
+// bitmap is cleared (the routing becomes empty: nothing is written out of bounds, every GEMM and
+// aggregation sees zero rows) and *overflow = 1 tells the caller the step is invalid; else 0.
+__global__ void __launch_bounds__(1024) k_given_guard(uint32_t* __restrict__ bm, long long nwords, long long cap,
+                                                      int* __restrict__ overflow) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  __shared__ unsigned long long s_tot;
+  if (threadIdx.x == 0) s_tot = 0ull;
+  __syncthreads();
+  unsigned long long c = 0;
+  for (long long i = threadIdx.x; i < nwords; i += blockDim.x) c += __popc(bm[i]);
+  atomicAdd(&s_tot, c);
+  __syncthreads();
+  const bool over = s_tot > (unsigned long long)cap;
+  if (over)
+    for (long long i = threadIdx.x; i < nwords; i += blockDim.x) bm[i] = 0u;
+  if (threadIdx.x == 0) *overflow = over ? 1 : 0;
+}
+
 // ---------------------------------------------------------------- TC top-K helpers
 // Inverse of ord_f32 (the ordered key of a non-negative-zero float gives the float back).
 __device__ __forceinline__ float unord_f32(uint32_t k) {
@@ -1270,6 +1291,10 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
   const int T = (int)L.T, E = L.E, K = L.K, W = L.W;
   if (L.mode == 2) {  // given routing: bitmap, counts, offsets, rows, CSR with raw gates
     launch_k(k_given_bitmap, W, 256, 0, st, L.S, T, E, W, L.bm_tc, L.ticket); ++nl;
+    if (L.overflow) {
+      launch_k(k_given_guard, 1, 1024, 0, st, L.bm_tc, (long long)E * W, L.cap, L.overflow);
+      ++nl;
+    }
     launch_k(k_popc_offsets, E, 1024, 0, st, L.bm_tc, W, L.wprefix, L.f, L.f_r, L.ticket, L.offsets, L.pad_offsets,
                                        L.tile_expert, L.num_tiles, L.tile_pairs, L.num_pairs); ++nl;
     launch_k(k_build_rows, dim3((W + 255) / 256, E), 256, 0, st, L.bm_tc, L.wprefix, W, L.f_r, L.pad_offsets,

@@ -551,7 +551,7 @@ int sonic_profile_collect(char* names, int name_len, float* ms, int max_records)
 }
 
 static sonic_status route_impl(const sonic_moe_desc* D, const float* S, const float* logits, sonic_routing* rt,
-                               void* ws, size_t ws_bytes, void* stream) {
+                               void* ws, size_t ws_bytes, void* stream, int* overflow = nullptr) {
   g_launches = 0;
   if (!valid_desc(D) || !S || !rt) return SONIC_ERR_INVALID_ARG;
   if (logits && (D->route_mode == SONIC_ROUTE_GIVEN || !aligned16(logits))) return SONIC_ERR_INVALID_ARG;
@@ -584,6 +584,8 @@ static sonic_status route_impl(const sonic_moe_desc* D, const float* S, const fl
   L.gate_raw = (D->flags & SONIC_F_GATE_RAW) ? 1 : 0;
   L.S = S;
   L.logits = logits;
+  L.overflow = overflow;
+  L.cap = (D->rows_cap > 0 && D->rows_cap < D->T * D->K) ? D->rows_cap : D->T * D->K;
   L.topk_ids = rt->topk_ids; L.topk_s = rt->topk_s; L.f = rt->f; L.f_r = rt->f_rounded;
   L.offsets = rt->offsets; L.pad_offsets = rt->pad_offsets; L.row_token = rt->row_token;
   L.row_gate = rt->row_gate; L.token_rowptr = rt->token_rowptr; L.token_rows = rt->token_rows;
@@ -615,6 +617,12 @@ static sonic_status route_impl(const sonic_moe_desc* D, const float* S, const fl
 sonic_status sonic_route(const sonic_moe_desc* D, const float* S, sonic_routing* rt, void* ws, size_t ws_bytes,
                          void* stream) {
   return route_impl(D, S, nullptr, rt, ws, ws_bytes, stream);
+}
+
+sonic_status sonic_route_given_capped(const sonic_moe_desc* D, const float* S, sonic_routing* rt, void* ws,
+                                      size_t ws_bytes, int* overflow, void* stream) {
+  if (!D || D->route_mode != SONIC_ROUTE_GIVEN || !overflow) return SONIC_ERR_INVALID_ARG;
+  return route_impl(D, S, nullptr, rt, ws, ws_bytes, stream, overflow);
 }
 
 sonic_status sonic_route_logits(const sonic_moe_desc* D, const float* logits, float* S_out, sonic_routing* rt,

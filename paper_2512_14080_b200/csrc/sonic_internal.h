@@ -35,6 +35,8 @@ struct RouteLaunch {
   uint32_t seed;  // SR-f draws
   const float* S;        // scores; with `logits` set, the S output buffer the fused softmax writes
   const float* logits;   // sonic_route_logits: router logits [T,E] (softmax fused), else null
+  int* overflow;         // sonic_route_given_capped: device flag (GIVEN routing over capacity), else null
+  long long cap;         //   the routed-pair capacity it guards
   // outputs
   int *topk_ids, *f, *f_r, *offsets, *pad_offsets, *row_token, *token_rowptr, *token_rows, *tile_expert,
       *num_tiles, *tile_pairs, *num_pairs;

@@ -156,8 +156,17 @@ class PeerComm:
 
     NB = 2  # count blocks exchanged per rank: send rows per destination, routed pairs per destination
 
-    def __init__(self, G, T, d, L, local_ranks, group=None, device=None):
+    def __init__(self, G, T, d, L, local_ranks, group=None, device=None, sync_free=False, cap_pairs=None):
+        """sync_free (NEXT-2): no host read of the count matrix.  Every block offset is read on the
+        device from the own count matrix (sonic_*_dev calls), the receive side works on the
+        capacity NS = T*G rows (rows past this step's received ones are zeroed, so they route
+        nowhere) and its routed pairs are sized by `cap_pairs` (default 2*T*K of the layer: twice the
+        average load) with the capacity guard of sonic_route_given_capped -- a step whose received
+        pairs exceed it is flagged (EPRank.overflowed()) and computes nothing on that rank.  The
+        whole layer step is then free of host synchronisation (and graph-capturable)."""
         self.G, self.T, self.d, self.L = G, T, d, L
+        self.sync_free = bool(sync_free)
+        self.cap_pairs = cap_pairs
         self.local = list(local_ranks)
         ns = T * G
         off, lay = 0, {}
@@ -206,7 +215,7 @@ class PeerComm:
     # ---------------------------------------------------------------- counts
     def exchange_counts_dev(self, send_dev):
         """Every rank stores its G send counts into row `rank` of every rank's count matrix; one host
-        read of the own matrix gives M[s][g] = rows s sends to g."""
+        read of the own matrix gives M[s][g] = rows s sends to g (none in sync_free mode)."""
         G, nb = self.G, self.NB
         for i, (rg, c) in enumerate(zip(self.regions, send_dev)):
             assert c.numel() == nb * G
@@ -215,6 +224,9 @@ class PeerComm:
                 rg.put_rows(c.to(torch.int32).contiguous(), nb * G * 4, [0] * G, [1] * G, [rg.rank] * G,
                             self.lay["counts"])
                 rg.barrier()
+        if self.sync_free:
+            self.M = None
+            return None, None
         Ms = []
         for i, rg in enumerate(self.regions):
             with self.rank_stream(i):
@@ -246,6 +258,15 @@ class PeerComm:
         """Fused pack + dispatch: each rank's kernel gathers src[send_token] straight into the
         destination ranks' `tag` area.  Returns the received rows of each local rank."""
         outs = []
+        if self.sync_free:  # destination rows from the count matrix on the device; capacity views
+            ns = self.T * self.G
+            for i, (rk, rg, src) in enumerate(zip(ranks, self.regions, srcs)):
+                with self.rank_stream(i):
+                    rg.barrier()
+                    rg.pack_dev(rk.desc(), self.G, rk.ctx["plan"], src, self.lay[tag], self.lay["counts"],
+                                self.NB * self.G)
+                    rg.barrier()
+            return [rg.view(self.lay[tag], (ns, self.d), torch.bfloat16) for rg in self.regions]
         for i, (rk, rg, src) in enumerate(zip(ranks, self.regions, srcs)):
             with self.rank_stream(i):
                 rg.barrier()
@@ -264,6 +285,19 @@ class PeerComm:
         outs = []
         ret = tag in self._RETURN
         area = self._RETURN.get(tag, tag)
+        if self.sync_free:
+            ns = self.T * self.G
+            for i, (rg, snd) in enumerate(zip(self.regions, sends)):
+                with self.rank_stream(i):
+                    row_bytes = snd[0].numel() * snd.element_size() if snd.dim() > 1 else snd.element_size()
+                    rg.barrier()
+                    rg.put_rows_dev(snd.contiguous(), row_bytes, 1 if ret else 0, self.lay["counts"],
+                                    self.NB * self.G, self.lay[area])
+                    rg.barrier()
+                    if not ret:  # received gate rows past this step's: zero, so they route nowhere
+                        rg.zero_tail(row_bytes, self.lay["counts"], self.NB * self.G, self.lay[area], ns)
+            return [rg.view(self.lay[area], (ns,) + tuple(snd.shape[1:]), snd.dtype)
+                    for rg, snd in zip(self.regions, sends)]
         for i, (rg, snd) in enumerate(zip(self.regions, sends)):
             with self.rank_stream(i):
                 row_bytes = snd[0].numel() * snd.element_size() if snd.dim() > 1 else snd.element_size()
@@ -335,19 +369,38 @@ class EPRank:
         sonic.sonic_ep_pack(self.desc(), self.G, self.ctx["plan"], src, send)
         return send
 
-    def compute_fwd(self, recv_x, recv_gate, pairs_in=0):
+    def compute_fwd(self, recv_x, recv_gate, pairs_in=0, cap_pairs=None):
         """pairs_in: routed (token, local expert) pairs in the received rows (0 = unknown: bound by
-        R_in * L) -- sizes H and the workspaces instead of R_in * L rows."""
+        R_in * L) -- sizes H and the workspaces instead of R_in * L rows.  cap_pairs (host-sync-free
+        mode): recv_x / recv_gate are the capacity views and the routed pairs are bounded by
+        cap_pairs with the overflow guard (overflowed())."""
         R_in = recv_x.shape[0]
         self.ctx.update(R_in=R_in, recv_x=recv_x)
         if R_in == 0:
             return recv_x.new_zeros(0, self.d)
+        if cap_pairs is not None:
+            ld = sonic.make_desc(R_in, self.d, self.n, self.L, self.L, mode=sonic.SONIC_ROUTE_GIVEN,
+                                 rows_cap=int(cap_pairs))
+            flag = self.ctx.get("overflow")
+            if flag is None:
+                flag = self.ctx["overflow"] = torch.zeros(1, dtype=torch.int32, device=recv_x.device)
+            lrt = sonic.sonic_route_given_capped(ld, recv_gate, flag)
+            O_part, H, _ = sonic.sonic_moe_fwd(ld, recv_x, self.W1, self.W2, lrt)
+            self.ctx.update(ldesc=ld, lrt=lrt, H=H)
+            return O_part
         ld = sonic.make_desc(R_in, self.d, self.n, self.L, self.L, mode=sonic.SONIC_ROUTE_GIVEN,
                              rows_cap=max(0, int(pairs_in)))
         lrt = sonic.sonic_route(ld, recv_gate.contiguous())
         O_part, H, _ = sonic.sonic_moe_fwd(ld, recv_x, self.W1, self.W2, lrt)
         self.ctx.update(ldesc=ld, lrt=lrt, H=H)
         return O_part
+
+    def overflowed(self):
+        """Host-sync-free mode: True when this rank's last step received more routed pairs than its
+        capacity (that step computed nothing here and must be re-run with exact sizing).  Reads the
+        device flag: call it after the step, not inside it."""
+        flag = self.ctx.get("overflow")
+        return bool(flag is not None and int(flag.item()) != 0)
 
     def combine_fwd(self, back):
         out = torch.empty(self.T, self.d, dtype=torch.bfloat16, device=back.device)
@@ -427,11 +480,18 @@ def ep_forward(ranks, comm, Xs, Ss):
         with comm.rank_stream(i):
             disp.append(r.plan_fwd(S))
     # the send counts are host arguments of the exchange: the only host synchronisation of the step
+    # (none with PeerComm(sync_free=True): the offsets are read on the device)
     send_both, recv_both = comm.exchange_counts_dev([c for _, c in disp])
     G = ranks[0].G
-    send_counts = [sb[:G] for sb in send_both]
-    recv_counts = [rb[:G] for rb in recv_both]
-    pairs_in = [sum(rb[G:2 * G]) for rb in recv_both]
+    sync_free = getattr(comm, "sync_free", False)
+    if sync_free:
+        send_counts = recv_counts = [None] * len(ranks)
+        cap = comm.cap_pairs if comm.cap_pairs is not None else 2 * ranks[0].T * ranks[0].K
+        pairs_in = [None] * len(ranks)
+    else:
+        send_counts = [sb[:G] for sb in send_both]
+        recv_counts = [rb[:G] for rb in recv_both]
+        pairs_in = [sum(rb[G:2 * G]) for rb in recv_both]
     for r, sc in zip(ranks, send_counts):
         r.ctx["counts"] = sc
     recv_x = _dispatch(ranks, comm, Xs, send_counts, recv_counts, "x")
@@ -439,7 +499,7 @@ def ep_forward(ranks, comm, Xs, Ss):
     parts = []
     for i, (r, x, g, pin) in enumerate(zip(ranks, recv_x, recv_g, pairs_in)):
         with comm.rank_stream(i):
-            parts.append(r.compute_fwd(x, g, pin))
+            parts.append(r.compute_fwd(x, g, cap_pairs=cap) if sync_free else r.compute_fwd(x, g, pin))
     back = comm.alltoallv(parts, recv_counts, send_counts, tag="y")
     outs = []
     for i, (r, rc, b) in enumerate(zip(ranks, recv_counts, back)):

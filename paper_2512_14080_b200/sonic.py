@@ -137,6 +137,15 @@ def lib():
         L.sonic_ep_pack_peer.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sonic_ep_plan), vp, vp, sz,
                                          P(ctypes.c_int32), vp]
         L.sonic_ep_pack_peer.restype = ctypes.c_int
+        L.sonic_ep_pack_peer_dev.argtypes = [P(sonic_moe_desc), ctypes.c_int, P(sonic_ep_plan), vp, vp, sz, sz,
+                                             ctypes.c_int, vp]
+        L.sonic_ep_pack_peer_dev.restype = ctypes.c_int
+        L.sonic_peer_put_rows_dev.argtypes = [vp, ctypes.c_int, vp, sz, ctypes.c_int, sz, ctypes.c_int, sz, vp]
+        L.sonic_peer_put_rows_dev.restype = ctypes.c_int
+        L.sonic_peer_zero_tail.argtypes = [vp, ctypes.c_int, sz, sz, ctypes.c_int, sz, ctypes.c_longlong, vp]
+        L.sonic_peer_zero_tail.restype = ctypes.c_int
+        L.sonic_route_given_capped.argtypes = [P(sonic_moe_desc), vp, P(sonic_routing), vp, sz, vp, vp]
+        L.sonic_route_given_capped.restype = ctypes.c_int
         L.sonic_peer_put_rows.argtypes = [vp, ctypes.c_int, vp, sz, P(ctypes.c_int32), P(ctypes.c_int32),
                                           P(ctypes.c_int32), sz, vp]
         L.sonic_peer_put_rows.restype = ctypes.c_int
@@ -256,6 +265,18 @@ def sonic_route(desc, S, rt=None, ws=None):
         ws = _ws(sonic_route_workspace_size(desc), S.device)
     _done(lib().sonic_route(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(ws), ws.numel(), _stream()),
            "sonic_route")
+    return rt
+
+
+def sonic_route_given_capped(desc, S, overflow, rt=None, ws=None):
+    """SONIC_ROUTE_GIVEN with the capacity guard: overflow (device int32 [1]) = 1 and an empty routing
+    when the routed pairs exceed desc.rows_cap."""
+    if rt is None:
+        rt = alloc_routing(desc, S.device)
+    if ws is None:
+        ws = _ws(sonic_route_workspace_size(desc), S.device)
+    _done(lib().sonic_route_given_capped(ctypes.byref(desc), _ptr(S), ctypes.byref(rt.c), _ptr(ws), ws.numel(),
+                                         _ptr(overflow), _stream()), "sonic_route_given_capped")
     return rt
 
 
@@ -472,6 +493,22 @@ class PeerRegion:
     def pack(self, desc, G, plan, src, region_off, dst_row0):
         _done(lib().sonic_ep_pack_peer(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(src), self.h,
                                        int(region_off), _i32(dst_row0), _stream()), "sonic_ep_pack_peer")
+
+    def pack_dev(self, desc, G, plan, src, region_off, counts_off, count_cols):
+        """Dispatch with the destination rows read on the device from the own count matrix."""
+        _done(lib().sonic_ep_pack_peer_dev(ctypes.byref(desc), G, ctypes.byref(plan.c), _ptr(src), self.h,
+                                           int(region_off), int(counts_off), int(count_cols), _stream()),
+              "sonic_ep_pack_peer_dev")
+
+    def put_rows_dev(self, src, row_bytes, direction, counts_off, count_cols, region_off):
+        """Block put with the blocks read on the device from the own count matrix (0 dispatch, 1 return)."""
+        _done(lib().sonic_peer_put_rows_dev(self.h, self.world, _ptr(src), int(row_bytes), int(direction),
+                                            int(counts_off), int(count_cols), int(region_off), _stream()),
+              "sonic_peer_put_rows_dev")
+
+    def zero_tail(self, row_bytes, counts_off, count_cols, region_off, cap_rows):
+        _done(lib().sonic_peer_zero_tail(self.h, self.world, int(row_bytes), int(counts_off), int(count_cols),
+                                         int(region_off), int(cap_rows), _stream()), "sonic_peer_zero_tail")
 
     def put_rows(self, src, row_bytes, src_row0, cnt, dst_row0, region_off):
         _done(lib().sonic_peer_put_rows(self.h, self.world, _ptr(src), int(row_bytes), _i32(src_row0), _i32(cnt),

@@ -16,7 +16,7 @@ from tests.parity import assert_close, f64
 pytestmark = pytest.mark.gpu
 
 
-def _run_ep(G, mode, E, comm_kind, T=768, d=128, n=64, K=4):
+def _run_ep(G, mode, E, comm_kind, T=768, d=128, n=64, K=4, steps=1, cap_pairs=None):
     m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
     base = make_inputs(T, d, n, E, K, seed=40, device="cuda")
     W1, W2 = base.W1, base.W2
@@ -24,14 +24,18 @@ def _run_ep(G, mode, E, comm_kind, T=768, d=128, n=64, K=4):
     ins = [make_inputs(T, d, n, E, K, seed=41 + r, device="cuda") for r in range(G)]
     ranks = [ep.EPRank(T, d, n, E, K, G, r, W1[r * L:(r + 1) * L].contiguous(), W2[r * L:(r + 1) * L].contiguous(),
                        mode=m) for r in range(G)]
-    comm = ep.SimComm(G) if comm_kind == "sim" else ep.PeerComm(G, T, d, L, range(G))
-    Os = ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins])
-    outs = ep.ep_backward(ranks, comm, [i.dO for i in ins])
+    comm = (ep.SimComm(G) if comm_kind == "sim" else
+            ep.PeerComm(G, T, d, L, range(G), sync_free=comm_kind == "peer_sf", cap_pairs=cap_pairs))
+    for _ in range(steps):  # later steps reuse the regions (stale rows of the earlier step)
+        Os = ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins])
+        outs = ep.ep_backward(ranks, comm, [i.dO for i in ins])
     torch.cuda.synchronize()
     res = [(Os[r].clone(), outs[r][0].clone(), outs[r][1].clone(), ranks[r].dW1.clone(), ranks[r].dW2.clone())
            for r in range(G)]
-    if comm_kind == "peer":
+    if comm_kind.startswith("peer"):
         comm.close()
+    if comm_kind == "peer_sf":
+        res.append([rk.overflowed() for rk in ranks])
     return res
 
 
@@ -148,3 +152,23 @@ def test_ep_zero_gate_pairs_keep_their_rows(comm_kind):
         assert_close(f"dS[{r}]", f64(outs[r][1])[rows], dSref)
     if comm_kind == "peer":
         comm.close()
+
+
+@pytest.mark.parametrize("G,mode,E", [(2, "tc", 16), (4, "tr", 16), (2, "tc", 64)])
+def test_ep_sync_free_equals_sim(G, mode, E):
+    """NEXT-2: the host-sync-free peer exchange (offsets read on the device, capacity-sized receive
+    side with the routed-pair guard) gives every rank bit-identical outputs to the staged exchange,
+    also on a second step over regions holding the first step's rows; no rank overflows."""
+    a = _run_ep(G, mode, E, "sim")
+    b = _run_ep(G, mode, E, "peer_sf", steps=2)
+    assert not any(b[G]), "unexpected capacity overflow"
+    for r in range(G):
+        for name, x, y in zip(("O", "dX", "dS", "dW1", "dW2"), a[r], b[r]):
+            assert torch.equal(x, y), f"rank {r} {name} differs between SimComm and the sync-free PeerComm"
+
+
+def test_ep_sync_free_overflow_is_flagged():
+    """A capacity below the received routed pairs: the guarded GIVEN routing empties the rank's
+    routing (nothing written out of bounds, its expert outputs are zero) and overflowed() says so."""
+    res = _run_ep(2, "tc", 16, "peer_sf", cap_pairs=64)
+    assert all(res[2])
