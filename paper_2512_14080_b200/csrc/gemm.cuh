@@ -311,6 +311,9 @@ __device__ __forceinline__ void tload3(void* dst, const CUtensorMap* m, uint64_t
 // pair).  Each pair TMA-loads half of the shared tile and multicasts it into both pairs' stage, so
 // the L2 -> SM operand traffic per MMA drops by a quarter; a stage is refilled once BOTH pairs' MMAs
 // have released it (empty barriers count the two pair leaders' commits).
+#ifndef SONIC_EXP_NOFENCE
+#define SONIC_EXP_NOFENCE 0  // timing ablation only (results may be wrong): no consumer-side proxy fence
+#endif
 #ifndef SONIC_STREAM_EF
 #define SONIC_STREAM_EF 2  // evict-first hint on the streamed TMA operand of dW1 (1) / dW2 (2): dW2 213 -> 209 us, dW1 unchanged (7B, 3 reps)
 #endif
@@ -623,7 +626,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           c_full += clock64() - cb;
 #endif
           // cp.async (generic proxy) data consumed by tcgen05.mma (async proxy)
-          if constexpr (GATHER) ptx::fence_proxy_async_smem();
+          if constexpr (GATHER && !SONIC_EXP_NOFENCE) ptx::fence_proxy_async_smem();  // (ablation: SONIC_EXP_NOFENCE, unsafe)
           ptx::tc_fence_after();
           const uint32_t a_base = ptx::smem_u32(smem + stage * STAGE_BYTES);
           const uint32_t b_base = a_base + A_BYTES;

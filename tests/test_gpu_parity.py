@@ -287,6 +287,9 @@ LOGIT_CASES = [
     ("tc_e384", 2048, 384, 8, sonic.SONIC_ROUTE_TC),
     ("tc_e40", 999, 40, 3, sonic.SONIC_ROUTE_TC),
     ("tc_e1000", 300, 1000, 16, sonic.SONIC_ROUTE_TC),
+    ("tc_T1_K1", 1, 64, 1, sonic.SONIC_ROUTE_TC),
+    ("tc_K_eq_E", 100, 32, 32, sonic.SONIC_ROUTE_TC),
+    ("tr_nrs", 1024, 64, 4, sonic.SONIC_ROUTE_TR_NRS),
 ]
 
 
@@ -401,6 +404,7 @@ def test_quantize_e4m3_bit_exact():
 
 
 FP8_CASES = [
+    ("fp8_tiny_T1", 1, 128, 128, 4, 2, "tc"),
     ("fp8_tc", 2048, 256, 128, 16, 4, "tc"),
     ("fp8_tr", 2048, 256, 128, 16, 4, "tr"),
     ("fp8_n256_ragged", 1000, 384, 256, 8, 2, "tc"),

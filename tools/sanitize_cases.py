@@ -37,7 +37,32 @@ CASES = [
     ("TR SR", 1000, 128, 64, 16, 4, R.SONIC_ROUTE_TR_SR, 0),
     ("TR NR-s", 1000, 128, 64, 16, 4, R.SONIC_ROUTE_TR_NRS, 0),
     ("many experts E=260 K=8", 1500, 64, 64, 260, 8, R.SONIC_ROUTE_TC, 0),
+    ("fp8 up-projection", 1000, 256, 128, 16, 4, R.SONIC_ROUTE_TC, R.SONIC_F_FP8_UP),
+    ("fp8 up-projection TR, n256", 777, 384, 256, 8, 2, R.SONIC_ROUTE_TR_NRF, R.SONIC_F_FP8_UP),
 ]
+
+
+def run_router_cases():
+    """NEXT-4 router: fused softmax routing (warp top-K path and row-softmax path), router GEMMs
+    and the whole router chain."""
+    for (T, d, E, K, m) in ((1000, 128, 64, 4, R.SONIC_ROUTE_TC), (999, 128, 40, 3, R.SONIC_ROUTE_TC),
+                            (1024, 128, 32, 2, R.SONIC_ROUTE_TR_NRF)):
+        g = torch.Generator(device="cuda").manual_seed(3)
+        X = torch.randn(T, d, device="cuda", generator=g).bfloat16()
+        Wr = (torch.randn(d, E, device="cuda", generator=g) / d ** 0.5).bfloat16()
+        desc = sonic.make_desc(T, d, 64, E, K, mode=m)
+        logits = sonic.sonic_router_fwd(desc, X, Wr)
+        S, rt = sonic.sonic_route_logits(desc, logits)
+        dS = torch.randn(sonic.sonic_rows_max(desc), device="cuda", generator=g)
+        dlog = sonic.sonic_router_bwd(desc, S, rt, dS)
+        dX = torch.zeros(T, d, dtype=torch.bfloat16, device="cuda")
+        sonic.sonic_router_grad(desc, X, Wr, dlog, dX=dX)
+        torch.cuda.synchronize()
+        print(f"case router T={T} E={E}: ok={bool(torch.isfinite(dX.float()).all())}", flush=True)
+    xq, sx = sonic.sonic_quantize_e4m3_rows(torch.randn(333, 136, device="cuda").bfloat16())
+    wq, sw = sonic.sonic_quantize_e4m3_cols(torch.randn(3, 100, 264, device="cuda").bfloat16())
+    torch.cuda.synchronize()
+    print("case e4m3 quantisers: ok", flush=True)
 
 
 def run_case(label, T, d, n, E, K, mode, flags):
@@ -87,5 +112,7 @@ if __name__ == "__main__":
         if a.only and not any(o in c[0] for o in a.only.split(",")):
             continue
         run_case(*c)
+    if not a.only or "router" in a.only:
+        run_router_cases()
     if a.ep or a.ep_peer:
         run_ep(peer=a.ep_peer)
