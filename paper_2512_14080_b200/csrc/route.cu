@@ -1011,8 +1011,11 @@ __global__ void __launch_bounds__(256) k_softmax_rows(const float* __restrict__ 
 // of Q9), then KT rounds of a two-step warp max (redux.sync on the score half, then on the expert
 // half among the lanes holding that score) pop the winners in order.  A block of 8 warps routes 32
 // consecutive tokens, i.e. one word of the per-expert bitmaps.
+#ifndef SONIC_TOPK_MINB
+#define SONIC_TOPK_MINB 1  // min blocks per SM for k_topk_warp's register budget (1 = no constraint)
+#endif
 template <int KT, int EPLMAX>
-__global__ void __launch_bounds__(256) k_topk_warp(const float* __restrict__ S, int T, int E, int W,
+__global__ void __launch_bounds__(256, SONIC_TOPK_MINB) k_topk_warp(const float* __restrict__ S, int T, int E, int W,
                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
                                                    uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket,
                                                    float* __restrict__ S_out, int* __restrict__ cnt_acc) {
