@@ -103,6 +103,42 @@ def test_invalid_arguments_are_rejected_before_any_launch(lib):
         assert lib.sonic_status_string(s)
 
 
+def test_round2_calls_validate_on_the_host(lib):
+    """The round-2 entry points reject bad arguments before any CUDA call (so on a CPU host too)."""
+    from paper_2512_14080_b200 import sonic
+    P = ctypes.c_void_p(1 << 20)
+    rt = sonic.sonic_routing(*([1 << 20] * len(sonic.ROUTING_FIELDS)))
+    d = sonic.make_desc(256, 64, 32, 8, 2)
+    dg = sonic.make_desc(256, 64, 32, 8, 8, mode=sonic.SONIC_ROUTE_GIVEN)
+    # fused softmax: null logits, GIVEN routing, misaligned logits
+    assert lib.sonic_route_logits(ctypes.byref(d), None, P, ctypes.byref(rt), P, 1 << 30, None) == -1
+    assert lib.sonic_route_logits(ctypes.byref(dg), P, P, ctypes.byref(rt), P, 1 << 30, None) == -1
+    assert lib.sonic_route_logits(ctypes.byref(d), ctypes.c_void_p((1 << 20) + 4), P, ctypes.byref(rt), P,
+                                  1 << 30, None) == -1
+    # capped GIVEN routing: not GIVEN, or no flag
+    flag = ctypes.c_void_p(1 << 21)
+    assert lib.sonic_route_given_capped(ctypes.byref(d), P, ctypes.byref(rt), P, 1 << 30, flag, None) == -1
+    assert lib.sonic_route_given_capped(ctypes.byref(dg), P, ctypes.byref(rt), P, 1 << 30, None, None) == -1
+    # router GEMMs: null operands; both outputs null; short workspace
+    assert lib.sonic_router_fwd(ctypes.byref(d), None, P, P, None) == -1
+    assert lib.sonic_router_grad(ctypes.byref(d), P, P, P, None, None, P, 1 << 30, None) == -1
+    assert lib.sonic_router_grad(ctypes.byref(d), P, P, P, P, P, P, 1, None) == -3
+    assert lib.sonic_router_grad_workspace_size(ctypes.byref(d)) == 256 * 8 * 2
+    # e4m3 quantisers: cols not a multiple of 8, misaligned, null
+    assert lib.sonic_quantize_e4m3_rows(P, 10, 12, P, P, None) == -1
+    assert lib.sonic_quantize_e4m3_rows(ctypes.c_void_p((1 << 20) + 2), 10, 16, P, P, None) == -1
+    assert lib.sonic_quantize_e4m3_cols(None, 1, 16, 16, P, P, None) == -1
+    assert lib.sonic_quantize_e4m3_cols(P, 1, 16, 12, P, P, None) == -1
+    # FP8 up-projection: n % 128 != 0 -> UNSUPPORTED (checked before the workspace)
+    d8 = sonic.make_desc(256, 128, 64, 8, 2, flags=sonic.SONIC_F_FP8_UP)
+    assert lib.sonic_moe_fwd(ctypes.byref(d8), P, P, P, ctypes.byref(rt), P, P, P, 1 << 40, None) == -2
+    # the fp8 workspace holds the e4m3 copies: bigger than the bf16 one
+    d8ok = sonic.make_desc(256, 128, 128, 8, 2, flags=sonic.SONIC_F_FP8_UP)
+    d16 = sonic.make_desc(256, 128, 128, 8, 2)
+    assert lib.sonic_fwd_workspace_size(ctypes.byref(d8ok)) >= (lib.sonic_fwd_workspace_size(ctypes.byref(d16)) +
+                                                                256 * 128 + 8 * 128 * 256)
+
+
 def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     from paper_2512_14080_b200 import sonic
     monkeypatch.setattr(sonic, "LIB_PATH", str(tmp_path / "missing.so"))
