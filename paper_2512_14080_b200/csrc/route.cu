@@ -1014,16 +1014,19 @@ __global__ void __launch_bounds__(256) k_softmax_rows(const float* __restrict__ 
 #ifndef SONIC_TOPK_MINB
 #define SONIC_TOPK_MINB 1  // min blocks per SM for k_topk_warp's register budget (1 = no constraint)
 #endif
-template <int KT, int EPLMAX>
+template <int KT, int EPLMAX, bool ST_SLAB = false>
 __global__ void __launch_bounds__(256, SONIC_TOPK_MINB) k_topk_warp(const float* __restrict__ S, int T, int E, int W,
                                                    int* __restrict__ topk_ids, float* __restrict__ topk_s,
                                                    uint32_t* __restrict__ bm_tc, unsigned* __restrict__ ticket,
-                                                   float* __restrict__ S_out, int* __restrict__ cnt_acc) {
+                                                   float* __restrict__ S_out, int* __restrict__ cnt_acc,
+                                                   float* __restrict__ ST) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
   constexpr int KP = KT <= 1 ? 1 : KT <= 2 ? 2 : KT <= 4 ? 4 : KT <= 8 ? 8 : 16;
   constexpr int LL = EPLMAX < KP ? EPLMAX : KP;  // lane list length
   __shared__ uint32_t words[32 * EPLMAX];
+  // token rounding / expert choice: S^T [E, T] (expert columns contiguous) through a transposing slab
+  __shared__ float slab[ST_SLAB ? 32 : 1][ST_SLAB ? 32 * EPLMAX + 1 : 1];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const int tok0 = blockIdx.x * 32;
   const int epl = E >> 5;
@@ -1051,6 +1054,13 @@ __global__ void __launch_bounds__(256, SONIC_TOPK_MINB) k_topk_warp(const float*
 #pragma unroll
       for (int j = 0; j < EPLMAX; ++j)
         if (j < epl) S_out[(size_t)t * E + 32 * j + lane] = v[u][j];
+    }
+    if constexpr (ST_SLAB) {
+      if (ST) {
+#pragma unroll
+        for (int j = 0; j < EPLMAX; ++j)
+          if (j < epl) slab[t - tok0][32 * j + lane] = v[u][j];
+      }
     }
     unsigned long long lst[LL];
 #pragma unroll
@@ -1094,6 +1104,13 @@ __global__ void __launch_bounds__(256, SONIC_TOPK_MINB) k_topk_warp(const float*
     }
   }
   __syncthreads();
+  if constexpr (ST_SLAB) {
+    if (ST) {  // warp w writes experts w, w + 8, ...: one 128-byte row of 32 tokens each
+      const int ntok = min(32, T - tok0);
+      if (lane < ntok)
+        for (int e = wp; e < E; e += 8) ST[(size_t)e * T + tok0 + lane] = slab[lane][e];
+    }
+  }
   for (int e = threadIdx.x; e < E; e += 256) {
     const uint32_t wd = words[e];
     bm_tc[(size_t)e * W + blockIdx.x] = wd;
@@ -1227,6 +1244,9 @@ __global__ void __launch_bounds__(TCB_THREADS) k_tc_build(const uint32_t* __rest
 #ifndef SONIC_TOPK_WARP_EMAX
 #define SONIC_TOPK_WARP_EMAX 128
 #endif
+#ifndef SONIC_TOPK_WARP_ST
+#define SONIC_TOPK_WARP_ST 1  // token rounding / expert choice also on the warp top-K (S^T through a smem slab)
+#endif
 
 template <int KT>
 int launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
@@ -1243,15 +1263,27 @@ int launch_topk_g4(const RouteLaunch& L, cudaStream_t st) {
   float* st_out = (L.mode == 1 || L.mode == 3) ? L.ST : nullptr;
   // warp per token: 7B / Qwen3 (E = 128) route 32.7 -> 27.3 us; at E = 384 (Kimi) slower than the
   // four-threads-per-token kernel (92.7 -> 106.3 us), so only for E <= SONIC_TOPK_WARP_EMAX
-  if (SONIC_TOPK_WARP && !st_out && E % 32 == 0 && E <= SONIC_TOPK_WARP_EMAX) {
+  if (SONIC_TOPK_WARP && (!st_out || SONIC_TOPK_WARP_ST) && E % 32 == 0 && E <= SONIC_TOPK_WARP_EMAX) {
     // with logits (sonic_route_logits) the softmax is fused here: reads logits, writes S, routes on S
     const float* in = L.logits ? L.logits : L.S;
     float* s_out = L.logits ? const_cast<float*>(L.S) : nullptr;
     // TC: the per-expert counts accumulate here (zeroed first) for the one-launch build, k_tc_build
     int* acc = (SONIC_TC_BUILD1 && L.mode == 0 && E <= TCB_THREADS) ? L.tokcnt : nullptr;
     if (acc) cudaMemsetAsync(acc, 0, (size_t)E * 4, st);
-    if (E <= 128) launch_k(k_topk_warp<KT, 4>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out, acc);
-    else launch_k(k_topk_warp<KT, 8>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out, acc);
+    if (st_out) {  // token rounding / expert choice: S^T written through the slab
+      if (E <= 128)
+        launch_k(k_topk_warp<KT, 4, true>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out,
+                 acc, st_out);
+      else
+        launch_k(k_topk_warp<KT, 8, true>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out,
+                 acc, st_out);
+    } else if (E <= 128) {
+      launch_k(k_topk_warp<KT, 4>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out, acc,
+               (float*)nullptr);
+    } else {
+      launch_k(k_topk_warp<KT, 8>, W, 256, 0, st, in, T, E, W, L.topk_ids, L.topk_s, L.bm_tc, L.ticket, s_out, acc,
+               (float*)nullptr);
+    }
     return 1;
   }
   int nl = 1;

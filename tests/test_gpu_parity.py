@@ -288,7 +288,7 @@ LOGIT_CASES = [
     ("tc_e40", 999, 40, 3, sonic.SONIC_ROUTE_TC),
     ("tc_e1000", 300, 1000, 16, sonic.SONIC_ROUTE_TC),
     ("tc_T1_K1", 1, 64, 1, sonic.SONIC_ROUTE_TC),
-    ("tc_K_eq_E", 100, 32, 32, sonic.SONIC_ROUTE_TC),
+    ("tc_K_eq_E", 100, 16, 16, sonic.SONIC_ROUTE_TC),  # K <= 16 (TC)
     ("tr_nrs", 1024, 64, 4, sonic.SONIC_ROUTE_TR_NRS),
 ]
 
