@@ -99,6 +99,38 @@ __device__ __forceinline__ uint32_t sr_draw24(uint32_t seed, uint32_t e) {
 // Rounding decision per expert.  rounding: 0 NR-f (strict '<': an exact M/2 tie
 // rounds down, Q11), 1 up, 2 down, 3 Balance-f (Alg. 6: sequential, one thread), 4 SR-f.
 // ec_cap >= 0: expert choice, every expert takes ec_cap tokens.
+// The per-expert rounding decisions (every subroutine but Balance-f, which is sequential over experts).
+__device__ __forceinline__ int tr_decide_one(int fe, int e, int T, int M, int rounding, uint32_t seed, int ec_cap) {
+  if (ec_cap >= 0) return ec_cap;
+  const int up_m = (fe + M - 1) / M * M;  // the M-multiple above f (uncapped: the NR-f comparison)
+  const int up = min(up_m, T);            // Q15: a chosen "up" is capped at T
+  const int dn = fe / M * M;
+  switch (rounding) {
+    case 1: return up;
+    case 2: return dn;
+    case 4: return (unsigned long long)sr_draw24(seed, (uint32_t)e) * (unsigned)M < ((unsigned long long)(fe - dn) << 24)
+                       ? up : dn;
+    default: return (up_m - fe) < (fe - dn) ? up : dn;  // strict '<': M/2 ties round down (Q11)
+  }
+}
+
+// k_expert_popc + the decision in one launch (the per-expert subroutines: the count of expert e is
+// all its decision needs): block e counts its bitmap row, then writes f[e] and f_r[e].
+__global__ void k_expert_popc_decide(const uint32_t* __restrict__ bm, int W, int* __restrict__ cnt,
+                                     int* __restrict__ f_r, int T, int M, int rounding, uint32_t seed, int ec_cap) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int e = blockIdx.x;
+  int c = 0;
+  for (int w = threadIdx.x; w < W; w += blockDim.x) c += __popc(bm[(size_t)e * W + w]);
+  int tot;
+  block_excl_scan(c, &tot);
+  if (threadIdx.x == 0) {
+    cnt[e] = tot;
+    f_r[e] = tr_decide_one(tot, e, T, M, rounding, seed, ec_cap);
+  }
+}
+
 __global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, int E, int T, int M, int rounding,
                             uint32_t seed, int ec_cap) {
   ptx::pdl_trigger();
@@ -118,25 +150,8 @@ __global__ void k_tr_decide(const int* __restrict__ f, int* __restrict__ f_r, in
     }
     return;
   }
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) {
-    if (ec_cap >= 0) {
-      f_r[e] = ec_cap;
-      continue;
-    }
-    const int fe = f[e];
-    const int up_m = (fe + M - 1) / M * M;  // the M-multiple above f (uncapped: the NR-f comparison)
-    const int up = min(up_m, T);            // Q15: a chosen "up" is capped at T
-    const int dn = fe / M * M;
-    int r;
-    switch (rounding) {
-      case 1: r = up; break;
-      case 2: r = dn; break;
-      case 4: r = (unsigned long long)sr_draw24(seed, (uint32_t)e) * (unsigned)M <
-                          ((unsigned long long)(fe - dn) << 24) ? up : dn; break;
-      default: r = (up_m - fe) < (fe - dn) ? up : dn; break;  // strict '<': M/2 ties round down (Q11)
-    }
-    f_r[e] = r;
-  }
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x)
+    f_r[e] = tr_decide_one(f[e], e, T, M, rounding, seed, ec_cap);
 }
 
 // ---------------------------------------------------------------- TR selection
@@ -1357,10 +1372,15 @@ int launch_route(const RouteLaunch& L, cudaStream_t st) {
       ec_cap = (int)std::min<long long>((avg + L.m_tile - 1) / L.m_tile * L.m_tile, T);
     }
     const bool nrs = !ec && L.rounding == 5;
-    launch_k(k_expert_popc, E, 1024, 0, st, L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
-    if (!nrs) {
-      launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile, L.rounding, L.seed, ec_cap);
+    if (!nrs && (ec || L.rounding != 3)) {  // per-expert decision: fused with the count
+      launch_k(k_expert_popc_decide, E, 1024, 0, st, L.bm_tc, W, L.f, L.f_r, T, L.m_tile, L.rounding, L.seed, ec_cap);
       ++nl;
+    } else {
+      launch_k(k_expert_popc, E, 1024, 0, st, L.bm_tc, W, nullptr, L.f, nullptr); ++nl;
+      if (!nrs) {  // Balance-f: one sequential pass over the experts
+        launch_k(k_tr_decide, (E + 255) / 256, 256, 0, st, L.f, L.f_r, E, T, L.m_tile, L.rounding, L.seed, ec_cap);
+        ++nl;
+      }
     }
     auto select_into = [&](int rescue, uint32_t* out, const int* fr_src) {
       if (W <= 1024)
