@@ -54,7 +54,7 @@ def test_default_arm_line_tiny():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("comm", ["nccl", "peer"])
+@pytest.mark.parametrize("comm", ["nccl", "peer", "peer_sf"])
 def test_two_rank_bench_line(comm):
     """The N > 1 path of bench.py (expert parallel, barriers, max-over-ranks timing, rank-0 line) with
     two ranks sharing the one GPU over gloo (SONIC_BENCH_SHARE_GPU; "nccl" then means the
@@ -68,7 +68,8 @@ def test_two_rank_bench_line(comm):
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
                         "--gpus", "2", "--config", "tiny", "--steps", "3", "--warmup", "3", "--e2e-steps", "2",
-                        "--comm", comm], capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+                        "--comm", comm[:4]] + (["--sync-free"] if comm == "peer_sf" else []),
+                       capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
     assert len(lines) == 1, r.stdout
