@@ -93,6 +93,55 @@ __global__ void __launch_bounds__(32) k_feed(const uint8_t* src, size_t footprin
   if (blockIdx.x == 0) sink[1] = c1 - c0;
 }
 
+#include <cuda.h>
+// TMA tensor loads as the GEMMs issue them: NB boxes of {64 bf16 cols (128 B), BR rows} per stage
+// (128B swizzle), one thread issuing, STAGES-deep ring -- the operand path of the TMA-fed kinds.
+template <int STAGES, int BR, int NB>
+__global__ void __launch_bounds__(32) k_feed_tma(const __grid_constant__ CUtensorMap map, int rows, int iters,
+                                                 unsigned long long* sink) {
+  extern __shared__ __align__(1024) uint8_t smem_t[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_t) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[STAGES];
+  constexpr int CH = NB * BR * 128;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(su32(&full[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  int it_row = blockIdx.x * 97;
+  uint32_t ph[STAGES] = {0};
+  auto issue = [&](int s) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(&full[s])), "r"(CH));
+    for (int b = 0; b < NB; ++b) {
+      const int r0 = (it_row % (rows / BR)) * BR;
+      asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                   ::"r"(su32(sm + s * CH + b * BR * 128)), "l"(&map), "r"(su32(&full[s])), "r"(64 * (b % 24)), "r"(r0)
+                   : "memory");
+    }
+    it_row += gridDim.x;
+  };
+  for (int s = 0; s < STAGES; ++s) issue(s);
+  const unsigned long long c0 = clock64();
+  unsigned long long acc = 0;
+  for (int it = 0; it < iters; ++it) {
+    const int s = it % STAGES;
+    asm volatile("{\n.reg .pred p;\nW: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n@!p bra W;\n}\n" ::"r"(su32(&full[s])),
+                 "r"(ph[s]));
+    ph[s] ^= 1;
+    acc += sm[s * CH + (it & 127)];
+    issue(s);
+  }
+  for (int s = 0; s < STAGES; ++s) {
+    const int k = (iters + s) % STAGES;
+    asm volatile("{\n.reg .pred p;\nW2: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n@!p bra W2;\n}\n" ::"r"(su32(&full[k])),
+                 "r"(ph[k]));
+    ph[k] ^= 1;
+  }
+  if (acc == 0xFFFFFFFFull) sink[0] = acc;
+  if (blockIdx.x == 0) sink[1] = clock64() - c0;
+}
+
 int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -142,6 +191,41 @@ int main() {
     printf("%-26s grid %3d  %8.1f GB/s into smem  %6.1f B/clk/SM  (%.3f ms, %.2f GHz)  %s\n", m.name, grid,
            bytes / ms / 1e6, (double)(iters + STAGES) * CHUNK / (double)h[1], ms, h[1] / (ms * 1e6),
            cudaGetErrorString(cudaGetLastError()));
+  }
+  {
+    // tensor-map TMA loads from an L2-resident [rows, 1536] bf16 matrix (24 column boxes of 64)
+    const int cols = 1536, rows = 16384;  // 48 MB
+    CUtensorMap map;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t es[2] = {1, 1};
+#define TFEED(BR, NB)                                                                                          \
+    {                                                                                                          \
+      cuuint32_t box[2] = {64, BR};                                                                            \
+      cuTensorMapEncodeTiled(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es,           \
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,                         \
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);            \
+      auto kt = k_feed_tma<6, BR, NB>;                                                                         \
+      const int smb = 6 * NB * BR * 128 + 1024;                                                                \
+      cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, smb);                              \
+      const int grid = sms, iters = 3000;                                                                      \
+      kt<<<grid, 32, smb>>>(map, rows, 100, sink);                                                             \
+      cudaEvent_t a, b;                                                                                        \
+      cudaEventCreate(&a);                                                                                     \
+      cudaEventCreate(&b);                                                                                     \
+      cudaEventRecord(a);                                                                                      \
+      kt<<<grid, 32, smb>>>(map, rows, iters, sink);                                                           \
+      cudaEventRecord(b);                                                                                      \
+      cudaEventSynchronize(b);                                                                                 \
+      float ms;                                                                                                \
+      cudaEventElapsedTime(&ms, a, b);                                                                         \
+      unsigned long long h[2];                                                                                 \
+      cudaMemcpy(h, sink, 16, cudaMemcpyDeviceToHost);                                                         \
+      const double bytes = (double)grid * (iters + 6) * NB * BR * 128;                                         \
+      printf("TMA tensor boxes 64x%-3d x%d per stage        %8.1f GB/s into smem  %6.1f B/clk/SM  %s\n", BR, NB,  \
+             bytes / ms / 1e6, (double)(iters + 6) * NB * BR * 128 / (double)h[1], cudaGetErrorString(cudaGetLastError())); \
+    }
+    TFEED(128, 2) TFEED(64, 4) TFEED(32, 8) TFEED(128, 1) TFEED(256, 1)
   }
   return 0;
 }
