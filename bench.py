@@ -93,7 +93,7 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4, fp8_up=False, w1_cached=False):
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,enforced.power.limit,{pw}")
 
     def __init__(self, dev):
         self.dev = dev
@@ -101,10 +101,23 @@ class ClockSampler:
         self.skip = 0
         self.path = os.path.join("/tmp", f"sonic_clocks_{os.getpid()}.csv")
 
+    @staticmethod
+    def power_field(dev):
+        # instantaneous board power where the driver has it (power.draw averages over ~1 s, longer than
+        # a short timed region); "power.draw" otherwise
+        try:
+            r = subprocess.run(["nvidia-smi", "-i", str(dev), "--query-gpu=power.draw.instant",
+                                "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+            float(r.stdout.strip().splitlines()[0])
+            return "power.draw.instant"
+        except Exception:
+            return "power.draw"
+
     def start(self):
         try:
             self.fh = open(self.path, "w")
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+            fields = self.FIELDS.format(pw=self.power_field(self.dev))
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={fields}",
                                           "--format=csv,noheader,nounits", "-lms", "20"], stdout=self.fh,
                                          stderr=subprocess.DEVNULL)
         except Exception:
@@ -125,7 +138,7 @@ class ClockSampler:
         self.proc.terminate()
         self.proc.wait()
         self.fh.close()
-        sms, mx, reasons = [], None, set()
+        sms, mx, reasons, pw, plim = [], None, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         lines = open(self.path).readlines()
         lines = lines[self.skip:] or lines[-1:]  # drop the idle sample(s) from before the timed region
@@ -141,9 +154,17 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
+            try:  # board power (instantaneous where available) against the enforced limit
+                pw.append(float(parts[8]) if len(parts) > 8 else float(parts[2]))
+                plim = float(parts[7]) if len(parts) > 7 else plim
+            except ValueError:
+                pass
         sms.sort()
+        pw.sort()
         med = sms[len(sms) // 2] if sms else None
-        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms)}
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sms),
+                "power_w": pw[len(pw) // 2] if pw else None, "power_w_max": pw[-1] if pw else None,
+                "power_limit_w": plim}
 
 
 # --------------------------------------------------------------------------- CPU oracle leg

@@ -62,6 +62,16 @@ struct GemmArgs {
   float* dS;                // DH: dS [rows] if n_tiles == 1, else partials [n_tiles][rows_max]
   long long rows_max;
   unsigned long long* dbg;  // SONIC_TIMING builds only: cycle counters (see sonic_api.cu)
+  int wide;                 // DOWN / DXT: mC0 is the 3-D [col block, row, 64 cols] view of the output and one
+                            // TMA store writes SONIC_WIDE_ST 64-column chunks (0: 2-D map, one store per chunk)
+  // DW1 / DW2 with SONIC_AGG_FUSE: the dX aggregation (Alg. 5's last kernel) of tokens
+  // [agg_t0, agg_t1) runs on this kernel's aggregator warp(s), contiguous token blocks per CTA
+  const __nv_bfloat16* agg_src;  // dX~ [rows, agg_d]
+  __nv_bfloat16* agg_dst;        // dX [T, agg_d]
+  const int* agg_rowptr;         // token CSR over grouped rows (expert-ascending)
+  const int* agg_rows;
+  long long agg_t0, agg_t1;
+  int agg_d;
   int accumulate;           // DW1 / DW2: add into the existing dW (SONIC_F_DW_ACCUMULATE) instead of overwriting
   int dw_bf16;              // DW1 / DW2: store dW as bf16 (SONIC_F_DW_BF16; the store map is then bf16)
   const float* sx;          // UP8: per-token scale of the e4m3 X rows [T]
@@ -78,9 +88,17 @@ template <> struct Traits<K_DXT>  { static constexpr bool vk = false, a_gather =
 template <> struct Traits<K_DW2>  { static constexpr bool vk = true,  a_gather = false, a_mn = true,  b_gather = true,  b_mn = true;  };
 template <> struct Traits<K_DW1>  { static constexpr bool vk = true,  a_gather = true,  a_mn = true,  b_gather = false, b_mn = true;  };
 
+// Gathered kinds: NP producer warps issue the cp.async gathers, 8 lanes per 128-byte row, so one
+// pass covers 4 * NP rows (SONIC_NP_VK for the varlen-K kinds, SONIC_NP_VM for the varlen-M ones).
+#ifndef SONIC_NP_VK
+#define SONIC_NP_VK 4
+#endif
+#ifndef SONIC_NP_VM
+#define SONIC_NP_VM 4
+#endif
 template <int KIND>
 __host__ __device__ constexpr int num_producer_warps() {
-  return (Traits<KIND>::a_gather || Traits<KIND>::b_gather) ? 4 : 1;
+  return (Traits<KIND>::a_gather || Traits<KIND>::b_gather) ? (Traits<KIND>::vk ? SONIC_NP_VK : SONIC_NP_VM) : 1;
 }
 // Epilogue warps: 4 (one per TMEM lane quarter).  SONIC_EPI_WARPS=8 puts two warps on each quarter,
 // each taking every other 64-column chunk; measured slower at 7B (725 vs 745 TF: fewer registers
@@ -102,9 +120,23 @@ template <int KIND>
 __host__ __device__ constexpr int epi_warps() {
   return KIND == K_DOWN ? SONIC_EPI_WARPS_DOWN : KIND == K_UP8 ? SONIC_EPI_WARPS_UP8 : EPI_WARPS;
 }
+// Fused dX aggregation (SONIC_AGG_FUSE = 1, varlen-K kinds): AGW aggregator warps after the
+// epilogue warps stream the grouped dX~ rows of their tokens into a shared-memory ring of AGG_SLOT-byte
+// slots with bulk copies (the TMA engine, not the LSU path the gather producers use) and sum them.
+#ifndef SONIC_AGG_FUSE
+#define SONIC_AGG_FUSE 0
+#endif
+#ifndef SONIC_AGG_RING
+#define SONIC_AGG_RING 49152  // bytes of row slots (7B: 16 slots of one 3 KB dX~ row)
+#endif
+constexpr int AGG_CHUNK = 2048;  // columns per work item at most (a 4 KB slot)
+template <int KIND>
+__host__ __device__ constexpr int agg_warps() { return (SONIC_AGG_FUSE && Traits<KIND>::vk) ? 1 : 0; }
+template <int KIND>
+__host__ __device__ constexpr int agg_bytes() { return agg_warps<KIND>() ? 1024 + SONIC_AGG_RING : 0; }
 template <int KIND>
 __host__ __device__ constexpr int gemm_threads() {
-  return 32 * (num_producer_warps<KIND>() + 1 + epi_warps<KIND>());
+  return 32 * (num_producer_warps<KIND>() + 1 + epi_warps<KIND>() + agg_warps<KIND>());
 }
 
 constexpr int GEMM_BM = 128;
@@ -115,8 +147,9 @@ constexpr int STG_BYTES = 4096;  // one epilogue staging buffer: 32 rows x 128 B
 #endif
 constexpr int SMEM_LIMIT = SONIC_SMEM_LIMIT;
 
-template <int BN, bool CTA2, bool HTMA, int NB_, bool HRING_ = false, int EPW_ = EPI_WARPS>
+template <int BN, bool CTA2, bool HTMA, int NB_, bool HRING_ = false, int EPW_ = EPI_WARPS, int XB_ = 0>
 struct GemmCfg {
+  static constexpr int XB = XB_;         // extra fixed bytes (the fused aggregation's ring)
   static constexpr int EPW = EPW_;       // epilogue warps
   static constexpr int EPH = EPW_ / 4;   // warps per TMEM lane quarter
   static constexpr int BNL = CTA2 ? BN / 2 : BN;  // B columns (or rows) held by this CTA
@@ -131,7 +164,7 @@ struct GemmCfg {
   static constexpr bool HRING = HRING_;
   static constexpr int HBUF_WARP = HRING ? 2 * 2 * STG_BYTES : HTMA ? 32 * 2 * HCOLS_WARP * 2 : 0;
   // + 1 KB alignment slack + barriers / dS exchange / TMEM address (< 1 KB)
-  static constexpr int FIXED = EPW * NB * STG_BYTES + EPW * HBUF_WARP + 1024 + 1024;
+  static constexpr int FIXED = EPW * NB * STG_BYTES + EPW * HBUF_WARP + 1024 + 1024 + XB;
   static constexpr int STAGES_RAW = (SMEM_LIMIT - FIXED) / (int)STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
@@ -139,16 +172,37 @@ struct GemmCfg {
                                         : (2 * BN <= 256) ? 256 : 512;
 };
 
+// Wide epilogue stores (DOWN, DXT): G = SONIC_WIDE_ST consecutive 64-column staging buffers go out
+// as ONE 3-D TMA store (box 64 x 32 rows x G column blocks) instead of G 4 KB stores.  These two
+// kinds have few k-blocks per tile (K = n or 2n), so their SM's TMA unit moves the operand tiles and
+// 64 KB of output per CTA per tile; each box costs the TMA unit a fixed issue overhead on top of its
+// bytes (tools/l2feed.cu: 4 KB boxes move 58 B/clk, 16 KB boxes 107 B/clk).
+#ifndef SONIC_WIDE_DOWN
+#define SONIC_WIDE_DOWN 1
+#endif
+#ifndef SONIC_WIDE_DXT
+#define SONIC_WIDE_DXT 1
+#endif
+#ifndef SONIC_WIDE_SLOTS
+#define SONIC_WIDE_SLOTS 1  // staging ring = SLOTS x G buffers per epilogue warp
+#endif
+template <int KIND>
+__host__ __device__ constexpr int wide_g() { return KIND == K_DOWN ? SONIC_WIDE_DOWN : KIND == K_DXT ? SONIC_WIDE_DXT : 1; }
 // DH with BN in {64, 128} reads H through TMA into per-warp smem buffers ("asynchronous
 // TMA load of H in the dH epilogue").  Staging ring depth NB: 2 (a deeper ring costs a mainloop
 // stage, measured slower).
 template <int KIND, int BN, bool CTA2>
+#ifndef SONIC_NB_DW
+#define SONIC_NB_DW 2  // staging ring depth of the weight-gradient kernels
+#endif
 #ifndef SONIC_NB_DOWN
 #define SONIC_NB_DOWN 2  // staging ring depth of the down-proj (4 measured the same at 7B)
 #endif
 using KCfg = GemmCfg<BN, CTA2, KIND == K_DH && BN <= 128,
-                     (KIND == K_DH && BN == 256) ? 0 : (KIND == K_DOWN ? SONIC_NB_DOWN : 2),
-                     KIND == K_DH && BN == 256, epi_warps<KIND>()>;
+                     (KIND == K_DH && BN == 256) ? 0
+                     : (wide_g<KIND>() > 1) ? wide_g<KIND>() * SONIC_WIDE_SLOTS
+                     : (KIND == K_DOWN ? SONIC_NB_DOWN : Traits<KIND>::vk ? SONIC_NB_DW : 2),
+                     KIND == K_DH && BN == 256, epi_warps<KIND>(), agg_bytes<KIND>()>;
 
 struct TileCoord {
   int e, row0, nt, mt, nkb, seg0;
@@ -229,6 +283,24 @@ __device__ __forceinline__ void gather16(uint32_t dst, const void* src, uint64_t
   else ptx::cp_async16(dst, src);
 }
 
+// fp32 += 8 bf16 (one 16-byte chunk), and 8 fp32 -> 8 bf16 (round to nearest even): the fused
+// aggregation's arithmetic, identical to aggregate.cu's
+__device__ __forceinline__ void acc8_bf16(float (&a)[8], const uint4& v) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    a[2 * i] += f.x;
+    a[2 * i + 1] += f.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8_bf16(const float (&a)[8]) {
+  uint4 o;
+  __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) oh[i] = __floats2bfloat162_rn(a[2 * i], a[2 * i + 1]);
+  return o;
+}
 __device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
 // sigma(x) = 0.5 tanh(x/2) + 0.5 with the SFU tanh (rel. err ~2^-11, far below bf16's 2^-8)
 __device__ __forceinline__ float tanh_approx(float x) {
@@ -274,6 +346,23 @@ struct StoreQ {
       ptx::bulk_commit();
     }
     sb = (i + 1) % NB;
+  }
+  // wide stores: the ring as NB / G slots of G consecutive buffers, one 3-D store per slot
+  template <int G>
+  __device__ __forceinline__ int acquire_slot(int lane) {
+    static_assert(NB % G == 0, "wide store slots");
+    wait_reads<NB / G - 1>(lane);
+    return sb;
+  }
+  template <int G>
+  __device__ __forceinline__ void issue_slot(int lane, int s, const CUtensorMap* map, int c0, int c1, int c2) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::tma_store_3d(map, base + s * G * STG_BYTES, c0, c1, c2);
+      ptx::bulk_commit();
+    }
+    sb = (s + 1) % (NB / G);
   }
   __device__ __forceinline__ void issue3d(int lane, int i, const CUtensorMap* map, int c0, int c1, int c2,
                                           bool add = false) {
@@ -440,47 +529,53 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         }
       }
     } else {
-      const int pt = threadIdx.x;  // 0..127
+      const int pt = threadIdx.x;  // 0..32 NP - 1
       const int c = pt & 7;        // 16-byte chunk within a 128-byte row
+      constexpr int RS = NP * 4;   // rows per pass (a multiple of 8: the swizzle phase is r0 & 7)
+      constexpr int JM = GEMM_BM / RS, JK = GEMM_BK / RS;
+      static_assert(RS % 8 == 0 && GEMM_BM % RS == 0 && GEMM_BK % RS == 0, "producer warp count");
       const uint64_t gpol = ptx::policy_evict_last();  // gathered rows are re-read by K experts' tiles
-      const int r0 = pt >> 3;      // rows r0 + 16 j
+      const int r0 = pt >> 3;      // rows r0 + RS j
       const uint32_t sw = (uint32_t)((c ^ (r0 & 7)) << 4);
       // Gather indices are prefetched one tile (varlen-M) / one stage (varlen-K) ahead so the
       // dependent cp.async addresses never wait on a global load.
-      int ntok[8];
+      int ntok[JM];
+#ifdef SONIC_TIMING
+      unsigned long long p_empty = 0, p_c0 = clock64();
+#endif
       // varlen-K prefetch ring: KPD k-blocks of gather indices in flight.  The index loads share
       // the LSU queue with the producers' own outstanding cp.async gathers, so their effective
       // latency is the gathers' (often HBM) latency: the deeper the ring the better until the
       // registers run out (16: 4 indices x 16 k-blocks per thread, no spills)
       constexpr int KPD = Tr::vk ? SONIC_KPD : 1;
       constexpr int KU = Tr::vk ? KPD : 1;
-      int ktok[KPD][4];
+      int ktok[KPD][JK];
       if constexpr (!Tr::vk) {
         if (t_first < total_tiles) {
           const TileCoord t0 = decode_tile<KIND, CTA2, MFAST>(args, t_first, rank);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) ntok[j] = t0.valid ? tok_of(args.row_token, t0.row0 + r0 + 16 * j) : 0;
+          for (int j = 0; j < JM; ++j) ntok[j] = t0.valid ? tok_of(args.row_token, t0.row0 + r0 + RS * j) : 0;
         }
       }
       for (int tile = t_first; tile < total_tiles; tile += t_step) {
         const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);
         const int n0 = tc.nt * BN + rank * BNL;
-        const uint8_t* srcM[8];  // byte addresses: a k-block is 128 bytes of a row (64 bf16 / 128 e4m3)
+        const uint8_t* srcM[JM];  // byte addresses: a k-block is 128 bytes of a row (64 bf16 / 128 e4m3)
         if constexpr (!Tr::vk) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < JM; ++j)
             srcM[j] = reinterpret_cast<const uint8_t*>(args.gsrc) + clamp_tok(ntok[j]) * args.gld * ESZ + c * 16;
           if (tile + t_step < total_tiles) {
             const TileCoord tn = decode_tile<KIND, CTA2, MFAST>(args, tile + t_step, rank);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ntok[j] = tn.valid ? tok_of(args.row_token, tn.row0 + r0 + 16 * j) : 0;
+            for (int j = 0; j < JM; ++j) ntok[j] = tn.valid ? tok_of(args.row_token, tn.row0 + r0 + RS * j) : 0;
           }
         } else {
 #pragma unroll
           for (int u = 0; u < KPD; ++u)
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              ktok[u][j] = u < tc.nkb ? tok_of(args.row_token, tc.seg0 + u * GEMM_BK + r0 + 16 * j) : 0;
+            for (int j = 0; j < JK; ++j)
+              ktok[u][j] = u < tc.nkb ? tok_of(args.row_token, tc.seg0 + u * GEMM_BK + r0 + RS * j) : 0;
         }
         // varlen-K A gather of a missing half: read column 0 (finite, never stored)
         const int acol0 = (Tr::a_gather && tc.valid) ? tc.mt * GEMM_BM : 0;
@@ -491,27 +586,33 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         for (int u = 0; u < KU; ++u) {
           const int kb = kb0 + u;
           if (kb >= tc.nkb) break;
-          const __nv_bfloat16* srcK[4];
+          const __nv_bfloat16* srcK[JK];
           if constexpr (Tr::vk) {
             const int col0 = Tr::a_gather ? acol0 : n0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) srcK[j] = args.gsrc + clamp_tok(ktok[u][j]) * args.gld + col0 + c * 8;
+            for (int j = 0; j < JK; ++j) srcK[j] = args.gsrc + clamp_tok(ktok[u][j]) * args.gld + col0 + c * 8;
             if constexpr (SONIC_L2PF > 0) {
               static_assert(SONIC_L2PF < KPD, "L2 prefetch reads the index ring");
               constexpr int NPF = Tr::a_gather ? 2 : BNL / 64;  // 128-byte lines per gathered row
               if (c < NPF && kb + SONIC_L2PF < tc.nkb) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
+                for (int j = 0; j < JK; ++j)
                   ptx::prefetch_l2(args.gsrc + clamp_tok(ktok[(u + SONIC_L2PF) % KPD][j]) * args.gld + col0 + 64 * c);
               }
             }
             if (kb + KPD < tc.nkb) {
               const int krow1 = tc.seg0 + (kb + KPD) * GEMM_BK;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) ktok[u][j] = tok_of(args.row_token, krow1 + r0 + 16 * j);
+              for (int j = 0; j < JK; ++j) ktok[u][j] = tok_of(args.row_token, krow1 + r0 + RS * j);
             }
           }
+#ifdef SONIC_TIMING
+          unsigned long long cpe = clock64();
+#endif
           ptx::mbar_wait(&empty[stage], phase ^ 1);
+#ifdef SONIC_TIMING
+          if (pt == 0) p_empty += clock64() - cpe;
+#endif
           uint8_t* sA = smem + stage * STAGE_BYTES;
           uint8_t* sB = sA + A_BYTES;
           uint64_t* bar = &full[stage];
@@ -572,19 +673,19 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             if constexpr (SONIC_L2PF > 0) {
               if (c == 0 && kb + SONIC_L2PF < tc.nkb) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) ptx::prefetch_l2(srcM[j] + (kb + SONIC_L2PF) * 128);
+                for (int j = 0; j < JM; ++j) ptx::prefetch_l2(srcM[j] + (kb + SONIC_L2PF) * 128);
               }
             }
             const uint32_t dst = ptx::smem_u32(sA) + r0 * 128 + sw;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) gather16(dst + j * 16 * 128, srcM[j] + kb * 128, gpol);
+            for (int j = 0; j < JM; ++j) gather16(dst + j * RS * 128, srcM[j] + kb * 128, gpol);
           } else {  // 64 gathered K-rows x (128 | BNL) MN-columns (MN-major)
             constexpr int NCH = Tr::a_gather ? 2 : BNL / 64;
             const uint32_t dst = ptx::smem_u32(Tr::a_gather ? sA : sB) + r0 * 128 + sw;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < JK; ++j)
 #pragma unroll
-              for (int jj = 0; jj < NCH; ++jj) gather16(dst + jj * 8192 + j * 16 * 128, srcK[j] + 64 * jj, gpol);
+              for (int jj = 0; jj < NCH; ++jj) gather16(dst + jj * 8192 + j * RS * 128, srcK[j] + 64 * jj, gpol);
           }
           ptx::cp_async_mbar_arrive(bar);  // arrives on this CTA's barrier when the copies land
           if (++stage == STAGES) {
@@ -594,6 +695,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         }
         }
       }
+#ifdef SONIC_TIMING
+      if (args.dbg && pt == 0) {
+        atomicAdd(args.dbg + 6, p_empty);
+        atomicAdd(args.dbg + 7, clock64() - p_c0);
+      }
+#endif
     }
   } else if (warp == NP) {
     // ============================================================ MMA issuer (leader) / relay (peer)
@@ -688,7 +795,7 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp < NP + 1 + Cfg::EPW) {
     // ============================================================ epilogue (Cfg::EPW warps)
     const int ew = warp - NP - 1;
     const int q = warp & 3;         // TMEM lane quarter this warp may access
@@ -900,6 +1007,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
         float gate = 1.f;
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
         constexpr int NCH = BN / (64 * Cfg::EPH);
+        static_assert(wide_g<KIND>() == 1 || Cfg::EPH == 1, "wide stores: one warp per TMEM lane quarter");
+        int wslot = 0;
         uint32_t r[2][2][32];
         auto col_of = [&](int j) { return 64 * half + j * 64 * Cfg::EPH; };
         auto live = [&](int j) { return j < NCH && tc.nt * BN + col_of(j) < args.N_dim; };
@@ -918,7 +1027,16 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             ptx::tmem_ld32(t_acc + col_of(j + 1), r[sl ^ 1][0]);
             ptx::tmem_ld32(t_acc + col_of(j + 1) + 32, r[sl ^ 1][1]);
           }
-          const int i = sq.acquire(lane);
+          constexpr int G = wide_g<KIND>();
+          constexpr bool WIDE = G > 1 && NCH % G == 0;  // a slot never spans two N tiles
+          int i, slot = 0;
+          if (WIDE && args.wide) {  // chunk j goes to buffer j % G of the current slot
+            if (j % G == 0) wslot = sq.template acquire_slot<G>(lane);
+            slot = wslot;
+            i = slot * G + j % G;
+          } else {
+            i = sq.acquire(lane);
+          }
           const uint32_t b = sq.addr(i);
 #pragma unroll
           for (int h = 0; h < 2; ++h)
@@ -931,7 +1049,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
                                 ptx::pack_bf16(gate * __uint_as_float(v[4]), gate * __uint_as_float(v[5])),
                                 ptx::pack_bf16(gate * __uint_as_float(v[6]), gate * __uint_as_float(v[7])));
             }
-          sq.issue(lane, i, &mC0, tc.nt * BN + col_of(j), wrow);
+          if (WIDE && args.wide) {
+            if (j % G == G - 1 || !live(j + 1))  // clipped at the last column block by the map
+              sq.template issue_slot<G>(lane, slot, &mC0, 0, wrow, (tc.nt * BN + col_of(j - j % G)) / 64);
+          } else {
+            sq.issue(lane, i, &mC0, tc.nt * BN + col_of(j), wrow);
+          }
           if (live(j + 1)) {
             ptx::tmem_ld_wait();
             ptx::tmem_regs_ready(r[sl ^ 1][0]);
@@ -1268,6 +1391,137 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
 #endif
     if (lane == 0) ptx::bulk_wait<0>();
     __syncwarp();
+  } else {
+    // ============================================================ fused dX aggregation (SONIC_AGG_FUSE)
+    // dX_t = sum of the token's dX~ rows in CSR (expert-ascending) order, fp32: exactly k_aggregate's
+    // arithmetic (Alg. 5).  Work items are (token, column chunk, row), in that order;
+    // item i lives in ring slot i % NS (parity (i / NS) & 1).  Lane k bulk-copies row k of the chunk
+    // being issued; the row lists are loaded two tokens ahead so no issue waits on an index load;
+    // the warp sums each (token, chunk) out of shared memory and stores dX with 16-byte stores.
+    if constexpr (agg_warps<KIND>() > 0) {
+      const long long ntok = args.agg_t1 - args.agg_t0;
+      const long long per = ntok > 0 ? (ntok + gridDim.x - 1) / gridDim.x : 0;
+      const long long tb = args.agg_t0 + (long long)blockIdx.x * per;
+      const long long te = min(args.agg_t1, tb + per);
+      if (tb < te) {
+        uint8_t* abase = reinterpret_cast<uint8_t*>(full) + 1024;
+        uint64_t* abar = reinterpret_cast<uint64_t*>(abase);  // [32]
+        int* tok_nr = reinterpret_cast<int*>(abase + 256);    // [64] per token (t - tb) & 63
+        int* tok_r0 = tok_nr + 64;                            // [64]
+        const uint32_t aslot = ptx::smem_u32(abase + 1024);
+        const int dd = args.agg_d;
+        const int CC = dd < AGG_CHUNK ? dd : AGG_CHUNK;  // columns per chunk
+        const int nch = (dd + CC - 1) / CC;
+        const uint32_t slot_b = (uint32_t)CC * 2;
+        const int NS = min(32, (int)(SONIC_AGG_RING / slot_b));
+        const __nv_bfloat16* src = args.agg_src;
+        if (lane == 0) {
+          for (int i = 0; i < NS; ++i) ptx::mbar_init(&abar[i], 1);
+          ptx::fence_barrier_init();
+        }
+        // row-list pipeline: (inr, irow) = token ti being issued, (nnr, nrow) = ti + 1, rpc = rowptr of ti + 2
+        auto rp_load = [&](long long t) { return (lane < 2 && t + lane <= te) ? __ldg(args.agg_rowptr + t + lane) : 0; };
+        auto list_of = [&](long long t, int rp, int& nr, int& row, int& r0) {
+          r0 = __shfl_sync(0xffffffffu, rp, 0);
+          nr = t < te ? __shfl_sync(0xffffffffu, rp, 1) - r0 : 0;
+          row = (lane < nr && lane < 32) ? __ldg(args.agg_rows + r0 + lane) : 0;
+        };
+        long long ti = tb;
+        int ic = 0, ni = 0, nc = 0;
+        int inr, irow, ir0, nnr, nrow, nr0;
+        list_of(tb, rp_load(tb), inr, irow, ir0);
+        list_of(tb + 1, rp_load(tb + 1), nnr, nrow, nr0);
+        int rpc = rp_load(tb + 2);
+        if (lane == 0) { tok_nr[0] = inr; tok_r0[0] = ir0; }
+        auto advance = [&]() {
+          ++ti;
+          ic = 0;
+          inr = nnr; irow = nrow; ir0 = nr0;
+          list_of(ti + 1, rpc, nnr, nrow, nr0);
+          rpc = rp_load(ti + 2);
+          if (lane == 0 && ti < te) { tok_nr[(ti - tb) & 63] = inr; tok_r0[(ti - tb) & 63] = ir0; }
+        };
+        long long t = tb;  // consumer token
+#ifdef SONIC_TIMING
+        unsigned long long ag_wait = 0, ag_c0 = clock64();
+#endif
+        auto issue = [&]() {
+          while (ti < te && ti - t < 48) {
+            if (inr == 0 || inr > NS) {  // no rows / summed straight from global memory
+              advance();
+              continue;
+            }
+            if (ni + inr > nc + NS) break;  // not enough free slots for this chunk's rows
+            if (lane < inr) {
+              const int sidx = (ni + lane) % NS;
+              const int cols = min(CC, dd - ic * CC);
+              ptx::mbar_arrive_expect_tx(&abar[sidx], (uint32_t)cols * 2);
+              ptx::bulk_g2s(aslot + sidx * slot_b, src + (long long)irow * dd + (long long)ic * CC, (uint32_t)cols * 2,
+                            &abar[sidx]);
+            }
+            ni += inr;
+            if (++ic == nch) advance();
+          }
+        };
+        __syncwarp();
+        for (; t < te; ++t) {
+          for (int c = 0; c < nch; ++c) {
+            issue();
+            __syncwarp();
+            const int nr = tok_nr[(t - tb) & 63], r0 = tok_r0[(t - tb) & 63];
+            const int cols = min(CC, dd - c * CC);
+            uint4* dst = reinterpret_cast<uint4*>(args.agg_dst + t * dd + (long long)c * CC);
+            if (nr > NS) {  // more rows than slots (token rounding / expert choice outliers)
+              const uint4* sv = reinterpret_cast<const uint4*>(src);
+              for (int v = lane; v < cols / 8; v += 32) {
+                float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                for (int k = 0; k < nr; ++k)
+                  acc8_bf16(a, ptx::ld_nc_v4(sv + ((long long)__ldg(args.agg_rows + r0 + k) * dd + (long long)c * CC) / 8 + v));
+                dst[v] = pack8_bf16(a);
+              }
+              continue;
+            }
+#ifdef SONIC_TIMING
+            unsigned long long cw0 = clock64();
+#endif
+            for (int k = 0; k < nr; ++k) ptx::mbar_wait(&abar[(nc + k) % NS], (uint32_t)((nc + k) / NS) & 1u);
+#ifdef SONIC_TIMING
+            ag_wait += clock64() - cw0;
+#endif
+            if (nr == 8) {  // top-8 routing: all eight row loads in flight, then the in-order sum
+              uint32_t sb[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) sb[u] = aslot + ((nc + u) % NS) * slot_b;
+              for (int v = lane; v < cols / 8; v += 32) {
+                float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                uint4 x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x[u] = ptx::ld_shared_v4(sb[u] + v * 16);
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc8_bf16(a, x[u]);
+                dst[v] = pack8_bf16(a);
+              }
+            } else {
+              for (int v = lane; v < cols / 8; v += 32) {
+                float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                for (int k = 0; k < nr; ++k) acc8_bf16(a, ptx::ld_shared_v4(aslot + ((nc + k) % NS) * slot_b + v * 16));
+                dst[v] = pack8_bf16(a);
+              }
+            }
+            nc += nr;
+            __syncwarp();  // every lane's reads of these slots are done before they are refilled
+            ptx::fence_proxy_async_smem();
+          }
+        }
+#ifdef SONIC_TIMING
+        if (args.dbg && lane == 0) {
+          atomicAdd(args.dbg + 8, clock64() - ag_c0);
+          atomicAdd(args.dbg + 9, ag_wait);
+          atomicAdd(args.dbg + 10, (unsigned long long)(te - tb));
+        }
+#endif
+      }
+    }
   }
 
   ptx::tc_fence_before();

@@ -101,6 +101,20 @@ bool map3d_u8(CUtensorMap* m, const void* ptr, long long E, long long rows, long
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// Wide-store view of a row-major bf16 [rows, cols] output (cols % 64 == 0): 3-D {64 columns, rows,
+// column block} with strides {cols * 2, 128} bytes; box {64, 32, G} = G stacked 32 x 128 B swizzled
+// staging buffers, i.e. G consecutive 64-column chunks of 32 rows in one TMA store.
+bool map_wide(CUtensorMap* m, const void* ptr, long long rows, long long cols, int G) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc || cols % 64) return false;
+  cuuint64_t gdim[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
+  cuuint64_t gstride[2] = {(cuuint64_t)(cols * 2), 128};
+  cuuint32_t box[3] = {64, 32, (cuuint32_t)G};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 // 3-D row-major [E, rows, cols] tensor; box {box_cols, box_rows, 1}; 128B swizzle.
 bool map3d(CUtensorMap* m, const void* ptr, bool f32, long long E, long long rows, long long cols, int box_cols,
            int box_rows) {
@@ -116,6 +130,9 @@ bool map3d(CUtensorMap* m, const void* ptr, bool f32, long long E, long long row
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+#ifndef SONIC_AGG_DW2_PCT
+#define SONIC_AGG_DW2_PCT 0  // SONIC_AGG_FUSE: share of the tokens aggregated inside dW2 (the rest: dW1)
+#endif
 #ifndef SONIC_BWD_OVERLAP
 #define SONIC_BWD_OVERLAP 0  // 7B, same run: 0 -> 2.186 ms, 1 -> 2.180, 3 -> 2.183 / 2.141: no measured gain, so serial (clean per-kernel attribution)
 #endif
@@ -203,8 +220,13 @@ bool launch_gemm_t(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);
   const double n = h[5] ? (double)h[5] : 1.0;
-  fprintf(stderr, "TIMING kind=%d BN=%d cta2=%d: mma_total %.0f  wait_tempty %.0f  wait_full %.0f | epi_wait_tfull %.0f  epi_busy %.0f (kcycles; epilogue counters summed over the pair)\n",
-          KIND, BN, (int)CTA2, h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3, h[3] / n / 1e3, h[4] / n / 1e3);
+  const double nc = n * (CTA2 ? 2.0 : 1.0);  // CTAs (gathered kinds' producer counters are per CTA)
+  fprintf(stderr, "TIMING kind=%d BN=%d cta2=%d: mma_total %.0f  wait_tempty %.0f  wait_full %.0f | epi_wait_tfull %.0f  epi_busy %.0f (kcycles; epilogue counters summed over the pair) | gather producer total %.0f wait_empty %.0f (per CTA)\n",
+          KIND, BN, (int)CTA2, h[0] / n / 1e3, h[1] / n / 1e3, h[2] / n / 1e3, h[3] / n / 1e3, h[4] / n / 1e3,
+          h[7] / nc / 1e3, h[6] / nc / 1e3);
+  if (h[10])
+    fprintf(stderr, "TIMING fused aggregation: %.0f kcycles per CTA, waiting on rows %.0f, %.0f cycles per token\n",
+            h[8] / nc / 1e3, h[9] / nc / 1e3, (double)h[8] / (double)h[10]);
 #else
   const cudaError_t err = cudaLaunchKernelEx(&cfg, kern, a, b, c0, c1, dmap, args);
   if (err != cudaSuccess) {
@@ -722,6 +744,10 @@ sonic_status sonic_moe_fwd(const sonic_moe_desc* D, const void* X, const void* W
       return SONIC_ERR_CUDA;
     GemmArgs a = g;
     a.n_tiles = d / BN; a.k_blocks = (n + 63) / 64; a.N_dim = d;
+    if (wide_g<K_DOWN>() > 1 && d % 64 == 0 && (BN / 64) % wide_g<K_DOWN>() == 0) {  // as the kernel's WIDE
+      if (!map_wide(&mC0, Ybuf, R, d, wide_g<K_DOWN>())) return SONIC_ERR_CUDA;
+      a.wide = 1;
+    }
     ProfScope ps("down", st);
     // multicast cluster: the pair tiles (m, 2j) and (m, 2j+1) share the A rows
     if (!launch_gemm<K_DOWN>(BN, mA, mB, mC0, mC0, a, grid, st, &mA64, a.n_tiles % 2 == 0)) return SONIC_ERR_CUDA;
@@ -812,6 +838,10 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
       !map2d(&mC6, dXt, false, R, d, 64, 32) || !map2d(&mA6h, dH, false, R, 2 * n, 64, 64))
     return SONIC_ERR_CUDA;
   a6.n_tiles = d / BN6; a6.k_blocks = (2 * n) / 64; a6.N_dim = d;
+  if (wide_g<K_DXT>() > 1 && d % 64 == 0 && (BN6 / 64) % wide_g<K_DXT>() == 0) {
+    if (!map_wide(&mC6, dXt, R, d, wide_g<K_DXT>())) return SONIC_ERR_CUDA;
+    a6.wide = 1;
+  }
   // K5 dW2_e = A'_e^T Gather(dO)   (varlen-K)
   const bool dw_bf16 = (D->flags & SONIC_F_DW_BF16) != 0;
   if (!map2d(&mA5, Ap, false, R, n, 64, 64) || !map2d(&mB5, dO, false, s.T, d, 64, 1) ||
@@ -882,6 +912,20 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
     if (!run_dw2()) return SONIC_ERR_CUDA;
     cudaStreamWaitEvent(st, ss.join, 0);
     if (!run_dw1()) return SONIC_ERR_CUDA;
+  } else if (SONIC_AGG_FUSE) {
+    // the dX aggregation runs inside the weight-gradient kernels (aggregator warp, gemm.cuh): the
+    // first SONIC_AGG_DW2_PCT % of the tokens in dW2, the rest in dW1
+    const long long t_split = s.T * SONIC_AGG_DW2_PCT / 100;
+    for (GemmArgs* a : {&a5, &a7}) {
+      a->agg_src = static_cast<const __nv_bfloat16*>(dXt);
+      a->agg_dst = static_cast<__nv_bfloat16*>(dX);
+      a->agg_rowptr = rt->token_rowptr;
+      a->agg_rows = rt->token_rows;
+      a->agg_d = d;
+    }
+    a5.agg_t0 = 0; a5.agg_t1 = t_split;
+    a7.agg_t0 = t_split; a7.agg_t1 = s.T;
+    if (!run_dw2() || !run_dw1()) return SONIC_ERR_CUDA;
   } else {
     if (!run_dw2() || !run_dw1()) return SONIC_ERR_CUDA;
     run_agg();
