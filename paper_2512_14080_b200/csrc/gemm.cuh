@@ -96,9 +96,18 @@ template <> struct Traits<K_DW1>  { static constexpr bool vk = true,  a_gather =
 #ifndef SONIC_NP_VM
 #define SONIC_NP_VM 4
 #endif
+// SONIC_G4_VK = 1: the varlen-K kinds gather their token rows with TMA tile::gather4 (4 rows x 128 B
+// per instruction, issued by 16 lanes of the single producer warp) instead of cp.async, so the
+// gathered bytes travel the TMA path and count on the stage's transaction barrier like the tiles.
+#ifndef SONIC_G4_VK
+#define SONIC_G4_VK 0
+#endif
+template <int KIND>
+__host__ __device__ constexpr bool g4_kind() { return SONIC_G4_VK && Traits<KIND>::vk; }
 template <int KIND>
 __host__ __device__ constexpr int num_producer_warps() {
-  return (Traits<KIND>::a_gather || Traits<KIND>::b_gather) ? (Traits<KIND>::vk ? SONIC_NP_VK : SONIC_NP_VM) : 1;
+  return ((Traits<KIND>::a_gather || Traits<KIND>::b_gather) && !g4_kind<KIND>())
+             ? (Traits<KIND>::vk ? SONIC_NP_VK : SONIC_NP_VM) : 1;
 }
 // Epilogue warps: 4 (one per TMEM lane quarter).  SONIC_EPI_WARPS=8 puts two warps on each quarter,
 // each taking every other 64-column chunk; measured slower at 7B (725 vs 745 TF: fewer registers
@@ -500,7 +509,72 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
     // ============================================================ producers
     int stage = 0;
     uint32_t phase = 0;
-    if constexpr (!GATHER) {
+    if constexpr (g4_kind<KIND>()) {
+      // TMA gather4: lane p < 16 gathers K-rows 4p .. 4p+3 of each k-block (both 64-column chunks);
+      // their gather indices run KPD k-blocks ahead in registers, as in the cp.async producer
+      constexpr int KPD = SONIC_KPD;
+      int ktok[KPD][4];
+      const int p = lane;
+      for (int tile = t_first; tile < total_tiles; tile += t_step) {
+        const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);
+        const int n0 = tc.nt * BN + rank * BNL;
+        const int gcol = Tr::a_gather ? ((tc.valid) ? tc.mt * GEMM_BM : 0) : n0;
+#pragma unroll
+        for (int u = 0; u < KPD; ++u)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            ktok[u][j] = (p < 16 && u < tc.nkb) ? tok_of(args.row_token, tc.seg0 + u * GEMM_BK + 4 * p + j) : 0;
+        for (int kb0 = 0; kb0 < tc.nkb; kb0 += KPD) {
+#pragma unroll
+          for (int u = 0; u < KPD; ++u) {
+            const int kb = kb0 + u;
+            if (kb >= tc.nkb) break;
+            const int g0 = (int)clamp_tok(ktok[u][0]), g1 = (int)clamp_tok(ktok[u][1]);
+            const int g2 = (int)clamp_tok(ktok[u][2]), g3 = (int)clamp_tok(ktok[u][3]);
+            if (p < 16 && kb + KPD < tc.nkb) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) ktok[u][j] = tok_of(args.row_token, tc.seg0 + (kb + KPD) * GEMM_BK + 4 * p + j);
+            }
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sA = smem + stage * STAGE_BYTES;
+            uint8_t* sB = sA + A_BYTES;
+            uint64_t* bar = &full[stage];
+            const int krow0 = tc.seg0 + kb * GEMM_BK;
+            if (lane == 0) {
+              if (leader) ptx::mbar_arrive_expect_tx(bar, STAGE_BYTES * (CTA2 ? 2 : 1));
+              if constexpr (KIND == K_DW2) {  // A' tile (MN-major): 64 rows x 128 M columns
+                const int m0 = tc.valid ? tc.mt * GEMM_BM : 0;
+                if constexpr (CTA2 && (SONIC_STREAM_EF & 2)) {
+                  ptx::tma_load_2d_cg2_hint(sA, &mA, bar, m0, krow0, ptx::policy_evict_first());
+                  ptx::tma_load_2d_cg2_hint(sA + 8192, &mA, bar, m0 + 64, krow0, ptx::policy_evict_first());
+                } else {
+                  tload2<CTA2>(sA, &mA, bar, m0, krow0);
+                  tload2<CTA2>(sA + 8192, &mA, bar, m0 + 64, krow0);
+                }
+              } else {  // DW1: dH tile (MN-major): 64 rows x BNL columns
+#pragma unroll
+                for (int j = 0; j < BNL / 64; ++j) tload2<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, krow0);
+              }
+            }
+            __syncwarp();
+            if (p < 16) {
+              constexpr int NCH = Tr::a_gather ? 2 : BNL / 64;
+              uint8_t* gdst = (Tr::a_gather ? sA : sB) + p * 512;
+              const CUtensorMap* gm = Tr::a_gather ? &mA : &mB;
+#pragma unroll
+              for (int jj = 0; jj < NCH; ++jj) {
+                if constexpr (CTA2) ptx::tma_gather4_cg2(gdst + jj * 8192, gm, bar, gcol + 64 * jj, g0, g1, g2, g3);
+                else ptx::tma_gather4(gdst + jj * 8192, gm, bar, gcol + 64 * jj, g0, g1, g2, g3);
+              }
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    } else if constexpr (!GATHER) {
       if (lane == 0) {
         for (int tile = t_first; tile < total_tiles; tile += t_step) {
           const TileCoord tc = decode_tile<KIND, CTA2, MFAST>(args, tile, rank);

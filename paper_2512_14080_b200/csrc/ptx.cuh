@@ -73,6 +73,9 @@ __device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
 }
+// Pair form of tma_gather4: completion counted on the LEADER CTA's mbarrier (as tma_load_2d_cg2).
+__device__ __forceinline__ void tma_gather4_cg2(void* dst, const CUtensorMap* map, uint64_t* bar, int col, int r0,
+                                                int r1, int r2, int r3);
 // 16-byte Ampere-style async copy global -> shared (LDGSTS), L1 bypass.
 // L2 prefetch size of the gather copies (SONIC_CPA_L2: 128 or 256 bytes)
 #ifndef SONIC_CPA_L2
@@ -311,6 +314,14 @@ __device__ __forceinline__ void tma_load_3d_cg2(void* dst, const CUtensorMap* ma
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(leader_bar(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_gather4_cg2(void* dst, const CUtensorMap* map, uint64_t* bar, int col, int r0,
+                                                int r1, int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(leader_bar(bar)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
       : "memory");
 }
 // Pair-form TMA load with an L2 eviction-priority hint (streamed operands marked evict-first so they

@@ -262,7 +262,7 @@ bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUten
     return cta2 && BN == 256 && launch_gemm_t<K_UP8, 256, true>(a, b, c0, c1, d, args, grid, st);
   } else {
     if constexpr (KIND == K_DOWN || KIND == K_DXT || KIND == K_DW2 || KIND == K_DW1) {
-      if (SONIC_MC4 && mc && cta2 && BN == 256)
+      if (SONIC_MC4 && !g4_kind<KIND>() && mc && cta2 && BN == 256)
         return launch_gemm_t<KIND, 256, true, true>(a, b, c0, c1, d, args, grid, st);
     }
     switch (BN) {
