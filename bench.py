@@ -537,6 +537,7 @@ def main():
                              gbs_paper=mm["paper"] / (avg * 1e-3) / 1e9, gbs_tight=mm["tight"] / (avg * 1e-3) / 1e9,
                              bound="tensor" if t_tensor >= t_hbm else "hbm",
                              roofline_ms=max(t_tensor, t_hbm), frac=max(t_tensor, t_hbm) / avg if avg else None,
+                             roofline_ms_tight=max(t_tensor, mm["tight"] / (bw_peak * 1e9) * 1e3),
                              tensor_peak=kpeak)
     dom = max(kernels, key=lambda k: kernels[k]["avg_ms"] * kernels[k]["launches_per_step"]) if kernels else None
     traffic = None
@@ -556,6 +557,8 @@ def main():
                     "frac": k["gbs_paper"] / bw_peak, "traffic": traffic,
                     "algorithmic_per_launch": model[dom]["paper"], "peak_source": peaks["source"] + " hbm_gbs"}
     layer_roof_ms = sum(kernels[k]["roofline_ms"] * kernels[k]["launches_per_step"] for k in kernels)
+    # SURVEY 8(d)'s second IO accounting: each gathered tensor read once (the L2-ideal gather)
+    layer_roof_tight_ms = sum(kernels[k]["roofline_ms_tight"] * kernels[k]["launches_per_step"] for k in kernels)
     exchange = None
     if use_ep:
         # NVLink bytes this rank moves per step (rows to / from the OTHER ranks): forward X rows +
@@ -676,6 +679,9 @@ def main():
         "tokens_per_s": T * world / (ms_step * 1e-3),
         "model_flops_per_step": flops_all, "rows_routed": R, "rows_padded": R_pad,
         "layer_roofline_ms": layer_roof_ms, "layer_roofline_frac": layer_roof_ms / ms_step,
+        "layer_roofline_tight_ms": layer_roof_tight_ms, "layer_roofline_tight_frac": layer_roof_tight_ms / ms_step,
+        # against the nominal dense bf16 figure (2.25 PFLOP/s, B200_PROFILING.md) beside the measured peaks
+        "pct_peak_spec": value / world / 2250.0,
         # the same metric without sonic_route (the paper's bounds exclude the router)
         "value_excl_route": (flops_all / ((ms_step - kernels["route"]["avg_ms"] * kernels["route"]["launches_per_step"])
                                           * 1e-3) / 1e12) if "route" in kernels else None,

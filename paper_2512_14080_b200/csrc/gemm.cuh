@@ -224,6 +224,9 @@ __device__ __forceinline__ int total_tiles_of(const GemmArgs& a) {
   else return (CTA2 ? *a.num_pairs : *a.num_m_tiles) * a.n_tiles;
 }
 
+#ifndef SONIC_DW1_PHASE
+#define SONIC_DW1_PHASE 0  // dW1 tile order in d-slice phases of this many M pairs (0: MFAST order)
+#endif
 // MFAST (varlen-K under MC, the dW1 order): the M-pair index runs fastest, so tiles 2k and 2k+1
 // -- the two pairs of a 4-CTA cluster -- share the expert and the N tile (and so the B operand)
 template <int KIND, bool CTA2, bool MFAST = false>
@@ -236,7 +239,19 @@ __device__ __forceinline__ TileCoord decode_tile(const GemmArgs& a, int tile, in
     c.e = tile / per_e;
     const int rem = tile - c.e * per_e;
     int mp;
-    if constexpr (MFAST) {
+    constexpr int PH = KIND == K_DW1 ? SONIC_DW1_PHASE : 0;
+    if (PH > 0 && mts % (PH > 0 ? PH : 1) == 0) {
+      // d-slice phases: the M pairs in groups of PH, phase-major, then expert, N tile, M pair -- X's
+      // columns of one phase (PH * 256 of d) stay in L2 while every expert gathers from them
+      const int g = PH > 0 ? PH : 1;
+      const int per_ph = a.E * a.n_tiles * g;
+      const int ph = tile / per_ph;
+      const int r1 = tile - ph * per_ph;
+      c.e = r1 / (a.n_tiles * g);
+      const int r2 = r1 - c.e * a.n_tiles * g;
+      c.nt = r2 / g;
+      mp = ph * g + (r2 - c.nt * g);
+    } else if constexpr (MFAST) {
       c.nt = rem / mts;
       mp = rem - c.nt * mts;
     } else {
