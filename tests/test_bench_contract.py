@@ -22,6 +22,22 @@ def _run(args, timeout=600):
     return json.loads(lines[0])
 
 
+def test_kernel_model_accountings():
+    """The tight IO accounting (each gathered tensor read once) never exceeds the paper's (gathered rows
+    counted R*d*2), and the two agree for the kernels without a gathered operand."""
+    sys.path.insert(0, ROOT)
+    import bench
+    T, d, n, E, K = 32768, 1536, 256, 128, 8
+    R = T * K
+    m = bench.kernel_model(T, d, n, E, K, R, R)
+    for k, v in m.items():
+        assert v["tight"] <= v["paper"], k
+    for k in ("down", "dXt", "agg_O", "agg_dX", "route"):
+        assert m[k]["tight"] == m[k]["paper"], k
+    # FLOPs per routed row: 18 d n over the six GEMMs (P:765)
+    assert sum(m[k]["flops"] for k in ("up", "down", "dH", "dW2", "dXt", "dW1")) == 18 * d * n * R
+
+
 def test_reference_arm_line():
     d = _run(["--impl", "reference", "--config", "tiny", "--steps", "1", "--warmup", "3"])
     assert BASE_KEYS <= set(d), BASE_KEYS - set(d)
@@ -45,6 +61,10 @@ def test_default_arm_line_tiny():
     # the headline is flushed and uninstrumented; warm and the instrumented breakdown pass sit beside it
     assert d["config"]["l2"].startswith("flushed") and d["warm"]["ms_per_step"] > 0
     assert d["breakdown_pass"]["ms_per_step"] > 0
+    # both IO accountings (the tight one never above the paper one) and the spec-peak share
+    assert 0 < d["layer_roofline_tight_ms"] <= d["layer_roofline_ms"] * (1 + 1e-9)
+    assert d["pct_peak_spec"] == pytest.approx(d["value"] / 2250.0)
+    assert "power_w" in d["clocks"] and "power_limit_w" in d["clocks"]
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else None
     if peaks and r["bound"] == "tensor":
