@@ -228,7 +228,8 @@ def workload_config(args, cfg):
             **({"ep_exchange": ("peer-memory kernels (CUDA IPC)" + (", host-sync-free (device offsets, capacity "
                                                                     "2*T*K pairs)" if getattr(args, "sync_free", False)
                                                                     else "")) if args.comm == "peer"
-                else "NCCL all-to-all-v"}
+                else "NCCL all-to-all-v" + (", chunked dispatch (self block first)" if getattr(args, "chunked", False)
+                                            else "")}
                if (args.gpus > 1 or getattr(args, "ep", False)) else {}),
             **({"dW": "bf16 (SONIC_F_DW_BF16)"} if getattr(args, "dw_bf16", False) else {}),
             **({"updown": "fused kernel (SONIC_F_FUSED_UPDOWN)"} if getattr(args, "fuse", False) else {}),
@@ -276,6 +277,9 @@ def main():
                     help="also run the step back to back for this many seconds (sustained / power-capped regime)")
     ap.add_argument("--sync-free", action="store_true",
                     help="with --comm peer: the host-sync-free exchange (offsets read on the device, NEXT-2)")
+    ap.add_argument("--chunked", action="store_true",
+                    help="EP (NCCL exchange): chunked dispatch -- the self block's GEMMs run while the remote "
+                         "blocks are exchanged (NEXT-2)")
     ap.add_argument("--graph", action="store_true",
                     help="capture one step in a CUDA graph and replay it in the timed passes (needs a step "
                          "without host synchronisation: the single-GPU path, or --comm peer --sync-free)")
@@ -388,7 +392,7 @@ def main():
         rk = ep.EPRank(T, d, n, E, K, G, rank, W1, W2, mode=mode)
 
         def run(Xa, Sa, dOa, slot=0):
-            (Oa,) = ep.ep_forward([rk], comm, [Xa], [Sa])
+            (Oa,) = ep.ep_forward([rk], comm, [Xa], [Sa], chunked=args.chunked)
             ((dXa, _),) = ep.ep_backward([rk], comm, [dOa])
             return Oa, dXa
 
@@ -401,6 +405,14 @@ def main():
             R_in = rk.ctx["R_in"]
             if R_in == 0:
                 return kernel_model(1, d, n, L, L, 0, 0)
+            if rk.ctx.get("chunked"):
+                # chunked dispatch: one launch of each kernel per chunk -- the per-launch model is the
+                # chunks' total work over the chunk count (an average, like the measured per-launch time)
+                ch = rk.ctx["chunks"]
+                Rr = sum(int(c["lrt"].offsets[L].item()) for c in ch)
+                Rp = sum(int(c["lrt"].pad_offsets[L].item()) for c in ch)
+                m = kernel_model(R_in, d, n, L, L, Rr, Rp)
+                return {k: {q: v / len(ch) for q, v in mm.items()} for k, mm in m.items()}
             lrt = rk.ctx["lrt"]
             return kernel_model(R_in, d, n, L, L, int(lrt.offsets[L].item()), int(lrt.pad_offsets[L].item()))
 

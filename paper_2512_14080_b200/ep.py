@@ -408,6 +408,64 @@ class EPRank:
         sonic.sonic_ep_combine(self.desc(), self.G, self.ctx["plan"], buf, out)
         return out
 
+    # -------------------------------------------------------------- chunked dispatch (NEXT-2)
+    # The received rows come in blocks by source rank; the block this rank sends itself is in its own
+    # send buffer before the exchange starts.  Chunked mode computes that block first, while the
+    # exchange of the remote blocks is in flight, then the remote rows before and after it: each
+    # chunk is a contiguous row range with its own GIVEN routing, H cache and workspace, writing its
+    # outputs straight into its rows of the return buffers.  The per-row arithmetic is the unchunked
+    # one (O, dX~, dS rows bit-identical); dW1 / dW2 sum the chunks (fp32, SONIC_F_DW_ACCUMULATE).
+    def chunk_begin(self, R_in):
+        self.ctx.update(R_in=R_in, chunks=[])
+
+    def compute_fwd_chunk(self, x, gate, out, pairs):
+        """Forward of one chunk (rows x [Rc, d], gates [Rc, L]) into out [Rc, d]."""
+        Rc = x.shape[0]
+        if Rc == 0:
+            return
+        ld = sonic.make_desc(Rc, self.d, self.n, self.L, self.L, mode=sonic.SONIC_ROUTE_GIVEN,
+                             rows_cap=max(0, int(pairs)))
+        lrt = sonic.sonic_route(ld, gate.contiguous())
+        _, H, _ = sonic.sonic_moe_fwd(ld, x, self.W1, self.W2, lrt, O=out)
+        self.ctx["chunks"].append(dict(ldesc=ld, lrt=lrt, H=H, x=x, rows=Rc))
+
+    def compute_bwd_chunk(self, k, do, dx_out, ds_out, split):
+        """Backward of chunk k on its dO rows: dX~ partial sums into dx_out, dense dS into ds_out; the
+        weight gradients now (split=False) or in compute_bwd_dw_chunk (split=True).  The first chunk
+        with dW overwrites self.dW1 / dW2, later ones accumulate into them."""
+        c = self.ctx["chunks"][k]
+        ld = c["ldesc"]
+        first = not self.ctx.get("dw_started")
+        fl = (sonic.SONIC_F_BWD_NO_DW if split else (0 if first else sonic.SONIC_F_DW_ACCUMULATE))
+        ldf = sonic.make_desc(ld.T, ld.d, ld.n, ld.E, ld.K, mode=ld.route_mode, flags=ld.flags | fl,
+                              rows_cap=ld.rows_cap)
+        if split:
+            _, _, _, dS, ws = sonic.sonic_moe_bwd(ldf, do, c["x"], c["H"], self.W1, self.W2, c["lrt"], dX=dx_out)
+            c.update(bws=ws, do=do)
+        else:
+            if first:
+                self.dW1 = torch.empty(self.L, self.d, 2 * self.n, device=do.device)
+                self.dW2 = torch.empty(self.L, self.n, self.d, device=do.device)
+                self.ctx["dw_started"] = True
+            _, _, _, dS, _ = sonic.sonic_moe_bwd(ldf, do, c["x"], c["H"], self.W1, self.W2, c["lrt"], dX=dx_out,
+                                                 dW1=self.dW1, dW2=self.dW2)
+        sonic.sonic_ep_ds_dense(ld, c["lrt"], dS, ds_out)
+
+    def compute_bwd_dw_chunk(self, k):
+        """Weight gradients of a split chunk from its part-1 dH / A' (same workspace)."""
+        c = self.ctx["chunks"][k]
+        ld = c["ldesc"]
+        first = not self.ctx.get("dw_started")
+        fl = sonic.SONIC_F_BWD_DW_ONLY | (0 if first else sonic.SONIC_F_DW_ACCUMULATE)
+        ldf = sonic.make_desc(ld.T, ld.d, ld.n, ld.E, ld.K, mode=ld.route_mode, flags=ld.flags | fl,
+                              rows_cap=ld.rows_cap)
+        if first:
+            self.dW1 = torch.empty(self.L, self.d, 2 * self.n, device=self.W1.device)
+            self.dW2 = torch.empty(self.L, self.n, self.d, device=self.W1.device)
+            self.ctx["dw_started"] = True
+        sonic.sonic_moe_bwd(ldf, c["do"], c["x"], c["H"], self.W1, self.W2, c["lrt"], dW1=self.dW1, dW2=self.dW2,
+                            ws=c["bws"])
+
     # -------------------------------------------------------------- backward
     def _ldesc(self, extra_flags):
         ld = self.ctx["ldesc"]
@@ -473,8 +531,53 @@ def _dispatch(ranks, comm, srcs, send_counts, recv_counts, tag):
     return comm.alltoallv(sends, send_counts, recv_counts, tag=tag)
 
 
-def ep_forward(ranks, comm, Xs, Ss):
-    """Forward of the EP layer over the local ranks -> [O_r]."""
+def _chunk_rows(r, sc, rc):
+    """(send offset, rows, recv offset) of rank r's self block."""
+    return sum(sc[: r.rank]), sc[r.rank], sum(rc[: r.rank])
+
+
+def _ep_forward_chunked(ranks, comm, Xs, disp, send_counts, recv_counts, recv_pairs):
+    """NEXT-2 chunked dispatch (staged exchange): the self block's up/down-projection runs while the
+    exchange of the remote blocks is in flight, then the remote rows before / after it."""
+    n = len(ranks)
+    sends = []
+    for i, (r, X) in enumerate(zip(ranks, Xs)):
+        with comm.rank_stream(i):
+            sends.append(r.pack(X))
+    gates = [g for g, _ in disp]
+    p_x = comm.alltoallv_start(sends, send_counts, recv_counts, tag="x")
+    p_g = comm.alltoallv_start(gates, send_counts, recv_counts, tag="gate")
+    parts, geo = [], []
+    for i, r in enumerate(ranks):
+        so, ns, ro = _chunk_rows(r, send_counts[i], recv_counts[i])
+        R_in = sum(recv_counts[i])
+        geo.append((so, ns, ro, R_in))
+        with comm.rank_stream(i):
+            part = torch.empty(R_in, r.d, dtype=torch.bfloat16, device=sends[i].device)
+            r.chunk_begin(R_in)
+            r.compute_fwd_chunk(sends[i][so:so + ns], gates[i][so:so + ns], part[ro:ro + ns],
+                                recv_pairs[i][r.rank])
+            parts.append(part)
+    recv_x = comm.alltoallv_finish(p_x)
+    recv_g = comm.alltoallv_finish(p_g)
+    for i, r in enumerate(ranks):
+        so, ns, ro, R_in = geo[i]
+        pr = recv_pairs[i]
+        with comm.rank_stream(i):
+            r.compute_fwd_chunk(recv_x[i][:ro], recv_g[i][:ro], parts[i][:ro], sum(pr[: r.rank]))
+            r.compute_fwd_chunk(recv_x[i][ro + ns:], recv_g[i][ro + ns:], parts[i][ro + ns:], sum(pr[r.rank + 1:]))
+    back = comm.alltoallv(parts, recv_counts, send_counts, tag="y")
+    outs = []
+    for i, (r, rc, b) in enumerate(zip(ranks, recv_counts, back)):
+        r.ctx["recv_counts"] = rc
+        with comm.rank_stream(i):
+            outs.append(r.combine_fwd(b))
+    return outs
+
+
+def ep_forward(ranks, comm, Xs, Ss, chunked=False):
+    """Forward of the EP layer over the local ranks -> [O_r].  chunked (staged exchange, NCCL or
+    SimComm): the self block is computed while the remote blocks are exchanged (NEXT-2)."""
     disp = []
     for i, (r, S) in enumerate(zip(ranks, Ss)):
         with comm.rank_stream(i):
@@ -494,6 +597,12 @@ def ep_forward(ranks, comm, Xs, Ss):
         pairs_in = [sum(rb[G:2 * G]) for rb in recv_both]
     for r, sc in zip(ranks, send_counts):
         r.ctx["counts"] = sc
+        r.ctx["chunked"] = False
+    if chunked and not sync_free and not hasattr(comm, "dispatch_packed"):
+        for r in ranks:
+            r.ctx["chunked"] = True
+        return _ep_forward_chunked(ranks, comm, Xs, disp, send_counts, recv_counts,
+                                   [rb[G:2 * G] for rb in recv_both])
     recv_x = _dispatch(ranks, comm, Xs, send_counts, recv_counts, "x")
     recv_g = comm.alltoallv([g for g, _ in disp], send_counts, recv_counts, tag="gate")
     parts = []
@@ -511,10 +620,63 @@ def ep_forward(ranks, comm, Xs, Ss):
     return outs
 
 
+def _ep_backward_chunked(ranks, comm, dOs, send_counts, recv_counts):
+    """Backward of a chunked forward: the self block's dH / dX~ / dS / dW while the remote dO rows
+    are exchanged, then the remote chunks' dX~ / dS, whose return exchange overlaps their dW."""
+    sends = []
+    for i, (r, dO) in enumerate(zip(ranks, dOs)):
+        with comm.rank_stream(i):
+            sends.append(r.pack(dO))
+    p_do = comm.alltoallv_start(sends, send_counts, recv_counts, tag="do")
+    dxs, dss, geo = [], [], []
+    for i, r in enumerate(ranks):
+        so, ns, ro = _chunk_rows(r, send_counts[i], recv_counts[i])
+        R_in = sum(recv_counts[i])
+        geo.append((so, ns, ro))
+        r.ctx["dw_started"] = False
+        with comm.rank_stream(i):
+            dx = torch.empty(R_in, r.d, dtype=torch.bfloat16, device=sends[i].device)
+            ds = torch.empty(R_in, r.L, dtype=torch.float32, device=sends[i].device)
+            k = 0
+            if ns:
+                r.compute_bwd_chunk(0, sends[i][so:so + ns], dx[ro:ro + ns], ds[ro:ro + ns], split=False)
+                k = 1
+            r.ctx["k_remote"] = k
+            dxs.append(dx)
+            dss.append(ds)
+    recv = comm.alltoallv_finish(p_do)
+    for i, r in enumerate(ranks):
+        so, ns, ro = geo[i]
+        with comm.rank_stream(i):
+            k = r.ctx["k_remote"]
+            for lo, hi in ((0, ro), (ro + ns, recv[i].shape[0])):
+                if hi > lo:
+                    r.compute_bwd_chunk(k, recv[i][lo:hi], dxs[i][lo:hi], dss[i][lo:hi], split=True)
+                    k += 1
+    p_dx = comm.alltoallv_start(dxs, recv_counts, send_counts, tag="dx")
+    p_ds = comm.alltoallv_start(dss, recv_counts, send_counts, tag="ds")
+    for i, r in enumerate(ranks):
+        with comm.rank_stream(i):
+            for k in range(r.ctx["k_remote"], len(r.ctx["chunks"])):
+                r.compute_bwd_dw_chunk(k)
+            if not r.ctx["dw_started"]:  # no rows at all: the local experts' gradients are zero
+                r.dW1 = torch.zeros(r.L, r.d, 2 * r.n, device=r.W1.device)
+                r.dW2 = torch.zeros(r.L, r.n, r.d, device=r.W1.device)
+    back_dx = comm.alltoallv_finish(p_dx)
+    back_ds = comm.alltoallv_finish(p_ds)
+    res = []
+    for i, (r, bx, bs) in enumerate(zip(ranks, back_dx, back_ds)):
+        with comm.rank_stream(i):
+            res.append(r.combine_bwd(bx, bs))
+    return res
+
+
 def ep_backward(ranks, comm, dOs):
     """Backward over the local ranks -> [(dX_r, dS_r)]; each rank keeps its local dW1 / dW2."""
     send_counts = [r.ctx["counts"] for r in ranks]
     recv_counts = [r.ctx["recv_counts"] for r in ranks]
+    if ranks[0].ctx.get("chunked"):
+        return _ep_backward_chunked(ranks, comm, dOs, send_counts, recv_counts)
     recv = _dispatch(ranks, comm, dOs, send_counts, recv_counts, "do")
     outs = []
     for i, (r, x) in enumerate(zip(ranks, recv)):

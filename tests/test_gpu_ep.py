@@ -16,7 +16,7 @@ from tests.parity import assert_close, f64
 pytestmark = pytest.mark.gpu
 
 
-def _run_ep(G, mode, E, comm_kind, T=768, d=128, n=64, K=4, steps=1, cap_pairs=None):
+def _run_ep(G, mode, E, comm_kind, T=768, d=128, n=64, K=4, steps=1, cap_pairs=None, chunked=False):
     m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
     base = make_inputs(T, d, n, E, K, seed=40, device="cuda")
     W1, W2 = base.W1, base.W2
@@ -27,7 +27,7 @@ def _run_ep(G, mode, E, comm_kind, T=768, d=128, n=64, K=4, steps=1, cap_pairs=N
     comm = (ep.SimComm(G) if comm_kind == "sim" else
             ep.PeerComm(G, T, d, L, range(G), sync_free=comm_kind == "peer_sf", cap_pairs=cap_pairs))
     for _ in range(steps):  # later steps reuse the regions (stale rows of the earlier step)
-        Os = ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins])
+        Os = ep.ep_forward(ranks, comm, [i.X for i in ins], [i.S for i in ins], chunked=chunked)
         outs = ep.ep_backward(ranks, comm, [i.dO for i in ins])
     torch.cuda.synchronize()
     res = [(Os[r].clone(), outs[r][0].clone(), outs[r][1].clone(), ranks[r].dW1.clone(), ranks[r].dW2.clone())
@@ -172,3 +172,19 @@ def test_ep_sync_free_overflow_is_flagged():
     routing (nothing written out of bounds, its expert outputs are zero) and overflowed() says so."""
     res = _run_ep(2, "tc", 16, "peer_sf", cap_pairs=64)
     assert all(res[2])
+
+
+@pytest.mark.parametrize("G,mode,E", [(1, "tc", 16), (2, "tc", 16), (4, "tr", 16), (4, "tc", 64)])
+def test_ep_chunked_equals_unchunked(G, mode, E):
+    """NEXT-2 chunked dispatch (the self block computed before the remote blocks arrive, each chunk
+    its own GIVEN routing and GEMMs): every row's arithmetic is the unchunked one, so O, dX and dS are
+    bit-identical; dW1 / dW2 sum the chunks' fp32 partials (SONIC_F_DW_ACCUMULATE), equal to the
+    one-pass sums up to fp32 reassociation."""
+    a = _run_ep(G, mode, E, "sim")
+    b = _run_ep(G, mode, E, "sim", chunked=True, steps=2)
+    for r in range(G):
+        for name, x, y in zip(("O", "dX", "dS"), a[r][:3], b[r][:3]):
+            assert torch.equal(x, y), f"rank {r} {name} differs between chunked and unchunked dispatch"
+        for name, x, y in zip(("dW1", "dW2"), a[r][3:], b[r][3:]):
+            err = (x - y).abs().max().item()
+            assert err <= 1e-5 * max(1.0, x.abs().max().item()), f"rank {r} {name}: max |diff| {err}"

@@ -40,9 +40,9 @@ def _worker(rank, world, port, mode, q, comm_kind="dist"):
         rk = ep.EPRank(T, d, n, E, K, world, rank, W1, W2, mode=m)
         # dist: host-staged all-to-all over gloo; peer: CUDA IPC regions (handles exchanged over gloo),
         # the dispatch/return kernels store into the other process's region, flag barriers order them
-        comm = (ep.DistComm() if comm_kind == "dist" else
+        comm = (ep.DistComm() if comm_kind.startswith("dist") else
                 ep.PeerComm(world, T, d, L, [rank], sync_free=comm_kind == "peer_sf"))
-        (O,) = ep.ep_forward([rk], comm, [X], [S])
+        (O,) = ep.ep_forward([rk], comm, [X], [S], chunked=comm_kind == "dist_chunked")
         ((dX, dS),) = ep.ep_backward([rk], comm, [dO])
         torch.cuda.synchronize()
         if comm_kind.startswith("peer"):
@@ -57,7 +57,8 @@ def _worker(rank, world, port, mode, q, comm_kind="dist"):
 
 
 @pytest.mark.parametrize("mode,comm_kind", [("tc", "dist"), ("tr", "dist"), ("tc", "peer"), ("tr", "peer"),
-                                            ("tc", "peer_sf"), ("tr", "peer_sf")])
+                                            ("tc", "peer_sf"), ("tr", "peer_sf"),
+                                            ("tc", "dist_chunked"), ("tr", "dist_chunked")])
 def test_ep_two_processes(mode, comm_kind):
     from oracle import moe_oracle as om
     from paper_2512_14080_b200.inputs import make_expert_weights, make_token_inputs
