@@ -425,6 +425,33 @@ def quantize_e4m3(M, axis):
     return q, np.squeeze(scale, axis=axis).astype(np.float64)
 
 
+def bf16_round(x):
+    """Round to the nearest bfloat16 value (ties to even) from float64 in one step: 8 significant
+    bits, so the grid around |x| in [2^e, 2^(e+1)) is 2^(e-7) (normals from 2^-126)."""
+    x = np.asarray(x, dtype=np.float64)
+    a = np.abs(x)
+    _, ex = np.frexp(np.where(a > 0, a, 1.0))
+    e = np.maximum(ex - 1, -126)
+    q = np.ldexp(1.0, e - 7)
+    return np.copysign(np.rint(a / q) * q, x)
+
+
+def fp8_dxt_rows(dH_e, sw_e):
+    """The e4m3 operand of the FP8 dX~ GEMM (NEXT-4, Q23): the stored (bf16) dH rows times the forward's
+    per-column W1 scales sw_e[j] in fp32 -- folding the weight scale, which varies along this GEMM's
+    reduction dimension j, into dH -- then quantised per row.  Returns (q [f_e, 2n], s [f_e])."""
+    dHb = bf16_round(dH_e).astype(np.float32)
+    M = (dHb * np.asarray(sw_e, dtype=np.float32)[None, :]).astype(np.float32)
+    return quantize_e4m3(M, axis=1)
+
+
+def expert_dxt_fp8(dH_e, W1q_e, sw_e):
+    """dX~_e on e4m3 operands: s_r * sum_j q_rj W1q_e[i, j] with (q, s) = fp8_dxt_rows(dH_e, sw_e):
+    = sum_j (s_r q_rj / sw_j) (sw_j W1q_e[i, j]), the definition on the dequantised operands."""
+    q, s = fp8_dxt_rows(dH_e, sw_e)
+    return _f64(s)[:, None] * (_f64(q) @ _f64(W1q_e).T)
+
+
 def fp8_up_operands(X, W1):
     """X [T,d] -> (Xq, sx [T]) per token row; W1 [E,d,2n] -> (W1q, sw [E,2n]) per output column."""
     Xq, sx = quantize_e4m3(X, axis=1)
@@ -523,10 +550,12 @@ def expert_backward(dOe, Xe, W1e, W2e, ge, He=None):
                        dXt=dHe @ W1e.T)                        # dX~_e = dH_e W1_e^T
 
 
-def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None):
+def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None, fp8_dxt=False):
     """Alg. 3 then Alg. 5 for every expert (``expert_backward``), then
     dX_t = sum_e pi_te dX~_e,t (Alg. 5's aggregation).
     ``experts`` restricts the work (dX then holds only those experts' terms).
+    fp8_dxt: dX~_e on e4m3 operands (``expert_dxt_fp8``; W1 quantised per column as in the forward's
+    fp8 up-projection); every other output is the bf16 path's.
     """
     dO, X, W1, W2 = _f64(dO), _f64(X), _f64(W1), _f64(W2)
     T, d = X.shape
@@ -536,10 +565,14 @@ def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None):
     dW1 = np.zeros((E, d, n2))
     dW2 = np.zeros((E, n, d))
     dS, dH, Ap, dXt = {}, {}, {}, {}
+    if fp8_dxt:
+        W1q, sw = quantize_e4m3(W1, axis=1)
     for e in (range(E) if experts is None else experts):
         toks = np.nonzero(rt.kept[:, e])[0]
         g = expert_backward(dO[toks], X[toks], W1[e], W2[e], rt.gate[toks, e],
                             None if H_cache is None else _f64(H_cache[e]))
+        if fp8_dxt:
+            g.dXt = expert_dxt_fp8(g.dH, W1q[e], sw[e])
         dW1[e], dW2[e] = g.dW1, g.dW2
         np.add.at(dX, toks, g.dXt)                             # dX_t = sum_e dX~_e,t
         dS[e], dH[e], Ap[e], dXt[e] = g.dS, g.dH, g.A_prime, g.dXt

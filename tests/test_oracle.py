@@ -668,3 +668,47 @@ def test_forward_fp8_up_is_the_quantised_definition():
     np.testing.assert_allclose(f8.O, ref.O, rtol=1e-12, atol=1e-12)
     full = om.forward(X, W1, W2, rt)
     assert np.linalg.norm(f8.O - full.O) / np.linalg.norm(full.O) < 0.1
+
+
+def test_bf16_round_against_torch():
+    """om.bf16_round against torch's bfloat16 cast (an independent library rounding, ties to even) on
+    fp32 values (where torch's single fp32 -> bf16 rounding is the exact one), incl. exact ties."""
+    rng = np.random.default_rng(11)
+    v = (rng.normal(size=4000) * np.exp2(rng.integers(-30, 30, size=4000))).astype(np.float32)
+    import torch
+    ties = (np.float32(1.0) + np.float32(2.0 ** -8) * np.arange(1, 64, 2, dtype=np.float32)).astype(np.float32)
+    v = np.concatenate([v, ties, -ties, np.float32([0.0, 1.0, -2.5])])
+    ref = torch.tensor(v).to(torch.bfloat16).float().numpy().astype(np.float64)
+    np.testing.assert_array_equal(om.bf16_round(v.astype(np.float64)), ref)
+
+
+def test_backward_fp8_dxt_is_the_quantised_definition():
+    """backward(fp8_dxt=True): dX~ is the definition on the dequantised operands -- dH~ = s q / sw
+    (the row-quantised dH' = bf16(dH) sw, the forward's W1 column scales divided back out) and
+    W1~ = W1q sw -- so the scales factor out exactly; dX stays within the quantisation error of the
+    bf16 backward; dW1 / dW2 / dS are untouched."""
+    rng = np.random.default_rng(5)
+    T, d, n, E, K = 40, 32, 16, 4, 2
+    X = rng.normal(size=(T, d))
+    W1 = rng.normal(size=(E, d, 2 * n)) / np.sqrt(d)
+    W2 = rng.normal(size=(E, n, d)) / np.sqrt(n)
+    dO = rng.normal(size=(T, d))
+    S = rng.random((T, E))
+    S /= S.sum(1, keepdims=True)
+    rt = om.route(S, K, mode="tc")
+    full = om.backward(dO, X, W1, W2, rt)
+    f8 = om.backward(dO, X, W1, W2, rt, fp8_dxt=True)
+    W1q, sw = om.quantize_e4m3(W1, axis=1)
+    dX_ref = np.zeros_like(full.dX)
+    for e in range(E):
+        toks = np.nonzero(rt.kept[:, e])[0]
+        q, s = om.fp8_dxt_rows(full.dH[e], sw[e])
+        dH_dq = s[:, None] * q / sw[e][None, :]
+        W1_dq = W1q[e] * sw[e][None, :]
+        np.add.at(dX_ref, toks, dH_dq @ W1_dq.T)
+    np.testing.assert_allclose(f8.dX, dX_ref, rtol=1e-10, atol=1e-12)
+    assert np.linalg.norm(f8.dX - full.dX) / np.linalg.norm(full.dX) < 0.1
+    for a, b in ((f8.dW1, full.dW1), (f8.dW2, full.dW2)):
+        np.testing.assert_array_equal(a, b)
+    for e in range(E):
+        np.testing.assert_array_equal(f8.dS[e], full.dS[e])
