@@ -47,7 +47,7 @@ def load_peaks():
 
 
 # --------------------------------------------------------------------------- FLOP / byte model
-def kernel_model(T, d, n, E, K, R, R_pad, dw=4, fp8_up=False, w1_cached=False):
+def kernel_model(T, d, n, E, K, R, R_pad, dw=4, fp8_up=False, w1_cached=False, fp8_dxt=False):
     """Algorithmic FLOPs and bytes per launch.
 
     R = routed rows (T*K under TC, sum f_r under TR).  'paper' bytes count gathered rows at
@@ -57,6 +57,7 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4, fp8_up=False, w1_cached=False):
     W1 = E * d * 2 * n * b
     W2 = E * n * d * b
     ab = 1 if fp8_up else b  # bytes per up-projection operand element (e4m3 with SONIC_F_FP8_UP)
+    xb = 1 if fp8_dxt else b  # bytes per dX~ operand element (e4m3 with SONIC_F_FP8_DXT)
     m = {
         "up": dict(flops=4 * R * d * n, paper=R * d * ab + W1 * ab // b + R * 2 * n * b + R * n * b,
                    tight=T * d * ab + W1 * ab // b + R * 2 * n * b + R * n * b),
@@ -69,7 +70,8 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4, fp8_up=False, w1_cached=False):
                    tight=T * d * b + W2 + 2 * R * 2 * n * b + R * n * b + R * 4),
         "dW2": dict(flops=2 * R * n * d, paper=R * n * b + R * d * b + E * n * d * dw,
                     tight=R * n * b + T * d * b + E * n * d * dw),
-        "dXt": dict(flops=4 * R * d * n, paper=R * 2 * n * b + W1 + R * d * b, tight=R * 2 * n * b + W1 + R * d * b),
+        "dXt": dict(flops=4 * R * d * n, paper=R * 2 * n * xb + W1 * xb // b + R * d * b,
+                    tight=R * 2 * n * xb + W1 * xb // b + R * d * b),
         "dW1": dict(flops=4 * R * d * n, paper=R * d * b + R * 2 * n * b + E * d * 2 * n * dw,
                     tight=T * d * b + R * 2 * n * b + E * d * 2 * n * dw),
         "agg_dX": dict(flops=0, paper=R * d * b + T * d * b, tight=R * d * b + T * d * b),
@@ -78,6 +80,9 @@ def kernel_model(T, d, n, E, K, R, R_pad, dw=4, fp8_up=False, w1_cached=False):
         "quant_fp8": dict(flops=0, paper=T * d * 3 + (0 if w1_cached else E * d * 2 * n * 3),
                           tight=T * d * 3 + (0 if w1_cached else E * d * 2 * n * 3)),
         "dS_reduce": dict(flops=0, paper=R * 8, tight=R * 8),
+        # SONIC_F_FP8_DXT: dH read, its e4m3 rows + scales written (+ W1's e4m3 copy unless cached)
+        "quant_dh": dict(flops=0, paper=R * 2 * n * 3 + R * 4 + (0 if w1_cached else E * d * 2 * n * 3),
+                         tight=R * 2 * n * 3 + R * 4 + (0 if w1_cached else E * d * 2 * n * 3)),
     }
     # bytes written (part of the totals above; reported, not a separate bound: write-only HBM traffic
     # reaches 6.2-7.0 TB/s on B200 with 16/32-byte or TMA stores, tools/hbm_write_probe.cu)
@@ -237,6 +242,8 @@ def workload_config(args, cfg):
                           ("; W1's e4m3 copy cached across steps (SONIC_F_FP8_W1_CACHED)"
                            if getattr(args, "fp8_w1_cached", False) else "")} if getattr(args, "fp8_up", False)
                else {}),
+            **({"dXt": "e4m3 operands (SONIC_F_FP8_DXT: dH x the forward's W1 column scales, per-row quantised)"}
+               if getattr(args, "fp8_dxt", False) else {}),
             **({"m_tile": args.m_tile} if getattr(args, "m_tile", 128) != 128 else {}),
             "l2": ("flushed before every timed step (memset of 2x L2 outside the step's event pair); warm "
                    "back-to-back number in `warm`") if getattr(args, "l2_flush", False) else
@@ -266,6 +273,8 @@ def main():
     ap.add_argument("--dw-bf16", action="store_true", help="SONIC_F_DW_BF16: weight gradients stored as bf16")
     ap.add_argument("--fp8-up", action="store_true",
                     help="SONIC_F_FP8_UP: the up-projection on e4m3 operands (NEXT-4; not the bf16 headline)")
+    ap.add_argument("--fp8-dxt", action="store_true",
+                    help="SONIC_F_FP8_DXT: dX~ on e4m3 operands (NEXT-4, DESIGN Q25; not the bf16 headline)")
     ap.add_argument("--fp8-w1-cached", action="store_true",
                     help="with --fp8-up: SONIC_F_FP8_W1_CACHED after the first step (W1's e4m3 copy reused, as in the "
                          "micro-batches of a gradient-accumulation step)")
@@ -337,7 +346,8 @@ def main():
     desc = sonic.make_desc(T, d, n, E, K, mode=mode, m_tile=args.m_tile,
                            flags=(sonic.SONIC_F_DW_BF16 if args.dw_bf16 else 0) |
                            (sonic.SONIC_F_FUSED_UPDOWN if args.fuse else 0) |
-                           (sonic.SONIC_F_FP8_UP if args.fp8_up else 0))
+                           (sonic.SONIC_F_FP8_UP if args.fp8_up else 0) |
+                           (sonic.SONIC_F_FP8_DXT if args.fp8_dxt else 0))
     use_ep = args.ep or world > 1
     if not use_ep:
         # ---- one GPU, all experts local: route + fwd + bwd through the C ABI
@@ -359,6 +369,7 @@ def main():
 
         # --fp8-w1-cached: the first forward quantises W1 into ws_f, later ones reuse it
         desc_f = [desc]
+        desc_b = [desc]
 
         def run(Xa, Sa, dOa, slot=0):
             O, dX = Obuf[slot], dXbuf[slot]
@@ -367,7 +378,8 @@ def main():
             if args.fp8_w1_cached and not (desc_f[0].flags & sonic.SONIC_F_FP8_W1_CACHED):
                 desc_f[0] = sonic.make_desc(T, d, n, E, K, mode=mode, m_tile=args.m_tile,
                                             flags=desc.flags | sonic.SONIC_F_FP8_W1_CACHED)
-            sonic.sonic_moe_bwd(desc, dOa, Xa, H, W1, W2, rt, dX, dW1, dW2, dS, ws_b)
+            sonic.sonic_moe_bwd(desc_b[0], dOa, Xa, H, W1, W2, rt, dX, dW1, dW2, dS, ws_b)
+            desc_b[0] = desc_f[0]  # the bwd workspace's e4m3 W1 copy is valid from the second step on
             return O, dX
 
         def routed_rows():
@@ -375,7 +387,7 @@ def main():
 
         def local_model(R, R_pad):
             return kernel_model(T, d, n, E, K, R, R_pad, dw=2 if args.dw_bf16 else 4, fp8_up=args.fp8_up,
-                                w1_cached=args.fp8_w1_cached)
+                                w1_cached=args.fp8_w1_cached, fp8_dxt=args.fp8_dxt)
     else:
         # ---- expert parallelism over the `world` GPUs (NCCL all-to-all), weak scaling: every rank
         #      brings its own T tokens and owns E/world experts (paper_2512_14080_b200/ep.py)
@@ -541,7 +553,7 @@ def main():
         mm = model.get(name, dict(flops=0, paper=0, tight=0, write=0))
         # the e4m3 up-projection is held to the fp8 peak: the measured bf16 peak x 2 (the guide's nominal
         # dense fp8 : bf16 ratio, 4.5 : 2.25 PFLOP/s)
-        kpeak = tf_peak * (2.0 if (args.fp8_up and name == "up") else 1.0)
+        kpeak = tf_peak * (2.0 if ((args.fp8_up and name == "up") or (args.fp8_dxt and name == "dXt")) else 1.0)
         t_tensor = mm["flops"] / (kpeak * 1e12) * 1e3
         t_hbm = mm["paper"] / (bw_peak * 1e9) * 1e3  # all algorithmic bytes at the measured copy rate
         kernels[name] = dict(avg_ms=avg, launches_per_step=cnt / args.steps, share=tot / ms_p if ms_p else None,
@@ -684,7 +696,9 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16+e4m3(up-proj)" if args.fp8_up else "bf16", "data": "synthetic",
+        "vs_baseline": None, "dtype": ("bf16+e4m3(" + ",".join(k for k, f in (("up-proj", args.fp8_up),
+                                                                               ("dX~", args.fp8_dxt)) if f) + ")")
+        if (args.fp8_up or args.fp8_dxt) else "bf16", "data": "synthetic",
         "config": workload_config(args, cfg),
         "pct_peak": value / world / peaks["bf16_tflops"],
         "pct_peak_sustained": value / world / peaks["bf16_tflops_sustained"],

@@ -107,6 +107,14 @@ typedef enum {
                                        and this workspace wrote them, e.g. the earlier micro-batches of a
                                        gradient-accumulation step): only X is quantised.  The caller
                                        guarantees it; stale weights are not detected. */
+#define SONIC_F_FP8_DXT       1024  /* sonic_moe_bwd: dX~ = dH W1_e^T on e4m3 operands (NEXT-4, reading Q25):
+                                       W1 quantised per output column exactly as SONIC_F_FP8_UP does (with
+                                       SONIC_F_FP8_W1_CACHED: the copy in THIS bwd workspace is reused), the
+                                       stored bf16 dH multiplied by those column scales in fp32 and quantised
+                                       per row, dX~ = (e4m3 x e4m3 -> fp32 sum) * row scale; dH, dS, dW1, dW2
+                                       stay bf16-path results.  Needs n % 64 == 0 and d % 256 == 0 (else
+                                       SONIC_ERR_UNSUPPORTED); the bwd workspace then also holds the e4m3
+                                       copies and scales.  Not with SONIC_F_BWD_DW_ONLY. */
 #define SONIC_F_DW_ACCUMULATE    4  /* sonic_moe_bwd: dW1 += ..., dW2 += ... (fp32 element-wise adds done by
                                        the TMA store unit; one add per element per call, so deterministic)
                                        instead of overwriting -- gradient accumulation over microbatches */
@@ -164,8 +172,10 @@ size_t sonic_fwd_workspace_size(const sonic_moe_desc *desc);  /* Y [rows_max,d] 
 size_t sonic_bwd_workspace_size(const sonic_moe_desc *desc);  /* dH, A', dX~ (bf16) + dS partials (fp32) */
 
 /* Byte offsets of the named transients inside the fwd / bwd workspace, for
- * inspection by tests: fwd {A, Y}; bwd {dH, A_prime, dXt, dS_part}.  which = 0 (fwd) or 1 (bwd).
- * The fwd A offset is SIZE_MAX when the up/down projections are fused (A is never materialised). */
+ * inspection by tests: fwd {A, Y}; bwd {dH, A_prime, dXt, dS_part}; bwd e4m3 buffers of
+ * SONIC_F_FP8_DXT {dH' codes, dH' row scales, W1 codes, W1 column scales}.  which = 0 (fwd), 1 (bwd)
+ * or 2 (bwd fp8).  The fwd A offset is SIZE_MAX when the up/down projections are fused (A is never
+ * materialised); the which = 2 offsets are SIZE_MAX without SONIC_F_FP8_DXT. */
 sonic_status sonic_workspace_offsets(const sonic_moe_desc *desc, int which, size_t offs_out[4]);
 
 /*

@@ -437,12 +437,18 @@ def bf16_round(x):
 
 
 def fp8_dxt_rows(dH_e, sw_e):
-    """The e4m3 operand of the FP8 dX~ GEMM (NEXT-4, Q23): the stored (bf16) dH rows times the forward's
+    """The e4m3 operand of the FP8 dX~ GEMM (NEXT-4, Q25): the stored (bf16) dH rows times the forward's
     per-column W1 scales sw_e[j] in fp32 -- folding the weight scale, which varies along this GEMM's
-    reduction dimension j, into dH -- then quantised per row.  Returns (q [f_e, 2n], s [f_e])."""
+    reduction dimension j, into dH -- then quantised per row: s = fl32(amax / 448) (1 where amax = 0),
+    r = fl32(1 / s), q = e4m3_round(fl32(M r)) (one multiply per element by the row's reciprocal scale).
+    Returns (q [f_e, 2n], s [f_e])."""
     dHb = bf16_round(dH_e).astype(np.float32)
     M = (dHb * np.asarray(sw_e, dtype=np.float32)[None, :]).astype(np.float32)
-    return quantize_e4m3(M, axis=1)
+    amax = np.max(np.abs(M), axis=1, keepdims=True).astype(np.float32)
+    scale = np.where(amax > 0, amax / np.float32(E4M3_MAX), np.float32(1.0)).astype(np.float32)
+    rcp = (np.float32(1.0) / scale).astype(np.float32)
+    q = e4m3_round((M * rcp).astype(np.float32))
+    return q, np.squeeze(scale, axis=1).astype(np.float64)
 
 
 def expert_dxt_fp8(dH_e, W1q_e, sw_e):
@@ -555,7 +561,8 @@ def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None, fp8_dxt=Fal
     dX_t = sum_e pi_te dX~_e,t (Alg. 5's aggregation).
     ``experts`` restricts the work (dX then holds only those experts' terms).
     fp8_dxt: dX~_e on e4m3 operands (``expert_dxt_fp8``; W1 quantised per column as in the forward's
-    fp8 up-projection); every other output is the bf16 path's.
+    fp8 up-projection) from the dH the method stores -- computed from the bf16-cached H and
+    rounded to bf16 (Q25); every other output is the bf16 path's.
     """
     dO, X, W1, W2 = _f64(dO), _f64(X), _f64(W1), _f64(W2)
     T, d = X.shape
@@ -572,7 +579,9 @@ def backward(dO, X, W1, W2, rt: Routing, experts=None, H_cache=None, fp8_dxt=Fal
         g = expert_backward(dO[toks], X[toks], W1[e], W2[e], rt.gate[toks, e],
                             None if H_cache is None else _f64(H_cache[e]))
         if fp8_dxt:
-            g.dXt = expert_dxt_fp8(g.dH, W1q[e], sw[e])
+            Hb = bf16_round(X[toks] @ W1[e] if H_cache is None else _f64(H_cache[e]))
+            gb = expert_backward(dO[toks], X[toks], W1[e], W2[e], rt.gate[toks, e], Hb)
+            g.dXt = expert_dxt_fp8(gb.dH, W1q[e], sw[e])
         dW1[e], dW2[e] = g.dW1, g.dW2
         np.add.at(dX, toks, g.dXt)                             # dX_t = sum_e dX~_e,t
         dS[e], dH[e], Ap[e], dXt[e] = g.dS, g.dH, g.A_prime, g.dXt

@@ -4,6 +4,7 @@
 //   columns: W1 [E, d, 2n] -> W1q [E, d, 2n] e4m3,  sw [E, 2n]  (per output column of each expert)
 // scale = amax / 448 in fp32 (1 where amax = 0), q = cvt.rn.satfinite.e4m3(fl32(x / scale)) --
 // exactly oracle.quantize_e4m3.  W1q keeps W1's layout (MN-major B operand: valid for e4m3).
+#include <algorithm>
 #include <cuda_bf16.h>
 #include <cuda_fp8.h>
 
@@ -131,6 +132,152 @@ __global__ void __launch_bounds__(256) k_quant_cols_e4m3(const __nv_bfloat16* __
     }
     *reinterpret_cast<uint2*>(qb + (size_t)k * N) = make_uint2(o[0], o[1]);
   }
+}
+
+// FP8 dX~ operand (SONIC_F_FP8_DXT, DESIGN Q25): grouped row r of dH [rows, cols = 2n] (bf16, expert
+// e = tile_expert[r / 128]) times the forward's per-column W1 scales sw[e][j] in fp32, quantised per
+// row with one multiply by the reciprocal row scale -- exactly oracle.fp8_dxt_rows.  One warp per row,
+// lanes over 8-column chunks (16-byte dH loads, two float4 scale loads); rows past the device-resident
+// row count (num_tiles * 128) are skipped.  HBM-bound: 3 bytes per element.
+__device__ __forceinline__ void scaled8(const uint4& v, const float4& s0, const float4& s1, float (&m)[8]) {
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+  const float2 c = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.z));
+  const float2 d = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.w));
+  m[0] = __fmul_rn(a.x, s0.x); m[1] = __fmul_rn(a.y, s0.y); m[2] = __fmul_rn(b.x, s0.z); m[3] = __fmul_rn(b.y, s0.w);
+  m[4] = __fmul_rn(c.x, s1.x); m[5] = __fmul_rn(c.y, s1.y); m[6] = __fmul_rn(d.x, s1.z); m[7] = __fmul_rn(d.y, s1.w);
+}
+__global__ void __launch_bounds__(256) k_quant_dh_e4m3(const __nv_bfloat16* __restrict__ dH, long long rows_max,
+                                                       int cols, const int* __restrict__ num_tiles,
+                                                       const int* __restrict__ tile_expert,
+                                                       const float* __restrict__ sw, uint8_t* __restrict__ q,
+                                                       float* __restrict__ scale) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const long long r = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= rows_max || r >= (long long)(*num_tiles) * GEMM_M) return;
+  const float4* swe = reinterpret_cast<const float4*>(sw + (size_t)__ldg(tile_expert + r / GEMM_M) * cols);
+  const uint4* src = reinterpret_cast<const uint4*>(dH + r * cols);
+  const int nch = cols / 8;
+  float amax = 0.f;
+  for (int c = lane; c < nch; c += 32) {
+    float m[8];
+    scaled8(__ldg(src + c), __ldg(swe + 2 * c), __ldg(swe + 2 * c + 1), m);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(m[i]));
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  const float s = scale_of(amax);
+  const float rcp = __frcp_rn(s);
+  if (lane == 0) scale[r] = s;
+  uint2* dst = reinterpret_cast<uint2*>(q + r * cols);
+  for (int c = lane; c < nch; c += 32) {  // the row's second pass hits L1 / L2
+    float m[8];
+    scaled8(__ldg(src + c), __ldg(swe + 2 * c), __ldg(swe + 2 * c + 1), m);
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i >> 2] |= (uint32_t)to_e4m3(__fmul_rn(m[i], rcp)) << (8 * (i & 3));
+    dst[c] = make_uint2(w[0], w[1]);
+  }
+}
+
+// cols <= 512 (n <= 256, the fine-grained configs): RW rows per warp held in registers across the
+// amax and the quantisation, all their loads issued together -- one memory round trip per RW rows
+// Persistent warps (grid = 2 blocks per SM): each warp walks its rows two at a time with the next two
+// rows' loads issued before the current ones are converted, so the loads stay in flight across the
+// conversion (short rows: a one-row-per-warp kernel leaves the SMs waiting on each row's round trip).
+__device__ __forceinline__ void quant_row_pair(const uint4 (&v)[2][2], const int (&e)[2], long long r, long long rlim,
+                                               int nch, int cols, int lane, const float* __restrict__ sw,
+                                               uint8_t* __restrict__ q, float* __restrict__ scale) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    if (r + k >= rlim) return;
+    const float4* swe = reinterpret_cast<const float4*>(sw + (size_t)e[k] * cols);
+    float amax = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= nch) continue;
+      float m[8];
+      scaled8(v[k][h], __ldg(swe + 2 * c), __ldg(swe + 2 * c + 1), m);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(m[i]));
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    const float s = scale_of(amax);
+    const float rcp = __frcp_rn(s);
+    if (lane == 0) scale[r + k] = s;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c >= nch) continue;
+      float m[8];
+      scaled8(v[k][h], __ldg(swe + 2 * c), __ldg(swe + 2 * c + 1), m);  // the scales again: L1 hits
+      uint32_t w[2];
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {  // two values per cvt (e4m3x2, round to nearest even, satfinite)
+        const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(m[4 * p], rcp), __fmul_rn(m[4 * p + 1], rcp)),
+                                                     __NV_SATFINITE, __NV_E4M3);
+        const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(m[4 * p + 2], rcp), __fmul_rn(m[4 * p + 3], rcp)),
+                                                     __NV_SATFINITE, __NV_E4M3);
+        w[p] = (lo & 0xFFFFu) | (hi << 16);
+      }
+      reinterpret_cast<uint2*>(q + (r + k) * cols)[c] = make_uint2(w[0], w[1]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) k_quant_dh_e4m3_regs(const __nv_bfloat16* __restrict__ dH, long long rows_max,
+                                                               int cols, const int* __restrict__ num_tiles,
+                                                               const int* __restrict__ tile_expert,
+                                                               const float* __restrict__ sw, uint8_t* __restrict__ q,
+                                                               float* __restrict__ scale) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const long long rlim = min(rows_max, (long long)(*num_tiles) * GEMM_M);
+  const int nch = cols / 8;  // <= 64: chunks lane and lane + 32
+  const long long step = (long long)gridDim.x * 8 * 2;
+  auto load = [&](long long r, uint4 (&v)[2][2], int (&e)[2]) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool ok = r + k < rlim;
+      e[k] = ok ? __ldg(tile_expert + (r + k) / GEMM_M) : 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        v[k][h] = (ok && lane + 32 * h < nch) ? __ldg(reinterpret_cast<const uint4*>(dH + (r + k) * cols) + lane + 32 * h)
+                                               : make_uint4(0u, 0u, 0u, 0u);
+    }
+  };
+  long long r = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2;
+  uint4 va[2][2], vb[2][2];
+  int ea[2], eb[2];
+  load(r, va, ea);
+  for (; r < rlim; r += 2 * step) {
+    load(r + step, vb, eb);  // the next pair in flight while this one converts
+    quant_row_pair(va, ea, r, rlim, nch, cols, lane, sw, q, scale);
+    if (r + step >= rlim) break;
+    load(r + 2 * step, va, ea);
+    quant_row_pair(vb, eb, r + step, rlim, nch, cols, lane, sw, q, scale);
+  }
+}
+
+void launch_quant_dh_e4m3(const void* dH, long long rows_max, int cols, const int* num_tiles, const int* tile_expert,
+                          const float* sw, void* q, float* scale, cudaStream_t st) {
+  if (cols <= 512) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const long long blocks = std::min<long long>(2LL * sms, (rows_max + 15) / 16);
+    launch_k(k_quant_dh_e4m3_regs, (int)std::max<long long>(1, blocks), 256, 0, st,
+             static_cast<const __nv_bfloat16*>(dH), rows_max, cols, num_tiles, tile_expert, sw,
+             static_cast<uint8_t*>(q), scale);
+    return;
+  }
+  launch_k(k_quant_dh_e4m3, (int)((rows_max + 7) / 8), 256, 0, st, static_cast<const __nv_bfloat16*>(dH), rows_max,
+           cols, num_tiles, tile_expert, sw, static_cast<uint8_t*>(q), scale);
 }
 
 void launch_quant_rows_e4m3(const void* X, long long rows, int cols, void* q, float* scale, cudaStream_t st) {

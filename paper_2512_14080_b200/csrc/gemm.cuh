@@ -37,7 +37,10 @@
 
 namespace sonic {
 
-enum GemmKind { K_UP = 0, K_DOWN = 1, K_DH = 2, K_DXT = 3, K_DW2 = 4, K_DW1 = 5, K_UP8 = 6 };
+enum GemmKind { K_UP = 0, K_DOWN = 1, K_DH = 2, K_DXT = 3, K_DW2 = 4, K_DW1 = 5, K_UP8 = 6, K_DXT8 = 7 };
+// K_DXT8: dX~ with e4m3 operands (SONIC_F_FP8_DXT, NEXT-4, DESIGN Q25): A = the row-quantised
+// dH' = bf16(dH) * sw (the forward's per-column W1 scales folded in), B = the forward's e4m3 W1 copy
+// (K-major here: W1q_e [d, 2n]); dX~ = sum * s_row in the DXT epilogue.  k-blocks of 128 e4m3.
 // K_UP8: the up-projection with e4m3 operands (SONIC_F_FP8_UP, NEXT-4): Gather(Xq) W1q_e with the
 // per-token scale sx and per-column scale sw applied to the fp32 sum in the epilogue, which is then
 // K_UP's (H, A in bf16).  A k-block is 128 e4m3 values: the same 128-byte rows, stages and
@@ -74,7 +77,7 @@ struct GemmArgs {
   int agg_d;
   int accumulate;           // DW1 / DW2: add into the existing dW (SONIC_F_DW_ACCUMULATE) instead of overwriting
   int dw_bf16;              // DW1 / DW2: store dW as bf16 (SONIC_F_DW_BF16; the store map is then bf16)
-  const float* sx;          // UP8: per-token scale of the e4m3 X rows [T]
+  const float* sx;          // UP8: per-token scale of the e4m3 X rows [T]; DXT8: per-row scale of the e4m3 dH' [rows]
   const float* sw;          // UP8: per-column scale of the e4m3 W1 [E, 2n]
 };
 
@@ -85,6 +88,7 @@ template <> struct Traits<K_UP8>  { static constexpr bool vk = false, a_gather =
 template <> struct Traits<K_DOWN> { static constexpr bool vk = false, a_gather = false, a_mn = false, b_gather = false, b_mn = true;  };
 template <> struct Traits<K_DH>   { static constexpr bool vk = false, a_gather = true,  a_mn = false, b_gather = false, b_mn = false; };
 template <> struct Traits<K_DXT>  { static constexpr bool vk = false, a_gather = false, a_mn = false, b_gather = false, b_mn = false; };
+template <> struct Traits<K_DXT8> { static constexpr bool vk = false, a_gather = false, a_mn = false, b_gather = false, b_mn = false; };
 template <> struct Traits<K_DW2>  { static constexpr bool vk = true,  a_gather = false, a_mn = true,  b_gather = true,  b_mn = true;  };
 template <> struct Traits<K_DW1>  { static constexpr bool vk = true,  a_gather = true,  a_mn = true,  b_gather = false, b_mn = true;  };
 
@@ -454,7 +458,8 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
   // bytes landing through TMA per stage per CTA (the non-gathered operands)
   constexpr uint32_t TMA_BYTES = !GATHER ? STAGE_BYTES : (Tr::a_gather ? Cfg::B_BYTES : A_BYTES);
   constexpr int MMA_M = CTA2 ? 2 * GEMM_BM : GEMM_BM;
-  constexpr bool F8 = KIND == K_UP8;  // e4m3 operands (kind::f8f6f4)
+  constexpr bool F8 = KIND == K_UP8 || KIND == K_DXT8;  // e4m3 operands (kind::f8f6f4)
+  constexpr int KBE = F8 ? 128 : GEMM_BK;               // operand elements per k-block (128 bytes)
   constexpr int ESZ = F8 ? 1 : 2;     // bytes per operand element
 
   extern __shared__ uint8_t smem_raw[];
@@ -603,12 +608,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             if constexpr (MC)  // half of the shared A tile (64 rows, box map mD) into both pairs
               ptx::tma_load_2d_cg2_mc(sA + pidx * 8192, &mD, bar, kb * GEMM_BK, tc.row0 + 64 * pidx, smask);
             else
-              tload2<CTA2>(sA, &mA, bar, kb * GEMM_BK, tc.row0);
+              tload2<CTA2>(sA, &mA, bar, kb * KBE, tc.row0);
             if constexpr (KIND == K_DOWN) {
 #pragma unroll
               for (int j = 0; j < BNL / 64; ++j) tload3<CTA2>(sB + j * 8192, &mB, bar, n0 + 64 * j, kb * GEMM_BK, tc.e);
-            } else {  // DXT: K-major weights, one box of BNL rows
-              tload3<CTA2>(sB, &mB, bar, kb * GEMM_BK, n0, tc.e);
+            } else {  // DXT / DXT8: K-major weights, one box of BNL rows
+              tload3<CTA2>(sB, &mB, bar, kb * KBE, n0, tc.e);
             }
             if (++stage == STAGES) {
               stage = 0;
@@ -1090,11 +1095,12 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
           write_row_bf16(sq.addr(i), lane, a);
           sq.issue(lane, i, &mC1, 0, wrow);  // columns >= n are clipped by the tensor map
         }
-      } else if constexpr ((KIND == K_DOWN || KIND == K_DXT) && SONIC_EPI_PIPE) {
+      } else if constexpr ((KIND == K_DOWN || KIND == K_DXT || KIND == K_DXT8) && SONIC_EPI_PIPE) {
         // TMEM loads run one 64-column chunk ahead of the convert + store of the current chunk, so
         // the tcgen05.ld latency is paid once per tile instead of twice per chunk.
         float gate = 1.f;
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
+        if constexpr (KIND == K_DXT8) gate = __ldg(args.sx + row);  // the row scale of the e4m3 dH'
         constexpr int NCH = BN / (64 * Cfg::EPH);
         static_assert(wide_g<KIND>() == 1 || Cfg::EPH == 1, "wide stores: one warp per TMEM lane quarter");
         int wslot = 0;
@@ -1150,9 +1156,10 @@ __global__ void __launch_bounds__(gemm_threads<KIND>(), 1)
             ptx::tmem_regs_ready(r[sl ^ 1][1]);
           }
         }
-      } else if constexpr (KIND == K_DOWN || KIND == K_DXT) {
+      } else if constexpr (KIND == K_DOWN || KIND == K_DXT || KIND == K_DXT8) {
         float gate = 1.f;
         if constexpr (KIND == K_DOWN) gate = __ldg(args.row_gate + row);
+        if constexpr (KIND == K_DXT8) gate = __ldg(args.sx + row);
 #pragma unroll 1
         for (int c = 64 * half; c < BN; c += 64 * Cfg::EPH) {
           if (tc.nt * BN + c >= args.N_dim) break;

@@ -89,6 +89,18 @@ bool map2d(CUtensorMap* m, const void* ptr, bool f32, long long rows, long long 
              gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// 2-D row-major [rows, cols] bytes (e4m3); box {box_cols, box_rows}; 128B swizzle.
+bool map2d_u8(CUtensorMap* m, const void* ptr, long long rows, long long cols, int box_cols, int box_rows) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)cols};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(ptr), gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 // 3-D row-major [E, rows, cols] bytes (e4m3); box {box_cols, box_rows, 1}; 128B swizzle.
 bool map3d_u8(CUtensorMap* m, const void* ptr, long long E, long long rows, long long cols, int box_cols, int box_rows) {
   EncodeTiledFn enc = get_encoder();
@@ -258,8 +270,8 @@ bool launch_gemm(int BN, const CUtensorMap& a, const CUtensorMap& b, const CUten
   const CUtensorMap& d = dmap ? *dmap : c0;
   const bool cta2 = use_cta2(BN);
   if (cta2) grid = std::max(2, grid & ~1);  // a pair needs both CTAs, even for a single pair tile
-  if constexpr (KIND == K_UP8) {  // e4m3: 2-CTA pairs of 256 columns only (fp8_up_ok)
-    return cta2 && BN == 256 && launch_gemm_t<K_UP8, 256, true>(a, b, c0, c1, d, args, grid, st);
+  if constexpr (KIND == K_UP8 || KIND == K_DXT8) {  // e4m3: 2-CTA pairs of 256 columns only (fp8_*_ok)
+    return cta2 && BN == 256 && launch_gemm_t<KIND, 256, true>(a, b, c0, c1, d, args, grid, st);
   } else {
     if constexpr (KIND == K_DOWN || KIND == K_DXT || KIND == K_DW2 || KIND == K_DW1) {
       if (SONIC_MC4 && !g4_kind<KIND>() && mc && cta2 && BN == 256)
@@ -457,7 +469,11 @@ FwdWs fwd_ws(const sonic_moe_desc* D) {
   w.total = o;
   return w;
 }
-struct BwdWs { size_t dH, Ap, dXt, dSp, total; int dh_tiles; };
+// SONIC_F_FP8_DXT (NEXT-4): dX~ on e4m3 operands; 2-CTA 256-column DXT tiles (d % 256 == 0) and
+// whole 128-element k-blocks of 2n (n % 64 == 0)
+bool fp8_dxt(const sonic_moe_desc* D) { return (D->flags & SONIC_F_FP8_DXT) != 0; }
+bool fp8_dxt_ok(const sonic_moe_desc* D) { return use_cta2(256) && D->n % 64 == 0 && D->d % 256 == 0; }
+struct BwdWs { size_t dH, Ap, dXt, dSp, dHq, sdh, W1q, sw, total; int dh_tiles; };
 BwdWs bwd_ws(const sonic_moe_desc* D) {
   const Shape s = shape_of(D);
   BwdWs w;
@@ -467,6 +483,13 @@ BwdWs bwd_ws(const sonic_moe_desc* D) {
   w.dXt = o; o += al((size_t)s.rows_max * s.d * 2);
   w.dh_tiles = s.n / dh_bn(s.n);
   w.dSp = o; o += w.dh_tiles > 1 ? al((size_t)w.dh_tiles * s.rows_max * 4) : 0;
+  w.dHq = w.sdh = w.W1q = w.sw = SIZE_MAX;
+  if (fp8_dxt(D)) {  // e4m3 dH' and W1 copies and their scales
+    w.dHq = o; o += al((size_t)s.rows_max * 2 * s.n);
+    w.sdh = o; o += al((size_t)s.rows_max * 4);
+    w.W1q = o; o += al((size_t)s.E * s.d * 2 * s.n);
+    w.sw = o; o += al((size_t)s.E * 2 * s.n * 4);
+  }
   w.total = o;
   return w;
 }
@@ -517,6 +540,9 @@ sonic_status sonic_workspace_offsets(const sonic_moe_desc* D, int which, size_t 
   } else if (which == 1) {
     const BwdWs w = bwd_ws(D);
     offs[0] = w.dH; offs[1] = w.Ap; offs[2] = w.dXt; offs[3] = w.dSp;
+  } else if (which == 2) {
+    const BwdWs w = bwd_ws(D);
+    offs[0] = w.dHq; offs[1] = w.sdh; offs[2] = w.W1q; offs[3] = w.sw;
   } else {
     return SONIC_ERR_INVALID_ARG;
   }
@@ -771,6 +797,7 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   if (!dO || !X || !H || !W1 || !W2 || !rt || (!dw_only && (!dX || !dS)) || (!no_dw && (!dW1 || !dW2)))
     return SONIC_ERR_INVALID_ARG;
   if (!supported_dims(D)) return SONIC_ERR_UNSUPPORTED;
+  if (fp8_dxt(D) && (!fp8_dxt_ok(D) || dw_only)) return fp8_dxt_ok(D) ? SONIC_ERR_INVALID_ARG : SONIC_ERR_UNSUPPORTED;
   const BwdWs w = bwd_ws(D);
   if (!ws || ws_bytes < w.total) return SONIC_ERR_WORKSPACE;
   for (const void* p : {dO, X, H, W1, W2, (const void*)dX, (const void*)dW1, (const void*)dW2, (const void*)dS,
@@ -863,6 +890,30 @@ sonic_status sonic_moe_bwd(const sonic_moe_desc* D, const void* dO, const void* 
   const int tiles7 = E * a7.m_tiles * a7.n_tiles;
 
   auto run_dxt = [&]() {
+    if (fp8_dxt(D)) {
+      // e4m3 dX~ (Q25): W1 per output column (the forward's quantisation), dH' = dH * sw per row
+      uint8_t* dHq = base + w.dHq;
+      float* sdh = reinterpret_cast<float*>(base + w.sdh);
+      uint8_t* W1q = base + w.W1q;
+      float* sw = reinterpret_cast<float*>(base + w.sw);
+      {
+        ProfScope ps("quant_dh", st);
+        if (!(D->flags & SONIC_F_FP8_W1_CACHED)) {
+          launch_quant_cols_e4m3(W1, E, d, 2 * n, W1q, sw, st);
+          g_launches += 3;
+        }
+        launch_quant_dh_e4m3(dH, R, 2 * n, rt->num_tiles, rt->tile_expert, sw, dHq, sdh, st);
+        ++g_launches;
+      }
+      CUtensorMap mA8, mB8, mC8;
+      if (!map2d_u8(&mA8, dHq, R, 2 * n, 128, 128) || !map3d_u8(&mB8, W1q, E, d, 2 * n, 128, bnl(BN6)) ||
+          !map2d(&mC8, dXt, false, R, d, 64, 32))
+        return false;
+      GemmArgs a8 = a6;
+      a8.k_blocks = (2 * n) / 128; a8.sx = sdh; a8.wide = 0;
+      ProfScope ps("dXt", st);
+      return launch_gemm<K_DXT8>(256, mA8, mB8, mC8, mC8, a8, grid, st);
+    }
     ProfScope ps("dXt", st);
     return launch_gemm<K_DXT>(BN6, mA6, mB6, mC6, mC6, a6, grid, st, &mA6h, a6.n_tiles % 2 == 0);
   };

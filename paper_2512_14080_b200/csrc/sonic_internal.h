@@ -71,6 +71,8 @@ void launch_ds_reduce(const float* part, int nparts, long long rows_max, const i
 // e4m3 quantisation (fp8.cu): per row of X [rows, cols]; per column of each W [batch, K, N]
 void launch_quant_rows_e4m3(const void* X, long long rows, int cols, void* q, float* scale, cudaStream_t st);
 void launch_quant_cols_e4m3(const void* W, int batch, int K, int N, void* q, float* scale, cudaStream_t st);
+void launch_quant_dh_e4m3(const void* dH, long long rows_max, int cols, const int* num_tiles, const int* tile_expert,
+                          const float* sw, void* q, float* scale, cudaStream_t st);
 
 // record the number of kernels the current C-ABI call launched (sonic_last_launch_count)
 void set_last_launch_count(int n);

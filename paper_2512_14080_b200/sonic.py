@@ -37,6 +37,7 @@ SONIC_F_NO_FUSED_UPDOWN = 64
 SONIC_F_FUSED_UPDOWN = 128
 SONIC_F_FP8_UP = 256
 SONIC_F_FP8_W1_CACHED = 512
+SONIC_F_FP8_DXT = 1024
 GEMM_M = 128
 
 ROUTING_FIELDS = ["topk_ids", "topk_s", "f", "f_rounded", "offsets", "pad_offsets", "row_token", "row_gate",

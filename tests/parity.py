@@ -169,7 +169,7 @@ def run_gpu(desc, inp, want_ws=True, poison=False):
         O, H, wsf = sonic.sonic_moe_fwd(desc, inp.X, inp.W1, inp.W2, rt)
         dX, dW1, dW2, dS, wsb = sonic.sonic_moe_bwd(desc, inp.dO, inp.X, H, inp.W1, inp.W2, rt)
     torch.cuda.synchronize()
-    out = dict(rt=rt, O=O, H=H, dX=dX, dW1=dW1, dW2=dW2, dS=dS)
+    out = dict(rt=rt, O=O, H=H, dX=dX, dW1=dW1, dW2=dW2, dS=dS, ws_bwd=wsb)
     if want_ws:
         offs = sonic.sonic_workspace_offsets(desc, 1)
         rows = sonic.sonic_rows_max(desc)
@@ -202,10 +202,11 @@ class _Lazy:
 def stream_parity(desc, inp, g, rto, check_ws=True):
     """(see _stream_parity)"""
     return _stream_parity(desc, inp, g, rto, check_ws=check_ws,
-                          fp8_up=bool(desc.flags & getattr(sonic, "SONIC_F_FP8_UP", 0)))
+                          fp8_up=bool(desc.flags & getattr(sonic, "SONIC_F_FP8_UP", 0)),
+                          fp8_dxt=bool(desc.flags & getattr(sonic, "SONIC_F_FP8_DXT", 0)))
 
 
-def _stream_parity(desc, inp, g, rto, check_ws=True, fp8_up=False):
+def _stream_parity(desc, inp, g, rto, check_ws=True, fp8_up=False, fp8_dxt=False):
     """Element-by-element parity of every output, one expert at a time (the oracle's per-expert
     stages ``expert_forward`` / ``expert_backward``, pinned in tests/test_oracle.py), so that the
     full BASELINE sizes fit in host memory.  Every routed row, token and weight element is compared;
@@ -234,6 +235,11 @@ def _stream_parity(desc, inp, g, rto, check_ws=True, fp8_up=False):
         else:
             He, Ae, Ye = om.expert_forward(Xe, W1[e], W2[e], ge)
         gr = om.expert_backward(dOe, Xe, W1[e], W2[e], ge, He)
+        if fp8_dxt:  # SONIC_F_FP8_DXT: dX~ on the e4m3 operands of Q25 (oracle.expert_dxt_fp8), from the
+            # dH the method stores: computed from the bf16-cached H, rounded to bf16
+            W1q_e, sw_e = om.quantize_e4m3(W1[e], axis=0)
+            dHb = om.expert_backward(dOe, Xe, W1[e], W2[e], ge, om.bf16_round(He)).dH
+            gr.dXt = om.expert_dxt_fp8(dHb, W1q_e, sw_e)
         np.add.at(O_ref, toks, Ye)
         np.add.at(dX_ref, toks, gr.dXt)
         acc["H"].add(f64(g["H"][lo: lo + fe]), He)

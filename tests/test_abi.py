@@ -137,6 +137,20 @@ def test_round2_calls_validate_on_the_host(lib):
     d16 = sonic.make_desc(256, 128, 128, 8, 2)
     assert lib.sonic_fwd_workspace_size(ctypes.byref(d8ok)) >= (lib.sonic_fwd_workspace_size(ctypes.byref(d16)) +
                                                                 256 * 128 + 8 * 128 * 256)
+    # FP8 dX~: d % 256 != 0 -> UNSUPPORTED; with SONIC_F_BWD_DW_ONLY (no dX~ to compute) -> INVALID_ARG;
+    # the bwd workspace then holds the e4m3 dH' rows, their scales and W1's e4m3 copy + column scales
+    dx8 = sonic.make_desc(256, 128, 128, 8, 2, flags=sonic.SONIC_F_FP8_DXT)
+    assert lib.sonic_moe_bwd(ctypes.byref(dx8), P, P, P, P, P, ctypes.byref(rt), P, P, P, P, P, 1 << 40, None) == -2
+    dx8ok = sonic.make_desc(256, 256, 128, 8, 2, flags=sonic.SONIC_F_FP8_DXT)
+    dx8dw = sonic.make_desc(256, 256, 128, 8, 2, flags=sonic.SONIC_F_FP8_DXT | sonic.SONIC_F_BWD_DW_ONLY)
+    assert lib.sonic_moe_bwd(ctypes.byref(dx8dw), P, P, P, P, P, ctypes.byref(rt), P, P, P, P, P, 1 << 40, None) == -1
+    d16b = sonic.make_desc(256, 256, 128, 8, 2)
+    rows = lib.sonic_rows_max(ctypes.byref(dx8ok))
+    assert lib.sonic_bwd_workspace_size(ctypes.byref(dx8ok)) >= (lib.sonic_bwd_workspace_size(ctypes.byref(d16b)) +
+                                                                 rows * 256 + rows * 4 + 8 * 256 * 256 + 8 * 256 * 4)
+    offs = (ctypes.c_size_t * 4)()
+    assert lib.sonic_workspace_offsets(ctypes.byref(dx8ok), 2, offs) == 0 and offs[0] != (1 << 64) - 1
+    assert lib.sonic_workspace_offsets(ctypes.byref(d16b), 2, offs) == 0 and offs[0] == (1 << 64) - 1
 
 
 def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):

@@ -425,6 +425,32 @@ def test_fp8_up_parity(case):
     print(name, {k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
 
 
+FP8_DXT_CASES = [
+    ("fp8dxt_tc", 2048, 256, 128, 16, 4, "tc", 0),
+    ("fp8dxt_tr", 2048, 256, 128, 16, 4, "tr", 0),
+    ("fp8dxt_n64_ragged", 1000, 512, 64, 8, 2, "tc", 0),
+    ("fp8dxt_7b_dims", 4096, 1536, 256, 8, 2, "tc", 0),
+    ("fp8dxt_with_fp8_up", 2048, 256, 128, 16, 4, "tc", 1),
+]
+
+
+@pytest.mark.parametrize("case", FP8_DXT_CASES, ids=[c[0] for c in FP8_DXT_CASES])
+def test_fp8_dxt_parity(case):
+    """SONIC_F_FP8_DXT: every output of route + fwd + bwd against the oracle whose dX~ runs on the
+    e4m3 operands of reading Q25 (backward(fp8_dxt=True): the stored bf16 dH times the forward's
+    per-column W1 scales, quantised per row, against the forward's e4m3 W1), within the north-star
+    criterion; dH, dS, dW1, dW2 are the bf16 path's.  The GPU quantises its own bf16 dH, the oracle the
+    bf16 rounding of its fp64 dH: where the two bf16 values differ by an ulp, an e4m3 code can flip
+    (~1/32 of those elements), a perturbation far inside the criterion."""
+    name, T, d, n, E, K, mode, up8 = case
+    inp = make_inputs(T, d, n, E, K, seed=13, device="cuda")
+    m = sonic.SONIC_ROUTE_TC if mode == "tc" else sonic.SONIC_ROUTE_TR_NRF
+    fl = sonic.SONIC_F_FP8_DXT | (sonic.SONIC_F_FP8_UP if up8 else 0)
+    desc = sonic.make_desc(T, d, n, E, K, mode=m, flags=fl)
+    stats = full_parity(desc, inp, mode=mode)
+    print(name, {k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
+
+
 def test_fp8_w1_cached_reuses_the_copy():
     """SONIC_F_FP8_W1_CACHED reuses the e4m3 W1 left in the workspace by the previous call: the same
     outputs as quantising again (same W1), and different from a call whose cached copy is stale."""

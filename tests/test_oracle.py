@@ -702,7 +702,10 @@ def test_backward_fp8_dxt_is_the_quantised_definition():
     dX_ref = np.zeros_like(full.dX)
     for e in range(E):
         toks = np.nonzero(rt.kept[:, e])[0]
-        q, s = om.fp8_dxt_rows(full.dH[e], sw[e])
+        Hb = om.bf16_round(X[toks] @ W1[e])  # the dH the method stores comes from the bf16-cached H
+        dHe = om.expert_backward(dO[toks], X[toks], W1[e], W2[e], rt.gate[toks, e], Hb).dH
+        q, s = om.fp8_dxt_rows(dHe, sw[e])
+        assert np.all(np.abs(q) <= 448) and np.all(s > 0)
         dH_dq = s[:, None] * q / sw[e][None, :]
         W1_dq = W1q[e] * sw[e][None, :]
         np.add.at(dX_ref, toks, dH_dq @ W1_dq.T)
