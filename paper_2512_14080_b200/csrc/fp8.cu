@@ -185,96 +185,96 @@ __global__ void __launch_bounds__(256) k_quant_dh_e4m3(const __nv_bfloat16* __re
 
 // cols <= 512 (n <= 256, the fine-grained configs): RW rows per warp held in registers across the
 // amax and the quantisation, all their loads issued together -- one memory round trip per RW rows
-// Persistent warps (grid = 2 blocks per SM): each warp walks its rows two at a time with the next two
-// rows' loads issued before the current ones are converted, so the loads stay in flight across the
-// conversion (short rows: a one-row-per-warp kernel leaves the SMs waiting on each row's round trip).
-__device__ __forceinline__ void quant_row_pair(const uint4 (&v)[2][2], const int (&e)[2], long long r, long long rlim,
-                                               int nch, int cols, int lane, const float* __restrict__ sw,
-                                               uint8_t* __restrict__ q, float* __restrict__ scale) {
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    if (r + k >= rlim) return;
-    const float4* swe = reinterpret_cast<const float4*>(sw + (size_t)e[k] * cols);
-    float amax = 0.f;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      if (c >= nch) continue;
-      float m[8];
-      scaled8(v[k][h], __ldg(swe + 2 * c), __ldg(swe + 2 * c + 1), m);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) amax = fmaxf(amax, fabsf(m[i]));
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    const float s = scale_of(amax);
-    const float rcp = __frcp_rn(s);
-    if (lane == 0) scale[r + k] = s;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int c = lane + 32 * h;
-      if (c >= nch) continue;
-      float m[8];
-      scaled8(v[k][h], __ldg(swe + 2 * c), __ldg(swe + 2 * c + 1), m);  // the scales again: L1 hits
-      uint32_t w[2];
-#pragma unroll
-      for (int p = 0; p < 2; ++p) {  // two values per cvt (e4m3x2, round to nearest even, satfinite)
-        const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(m[4 * p], rcp), __fmul_rn(m[4 * p + 1], rcp)),
-                                                     __NV_SATFINITE, __NV_E4M3);
-        const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(m[4 * p + 2], rcp), __fmul_rn(m[4 * p + 3], rcp)),
-                                                     __NV_SATFINITE, __NV_E4M3);
-        w[p] = (lo & 0xFFFFu) | (hi << 16);
-      }
-      reinterpret_cast<uint2*>(q + (r + k) * cols)[c] = make_uint2(w[0], w[1]);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256, 2) k_quant_dh_e4m3_regs(const __nv_bfloat16* __restrict__ dH, long long rows_max,
-                                                               int cols, const int* __restrict__ num_tiles,
-                                                               const int* __restrict__ tile_expert,
-                                                               const float* __restrict__ sw, uint8_t* __restrict__ q,
-                                                               float* __restrict__ scale) {
+// cols = 32 * EPL (EPL = 4, 8, 12, 16: 2n <= 512): a warp takes blocks of QB consecutive rows (inside
+// one 128-row tile, so one expert): the expert's EPL column scales per lane are loaded once per
+// block; lane l holds the EPL contiguous elements [EPL l, EPL l + EPL) of a row in registers through
+// both the amax and the conversion (8-byte dH loads, two values per e4m3x2 conversion, one EPL-byte
+// store), with the next row's loads issued before the current row is converted.
+constexpr int QB = 16;
+template <int EPL>
+__global__ void __launch_bounds__(256) k_quant_dh_e4m3_lane(const __nv_bfloat16* __restrict__ dH, long long rows_max,
+                                                            int cols, const int* __restrict__ num_tiles,
+                                                            const int* __restrict__ tile_expert,
+                                                            const float* __restrict__ sw, uint8_t* __restrict__ q,
+                                                            float* __restrict__ scale) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  constexpr int NV = EPL / 4;  // 8-byte dH loads (4 bf16) per lane
   const int lane = threadIdx.x & 31;
   const long long rlim = min(rows_max, (long long)(*num_tiles) * GEMM_M);
-  const int nch = cols / 8;  // <= 64: chunks lane and lane + 32
-  const long long step = (long long)gridDim.x * 8 * 2;
-  auto load = [&](long long r, uint4 (&v)[2][2], int (&e)[2]) {
+  auto load = [&](long long rr, uint2 (&w)[NV]) {
+    if (rr < rlim) {
+      const uint2* src = reinterpret_cast<const uint2*>(dH + rr * cols) + lane * NV;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool ok = r + k < rlim;
-      e[k] = ok ? __ldg(tile_expert + (r + k) / GEMM_M) : 0;
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        v[k][h] = (ok && lane + 32 * h < nch) ? __ldg(reinterpret_cast<const uint4*>(dH + (r + k) * cols) + lane + 32 * h)
-                                               : make_uint4(0u, 0u, 0u, 0u);
+      for (int k = 0; k < NV; ++k) w[k] = __ldg(src + k);
     }
   };
-  long long r = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * 2;
-  uint4 va[2][2], vb[2][2];
-  int ea[2], eb[2];
-  load(r, va, ea);
-  for (; r < rlim; r += 2 * step) {
-    load(r + step, vb, eb);  // the next pair in flight while this one converts
-    quant_row_pair(va, ea, r, rlim, nch, cols, lane, sw, q, scale);
-    if (r + step >= rlim) break;
-    load(r + 2 * step, va, ea);
-    quant_row_pair(vb, eb, r + step, rlim, nch, cols, lane, sw, q, scale);
+  for (long long b0 = ((long long)blockIdx.x * 8 + (threadIdx.x >> 5)) * QB; b0 < rlim;
+       b0 += (long long)gridDim.x * 8 * QB) {
+    const float4* s4 = reinterpret_cast<const float4*>(sw + (size_t)__ldg(tile_expert + b0 / GEMM_M) * cols) + lane * NV;
+    float4 sc[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sc[k] = __ldg(s4 + k);
+    uint2 v[NV];
+    load(b0, v);
+    const int nrow = (int)min((long long)QB, rlim - b0);
+    for (int i = 0; i < nrow; ++i) {
+      const long long r = b0 + i;
+      uint2 vn[NV];
+      load(i + 1 < nrow ? r + 1 : rlim, vn);  // in flight while this row converts
+      float m[EPL];
+      float amax = 0.f;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[k].x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[k].y));
+        m[4 * k] = __fmul_rn(a.x, sc[k].x);
+        m[4 * k + 1] = __fmul_rn(a.y, sc[k].y);
+        m[4 * k + 2] = __fmul_rn(b.x, sc[k].z);
+        m[4 * k + 3] = __fmul_rn(b.y, sc[k].w);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) amax = fmaxf(amax, fabsf(m[4 * k + t]));
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      const float s = scale_of(amax);
+      const float rcp = __frcp_rn(s);
+      if (lane == 0) scale[r] = s;
+      uint32_t w[NV];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(m[4 * k], rcp), __fmul_rn(m[4 * k + 1], rcp)),
+                                                     __NV_SATFINITE, __NV_E4M3);
+        const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(__fmul_rn(m[4 * k + 2], rcp), __fmul_rn(m[4 * k + 3], rcp)),
+                                                     __NV_SATFINITE, __NV_E4M3);
+        w[k] = (lo & 0xFFFFu) | (hi << 16);
+      }
+      uint32_t* dst = reinterpret_cast<uint32_t*>(q + r * cols) + lane * NV;
+      if constexpr (NV == 4) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+      else if constexpr (NV == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+      else
+#pragma unroll
+        for (int k = 0; k < NV; ++k) dst[k] = w[k];
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[k] = vn[k];
+    }
   }
 }
 
 void launch_quant_dh_e4m3(const void* dH, long long rows_max, int cols, const int* num_tiles, const int* tile_expert,
                           const float* sw, void* q, float* scale, cudaStream_t st) {
-  if (cols <= 512) {
+  if (cols <= 512 && cols % 128 == 0) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const long long blocks = std::min<long long>(2LL * sms, (rows_max + 15) / 16);
-    launch_k(k_quant_dh_e4m3_regs, (int)std::max<long long>(1, blocks), 256, 0, st,
-             static_cast<const __nv_bfloat16*>(dH), rows_max, cols, num_tiles, tile_expert, sw,
-             static_cast<uint8_t*>(q), scale);
-    return;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(8LL * sms, (rows_max + 8 * QB - 1) / (8 * QB)));
+    const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(dH);
+    uint8_t* qq = static_cast<uint8_t*>(q);
+    switch (cols / 32) {
+      case 4: launch_k(k_quant_dh_e4m3_lane<4>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      case 8: launch_k(k_quant_dh_e4m3_lane<8>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      case 12: launch_k(k_quant_dh_e4m3_lane<12>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      default: launch_k(k_quant_dh_e4m3_lane<16>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+    }
   }
   launch_k(k_quant_dh_e4m3, (int)((rows_max + 7) / 8), 256, 0, st, static_cast<const __nv_bfloat16*>(dH), rows_max,
            cols, num_tiles, tile_expert, sw, static_cast<uint8_t*>(q), scale);
