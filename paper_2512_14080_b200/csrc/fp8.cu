@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) k_quant_dh_e4m3(const __nv_bfloat16* __re
 
 // cols <= 512 (n <= 256, the fine-grained configs): RW rows per warp held in registers across the
 // amax and the quantisation, all their loads issued together -- one memory round trip per RW rows
-// cols = 32 * EPL (EPL = 4, 8, 12, 16: 2n <= 512): a warp takes blocks of QB consecutive rows (inside
+// cols = 32 * EPL (EPL = 4, 8, 12, 16, 24, 32, 48, 64: 2n <= 2048): a warp takes blocks of QB consecutive rows (inside
 // one 128-row tile, so one expert): the expert's EPL column scales per lane are loaded once per
 // block; lane l holds the EPL contiguous elements [EPL l, EPL l + EPL) of a row in registers through
 // both the amax and the conversion (8-byte dH loads, two values per e4m3x2 conversion, one EPL-byte
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256) k_quant_dh_e4m3_lane(const __nv_bfloat16*
 
 void launch_quant_dh_e4m3(const void* dH, long long rows_max, int cols, const int* num_tiles, const int* tile_expert,
                           const float* sw, void* q, float* scale, cudaStream_t st) {
-  if (cols <= 512 && cols % 128 == 0) {
+  if (cols <= 2048 && cols % 128 == 0 && (cols <= 512 || cols % 512 == 0 || cols == 768 || cols == 1536)) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int blocks = (int)std::max<long long>(1, std::min<long long>(8LL * sms, (rows_max + 8 * QB - 1) / (8 * QB)));
@@ -273,7 +273,11 @@ void launch_quant_dh_e4m3(const void* dH, long long rows_max, int cols, const in
       case 4: launch_k(k_quant_dh_e4m3_lane<4>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
       case 8: launch_k(k_quant_dh_e4m3_lane<8>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
       case 12: launch_k(k_quant_dh_e4m3_lane<12>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
-      default: launch_k(k_quant_dh_e4m3_lane<16>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      case 16: launch_k(k_quant_dh_e4m3_lane<16>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      case 24: launch_k(k_quant_dh_e4m3_lane<24>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      case 32: launch_k(k_quant_dh_e4m3_lane<32>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      case 48: launch_k(k_quant_dh_e4m3_lane<48>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
+      default: launch_k(k_quant_dh_e4m3_lane<64>, blocks, 256, 0, st, src, rows_max, cols, num_tiles, tile_expert, sw, qq, scale); return;
     }
   }
   launch_k(k_quant_dh_e4m3, (int)((rows_max + 7) / 8), 256, 0, st, static_cast<const __nv_bfloat16*>(dH), rows_max,

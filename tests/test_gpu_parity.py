@@ -431,6 +431,8 @@ FP8_DXT_CASES = [
     ("fp8dxt_n64_ragged", 1000, 512, 64, 8, 2, "tc", 0),
     ("fp8dxt_7b_dims", 4096, 1536, 256, 8, 2, "tc", 0),
     ("fp8dxt_with_fp8_up", 2048, 256, 128, 16, 4, "tc", 1),
+    ("fp8dxt_qwen3_dims", 2048, 2048, 768, 8, 2, "tr", 0),
+    ("fp8dxt_2n_640_generic", 1024, 256, 320, 4, 2, "tc", 0),
 ]
 
 
