@@ -115,19 +115,38 @@ def sampled_parity(cfg_name, mode, n_tokens=192, n_experts=3, seed=0):
     return stats
 
 
-def full_size_parity(cfg_name, mode, seed=0):
+def full_size_parity(cfg_name, mode, seed=0, flags=0, **kw):
     """BASELINE-size parity, not sampled: routing bit-exact in full, and every element of O, H, A,
     dH, A', dS, dX, dW1, dW2 against the fp64 oracle, streamed one expert at a time
     (tests/parity.stream_parity; P:1774 "Both yield identical results")."""
     c = CONFIGS[cfg_name]
-    inp = make_inputs(**c, seed=seed, device="cuda")
-    desc = sonic.make_desc(c["T"], c["d"], c["n"], c["E"], c["K"], mode=_mode(mode))
+    inp = make_inputs(**c, seed=seed, device="cuda", **kw)
+    desc = sonic.make_desc(c["T"], c["d"], c["n"], c["E"], c["K"], mode=_mode(mode), flags=flags)
     return full_parity(desc, inp, mode=mode)
 
 
 @pytest.mark.parametrize("mode", ["tc", "tr"])
 def test_7b_full(mode):
     stats = full_size_parity("7b", mode)
+    print({k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
+
+
+def test_7b_full_second_seed_skewed_tr():
+    """SURVEY 8(d)'s 7B parity seeds (0-2) and its stress variant: seed 1, per-expert logit bias
+    0.5 N(0,1) (skewed expert loads, many rounded-up and rounded-down experts), token rounding."""
+    stats = full_size_parity("7b", "tr", seed=1, skew=0.5)
+    print({k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
+
+
+def test_7b_full_fp8_up_and_dxt():
+    """NEXT-4 at the full 7B size: the e4m3 up-projection and e4m3 dX~ against the quantisation-aware
+    oracle (forward(fp8_up=True), backward(fp8_dxt=True) steps), every element."""
+    stats = full_size_parity("7b", "tc", seed=0, flags=sonic.SONIC_F_FP8_UP | sonic.SONIC_F_FP8_DXT)
+    print({k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
+
+
+def test_7b_full_third_seed_tc():
+    stats = full_size_parity("7b", "tc", seed=2)
     print({k: f"{v[0]:.2e}/{v[1]:.2e}" for k, v in stats.items()})
 
 
