@@ -174,7 +174,7 @@ def test_ep_sync_free_overflow_is_flagged():
     assert all(res[2])
 
 
-@pytest.mark.parametrize("G,mode,E", [(1, "tc", 16), (2, "tc", 16), (4, "tr", 16), (4, "tc", 64)])
+@pytest.mark.parametrize("G,mode,E", [(1, "tc", 16), (2, "tc", 16), (4, "tr", 16), (4, "tc", 64), (8, "tr", 64)])
 def test_ep_chunked_equals_unchunked(G, mode, E):
     """NEXT-2 chunked dispatch (the self block computed before the remote blocks arrive, each chunk
     its own GIVEN routing and GEMMs): every row's arithmetic is the unchunked one, so O, dX and dS are
