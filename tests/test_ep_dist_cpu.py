@@ -74,3 +74,32 @@ def test_simcomm_count_blocks():
     recv = SimComm(G).exchange_counts(send)
     for g in range(G):
         assert recv[g] == [100 * s + g for s in range(G)] + [1000 * s + g for s in range(G)]
+
+
+def test_chunked_dispatch_geometry():
+    """NEXT-2 chunked dispatch, host side: for every rank the self block (taken from the rank's own send
+    buffer) and the remote rows before / after it partition the received rows exactly once, the self
+    block is as long in the send buffer as in the receive buffer, and the routed-pair bounds of the
+    chunks add up to the rank's total (ep._chunk_rows and the pair slices of _ep_forward_chunked)."""
+    import random
+    from paper_2512_14080_b200 import ep
+
+    class R:  # the fields _chunk_rows reads
+        def __init__(self, rank):
+            self.rank = rank
+
+    rnd = random.Random(7)
+    for G in (1, 2, 3, 8):
+        M = [[rnd.choice([0, 0, 1, 5, 17, 128]) for _ in range(G)] for _ in range(G)]  # M[s][g]: rows s -> g
+        P = [[m * rnd.randint(1, 4) for m in row] for row in M]                        # routed pairs s -> g
+        for r in range(G):
+            sc = M[r]                          # this rank's send counts per destination
+            rc = [M[s][r] for s in range(G)]   # rows received from each source
+            so, ns, ro = ep._chunk_rows(R(r), sc, rc)
+            R_in = sum(rc)
+            assert ns == sc[r] == rc[r] and so == sum(sc[:r]) and ro == sum(rc[:r])
+            spans = [(ro, ro + ns), (0, ro), (ro + ns, R_in)]
+            covered = sorted(i for lo, hi in spans for i in range(lo, hi))
+            assert covered == list(range(R_in))
+            pr = [P[s][r] for s in range(G)]
+            assert pr[r] + sum(pr[:r]) + sum(pr[r + 1:]) == sum(pr)
