@@ -433,6 +433,8 @@ FP8_DXT_CASES = [
     ("fp8dxt_with_fp8_up", 2048, 256, 128, 16, 4, "tc", 1),
     ("fp8dxt_qwen3_dims", 2048, 2048, 768, 8, 2, "tr", 0),
     ("fp8dxt_2n_640_generic", 1024, 256, 320, 4, 2, "tc", 0),
+    ("fp8dxt_T1", 1, 256, 64, 4, 2, "tc", 0),
+    ("fp8dxt_empty_experts", 40, 256, 128, 32, 2, "tr", 1),
 ]
 
 
